@@ -1,0 +1,113 @@
+/*
+ * linkcert_b200 — C-ABI of the B200-native direct-summation Gauss linking
+ * number path (arXiv 2106.12655; reference package `linkcert`).
+ *
+ * Conventions
+ *   - Every int-returning call returns 0 (LC_OK) on success or an LC_ERR_*
+ *     code; lc_last_error() then holds a thread-local message.
+ *   - Host pointers are caller-owned and only read/written during the call.
+ *     Calls marked [device] take device pointers and are stream-ordered on
+ *     the context's stream.
+ *   - Vertex buffers are float64 AoS (n, 3), C order, WITHOUT the closing
+ *     vertex (the library closes every loop, linkcert/direct.py:164-166).
+ *     vert_off has L+1 entries, vert_off[0] == 0; loop v owns rows
+ *     [vert_off[v], vert_off[v+1]).
+ *   - Pair lists are int32 (P, 2) rows (i, j), i < j — linkcert PairList
+ *     (pls.py:17-45).  For pair (i, j) the sum is link_direct(loop i, loop j)
+ *     (certify.py:114): loop i is the inner loop `l`, loop j the outer `k`.
+ *   - Results are deterministic: bitwise identical run to run and for any
+ *     split of the work-item range across GPUs.
+ *   - Calls on one context are serialized; contexts are independent.
+ */
+#ifndef LINKCERT_B200_H
+#define LINKCERT_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define LC_API __attribute__((visibility("default")))
+#else
+#define LC_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LC_ABI_VERSION 1
+
+enum {
+    LC_OK = 0,
+    LC_ERR_CUDA = 1,
+    LC_ERR_ARG = 2,
+    LC_ERR_STATE = 3,
+    LC_ERR_DISCRETIZE = 4,
+    LC_ERR_VALIDATION = 5
+};
+
+/* Arithmetic variant of the Gauss-sum kernel (all FP64). */
+enum {
+    LC_GAUSS_PHASE = 0, /* default: shared corner terms + turn-counted phase product */
+    LC_GAUSS_ATAN = 1,  /* shared corner terms + one fused atan2 per segment pair   */
+    LC_GAUSS_REF = 2    /* reference formula per pair, no FMA, two atan2            */
+};
+
+/* Per-pair result flags (lc_evaluate_pairs flags_out). */
+#define LC_FLAG_NAN 1u       /* raw is NaN: round() raises ValueError (kernels.py:68) */
+#define LC_FLAG_AMBIGUOUS 2u /* |raw - rint(raw)| > 0.25 (kernels.py:19-20,69-72)     */
+
+typedef struct lc_ctx lc_ctx;
+
+LC_API int lc_abi_version(void);
+LC_API const char *lc_last_error(void);
+LC_API int lc_device_count(int *count);
+
+/* One context per device; owns a non-blocking stream and cached device buffers. */
+LC_API lc_ctx *lc_create(int device);
+LC_API void lc_destroy(lc_ctx *ctx);
+/* Use a caller stream (e.g. torch.cuda.current_stream().cuda_stream); NULL = own stream. */
+LC_API int lc_set_stream(lc_ctx *ctx, void *cuda_stream);
+LC_API int lc_synchronize(lc_ctx *ctx);
+
+/* ---- Gauss sum (replaces linkcert/direct.py + certify._evaluate_pairs) ---- */
+
+/* Batched drop-in for certify._evaluate_pairs (certify.py:108-127) with the
+ * DS branch of kernels.compute_link (kernels.py:45-73): raw[p] = link_direct
+ * of pair p, lk[p] = half-to-even rounding, flags[p] = LC_FLAG_*. */
+LC_API int lc_evaluate_pairs(lc_ctx *ctx, const double *verts, const int64_t *vert_off, int64_t L,
+                      const int32_t *pairs, int64_t P, int mode, double *raw, int64_t *lk,
+                      uint8_t *flags);
+
+/* Drop-in for direct.link_direct(loop1, loop2, "atan") (direct.py:149-161). */
+LC_API int lc_link_direct(lc_ctx *ctx, const double *loop1, int64_t n1, const double *loop2, int64_t n2,
+                   int mode, double *raw);
+
+/* Drop-in for direct.segment_pair_lambda (direct.py:137-146), batched:
+ * quads (n, 12) = (l_j, l_j1, k_i, k_i1) rows; out (n,). */
+LC_API int lc_segment_pair_lambda(lc_ctx *ctx, const double *quads, int64_t n, double *out);
+
+/* Duration (CUDA events on the context stream) of the last Gauss-sum kernel. */
+LC_API int lc_last_gauss_ms(lc_ctx *ctx, float *ms);
+
+/* Device-resident staging for repeated / sharded evaluation.
+ * lc_stage_polylines uploads polylines + pairs and builds the work items.
+ * lc_gauss_run evaluates items [item_begin, item_end) [device] into
+ * partials_dev (NULL = internal buffer of n_items doubles; an external
+ * buffer must hold n_items doubles and is indexed by absolute item id).
+ * lc_gauss_reduce reduces all n_items partials per pair in fixed order and
+ * copies raw/lk/flags (P each; any may be NULL) to the host. */
+LC_API int lc_stage_polylines(lc_ctx *ctx, const double *verts, const int64_t *vert_off, int64_t L,
+                       const int32_t *pairs, int64_t P, int64_t *n_items);
+LC_API int lc_gauss_run(lc_ctx *ctx, int mode, int64_t item_begin, int64_t item_end, double *partials_dev);
+LC_API int lc_gauss_reduce(lc_ctx *ctx, const double *partials_dev, double *raw, int64_t *lk, uint8_t *flags);
+/* Duration of the last lc_gauss_run kernel (waits for it). */
+LC_API int lc_gauss_event_ms(lc_ctx *ctx, float *ms);
+
+/* FP64 DFMA-chain throughput probe (roofline denominator), FLOP/s. */
+LC_API int lc_probe_fp64_peak(lc_ctx *ctx, double *flops, float *ms);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LINKCERT_B200_H */

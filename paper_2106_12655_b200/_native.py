@@ -1,0 +1,228 @@
+"""ctypes binding of liblinkcert_b200.so (include/linkcert_b200.h).
+
+There is no CPU fallback: if the library or a CUDA device is missing, every
+entry point raises NativeUnavailable.  The library is built in-tree by
+``python -m paper_2106_12655_b200.build`` (``__graft_entry__.build()``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "liblinkcert_b200.so"
+
+LC_OK = 0
+LC_ERR_CUDA = 1
+LC_ERR_ARG = 2
+LC_ERR_STATE = 3
+LC_ERR_DISCRETIZE = 4
+LC_ERR_VALIDATION = 5
+
+GAUSS_PHASE = 0
+GAUSS_ATAN = 1
+GAUSS_REF = 2
+GAUSS_MODES = {"phase": GAUSS_PHASE, "atan": GAUSS_ATAN, "ref": GAUSS_REF}
+
+FLAG_NAN = 1
+FLAG_AMBIGUOUS = 2
+
+_c_double_p = ctypes.POINTER(ctypes.c_double)
+_c_int64_p = ctypes.POINTER(ctypes.c_int64)
+_c_int32_p = ctypes.POINTER(ctypes.c_int32)
+_c_uint8_p = ctypes.POINTER(ctypes.c_uint8)
+_c_float_p = ctypes.POINTER(ctypes.c_float)
+_vp = ctypes.c_void_p
+
+# name -> (restype, argtypes); exactly the symbols of include/linkcert_b200.h
+SIGNATURES = {
+    "lc_abi_version": (ctypes.c_int, []),
+    "lc_last_error": (ctypes.c_char_p, []),
+    "lc_device_count": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
+    "lc_create": (_vp, [ctypes.c_int]),
+    "lc_destroy": (None, [_vp]),
+    "lc_set_stream": (ctypes.c_int, [_vp, _vp]),
+    "lc_synchronize": (ctypes.c_int, [_vp]),
+    "lc_evaluate_pairs": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64,
+                                          ctypes.c_int, _vp, _vp, _vp]),
+    "lc_link_direct": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64, ctypes.c_int, _vp]),
+    "lc_segment_pair_lambda": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp]),
+    "lc_last_gauss_ms": (ctypes.c_int, [_vp, _c_float_p]),
+    "lc_stage_polylines": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64, _c_int64_p]),
+    "lc_gauss_run": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, _vp]),
+    "lc_gauss_reduce": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
+    "lc_gauss_event_ms": (ctypes.c_int, [_vp, _c_float_p]),
+    "lc_probe_fp64_peak": (ctypes.c_int, [_vp, _c_double_p, _c_float_p]),
+}
+
+
+class NativeUnavailable(RuntimeError):
+    """The sm_100a library or a CUDA device is not available (no CPU fallback)."""
+
+
+class NativeError(RuntimeError):
+    def __init__(self, code, message):
+        super().__init__(f"liblinkcert_b200 error {code}: {message}")
+        self.code = code
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load_library():
+    """Load and type the shared library (no device needed)."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise NativeUnavailable(
+                f"{LIB_PATH} is missing; build it with `python -m paper_2106_12655_b200.build`"
+            )
+        lib = ctypes.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def _check(rc):
+    if rc != LC_OK:
+        msg = _lib.lc_last_error().decode(errors="replace")
+        raise NativeError(rc, msg)
+
+
+def _ptr(a):
+    return a.ctypes.data_as(ctypes.c_void_p) if a is not None and a.size else None
+
+
+def default_device():
+    for key in ("LINKCERT_DEVICE", "LOCAL_RANK"):
+        if key in os.environ:
+            return int(os.environ[key])
+    return 0
+
+
+class Context:
+    """One library context (device + stream + cached device buffers)."""
+
+    def __init__(self, device=None):
+        lib = load_library()
+        n = ctypes.c_int(0)
+        if lib.lc_device_count(ctypes.byref(n)) != LC_OK or n.value == 0:
+            raise NativeUnavailable("no CUDA device visible to liblinkcert_b200 (there is no CPU fallback)")
+        self.device = default_device() if device is None else device
+        if self.device >= n.value:
+            self.device = self.device % n.value
+        h = lib.lc_create(self.device)
+        if not h:
+            raise NativeUnavailable(f"lc_create({self.device}) failed: {lib.lc_last_error().decode()}")
+        self.handle = ctypes.c_void_p(h)
+        self.lib = lib
+        self.lock = threading.Lock()
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and self.lib is not None:
+            try:
+                self.lib.lc_destroy(h)
+            except Exception:
+                pass
+
+    # ---- Gauss sum ----------------------------------------------------------
+    def evaluate_pairs(self, verts, vert_off, pairs, mode=GAUSS_PHASE):
+        """raw, lk, flags for every pair (host arrays in, host arrays out)."""
+        verts = np.ascontiguousarray(verts, dtype=np.float64)
+        vert_off = np.ascontiguousarray(vert_off, dtype=np.int64)
+        pairs = np.ascontiguousarray(pairs, dtype=np.int32).reshape(-1, 2)
+        P = pairs.shape[0]
+        raw = np.empty(P, dtype=np.float64)
+        lk = np.empty(P, dtype=np.int64)
+        flags = np.empty(P, dtype=np.uint8)
+        with self.lock:
+            _check(self.lib.lc_evaluate_pairs(self.handle, _ptr(verts), _ptr(vert_off), len(vert_off) - 1,
+                                              _ptr(pairs), P, int(mode), _ptr(raw), _ptr(lk), _ptr(flags)))
+        return raw, lk, flags
+
+    def link_direct(self, loop1, loop2, mode=GAUSS_PHASE):
+        a = np.ascontiguousarray(loop1, dtype=np.float64)
+        b = np.ascontiguousarray(loop2, dtype=np.float64)
+        out = ctypes.c_double(0.0)
+        with self.lock:
+            _check(self.lib.lc_link_direct(self.handle, _ptr(a), a.shape[0], _ptr(b), b.shape[0], int(mode),
+                                           ctypes.byref(out)))
+        return out.value
+
+    def segment_pair_lambda(self, quads):
+        q = np.ascontiguousarray(quads, dtype=np.float64).reshape(-1, 12)
+        out = np.empty(q.shape[0], dtype=np.float64)
+        with self.lock:
+            _check(self.lib.lc_segment_pair_lambda(self.handle, _ptr(q), q.shape[0], _ptr(out)))
+        return out
+
+    def last_gauss_ms(self):
+        ms = ctypes.c_float(0.0)
+        _check(self.lib.lc_last_gauss_ms(self.handle, ctypes.byref(ms)))
+        return ms.value
+
+    def stage_polylines(self, verts, vert_off, pairs):
+        verts = np.ascontiguousarray(verts, dtype=np.float64)
+        vert_off = np.ascontiguousarray(vert_off, dtype=np.int64)
+        pairs = np.ascontiguousarray(pairs, dtype=np.int32).reshape(-1, 2)
+        n = ctypes.c_int64(0)
+        with self.lock:
+            _check(self.lib.lc_stage_polylines(self.handle, _ptr(verts), _ptr(vert_off), len(vert_off) - 1,
+                                               _ptr(pairs), pairs.shape[0], ctypes.byref(n)))
+        self._staged_pairs = pairs.shape[0]
+        return n.value
+
+    def gauss_run(self, mode, item_begin, item_end, partials_dev_ptr=None):
+        with self.lock:
+            _check(self.lib.lc_gauss_run(self.handle, int(mode), int(item_begin), int(item_end),
+                                         ctypes.c_void_p(partials_dev_ptr) if partials_dev_ptr else None))
+
+    def gauss_reduce(self, partials_dev_ptr=None):
+        P = self._staged_pairs
+        raw = np.empty(P, dtype=np.float64)
+        lk = np.empty(P, dtype=np.int64)
+        flags = np.empty(P, dtype=np.uint8)
+        with self.lock:
+            _check(self.lib.lc_gauss_reduce(self.handle,
+                                            ctypes.c_void_p(partials_dev_ptr) if partials_dev_ptr else None,
+                                            _ptr(raw), _ptr(lk), _ptr(flags)))
+        return raw, lk, flags
+
+    def gauss_event_ms(self):
+        ms = ctypes.c_float(0.0)
+        _check(self.lib.lc_gauss_event_ms(self.handle, ctypes.byref(ms)))
+        return ms.value
+
+    def synchronize(self):
+        _check(self.lib.lc_synchronize(self.handle))
+
+    def probe_fp64_peak(self):
+        flops = ctypes.c_double(0.0)
+        ms = ctypes.c_float(0.0)
+        _check(self.lib.lc_probe_fp64_peak(self.handle, ctypes.byref(flops), ctypes.byref(ms)))
+        return flops.value, ms.value
+
+
+_ctx = {}
+_ctx_lock = threading.Lock()
+
+
+def context(device=None) -> Context:
+    dev = default_device() if device is None else device
+    with _ctx_lock:
+        c = _ctx.get(dev)
+        if c is None:
+            c = Context(dev)
+            _ctx[dev] = c
+        return c

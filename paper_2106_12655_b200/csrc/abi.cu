@@ -1,0 +1,202 @@
+// extern "C" boundary of liblinkcert_b200.so — see include/linkcert_b200.h.
+//
+// Every entry point returns 0 on success or an lc::Code; no C++ exception
+// crosses the ABI.  The library owns device buffers (grow-only, cached in the
+// context); callers own every host buffer they pass.  Calls on one context
+// are serialized by its mutex.
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "gauss.cuh"
+#include "pipeline.cuh"
+
+namespace lc {
+double probe_dfma_flops(cudaStream_t s, float *elapsed_ms);
+}
+
+using namespace lc;
+
+static thread_local std::string g_last_error;
+
+struct lc_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::mutex mu;
+    Pipeline pipe;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    float last_gauss_ms = 0.f;
+};
+
+template <class F>
+static int guarded(lc_ctx *ctx, F &&f) {
+    try {
+        if (!ctx) throw Error(LC_ERR_ARG, "null context");
+        std::lock_guard<std::mutex> lock(ctx->mu);
+        LC_CUDA(cudaSetDevice(ctx->device));
+        f();
+        return LC_OK;
+    } catch (const Error &e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::exception &e) {
+        g_last_error = e.what();
+        return LC_ERR_STATE;
+    } catch (...) {
+        g_last_error = "unknown error";
+        return LC_ERR_STATE;
+    }
+}
+
+extern "C" {
+
+int lc_abi_version(void) { return LC_ABI_VERSION; }
+
+const char *lc_last_error(void) { return g_last_error.c_str(); }
+
+int lc_device_count(int *count) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+        g_last_error = cudaGetErrorString(e);
+        *count = 0;
+        return LC_ERR_CUDA;
+    }
+    *count = n;
+    return LC_OK;
+}
+
+lc_ctx *lc_create(int device) {
+    lc_ctx *ctx = new lc_ctx();
+    ctx->device = device;
+    try {
+        LC_CUDA(cudaSetDevice(device));
+        LC_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        ctx->own_stream = true;
+        LC_CUDA(cudaEventCreate(&ctx->ev0));
+        LC_CUDA(cudaEventCreate(&ctx->ev1));
+        ctx->pipe.init(ctx->stream);
+    } catch (const std::exception &e) {
+        g_last_error = e.what();
+        delete ctx;
+        return nullptr;
+    }
+    return ctx;
+}
+
+void lc_destroy(lc_ctx *ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    ctx->pipe.release();
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->own_stream && ctx->stream) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaStreamDestroy(ctx->stream);
+    }
+    delete ctx;
+}
+
+int lc_set_stream(lc_ctx *ctx, void *stream) {
+    return guarded(ctx, [&] {
+        LC_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+        ctx->own_stream = stream == nullptr;
+        if (stream) ctx->stream = (cudaStream_t)stream;
+        else LC_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        ctx->pipe.set_stream(ctx->stream);
+    });
+}
+
+int lc_synchronize(lc_ctx *ctx) {
+    return guarded(ctx, [&] { LC_CUDA(cudaStreamSynchronize(ctx->stream)); });
+}
+
+// ---------------------------------------------------------------- Gauss sum
+
+int lc_evaluate_pairs(lc_ctx *ctx, const double *verts, const int64_t *vert_off, int64_t L,
+                      const int32_t *pairs, int64_t P, int mode, double *raw, int64_t *lk,
+                      uint8_t *flags) {
+    return guarded(ctx, [&] {
+        if (L < 0 || P < 0 || (L > 0 && (!verts || !vert_off)) || (P > 0 && !pairs))
+            throw Error(LC_ERR_ARG, "lc_evaluate_pairs: bad arguments");
+        ctx->pipe.upload_polylines(verts, vert_off, L);
+        ctx->pipe.upload_pairs(pairs, P);
+        ctx->pipe.build_gauss_items();
+        ctx->pipe.run_gauss(mode, 0, ctx->pipe.n_items, nullptr, ctx->ev0, ctx->ev1);
+        ctx->pipe.reduce_pairs(nullptr);
+        ctx->pipe.download_results(raw, lk, flags);
+        LC_CUDA(cudaEventElapsedTime(&ctx->last_gauss_ms, ctx->ev0, ctx->ev1));
+    });
+}
+
+int lc_link_direct(lc_ctx *ctx, const double *loop1, int64_t n1, const double *loop2, int64_t n2,
+                   int mode, double *raw) {
+    return guarded(ctx, [&] {
+        if (!loop1 || !loop2 || n1 < 1 || n2 < 1) throw Error(LC_ERR_ARG, "lc_link_direct: bad arguments");
+        std::vector<double> v((size_t)(n1 + n2) * 3);
+        std::copy(loop1, loop1 + 3 * n1, v.begin());
+        std::copy(loop2, loop2 + 3 * n2, v.begin() + 3 * n1);
+        const int64_t off[3] = {0, n1, n1 + n2};
+        const int32_t pr[2] = {0, 1};
+        int64_t lk = 0;
+        uint8_t fl = 0;
+        ctx->pipe.upload_polylines(v.data(), off, 2);
+        ctx->pipe.upload_pairs(pr, 1);
+        ctx->pipe.build_gauss_items();
+        ctx->pipe.run_gauss(mode, 0, ctx->pipe.n_items, nullptr, ctx->ev0, ctx->ev1);
+        ctx->pipe.reduce_pairs(nullptr);
+        ctx->pipe.download_results(raw, &lk, &fl);
+    });
+}
+
+int lc_segment_pair_lambda(lc_ctx *ctx, const double *quads, int64_t n, double *out) {
+    return guarded(ctx, [&] {
+        if (n < 0 || (n > 0 && (!quads || !out))) throw Error(LC_ERR_ARG, "lc_segment_pair_lambda: bad arguments");
+        ctx->pipe.segment_pair_lambda(quads, n, out);
+    });
+}
+
+int lc_last_gauss_ms(lc_ctx *ctx, float *ms) {
+    return guarded(ctx, [&] { *ms = ctx->last_gauss_ms; });
+}
+
+// Device-resident staging (bench / multi-GPU): upload once, run many times.
+int lc_stage_polylines(lc_ctx *ctx, const double *verts, const int64_t *vert_off, int64_t L,
+                       const int32_t *pairs, int64_t P, int64_t *n_items) {
+    return guarded(ctx, [&] {
+        ctx->pipe.upload_polylines(verts, vert_off, L);
+        ctx->pipe.upload_pairs(pairs, P);
+        ctx->pipe.build_gauss_items();
+        *n_items = ctx->pipe.n_items;
+    });
+}
+
+int lc_gauss_run(lc_ctx *ctx, int mode, int64_t item_begin, int64_t item_end, double *partials_dev) {
+    return guarded(ctx, [&] {
+        if (item_begin < 0 || item_end > ctx->pipe.n_items || item_begin > item_end)
+            throw Error(LC_ERR_ARG, "lc_gauss_run: item range out of bounds");
+        ctx->pipe.run_gauss(mode, item_begin, item_end, partials_dev, ctx->ev0, ctx->ev1);
+    });
+}
+
+int lc_gauss_reduce(lc_ctx *ctx, const double *partials_dev, double *raw, int64_t *lk, uint8_t *flags) {
+    return guarded(ctx, [&] {
+        ctx->pipe.reduce_pairs(partials_dev);
+        ctx->pipe.download_results(raw, lk, flags);
+    });
+}
+
+int lc_gauss_event_ms(lc_ctx *ctx, float *ms) {
+    return guarded(ctx, [&] {
+        LC_CUDA(cudaEventSynchronize(ctx->ev1));
+        LC_CUDA(cudaEventElapsedTime(ms, ctx->ev0, ctx->ev1));
+    });
+}
+
+int lc_probe_fp64_peak(lc_ctx *ctx, double *flops, float *ms) {
+    return guarded(ctx, [&] { *flops = probe_dfma_flops(ctx->stream, ms); });
+}
+
+}  // extern "C"

@@ -1,0 +1,54 @@
+// Shared helpers for the linkcert-b200 sm_100a kernels and the C-ABI layer.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/linkcert_b200.h"
+
+namespace lc {
+
+// Errors raised inside the library are C++ exceptions; the C-ABI layer
+// (abi.cu) catches every one of them and turns it into a return code plus a
+// thread-local message — nothing crosses the extern "C" boundary.
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+
+inline void check_cuda(cudaError_t e, const char *what, const char *file, int line) {
+    if (e != cudaSuccess) {
+        char buf[512];
+        snprintf(buf, sizeof buf, "%s failed at %s:%d: %s", what, file, line, cudaGetErrorString(e));
+        throw Error(LC_ERR_CUDA, buf);
+    }
+}
+#define LC_CUDA(x) ::lc::check_cuda((x), #x, __FILE__, __LINE__)
+#define LC_CHECK_LAUNCH() ::lc::check_cuda(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+// Grow-only stream-ordered device buffer.
+struct DevBuf {
+    void *ptr = nullptr;
+    size_t bytes = 0;
+    void reserve(size_t n, cudaStream_t s) {
+        if (n <= bytes) return;
+        if (ptr) LC_CUDA(cudaFreeAsync(ptr, s));
+        size_t want = n < 256 ? 256 : n + n / 4;
+        LC_CUDA(cudaMallocAsync(&ptr, want, s));
+        bytes = want;
+    }
+    void release(cudaStream_t s) {
+        if (ptr) cudaFreeAsync(ptr, s);
+        ptr = nullptr;
+        bytes = 0;
+    }
+    template <class T> T *as() const { return static_cast<T *>(ptr); }
+};
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace lc

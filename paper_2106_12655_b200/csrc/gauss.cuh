@@ -1,0 +1,66 @@
+// Gauss-sum work-item layer: declarations shared by gauss.cu and abi.cu.
+#pragma once
+#include "common.cuh"
+
+namespace lc {
+
+// Arithmetic variants of the per-lane strip evaluation (all FP64):
+//   GAUSS_PHASE : default. Arai terms with corner vectors/norms/edge dots shared
+//                 between neighbouring segment pairs, and the per-pair angles
+//                 atan2(p,d1)+atan2(p,d2) accumulated as an exact-turn-counted
+//                 complex phase product (one atan2 per lane strip).
+//   GAUSS_ATAN  : same sharing, one fused atan2 per segment pair with the
+//                 exact full-turn correction (direct.py:120-123 rule).
+//   GAUSS_REF   : the reference formula evaluated per pair from scratch with
+//                 no FMA contraction and two atan2 (direct.py:19-46); used to
+//                 freeze F_pair and as a numerics cross-check.
+enum GaussMode : int { GAUSS_PHASE = 0, GAUSS_ATAN = 1, GAUSS_REF = 2 };
+
+constexpr int kRowsPerLane = 4;     // outer-loop (k) segments held per lane
+constexpr int kMaxColsPerLane = 2048;
+
+// Per loop-pair tiling, built on the device from the pair list.
+struct PairGeom {
+    int64_t row_off;   // first vertex of the row loop (loop j of pair (i,j): "k")
+    int64_t col_off;   // first vertex of the column loop (loop i: "l")
+    int32_t nrows;     // segments of the row loop
+    int32_t ncols;     // segments of the column loop
+    int32_t rb_log2;   // lanes of one item split as (1<<rb_log2) row blocks x (32>>rb_log2) column strips
+    int32_t cl;        // columns per lane strip
+    int32_t items_r;   // item grid of this pair
+    int32_t items_c;
+};
+
+// Builds PairGeom[P] and item_off[P+1] (exclusive prefix of items per pair).
+// voff: closed-loop SoA vertex offsets (L+1). Returns total item count (syncs).
+int64_t build_items(const int32_t *d_pairs, int64_t P, const int64_t *d_voff, PairGeom *d_pg,
+                    int64_t *d_item_off, void *d_scan_tmp, size_t scan_tmp_bytes, cudaStream_t s);
+size_t build_items_scan_bytes(int64_t P);
+
+// Evaluates items [item_begin, item_end) into partials[item] (absolute index).
+void launch_gauss_items(int mode, const double *X, const double *Y, const double *Z,
+                        const PairGeom *pg, const int64_t *item_off, int64_t P,
+                        int64_t item_begin, int64_t item_end, unsigned long long *counter,
+                        double *partials, cudaStream_t s);
+
+// raw[p] = fixed-order sum of the pair's item partials; lk = rint(raw);
+// flags bit0 = NaN, bit1 = |raw - rint(raw)| > 0.25 (kernels.py:19-20,69-72).
+void launch_reduce_pairs(const double *partials, const int64_t *item_off, int64_t P, double *raw,
+                         int64_t *lk, uint8_t *flags, cudaStream_t s);
+
+// Writes the closed SoA vertex arrays scaled by an exact power of two from
+// an AoS (n,3) buffer with per-loop offsets (no closing vertex in the input).
+void launch_pack_closed_soa(const double *aos, const int64_t *in_off, const int64_t *voff, int64_t L,
+                            int64_t total_closed, const int *d_exp, double *X, double *Y, double *Z,
+                            cudaStream_t s);
+
+// d_exp <- biased exponent field of max |aos[k]| over n doubles (atomicMax;
+// caller zeroes d_exp first).  The pack kernel scales by 2^-(field-1023).
+void launch_max_exponent(const double *aos, int64_t n, int *d_exp, cudaStream_t s);
+
+// out[k] = reference _pair_lambda of quads[k] = (l_j, l_j1, k_i, k_i1), 12 doubles each.
+void launch_segment_pairs(const double *quads, int64_t n, double *out, cudaStream_t s);
+
+int num_sms();
+
+}  // namespace lc
