@@ -103,6 +103,62 @@ LC_API int lc_gauss_reduce(lc_ctx *ctx, const double *partials_dev, double *raw,
 /* Duration of the last lc_gauss_run kernel (waits for it). */
 LC_API int lc_gauss_event_ms(lc_ctx *ctx, float *ms);
 
+/* ---- Model pipeline: PLS -> discretize -> Gauss sum, device resident ----
+ *
+ * Model = packed monomial cubics, the arrays of linkcert LoopGeometry
+ * (geometry.py:206-296): coeffs (M, 4, 3) float64 (a0..a3 rows), t (M, 2)
+ * parameter domains, loop_off (L+1) segment offsets per loop. */
+LC_API int lc_model_upload(lc_ctx *ctx, const double *coeffs, const double *t, const int64_t *loop_off,
+                           int64_t L);
+/* Drop-in for geometry.tight_boxes (geometry.py:113-152): coeffs (m,4,3),
+ * t (m,2) domains -> lo, hi (m,3).  Independent of the uploaded model. */
+LC_API int lc_tight_boxes(lc_ctx *ctx, const double *coeffs, const double *t, int64_t m, double *lo,
+                          double *hi);
+/* Loop AABBs, unions of tight segment boxes (pls.py:48-56): lo, hi (L, 3). */
+LC_API int lc_loop_boxes(lc_ctx *ctx, double *lo, double *hi);
+/* Drop-in for pls.potential_link_search (pls.py:59-73): closed-interval box
+ * overlap, i < j, minus excluded keys ((min<<32)|max, sorted unique),
+ * sorted.  The pair list stays on the device; lc_get_pairs copies it out. */
+LC_API int lc_potential_link_search(lc_ctx *ctx, const uint64_t *excluded_keys, int64_t n_excl,
+                                    int64_t *n_pairs);
+LC_API int lc_get_pairs(lc_ctx *ctx, int32_t *pairs);
+/* Replace the device pair list (a caller-built PairList for lc_discretize). */
+LC_API int lc_set_pairs(lc_ctx *ctx, const int32_t *pairs, int64_t P);
+
+/* Discretization error kinds (lc_discretize_error). */
+enum {
+    LC_DISC_OK = 0,
+    LC_DISC_ZERO_LENGTH = 1,      /* ZeroLengthInput, loops = (idx,)                 */
+    LC_DISC_CURVES_INTERSECT = 2, /* CurvesIntersect, loops = (a, b)                  */
+    LC_DISC_SUBSEG_BUDGET = 3,    /* PassLimitExceeded, loops = (i,) max_subsegments  */
+    LC_DISC_PASS_BUDGET = 4,      /* PassLimitExceeded, loops = busy, max_passes      */
+    LC_DISC_INVALID_POLYLINE = 5  /* ValidationError from PolylineLoop, detail = 1 <3 vertices,
+                                     2 non-finite, 3 zero-length segment            */
+};
+/* Drop-in for discretize.discretize (discretize.py:112-191) over the device
+ * model and pair list.  Returns LC_ERR_DISCRETIZE or LC_ERR_VALIDATION for
+ * the reference's DiscretizationError / ValidationError; details from
+ * lc_discretize_error.  Output polylines stay on the device (they are the
+ * Gauss-sum input); lc_get_polylines copies them out (AoS (V,3) + (L+1)). */
+LC_API int lc_discretize(lc_ctx *ctx, double xi, double epsilon, int max_passes, int64_t max_subsegments,
+                         int64_t *n_vertices, int *passes);
+LC_API int lc_discretize_error(lc_ctx *ctx, int *kind, int *detail, int64_t *loops, int64_t cap,
+                               int64_t *n_loops);
+LC_API int lc_get_polylines(lc_ctx *ctx, double *verts, int64_t *vert_off);
+/* Build the Gauss-sum work items for the device polylines + pair list. */
+LC_API int lc_prepare_gauss(lc_ctx *ctx, int64_t *n_items);
+/* Gauss sum over the device polylines and pair list; results to the host. */
+LC_API int lc_evaluate_staged(lc_ctx *ctx, int mode, double *raw, int64_t *lk, uint8_t *flags);
+/* Whole device path on the resident model: PLS -> discretize -> items ->
+ * Gauss sum -> rounding (certify._prepare + _evaluate_pairs, certify.py:108-138).
+ * Results stay on the device; lc_get_pairs / lc_get_results copy them out. */
+LC_API int lc_run_pipeline(lc_ctx *ctx, const uint64_t *excluded_keys, int64_t n_excl, double xi,
+                           double epsilon, int max_passes, int64_t max_subsegments, int mode,
+                           int64_t *n_pairs);
+LC_API int lc_get_results(lc_ctx *ctx, double *raw, int64_t *lk, uint8_t *flags);
+/* Device times (ms) of the last pipeline: [PLS, discretize, Gauss kernel, reduce]. */
+LC_API int lc_stage_times(lc_ctx *ctx, float *ms);
+
 /* FP64 DFMA-chain throughput probe (roofline denominator), FLOP/s. */
 LC_API int lc_probe_fp64_peak(lc_ctx *ctx, double *flops, float *ms);
 

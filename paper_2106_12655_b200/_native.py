@@ -57,7 +57,43 @@ SIGNATURES = {
     "lc_gauss_reduce": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "lc_gauss_event_ms": (ctypes.c_int, [_vp, _c_float_p]),
     "lc_probe_fp64_peak": (ctypes.c_int, [_vp, _c_double_p, _c_float_p]),
+    "lc_model_upload": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int64]),
+    "lc_tight_boxes": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, _vp, _vp]),
+    "lc_loop_boxes": (ctypes.c_int, [_vp, _vp, _vp]),
+    "lc_potential_link_search": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _c_int64_p]),
+    "lc_get_pairs": (ctypes.c_int, [_vp, _vp]),
+    "lc_set_pairs": (ctypes.c_int, [_vp, _vp, ctypes.c_int64]),
+    "lc_discretize": (ctypes.c_int, [_vp, ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_int64,
+                                      _c_int64_p, ctypes.POINTER(ctypes.c_int)]),
+    "lc_discretize_error": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                            _vp, ctypes.c_int64, _c_int64_p]),
+    "lc_get_polylines": (ctypes.c_int, [_vp, _vp, _vp]),
+    "lc_prepare_gauss": (ctypes.c_int, [_vp, _c_int64_p]),
+    "lc_evaluate_staged": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, _vp]),
+    "lc_run_pipeline": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                                        ctypes.c_int64, ctypes.c_int, _c_int64_p]),
+    "lc_get_results": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    "lc_stage_times": (ctypes.c_int, [_vp, _c_float_p]),
 }
+
+# lc_discretize_error kinds
+DISC_OK = 0
+DISC_ZERO_LENGTH = 1
+DISC_CURVES_INTERSECT = 2
+DISC_SUBSEG_BUDGET = 3
+DISC_PASS_BUDGET = 4
+DISC_INVALID_POLYLINE = 5
+
+
+class DiscretizeFailure(Exception):
+    """Structured discretization failure reported by the device (mapped to the
+    reference exception types by paper_2106_12655_b200.discretize)."""
+
+    def __init__(self, kind, detail, loops):
+        super().__init__(f"discretization failure kind={kind} detail={detail} loops={loops}")
+        self.kind = kind
+        self.detail = detail
+        self.loops = tuple(int(x) for x in loops)
 
 
 class NativeUnavailable(RuntimeError):
@@ -206,6 +242,126 @@ class Context:
 
     def synchronize(self):
         _check(self.lib.lc_synchronize(self.handle))
+
+    # ---- model pipeline -------------------------------------------------------
+    def tight_boxes(self, coeffs, t):
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.float64).reshape(-1, 4, 3)
+        t = np.ascontiguousarray(t, dtype=np.float64).reshape(-1, 2)
+        m = coeffs.shape[0]
+        lo = np.empty((m, 3))
+        hi = np.empty((m, 3))
+        with self.lock:
+            _check(self.lib.lc_tight_boxes(self.handle, _ptr(coeffs), _ptr(t), m, _ptr(lo), _ptr(hi)))
+        return lo, hi
+
+    def upload_model(self, coeffs, t, loop_off):
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+        t = np.ascontiguousarray(t, dtype=np.float64)
+        loop_off = np.ascontiguousarray(loop_off, dtype=np.int64)
+        with self.lock:
+            _check(self.lib.lc_model_upload(self.handle, _ptr(coeffs), _ptr(t), _ptr(loop_off), len(loop_off) - 1))
+        self._L = len(loop_off) - 1
+
+    def loop_boxes(self):
+        lo = np.empty((self._L, 3))
+        hi = np.empty((self._L, 3))
+        with self.lock:
+            _check(self.lib.lc_loop_boxes(self.handle, _ptr(lo), _ptr(hi)))
+        return lo, hi
+
+    def potential_link_search(self, excluded_keys=None):
+        ex = np.ascontiguousarray(excluded_keys if excluded_keys is not None else [], dtype=np.uint64)
+        n = ctypes.c_int64(0)
+        with self.lock:
+            _check(self.lib.lc_potential_link_search(self.handle, _ptr(ex), ex.size, ctypes.byref(n)))
+        self._staged_pairs = n.value
+        return n.value
+
+    def get_pairs(self):
+        out = np.empty((self._staged_pairs, 2), dtype=np.int32)
+        with self.lock:
+            _check(self.lib.lc_get_pairs(self.handle, _ptr(out)))
+        return out
+
+    def set_pairs(self, pairs):
+        pairs = np.ascontiguousarray(pairs, dtype=np.int32).reshape(-1, 2)
+        with self.lock:
+            _check(self.lib.lc_set_pairs(self.handle, _ptr(pairs), pairs.shape[0]))
+        self._staged_pairs = pairs.shape[0]
+
+    def _disc_error(self):
+        kind = ctypes.c_int(0)
+        detail = ctypes.c_int(0)
+        n = ctypes.c_int64(0)
+        _check(self.lib.lc_discretize_error(self.handle, ctypes.byref(kind), ctypes.byref(detail), None, 0,
+                                            ctypes.byref(n)))
+        loops = np.zeros(max(n.value, 1), dtype=np.int64)
+        _check(self.lib.lc_discretize_error(self.handle, ctypes.byref(kind), ctypes.byref(detail), _ptr(loops),
+                                            n.value, ctypes.byref(n)))
+        return DiscretizeFailure(kind.value, detail.value, loops[:n.value].tolist())
+
+    def discretize(self, xi, epsilon, max_passes, max_subsegments):
+        """Run device discretization; returns (n_vertices, passes) or raises DiscretizeFailure."""
+        nv = ctypes.c_int64(0)
+        passes = ctypes.c_int(0)
+        with self.lock:
+            rc = self.lib.lc_discretize(self.handle, float(xi), float(epsilon), int(max_passes), int(max_subsegments),
+                                        ctypes.byref(nv), ctypes.byref(passes))
+            if rc in (LC_ERR_DISCRETIZE, LC_ERR_VALIDATION):
+                raise self._disc_error()
+            _check(rc)
+        self._nverts = nv.value
+        return nv.value, passes.value
+
+    def get_polylines(self):
+        verts = np.empty((self._nverts, 3))
+        off = np.empty(self._L + 1, dtype=np.int64)
+        with self.lock:
+            _check(self.lib.lc_get_polylines(self.handle, _ptr(verts), _ptr(off)))
+        return verts, off
+
+    def evaluate_staged(self, mode=GAUSS_PHASE):
+        P = self._staged_pairs
+        raw = np.empty(P)
+        lk = np.empty(P, dtype=np.int64)
+        flags = np.empty(P, dtype=np.uint8)
+        with self.lock:
+            _check(self.lib.lc_evaluate_staged(self.handle, int(mode), _ptr(raw), _ptr(lk), _ptr(flags)))
+        return raw, lk, flags
+
+    def prepare_gauss(self):
+        n = ctypes.c_int64(0)
+        with self.lock:
+            _check(self.lib.lc_prepare_gauss(self.handle, ctypes.byref(n)))
+        return n.value
+
+    def run_pipeline(self, excluded_keys, xi, epsilon, max_passes, max_subsegments, mode=GAUSS_PHASE):
+        """PLS -> discretize -> Gauss on the uploaded model; returns P (results stay on device)."""
+        ex = np.ascontiguousarray(excluded_keys if excluded_keys is not None else [], dtype=np.uint64)
+        n = ctypes.c_int64(0)
+        with self.lock:
+            rc = self.lib.lc_run_pipeline(self.handle, _ptr(ex), ex.size, float(xi), float(epsilon), int(max_passes),
+                                          int(max_subsegments), int(mode), ctypes.byref(n))
+            if rc in (LC_ERR_DISCRETIZE, LC_ERR_VALIDATION):
+                raise self._disc_error()
+            _check(rc)
+        self._staged_pairs = n.value
+        return n.value
+
+    def get_results(self):
+        P = self._staged_pairs
+        raw = np.empty(P)
+        lk = np.empty(P, dtype=np.int64)
+        flags = np.empty(P, dtype=np.uint8)
+        with self.lock:
+            _check(self.lib.lc_get_results(self.handle, _ptr(raw), _ptr(lk), _ptr(flags)))
+        return raw, lk, flags
+
+    def stage_times(self):
+        ms = (ctypes.c_float * 4)()
+        with self.lock:
+            _check(self.lib.lc_stage_times(self.handle, ms))
+        return {"pls": ms[0], "discretize": ms[1], "gauss": ms[2], "reduce": ms[3]}
 
     def probe_fp64_peak(self):
         flops = ctypes.c_double(0.0)

@@ -27,6 +27,7 @@ struct lc_ctx {
     Pipeline pipe;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     float last_gauss_ms = 0.f;
+    DevBuf tb_coeffs, tb_t, tb_box, tb_loop, tb_off, tb_flag;   // lc_tight_boxes scratch
 };
 
 template <class F>
@@ -148,6 +149,7 @@ int lc_link_direct(lc_ctx *ctx, const double *loop1, int64_t n1, const double *l
         ctx->pipe.run_gauss(mode, 0, ctx->pipe.n_items, nullptr, ctx->ev0, ctx->ev1);
         ctx->pipe.reduce_pairs(nullptr);
         ctx->pipe.download_results(raw, &lk, &fl);
+        LC_CUDA(cudaEventElapsedTime(&ctx->last_gauss_ms, ctx->ev0, ctx->ev1));
     });
 }
 
@@ -192,6 +194,155 @@ int lc_gauss_event_ms(lc_ctx *ctx, float *ms) {
     return guarded(ctx, [&] {
         LC_CUDA(cudaEventSynchronize(ctx->ev1));
         LC_CUDA(cudaEventElapsedTime(ms, ctx->ev0, ctx->ev1));
+    });
+}
+
+// ------------------------------------------------------- model pipeline
+
+int lc_tight_boxes(lc_ctx *ctx, const double *coeffs, const double *t, int64_t m, double *lo, double *hi) {
+    return guarded(ctx, [&] {
+        if (m < 0 || (m > 0 && (!coeffs || !t || !lo || !hi))) throw Error(LC_ERR_ARG, "lc_tight_boxes: bad arguments");
+        if (m == 0) return;
+        cudaStream_t s = ctx->stream;
+        ctx->tb_coeffs.reserve(sizeof(double) * 12 * m, s);
+        ctx->tb_t.reserve(sizeof(double) * 2 * m, s);
+        ctx->tb_box.reserve(sizeof(double) * 6 * m, s);
+        ctx->tb_loop.reserve(sizeof(int32_t) * m, s);
+        ctx->tb_off.reserve(sizeof(int64_t) * 2, s);
+        ctx->tb_flag.reserve(sizeof(int), s);
+        const int64_t off[2] = {0, m};
+        LC_CUDA(cudaMemcpyAsync(ctx->tb_coeffs.ptr, coeffs, sizeof(double) * 12 * m, cudaMemcpyHostToDevice, s));
+        LC_CUDA(cudaMemcpyAsync(ctx->tb_t.ptr, t, sizeof(double) * 2 * m, cudaMemcpyHostToDevice, s));
+        LC_CUDA(cudaMemcpyAsync(ctx->tb_off.ptr, off, sizeof off, cudaMemcpyHostToDevice, s));
+        launch_seg_boxes(ctx->tb_coeffs.as<double>(), ctx->tb_t.as<double>(), ctx->tb_off.as<int64_t>(), 1, m, -1.0,
+                         ctx->tb_box.as<double>(), ctx->tb_loop.as<int32_t>(), ctx->tb_flag.as<int>(), s);
+        std::vector<double> b((size_t)6 * m);
+        LC_CUDA(cudaMemcpyAsync(b.data(), ctx->tb_box.ptr, sizeof(double) * 6 * m, cudaMemcpyDeviceToHost, s));
+        LC_CUDA(cudaStreamSynchronize(s));
+        for (int64_t k = 0; k < m; ++k)
+            for (int d = 0; d < 3; ++d) {
+                lo[3 * k + d] = b[d * m + k];
+                hi[3 * k + d] = b[(3 + d) * m + k];
+            }
+    });
+}
+
+int lc_model_upload(lc_ctx *ctx, const double *coeffs, const double *t, const int64_t *loop_off, int64_t L) {
+    return guarded(ctx, [&] {
+        if (L < 0 || !loop_off || (L > 0 && loop_off[L] > 0 && (!coeffs || !t)))
+            throw Error(LC_ERR_ARG, "lc_model_upload: bad arguments");
+        ctx->pipe.upload_model(coeffs, t, loop_off, L);
+    });
+}
+
+int lc_loop_boxes(lc_ctx *ctx, double *lo, double *hi) {
+    return guarded(ctx, [&] { ctx->pipe.download_loop_boxes(lo, hi); });
+}
+
+int lc_potential_link_search(lc_ctx *ctx, const uint64_t *excluded_keys, int64_t n_excl, int64_t *n_pairs) {
+    return guarded(ctx, [&] {
+        if (n_excl < 0 || (n_excl > 0 && !excluded_keys)) throw Error(LC_ERR_ARG, "bad excluded keys");
+        for (int64_t k = 1; k < n_excl; ++k)
+            if (excluded_keys[k] <= excluded_keys[k - 1]) throw Error(LC_ERR_ARG, "excluded keys must be sorted unique");
+        *n_pairs = ctx->pipe.potential_link_search(excluded_keys, n_excl);
+    });
+}
+
+int lc_get_pairs(lc_ctx *ctx, int32_t *pairs) {
+    return guarded(ctx, [&] { ctx->pipe.download_pairs(pairs); });
+}
+
+int lc_set_pairs(lc_ctx *ctx, const int32_t *pairs, int64_t P) {
+    return guarded(ctx, [&] {
+        if (P < 0 || (P > 0 && !pairs)) throw Error(LC_ERR_ARG, "bad pair list");
+        ctx->pipe.upload_pairs(pairs, P);
+    });
+}
+
+static int run_discretize_abi(lc_ctx *ctx, double xi, double epsilon, int max_passes, int64_t max_subsegments,
+                              int64_t *n_vertices, int *passes) {
+    int rc = LC_OK;
+    int g = guarded(ctx, [&] {
+        DiscParams prm;
+        prm.xi = xi;
+        prm.epsilon = epsilon;
+        prm.max_passes = max_passes;
+        prm.max_subsegments = max_subsegments;
+        const bool ok = ctx->pipe.discretize(prm);
+        if (passes) *passes = ctx->pipe.dout.passes;
+        if (!ok) {
+            rc = ctx->pipe.derr.kind == DISC_INVALID_POLYLINE ? LC_ERR_VALIDATION : LC_ERR_DISCRETIZE;
+            return;
+        }
+        if (n_vertices) *n_vertices = ctx->pipe.V;
+    });
+    if (g != LC_OK) return g;
+    if (rc != LC_OK) g_last_error = "discretization failed (see lc_discretize_error)";
+    return rc;
+}
+
+int lc_discretize(lc_ctx *ctx, double xi, double epsilon, int max_passes, int64_t max_subsegments,
+                  int64_t *n_vertices, int *passes) {
+    return run_discretize_abi(ctx, xi, epsilon, max_passes, max_subsegments, n_vertices, passes);
+}
+
+int lc_discretize_error(lc_ctx *ctx, int *kind, int *detail, int64_t *loops, int64_t cap, int64_t *n_loops) {
+    return guarded(ctx, [&] {
+        const DiscError &e = ctx->pipe.derr;
+        *kind = e.kind;
+        *detail = e.detail;
+        *n_loops = (int64_t)e.loops.size();
+        for (int64_t k = 0; k < cap && k < (int64_t)e.loops.size(); ++k) loops[k] = e.loops[k];
+    });
+}
+
+int lc_get_polylines(lc_ctx *ctx, double *verts, int64_t *vert_off) {
+    return guarded(ctx, [&] { ctx->pipe.download_polylines(verts, vert_off); });
+}
+
+int lc_prepare_gauss(lc_ctx *ctx, int64_t *n_items) {
+    return guarded(ctx, [&] {
+        ctx->pipe.build_gauss_items();
+        *n_items = ctx->pipe.n_items;
+    });
+}
+
+int lc_evaluate_staged(lc_ctx *ctx, int mode, double *raw, int64_t *lk, uint8_t *flags) {
+    return guarded(ctx, [&] {
+        ctx->pipe.build_gauss_items();
+        ctx->pipe.run_gauss(mode, 0, ctx->pipe.n_items, nullptr, nullptr, nullptr);
+        ctx->pipe.reduce_pairs(nullptr);
+        ctx->pipe.download_results(raw, lk, flags);
+        ctx->last_gauss_ms = ctx->pipe.stage_ms(EV_GAUSS0, EV_GAUSS1);
+    });
+}
+
+int lc_run_pipeline(lc_ctx *ctx, const uint64_t *excluded_keys, int64_t n_excl, double xi, double epsilon,
+                    int max_passes, int64_t max_subsegments, int mode, int64_t *n_pairs) {
+    int rc = lc_potential_link_search(ctx, excluded_keys, n_excl, n_pairs);
+    if (rc != LC_OK) return rc;
+    int64_t nv = 0;
+    int passes = 0;
+    rc = run_discretize_abi(ctx, xi, epsilon, max_passes, max_subsegments, &nv, &passes);
+    if (rc != LC_OK) return rc;
+    return guarded(ctx, [&] {
+        ctx->pipe.build_gauss_items();
+        ctx->pipe.run_gauss(mode, 0, ctx->pipe.n_items, nullptr, nullptr, nullptr);
+        ctx->pipe.reduce_pairs(nullptr);
+    });
+}
+
+int lc_get_results(lc_ctx *ctx, double *raw, int64_t *lk, uint8_t *flags) {
+    return guarded(ctx, [&] { ctx->pipe.download_results(raw, lk, flags); });
+}
+
+int lc_stage_times(lc_ctx *ctx, float *ms) {
+    return guarded(ctx, [&] {
+        Pipeline &p = ctx->pipe;
+        ms[0] = p.stage_ms(EV_BEGIN, EV_PLS);
+        ms[1] = p.stage_ms(EV_PLS, EV_DISC);
+        ms[2] = p.stage_ms(EV_GAUSS0, EV_GAUSS1);
+        ms[3] = p.stage_ms(EV_GAUSS1, EV_END);
     });
 }
 

@@ -1,0 +1,66 @@
+// Adaptive homotopy-safe discretization on the device (linkcert/discretize.py:112-191).
+#pragma once
+#include <vector>
+
+#include "common.cuh"
+
+namespace lc {
+
+enum DiscErrKind : int {
+    DISC_OK = 0,
+    DISC_ZERO_LENGTH = 1,       // ZeroLengthInput, loops = (idx,)
+    DISC_CURVES_INTERSECT = 2,  // CurvesIntersect, loops = (a, b) sorted
+    DISC_SUBSEG_BUDGET = 3,     // PassLimitExceeded, loops = (i,)   (max_subsegments)
+    DISC_PASS_BUDGET = 4,       // PassLimitExceeded, loops = busy   (max_passes)
+    DISC_INVALID_POLYLINE = 5,  // ValidationError from PolylineLoop, loops = (idx,), detail = reason
+};
+
+enum PolylineInvalid : int { PL_OK = 0, PL_TOO_FEW = 1, PL_NONFINITE = 2, PL_ZERO_SEGMENT = 3 };
+
+struct DiscError {
+    int kind = DISC_OK;
+    int detail = 0;
+    std::vector<int64_t> loops;
+};
+
+struct DiscParams {
+    double xi = 1.0;
+    double epsilon = 2.220446049250313e-16;   // discretize.py:27 (MACHINE_EPS)
+    int max_passes = 64;
+    int64_t max_subsegments = int64_t(1) << 22;
+};
+
+struct DiscScratch {
+    DevBuf paired, act_seg, act_loop, act_tlo, act_thi, act_off, nxt_seg, nxt_loop, nxt_tlo, nxt_thi, nxt_off,
+        nxt_partner, box, nxt_box, skey[3], sperm[3], iota, pair_axis, sweep_off, mark, first_pair, mark_scan,
+        done_seg, done_tlo, done_seg2, done_tlo2, sort_idx, sort_idx2, done_cnt, done_off, bad_first, counters,
+        cub_tmp, loop_err, val_flags, ucnt;
+    int64_t cap_act = 0, cap_done = 0;
+};
+
+struct DiscInput {
+    const double *coeffs;    // (M, 12)
+    const double *t;         // (M, 2)
+    const int64_t *loff;     // (L+1)
+    const int32_t *seg_loop; // (M)
+    const double *seg_box;   // SoA 6 x M
+    const double *loop_box;  // SoA 6 x L
+    int64_t L, M;
+    const int32_t *pairs;    // (P, 2), sorted PairList
+    int64_t P;
+};
+
+struct DiscOutput {
+    DevBuf verts;     // AoS (V, 3), start points, no closing vertex
+    DevBuf vert_off;  // (L+1)
+    int64_t V = 0;
+    int passes = 0;
+    int64_t splits = 0;
+};
+
+// Returns false and fills *err on a reference error (nothing else is thrown
+// for input-dependent failures).
+bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc, DiscOutput &out,
+                    DiscError *err, cudaStream_t s);
+
+}  // namespace lc

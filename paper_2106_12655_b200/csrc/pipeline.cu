@@ -6,24 +6,145 @@
 
 namespace lc {
 
-void Pipeline::init(cudaStream_t st) { s = st; }
+namespace {
+__global__ void closed_offsets_kernel(const int64_t *__restrict__ off, int64_t L, int64_t *__restrict__ voff) {
+    const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (l <= L) voff[l] = off[l] + l;
+}
+}  // namespace
+
+void Pipeline::init(cudaStream_t st) {
+    s = st;
+    for (auto &e : ev) LC_CUDA(cudaEventCreate(&e));
+}
 
 void Pipeline::release() {
-    DevBuf *bufs[] = {&d_aos, &d_in_off, &d_voff, &d_X, &d_Y, &d_Z, &d_exp, &d_pairs, &d_pg,
-                      &d_item_off, &d_scan, &d_counter, &d_partials, &d_raw, &d_lk, &d_flags,
-                      &d_quads, &d_qout};
+    DevBuf *bufs[] = {&d_coeffs, &d_t, &d_loff, &d_seg_box, &d_seg_loop, &d_loop_box, &d_aos, &d_in_off, &d_voff,
+                      &d_X, &d_Y, &d_Z, &d_exp, &d_pairs, &d_pg, &d_item_off, &d_scan, &d_counter, &d_partials,
+                      &d_raw, &d_lk, &d_flags, &d_quads, &d_qout, &dout.verts, &dout.vert_off};
     for (DevBuf *b : bufs) b->release(s);
+    DevBuf *pb[] = {&pls_sc.keys, &pls_sc.keys_sorted, &pls_sc.idx, &pls_sc.perm, &pls_sc.counts, &pls_sc.offs,
+                    &pls_sc.cub_tmp, &pls_sc.pair_keys, &pls_sc.pair_keys_sorted, &pls_sc.axis, &pls_sc.excl};
+    for (DevBuf *b : pb) b->release(s);
+    DiscScratch &d = disc_sc;
+    DevBuf *db[] = {&d.paired, &d.act_seg, &d.act_loop, &d.act_tlo, &d.act_thi, &d.act_off, &d.nxt_seg,
+                    &d.nxt_loop, &d.nxt_tlo, &d.nxt_thi, &d.nxt_off, &d.nxt_partner, &d.box, &d.nxt_box,
+                    &d.skey[0], &d.skey[1], &d.skey[2], &d.sperm[0], &d.sperm[1], &d.sperm[2], &d.iota,
+                    &d.pair_axis, &d.sweep_off, &d.mark, &d.first_pair, &d.mark_scan, &d.done_seg, &d.done_tlo,
+                    &d.done_seg2, &d.done_tlo2, &d.sort_idx, &d.sort_idx2, &d.done_cnt, &d.done_off,
+                    &d.bad_first, &d.counters, &d.cub_tmp, &d.loop_err, &d.val_flags, &d.ucnt};
+    for (DevBuf *b : db) b->release(s);
     if (s) cudaStreamSynchronize(s);
-    h_stage.release();
+    for (auto &e : ev)
+        if (e) cudaEventDestroy(e);
 }
+
+float Pipeline::stage_ms(int e0, int e1) {
+    float ms = 0.f;
+    LC_CUDA(cudaEventSynchronize(ev[e1]));
+    LC_CUDA(cudaEventElapsedTime(&ms, ev[e0], ev[e1]));
+    return ms;
+}
+
+// ------------------------------------------------------------------ model
+
+void Pipeline::upload_model(const double *coeffs, const double *t, const int64_t *loff, int64_t nloops) {
+    L = nloops;
+    M = L > 0 ? loff[L] : 0;
+    if (L > 0 && loff[0] != 0) throw Error(LC_ERR_ARG, "loop offsets must start at 0");
+    for (int64_t l = 0; l < L; ++l)
+        if (loff[l + 1] < loff[l]) throw Error(LC_ERR_ARG, "loop offsets must be non-decreasing");
+    d_coeffs.reserve(sizeof(double) * 12 * (M > 0 ? M : 1), s);
+    d_t.reserve(sizeof(double) * 2 * (M > 0 ? M : 1), s);
+    d_loff.reserve(sizeof(int64_t) * (L + 1), s);
+    d_seg_box.reserve(sizeof(double) * 6 * (M > 0 ? M : 1), s);
+    d_seg_loop.reserve(sizeof(int32_t) * (M > 0 ? M : 1), s);
+    d_loop_box.reserve(sizeof(double) * 6 * (L > 0 ? L : 1), s);
+    d_exp.reserve(sizeof(int) * 2, s);
+    if (M > 0) {
+        LC_CUDA(cudaMemcpyAsync(d_coeffs.ptr, coeffs, sizeof(double) * 12 * M, cudaMemcpyHostToDevice, s));
+        LC_CUDA(cudaMemcpyAsync(d_t.ptr, t, sizeof(double) * 2 * M, cudaMemcpyHostToDevice, s));
+    }
+    LC_CUDA(cudaMemcpyAsync(d_loff.ptr, loff, sizeof(int64_t) * (L + 1), cudaMemcpyHostToDevice, s));
+    // tight segment boxes + loop boxes (shared by PLS and discretization pass 1)
+    launch_seg_boxes(d_coeffs.as<double>(), d_t.as<double>(), d_loff.as<int64_t>(), L, M, -1.0,
+                     d_seg_box.as<double>(), d_seg_loop.as<int32_t>(), d_exp.as<int>() + 1, s);
+    launch_loop_boxes(d_seg_box.as<double>(), M, d_loff.as<int64_t>(), L, d_loop_box.as<double>(), s);
+    model_ready = true;
+    polylines_ready = false;
+    P = 0;
+    // the caller's host buffers may be released after return
+    LC_CUDA(cudaStreamSynchronize(s));
+}
+
+int64_t Pipeline::potential_link_search(const uint64_t *excl_keys, int64_t n_excl) {
+    if (!model_ready) throw Error(LC_ERR_STATE, "no model uploaded");
+    LC_CUDA(cudaEventRecord(ev[EV_BEGIN], s));
+    P = run_pls(d_loop_box.as<double>(), L, excl_keys, n_excl, pls_sc, d_pairs, s);
+    LC_CUDA(cudaEventRecord(ev[EV_PLS], s));
+    return P;
+}
+
+bool Pipeline::discretize(const DiscParams &prm) {
+    if (!model_ready) throw Error(LC_ERR_STATE, "no model uploaded");
+    DiscInput in{d_coeffs.as<double>(), d_t.as<double>(), d_loff.as<int64_t>(), d_seg_loop.as<int32_t>(),
+                 d_seg_box.as<double>(), d_loop_box.as<double>(), L, M, d_pairs.as<int32_t>(), P};
+    derr = DiscError();
+    polylines_ready = false;
+    if (!run_discretize(in, prm, disc_sc, dout, &derr, s)) return false;
+    // Gauss input: closed SoA, scaled by an exact power of two
+    V = dout.V;
+    Vc = V + L;
+    d_voff.reserve(sizeof(int64_t) * (L + 1), s);
+    d_X.reserve(sizeof(double) * (Vc + 1), s);
+    d_Y.reserve(sizeof(double) * (Vc + 1), s);
+    d_Z.reserve(sizeof(double) * (Vc + 1), s);
+    closed_offsets_kernel<<<(unsigned)ceil_div(L + 1, 256), 256, 0, s>>>(dout.vert_off.as<int64_t>(), L,
+                                                                          d_voff.as<int64_t>());
+    LC_CHECK_LAUNCH();
+    LC_CUDA(cudaMemsetAsync(d_exp.ptr, 0, sizeof(int), s));
+    launch_max_exponent(dout.verts.as<double>(), 3 * V, d_exp.as<int>(), s);
+    launch_pack_closed_soa(dout.verts.as<double>(), dout.vert_off.as<int64_t>(), d_voff.as<int64_t>(), L, Vc,
+                           d_exp.as<int>(), d_X.as<double>(), d_Y.as<double>(), d_Z.as<double>(), s);
+    LC_CUDA(cudaEventRecord(ev[EV_DISC], s));
+    polylines_ready = true;
+    return true;
+}
+
+void Pipeline::download_loop_boxes(double *lo, double *hi) {
+    if (!model_ready) throw Error(LC_ERR_STATE, "no model uploaded");
+    std::vector<double> b((size_t)6 * L);
+    if (L > 0)
+        LC_CUDA(cudaMemcpyAsync(b.data(), d_loop_box.ptr, sizeof(double) * 6 * L, cudaMemcpyDeviceToHost, s));
+    LC_CUDA(cudaStreamSynchronize(s));
+    for (int64_t l = 0; l < L; ++l)
+        for (int d = 0; d < 3; ++d) {
+            lo[3 * l + d] = b[d * L + l];
+            hi[3 * l + d] = b[(3 + d) * L + l];
+        }
+}
+
+void Pipeline::download_polylines(double *verts, int64_t *vert_off) {
+    if (!polylines_ready) throw Error(LC_ERR_STATE, "no discretized polylines");
+    if (V > 0 && verts)
+        LC_CUDA(cudaMemcpyAsync(verts, dout.verts.ptr, sizeof(double) * 3 * V, cudaMemcpyDeviceToHost, s));
+    if (vert_off)
+        LC_CUDA(cudaMemcpyAsync(vert_off, dout.vert_off.ptr, sizeof(int64_t) * (L + 1), cudaMemcpyDeviceToHost, s));
+    LC_CUDA(cudaStreamSynchronize(s));
+}
+
+// ------------------------------------------------------------------ gauss
 
 // Host AoS polylines (no closing vertex; loop v = rows [vert_off[v], vert_off[v+1]))
 // -> device closed SoA with vertex 0 repeated at the end of every loop
 // (direct.py:164-166 _closed), scaled by an exact power of two.
 void Pipeline::upload_polylines(const double *verts, const int64_t *vert_off, int64_t nloops) {
     L = nloops;
+    model_ready = false;
     V = L > 0 ? vert_off[L] - vert_off[0] : 0;
     if (L > 0 && vert_off[0] != 0) throw Error(LC_ERR_ARG, "vert_off[0] must be 0");
+    for (int64_t l = 0; l < L; ++l)
+        if (vert_off[l + 1] < vert_off[l]) throw Error(LC_ERR_ARG, "vert_off must be non-decreasing");
     h_voff.resize((size_t)L + 1);
     for (int64_t v = 0; v <= L; ++v) h_voff[v] = (L > 0 ? vert_off[v] : 0) + v;
     Vc = V + L;
@@ -33,7 +154,7 @@ void Pipeline::upload_polylines(const double *verts, const int64_t *vert_off, in
     d_X.reserve(sizeof(double) * (size_t)(Vc + 1), s);
     d_Y.reserve(sizeof(double) * (size_t)(Vc + 1), s);
     d_Z.reserve(sizeof(double) * (size_t)(Vc + 1), s);
-    d_exp.reserve(sizeof(int), s);
+    d_exp.reserve(sizeof(int) * 2, s);
     if (V > 0) LC_CUDA(cudaMemcpyAsync(d_aos.ptr, verts, sizeof(double) * 3 * V, cudaMemcpyHostToDevice, s));
     if (L > 0) {
         LC_CUDA(cudaMemcpyAsync(d_in_off.ptr, vert_off, sizeof(int64_t) * (L + 1), cudaMemcpyHostToDevice, s));
@@ -43,7 +164,7 @@ void Pipeline::upload_polylines(const double *verts, const int64_t *vert_off, in
     launch_max_exponent(d_aos.as<double>(), 3 * V, d_exp.as<int>(), s);
     launch_pack_closed_soa(d_aos.as<double>(), d_in_off.as<int64_t>(), d_voff.as<int64_t>(), L, Vc,
                            d_exp.as<int>(), d_X.as<double>(), d_Y.as<double>(), d_Z.as<double>(), s);
-    // the caller's host buffers may be released after return
+    polylines_ready = true;
     LC_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -58,7 +179,13 @@ void Pipeline::upload_pairs(const int32_t *pairs, int64_t npairs) {
     LC_CUDA(cudaStreamSynchronize(s));
 }
 
+void Pipeline::download_pairs(int32_t *pairs) {
+    if (P > 0) LC_CUDA(cudaMemcpyAsync(pairs, d_pairs.ptr, sizeof(int32_t) * 2 * P, cudaMemcpyDeviceToHost, s));
+    LC_CUDA(cudaStreamSynchronize(s));
+}
+
 void Pipeline::build_gauss_items() {
+    if (!polylines_ready) throw Error(LC_ERR_STATE, "no polylines staged");
     d_pg.reserve(sizeof(PairGeom) * (size_t)(P > 0 ? P : 1), s);
     d_item_off.reserve(sizeof(int64_t) * (size_t)(P + 1), s);
     const size_t scan_bytes = build_items_scan_bytes(P > 0 ? P : 1);
@@ -76,17 +203,18 @@ void Pipeline::run_gauss(int mode, int64_t item_begin, int64_t item_end, double 
                          cudaEvent_t ev0, cudaEvent_t ev1) {
     if (mode < GAUSS_PHASE || mode > GAUSS_REF) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
     double *out = partials_ext ? partials_ext : d_partials.as<double>();
-    if (ev0) LC_CUDA(cudaEventRecord(ev0, s));
+    LC_CUDA(cudaEventRecord(ev0 ? ev0 : ev[EV_GAUSS0], s));
     launch_gauss_items(mode, d_X.as<double>(), d_Y.as<double>(), d_Z.as<double>(), d_pg.as<PairGeom>(),
                        d_item_off.as<int64_t>(), P, item_begin, item_end,
                        d_counter.as<unsigned long long>(), out, s);
-    if (ev1) LC_CUDA(cudaEventRecord(ev1, s));
+    LC_CUDA(cudaEventRecord(ev1 ? ev1 : ev[EV_GAUSS1], s));
 }
 
 void Pipeline::reduce_pairs(const double *partials_ext) {
     const double *in = partials_ext ? partials_ext : d_partials.as<double>();
     launch_reduce_pairs(in, d_item_off.as<int64_t>(), P, d_raw.as<double>(), d_lk.as<int64_t>(),
                         d_flags.as<uint8_t>(), s);
+    LC_CUDA(cudaEventRecord(ev[EV_END], s));
 }
 
 void Pipeline::download_results(double *raw, int64_t *lk, uint8_t *flags) {

@@ -1,0 +1,222 @@
+"""Parity of the sm_100a path (through the C-ABI) with the reference goldens and the oracle.
+
+Bars (BASELINE.json north_star): integer linking numbers, PLS pair sets,
+discretized vertices and verify lists bit-exact; raw per-pair sums within
+RAW_TOL = 1e-9 absolute.
+"""
+
+import hashlib
+import warnings
+
+import numpy as np
+import pytest
+
+import cases
+import paper_2106_12655_b200 as lc
+from paper_2106_12655_b200 import _native
+from paper_2106_12655_b200.certify import ABORTED, FAIL, PASS
+
+pytestmark = pytest.mark.gpu
+
+RAW_TOL = 1e-9
+MODES = [_native.GAUSS_PHASE, _native.GAUSS_ATAN, _native.GAUSS_REF]
+
+
+def test_segment_pair_lambda(gpu, golden_arrays):
+    q = golden_arrays["quads"]
+    got = gpu.segment_pair_lambda(q)
+    want = golden_arrays["quads_lambda"]
+    assert np.max(np.abs(got - want)) < 1e-13
+    assert lc.segment_pair_lambda(q[0, 0:3], q[0, 3:6], q[0, 6:9], q[0, 9:12]) == pytest.approx(want[0], abs=1e-15)
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("name", list(cases.link_cases()))
+def test_link_direct_modes(gpu, golden, name, mode):
+    g = golden["links"][name]
+    m = cases.link_cases()[name]
+    assert cases.fingerprint(m) == g["fingerprint"]
+    a, b = (lp.start_points() for lp in m.loops)
+    raw = gpu.link_direct(a, b, mode)
+    assert abs(raw - g["atan"]) < RAW_TOL
+    assert round(raw) == round(g["atan"])
+    assert abs(gpu.link_direct(b, a, mode) - g["atan_swapped"]) < RAW_TOL
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("k", range(4))
+def test_random_polygons(gpu, golden, golden_arrays, k, mode):
+    a, b = golden_arrays[f"rand_a{k}"], golden_arrays[f"rand_b{k}"]
+    assert abs(gpu.link_direct(a, b, mode) - golden["links"][f"random_{k}"]["atan"]) < RAW_TOL
+
+
+ALL_CERTS = list(cases.cert_models(full=True))
+
+
+@pytest.fixture(scope="module")
+def cert_models():
+    return cases.cert_models(full=True)
+
+
+@pytest.mark.parametrize("name", ALL_CERTS)
+def test_pls_pairs_exact(golden, golden_arrays, cert_models, name):
+    m = cert_models[name]
+    assert cases.fingerprint(m) == golden["certs"][name]["fingerprint"]
+    pl = lc.potential_link_search(m)
+    assert np.array_equal(pl.array, golden_arrays[f"{name}__pairs"])
+
+
+@pytest.mark.parametrize("name", ALL_CERTS)
+def test_discretize_bitwise(golden, golden_arrays, cert_models, name):
+    m = cert_models[name]
+    polys = lc.discretize(m, lc.potential_link_search(m))
+    verts = np.concatenate([p.vertices for p in polys])
+    assert len(verts) == golden["certs"][name]["discretized_vertices"]
+    assert hashlib.sha256(verts.tobytes()).hexdigest() == golden["certs"][name]["discretized_sha256"]
+
+
+@pytest.mark.parametrize("name", ALL_CERTS)
+def test_certificate_exact(golden, golden_arrays, cert_models, name):
+    m = cert_models[name]
+    timings = {}
+    mat = lc.compute_linking_matrix(m, timings=timings)
+    assert np.array_equal(mat.array, golden_arrays[f"{name}__entries"])
+    assert mat.model_digest == golden["certs"][name]["digest"]
+    assert mat.kernel_tag == "ds:atan"
+    assert {"pls", "discretize", "kernel"} <= set(timings)
+
+
+@pytest.mark.parametrize("name", ["grid6_pull", "e4in1_32x32_pull165", "kusari_small_after", "kusari_full_after"])
+def test_verify_reports_exact(golden, name):
+    g = golden["verify"][name]
+    before, after = cases.edit_cases(full=name.startswith("kusari_full"))[name]
+    assert cases.fingerprint(after) == g["after_fingerprint"]
+    cert = lc.compute_linking_matrix(before)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        rep = lc.verify(after, cert)
+        rep_ee = lc.verify(after, cert, early_exit=True)
+    for r, want in ((rep, g["full"]), (rep_ee, g["early_exit"])):
+        assert r.status == want["status"]
+        assert [list(p) for p in r.destroyed] == want["destroyed"]
+        assert [list(p) for p in r.created] == want["created"]
+        assert [list(p) for p in r.changed] == want["changed"]
+        assert (list(r.first_failure) if r.first_failure else None) == want["first_failure"]
+    assert lc.verify(before, cert).status == PASS
+
+
+@pytest.mark.parametrize("name", list(cases.disc_error_cases()))
+def test_discretize_errors(golden, golden_arrays, name):
+    g = golden["discretize"][name]
+    m, prs, kw = cases.disc_error_cases()[name]
+    params = lc.DiscretizationParams(**kw)
+    if g["ok"]:
+        polys = lc.discretize(m, lc.PairList(tuple(prs)), params)
+        assert np.array_equal(np.concatenate([p.vertices for p in polys]), golden_arrays[f"disc_{name}__verts"])
+    else:
+        with pytest.raises(lc.DiscretizationError) as e:
+            lc.discretize(m, lc.PairList(tuple(prs)), params)
+        assert e.value.kind == g["kind"]
+        assert list(e.value.loops) == g["loops"]
+        assert str(e.value) == g["message"]
+
+
+def test_raw_parity_vs_oracle_seeded(gpu, oracle):
+    """Seeded random loop batches: raw within RAW_TOL, integers exact, every mode."""
+    rng = np.random.default_rng(7)
+    loops = [rng.normal(size=(int(n), 3)) * 2.0 for n in rng.integers(3, 300, size=40)]
+    off = np.concatenate([[0], np.cumsum([len(x) for x in loops])]).astype(np.int64)
+    verts = np.concatenate(loops)
+    pairs = np.array([(i, j) for i in range(40) for j in range(i + 1, 40)], dtype=np.int32)
+    want = oracle.evaluate_pairs(verts, off, pairs)
+    for mode in MODES:
+        raw, lk, flags = gpu.evaluate_pairs(verts, off, pairs, mode)
+        assert np.max(np.abs(raw - want)) < RAW_TOL
+        ok = np.abs(want - np.round(want)) <= 0.25
+        assert np.array_equal(lk[ok], np.round(want[ok]).astype(np.int64))
+
+
+def test_deterministic_and_split_invariant(gpu):
+    """Bitwise identical raw sums run to run and for any split of the item range (multi-GPU contract)."""
+    import torch
+
+    m = lc.generators.kusari_tube(n_around=24, rows=8, partial=10)
+    coeffs, t, off = m.packed()
+    gpu.upload_model(coeffs, t, off)
+    gpu.run_pipeline(None, m.xi, 2.220446049250313e-16, 64, 1 << 22)
+    raw0, lk0, _ = gpu.get_results()
+    raw1, lk1, _ = gpu.evaluate_staged(_native.GAUSS_PHASE)
+    assert np.array_equal(raw0.view(np.int64), raw1.view(np.int64))
+    n = gpu.prepare_gauss()
+    for world in (2, 3, 8):
+        buf = torch.zeros(n, dtype=torch.float64, device="cuda")
+        for r in range(world):
+            b, e, _ = lc.certify.item_range(n, r, world)
+            gpu.gauss_run(_native.GAUSS_PHASE, b, e, buf.data_ptr())
+        gpu.synchronize()
+        raw2, lk2, _ = gpu.gauss_reduce(buf.data_ptr())
+        assert np.array_equal(raw0.view(np.int64), raw2.view(np.int64))
+
+
+def test_big_pair_accuracy(gpu, oracle):
+    """C5-style ribbon: 20k x 20k vs the oracle, 100k x 100k vs the analytic lambda."""
+    a, b = lc.generators.ribbon_pair(10, 20000)
+    want = oracle.link_direct(a, b)
+    for mode in MODES:
+        assert abs(gpu.link_direct(a, b, mode) - want) < RAW_TOL
+    a, b = lc.generators.ribbon_pair(10, 100000)
+    for mode in (_native.GAUSS_PHASE, _native.GAUSS_ATAN):
+        assert abs(gpu.link_direct(a, b, mode) - 10.0) < RAW_TOL
+
+
+def test_knit_tube_rows_sample(gpu, oracle):
+    """C4 building block at reduced size: adjacent courses link -W; rows sample vs oracle."""
+    m = lc.generators.knit_tube(courses=4, n=20000, W=100)
+    mat = lc.compute_linking_matrix(m)
+    assert mat.entries == ((0, 1, -100), (1, 2, -100), (2, 3, -100))
+    a, b = (lp.control_points for lp in m.loops[:2])
+    full = oracle.link_direct(a, b)
+    assert abs(gpu.link_direct(a, b) - full) < RAW_TOL
+
+
+def test_edge_cases(gpu):
+    ex, ey, ez = np.eye(3)
+    with pytest.raises(lc.ValidationError):
+        lc.potential_link_search(lc.CurveModel([]))
+    single = lc.CurveModel([lc.LoopGeometry.from_polyline(cases.circ(8, (0, 0, 0), ex, ey))])
+    assert len(lc.potential_link_search(single)) == 0
+    assert lc.compute_linking_matrix(single).entries == ()
+    a = cases.circ(16, (0, 0, 0), ex, ey)
+    b = cases.circ(16, (1.0, 0, 0), ez, ex)
+    hopf = lc.CurveModel([lc.LoopGeometry.from_polyline(p) for p in (a, b)])
+    assert lc.compute_linking_matrix(hopf, excluded={(1, 0)}).entries == ()
+    assert lc.compute_linking_matrix(hopf).entries == ((0, 1, 1),)
+    # NaN raw -> ValueError like round(nan)
+    nan = a.copy()
+    nan[3, 0] = np.nan
+    with pytest.raises(ValueError):
+        lc.compute_link(nan, b)
+    # empty pair list through the batched seam
+    raw, lk, flags = gpu.evaluate_pairs(np.concatenate([a, b]), np.array([0, 16, 32]), np.zeros((0, 2), np.int32))
+    assert raw.shape == (0,)
+
+
+def test_env_mode_selection(monkeypatch):
+    ex, ey, ez = np.eye(3)
+    a = cases.circ(100, (0, 0, 0), ex, ey)
+    b = cases.circ(100, (1.0, 0, 0), ez, ex)
+    for name in ("phase", "atan", "ref"):
+        monkeypatch.setenv("LINKCERT_GAUSS_MODE", name)
+        assert lc.link_direct(a, b) == pytest.approx(1.0, abs=1e-12)
+    monkeypatch.setenv("LINKCERT_GAUSS_MODE", "bogus")
+    with pytest.raises(ValueError):
+        lc.link_direct(a, b)
+
+
+def test_no_cpu_fallback_when_library_missing(monkeypatch, tmp_path):
+    """The product path must fail loudly without the CUDA library (no oracle, no numpy fallback)."""
+    monkeypatch.setattr(_native, "LIB_PATH", tmp_path / "missing.so")
+    monkeypatch.setattr(_native, "_lib", None)
+    monkeypatch.setattr(_native, "_ctx", {})
+    with pytest.raises(_native.NativeUnavailable):
+        lc.link_direct(np.eye(3), np.eye(3) + 5)
