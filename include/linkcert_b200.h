@@ -159,6 +159,29 @@ LC_API int lc_get_results(lc_ctx *ctx, double *raw, int64_t *lk, uint8_t *flags)
 /* Device times (ms) of the last pipeline: [PLS, discretize, Gauss kernel, reduce]. */
 LC_API int lc_stage_times(lc_ctx *ctx, float *ms);
 
+/* ---- Canonical model serialization (host, multithreaded) ----
+ * Bytes of json.dumps(model_to_dict(model), sort_keys=True,
+ * separators=(",", ":")) (model_io.py:122-172) for a packed model; the
+ * caller hashes them (SHA-256) to obtain model_digest.  closed: one byte per
+ * loop (NULL = all closed).  Returns the length, -1 for a non-finite
+ * coordinate, -2 if cap is too small (size with lc_model_json_bound). */
+LC_API int64_t lc_model_json_bound(const int64_t *loop_off, int64_t L);
+LC_API int64_t lc_model_json(const double *coeffs, const double *t, const int64_t *loop_off,
+                             const uint8_t *closed, int64_t L, int nthreads, char *out, int64_t cap);
+/* Drop-in for model_io.model_digest (model_io.py:169-172): SHA-256 hex (65
+ * bytes incl. NUL) of the canonical JSON, formatted on nthreads workers and
+ * hashed in stream order (SHA-NI when available).  -1: non-finite coordinate. */
+LC_API int lc_model_digest(const double *coeffs, const double *t, const int64_t *loop_off,
+                           const uint8_t *closed, int64_t L, int nthreads, char *hex_out);
+/* SHA-256 hex of a buffer (test hook; force_portable skips SHA-NI); returns 1 if SHA-NI exists. */
+LC_API int lc_sha256_hex(const void *data, int64_t n, int force_portable, char *hex_out);
+/* CPython float.__repr__ of x into out (>= 32 bytes); returns the length. */
+LC_API int lc_float_repr(double x, char *out);
+
+/* Kernel launches issued by the library so far, all contexts (own kernels
+ * exactly; each CUB device-algorithm call counted once). */
+LC_API long long lc_launch_count(void);
+
 /* FP64 DFMA-chain throughput probe (roofline denominator), FLOP/s. */
 LC_API int lc_probe_fp64_peak(lc_ctx *ctx, double *flops, float *ms);
 

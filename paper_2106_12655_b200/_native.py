@@ -74,7 +74,61 @@ SIGNATURES = {
                                         ctypes.c_int64, ctypes.c_int, _c_int64_p]),
     "lc_get_results": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "lc_stage_times": (ctypes.c_int, [_vp, _c_float_p]),
+    "lc_model_json_bound": (ctypes.c_int64, [_vp, ctypes.c_int64]),
+    "lc_model_json": (ctypes.c_int64, [_vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, ctypes.c_int64]),
+    "lc_float_repr": (ctypes.c_int, [ctypes.c_double, ctypes.c_char_p]),
+    "lc_model_digest": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p]),
+    "lc_sha256_hex": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p]),
+    "lc_launch_count": (ctypes.c_longlong, []),
 }
+
+
+def launch_count():
+    return int(load_library().lc_launch_count())
+
+
+def model_digest(coeffs, t, loop_off, closed=None, nthreads=0):
+    """SHA-256 hex of the canonical model JSON (host C++; GIL released); None if non-finite."""
+    lib = load_library()
+    coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+    t = np.ascontiguousarray(t, dtype=np.float64)
+    loop_off = np.ascontiguousarray(loop_off, dtype=np.int64)
+    cl = None if closed is None else np.ascontiguousarray(closed, dtype=np.uint8)
+    out = ctypes.create_string_buffer(65)
+    rc = lib.lc_model_digest(_ptr(coeffs), _ptr(t), _ptr(loop_off), _ptr(cl), len(loop_off) - 1, int(nthreads), out)
+    return None if rc != 0 else out.value.decode()
+
+
+def sha256_hex(data, force_portable=False):
+    buf = np.frombuffer(bytes(data), dtype=np.uint8)
+    out = ctypes.create_string_buffer(65)
+    has = load_library().lc_sha256_hex(_ptr(buf), buf.size, int(force_portable), out)
+    return out.value.decode(), bool(has)
+
+
+def model_json(coeffs, t, loop_off, closed=None, nthreads=0):
+    """Canonical json-curves bytes of a packed model (host C++, GIL released)."""
+    lib = load_library()
+    coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+    t = np.ascontiguousarray(t, dtype=np.float64)
+    loop_off = np.ascontiguousarray(loop_off, dtype=np.int64)
+    L = len(loop_off) - 1
+    cl = None if closed is None else np.ascontiguousarray(closed, dtype=np.uint8)
+    cap = lib.lc_model_json_bound(_ptr(loop_off), L)
+    buf = np.empty(cap, dtype=np.uint8)
+    n = lib.lc_model_json(_ptr(coeffs), _ptr(t), _ptr(loop_off), _ptr(cl), L, int(nthreads),
+                          buf.ctypes.data_as(ctypes.c_void_p), cap)
+    if n == -1:
+        return None
+    if n < 0:
+        raise NativeError(LC_ERR_STATE, "lc_model_json: buffer too small")
+    return memoryview(buf)[:n]
+
+
+def float_repr(x):
+    out = ctypes.create_string_buffer(40)
+    n = load_library().lc_float_repr(float(x), out)
+    return out.raw[:n].decode()
 
 # lc_discretize_error kinds
 DISC_OK = 0
@@ -242,6 +296,11 @@ class Context:
 
     def synchronize(self):
         _check(self.lib.lc_synchronize(self.handle))
+
+    def set_stream(self, cuda_stream_ptr):
+        """Launch on a caller stream (e.g. torch.cuda.current_stream().cuda_stream); 0/None = own stream."""
+        with self.lock:
+            _check(self.lib.lc_set_stream(self.handle, ctypes.c_void_p(cuda_stream_ptr) if cuda_stream_ptr else None))
 
     # ---- model pipeline -------------------------------------------------------
     def tight_boxes(self, coeffs, t):

@@ -14,8 +14,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "liblinkcert_b200.so"
-SOURCES = ["abi.cu", "pipeline.cu", "gauss.cu", "pls.cu", "discretize.cu", "probe.cu"]
-HEADERS = ["common.cuh", "gauss.cuh", "pipeline.cuh", "pls.cuh", "discretize.cuh"]
+SOURCES = ["abi.cu", "pipeline.cu", "gauss.cu", "pls.cu", "discretize.cu", "probe.cu", "digest.cpp"]
+HEADERS = ["common.cuh", "gauss.cuh", "pipeline.cuh", "pls.cuh", "discretize.cuh", "geom.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 NVCC_FLAGS = [

@@ -218,16 +218,16 @@ def _sharded_gauss(ctx, mode, dist):
     return ctx.gauss_reduce(gathered.data_ptr())
 
 
-def run_device_pipeline(model: CurveModel, excluded=(), params=None, timings=None, ctx=None):
-    """PLS -> discretize -> Gauss sum on the GPU.  Returns (pairs int32 (P,2), raw, lk, flags, ctx)."""
-    params = params or DiscretizationParams()
-    mode = gauss_mode()
+def device_step(ctx, xi, excl_keys, params, mode=None, timings=None):
+    """One pass of the hot path over the model resident on `ctx`:
+    PLS -> discretize -> Gauss sum (sharded + all-gathered under torch.distributed).
+    Returns (pairs int32 (P,2), raw, lk, flags) on the host."""
+    mode = gauss_mode() if mode is None else mode
     t0 = time.perf_counter()
-    ctx = upload(model, ctx)
-    ctx.potential_link_search(excluded_keys(excluded))
+    ctx.potential_link_search(excl_keys)
     t1 = time.perf_counter()
     try:
-        ctx.discretize(model.xi, params.epsilon, params.max_passes, params.max_subsegments)
+        ctx.discretize(xi, params.epsilon, params.max_passes, params.max_subsegments)
     except _native.DiscretizeFailure as fail:
         raise_for_failure(fail, params)
     t2 = time.perf_counter()
@@ -237,12 +237,37 @@ def run_device_pipeline(model: CurveModel, excluded=(), params=None, timings=Non
     else:
         raw, lk, flags = ctx.evaluate_staged(mode)
     pairs = ctx.get_pairs()
-    t3 = time.perf_counter()
     if timings is not None:
-        timings["pls"] = t1 - t0
+        timings["pls"] = timings.get("upload", 0.0) + (t1 - t0)
         timings["discretize"] = t2 - t1
-        timings["kernel"] = t3 - t2
+        timings["kernel"] = time.perf_counter() - t2
+    return pairs, raw, lk, flags
+
+
+def run_device_pipeline(model: CurveModel, excluded=(), params=None, timings=None, ctx=None):
+    """Upload the packed model, then device_step.  Returns (pairs, raw, lk, flags, ctx)."""
+    params = params or DiscretizationParams()
+    t0 = time.perf_counter()
+    ctx = upload(model, ctx)
+    if timings is not None:
+        timings["upload"] = time.perf_counter() - t0
+    pairs, raw, lk, flags = device_step(ctx, model.xi, excluded_keys(excluded), params, timings=timings)
+    if timings is not None:
+        timings.pop("upload", None)
     return pairs, raw, lk, flags, ctx
+
+
+_digest_pool = None
+
+
+def _digest_async(model):
+    """model_digest on a helper thread (native, GIL released) to overlap it with the GPU."""
+    global _digest_pool
+    if _digest_pool is None:
+        from concurrent.futures import ThreadPoolExecutor
+
+        _digest_pool = ThreadPoolExecutor(max_workers=1, thread_name_prefix="linkcert-digest")
+    return _digest_pool.submit(model_digest, model)
 
 
 def _raise_for_flags(raw, flags, order=None):
@@ -307,14 +332,21 @@ def compute_linking_matrix(
         arr = np.zeros((0, 3), dtype=np.int64)
         if timings is not None:
             timings.update(pls=0.0, discretize=0.0, kernel=0.0)
+        digest = model_digest(model)
     else:
-        pairs, raw, lk, flags, _ = run_device_pipeline(model, excluded, params, timings)
-        _raise_for_flags(raw, flags)
+        fut = _digest_async(model)
+        try:
+            pairs, raw, lk, flags, _ = run_device_pipeline(model, excluded, params, timings)
+            _raise_for_flags(raw, flags)
+        except Exception:
+            fut.result()          # a serialization error would have surfaced last in the reference
+            raise
         keep = lk != 0
         arr = np.empty((int(keep.sum()), 3), dtype=np.int64)
         arr[:, :2] = pairs[keep]
         arr[:, 2] = lk[keep]
-    return LinkMatrix._from_array(model.num_loops, arr, model_digest(model), choice.tag, {})
+        digest = fut.result()
+    return LinkMatrix._from_array(model.num_loops, arr, digest, choice.tag, {})
 
 
 def verify(
@@ -335,19 +367,29 @@ def verify(
             message=(f"loop count mismatch: model has {model.num_loops}, "
                      f"certificate has {reference.num_loops}"),
         )
-    digest = model_digest(model)
-    if reference.model_digest and digest != reference.model_digest:
-        warnings.warn("model digest differs from certificate digest (deformed model?)", stacklevel=2)
-    if model.num_loops < 1:
-        raise ValidationError("model has no loops")
-    if model.num_loops == 1:
-        pairs = np.zeros((0, 2), dtype=np.int32)
-        raw = np.zeros(0)
-        lk = np.zeros(0, dtype=np.int64)
-        flags = np.zeros(0, dtype=np.uint8)
-    else:
-        pairs, raw, lk, flags, _ = run_device_pipeline(model, excluded, params)
+    # the digest (host, native) overlaps the device pipeline; its check and
+    # warning come first, as in the reference (certify.py:188-193)
+    fut = _digest_async(model)
+    try:
+        if model.num_loops < 1:
+            raise ValidationError("model has no loops")
+        if model.num_loops == 1:
+            pairs = np.zeros((0, 2), dtype=np.int32)
+            raw = np.zeros(0)
+            lk = np.zeros(0, dtype=np.int64)
+            flags = np.zeros(0, dtype=np.uint8)
+        else:
+            pairs, raw, lk, flags, _ = run_device_pipeline(model, excluded, params)
+    except Exception:
+        _warn_digest(fut.result(), reference)
+        raise
+    _warn_digest(fut.result(), reference)
     return diff_arrays(reference.array, pairs, raw, lk, flags, early_exit)
+
+
+def _warn_digest(digest, reference):
+    if reference.model_digest and digest != reference.model_digest:
+        warnings.warn("model digest differs from certificate digest (deformed model?)", stacklevel=3)
 
 
 def _lookup(sorted_keys, query):

@@ -346,6 +346,8 @@ int lc_stage_times(lc_ctx *ctx, float *ms) {
     });
 }
 
+long long lc_launch_count(void) { return launch_counter().load(); }
+
 int lc_probe_fp64_peak(lc_ctx *ctx, double *flops, float *ms) {
     return guarded(ctx, [&] { *flops = probe_dfma_flops(ctx->stream, ms); });
 }

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <stdexcept>
@@ -27,8 +28,25 @@ inline void check_cuda(cudaError_t e, const char *what, const char *file, int li
         throw Error(LC_ERR_CUDA, buf);
     }
 }
+// Kernel launches issued by the library (own kernels: one count per
+// LC_CHECK_LAUNCH; CUB device algorithms: one count per LC_CUB call, i.e. a
+// lower bound on their kernels).  Read with lc_launch_count().
+inline std::atomic<long long> &launch_counter() {
+    static std::atomic<long long> c{0};
+    return c;
+}
+
 #define LC_CUDA(x) ::lc::check_cuda((x), #x, __FILE__, __LINE__)
-#define LC_CHECK_LAUNCH() ::lc::check_cuda(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+#define LC_CHECK_LAUNCH()                                                            \
+    do {                                                                             \
+        ::lc::launch_counter().fetch_add(1, std::memory_order_relaxed);              \
+        ::lc::check_cuda(cudaGetLastError(), "kernel launch", __FILE__, __LINE__);   \
+    } while (0)
+#define LC_CUB(x)                                                                    \
+    do {                                                                             \
+        ::lc::launch_counter().fetch_add(1, std::memory_order_relaxed);              \
+        ::lc::check_cuda((x), #x, __FILE__, __LINE__);                               \
+    } while (0)
 
 // Grow-only stream-ordered device buffer.
 struct DevBuf {

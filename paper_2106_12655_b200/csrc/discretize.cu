@@ -366,9 +366,11 @@ int validate(const double *verts, const int64_t *off, int64_t L, int64_t n, cons
     LC_CUDA(cudaMemsetAsync(sc.val_flags.ptr, 0, sizeof(unsigned) * L, s));
     const int init = INT_MAX;
     LC_CUDA(cudaMemcpyAsync(sc.loop_err.ptr, &init, sizeof(int), cudaMemcpyHostToDevice, s));
-    if (n > 0)
+    if (n > 0) {
         validate_vertices_kernel<<<grid_for(n), 256, 0, s>>>(verts, off, L, n, paired, want, thr,
                                                              sc.val_flags.as<unsigned>());
+        LC_CHECK_LAUNCH();
+    }
     validate_loops_kernel<<<grid_for(L), 256, 0, s>>>(off, L, paired, want, sc.val_flags.as<unsigned>(),
                                                       sc.loop_err.as<int>());
     LC_CHECK_LAUNCH();
@@ -380,7 +382,7 @@ void scan_i64(const int64_t *in, int64_t *out, int64_t n, DiscScratch &sc, cudaS
     cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, (int)n);
     sc.cub_tmp.reserve(bytes, s);
     bytes = sc.cub_tmp.bytes;
-    LC_CUDA(cub::DeviceScan::ExclusiveSum(sc.cub_tmp.ptr, bytes, in, out, (int)n, s));
+    LC_CUB(cub::DeviceScan::ExclusiveSum(sc.cub_tmp.ptr, bytes, in, out, (int)n, s));
 }
 
 }  // namespace
@@ -483,7 +485,7 @@ bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc,
                                                 sc.act_off.as<int64_t>(), sc.act_off.as<int64_t>() + 1);
             sc.cub_tmp.reserve(bytes, s);
             bytes = sc.cub_tmp.bytes;
-            LC_CUDA(cub::DeviceSegmentedSort::SortPairs(sc.cub_tmp.ptr, bytes, tmpkey.as<double>(),
+            LC_CUB(cub::DeviceSegmentedSort::SortPairs(sc.cub_tmp.ptr, bytes, tmpkey.as<double>(),
                                                         sc.skey[a].as<double>(), sc.iota.as<int32_t>(),
                                                         sc.sperm[a].as<int32_t>(), (int)n_act, (int)L,
                                                         sc.act_off.as<int64_t>(), sc.act_off.as<int64_t>() + 1, s));
@@ -622,14 +624,14 @@ bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc,
         size_t bytes = sc.cub_tmp.bytes;
         // by tlo (scratch key copy in done_tlo2 -> sorted into skey[0])
         sc.skey[0].reserve(sizeof(double) * n_done, s);
-        LC_CUDA(cub::DeviceRadixSort::SortPairs(sc.cub_tmp.ptr, bytes, sc.done_tlo2.as<double>(), sc.skey[0].as<double>(),
+        LC_CUB(cub::DeviceRadixSort::SortPairs(sc.cub_tmp.ptr, bytes, sc.done_tlo2.as<double>(), sc.skey[0].as<double>(),
                                                 sc.iota.as<int32_t>(), sc.sort_idx.as<int32_t>(), (int)n_done, 0, 64, s));
         gather_seg_kernel<<<grid_for(n_done), 256, 0, s>>>(sc.sort_idx.as<int32_t>(), n_done, sc.done_seg.as<int32_t>(),
                                                           sc.done_seg2.as<int32_t>());
         LC_CHECK_LAUNCH();
         sc.sperm[0].reserve(sizeof(int32_t) * n_done, s);
         bytes = sc.cub_tmp.bytes;
-        LC_CUDA(cub::DeviceRadixSort::SortPairs(sc.cub_tmp.ptr, bytes, sc.done_seg2.as<int32_t>(),
+        LC_CUB(cub::DeviceRadixSort::SortPairs(sc.cub_tmp.ptr, bytes, sc.done_seg2.as<int32_t>(),
                                                 sc.sperm[0].as<int32_t>(), sc.sort_idx.as<int32_t>(),
                                                 sc.sort_idx2.as<int32_t>(), (int)n_done, 0, 32, s));
         seg_sorted = sc.sperm[0].as<int32_t>();
@@ -638,9 +640,11 @@ bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc,
     // per-loop output counts and offsets
     sc.done_cnt.reserve(sizeof(unsigned long long) * (L + 1), s);
     LC_CUDA(cudaMemsetAsync(sc.done_cnt.ptr, 0, sizeof(unsigned long long) * (L + 1), s));
-    if (n_done > 0)
+    if (n_done > 0) {
         done_hist_kernel<<<grid_for(n_done), 256, 0, s>>>(seg_sorted, n_done, in.seg_loop,
                                                           sc.done_cnt.as<unsigned long long>());
+        LC_CHECK_LAUNCH();
+    }
     sc.counters.reserve(sizeof(int64_t) * 2 * (L + 1), s);
     int64_t *ocnt = sc.counters.as<int64_t>(), *dcnt = ocnt + (L + 1);
     out_counts_kernel<<<grid_for(L + 1), 256, 0, s>>>(sc.done_cnt.as<unsigned long long>(), sc.paired.as<uint8_t>(),
@@ -656,6 +660,7 @@ bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc,
         write_done_kernel<<<grid_for(n_done), 256, 0, s>>>(n_done, seg_sorted, sc.done_tlo.as<double>(), t_idx, in.seg_loop,
                                                            in.coeffs, out.vert_off.as<int64_t>(), sc.done_off.as<int64_t>(),
                                                            out.verts.as<double>());
+    if (n_done > 0) LC_CHECK_LAUNCH();
     if (M > 0)
         write_unpaired_kernel<<<grid_for(M), 256, 0, s>>>(M, in.seg_loop, sc.paired.as<uint8_t>(), in.loff, in.coeffs, in.t,
                                                           out.vert_off.as<int64_t>(), out.verts.as<double>());

@@ -392,7 +392,7 @@ int64_t build_items(const int32_t *d_pairs, int64_t P, const int64_t *d_voff, Pa
     pair_geom_kernel<<<(unsigned)ceil_div(P, 256), 256, 0, s>>>(d_pairs, P, d_voff, d_pg, d_item_off);
     LC_CHECK_LAUNCH();
     size_t bytes = scan_tmp_bytes;
-    LC_CUDA(cub::DeviceScan::ExclusiveSum(d_scan_tmp, bytes, d_item_off, d_item_off, (int)(P + 1), s));
+    LC_CUB(cub::DeviceScan::ExclusiveSum(d_scan_tmp, bytes, d_item_off, d_item_off, (int)(P + 1), s));
     int64_t total = 0;
     LC_CUDA(cudaMemcpyAsync(&total, d_item_off + P, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     LC_CUDA(cudaStreamSynchronize(s));

@@ -212,7 +212,7 @@ int64_t run_pls(const double *loop_box, int64_t L, const uint64_t *h_excl, int64
     cub::DeviceScan::ExclusiveSum(nullptr, b2, (int64_t *)nullptr, (int64_t *)nullptr, (int)(L + 1));
     sc.cub_tmp.reserve(b1 > b2 ? b1 : b2, s);
     size_t bytes = sc.cub_tmp.bytes;
-    LC_CUDA(cub::DeviceRadixSort::SortPairs(sc.cub_tmp.ptr, bytes, sc.keys.as<double>(), sc.keys_sorted.as<double>(),
+    LC_CUB(cub::DeviceRadixSort::SortPairs(sc.cub_tmp.ptr, bytes, sc.keys.as<double>(), sc.keys_sorted.as<double>(),
                                             sc.idx.as<int32_t>(), sc.perm.as<int32_t>(), (int)L, 0, 64, s));
     const unsigned grid = (unsigned)ceil_div(L, 128);
     LC_CUDA(cudaMemsetAsync(sc.counts.as<int64_t>() + L, 0, sizeof(int64_t), s));
@@ -221,7 +221,7 @@ int64_t run_pls(const double *loop_box, int64_t L, const uint64_t *h_excl, int64
                                              sc.counts.as<int64_t>(), nullptr, nullptr);
     LC_CHECK_LAUNCH();
     bytes = sc.cub_tmp.bytes;
-    LC_CUDA(cub::DeviceScan::ExclusiveSum(sc.cub_tmp.ptr, bytes, sc.counts.as<int64_t>(), sc.offs.as<int64_t>(),
+    LC_CUB(cub::DeviceScan::ExclusiveSum(sc.cub_tmp.ptr, bytes, sc.counts.as<int64_t>(), sc.offs.as<int64_t>(),
                                           (int)(L + 1), s));
     int64_t P = 0;
     LC_CUDA(cudaMemcpyAsync(&P, sc.offs.as<int64_t>() + L, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -237,7 +237,7 @@ int64_t run_pls(const double *loop_box, int64_t L, const uint64_t *h_excl, int64
     cub::DeviceRadixSort::SortKeys(nullptr, b3, (uint64_t *)nullptr, (uint64_t *)nullptr, (int)P);
     sc.cub_tmp.reserve(b3, s);
     bytes = sc.cub_tmp.bytes;
-    LC_CUDA(cub::DeviceRadixSort::SortKeys(sc.cub_tmp.ptr, bytes, sc.pair_keys.as<uint64_t>(),
+    LC_CUB(cub::DeviceRadixSort::SortKeys(sc.cub_tmp.ptr, bytes, sc.pair_keys.as<uint64_t>(),
                                            sc.pair_keys_sorted.as<uint64_t>(), (int)P, 0, 64, s));
     pairs.reserve(sizeof(int32_t) * 2 * P, s);
     unpack_pairs_kernel<<<(unsigned)ceil_div(P, 256), 256, 0, s>>>(sc.pair_keys_sorted.as<uint64_t>(), P,

@@ -14,6 +14,7 @@ import math
 
 import numpy as np
 
+from . import _native
 from .geometry import CurveModel, ValidationError
 
 
@@ -55,7 +56,32 @@ def model_to_dict(model: CurveModel, extra=None) -> dict:
     return doc
 
 
+def canonical_json(model: CurveModel):
+    """Bytes of json.dumps(model_to_dict(model), sort_keys=True, separators=(",", ":")),
+    formatted by the library's multithreaded writer (csrc/digest.cpp)."""
+    coeffs, t, off = model.packed()
+    closed = np.fromiter((lp.closed for lp in model.loops), dtype=np.uint8, count=model.num_loops)
+    blob = _native.model_json(coeffs, t, off, None if closed.all() else closed)
+    if blob is None:
+        raise ValidationError("cannot serialize non-finite coordinate")
+    return blob
+
+
 def model_digest(model: CurveModel) -> str:
-    """SHA-256 hex digest of the canonical json-curves serialization (model_io.py:169-172)."""
+    """SHA-256 hex digest of the canonical json-curves serialization (model_io.py:169-172).
+
+    Formatting and hashing run in the library (csrc/digest.cpp) on all host
+    cores with the GIL released, so callers can overlap it with GPU work.
+    """
+    coeffs, t, off = model.packed()
+    closed = np.fromiter((lp.closed for lp in model.loops), dtype=np.uint8, count=model.num_loops)
+    digest = _native.model_digest(coeffs, t, off, None if closed.all() else closed)
+    if digest is None:
+        raise ValidationError("cannot serialize non-finite coordinate")
+    return digest
+
+
+def model_digest_python(model: CurveModel) -> str:
+    """Straight json.dumps restatement (cross-check for canonical_json in the tests)."""
     blob = json.dumps(model_to_dict(model), sort_keys=True, separators=(",", ":"))
     return hashlib.sha256(blob.encode()).hexdigest()
