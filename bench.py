@@ -41,8 +41,9 @@ sys.path.insert(0, str(ROOT))
 METRIC = "Gauss-sum segment-pairs/sec (FP64)"
 UNIT = "seg-pairs/s"
 # Algorithmic FP64 FLOPs per segment pair of the reference formula (direct.py:19-46):
-# dynamic DFMA*2 + DMUL + DADD of the GAUSS_REF kernel measured with ncu.
-F_PAIR = 382.0
+# dynamic 2*DFMA + DMUL + DADD of the GAUSS_REF kernel measured with ncu
+# (profiles/r01/SUMMARY.md): 261.8 -> frozen at 262.
+F_PAIR = 262.0
 L2_FLUSH_BYTES = 512 << 20
 
 

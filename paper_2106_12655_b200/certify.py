@@ -212,10 +212,28 @@ def _sharded_gauss(ctx, mode, dist):
     full = torch.zeros(per * world, dtype=torch.float64, device=dev)
     ctx.gauss_run(mode, b, e, full.data_ptr())
     ctx.synchronize()
-    gathered = torch.empty_like(full)
-    dist.all_gather_into_tensor(gathered, full[rank * per:(rank + 1) * per].contiguous())
+    gathered = gather_item_partials(dist, full, rank, per)
     torch.cuda.synchronize(dev)
     return ctx.gauss_reduce(gathered.data_ptr())
+
+
+def gather_item_partials(dist, full, rank, per):
+    """All ranks' contiguous item slices -> one array indexed by absolute item id.
+
+    `full` holds this rank's partials at [rank*per, (rank+1)*per); the result
+    is bitwise the single-GPU partial array (no arithmetic on the values), so
+    the fixed-order per-pair reduction that follows is world-size independent.
+    """
+    import torch
+
+    mine = full[rank * per:(rank + 1) * per].contiguous()
+    if dist.get_backend() == "nccl":
+        out = torch.empty_like(full)
+        dist.all_gather_into_tensor(out, mine)
+        return out
+    parts = [torch.empty_like(mine) for _ in range(dist.get_world_size())]
+    dist.all_gather(parts, mine)
+    return torch.cat(parts)
 
 
 def device_step(ctx, xi, excl_keys, params, mode=None, timings=None):

@@ -17,6 +17,16 @@ GOLDEN = Path(__file__).resolve().parent / "golden"
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and liblinkcert_b200.so")
+    # the library (and the oracle) are built in-tree by __graft_entry__.build();
+    # build them here only if they are missing (nvcc cross-compiles without a GPU)
+    from paper_2106_12655_b200 import build
+
+    if not build.LIB.exists():
+        build.build()
+    if not (ROOT / "oracle" / "liboracle_gauss.so").exists():
+        import linkcert_oracle
+
+        linkcert_oracle.build()
 
 
 def circle_points(n, center=(0.0, 0.0, 0.0), u=(1.0, 0.0, 0.0), v=(0.0, 1.0, 0.0), radius=1.0):
