@@ -373,10 +373,11 @@ class Context:
         return nv.value, passes.value
 
     def get_polylines(self):
-        verts = np.empty((self._nverts, 3))
         off = np.empty(self._L + 1, dtype=np.int64)
         with self.lock:
-            _check(self.lib.lc_get_polylines(self.handle, _ptr(verts), _ptr(off)))
+            _check(self.lib.lc_get_polylines(self.handle, None, _ptr(off)))
+            verts = np.empty((int(off[-1]) if len(off) else 0, 3))
+            _check(self.lib.lc_get_polylines(self.handle, _ptr(verts), None))
         return verts, off
 
     def evaluate_staged(self, mode=GAUSS_PHASE):

@@ -7,7 +7,7 @@
 //                                 k = loop j (outer, "rows")
 // and sums lambda(l_c, l_c+1, k_r, k_r+1) over all r < N_k, c < N_l.
 //
-// Work decomposition (DESIGN.md §3): every pair is cut into warp items.  A
+// Work decomposition (DESIGN.md §3.1): every pair is cut into warp items.  A
 // warp item covers (1<<rb_log2) row blocks of kRowsPerLane rows times
 // (32>>rb_log2) column strips of `cl` columns; each lane owns one
 // (row block, column strip) and walks its strip column by column, keeping
@@ -15,7 +15,8 @@
 // a segment pair are vertex-pair differences r(c, m) = l_c - k_m, so a
 // column step computes one new difference vector, norm and two edge dot
 // products per row vertex and reuses the previous column's values — the
-// operands are bitwise the ones the reference formula would form.
+// operands the reference formula forms.  Column steps alternate between two
+// register sets (no array shifting) and contain no branches.
 // Item partials go through a warp butterfly (fixed order) into
 // partials[item]; pairs are reduced from their contiguous item range in a
 // fixed order, so raw sums are identical run to run and for any split of
@@ -31,32 +32,37 @@ namespace {
 constexpr double kTwoPi = 6.283185307179586;          // 2.0 * math.pi (direct.py:16)
 constexpr double kInvTwoPi = 0.15915494309189535;     // 1 / (2 pi), correctly rounded
 
-__device__ __forceinline__ int sign_bit(double x) { return (int)((unsigned)__double2hiint(x) >> 31); }
+__device__ __forceinline__ int sbit(double x) { return (int)((unsigned)__double2hiint(x) >> 31); }
 
-// S <- S * (zx + i zy), counting full turns so that
-//   arg_total = 2*pi*turns + atan2(S.y, S.x)   (atan2 semantics incl. signed zero)
-// Classification by the sign bit of the imaginary part: "upper" = arg in
-// [+0, pi], "lower" = arg in [-pi, -0].  Two factors in the same half whose
-// product lands in the other half wrapped by one turn in that direction —
-// the full-turn rule of _link_angle_sum (direct.py:120-123), which is exact
-// given the computed product.
-__device__ __forceinline__ void phase_mul(double &sx, double &sy, double zx, double zy, int &turns) {
-    const double ux = sx * zx - sy * zy;
-    const double uy = sx * zy + sy * zx;
-    const int ss = sign_bit(sy), sz = sign_bit(zy), su = sign_bit(uy);
-    turns += ((ss == sz) & (su != ss)) ? (1 - 2 * ss) : 0;
-    sx = ux;
-    sy = uy;
+// U = A * B counting full turns so that, along a product chain,
+//   sum of factor angles = 2*pi*turns + atan2(U.y, U.x)   (atan2 signed-zero semantics).
+// Half planes by the sign bit of the imaginary part ("upper": arg in [+0, pi],
+// "lower": [-pi, -0]); two factors in the same half whose product lands in the
+// other half wrapped by one turn — the full-turn rule of _link_angle_sum
+// (direct.py:120-123), exact given the computed product.  With a = sb(A.y),
+// b = sb(B.y), c = sb(U.y) the wrap is (a == b) ? c - a : 0.
+__device__ __forceinline__ void cmul_w(double ax, double ay, double bx, double by, double &ux, double &uy,
+                                       int &turns) {
+    ux = fma(ax, bx, -ay * by);
+    uy = fma(ax, by, ay * bx);
+    const int sa = sbit(ay), sb = sbit(by), su = sbit(uy);
+    turns += (sa == sb) ? (su - sa) : 0;
 }
 
-// Rescale S by an exact power of two so max(|Sx|,|Sy|) is in [1, 2).
-__device__ __forceinline__ void phase_renorm(double &sx, double &sy) {
-    const int ex = __double2hiint(sx) & 0x7ff00000;
-    const int ey = __double2hiint(sy) & 0x7ff00000;
-    const int e = ex > ey ? ex : ey;
-    const double scale = __hiloint2double(0x7fe00000 - e, 0);
-    sx *= scale;
-    sy *= scale;
+// sqrt(x) for x >= 0 without the libdevice special-case branch: MUFU rsqrt
+// seed + 2 Newton steps, s = x * y (~2 ulp; the norms only enter the d1/d2
+// denominators).  LC_SQRT_HERON adds a Heron correction (<= 1 ulp).
+__device__ __forceinline__ double sqrt_nb(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double h = 0.5 * x;
+    y = fma(y, fma(-h * y, y, 0.5), y);
+    y = fma(y, fma(-h * y, y, 0.5), y);
+    double s = x * y;
+#ifdef LC_SQRT_HERON
+    s = fma(fma(-s, s, x), 0.5 * y, s);
+#endif
+    return x > 0.0 ? s : 0.0;
 }
 
 // Reference _pair_lambda with the IEEE operation sequence of the numba
@@ -90,124 +96,159 @@ __device__ __forceinline__ double ref_pair_lambda(double ljx, double ljy, double
 #undef M_
 }
 
+// ------------------------------------------------------------ lane strip
+
+constexpr int R = kRowsPerLane;
+
+struct Col {   // one column: r(c, m) = l_c - k_m, |r(c, m)|, v[m] = r(c,m).r(c,m+1)
+    double x[R + 1], y[R + 1], z[R + 1], n[R + 1], v[R];
+};
+
+__device__ __forceinline__ void col_fill(Col &B, double lx, double ly, double lz, const double *kx, const double *ky,
+                                         const double *kz) {
+#pragma unroll
+    for (int m = 0; m <= R; ++m) {
+        B.x[m] = lx - kx[m];
+        B.y[m] = ly - ky[m];
+        B.z[m] = lz - kz[m];
+        B.n[m] = sqrt_nb(fma(B.z[m], B.z[m], fma(B.y[m], B.y[m], B.x[m] * B.x[m])));
+    }
+#pragma unroll
+    for (int m = 0; m < R; ++m) B.v[m] = fma(B.z[m], B.z[m + 1], fma(B.y[m], B.y[m + 1], B.x[m] * B.x[m + 1]));
+}
+
+// Arai terms of pair (row m, column c) (direct.py:21-46): corner vectors a = r(c,m),
+// b = r(c,m+1), c = r(c+1,m+1), d = r(c+1,m); shared dots ab = A.v[m],
+// dc = B.v[m], ad = h[m], bc = h[m+1] with h[m] = r(c,m).r(c+1,m).
+// Returns w = (d1 + i p)(d2 + i p) = (xp, yp); its wrap (z1, z2 share the sign
+// bit of p) goes to `turns`.  A degenerate w == 0 (p = 0 and d1 or d2 = 0)
+// contributes the exact atan2(+-0, d) half turns instead and w := 1.
+__device__ __forceinline__ void pair_w(const Col &A, const Col &B, const double *h, int m, double &wx, double &wy,
+                                       int &turns, int &halves) {
+    const double ax = A.x[m], ay = A.y[m], az = A.z[m];
+    const double bx = A.x[m + 1], by = A.y[m + 1], bz = A.z[m + 1];
+    const double cx = B.x[m + 1], cy = B.y[m + 1], cz = B.z[m + 1];
+    const double an = A.n[m], bn = A.n[m + 1], cn = B.n[m + 1], dn = B.n[m];
+    const double ab = A.v[m], dc = B.v[m], ad = h[m], bc = h[m + 1];
+    const double ca = fma(cz, az, fma(cy, ay, cx * ax));
+    const double p = fma(az, fma(bx, cy, -by * cx), fma(ay, fma(bz, cx, -bx * cz), ax * fma(by, cz, -bz * cy)));
+    // d1 = an bn cn + ab cn + bc an + ca bn, d2 = an dn cn + ad cn + dc an + ca dn
+    const double t1 = fma(an, cn, ca);
+    const double d1 = fma(bn, t1, fma(cn, ab, an * bc));
+    const double d2 = fma(dn, t1, fma(cn, ad, an * dc));
+    const double xp = fma(d1, d2, -p * p);
+    const double yp = p * (d1 + d2);
+    const bool deg = (xp == 0.0) & (yp == 0.0);
+    const int sp = sbit(p);
+    turns += deg ? 0 : (sbit(yp) - sp);
+    const int hs = sbit(d1) + sbit(d2);
+    halves += deg ? (sp ? -hs : hs) : 0;
+    wx = deg ? 1.0 : xp;
+    wy = deg ? 0.0 : yp;
+}
+
+struct Acc {
+    double sx = 1.0, sy = 0.0;   // GAUSS_PHASE: phase product
+    double ang = 0.0;            // GAUSS_ATAN: sum of fused angles (radians)
+    int turns = 0, halves = 0;
+};
+
+template <int MODE, bool FULL>
+__device__ __forceinline__ void col_step(const Col &A, Col &B, double lx, double ly, double lz, const double *kx,
+                                         const double *ky, const double *kz, const bool *rv, Acc &acc) {
+    col_fill(B, lx, ly, lz, kx, ky, kz);
+    double h[R + 1];
+#pragma unroll
+    for (int m = 0; m <= R; ++m) h[m] = fma(A.z[m], B.z[m], fma(A.y[m], B.y[m], A.x[m] * B.x[m]));
+    double wx[R], wy[R];
+#pragma unroll
+    for (int m = 0; m < R; ++m) {
+        int t = 0, hv = 0;
+        pair_w(A, B, h, m, wx[m], wy[m], t, hv);
+        if (!FULL && !rv[m]) {
+            wx[m] = 1.0;
+            wy[m] = 0.0;
+            t = hv = 0;
+        }
+        acc.turns += t;
+        acc.halves += hv;
+    }
+    if (MODE == GAUSS_ATAN) {
+#pragma unroll
+        for (int m = 0; m < R; ++m) acc.ang += atan2(wy[m], wx[m]);
+    } else {
+        // product tree (w0 w1)(w2 w3), S *= W, then renormalize S by an exact power of two
+        double ax, ay, bx, by, ux, uy, nx, ny;
+        cmul_w(wx[0], wy[0], wx[1], wy[1], ax, ay, acc.turns);
+        cmul_w(wx[2], wy[2], wx[3], wy[3], bx, by, acc.turns);
+        cmul_w(ax, ay, bx, by, ux, uy, acc.turns);
+        cmul_w(acc.sx, acc.sy, ux, uy, nx, ny, acc.turns);
+        const int ex = __double2hiint(nx) & 0x7ff00000, ey = __double2hiint(ny) & 0x7ff00000;
+        const double scale = __hiloint2double(0x7fe00000 - (ex > ey ? ex : ey), 0);
+        acc.sx = nx * scale;
+        acc.sy = ny * scale;
+    }
+}
+
 // Sum over rows [row0, row0+R) x columns [c0, c1) of one pair, in turns.
-template <int MODE>
+template <int MODE, bool FULL>
 __device__ double lane_strip(const double *__restrict__ X, const double *__restrict__ Y,
-                             const double *__restrict__ Z, int64_t row_off, int nrows,
-                             int64_t col_off, int row0, int c0, int c1) {
-    constexpr int R = kRowsPerLane;
+                             const double *__restrict__ Z, int64_t row_off, int nrows, int64_t col_off, int row0,
+                             int c0, int c1) {
     double kx[R + 1], ky[R + 1], kz[R + 1];
     bool rv[R];
 #pragma unroll
     for (int m = 0; m <= R; ++m) {
-        const int v = min(row0 + m, nrows);   // closing vertex sits at index nrows
+        const int v = FULL ? row0 + m : min(row0 + m, nrows);   // closing vertex sits at index nrows
         kx[m] = __ldg(X + row_off + v);
         ky[m] = __ldg(Y + row_off + v);
         kz[m] = __ldg(Z + row_off + v);
     }
 #pragma unroll
-    for (int m = 0; m < R; ++m) rv[m] = row0 + m < nrows;
-
-    if (MODE == GAUSS_REF) {
-        double acc = 0.0;
-        double lx = __ldg(X + col_off + c0), ly = __ldg(Y + col_off + c0), lz = __ldg(Z + col_off + c0);
-        for (int c = c0; c < c1; ++c) {
-            const double nx = __ldg(X + col_off + c + 1), ny = __ldg(Y + col_off + c + 1),
-                         nz = __ldg(Z + col_off + c + 1);
-#pragma unroll
-            for (int m = 0; m < R; ++m) {
-                if (rv[m])
-                    acc = __dadd_rn(acc, ref_pair_lambda(lx, ly, lz, nx, ny, nz, kx[m], ky[m], kz[m],
-                                                         kx[m + 1], ky[m + 1], kz[m + 1]));
-            }
-            lx = nx;
-            ly = ny;
-            lz = nz;
-        }
-        return acc;
+    for (int m = 0; m < R; ++m) rv[m] = FULL || row0 + m < nrows;
+    const double *px = X + col_off, *py = Y + col_off, *pz = Z + col_off;
+    Col A, B;
+    col_fill(A, __ldg(px + c0), __ldg(py + c0), __ldg(pz + c0), kx, ky, kz);
+    Acc acc;
+    int c = c0;
+    for (; c + 2 <= c1; c += 2) {
+        const double l1x = __ldg(px + c + 1), l1y = __ldg(py + c + 1), l1z = __ldg(pz + c + 1);
+        const double l2x = __ldg(px + c + 2), l2y = __ldg(py + c + 2), l2z = __ldg(pz + c + 2);
+        col_step<MODE, FULL>(A, B, l1x, l1y, l1z, kx, ky, kz, rv, acc);
+        col_step<MODE, FULL>(B, A, l2x, l2y, l2z, kx, ky, kz, rv, acc);
     }
+    if (c < c1) col_step<MODE, FULL>(A, B, __ldg(px + c + 1), __ldg(py + c + 1), __ldg(pz + c + 1), kx, ky, kz, rv, acc);
+    const double frac = MODE == GAUSS_ATAN ? acc.ang * kInvTwoPi : atan2(acc.sy, acc.sx) * kInvTwoPi;
+    return (double)acc.turns + 0.5 * (double)acc.halves + frac;
+}
 
-    // Previous column: r(c, m) = l_c - k_m, its norm, and v[m] = r(c,m).r(c,m+1).
-    double rx[R + 1], ry[R + 1], rz[R + 1], rn[R + 1], vv[R];
-    {
-        const double lx = __ldg(X + col_off + c0), ly = __ldg(Y + col_off + c0), lz = __ldg(Z + col_off + c0);
+// GAUSS_REF: the reference formula per pair from scratch (two atan2, no contraction).
+__device__ double lane_strip_ref(const double *__restrict__ X, const double *__restrict__ Y,
+                                 const double *__restrict__ Z, int64_t row_off, int nrows, int64_t col_off, int row0,
+                                 int c0, int c1) {
+    double kx[R + 1], ky[R + 1], kz[R + 1];
 #pragma unroll
-        for (int m = 0; m <= R; ++m) {
-            rx[m] = lx - kx[m];
-            ry[m] = ly - ky[m];
-            rz[m] = lz - kz[m];
-            rn[m] = sqrt(rx[m] * rx[m] + ry[m] * ry[m] + rz[m] * rz[m]);
-        }
-#pragma unroll
-        for (int m = 0; m < R; ++m) vv[m] = rx[m] * rx[m + 1] + ry[m] * ry[m + 1] + rz[m] * rz[m + 1];
+    for (int m = 0; m <= R; ++m) {
+        const int v = min(row0 + m, nrows);
+        kx[m] = __ldg(X + row_off + v);
+        ky[m] = __ldg(Y + row_off + v);
+        kz[m] = __ldg(Z + row_off + v);
     }
-
-    double sx = 1.0, sy = 0.0;   // PHASE accumulator
-    double ang = 0.0;            // ATAN accumulator (radians)
-    int turns = 0, halves = 0;
-
-    double nlx = __ldg(X + col_off + c0 + 1), nly = __ldg(Y + col_off + c0 + 1), nlz = __ldg(Z + col_off + c0 + 1);
+    double acc = 0.0;
+    double lx = __ldg(X + col_off + c0), ly = __ldg(Y + col_off + c0), lz = __ldg(Z + col_off + c0);
     for (int c = c0; c < c1; ++c) {
-        const double lx = nlx, ly = nly, lz = nlz;
-        if (c + 2 <= c1) {
-            nlx = __ldg(X + col_off + c + 2);
-            nly = __ldg(Y + col_off + c + 2);
-            nlz = __ldg(Z + col_off + c + 2);
-        }
-        double qx[R + 1], qy[R + 1], qz[R + 1], qn[R + 1], hh[R + 1], ww[R];
-#pragma unroll
-        for (int m = 0; m <= R; ++m) {
-            qx[m] = lx - kx[m];
-            qy[m] = ly - ky[m];
-            qz[m] = lz - kz[m];
-            qn[m] = sqrt(qx[m] * qx[m] + qy[m] * qy[m] + qz[m] * qz[m]);
-            hh[m] = rx[m] * qx[m] + ry[m] * qy[m] + rz[m] * qz[m];   // r(c,m) . r(c+1,m)
-        }
-#pragma unroll
-        for (int m = 0; m < R; ++m) ww[m] = qx[m] * qx[m + 1] + qy[m] * qy[m + 1] + qz[m] * qz[m + 1];
-
+        const double nx = __ldg(X + col_off + c + 1), ny = __ldg(Y + col_off + c + 1), nz = __ldg(Z + col_off + c + 1);
 #pragma unroll
         for (int m = 0; m < R; ++m) {
-            // Corner vectors of pair (row m, column c): a = r(c,m), b = r(c,m+1),
-            // c = r(c+1,m+1), d = r(c+1,m)  (direct.py:21-32).
-            const double ax = rx[m], ay = ry[m], az = rz[m];
-            const double bx = rx[m + 1], by = ry[m + 1], bz = rz[m + 1];
-            const double cx = qx[m + 1], cy = qy[m + 1], cz = qz[m + 1];
-            const double an = rn[m], bn = rn[m + 1], cn = qn[m + 1], dn = qn[m];
-            const double ab = vv[m], bc = hh[m + 1], ad = hh[m], dc = ww[m];
-            const double ca = cx * ax + cy * ay + cz * az;
-            const double p = ax * (by * cz - bz * cy) + ay * (bz * cx - bx * cz) + az * (bx * cy - by * cx);
-            const double d1 = an * bn * cn + ab * cn + bc * an + ca * bn;
-            const double d2 = an * dn * cn + ad * cn + dc * an + ca * dn;
-            if (!rv[m]) continue;
-            if (p == 0.0) {
-                // atan2(+-0, d) is +-pi for d < 0 or d == -0, else +-0: exact half turns.
-                const int hsum = sign_bit(d1) + sign_bit(d2);
-                halves += sign_bit(p) ? -hsum : hsum;
-            } else if (MODE == GAUSS_PHASE) {
-                phase_mul(sx, sy, d1, p, turns);
-                phase_mul(sx, sy, d2, p, turns);
-            } else {
-                const double xp = d1 * d2 - p * p;
-                const double yp = p * (d1 + d2);
-                ang += atan2(yp, xp);
-                const int sp = sign_bit(p);
-                turns += (sign_bit(yp) != sp) ? (1 - 2 * sp) : 0;
-            }
+            if (row0 + m < nrows)
+                acc = __dadd_rn(acc, ref_pair_lambda(lx, ly, lz, nx, ny, nz, kx[m], ky[m], kz[m], kx[m + 1], ky[m + 1],
+                                                     kz[m + 1]));
         }
-        if (MODE == GAUSS_PHASE) phase_renorm(sx, sy);
-#pragma unroll
-        for (int m = 0; m <= R; ++m) {
-            rx[m] = qx[m];
-            ry[m] = qy[m];
-            rz[m] = qz[m];
-            rn[m] = qn[m];
-        }
-#pragma unroll
-        for (int m = 0; m < R; ++m) vv[m] = ww[m];
+        lx = nx;
+        ly = ny;
+        lz = nz;
     }
-    const double frac = (MODE == GAUSS_PHASE) ? atan2(sy, sx) * kInvTwoPi : ang * kInvTwoPi;
-    return (double)turns + 0.5 * (double)halves + frac;
+    return acc;
 }
 
 __device__ __forceinline__ int64_t find_pair(const int64_t *__restrict__ item_off, int64_t P, int64_t it) {
@@ -220,11 +261,11 @@ __device__ __forceinline__ int64_t find_pair(const int64_t *__restrict__ item_of
     return lo;
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(128) gauss_items_kernel(
+template <int MODE, int MINB>
+__global__ void __launch_bounds__(128, MINB) gauss_items_kernel(
     const double *__restrict__ X, const double *__restrict__ Y, const double *__restrict__ Z,
-    const PairGeom *__restrict__ pg, const int64_t *__restrict__ item_off, int64_t P,
-    int64_t item_begin, int64_t item_end, unsigned long long *__restrict__ counter,
+    const PairGeom *__restrict__ pg, const int64_t *__restrict__ item_off, const int32_t *__restrict__ item_pair,
+    int64_t P, int64_t item_begin, int64_t item_end, unsigned long long *__restrict__ counter,
     double *__restrict__ partials) {
     const int lane = threadIdx.x & 31;
     for (;;) {
@@ -233,19 +274,26 @@ __global__ void __launch_bounds__(128) gauss_items_kernel(
         k = __shfl_sync(0xffffffffu, k, 0);
         const int64_t it = item_begin + (int64_t)k;
         if (it >= item_end) break;
-        const int64_t p = find_pair(item_off, P, it);
+        const int64_t p = item_pair ? (int64_t)__ldg(item_pair + it) : find_pair(item_off, P, it);
         const PairGeom g = pg[p];
         const int64_t local = it - __ldg(item_off + p);
         const int ir = (int)(local / g.items_c), ic = (int)(local % g.items_c);
         const int rbm = (1 << g.rb_log2) - 1;
         const int my_rb = lane & rbm, my_cs = lane >> g.rb_log2;
-        const int row0 = ((ir << g.rb_log2) + my_rb) * kRowsPerLane;
+        const int row0 = ((ir << g.rb_log2) + my_rb) * R;
         const int64_t c0l = ((int64_t)ic * (32 >> g.rb_log2) + my_cs) * g.cl;
         const int c0 = (int)(c0l < g.ncols ? c0l : g.ncols);
         const int c1 = min(c0 + g.cl, g.ncols);
         double val = 0.0;
-        if (row0 < g.nrows && c0 < c1)
-            val = lane_strip<MODE>(X, Y, Z, g.row_off, g.nrows, g.col_off, row0, c0, c1);
+        if (row0 < g.nrows && c0 < c1) {
+            if (MODE == GAUSS_REF) {
+                val = lane_strip_ref(X, Y, Z, g.row_off, g.nrows, g.col_off, row0, c0, c1);
+            } else if (row0 + R <= g.nrows) {
+                val = lane_strip<MODE, true>(X, Y, Z, g.row_off, g.nrows, g.col_off, row0, c0, c1);
+            } else {
+                val = lane_strip<MODE, false>(X, Y, Z, g.row_off, g.nrows, g.col_off, row0, c0, c1);
+            }
+        }
 #pragma unroll
         for (int off = 16; off; off >>= 1) val += __shfl_xor_sync(0xffffffffu, val, off);
         if (lane == 0) partials[it] = val;
@@ -263,14 +311,14 @@ __global__ void pair_geom_kernel(const int32_t *__restrict__ pairs, int64_t P,
     g.row_off = voff[j];
     g.ncols = (int)(voff[i + 1] - voff[i] - 1);
     g.nrows = (int)(voff[j + 1] - voff[j] - 1);
-    const int nb = (g.nrows + kRowsPerLane - 1) / kRowsPerLane;
+    const int nb = (g.nrows + R - 1) / R;
     int rbl = 0;
     while ((1 << rbl) < nb && rbl < 5) ++rbl;
     g.rb_log2 = rbl;
     const int cs = 32 >> rbl;
     const int cl = (g.ncols + cs - 1) / cs;
     g.cl = cl < kMaxColsPerLane ? (cl > 0 ? cl : 1) : kMaxColsPerLane;
-    g.items_r = (g.nrows + (kRowsPerLane << rbl) - 1) / (kRowsPerLane << rbl);
+    g.items_r = (g.nrows + (R << rbl) - 1) / (R << rbl);
     const int64_t span = (int64_t)cs * g.cl;
     g.items_c = (int)((g.ncols + span - 1) / span);
     if (g.nrows <= 0 || g.ncols <= 0) g.items_r = g.items_c = 0;
@@ -320,7 +368,7 @@ __global__ void pack_closed_soa_kernel(const double *__restrict__ aos, const int
     const int64_t local = v - voff[lo];
     const int64_t n = in_off[lo + 1] - in_off[lo];
     const int64_t src = in_off[lo] + (local < n ? local : 0);   // closing vertex repeats vertex 0
-    int e = *d_exp - 1023;                       // unbiased exponent of max |coord|
+    int e = *d_exp - 1023;                                         // unbiased exponent of max |coord|
     e = e < -1022 ? -1022 : (e > 1022 ? 1022 : e);
     const double scale = __hiloint2double((1023 - e) << 20, 0);   // 2^-e, exact
     X[v] = aos[3 * src + 0] * scale;
@@ -349,7 +397,19 @@ __global__ void segment_pairs_kernel(const double *__restrict__ q, int64_t n, do
     out[k] = ref_pair_lambda(a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7], a[8], a[9], a[10], a[11]);
 }
 
+__global__ void item_pair_kernel(const int64_t *__restrict__ item_off, int64_t P, int64_t n_items,
+                                 int32_t *__restrict__ item_pair) {
+    const int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (it < n_items) item_pair[it] = (int32_t)find_pair(item_off, P, it);
+}
+
 }  // namespace
+
+void launch_item_pairs(const int64_t *item_off, int64_t P, int64_t n_items, int32_t *item_pair, cudaStream_t s) {
+    if (n_items == 0) return;
+    item_pair_kernel<<<(unsigned)ceil_div(n_items, 256), 256, 0, s>>>(item_off, P, n_items, item_pair);
+    LC_CHECK_LAUNCH();
+}
 
 void launch_segment_pairs(const double *quads, int64_t n, double *out, cudaStream_t s) {
     if (n == 0) return;
@@ -400,32 +460,28 @@ int64_t build_items(const int32_t *d_pairs, int64_t P, const int64_t *d_voff, Pa
 }
 
 void launch_gauss_items(int mode, const double *X, const double *Y, const double *Z, const PairGeom *pg,
-                        const int64_t *item_off, int64_t P, int64_t item_begin, int64_t item_end,
-                        unsigned long long *counter, double *partials, cudaStream_t s) {
+                        const int64_t *item_off, const int32_t *item_pair, int64_t P, int64_t item_begin,
+                        int64_t item_end, unsigned long long *counter, double *partials, cudaStream_t s) {
     if (item_end <= item_begin) return;
     LC_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s));
+    using Kern = void (*)(const double *, const double *, const double *, const PairGeom *, const int64_t *,
+                          const int32_t *, int64_t, int64_t, int64_t, unsigned long long *, double *);
+    // GAUSS_PHASE_OCC3/4: the phase kernel compiled for 3 / 4 resident CTAs (A/B variants)
+    static const Kern table[] = {gauss_items_kernel<GAUSS_PHASE, 1>, gauss_items_kernel<GAUSS_ATAN, 1>,
+                                 gauss_items_kernel<GAUSS_REF, 1>, gauss_items_kernel<GAUSS_PHASE, 3>,
+                                 gauss_items_kernel<GAUSS_PHASE, 4>};
+    if (mode < 0 || mode >= (int)(sizeof table / sizeof table[0])) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
+    const Kern fn = table[mode];
     int per_sm = 0;
     const int threads = 128;
-    const void *fn = mode == GAUSS_PHASE ? (const void *)gauss_items_kernel<GAUSS_PHASE>
-                     : mode == GAUSS_ATAN ? (const void *)gauss_items_kernel<GAUSS_ATAN>
-                                          : (const void *)gauss_items_kernel<GAUSS_REF>;
-    LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0));
+    LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void *)fn, threads, 0));
     if (per_sm < 1) per_sm = 1;
     const int64_t warps_needed = item_end - item_begin;
     int64_t blocks = (int64_t)num_sms() * per_sm;
     const int64_t blocks_needed = ceil_div(warps_needed, threads / 32);
     if (blocks > blocks_needed) blocks = blocks_needed;
-    switch (mode) {
-        case GAUSS_PHASE:
-            gauss_items_kernel<GAUSS_PHASE><<<(unsigned)blocks, threads, 0, s>>>(X, Y, Z, pg, item_off, P, item_begin, item_end, counter, partials);
-            break;
-        case GAUSS_ATAN:
-            gauss_items_kernel<GAUSS_ATAN><<<(unsigned)blocks, threads, 0, s>>>(X, Y, Z, pg, item_off, P, item_begin, item_end, counter, partials);
-            break;
-        default:
-            gauss_items_kernel<GAUSS_REF><<<(unsigned)blocks, threads, 0, s>>>(X, Y, Z, pg, item_off, P, item_begin, item_end, counter, partials);
-            break;
-    }
+    fn<<<(unsigned)blocks, threads, 0, s>>>(X, Y, Z, pg, item_off, item_pair, P, item_begin, item_end, counter,
+                                            partials);
     LC_CHECK_LAUNCH();
 }
 
@@ -440,7 +496,8 @@ void launch_pack_closed_soa(const double *aos, const int64_t *in_off, const int6
                             int64_t total_closed, const int *d_exp, double *X, double *Y, double *Z,
                             cudaStream_t s) {
     if (total_closed == 0) return;
-    pack_closed_soa_kernel<<<(unsigned)ceil_div(total_closed, 256), 256, 0, s>>>(aos, in_off, voff, L, total_closed, d_exp, X, Y, Z);
+    pack_closed_soa_kernel<<<(unsigned)ceil_div(total_closed, 256), 256, 0, s>>>(aos, in_off, voff, L, total_closed,
+                                                                                  d_exp, X, Y, Z);
     LC_CHECK_LAUNCH();
 }
 

@@ -14,7 +14,7 @@ namespace lc {
 //   GAUSS_REF   : the reference formula evaluated per pair from scratch with
 //                 no FMA contraction and two atan2 (direct.py:19-46); used to
 //                 freeze F_pair and as a numerics cross-check.
-enum GaussMode : int { GAUSS_PHASE = 0, GAUSS_ATAN = 1, GAUSS_REF = 2 };
+enum GaussMode : int { GAUSS_PHASE = 0, GAUSS_ATAN = 1, GAUSS_REF = 2, GAUSS_PHASE_OCC3 = 3, GAUSS_PHASE_OCC4 = 4 };
 
 constexpr int kRowsPerLane = 4;     // outer-loop (k) segments held per lane
 constexpr int kMaxColsPerLane = 2048;
@@ -39,9 +39,12 @@ size_t build_items_scan_bytes(int64_t P);
 
 // Evaluates items [item_begin, item_end) into partials[item] (absolute index).
 void launch_gauss_items(int mode, const double *X, const double *Y, const double *Z,
-                        const PairGeom *pg, const int64_t *item_off, int64_t P,
+                        const PairGeom *pg, const int64_t *item_off, const int32_t *item_pair, int64_t P,
                         int64_t item_begin, int64_t item_end, unsigned long long *counter,
                         double *partials, cudaStream_t s);
+
+// item_pair[it] = pair of work item `it` (replaces a per-item binary search).
+void launch_item_pairs(const int64_t *item_off, int64_t P, int64_t n_items, int32_t *item_pair, cudaStream_t s);
 
 // raw[p] = fixed-order sum of the pair's item partials; lk = rint(raw);
 // flags bit0 = NaN, bit1 = |raw - rint(raw)| > 0.25 (kernels.py:19-20,69-72).

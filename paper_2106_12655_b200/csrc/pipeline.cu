@@ -20,7 +20,8 @@ void Pipeline::init(cudaStream_t st) {
 
 void Pipeline::release() {
     DevBuf *bufs[] = {&d_coeffs, &d_t, &d_loff, &d_seg_box, &d_seg_loop, &d_loop_box, &d_aos, &d_in_off, &d_voff,
-                      &d_X, &d_Y, &d_Z, &d_exp, &d_pairs, &d_pg, &d_item_off, &d_scan, &d_counter, &d_partials,
+                      &d_X, &d_Y, &d_Z, &d_exp, &d_pairs, &d_pg, &d_item_off, &d_item_pair, &d_scan, &d_counter,
+                      &d_partials,
                       &d_raw, &d_lk, &d_flags, &d_quads, &d_qout, &dout.verts, &dout.vert_off};
     for (DevBuf *b : bufs) b->release(s);
     DevBuf *pb[] = {&pls_sc.keys, &pls_sc.keys_sorted, &pls_sc.idx, &pls_sc.perm, &pls_sc.counts, &pls_sc.offs,
@@ -194,6 +195,8 @@ void Pipeline::build_gauss_items() {
     n_items = build_items(d_pairs.as<int32_t>(), P, d_voff.as<int64_t>(), d_pg.as<PairGeom>(),
                           d_item_off.as<int64_t>(), d_scan.ptr, d_scan.bytes, s);
     d_partials.reserve(sizeof(double) * (size_t)(n_items > 0 ? n_items : 1), s);
+    d_item_pair.reserve(sizeof(int32_t) * (size_t)(n_items > 0 ? n_items : 1), s);
+    launch_item_pairs(d_item_off.as<int64_t>(), P, n_items, d_item_pair.as<int32_t>(), s);
     d_raw.reserve(sizeof(double) * (size_t)(P > 0 ? P : 1), s);
     d_lk.reserve(sizeof(int64_t) * (size_t)(P > 0 ? P : 1), s);
     d_flags.reserve((size_t)(P > 0 ? P : 1), s);
@@ -201,11 +204,11 @@ void Pipeline::build_gauss_items() {
 
 void Pipeline::run_gauss(int mode, int64_t item_begin, int64_t item_end, double *partials_ext,
                          cudaEvent_t ev0, cudaEvent_t ev1) {
-    if (mode < GAUSS_PHASE || mode > GAUSS_REF) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
+    if (mode < GAUSS_PHASE || mode > 5) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
     double *out = partials_ext ? partials_ext : d_partials.as<double>();
     LC_CUDA(cudaEventRecord(ev0 ? ev0 : ev[EV_GAUSS0], s));
     launch_gauss_items(mode, d_X.as<double>(), d_Y.as<double>(), d_Z.as<double>(), d_pg.as<PairGeom>(),
-                       d_item_off.as<int64_t>(), P, item_begin, item_end,
+                       d_item_off.as<int64_t>(), d_item_pair.as<int32_t>(), P, item_begin, item_end,
                        d_counter.as<unsigned long long>(), out, s);
     LC_CUDA(cudaEventRecord(ev1 ? ev1 : ev[EV_GAUSS1], s));
 }
