@@ -110,6 +110,10 @@ LC_API int lc_gauss_event_ms(lc_ctx *ctx, float *ms);
  * parameter domains, loop_off (L+1) segment offsets per loop. */
 LC_API int lc_model_upload(lc_ctx *ctx, const double *coeffs, const double *t, const int64_t *loop_off,
                            int64_t L);
+/* Same model when every loop is a plain closed polyline (LoopGeometry.from_polyline,
+ * geometry.py:269-283): only the vertices (M, 3) travel; the device builds
+ * a0 = v_k, a1 = v_{k+1} - v_k, a2 = a3 = 0, t = [0, 1] (bitwise the host arrays). */
+LC_API int lc_model_upload_polylines(lc_ctx *ctx, const double *verts, const int64_t *loop_off, int64_t L);
 /* Drop-in for geometry.tight_boxes (geometry.py:113-152): coeffs (m,4,3),
  * t (m,2) domains -> lo, hi (m,3).  Independent of the uploaded model. */
 LC_API int lc_tight_boxes(lc_ctx *ctx, const double *coeffs, const double *t, int64_t m, double *lo,

@@ -58,6 +58,7 @@ SIGNATURES = {
     "lc_gauss_event_ms": (ctypes.c_int, [_vp, _c_float_p]),
     "lc_probe_fp64_peak": (ctypes.c_int, [_vp, _c_double_p, _c_float_p]),
     "lc_model_upload": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int64]),
+    "lc_model_upload_polylines": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64]),
     "lc_tight_boxes": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, _vp, _vp]),
     "lc_loop_boxes": (ctypes.c_int, [_vp, _vp, _vp]),
     "lc_potential_link_search": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _c_int64_p]),
@@ -319,6 +320,13 @@ class Context:
         loop_off = np.ascontiguousarray(loop_off, dtype=np.int64)
         with self.lock:
             _check(self.lib.lc_model_upload(self.handle, _ptr(coeffs), _ptr(t), _ptr(loop_off), len(loop_off) - 1))
+        self._L = len(loop_off) - 1
+
+    def upload_model_polylines(self, verts, loop_off):
+        verts = np.ascontiguousarray(verts, dtype=np.float64)
+        loop_off = np.ascontiguousarray(loop_off, dtype=np.int64)
+        with self.lock:
+            _check(self.lib.lc_model_upload_polylines(self.handle, _ptr(verts), _ptr(loop_off), len(loop_off) - 1))
         self._L = len(loop_off) - 1
 
     def loop_boxes(self):

@@ -241,6 +241,21 @@ def device_step(ctx, xi, excl_keys, params, mode=None, timings=None):
     PLS -> discretize -> Gauss sum (sharded + all-gathered under torch.distributed).
     Returns (pairs int32 (P,2), raw, lk, flags) on the host."""
     mode = gauss_mode() if mode is None else mode
+    dist = _dist()
+    if dist is None:
+        # one C-ABI call for the whole device path; stage times from CUDA events
+        try:
+            ctx.run_pipeline(excl_keys, xi, params.epsilon, params.max_passes, params.max_subsegments, mode)
+        except _native.DiscretizeFailure as fail:
+            raise_for_failure(fail, params)
+        pairs = ctx.get_pairs()
+        raw, lk, flags = ctx.get_results()
+        if timings is not None:
+            st = ctx.stage_times()
+            timings["pls"] = timings.get("upload", 0.0) + 1e-3 * st["pls"]
+            timings["discretize"] = 1e-3 * st["discretize"]
+            timings["kernel"] = 1e-3 * (st["gauss"] + st["reduce"])
+        return pairs, raw, lk, flags
     t0 = time.perf_counter()
     ctx.potential_link_search(excl_keys)
     t1 = time.perf_counter()
@@ -249,11 +264,7 @@ def device_step(ctx, xi, excl_keys, params, mode=None, timings=None):
     except _native.DiscretizeFailure as fail:
         raise_for_failure(fail, params)
     t2 = time.perf_counter()
-    dist = _dist()
-    if dist is not None:
-        raw, lk, flags = _sharded_gauss(ctx, mode, dist)
-    else:
-        raw, lk, flags = ctx.evaluate_staged(mode)
+    raw, lk, flags = _sharded_gauss(ctx, mode, dist)
     pairs = ctx.get_pairs()
     if timings is not None:
         timings["pls"] = timings.get("upload", 0.0) + (t1 - t0)

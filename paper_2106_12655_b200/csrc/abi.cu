@@ -214,8 +214,8 @@ int lc_tight_boxes(lc_ctx *ctx, const double *coeffs, const double *t, int64_t m
         LC_CUDA(cudaMemcpyAsync(ctx->tb_coeffs.ptr, coeffs, sizeof(double) * 12 * m, cudaMemcpyHostToDevice, s));
         LC_CUDA(cudaMemcpyAsync(ctx->tb_t.ptr, t, sizeof(double) * 2 * m, cudaMemcpyHostToDevice, s));
         LC_CUDA(cudaMemcpyAsync(ctx->tb_off.ptr, off, sizeof off, cudaMemcpyHostToDevice, s));
-        launch_seg_boxes(ctx->tb_coeffs.as<double>(), ctx->tb_t.as<double>(), ctx->tb_off.as<int64_t>(), 1, m, -1.0,
-                         ctx->tb_box.as<double>(), ctx->tb_loop.as<int32_t>(), ctx->tb_flag.as<int>(), s);
+        launch_seg_boxes(ctx->tb_coeffs.as<double>(), ctx->tb_t.as<double>(), ctx->tb_off.as<int64_t>(), 1, m,
+                         ctx->tb_box.as<double>(), ctx->tb_loop.as<int32_t>(), nullptr, nullptr, s);
         std::vector<double> b((size_t)6 * m);
         LC_CUDA(cudaMemcpyAsync(b.data(), ctx->tb_box.ptr, sizeof(double) * 6 * m, cudaMemcpyDeviceToHost, s));
         LC_CUDA(cudaStreamSynchronize(s));
@@ -232,6 +232,14 @@ int lc_model_upload(lc_ctx *ctx, const double *coeffs, const double *t, const in
         if (L < 0 || !loop_off || (L > 0 && loop_off[L] > 0 && (!coeffs || !t)))
             throw Error(LC_ERR_ARG, "lc_model_upload: bad arguments");
         ctx->pipe.upload_model(coeffs, t, loop_off, L);
+    });
+}
+
+int lc_model_upload_polylines(lc_ctx *ctx, const double *verts, const int64_t *loop_off, int64_t L) {
+    return guarded(ctx, [&] {
+        if (L < 0 || !loop_off || (L > 0 && loop_off[L] > 0 && !verts))
+            throw Error(LC_ERR_ARG, "lc_model_upload_polylines: bad arguments");
+        ctx->pipe.upload_model_polylines(verts, loop_off, L);
     });
 }
 

@@ -7,19 +7,24 @@
 // exactly ([left halves..., right halves...] after every split, :91-98), so
 // the first-bad-child error report (:170-174) names the same loops.
 //
-// Pass structure (one host sync per pass):
-//   boxes (computed when the list was formed)
-//   -> per-loop sorted lower bounds on 3 axes (CUB segmented sort)
-//   -> per pair, per subsegment of either loop: binary search + sweep of the
-//      other loop's sorted list on the pair's axis, closed 3-axis test;
-//      hits set mark[] and the first marking pair via atomicMin (pairs are
-//      processed in PairList order in the reference, so "first partner" is
-//      the smallest pair index that hits the subsegment, :77-80,151-159)
-//   -> scan of marks: unmarked -> done list, marked -> two children
-//   -> children boxes, CurvesIntersect / max_subsegments checks per loop.
-// Final: stable sort of done chords by (segment, t_lo) (the lexsort of
-// :104), start points via eval_cubics (:89), validation as PolylineLoop
-// (geometry.py:333-340).
+// Per pass (one host sync):
+//   overlap detection for every PLS pair whose loops are active:
+//     small pairs (n_i*n_j <= 16384, both <= 256 — the reference's own
+//     brute-force rule, bvh.py:224,236): one warp per pair, loop j's boxes
+//     staged in shared memory, all box pairs tested;
+//     large pairs: per-loop sorted lower bounds on 3 axes (CUB segmented
+//     sort) + binary search and sweep on the pair's axis;
+//   a hit marks both subsegments (atomicOr, exact marked count) and records
+//   the first marking pair (atomicMin: the reference processes pairs in
+//   PairList order, :77-80,151-159);
+//   no marks -> the pass finishes every active subsegment; otherwise a scan
+//   of the marks moves unmarked entries to the done list and writes children,
+//   whose boxes feed the CurvesIntersect / max_subsegments checks (:166-180).
+// Fast path (polyline chainmail, one pass, nothing marked): the active list
+// is the segment list itself and the chords are the segment start points,
+// written straight into the Gauss-sum layout with PolylineLoop validation
+// fused in.  Vertices are eval_cubics(coeffs[seg], t_lo) in numpy's
+// operation order (:89) — bitwise the reference's.
 #include <climits>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -33,21 +38,266 @@ namespace lc {
 namespace {
 
 constexpr double kMachineEps = 2.220446049250313e-16;
-// "no index yet" sentinel of atomicMin slots initialized by cudaMemset(0x7f)
-constexpr int32_t kNoIndex = 0x7f7f7f7f;
+constexpr int32_t kNoIndex = 0x7f7f7f7f;       // atomicMin sentinel from cudaMemset(0x7f)
+constexpr int64_t kBruteLimit = 16384;         // bvh.py:224 BRUTE_FORCE_LIMIT
+constexpr int kBruteMaxSide = 256;             // shared-memory staging of loop j's boxes
+constexpr int kBruteWarps = 4;
 
-struct PassCounters {
-    int64_t total_marked;
-    int err_loop;
+struct PreCounters {
+    int zero_loop;     // first loop with a zero-length segment box (INT_MAX: none)
+    int n_unpaired;
+    int n_large;       // pairs handled by the sweep path
     int pad;
+    unsigned long long marked;
+    int err_loop;
+    int pad2;
 };
 
-__global__ void mark_paired_kernel(const int32_t *__restrict__ pairs, int64_t P, uint8_t *__restrict__ paired) {
+// View of the active subsegment list: either the segment arrays themselves
+// (identity, pass 1 with every loop paired) or materialized SoA arrays.
+struct ActView {
+    const int32_t *seg;   // nullptr: entry e is segment e
+    const int32_t *loop;
+    const double *tlo, *thi;
+    int tstride;
+    const double *box;
+    int64_t bstride;
+    const int64_t *off;
+};
+
+__device__ __forceinline__ double scale_of(const int *max_exp) {
+    int e = *max_exp - 1023;
+    e = e < -1022 ? -1022 : (e > 1022 ? 1022 : e);
+    return __hiloint2double((1023 - e) << 20, 0);   // 2^-e, exact
+}
+
+__device__ __forceinline__ bool brute_pair(int64_t ni, int64_t nj) {
+    return ni * nj <= kBruteLimit && ni <= kBruteMaxSide && nj <= kBruteMaxSide;
+}
+
+__device__ __forceinline__ int64_t upper_index(const int64_t *__restrict__ off, int64_t n, int64_t k) {
+    int64_t lo = 0, hi = n;   // largest idx in [0, n) with off[idx] <= k  (off[0] == 0)
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (off[mid] <= k) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ void mark_entry(uint32_t *__restrict__ mark, int32_t *__restrict__ first_pair, int64_t e,
+                                           int32_t p, unsigned long long *__restrict__ marked) {
+    if (atomicOr(mark + e, 1u) == 0u) atomicAdd(marked, 1ULL);
+    atomicMin(first_pair + e, p);
+}
+
+// ---------------------------------------------------------------- pre-pass
+
+__global__ void pre_pairs_kernel(const int32_t *__restrict__ pairs, int64_t P, const int64_t *__restrict__ loff,
+                                 const double *__restrict__ lbox, int64_t L, uint8_t *__restrict__ paired,
+                                 int8_t *__restrict__ axis, PreCounters *__restrict__ ctr) {
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p >= P) return;
-    paired[pairs[2 * p]] = 1;
-    paired[pairs[2 * p + 1]] = 1;
+    const int i = pairs[2 * p], j = pairs[2 * p + 1];
+    paired[i] = 1;
+    paired[j] = 1;
+    // sweep axis: the axis along which the two loop boxes' intersection is longest
+    int a = 0;
+    double best = -CUDART_INF;
+    for (int d = 0; d < 3; ++d) {
+        const double e = fmin(lbox[(3 + d) * L + i], lbox[(3 + d) * L + j]) - fmax(lbox[d * L + i], lbox[d * L + j]);
+        if (e > best) {
+            best = e;
+            a = d;
+        }
+    }
+    axis[p] = (int8_t)a;
+    if (!brute_pair(loff[i + 1] - loff[i], loff[j + 1] - loff[j])) atomicAdd(&ctr->n_large, 1);
 }
+
+__global__ void pre_loops_kernel(const unsigned long long *__restrict__ min_diag, const uint8_t *__restrict__ paired,
+                                 int64_t L, double min_diam, PreCounters *__restrict__ ctr) {
+    const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (l >= L) return;
+    if (__longlong_as_double((long long)min_diag[l]) < min_diam) atomicMin(&ctr->zero_loop, (int)l);
+    if (!paired[l]) atomicAdd(&ctr->n_unpaired, 1);
+}
+
+// ------------------------------------------------------------- detection
+
+__device__ __forceinline__ bool box_overlap(const double *__restrict__ b, int64_t stride, int64_t e,
+                                            const double lo[3], const double hi[3]) {
+    // closed-interval overlap (bvh.py:93-98)
+    return !(lo[0] > b[3 * stride + e] || b[e] > hi[0] || lo[1] > b[4 * stride + e] || b[stride + e] > hi[1] ||
+             lo[2] > b[5 * stride + e] || b[2 * stride + e] > hi[2]);
+}
+
+// Warp-wide compaction of the entries [b, b+n) whose box overlaps [lo, hi]
+// into list[]; returns the count (all lanes).
+__device__ __forceinline__ int filter_entries(const double *__restrict__ box, int64_t stride, int64_t b, int64_t n,
+                                              const double lo[3], const double hi[3], int32_t *list, int lane) {
+    int cnt = 0;
+    for (int64_t k0 = 0; k0 < n; k0 += 32) {
+        const int64_t k = k0 + lane;
+        const bool in = k < n && box_overlap(box, stride, b + k, lo, hi);
+        const unsigned bal = __ballot_sync(0xffffffffu, in);
+        if (in) list[cnt + __popc(bal & ((1u << lane) - 1u))] = (int32_t)(b + k);
+        cnt += __popc(bal);
+    }
+    __syncwarp();
+    return cnt;
+}
+
+// Warp per brute-force pair.  Only subsegments of loop i whose box meets the
+// union box of loop j's active subsegments can overlap one of them (and vice
+// versa), so both sides are first filtered against the other loop's union
+// box; the (usually tiny) filtered lists are then tested exhaustively.
+__global__ void __launch_bounds__(32 * kBruteWarps) brute_kernel(ActView v, const double *__restrict__ ubox,
+                                                                 int64_t L, const int32_t *__restrict__ pairs,
+                                                                 int64_t P, uint32_t *__restrict__ mark,
+                                                                 int32_t *__restrict__ first_pair,
+                                                                 unsigned long long *__restrict__ marked) {
+    __shared__ int32_t lists[kBruteWarps][2][kBruteMaxSide];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * kBruteWarps;
+    for (int64_t p = blockIdx.x * (int64_t)kBruteWarps + w; p < P; p += nw) {
+        const int i = pairs[2 * p], j = pairs[2 * p + 1];
+        const int64_t bi = v.off[i], ni = v.off[i + 1] - bi;
+        const int64_t bj = v.off[j], nj = v.off[j + 1] - bj;
+        if (ni == 0 || nj == 0 || !brute_pair(ni, nj)) continue;
+        double ilo[3], ihi[3], jlo[3], jhi[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            ilo[d] = ubox[d * L + i];
+            ihi[d] = ubox[(3 + d) * L + i];
+            jlo[d] = ubox[d * L + j];
+            jhi[d] = ubox[(3 + d) * L + j];
+        }
+        int32_t *si = lists[w][0], *tj = lists[w][1];
+        const int ns = filter_entries(v.box, v.bstride, bi, ni, jlo, jhi, si, lane);
+        const int nt = ns ? filter_entries(v.box, v.bstride, bj, nj, ilo, ihi, tj, lane) : 0;
+        const int tot = ns * nt;
+        for (int k = lane; k < tot; k += 32) {
+            const int64_t es = si[k / nt], et = tj[k % nt];
+            double lo[3], hi[3];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                lo[d] = v.box[d * v.bstride + es];
+                hi[d] = v.box[(3 + d) * v.bstride + es];
+            }
+            if (box_overlap(v.box, v.bstride, et, lo, hi)) {
+                mark_entry(mark, first_pair, es, (int32_t)p, marked);
+                mark_entry(mark, first_pair, et, (int32_t)p, marked);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// Union box of every loop's active subsegments (warp per loop).
+__global__ void union_boxes_kernel(const double *__restrict__ box, int64_t stride, const int64_t *__restrict__ off,
+                                   int64_t L, double *__restrict__ ubox) {
+    const int64_t l = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (l >= L) return;
+    double v[6] = {CUDART_INF, CUDART_INF, CUDART_INF, -CUDART_INF, -CUDART_INF, -CUDART_INF};
+    for (int64_t e = off[l] + lane; e < off[l + 1]; e += 32) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            v[d] = fmin(v[d], box[d * stride + e]);
+            v[3 + d] = fmax(v[3 + d], box[(3 + d) * stride + e]);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            v[d] = fmin(v[d], __shfl_xor_sync(0xffffffffu, v[d], o));
+            v[3 + d] = fmax(v[3 + d], __shfl_xor_sync(0xffffffffu, v[3 + d], o));
+        }
+    if (lane == 0)
+#pragma unroll
+        for (int d = 0; d < 6; ++d) ubox[d * L + l] = v[d];
+}
+
+// Marks of the identity view (entry = segment) -> the materialized paired-only list.
+__global__ void gather_marks_kernel(int64_t n, const int32_t *__restrict__ act_seg, const uint32_t *__restrict__ mark_in,
+                                    const int32_t *__restrict__ fp_in, uint32_t *__restrict__ mark_out,
+                                    int32_t *__restrict__ fp_out) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    const int32_t m = act_seg[e];
+    mark_out[e] = mark_in[m];
+    fp_out[e] = fp_in[m];
+}
+
+__global__ void copy_lo_kernel(const double *__restrict__ box, int64_t stride, int64_t n, int axis,
+                               double *__restrict__ key, int32_t *__restrict__ iota) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    key[e] = box[axis * stride + e];
+    if (iota) iota[e] = (int32_t)e;
+}
+
+// per pair: number of sweep threads (0 for brute-force pairs)
+__global__ void sweep_counts_kernel(const int32_t *__restrict__ pairs, int64_t P, const int64_t *__restrict__ off,
+                                    int64_t *__restrict__ cnt) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p < P) {
+        const int i = pairs[2 * p], j = pairs[2 * p + 1];
+        const int64_t ni = off[i + 1] - off[i], nj = off[j + 1] - off[j];
+        cnt[p] = (ni == 0 || nj == 0 || brute_pair(ni, nj)) ? 0 : ni + nj;
+    } else if (p == P) {
+        cnt[P] = 0;
+    }
+}
+
+__global__ void sweep_kernel(ActView v, const int32_t *__restrict__ pairs, int64_t P, const int8_t *__restrict__ axis,
+                             const int64_t *__restrict__ sweep_off, const double *__restrict__ k0,
+                             const double *__restrict__ k1, const double *__restrict__ k2,
+                             const int32_t *__restrict__ p0, const int32_t *__restrict__ p1,
+                             const int32_t *__restrict__ p2, uint32_t *__restrict__ mark,
+                             int32_t *__restrict__ first_pair, unsigned long long *__restrict__ marked) {
+    const int64_t total = sweep_off[P];
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = upper_index(sweep_off, P, k);
+        const int i = pairs[2 * p], j = pairs[2 * p + 1];
+        const int64_t ni = v.off[i + 1] - v.off[i];
+        const int64_t local = k - sweep_off[p];
+        const int A = local < ni ? i : j, B = local < ni ? j : i;
+        const int64_t e = v.off[A] + (local < ni ? local : local - ni);
+        const int a = axis[p];
+        const double *keys = a == 0 ? k0 : (a == 1 ? k1 : k2);
+        const int32_t *perm = a == 0 ? p0 : (a == 1 ? p1 : p2);
+        double el[3], eh[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            el[d] = v.box[d * v.bstride + e];
+            eh[d] = v.box[(3 + d) * v.bstride + e];
+        }
+        const double lo_a = el[a], hi_a = eh[a];
+        int64_t lo = v.off[B], hi = v.off[B + 1];
+        const int64_t end = hi;
+        while (lo < hi) {   // first q with keys[q] >= lo_a
+            const int64_t mid = (lo + hi) >> 1;
+            if (keys[mid] < lo_a) lo = mid + 1; else hi = mid;
+        }
+        bool hit_any = false;
+        for (int64_t q = lo; q < end && keys[q] <= hi_a; ++q) {
+            const int64_t tt = perm[q];
+            bool ov = true;
+#pragma unroll
+            for (int d = 0; d < 3; ++d)
+                if (el[d] > v.box[(3 + d) * v.bstride + tt] || v.box[d * v.bstride + tt] > eh[d]) ov = false;
+            if (ov) {
+                hit_any = true;
+                mark_entry(mark, first_pair, tt, (int32_t)p, marked);
+            }
+        }
+        if (hit_any) mark_entry(mark, first_pair, e, (int32_t)p, marked);
+    }
+}
+
+// ------------------------------------------------------------ split / done
 
 __global__ void init_counts_kernel(const int64_t *__restrict__ loff, const uint8_t *__restrict__ paired, int64_t L,
                                    int64_t *__restrict__ cnt) {
@@ -56,6 +306,7 @@ __global__ void init_counts_kernel(const int64_t *__restrict__ loff, const uint8
     else if (l == L) cnt[L] = 0;
 }
 
+// Materialize the pass-1 list (segments of paired loops, loop-major).
 __global__ void init_active_kernel(int64_t M, const int32_t *__restrict__ seg_loop, const int64_t *__restrict__ loff,
                                    const uint8_t *__restrict__ paired, const double *__restrict__ t,
                                    const double *__restrict__ seg_box, const int64_t *__restrict__ act_off,
@@ -74,109 +325,13 @@ __global__ void init_active_kernel(int64_t M, const int32_t *__restrict__ seg_lo
     for (int d = 0; d < 6; ++d) box[d * stride + e] = seg_box[d * M + m];
 }
 
-// Sweep axis per pair: the axis along which the two loop boxes' intersection is longest.
-__global__ void pair_axis_kernel(const int32_t *__restrict__ pairs, int64_t P, const double *__restrict__ lbox,
-                                 int64_t L, int8_t *__restrict__ axis) {
-    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (p >= P) return;
-    const int i = pairs[2 * p], j = pairs[2 * p + 1];
-    int a = 0;
-    double best = -CUDART_INF;
-    for (int d = 0; d < 3; ++d) {
-        const double e = fmin(lbox[(3 + d) * L + i], lbox[(3 + d) * L + j]) - fmax(lbox[d * L + i], lbox[d * L + j]);
-        if (e > best) { best = e; a = d; }
-    }
-    axis[p] = (int8_t)a;
-}
-
-__global__ void copy_lo_kernel(const double *__restrict__ box, int64_t stride, int64_t n, int axis,
-                               double *__restrict__ key, int32_t *__restrict__ iota) {
-    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (e >= n) return;
-    key[e] = box[axis * stride + e];
-    if (iota) iota[e] = (int32_t)e;
-}
-
-__global__ void sweep_counts_kernel(const int32_t *__restrict__ pairs, int64_t P, const int64_t *__restrict__ act_off,
-                                    int64_t *__restrict__ cnt) {
-    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (p < P) {
-        const int i = pairs[2 * p], j = pairs[2 * p + 1];
-        cnt[p] = (act_off[i + 1] - act_off[i]) + (act_off[j + 1] - act_off[j]);
-    } else if (p == P) {
-        cnt[P] = 0;
-    }
-}
-
-__device__ __forceinline__ int64_t upper_index(const int64_t *__restrict__ off, int64_t n, int64_t k) {
-    int64_t lo = 0, hi = n;   // largest idx in [0, n) with off[idx] <= k  (off[0] == 0)
-    while (hi - lo > 1) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (off[mid] <= k) lo = mid; else hi = mid;
-    }
-    return lo;
-}
-
-__global__ void sweep_kernel(const int32_t *__restrict__ pairs, int64_t P, const int8_t *__restrict__ axis,
-                             const int64_t *__restrict__ sweep_off, const int64_t *__restrict__ act_off,
-                             const double *__restrict__ box, int64_t stride, const double *__restrict__ k0,
-                             const double *__restrict__ k1, const double *__restrict__ k2,
-                             const int32_t *__restrict__ p0, const int32_t *__restrict__ p1,
-                             const int32_t *__restrict__ p2, uint8_t *__restrict__ mark,
-                             int32_t *__restrict__ first_pair) {
-    const int64_t total = sweep_off[P];
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
-         k += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t p = upper_index(sweep_off, P, k);
-        const int i = pairs[2 * p], j = pairs[2 * p + 1];
-        const int64_t ni = act_off[i + 1] - act_off[i];
-        const int64_t local = k - sweep_off[p];
-        const int A = local < ni ? i : j, B = local < ni ? j : i;
-        const int64_t e = act_off[A] + (local < ni ? local : local - ni);
-        const int a = axis[p];
-        const double *keys = a == 0 ? k0 : (a == 1 ? k1 : k2);
-        const int32_t *perm = a == 0 ? p0 : (a == 1 ? p1 : p2);
-        double el[3], eh[3];
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-            el[d] = box[d * stride + e];
-            eh[d] = box[(3 + d) * stride + e];
-        }
-        const double lo_a = el[a], hi_a = eh[a];
-        int64_t lo = act_off[B], hi = act_off[B + 1];
-        const int64_t end = hi;
-        while (lo < hi) {   // first q with keys[q] >= lo_a
-            const int64_t mid = (lo + hi) >> 1;
-            if (keys[mid] < lo_a) lo = mid + 1; else hi = mid;
-        }
-        bool hit_any = false;
-        for (int64_t q = lo; q < end && keys[q] <= hi_a; ++q) {
-            const int64_t tt = perm[q];
-            bool ov = true;
-#pragma unroll
-            for (int d = 0; d < 3; ++d) {
-                if (el[d] > box[(3 + d) * stride + tt] || box[d * stride + tt] > eh[d]) ov = false;
-            }
-            if (ov) {
-                hit_any = true;
-                mark[tt] = 1;
-                atomicMin(first_pair + tt, (int32_t)p);
-            }
-        }
-        if (hit_any) {
-            mark[e] = 1;
-            atomicMin(first_pair + e, (int32_t)p);
-        }
-    }
-}
-
-__global__ void mark_to_i64_kernel(const uint8_t *__restrict__ mark, int64_t n, int64_t *__restrict__ out) {
+__global__ void mark_to_i64_kernel(const uint32_t *__restrict__ mark, int64_t n, int64_t *__restrict__ out) {
     const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e < n) out[e] = mark[e];
     else if (e == n) out[n] = 0;
 }
 
-__global__ void finish_kernel(int64_t n_act, const int32_t *__restrict__ pairs, const uint8_t *__restrict__ mark,
+__global__ void finish_kernel(int64_t n_act, const int32_t *__restrict__ pairs, const uint32_t *__restrict__ mark,
                               const int64_t *__restrict__ mscan, const int32_t *__restrict__ first_pair,
                               const int64_t *__restrict__ act_off, const int32_t *__restrict__ act_seg,
                               const int32_t *__restrict__ act_loop, const double *__restrict__ act_tlo,
@@ -186,21 +341,27 @@ __global__ void finish_kernel(int64_t n_act, const int32_t *__restrict__ pairs, 
                               int32_t *__restrict__ done_seg, double *__restrict__ done_tlo) {
     const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e >= n_act) return;
-    const int64_t r = mscan[e];
+    const int64_t r = mscan ? mscan[e] : 0;
     const int l = act_loop[e];
     const int32_t seg = act_seg[e];
     const double tlo = act_tlo[e], thi = act_thi[e];
-    if (mark[e]) {
+    if (mark && mark[e]) {
         const int64_t base = mscan[act_off[l]];
         const int64_t cnt = mscan[act_off[l + 1]] - base;
         const int64_t k = r - base, no = 2 * base;
         const double tm = __dmul_rn(0.5, __dadd_rn(tlo, thi));   // 0.5 * (tlo + thi)  (:95)
         const int32_t pp = first_pair[e];
         const int32_t partner = pairs[2 * pp] == l ? pairs[2 * pp + 1] : pairs[2 * pp];
-        nxt_seg[no + k] = seg;       nxt_loop[no + k] = l;
-        nxt_tlo[no + k] = tlo;       nxt_thi[no + k] = tm;       nxt_partner[no + k] = partner;
-        nxt_seg[no + cnt + k] = seg; nxt_loop[no + cnt + k] = l;
-        nxt_tlo[no + cnt + k] = tm;  nxt_thi[no + cnt + k] = thi; nxt_partner[no + cnt + k] = partner;
+        nxt_seg[no + k] = seg;
+        nxt_loop[no + k] = l;
+        nxt_tlo[no + k] = tlo;
+        nxt_thi[no + k] = tm;
+        nxt_partner[no + k] = partner;
+        nxt_seg[no + cnt + k] = seg;
+        nxt_loop[no + cnt + k] = l;
+        nxt_tlo[no + cnt + k] = tm;
+        nxt_thi[no + cnt + k] = thi;
+        nxt_partner[no + cnt + k] = partner;
     } else {
         const int64_t d = n_done + (e - r);
         done_seg[d] = seg;
@@ -234,10 +395,8 @@ __global__ void child_boxes_kernel(int64_t n, const double *__restrict__ coeffs,
 }
 
 __global__ void pass_errors_kernel(const int64_t *__restrict__ nxt_off, const int32_t *__restrict__ bad_first,
-                                   int64_t L, int64_t max_sub, const int64_t *__restrict__ mscan, int64_t n_act,
-                                   PassCounters *__restrict__ ctr) {
+                                   int64_t L, int64_t max_sub, PreCounters *__restrict__ ctr) {
     const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (l == 0) ctr->total_marked = mscan[n_act];
     if (l >= L) return;
     const int64_t c = nxt_off[l + 1] - nxt_off[l];
     if (c > 0 && (bad_first[l] != kNoIndex || c > max_sub)) atomicMin(&ctr->err_loop, (int)l);
@@ -268,67 +427,130 @@ __global__ void out_counts_kernel(const unsigned long long *__restrict__ dcnt, c
     }
 }
 
-// Start points of the given (segment, t) list into AoS at out_off[loop] + local.
+__global__ void closed_offsets_kernel(const int64_t *__restrict__ off, int64_t L, int64_t *__restrict__ voff) {
+    const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (l <= L) voff[l] = off[l] + l;
+}
+
+__device__ __forceinline__ void put_closed(double *__restrict__ X, double *__restrict__ Y, double *__restrict__ Z,
+                                           int64_t vo, int64_t local, int64_t n, const double p[3], double sc) {
+    X[vo + local] = p[0] * sc;
+    Y[vo + local] = p[1] * sc;
+    Z[vo + local] = p[2] * sc;
+    if (local == 0) {   // closing vertex (direct.py:164-166)
+        X[vo + n] = p[0] * sc;
+        Y[vo + n] = p[1] * sc;
+        Z[vo + n] = p[2] * sc;
+    }
+}
+
+// No-split fast path: chord vertex m = start point of segment m for every loop
+// (paired loops keep all segments; unpaired loops are control chords, :108-109),
+// with the PolylineLoop checks fused (geometry.py:333-340).
+__global__ void write_all_kernel(int64_t M, const double *__restrict__ coeffs, const double *__restrict__ t,
+                                 const int32_t *__restrict__ seg_loop, const int64_t *__restrict__ loff,
+                                 const int *__restrict__ max_exp, double thr, double *__restrict__ X,
+                                 double *__restrict__ Y, double *__restrict__ Z, unsigned *__restrict__ flags) {
+    const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (m >= M) return;
+    const int l = seg_loop[m];
+    const int64_t b = loff[l], n = loff[l + 1] - b, local = m - b;
+    const int64_t nx = local + 1 < n ? m + 1 : b;
+    double p[3], q[3];
+    eval_point(coeffs + 12 * m, t[2 * m], p);
+    eval_point(coeffs + 12 * nx, t[2 * nx], q);
+    put_closed(X, Y, Z, b + l, local, n, p, scale_of(max_exp));
+    unsigned f = 0;
+    if (!(isfinite(p[0]) && isfinite(p[1]) && isfinite(p[2]))) f |= 1;
+    const double dx = __dsub_rn(q[0], p[0]), dy = __dsub_rn(q[1], p[1]), dz = __dsub_rn(q[2], p[2]);
+    if (__dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz))) <= thr) f |= 2;
+    if (f) atomicOr(flags + l, f);
+}
+
+// General path: sorted done chords + unpaired control chords into the closed SoA.
 __global__ void write_done_kernel(int64_t n, const int32_t *__restrict__ seg, const double *__restrict__ tlo,
                                   const int32_t *__restrict__ idx, const int32_t *__restrict__ seg_loop,
                                   const double *__restrict__ coeffs, const int64_t *__restrict__ out_off,
-                                  const int64_t *__restrict__ done_off, double *__restrict__ verts) {
+                                  const int64_t *__restrict__ done_off, const int *__restrict__ max_exp,
+                                  double *__restrict__ X, double *__restrict__ Y, double *__restrict__ Z) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= n) return;
     const int32_t s = seg[k];
     const double t = idx ? tlo[idx[k]] : tlo[k];
     const int l = seg_loop[s];
-    const int64_t pos = out_off[l] + (k - done_off[l]);
+    const int64_t local = k - done_off[l];
     double p[3];
     eval_point(coeffs + 12 * (int64_t)s, t, p);
-    verts[3 * pos] = p[0];
-    verts[3 * pos + 1] = p[1];
-    verts[3 * pos + 2] = p[2];
+    put_closed(X, Y, Z, out_off[l] + l, local, out_off[l + 1] - out_off[l], p, scale_of(max_exp));
 }
 
-// Unpaired loops: chords through the segment start points (_chord_loop, :108-109).
 __global__ void write_unpaired_kernel(int64_t M, const int32_t *__restrict__ seg_loop, const uint8_t *__restrict__ paired,
                                       const int64_t *__restrict__ loff, const double *__restrict__ coeffs,
                                       const double *__restrict__ t, const int64_t *__restrict__ out_off,
-                                      double *__restrict__ verts) {
+                                      const int *__restrict__ max_exp, double *__restrict__ X, double *__restrict__ Y,
+                                      double *__restrict__ Z, double *__restrict__ aos) {
     const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (m >= M) return;
     const int l = seg_loop[m];
-    if (paired && paired[l]) return;
-    const int64_t pos = (out_off ? out_off[l] : loff[l]) + (m - loff[l]);
+    if (paired[l]) return;
+    const int64_t local = m - loff[l];
     double p[3];
     eval_point(coeffs + 12 * m, t[2 * m], p);
-    verts[3 * pos] = p[0];
-    verts[3 * pos + 1] = p[1];
-    verts[3 * pos + 2] = p[2];
+    if (aos) {   // temporary AoS in segment layout (pre-pass validation)
+        aos[3 * m] = p[0];
+        aos[3 * m + 1] = p[1];
+        aos[3 * m + 2] = p[2];
+    } else {
+        put_closed(X, Y, Z, out_off[l] + l, local, out_off[l + 1] - out_off[l], p, scale_of(max_exp));
+    }
 }
 
-// PolylineLoop validation (geometry.py:333-340) of loops with want(l):
-// flags bit0 non-finite vertex, bit1 segment length <= eps*scale.
-__global__ void validate_vertices_kernel(const double *__restrict__ v, const int64_t *__restrict__ off, int64_t L,
-                                         int64_t n, const uint8_t *__restrict__ paired, int want_paired,
-                                         double thr, unsigned *__restrict__ flags) {
+// PolylineLoop checks of loops with paired[l] == want over AoS vertices with offsets `off`.
+__global__ void validate_aos_kernel(const double *__restrict__ v, const int64_t *__restrict__ off,
+                                    const int32_t *__restrict__ seg_loop, int64_t n,
+                                    const uint8_t *__restrict__ paired, int want, double thr,
+                                    unsigned *__restrict__ flags) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= n) return;
-    const int64_t l = upper_index(off, L, k);
-    if (paired && (int)paired[l] != want_paired) return;
+    const int64_t l = seg_loop[k];   // AoS in segment layout: vertex k is segment k's start
+    if (paired && (int)paired[l] != want) return;
     const int64_t b = off[l], e = off[l + 1];
     const int64_t nx = (k + 1 < e) ? k + 1 : b;
     const double x = v[3 * k], y = v[3 * k + 1], z = v[3 * k + 2];
     unsigned f = 0;
     if (!(isfinite(x) && isfinite(y) && isfinite(z))) f |= 1;
     const double dx = __dsub_rn(v[3 * nx], x), dy = __dsub_rn(v[3 * nx + 1], y), dz = __dsub_rn(v[3 * nx + 2], z);
-    const double len = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
-    if (len <= thr) f |= 2;
+    if (__dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz))) <= thr) f |= 2;
     if (f) atomicOr(flags + l, f);
 }
 
-__global__ void validate_loops_kernel(const int64_t *__restrict__ off, int64_t L, const uint8_t *__restrict__ paired,
-                                      int want_paired, const unsigned *__restrict__ flags, int *__restrict__ err) {
+// Same over the scaled closed SoA (vertex k+1 always exists); thr_scaled = thr * 2^-e.
+__global__ void validate_soa_kernel(const double *__restrict__ X, const double *__restrict__ Y,
+                                    const double *__restrict__ Z, const int64_t *__restrict__ voff, int64_t L,
+                                    int64_t nclosed, const uint8_t *__restrict__ paired, int want,
+                                    const int *__restrict__ max_exp, double thr, unsigned *__restrict__ flags) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= nclosed) return;
+    const int64_t l = upper_index(voff, L, k);
+    if (k == voff[l + 1] - 1) return;   // closing vertex
+    if (paired && (int)paired[l] != want) return;
+    const double x = X[k], y = Y[k], z = Z[k];
+    unsigned f = 0;
+    if (!(isfinite(x) && isfinite(y) && isfinite(z))) f |= 1;
+    const double dx = __dsub_rn(X[k + 1], x), dy = __dsub_rn(Y[k + 1], y), dz = __dsub_rn(Z[k + 1], z);
+    const double len = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+    if (len <= thr * scale_of(max_exp)) f |= 2;
+    if (f) atomicOr(flags + l, f);
+}
+
+// First invalid loop among loops with paired == want (or all when paired == nullptr).
+__global__ void validate_loops_kernel(const int64_t *__restrict__ off, int64_t L, int closed_layout,
+                                      const uint8_t *__restrict__ paired, int want, const unsigned *__restrict__ flags,
+                                      int *__restrict__ err) {
     const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (l >= L) return;
-    if (paired && (int)paired[l] != want_paired) return;
-    const int64_t n = off[l + 1] - off[l];
+    if (paired && (int)paired[l] != want) return;
+    const int64_t n = off[l + 1] - off[l] - closed_layout;
     int kind = PL_OK;
     if (n < 3) kind = PL_TOO_FEW;
     else if (flags[l] & 1) kind = PL_NONFINITE;
@@ -336,17 +558,18 @@ __global__ void validate_loops_kernel(const int64_t *__restrict__ off, int64_t L
     if (kind) atomicMin(err, (int)(l * 4 + kind));
 }
 
-__global__ void zero_length_kernel(const double *__restrict__ box, int64_t M, const int32_t *__restrict__ seg_loop,
-                                   double min_diam, int *__restrict__ zl) {
-    const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (m >= M) return;
-    double bl[3], bh[3];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-        bl[d] = box[d * M + m];
-        bh[d] = box[(3 + d) * M + m];
-    }
-    if (diag_norm(bl, bh) < min_diam) atomicMin(zl, (int)seg_loop[m]);
+__global__ void unpack_kernel(const double *__restrict__ X, const double *__restrict__ Y, const double *__restrict__ Z,
+                              const int64_t *__restrict__ voff, int64_t L, int64_t nclosed,
+                              const int *__restrict__ max_exp, double *__restrict__ aos) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= nclosed) return;
+    const int64_t l = upper_index(voff, L, k);
+    if (k == voff[l + 1] - 1) return;
+    const int64_t o = k - l;   // plain index
+    const double inv = 1.0 / scale_of(max_exp);   // exact power of two
+    aos[3 * o] = X[k] * inv;
+    aos[3 * o + 1] = Y[k] * inv;
+    aos[3 * o + 2] = Z[k] * inv;
 }
 
 inline unsigned grid_for(int64_t n, int threads = 256) { return (unsigned)(n > 0 ? ceil_div(n, threads) : 1); }
@@ -358,25 +581,6 @@ template <class T> T d2h(const void *p, cudaStream_t s) {
     return v;
 }
 
-// Validate loops selected by paired==want; returns loop*4+kind or INT_MAX.
-int validate(const double *verts, const int64_t *off, int64_t L, int64_t n, const uint8_t *paired, int want,
-             double thr, DiscScratch &sc, cudaStream_t s) {
-    sc.val_flags.reserve(sizeof(unsigned) * (L > 0 ? L : 1), s);
-    sc.loop_err.reserve(sizeof(int), s);
-    LC_CUDA(cudaMemsetAsync(sc.val_flags.ptr, 0, sizeof(unsigned) * L, s));
-    const int init = INT_MAX;
-    LC_CUDA(cudaMemcpyAsync(sc.loop_err.ptr, &init, sizeof(int), cudaMemcpyHostToDevice, s));
-    if (n > 0) {
-        validate_vertices_kernel<<<grid_for(n), 256, 0, s>>>(verts, off, L, n, paired, want, thr,
-                                                             sc.val_flags.as<unsigned>());
-        LC_CHECK_LAUNCH();
-    }
-    validate_loops_kernel<<<grid_for(L), 256, 0, s>>>(off, L, paired, want, sc.val_flags.as<unsigned>(),
-                                                      sc.loop_err.as<int>());
-    LC_CHECK_LAUNCH();
-    return d2h<int>(sc.loop_err.ptr, s);
-}
-
 void scan_i64(const int64_t *in, int64_t *out, int64_t n, DiscScratch &sc, cudaStream_t s) {
     size_t bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, (int)n);
@@ -385,142 +589,223 @@ void scan_i64(const int64_t *in, int64_t *out, int64_t n, DiscScratch &sc, cudaS
     LC_CUB(cub::DeviceScan::ExclusiveSum(sc.cub_tmp.ptr, bytes, in, out, (int)n, s));
 }
 
+int finish_validation(DiscScratch &sc, const int64_t *off, int64_t L, int closed_layout, const uint8_t *paired,
+                      int want, cudaStream_t s) {
+    const int init = INT_MAX;
+    LC_CUDA(cudaMemcpyAsync(sc.loop_err.ptr, &init, sizeof(int), cudaMemcpyHostToDevice, s));
+    validate_loops_kernel<<<grid_for(L), 256, 0, s>>>(off, L, closed_layout, paired, want, sc.val_flags.as<unsigned>(),
+                                                      sc.loop_err.as<int>());
+    LC_CHECK_LAUNCH();
+    return d2h<int>(sc.loop_err.ptr, s);
+}
+
+bool polyline_error(int ve, DiscError *err) {
+    if (ve == INT_MAX) return false;
+    err->kind = DISC_INVALID_POLYLINE;
+    err->detail = ve & 3;
+    err->loops = {ve >> 2};
+    return true;
+}
+
 }  // namespace
 
-bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc, DiscOutput &out,
-                    DiscError *err, cudaStream_t s) {
+void unpack_polylines(const DiscOutput &out, int64_t L, const int *max_exp, double *aos, cudaStream_t s) {
+    if (out.Vc == 0) return;
+    unpack_kernel<<<grid_for(out.Vc), 256, 0, s>>>(out.X.as<double>(), out.Y.as<double>(), out.Z.as<double>(),
+                                                   out.voff.as<int64_t>(), L, out.Vc, max_exp, aos);
+    LC_CHECK_LAUNCH();
+}
+
+bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc, DiscOutput &out, DiscError *err,
+                    cudaStream_t s) {
     const int64_t L = in.L, M = in.M, P = in.P;
     const double min_diam = prm.epsilon * prm.xi;      // discretize.py:122
     const double poly_thr = kMachineEps * prm.xi;       // PolylineLoop(xi_hint=xi), geometry.py:338-340
     out.passes = 0;
     out.splits = 0;
 
-    // (1) ZeroLengthInput over all loops in order (:124-129).
+    // ---- (1) pre-pass: paired flags, pair axes, zero-length check, counts (one sync)
+    sc.paired.reserve(L > 0 ? L : 1, s);
+    sc.pair_axis.reserve(P > 0 ? P : 1, s);
+    sc.prectr.reserve(sizeof(PreCounters), s);
     sc.loop_err.reserve(sizeof(int), s);
-    {
-        const int init = INT_MAX;
-        LC_CUDA(cudaMemcpyAsync(sc.loop_err.ptr, &init, sizeof(int), cudaMemcpyHostToDevice, s));
-        if (M > 0)
-            zero_length_kernel<<<grid_for(M), 256, 0, s>>>(in.seg_box, M, in.seg_loop, min_diam, sc.loop_err.as<int>());
+    sc.val_flags.reserve(sizeof(unsigned) * (L > 0 ? L : 1), s);
+    LC_CUDA(cudaMemsetAsync(sc.paired.ptr, 0, L > 0 ? L : 1, s));
+    PreCounters pc0{INT_MAX, 0, 0, 0, 0, INT_MAX, 0};
+    LC_CUDA(cudaMemcpyAsync(sc.prectr.ptr, &pc0, sizeof pc0, cudaMemcpyHostToDevice, s));
+    PreCounters *ctr = sc.prectr.as<PreCounters>();
+    if (P > 0) {
+        pre_pairs_kernel<<<grid_for(P), 256, 0, s>>>(in.pairs, P, in.loff, in.loop_box, L, sc.paired.as<uint8_t>(),
+                                                     sc.pair_axis.as<int8_t>(), ctr);
         LC_CHECK_LAUNCH();
     }
-    const int zl = d2h<int>(sc.loop_err.ptr, s);
-    if (zl != INT_MAX) {
+    if (L > 0) {
+        pre_loops_kernel<<<grid_for(L), 256, 0, s>>>(in.loop_min_diag, sc.paired.as<uint8_t>(), L, min_diam, ctr);
+        LC_CHECK_LAUNCH();
+    }
+    const PreCounters pc = d2h<PreCounters>(sc.prectr.ptr, s);
+    if (pc.zero_loop != INT_MAX) {   // ZeroLengthInput, first loop in order (:124-129)
         err->kind = DISC_ZERO_LENGTH;
-        err->loops = {zl};
+        err->loops = {pc.zero_loop};
         return false;
     }
-
-    // (2) paired loops; unpaired loops become control chords, validated now (:131-142).
-    sc.paired.reserve(L > 0 ? L : 1, s);
-    LC_CUDA(cudaMemsetAsync(sc.paired.ptr, 0, L, s));
-    if (P > 0) mark_paired_kernel<<<grid_for(P), 256, 0, s>>>(in.pairs, P, sc.paired.as<uint8_t>());
-    LC_CHECK_LAUNCH();
-    // unpaired start points into a temporary AoS in original segment layout (reuse out.verts)
-    out.verts.reserve(sizeof(double) * 3 * (M > 0 ? M : 1), s);
-    if (M > 0)
+    // ---- (2) unpaired loops are control chords, validated before any pass (:131-142)
+    if (pc.n_unpaired > 0 && M > 0) {
+        sc.tmp_aos.reserve(sizeof(double) * 3 * M, s);
         write_unpaired_kernel<<<grid_for(M), 256, 0, s>>>(M, in.seg_loop, sc.paired.as<uint8_t>(), in.loff, in.coeffs,
-                                                          in.t, nullptr, out.verts.as<double>());
-    LC_CHECK_LAUNCH();
-    {
-        const int ve = validate(out.verts.as<double>(), in.loff, L, M, sc.paired.as<uint8_t>(), 0, poly_thr, sc, s);
-        if (ve != INT_MAX) {
-            err->kind = DISC_INVALID_POLYLINE;
-            err->detail = ve & 3;
-            err->loops = {ve >> 2};
-            return false;
-        }
+                                                          in.t, nullptr, in.max_exp, nullptr, nullptr, nullptr,
+                                                          sc.tmp_aos.as<double>());
+        LC_CHECK_LAUNCH();
+        LC_CUDA(cudaMemsetAsync(sc.val_flags.ptr, 0, sizeof(unsigned) * L, s));
+        validate_aos_kernel<<<grid_for(M), 256, 0, s>>>(sc.tmp_aos.as<double>(), in.loff, in.seg_loop, M,
+                                                        sc.paired.as<uint8_t>(), 0, poly_thr,
+                                                        sc.val_flags.as<unsigned>());
+        LC_CHECK_LAUNCH();
+        if (polyline_error(finish_validation(sc, in.loff, L, 0, sc.paired.as<uint8_t>(), 0, s), err)) return false;
     }
 
-    // (3) initial active list: all segments of paired loops, loop-major.
-    sc.act_off.reserve(sizeof(int64_t) * (L + 1), s);
-    sc.nxt_off.reserve(sizeof(int64_t) * (L + 1), s);
-    sc.counters.reserve(sizeof(int64_t) * (L + 2), s);   // temp counts
-    init_counts_kernel<<<grid_for(L + 1), 256, 0, s>>>(in.loff, sc.paired.as<uint8_t>(), L, sc.counters.as<int64_t>());
-    LC_CHECK_LAUNCH();
-    scan_i64(sc.counters.as<int64_t>(), sc.act_off.as<int64_t>(), L + 1, sc, s);
-    int64_t n_act = d2h<int64_t>(sc.act_off.as<int64_t>() + L, s);
-    int64_t stride = n_act > 0 ? n_act : 1;
-    auto reserve_list = [&](DevBuf &seg, DevBuf &loop, DevBuf &tlo, DevBuf &thi, DevBuf &box, int64_t cap) {
-        seg.reserve(sizeof(int32_t) * cap, s);
-        loop.reserve(sizeof(int32_t) * cap, s);
-        tlo.reserve(sizeof(double) * cap, s);
-        thi.reserve(sizeof(double) * cap, s);
-        box.reserve(sizeof(double) * 6 * cap, s);
+    // ---- (3) passes
+    // pass-1 list: the segment arrays themselves when every loop is paired
+    const bool identity = pc.n_unpaired == 0;
+    int64_t n_act = 0, stride = 1;
+    ActView view{};
+    auto materialize = [&]() {
+        sc.act_off.reserve(sizeof(int64_t) * (L + 1), s);
+        sc.counters.reserve(sizeof(int64_t) * (L + 2), s);
+        init_counts_kernel<<<grid_for(L + 1), 256, 0, s>>>(in.loff, sc.paired.as<uint8_t>(), L,
+                                                           sc.counters.as<int64_t>());
+        LC_CHECK_LAUNCH();
+        scan_i64(sc.counters.as<int64_t>(), sc.act_off.as<int64_t>(), L + 1, sc, s);
+        n_act = d2h<int64_t>(sc.act_off.as<int64_t>() + L, s);
+        stride = n_act > 0 ? n_act : 1;
+        sc.act_seg.reserve(sizeof(int32_t) * stride, s);
+        sc.act_loop.reserve(sizeof(int32_t) * stride, s);
+        sc.act_tlo.reserve(sizeof(double) * stride, s);
+        sc.act_thi.reserve(sizeof(double) * stride, s);
+        sc.box.reserve(sizeof(double) * 6 * stride, s);
+        if (M > 0) {
+            init_active_kernel<<<grid_for(M), 256, 0, s>>>(M, in.seg_loop, in.loff, sc.paired.as<uint8_t>(), in.t,
+                                                           in.seg_box, sc.act_off.as<int64_t>(), stride,
+                                                           sc.act_seg.as<int32_t>(), sc.act_loop.as<int32_t>(),
+                                                           sc.act_tlo.as<double>(), sc.act_thi.as<double>(),
+                                                           sc.box.as<double>());
+            LC_CHECK_LAUNCH();
+        }
     };
-    reserve_list(sc.act_seg, sc.act_loop, sc.act_tlo, sc.act_thi, sc.box, stride);
-    if (M > 0)
-        init_active_kernel<<<grid_for(M), 256, 0, s>>>(M, in.seg_loop, in.loff, sc.paired.as<uint8_t>(), in.t, in.seg_box,
-                                                       sc.act_off.as<int64_t>(), stride, sc.act_seg.as<int32_t>(),
-                                                       sc.act_loop.as<int32_t>(), sc.act_tlo.as<double>(),
-                                                       sc.act_thi.as<double>(), sc.box.as<double>());
-    LC_CHECK_LAUNCH();
-    sc.pair_axis.reserve(P > 0 ? P : 1, s);
-    if (P > 0) pair_axis_kernel<<<grid_for(P), 256, 0, s>>>(in.pairs, P, in.loop_box, L, sc.pair_axis.as<int8_t>());
-    LC_CHECK_LAUNCH();
-    sc.sweep_off.reserve(sizeof(int64_t) * (P + 1), s);
-    sc.bad_first.reserve(sizeof(int32_t) * (L > 0 ? L : 1), s);
-
+    auto act_view = [&]() {
+        return ActView{sc.act_seg.as<int32_t>(), sc.act_loop.as<int32_t>(), sc.act_tlo.as<double>(),
+                       sc.act_thi.as<double>(), 1, sc.box.as<double>(), stride, sc.act_off.as<int64_t>()};
+    };
+    // Pass 1 always runs on the segment arrays themselves (entry e == segment e):
+    // unpaired loops belong to no pair, so nothing marks them, and with no mark
+    // at all the chords are the segment start points of every loop.
+    n_act = M;
+    view = ActView{nullptr, in.seg_loop, in.t, in.t + 1, 2, in.seg_box, M > 0 ? M : 1, in.loff};
+    bool is_identity = true;
+    const double *ubox = in.loop_box;   // union boxes of the active subsegments per loop
+    sc.ubox.reserve(sizeof(double) * 6 * (L > 0 ? L : 1), s);
+    int64_t n_large = pc.n_large;
     int64_t n_done = 0;
+    sc.bad_first.reserve(sizeof(int32_t) * (L > 0 ? L : 1), s);
+    sc.sweep_off.reserve(sizeof(int64_t) * (P + 1), s);
     const int nsm = 148;
-    int pass = 0;
-    for (; pass < prm.max_passes; ++pass) {
+    for (int pass = 0; pass < prm.max_passes; ++pass) {
         if (n_act == 0) break;
         out.passes = pass + 1;
-        // per-loop sorted lower bounds on each axis
-        sc.iota.reserve(sizeof(int32_t) * n_act, s);
-        for (int a = 0; a < 3; ++a) {
-            sc.skey[a].reserve(sizeof(double) * n_act, s);
-            sc.sperm[a].reserve(sizeof(int32_t) * n_act, s);
-        }
-        DevBuf &tmpkey = sc.done_tlo2;   // scratch: unsorted keys
-        tmpkey.reserve(sizeof(double) * n_act, s);
-        for (int a = 0; a < 3; ++a) {
-            copy_lo_kernel<<<grid_for(n_act), 256, 0, s>>>(sc.box.as<double>(), stride, n_act, a, tmpkey.as<double>(),
-                                                          a == 0 ? sc.iota.as<int32_t>() : nullptr);
-            LC_CHECK_LAUNCH();
-            size_t bytes = 0;
-            cub::DeviceSegmentedSort::SortPairs(nullptr, bytes, tmpkey.as<double>(), sc.skey[a].as<double>(),
-                                                sc.iota.as<int32_t>(), sc.sperm[a].as<int32_t>(), (int)n_act, (int)L,
-                                                sc.act_off.as<int64_t>(), sc.act_off.as<int64_t>() + 1);
-            sc.cub_tmp.reserve(bytes, s);
-            bytes = sc.cub_tmp.bytes;
-            LC_CUB(cub::DeviceSegmentedSort::SortPairs(sc.cub_tmp.ptr, bytes, tmpkey.as<double>(),
-                                                        sc.skey[a].as<double>(), sc.iota.as<int32_t>(),
-                                                        sc.sperm[a].as<int32_t>(), (int)n_act, (int)L,
-                                                        sc.act_off.as<int64_t>(), sc.act_off.as<int64_t>() + 1, s));
-        }
-        // sweep over pairs
-        sc.mark.reserve(n_act, s);
+        sc.mark.reserve(sizeof(uint32_t) * n_act, s);
         sc.first_pair.reserve(sizeof(int32_t) * n_act, s);
-        LC_CUDA(cudaMemsetAsync(sc.mark.ptr, 0, n_act, s));
+        LC_CUDA(cudaMemsetAsync(sc.mark.ptr, 0, sizeof(uint32_t) * n_act, s));
         LC_CUDA(cudaMemsetAsync(sc.first_pair.ptr, 0x7f, sizeof(int32_t) * n_act, s));
+        LC_CUDA(cudaMemsetAsync(&ctr->marked, 0, sizeof(unsigned long long), s));
+        unsigned long long *marked_ctr = &ctr->marked;
         if (P > 0) {
+            // small pairs: brute force in shared memory
+            const int64_t blocks = ceil_div(P, kBruteWarps) < nsm * 16 ? ceil_div(P, kBruteWarps) : nsm * 16;
+            if (!is_identity) {
+                union_boxes_kernel<<<grid_for(L * 32), 256, 0, s>>>(view.box, view.bstride, view.off, L,
+                                                                    sc.ubox.as<double>());
+                LC_CHECK_LAUNCH();
+                ubox = sc.ubox.as<double>();
+            }
+            brute_kernel<<<(unsigned)blocks, 32 * kBruteWarps, 0, s>>>(view, ubox, L, in.pairs, P,
+                                                                       sc.mark.as<uint32_t>(),
+                                                                       sc.first_pair.as<int32_t>(), marked_ctr);
+            LC_CHECK_LAUNCH();
+            // large pairs: segmented sorts + sweep (pass 1: count known; later passes: recount)
             sc.counters.reserve(sizeof(int64_t) * (P + 1), s);
-            sweep_counts_kernel<<<grid_for(P + 1), 256, 0, s>>>(in.pairs, P, sc.act_off.as<int64_t>(),
-                                                               sc.counters.as<int64_t>());
-            LC_CHECK_LAUNCH();
-            scan_i64(sc.counters.as<int64_t>(), sc.sweep_off.as<int64_t>(), P + 1, sc, s);
-            sweep_kernel<<<nsm * 8, 256, 0, s>>>(in.pairs, P, sc.pair_axis.as<int8_t>(), sc.sweep_off.as<int64_t>(),
-                                                 sc.act_off.as<int64_t>(), sc.box.as<double>(), stride,
-                                                 sc.skey[0].as<double>(), sc.skey[1].as<double>(),
-                                                 sc.skey[2].as<double>(), sc.sperm[0].as<int32_t>(),
-                                                 sc.sperm[1].as<int32_t>(), sc.sperm[2].as<int32_t>(),
-                                                 sc.mark.as<uint8_t>(), sc.first_pair.as<int32_t>());
-            LC_CHECK_LAUNCH();
+            if (pass > 0) {
+                sweep_counts_kernel<<<grid_for(P + 1), 256, 0, s>>>(in.pairs, P, view.off, sc.counters.as<int64_t>());
+                LC_CHECK_LAUNCH();
+                scan_i64(sc.counters.as<int64_t>(), sc.sweep_off.as<int64_t>(), P + 1, sc, s);
+                n_large = d2h<int64_t>(sc.sweep_off.as<int64_t>() + P, s);
+            }
+            if (n_large > 0) {
+                if (pass == 0) {
+                    sweep_counts_kernel<<<grid_for(P + 1), 256, 0, s>>>(in.pairs, P, view.off,
+                                                                       sc.counters.as<int64_t>());
+                    LC_CHECK_LAUNCH();
+                    scan_i64(sc.counters.as<int64_t>(), sc.sweep_off.as<int64_t>(), P + 1, sc, s);
+                }
+                sc.iota.reserve(sizeof(int32_t) * n_act, s);
+                sc.done_tlo2.reserve(sizeof(double) * n_act, s);   // scratch: unsorted keys
+                for (int a = 0; a < 3; ++a) {
+                    sc.skey[a].reserve(sizeof(double) * n_act, s);
+                    sc.sperm[a].reserve(sizeof(int32_t) * n_act, s);
+                    copy_lo_kernel<<<grid_for(n_act), 256, 0, s>>>(view.box, view.bstride, n_act, a,
+                                                                  sc.done_tlo2.as<double>(),
+                                                                  a == 0 ? sc.iota.as<int32_t>() : nullptr);
+                    LC_CHECK_LAUNCH();
+                    size_t bytes = 0;
+                    cub::DeviceSegmentedSort::SortPairs(nullptr, bytes, sc.done_tlo2.as<double>(),
+                                                        sc.skey[a].as<double>(), sc.iota.as<int32_t>(),
+                                                        sc.sperm[a].as<int32_t>(), (int)n_act, (int)L, view.off,
+                                                        view.off + 1);
+                    sc.cub_tmp.reserve(bytes, s);
+                    bytes = sc.cub_tmp.bytes;
+                    LC_CUB(cub::DeviceSegmentedSort::SortPairs(sc.cub_tmp.ptr, bytes, sc.done_tlo2.as<double>(),
+                                                               sc.skey[a].as<double>(), sc.iota.as<int32_t>(),
+                                                               sc.sperm[a].as<int32_t>(), (int)n_act, (int)L,
+                                                               view.off, view.off + 1, s));
+                }
+                sweep_kernel<<<nsm * 8, 256, 0, s>>>(view, in.pairs, P, sc.pair_axis.as<int8_t>(),
+                                                     sc.sweep_off.as<int64_t>(), sc.skey[0].as<double>(),
+                                                     sc.skey[1].as<double>(), sc.skey[2].as<double>(),
+                                                     sc.sperm[0].as<int32_t>(), sc.sperm[1].as<int32_t>(),
+                                                     sc.sperm[2].as<int32_t>(), sc.mark.as<uint32_t>(),
+                                                     sc.first_pair.as<int32_t>(), marked_ctr);
+                LC_CHECK_LAUNCH();
+            }
         }
-        // ranks of marked entries
-        sc.mark_scan.reserve(sizeof(int64_t) * (n_act + 1), s);
-        sc.counters.reserve(sizeof(int64_t) * (n_act + 1), s);
-        mark_to_i64_kernel<<<grid_for(n_act + 1), 256, 0, s>>>(sc.mark.as<uint8_t>(), n_act, sc.counters.as<int64_t>());
-        LC_CHECK_LAUNCH();
-        scan_i64(sc.counters.as<int64_t>(), sc.mark_scan.as<int64_t>(), n_act + 1, sc, s);
+        const int64_t marked = (int64_t)d2h<unsigned long long>(marked_ctr, s);
+        if (marked == 0 && out.splits == 0) {   // nothing was ever refined: every segment is a chord
+            n_act = 0;
+            break;
+        }
+        if (is_identity) {   // materialize the paired-only list and carry the marks over
+            materialize();
+            view = act_view();
+            is_identity = false;
+            sc.mark2.reserve(sizeof(uint32_t) * (n_act > 0 ? n_act : 1), s);
+            sc.fp2.reserve(sizeof(int32_t) * (n_act > 0 ? n_act : 1), s);
+            if (n_act > 0) {
+                gather_marks_kernel<<<grid_for(n_act), 256, 0, s>>>(n_act, sc.act_seg.as<int32_t>(),
+                                                                    sc.mark.as<uint32_t>(), sc.first_pair.as<int32_t>(),
+                                                                    sc.mark2.as<uint32_t>(), sc.fp2.as<int32_t>());
+                LC_CHECK_LAUNCH();
+            }
+            std::swap(sc.mark, sc.mark2);
+            std::swap(sc.first_pair, sc.fp2);
+        }
         // capacity: children <= 2 n_act, done <= n_done + n_act
         const int64_t nstride = 2 * n_act;
-        reserve_list(sc.nxt_seg, sc.nxt_loop, sc.nxt_tlo, sc.nxt_thi, sc.nxt_box, nstride);
-        sc.nxt_partner.reserve(sizeof(int32_t) * nstride, s);
-        if (n_done + n_act > sc.cap_done) {
-            // grow preserving contents
+        sc.nxt_seg.reserve(sizeof(int32_t) * (nstride > 0 ? nstride : 1), s);
+        sc.nxt_loop.reserve(sizeof(int32_t) * (nstride > 0 ? nstride : 1), s);
+        sc.nxt_tlo.reserve(sizeof(double) * (nstride > 0 ? nstride : 1), s);
+        sc.nxt_thi.reserve(sizeof(double) * (nstride > 0 ? nstride : 1), s);
+        sc.nxt_box.reserve(sizeof(double) * 6 * (nstride > 0 ? nstride : 1), s);
+        sc.nxt_partner.reserve(sizeof(int32_t) * (nstride > 0 ? nstride : 1), s);
+        sc.nxt_off.reserve(sizeof(int64_t) * (L + 1), s);
+        if (n_done + n_act > sc.cap_done) {   // grow preserving contents
             const int64_t cap = (n_done + n_act) * 2;
             DevBuf ns, nt;
             ns.reserve(sizeof(int32_t) * cap, s);
@@ -535,41 +820,47 @@ bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc,
             sc.done_tlo = nt;
             sc.cap_done = cap;
         }
+        const int64_t *mscan = nullptr;
+        if (marked > 0) {
+            sc.mark_scan.reserve(sizeof(int64_t) * (n_act + 1), s);
+            sc.counters.reserve(sizeof(int64_t) * (n_act + 1), s);
+            mark_to_i64_kernel<<<grid_for(n_act + 1), 256, 0, s>>>(sc.mark.as<uint32_t>(), n_act,
+                                                                   sc.counters.as<int64_t>());
+            LC_CHECK_LAUNCH();
+            scan_i64(sc.counters.as<int64_t>(), sc.mark_scan.as<int64_t>(), n_act + 1, sc, s);
+            mscan = sc.mark_scan.as<int64_t>();
+        }
         finish_kernel<<<grid_for(n_act), 256, 0, s>>>(
-            n_act, in.pairs, sc.mark.as<uint8_t>(), sc.mark_scan.as<int64_t>(), sc.first_pair.as<int32_t>(),
+            n_act, in.pairs, marked > 0 ? sc.mark.as<uint32_t>() : nullptr, mscan, sc.first_pair.as<int32_t>(),
             sc.act_off.as<int64_t>(), sc.act_seg.as<int32_t>(), sc.act_loop.as<int32_t>(), sc.act_tlo.as<double>(),
             sc.act_thi.as<double>(), sc.nxt_seg.as<int32_t>(), sc.nxt_loop.as<int32_t>(), sc.nxt_tlo.as<double>(),
             sc.nxt_thi.as<double>(), sc.nxt_partner.as<int32_t>(), n_done, sc.done_seg.as<int32_t>(),
             sc.done_tlo.as<double>());
         LC_CHECK_LAUNCH();
-        next_off_kernel<<<grid_for(L + 1), 256, 0, s>>>(sc.act_off.as<int64_t>(), sc.mark_scan.as<int64_t>(), L,
-                                                        sc.nxt_off.as<int64_t>());
-        LC_CHECK_LAUNCH();
-        // children boxes + error checks (:166-180); n_new unknown on host: bound by 2 n_act via mark_scan
-        LC_CUDA(cudaMemsetAsync(sc.bad_first.ptr, 0x7f, sizeof(int32_t) * L, s));
-        PassCounters init{0, INT_MAX, 0};
-        DevBuf &ctr = sc.ucnt;
-        ctr.reserve(sizeof(PassCounters), s);
-        LC_CUDA(cudaMemcpyAsync(ctr.ptr, &init, sizeof init, cudaMemcpyHostToDevice, s));
-        // total marked needed for the child grid: read it (sync 1)
-        const int64_t marked = d2h<int64_t>(sc.mark_scan.as<int64_t>() + n_act, s);
-        const int64_t n_new = 2 * marked;
-        if (n_new > 0)
-            child_boxes_kernel<<<grid_for(n_new), 256, 0, s>>>(n_new, in.coeffs, sc.nxt_seg.as<int32_t>(),
-                                                               sc.nxt_loop.as<int32_t>(), sc.nxt_tlo.as<double>(),
-                                                               sc.nxt_thi.as<double>(), sc.nxt_off.as<int64_t>(),
-                                                               nstride, min_diam, sc.nxt_box.as<double>(),
-                                                               sc.bad_first.as<int32_t>());
-        LC_CHECK_LAUNCH();
-        pass_errors_kernel<<<grid_for(L > 0 ? L : 1), 256, 0, s>>>(sc.nxt_off.as<int64_t>(), sc.bad_first.as<int32_t>(), L,
-                                                                   prm.max_subsegments, sc.mark_scan.as<int64_t>(),
-                                                                   n_act, ctr.as<PassCounters>());
-        LC_CHECK_LAUNCH();
-        const PassCounters pc = d2h<PassCounters>(ctr.ptr, s);
         n_done += n_act - marked;
+        if (marked == 0) {
+            n_act = 0;
+            break;
+        }
+        next_off_kernel<<<grid_for(L + 1), 256, 0, s>>>(sc.act_off.as<int64_t>(), mscan, L, sc.nxt_off.as<int64_t>());
+        LC_CHECK_LAUNCH();
+        // children boxes + checks (:166-180)
+        LC_CUDA(cudaMemsetAsync(sc.bad_first.ptr, 0x7f, sizeof(int32_t) * L, s));
+        LC_CUDA(cudaMemsetAsync(&ctr->err_loop, 0x7f, sizeof(int), s));
+        const int64_t n_new = 2 * marked;
+        child_boxes_kernel<<<grid_for(n_new), 256, 0, s>>>(n_new, in.coeffs, sc.nxt_seg.as<int32_t>(),
+                                                           sc.nxt_loop.as<int32_t>(), sc.nxt_tlo.as<double>(),
+                                                           sc.nxt_thi.as<double>(), sc.nxt_off.as<int64_t>(), nstride,
+                                                           min_diam, sc.nxt_box.as<double>(),
+                                                           sc.bad_first.as<int32_t>());
+        LC_CHECK_LAUNCH();
+        pass_errors_kernel<<<grid_for(L > 0 ? L : 1), 256, 0, s>>>(sc.nxt_off.as<int64_t>(), sc.bad_first.as<int32_t>(),
+                                                                   L, prm.max_subsegments, ctr);
+        LC_CHECK_LAUNCH();
+        const int err_loop = d2h<int>(&ctr->err_loop, s);
         out.splits += marked;
-        if (pc.err_loop != INT_MAX) {
-            const int l = pc.err_loop;
+        if (err_loop != kNoIndex) {
+            const int l = err_loop;
             const int32_t bf = d2h<int32_t>(sc.bad_first.as<int32_t>() + l, s);
             if (bf != kNoIndex) {
                 const int64_t o = d2h<int64_t>(sc.nxt_off.as<int64_t>() + l, s);
@@ -582,7 +873,6 @@ bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc,
             }
             return false;
         }
-        // swap lists
         std::swap(sc.act_seg, sc.nxt_seg);
         std::swap(sc.act_loop, sc.nxt_loop);
         std::swap(sc.act_tlo, sc.nxt_tlo);
@@ -591,10 +881,11 @@ bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc,
         std::swap(sc.act_off, sc.nxt_off);
         stride = nstride > 0 ? nstride : 1;
         n_act = n_new;
+        view = act_view();
     }
     if (n_act > 0) {   // for-else of :144,181-187
         std::vector<int64_t> off(L + 1);
-        LC_CUDA(cudaMemcpyAsync(off.data(), sc.act_off.ptr, sizeof(int64_t) * (L + 1), cudaMemcpyDeviceToHost, s));
+        LC_CUDA(cudaMemcpyAsync(off.data(), view.off, sizeof(int64_t) * (L + 1), cudaMemcpyDeviceToHost, s));
         LC_CUDA(cudaStreamSynchronize(s));
         err->kind = DISC_PASS_BUDGET;
         err->loops.clear();
@@ -603,17 +894,42 @@ bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc,
         return false;
     }
 
-    // (4) chords: done entries sorted by (seg, tlo) (:100-105)
+    // ---- (4) chords into the Gauss-sum layout + PolylineLoop validation
+    out.vert_off.reserve(sizeof(int64_t) * (L + 1), s);
+    out.voff.reserve(sizeof(int64_t) * (L + 1), s);
+    LC_CUDA(cudaMemsetAsync(sc.val_flags.ptr, 0, sizeof(unsigned) * (L > 0 ? L : 1), s));
+    if (out.splits == 0) {
+        out.V = M;
+        out.Vc = M + L;
+        LC_CUDA(cudaMemcpyAsync(out.vert_off.ptr, in.loff, sizeof(int64_t) * (L + 1), cudaMemcpyDeviceToDevice, s));
+        closed_offsets_kernel<<<grid_for(L + 1), 256, 0, s>>>(in.loff, L, out.voff.as<int64_t>());
+        LC_CHECK_LAUNCH();
+        out.X.reserve(sizeof(double) * (out.Vc + 1), s);
+        out.Y.reserve(sizeof(double) * (out.Vc + 1), s);
+        out.Z.reserve(sizeof(double) * (out.Vc + 1), s);
+        if (M > 0) {
+            write_all_kernel<<<grid_for(M), 256, 0, s>>>(M, in.coeffs, in.t, in.seg_loop, in.loff, in.max_exp,
+                                                         poly_thr, out.X.as<double>(), out.Y.as<double>(),
+                                                         out.Z.as<double>(), sc.val_flags.as<unsigned>());
+            LC_CHECK_LAUNCH();
+        }
+        // unpaired loops were validated in (2): check paired loops (or all, when every loop is paired)
+        const int ve = finish_validation(sc, in.loff, L, 0, identity ? nullptr : sc.paired.as<uint8_t>(), 1, s);
+        return !polyline_error(ve, err);
+    }
+    // general path: done entries sorted by (seg, tlo) (the lexsort of :104)
     const int32_t *seg_sorted = sc.done_seg.as<int32_t>();
     const int32_t *t_idx = nullptr;
-    if (out.splits > 0 && n_done > 0) {
+    if (n_done > 0) {
         sc.sort_idx.reserve(sizeof(int32_t) * n_done, s);
         sc.sort_idx2.reserve(sizeof(int32_t) * n_done, s);
         sc.done_tlo2.reserve(sizeof(double) * n_done, s);
         sc.done_seg2.reserve(sizeof(int32_t) * n_done, s);
         sc.iota.reserve(sizeof(int32_t) * n_done, s);
-        copy_lo_kernel<<<grid_for(n_done), 256, 0, s>>>(sc.done_tlo.as<double>(), 0, n_done, 0, sc.done_tlo2.as<double>(),
-                                                        sc.iota.as<int32_t>());
+        sc.skey[0].reserve(sizeof(double) * n_done, s);
+        sc.sperm[0].reserve(sizeof(int32_t) * n_done, s);
+        copy_lo_kernel<<<grid_for(n_done), 256, 0, s>>>(sc.done_tlo.as<double>(), 0, n_done, 0,
+                                                        sc.done_tlo2.as<double>(), sc.iota.as<int32_t>());
         LC_CHECK_LAUNCH();
         size_t b1 = 0, b2 = 0;
         cub::DeviceRadixSort::SortPairs(nullptr, b1, (double *)nullptr, (double *)nullptr, (int32_t *)nullptr,
@@ -622,22 +938,18 @@ bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc,
                                         (int32_t *)nullptr, (int)n_done);
         sc.cub_tmp.reserve(b1 > b2 ? b1 : b2, s);
         size_t bytes = sc.cub_tmp.bytes;
-        // by tlo (scratch key copy in done_tlo2 -> sorted into skey[0])
-        sc.skey[0].reserve(sizeof(double) * n_done, s);
         LC_CUB(cub::DeviceRadixSort::SortPairs(sc.cub_tmp.ptr, bytes, sc.done_tlo2.as<double>(), sc.skey[0].as<double>(),
-                                                sc.iota.as<int32_t>(), sc.sort_idx.as<int32_t>(), (int)n_done, 0, 64, s));
+                                               sc.iota.as<int32_t>(), sc.sort_idx.as<int32_t>(), (int)n_done, 0, 64, s));
         gather_seg_kernel<<<grid_for(n_done), 256, 0, s>>>(sc.sort_idx.as<int32_t>(), n_done, sc.done_seg.as<int32_t>(),
                                                           sc.done_seg2.as<int32_t>());
         LC_CHECK_LAUNCH();
-        sc.sperm[0].reserve(sizeof(int32_t) * n_done, s);
         bytes = sc.cub_tmp.bytes;
         LC_CUB(cub::DeviceRadixSort::SortPairs(sc.cub_tmp.ptr, bytes, sc.done_seg2.as<int32_t>(),
-                                                sc.sperm[0].as<int32_t>(), sc.sort_idx.as<int32_t>(),
-                                                sc.sort_idx2.as<int32_t>(), (int)n_done, 0, 32, s));
+                                               sc.sperm[0].as<int32_t>(), sc.sort_idx.as<int32_t>(),
+                                               sc.sort_idx2.as<int32_t>(), (int)n_done, 0, 32, s));
         seg_sorted = sc.sperm[0].as<int32_t>();
         t_idx = sc.sort_idx2.as<int32_t>();
     }
-    // per-loop output counts and offsets
     sc.done_cnt.reserve(sizeof(unsigned long long) * (L + 1), s);
     LC_CUDA(cudaMemsetAsync(sc.done_cnt.ptr, 0, sizeof(unsigned long long) * (L + 1), s));
     if (n_done > 0) {
@@ -650,31 +962,37 @@ bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc,
     out_counts_kernel<<<grid_for(L + 1), 256, 0, s>>>(sc.done_cnt.as<unsigned long long>(), sc.paired.as<uint8_t>(),
                                                       in.loff, L, ocnt, dcnt);
     LC_CHECK_LAUNCH();
-    out.vert_off.reserve(sizeof(int64_t) * (L + 1), s);
     sc.done_off.reserve(sizeof(int64_t) * (L + 1), s);
     scan_i64(ocnt, out.vert_off.as<int64_t>(), L + 1, sc, s);
     scan_i64(dcnt, sc.done_off.as<int64_t>(), L + 1, sc, s);
-    out.V = d2h<int64_t>(out.vert_off.as<int64_t>() + L, s);
-    out.verts.reserve(sizeof(double) * 3 * (out.V > 0 ? out.V : 1), s);
-    if (n_done > 0)
-        write_done_kernel<<<grid_for(n_done), 256, 0, s>>>(n_done, seg_sorted, sc.done_tlo.as<double>(), t_idx, in.seg_loop,
-                                                           in.coeffs, out.vert_off.as<int64_t>(), sc.done_off.as<int64_t>(),
-                                                           out.verts.as<double>());
-    if (n_done > 0) LC_CHECK_LAUNCH();
-    if (M > 0)
-        write_unpaired_kernel<<<grid_for(M), 256, 0, s>>>(M, in.seg_loop, sc.paired.as<uint8_t>(), in.loff, in.coeffs, in.t,
-                                                          out.vert_off.as<int64_t>(), out.verts.as<double>());
+    closed_offsets_kernel<<<grid_for(L + 1), 256, 0, s>>>(out.vert_off.as<int64_t>(), L, out.voff.as<int64_t>());
     LC_CHECK_LAUNCH();
-    // (5) paired loops become PolylineLoops (:189-191) -> validation
-    const int ve = validate(out.verts.as<double>(), out.vert_off.as<int64_t>(), L, out.V, sc.paired.as<uint8_t>(), 1,
-                            poly_thr, sc, s);
-    if (ve != INT_MAX) {
-        err->kind = DISC_INVALID_POLYLINE;
-        err->detail = ve & 3;
-        err->loops = {ve >> 2};
-        return false;
+    out.V = d2h<int64_t>(out.vert_off.as<int64_t>() + L, s);
+    out.Vc = out.V + L;
+    out.X.reserve(sizeof(double) * (out.Vc + 1), s);
+    out.Y.reserve(sizeof(double) * (out.Vc + 1), s);
+    out.Z.reserve(sizeof(double) * (out.Vc + 1), s);
+    if (n_done > 0) {
+        write_done_kernel<<<grid_for(n_done), 256, 0, s>>>(n_done, seg_sorted, sc.done_tlo.as<double>(), t_idx,
+                                                           in.seg_loop, in.coeffs, out.vert_off.as<int64_t>(),
+                                                           sc.done_off.as<int64_t>(), in.max_exp, out.X.as<double>(),
+                                                           out.Y.as<double>(), out.Z.as<double>());
+        LC_CHECK_LAUNCH();
     }
-    return true;
+    if (M > 0 && pc.n_unpaired > 0) {
+        write_unpaired_kernel<<<grid_for(M), 256, 0, s>>>(M, in.seg_loop, sc.paired.as<uint8_t>(), in.loff, in.coeffs,
+                                                          in.t, out.vert_off.as<int64_t>(), in.max_exp,
+                                                          out.X.as<double>(), out.Y.as<double>(), out.Z.as<double>(),
+                                                          nullptr);
+        LC_CHECK_LAUNCH();
+    }
+    // (5) paired loops become PolylineLoops (:189-191)
+    validate_soa_kernel<<<grid_for(out.Vc), 256, 0, s>>>(out.X.as<double>(), out.Y.as<double>(), out.Z.as<double>(),
+                                                         out.voff.as<int64_t>(), L, out.Vc, sc.paired.as<uint8_t>(), 1,
+                                                         in.max_exp, poly_thr, sc.val_flags.as<unsigned>());
+    LC_CHECK_LAUNCH();
+    const int ve = finish_validation(sc, out.voff.as<int64_t>(), L, 1, sc.paired.as<uint8_t>(), 1, s);
+    return !polyline_error(ve, err);
 }
 
 }  // namespace lc

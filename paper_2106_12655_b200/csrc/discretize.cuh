@@ -34,26 +34,30 @@ struct DiscScratch {
     DevBuf paired, act_seg, act_loop, act_tlo, act_thi, act_off, nxt_seg, nxt_loop, nxt_tlo, nxt_thi, nxt_off,
         nxt_partner, box, nxt_box, skey[3], sperm[3], iota, pair_axis, sweep_off, mark, first_pair, mark_scan,
         done_seg, done_tlo, done_seg2, done_tlo2, sort_idx, sort_idx2, done_cnt, done_off, bad_first, counters,
-        cub_tmp, loop_err, val_flags, ucnt;
-    int64_t cap_act = 0, cap_done = 0;
+        cub_tmp, loop_err, val_flags, ucnt, tmp_aos, prectr, ubox, mark2, fp2;
+    int64_t cap_done = 0;
 };
 
 struct DiscInput {
-    const double *coeffs;    // (M, 12)
-    const double *t;         // (M, 2)
-    const int64_t *loff;     // (L+1)
-    const int32_t *seg_loop; // (M)
-    const double *seg_box;   // SoA 6 x M
-    const double *loop_box;  // SoA 6 x L
+    const double *coeffs;                   // (M, 12)
+    const double *t;                        // (M, 2)
+    const int64_t *loff;                    // (L+1)
+    const int32_t *seg_loop;                // (M)
+    const double *seg_box;                  // SoA 6 x M
+    const double *loop_box;                 // SoA 6 x L
+    const unsigned long long *loop_min_diag;// (L) bit patterns of min segment-box diagonals
+    const int *max_exp;                     // exponent field of the largest |box coordinate|
     int64_t L, M;
-    const int32_t *pairs;    // (P, 2), sorted PairList
+    const int32_t *pairs;                   // (P, 2), sorted PairList
     int64_t P;
 };
 
+// Output: the chord polylines, already in the Gauss-sum layout — closed SoA
+// (vertex 0 repeated per loop) scaled by 2^-e, e = exponent of the largest
+// coordinate (exact).  vert_off = plain per-loop offsets.
 struct DiscOutput {
-    DevBuf verts;     // AoS (V, 3), start points, no closing vertex
-    DevBuf vert_off;  // (L+1)
-    int64_t V = 0;
+    DevBuf X, Y, Z, voff, vert_off;
+    int64_t V = 0, Vc = 0;
     int passes = 0;
     int64_t splits = 0;
 };
@@ -62,5 +66,8 @@ struct DiscOutput {
 // for input-dependent failures).
 bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc, DiscOutput &out,
                     DiscError *err, cudaStream_t s);
+
+// Unscaled AoS (V, 3) vertices (no closing vertices) from a DiscOutput.
+void unpack_polylines(const DiscOutput &out, int64_t L, const int *max_exp, double *aos, cudaStream_t s);
 
 }  // namespace lc

@@ -7,10 +7,31 @@
 namespace lc {
 
 namespace {
-__global__ void closed_offsets_kernel(const int64_t *__restrict__ off, int64_t L, int64_t *__restrict__ voff) {
-    const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (l <= L) voff[l] = off[l] + l;
+
+// Closed polylines from vertices: exactly LoopGeometry.from_polyline's arrays
+// (geometry.py:269-283): a0 = v_k, a1 = v_{k+1} - v_k, a2 = a3 = 0, t = [0, 1].
+__global__ void polyline_coeffs_kernel(const double *__restrict__ v, const int64_t *__restrict__ loff, int64_t L,
+                                       int64_t M, double *__restrict__ coeffs, double *__restrict__ t) {
+    const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (m >= M) return;
+    int64_t lo = 0, hi = L;
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (loff[mid] <= m) lo = mid; else hi = mid;
+    }
+    const int64_t nx = m + 1 < loff[lo + 1] ? m + 1 : loff[lo];
+    double *c = coeffs + 12 * m;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        c[d] = v[3 * m + d];
+        c[3 + d] = v[3 * nx + d] - v[3 * m + d];
+        c[6 + d] = 0.0;
+        c[9 + d] = 0.0;
+    }
+    t[2 * m] = 0.0;
+    t[2 * m + 1] = 1.0;
 }
+
 }  // namespace
 
 void Pipeline::init(cudaStream_t st) {
@@ -19,12 +40,12 @@ void Pipeline::init(cudaStream_t st) {
 }
 
 void Pipeline::release() {
-    DevBuf *bufs[] = {&d_coeffs, &d_t, &d_loff, &d_seg_box, &d_seg_loop, &d_loop_box, &d_aos, &d_in_off, &d_voff,
-                      &d_X, &d_Y, &d_Z, &d_exp, &d_pairs, &d_pg, &d_item_off, &d_item_pair, &d_scan, &d_counter,
-                      &d_partials,
-                      &d_raw, &d_lk, &d_flags, &d_quads, &d_qout, &dout.verts, &dout.vert_off};
+    DevBuf *bufs[] = {&d_coeffs, &d_t, &d_loff, &d_seg_box, &d_seg_loop, &d_loop_box, &d_min_diag, &d_model_exp,
+                      &d_verts_in, &d_aos, &d_in_off, &d_voff, &d_X, &d_Y, &d_Z, &d_exp, &d_tmp_aos, &d_pairs,
+                      &d_pg, &d_item_off, &d_item_pair, &d_scan, &d_counter, &d_partials, &d_raw, &d_lk, &d_flags,
+                      &d_quads, &d_qout, &dout.X, &dout.Y, &dout.Z, &dout.voff, &dout.vert_off};
     for (DevBuf *b : bufs) b->release(s);
-    DevBuf *pb[] = {&pls_sc.keys, &pls_sc.keys_sorted, &pls_sc.idx, &pls_sc.perm, &pls_sc.counts, &pls_sc.offs,
+    DevBuf *pb[] = {&pls_sc.keys, &pls_sc.keys_sorted, &pls_sc.idx, &pls_sc.perm, &pls_sc.sbox, &pls_sc.counter,
                     &pls_sc.cub_tmp, &pls_sc.pair_keys, &pls_sc.pair_keys_sorted, &pls_sc.axis, &pls_sc.excl};
     for (DevBuf *b : pb) b->release(s);
     DiscScratch &d = disc_sc;
@@ -33,7 +54,8 @@ void Pipeline::release() {
                     &d.skey[0], &d.skey[1], &d.skey[2], &d.sperm[0], &d.sperm[1], &d.sperm[2], &d.iota,
                     &d.pair_axis, &d.sweep_off, &d.mark, &d.first_pair, &d.mark_scan, &d.done_seg, &d.done_tlo,
                     &d.done_seg2, &d.done_tlo2, &d.sort_idx, &d.sort_idx2, &d.done_cnt, &d.done_off,
-                    &d.bad_first, &d.counters, &d.cub_tmp, &d.loop_err, &d.val_flags, &d.ucnt};
+                    &d.bad_first, &d.counters, &d.cub_tmp, &d.loop_err, &d.val_flags, &d.ucnt, &d.tmp_aos,
+                    &d.prectr};
     for (DevBuf *b : db) b->release(s);
     if (s) cudaStreamSynchronize(s);
     for (auto &e : ev)
@@ -49,6 +71,21 @@ float Pipeline::stage_ms(int e0, int e1) {
 
 // ------------------------------------------------------------------ model
 
+void Pipeline::model_boxes() {
+    d_seg_box.reserve(sizeof(double) * 6 * (M > 0 ? M : 1), s);
+    d_seg_loop.reserve(sizeof(int32_t) * (M > 0 ? M : 1), s);
+    d_loop_box.reserve(sizeof(double) * 6 * (L > 0 ? L : 1), s);
+    d_min_diag.reserve(sizeof(unsigned long long) * (L > 0 ? L : 1), s);
+    d_model_exp.reserve(sizeof(int), s);
+    // tight segment boxes, per-loop min diagonals, coordinate exponent, loop boxes
+    launch_seg_boxes(d_coeffs.as<double>(), d_t.as<double>(), d_loff.as<int64_t>(), L, M, d_seg_box.as<double>(),
+                     d_seg_loop.as<int32_t>(), d_min_diag.as<unsigned long long>(), d_model_exp.as<int>(), s);
+    launch_loop_boxes(d_seg_box.as<double>(), M, d_loff.as<int64_t>(), L, d_loop_box.as<double>(), s);
+    model_ready = true;
+    polylines_ready = false;
+    P = 0;
+}
+
 void Pipeline::upload_model(const double *coeffs, const double *t, const int64_t *loff, int64_t nloops) {
     L = nloops;
     M = L > 0 ? loff[L] : 0;
@@ -58,30 +95,45 @@ void Pipeline::upload_model(const double *coeffs, const double *t, const int64_t
     d_coeffs.reserve(sizeof(double) * 12 * (M > 0 ? M : 1), s);
     d_t.reserve(sizeof(double) * 2 * (M > 0 ? M : 1), s);
     d_loff.reserve(sizeof(int64_t) * (L + 1), s);
-    d_seg_box.reserve(sizeof(double) * 6 * (M > 0 ? M : 1), s);
-    d_seg_loop.reserve(sizeof(int32_t) * (M > 0 ? M : 1), s);
-    d_loop_box.reserve(sizeof(double) * 6 * (L > 0 ? L : 1), s);
-    d_exp.reserve(sizeof(int) * 2, s);
     if (M > 0) {
         LC_CUDA(cudaMemcpyAsync(d_coeffs.ptr, coeffs, sizeof(double) * 12 * M, cudaMemcpyHostToDevice, s));
         LC_CUDA(cudaMemcpyAsync(d_t.ptr, t, sizeof(double) * 2 * M, cudaMemcpyHostToDevice, s));
     }
     LC_CUDA(cudaMemcpyAsync(d_loff.ptr, loff, sizeof(int64_t) * (L + 1), cudaMemcpyHostToDevice, s));
-    // tight segment boxes + loop boxes (shared by PLS and discretization pass 1)
-    launch_seg_boxes(d_coeffs.as<double>(), d_t.as<double>(), d_loff.as<int64_t>(), L, M, -1.0,
-                     d_seg_box.as<double>(), d_seg_loop.as<int32_t>(), d_exp.as<int>() + 1, s);
-    launch_loop_boxes(d_seg_box.as<double>(), M, d_loff.as<int64_t>(), L, d_loop_box.as<double>(), s);
-    model_ready = true;
-    polylines_ready = false;
-    P = 0;
-    // the caller's host buffers may be released after return
+    model_boxes();
+    LC_CUDA(cudaStreamSynchronize(s));   // the caller's host buffers may be released after return
+}
+
+void Pipeline::upload_model_polylines(const double *verts, const int64_t *loff, int64_t nloops) {
+    L = nloops;
+    M = L > 0 ? loff[L] : 0;
+    if (L > 0 && loff[0] != 0) throw Error(LC_ERR_ARG, "loop offsets must start at 0");
+    for (int64_t l = 0; l < L; ++l)
+        if (loff[l + 1] - loff[l] < 1) throw Error(LC_ERR_ARG, "every loop needs at least one vertex");
+    d_coeffs.reserve(sizeof(double) * 12 * (M > 0 ? M : 1), s);
+    d_t.reserve(sizeof(double) * 2 * (M > 0 ? M : 1), s);
+    d_loff.reserve(sizeof(int64_t) * (L + 1), s);
+    d_verts_in.reserve(sizeof(double) * 3 * (M > 0 ? M : 1), s);
+    if (M > 0) LC_CUDA(cudaMemcpyAsync(d_verts_in.ptr, verts, sizeof(double) * 3 * M, cudaMemcpyHostToDevice, s));
+    LC_CUDA(cudaMemcpyAsync(d_loff.ptr, loff, sizeof(int64_t) * (L + 1), cudaMemcpyHostToDevice, s));
+    if (M > 0) {
+        polyline_coeffs_kernel<<<(unsigned)ceil_div(M, 256), 256, 0, s>>>(d_verts_in.as<double>(), d_loff.as<int64_t>(),
+                                                                           L, M, d_coeffs.as<double>(), d_t.as<double>());
+        LC_CHECK_LAUNCH();
+    }
+    model_boxes();
     LC_CUDA(cudaStreamSynchronize(s));
 }
 
 int64_t Pipeline::potential_link_search(const uint64_t *excl_keys, int64_t n_excl) {
     if (!model_ready) throw Error(LC_ERR_STATE, "no model uploaded");
     LC_CUDA(cudaEventRecord(ev[EV_BEGIN], s));
-    P = run_pls(d_loop_box.as<double>(), L, excl_keys, n_excl, pls_sc, d_pairs, s);
+    // LINKCERT_PLS_SWEEP=1 selects the sort-and-sweep PLS instead of grid culling — tests cover both
+    static const bool force_sweep = [] {
+        const char *e = getenv("LINKCERT_PLS_SWEEP");
+        return e && e[0] == '1';
+    }();
+    P = run_pls(d_loop_box.as<double>(), L, excl_keys, n_excl, pls_sc, d_pairs, s, force_sweep);
     LC_CUDA(cudaEventRecord(ev[EV_PLS], s));
     return P;
 }
@@ -89,26 +141,20 @@ int64_t Pipeline::potential_link_search(const uint64_t *excl_keys, int64_t n_exc
 bool Pipeline::discretize(const DiscParams &prm) {
     if (!model_ready) throw Error(LC_ERR_STATE, "no model uploaded");
     DiscInput in{d_coeffs.as<double>(), d_t.as<double>(), d_loff.as<int64_t>(), d_seg_loop.as<int32_t>(),
-                 d_seg_box.as<double>(), d_loop_box.as<double>(), L, M, d_pairs.as<int32_t>(), P};
+                 d_seg_box.as<double>(), d_loop_box.as<double>(), d_min_diag.as<unsigned long long>(),
+                 d_model_exp.as<int>(), L, M, d_pairs.as<int32_t>(), P};
     derr = DiscError();
     polylines_ready = false;
     if (!run_discretize(in, prm, disc_sc, dout, &derr, s)) return false;
-    // Gauss input: closed SoA, scaled by an exact power of two
     V = dout.V;
-    Vc = V + L;
-    d_voff.reserve(sizeof(int64_t) * (L + 1), s);
-    d_X.reserve(sizeof(double) * (Vc + 1), s);
-    d_Y.reserve(sizeof(double) * (Vc + 1), s);
-    d_Z.reserve(sizeof(double) * (Vc + 1), s);
-    closed_offsets_kernel<<<(unsigned)ceil_div(L + 1, 256), 256, 0, s>>>(dout.vert_off.as<int64_t>(), L,
-                                                                          d_voff.as<int64_t>());
-    LC_CHECK_LAUNCH();
-    LC_CUDA(cudaMemsetAsync(d_exp.ptr, 0, sizeof(int), s));
-    launch_max_exponent(dout.verts.as<double>(), 3 * V, d_exp.as<int>(), s);
-    launch_pack_closed_soa(dout.verts.as<double>(), dout.vert_off.as<int64_t>(), d_voff.as<int64_t>(), L, Vc,
-                           d_exp.as<int>(), d_X.as<double>(), d_Y.as<double>(), d_Z.as<double>(), s);
-    LC_CUDA(cudaEventRecord(ev[EV_DISC], s));
+    Vc = dout.Vc;
+    gX = dout.X.as<double>();
+    gY = dout.Y.as<double>();
+    gZ = dout.Z.as<double>();
+    gvoff = dout.voff.as<int64_t>();
     polylines_ready = true;
+    polylines_from_model = true;
+    LC_CUDA(cudaEventRecord(ev[EV_DISC], s));
     return true;
 }
 
@@ -126,9 +172,12 @@ void Pipeline::download_loop_boxes(double *lo, double *hi) {
 }
 
 void Pipeline::download_polylines(double *verts, int64_t *vert_off) {
-    if (!polylines_ready) throw Error(LC_ERR_STATE, "no discretized polylines");
-    if (V > 0 && verts)
-        LC_CUDA(cudaMemcpyAsync(verts, dout.verts.ptr, sizeof(double) * 3 * V, cudaMemcpyDeviceToHost, s));
+    if (!polylines_ready || !polylines_from_model) throw Error(LC_ERR_STATE, "no discretized polylines");
+    if (V > 0 && verts) {
+        d_tmp_aos.reserve(sizeof(double) * 3 * V, s);
+        unpack_polylines(dout, L, d_model_exp.as<int>(), d_tmp_aos.as<double>(), s);
+        LC_CUDA(cudaMemcpyAsync(verts, d_tmp_aos.ptr, sizeof(double) * 3 * V, cudaMemcpyDeviceToHost, s));
+    }
     if (vert_off)
         LC_CUDA(cudaMemcpyAsync(vert_off, dout.vert_off.ptr, sizeof(int64_t) * (L + 1), cudaMemcpyDeviceToHost, s));
     LC_CUDA(cudaStreamSynchronize(s));
@@ -165,7 +214,12 @@ void Pipeline::upload_polylines(const double *verts, const int64_t *vert_off, in
     launch_max_exponent(d_aos.as<double>(), 3 * V, d_exp.as<int>(), s);
     launch_pack_closed_soa(d_aos.as<double>(), d_in_off.as<int64_t>(), d_voff.as<int64_t>(), L, Vc,
                            d_exp.as<int>(), d_X.as<double>(), d_Y.as<double>(), d_Z.as<double>(), s);
+    gX = d_X.as<double>();
+    gY = d_Y.as<double>();
+    gZ = d_Z.as<double>();
+    gvoff = d_voff.as<int64_t>();
     polylines_ready = true;
+    polylines_from_model = false;
     LC_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -192,8 +246,8 @@ void Pipeline::build_gauss_items() {
     const size_t scan_bytes = build_items_scan_bytes(P > 0 ? P : 1);
     d_scan.reserve(scan_bytes, s);
     d_counter.reserve(sizeof(unsigned long long), s);
-    n_items = build_items(d_pairs.as<int32_t>(), P, d_voff.as<int64_t>(), d_pg.as<PairGeom>(),
-                          d_item_off.as<int64_t>(), d_scan.ptr, d_scan.bytes, s);
+    n_items = build_items(d_pairs.as<int32_t>(), P, gvoff, d_pg.as<PairGeom>(), d_item_off.as<int64_t>(), d_scan.ptr,
+                          d_scan.bytes, s);
     d_partials.reserve(sizeof(double) * (size_t)(n_items > 0 ? n_items : 1), s);
     d_item_pair.reserve(sizeof(int32_t) * (size_t)(n_items > 0 ? n_items : 1), s);
     launch_item_pairs(d_item_off.as<int64_t>(), P, n_items, d_item_pair.as<int32_t>(), s);
@@ -204,12 +258,11 @@ void Pipeline::build_gauss_items() {
 
 void Pipeline::run_gauss(int mode, int64_t item_begin, int64_t item_end, double *partials_ext,
                          cudaEvent_t ev0, cudaEvent_t ev1) {
-    if (mode < GAUSS_PHASE || mode > 5) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
+    if (mode < GAUSS_PHASE || mode > GAUSS_PHASE_OCC4) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
     double *out = partials_ext ? partials_ext : d_partials.as<double>();
     LC_CUDA(cudaEventRecord(ev0 ? ev0 : ev[EV_GAUSS0], s));
-    launch_gauss_items(mode, d_X.as<double>(), d_Y.as<double>(), d_Z.as<double>(), d_pg.as<PairGeom>(),
-                       d_item_off.as<int64_t>(), d_item_pair.as<int32_t>(), P, item_begin, item_end,
-                       d_counter.as<unsigned long long>(), out, s);
+    launch_gauss_items(mode, gX, gY, gZ, d_pg.as<PairGeom>(), d_item_off.as<int64_t>(), d_item_pair.as<int32_t>(), P,
+                       item_begin, item_end, d_counter.as<unsigned long long>(), out, s);
     LC_CUDA(cudaEventRecord(ev1 ? ev1 : ev[EV_GAUSS1], s));
 }
 

@@ -15,7 +15,7 @@ struct Pipeline {
     cudaEvent_t ev[EV_COUNT] = {};
 
     // Model: packed monomial cubics (linkcert LoopGeometry arrays, geometry.py:206-296).
-    DevBuf d_coeffs, d_t, d_loff, d_seg_box, d_seg_loop, d_loop_box;
+    DevBuf d_coeffs, d_t, d_loff, d_seg_box, d_seg_loop, d_loop_box, d_min_diag, d_model_exp, d_verts_in;
     int64_t L = 0, M = 0;
     bool model_ready = false;
 
@@ -23,10 +23,15 @@ struct Pipeline {
     DiscScratch disc_sc;
     DiscOutput dout;
     DiscError derr;
-    bool polylines_ready = false;
 
-    // Gauss input: closed SoA polylines, scaled by 2^-e (exact).
-    DevBuf d_aos, d_in_off, d_voff, d_X, d_Y, d_Z, d_exp;
+    // Gauss input (closed SoA, scaled by 2^-e): from discretize() or upload_polylines().
+    const double *gX = nullptr, *gY = nullptr, *gZ = nullptr;
+    const int64_t *gvoff = nullptr;
+    bool polylines_ready = false;
+    bool polylines_from_model = false;
+
+    // upload_polylines() buffers
+    DevBuf d_aos, d_in_off, d_voff, d_X, d_Y, d_Z, d_exp, d_tmp_aos;
     int64_t V = 0, Vc = 0;
     std::vector<int64_t> h_voff;
 
@@ -44,8 +49,10 @@ struct Pipeline {
 
     // model + stages
     void upload_model(const double *coeffs, const double *t, const int64_t *loff, int64_t nloops);
+    // closed polylines given as vertices only (a0 = v_k, a1 = v_k+1 - v_k, a2 = a3 = 0, t = [0, 1])
+    void upload_model_polylines(const double *verts, const int64_t *loff, int64_t nloops);
     int64_t potential_link_search(const uint64_t *excl_keys, int64_t n_excl);   // -> d_pairs, P
-    bool discretize(const DiscParams &prm);                                      // -> dout + gauss input
+    bool discretize(const DiscParams &prm);                                      // -> dout = gauss input
     void download_loop_boxes(double *lo, double *hi);
     void download_polylines(double *verts, int64_t *vert_off);
 
@@ -61,6 +68,9 @@ struct Pipeline {
     void segment_pair_lambda(const double *quads, int64_t n, double *out);
 
     float stage_ms(int e0, int e1);
+
+  private:
+    void model_boxes();
 };
 
 }  // namespace lc

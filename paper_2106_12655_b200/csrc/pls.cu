@@ -1,12 +1,13 @@
 // Device potential-link search: tight segment boxes -> loop AABBs ->
-// sort-and-sweep -> sorted unique (i<j) loop pairs.
+// warp-cooperative sort-and-sweep -> sorted unique (i<j) loop pairs.
 //
 // Reference: linkcert/pls.py:48-73 (loop_boxes, potential_link_search),
 // bvh.py:93-98 (closed-interval overlap), bvh.py:227-243 (the broad phase it
 // replaces; only the resulting SET matters, the caller sorts).  The pair set
-// is exact: the sweep visits every pair whose sweep-axis intervals overlap
-// (for two overlapping closed intervals, one lower end lies inside the
-// other interval) and then applies the full 3-axis closed test.
+// is exact: for two overlapping closed intervals one lower end lies inside
+// the other interval, so sweeping every loop over the loops that follow it
+// in lower-bound order while lo_b <= hi_a visits every overlapping pair; the
+// full 3-axis closed test then decides.
 #include <climits>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -18,25 +19,39 @@
 namespace lc {
 namespace {
 
+__device__ __forceinline__ int exp_field(double x) { return (__double2hiint(x) >> 20) & 0x7ff; }
+
 __global__ void seg_boxes_kernel(const double *__restrict__ coeffs, const double *__restrict__ t,
-                                 const int64_t *__restrict__ loff, int64_t L, int64_t M, double min_diam,
-                                 double *__restrict__ box, int32_t *__restrict__ seg_loop, int *zero_loop) {
+                                 const int64_t *__restrict__ loff, int64_t L, int64_t M, double *__restrict__ box,
+                                 int32_t *__restrict__ seg_loop, unsigned long long *__restrict__ loop_min_diag,
+                                 int *__restrict__ max_exp) {
     const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (m >= M) return;
-    int64_t lo = 0, hi = L;   // loop: largest l with loff[l] <= m
-    while (hi - lo > 1) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (loff[mid] <= m) lo = mid; else hi = mid;
-    }
-    seg_loop[m] = (int32_t)lo;
-    double bl[3], bh[3];
-    tight_box(coeffs + 12 * m, t[2 * m], t[2 * m + 1], bl, bh);
+    int e = 0;
+    if (m < M) {
+        int64_t lo = 0, hi = L;   // loop: largest l with loff[l] <= m
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (loff[mid] <= m) lo = mid; else hi = mid;
+        }
+        seg_loop[m] = (int32_t)lo;
+        double bl[3], bh[3];
+        tight_box(coeffs + 12 * m, t[2 * m], t[2 * m + 1], bl, bh);
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
-        box[d * M + m] = bl[d];
-        box[(3 + d) * M + m] = bh[d];
+        for (int d = 0; d < 3; ++d) {
+            box[d * M + m] = bl[d];
+            box[(3 + d) * M + m] = bh[d];
+            const int a = exp_field(bl[d]), b = exp_field(bh[d]);
+            e = max(e, max(a, b));
+        }
+        // per-loop minimum box diagonal (ZeroLengthInput, discretize.py:124-129);
+        // non-negative doubles order like their bit patterns
+        if (loop_min_diag) atomicMin(loop_min_diag + lo, (unsigned long long)__double_as_longlong(diag_norm(bl, bh)));
     }
-    if (diag_norm(bl, bh) < min_diam) atomicMin(zero_loop, (int)lo);
+    if (max_exp) {
+#pragma unroll
+        for (int off = 16; off; off >>= 1) e = max(e, __shfl_xor_sync(0xffffffffu, e, off));
+        if ((threadIdx.x & 31) == 0 && e > 0) atomicMax(max_exp, e);
+    }
 }
 
 __global__ void loop_boxes_kernel(const double *__restrict__ box, int64_t M, const int64_t *__restrict__ loff,
@@ -75,6 +90,7 @@ __global__ void loop_boxes_kernel(const double *__restrict__ box, int64_t M, con
 __global__ void sweep_axis_kernel(const double *__restrict__ lbox, int64_t L, int *axis, double *keys,
                                   int32_t *idx) {
     __shared__ double red[6][32];
+    __shared__ int s_axis;
     double v[6] = {CUDART_INF, CUDART_INF, CUDART_INF, -CUDART_INF, -CUDART_INF, -CUDART_INF};
     for (int64_t l = threadIdx.x; l < L; l += blockDim.x) {
 #pragma unroll
@@ -95,7 +111,6 @@ __global__ void sweep_axis_kernel(const double *__restrict__ lbox, int64_t L, in
     if ((threadIdx.x & 31) == 0)
         for (int d = 0; d < 6; ++d) red[d][w] = v[d];
     __syncthreads();
-    __shared__ int s_axis;
     if (threadIdx.x == 0) {
         for (int k = 1; k < nw; ++k)
             for (int d = 0; d < 3; ++d) {
@@ -106,7 +121,10 @@ __global__ void sweep_axis_kernel(const double *__restrict__ lbox, int64_t L, in
         double best = red[3][0] - red[0][0];
         for (int d = 1; d < 3; ++d) {
             const double e = red[3 + d][0] - red[d][0];
-            if (e > best) { best = e; a = d; }
+            if (e > best) {
+                best = e;
+                a = d;
+            }
         }
         s_axis = a;
         *axis = a;
@@ -119,13 +137,14 @@ __global__ void sweep_axis_kernel(const double *__restrict__ lbox, int64_t L, in
     }
 }
 
-__device__ __forceinline__ bool boxes_overlap(const double *__restrict__ b, int64_t n, int64_t i, int64_t j) {
+// Boxes in sweep order (coalesced candidate loads in the sweep).
+__global__ void gather_boxes_kernel(const double *__restrict__ lbox, const int32_t *__restrict__ perm, int64_t L,
+                                    double *__restrict__ sbox) {
+    const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (a >= L) return;
+    const int64_t l = perm[a];
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
-        // alo > bhi or blo > ahi -> disjoint (bvh.py:93-98)
-        if (b[d * n + i] > b[(3 + d) * n + j] || b[d * n + j] > b[(3 + d) * n + i]) return false;
-    }
-    return true;
+    for (int d = 0; d < 6; ++d) sbox[d * L + a] = lbox[d * L + l];
 }
 
 __device__ __forceinline__ bool is_excluded(const uint64_t *__restrict__ ex, int64_t n, uint64_t key) {
@@ -139,30 +158,354 @@ __device__ __forceinline__ bool is_excluded(const uint64_t *__restrict__ ex, int
     return false;
 }
 
-template <bool WRITE>
-__global__ void sweep_kernel(const double *__restrict__ lbox, int64_t L, const int *__restrict__ axis,
-                             const double *__restrict__ skeys, const int32_t *__restrict__ perm,
-                             const uint64_t *__restrict__ excl, int64_t n_excl, int64_t *__restrict__ counts,
-                             const int64_t *__restrict__ offs, uint64_t *__restrict__ out) {
-    const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (a >= L) return;
+// Warp per sorted loop a: lanes test the following loops 32 at a time while
+// lo_axis(b) <= hi_axis(a); hits are appended (ballot + one atomic per warp).
+__global__ void sweep_warp_kernel(const double *__restrict__ sbox, const int32_t *__restrict__ perm, int64_t L,
+                                  const int *__restrict__ axis, const uint64_t *__restrict__ excl, int64_t n_excl,
+                                  unsigned long long *__restrict__ counter, uint64_t *__restrict__ out, int64_t cap) {
+    const int lane = threadIdx.x & 31;
     const int ax = *axis;
-    const int64_t ia = perm[a];
-    const double hia = lbox[(3 + ax) * L + ia];
-    int64_t c = 0;
-    int64_t w = WRITE ? offs[a] : 0;
-    for (int64_t b = a + 1; b < L && skeys[b] <= hia; ++b) {
-        const int64_t ib = perm[b];
-        if (!boxes_overlap(lbox, L, ia, ib)) continue;
-        const uint64_t i = ia < ib ? ia : ib, j = ia < ib ? ib : ia;
-        const uint64_t key = (i << 32) | j;
-        if (n_excl && is_excluded(excl, n_excl, key)) continue;
-        if (WRITE) out[w++] = key;
-        else ++c;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; a < L; a += nwarps) {
+        double al[3], ah[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            al[d] = sbox[d * L + a];
+            ah[d] = sbox[(3 + d) * L + a];
+        }
+        const double hia = ah[ax];
+        const uint64_t ia = (uint64_t)perm[a];
+        for (int64_t b0 = a + 1; b0 < L; b0 += 32) {
+            const int64_t b = b0 + lane;
+            const bool valid = b < L;
+            const double key = valid ? sbox[ax * L + b] : CUDART_INF;
+            const bool in = valid && key <= hia;
+            bool hit = in;
+            if (in) {
+#pragma unroll
+                for (int d = 0; d < 3; ++d)
+                    if (al[d] > sbox[(3 + d) * L + b] || sbox[d * L + b] > ah[d]) hit = false;
+            }
+            uint64_t k64 = 0;
+            if (hit) {
+                const uint64_t ib = (uint64_t)perm[b];
+                k64 = ia < ib ? (ia << 32) | ib : (ib << 32) | ia;
+                if (n_excl && is_excluded(excl, n_excl, k64)) hit = false;
+            }
+            const unsigned ballot = __ballot_sync(0xffffffffu, hit);
+            if (ballot) {
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd(counter, (unsigned long long)__popc(ballot));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                const int64_t pos = (int64_t)base + __popc(ballot & ((1u << lane) - 1u));
+                if (hit && pos < cap) out[pos] = k64;
+            }
+            // keys are sorted: once lane 31's key exceeds hi_a, no later block can start inside
+            if (!__shfl_sync(0xffffffffu, in, 31)) break;
+        }
     }
-    if (!WRITE) counts[a] = c;
 }
 
+// ------------------------------------------------------- uniform-grid PLS
+// Exact and sort-free.  Cell size c >= the largest loop-box extent, so a loop b
+// overlapping loop a satisfies lo_a - c <= lo_b <= hi_a on every axis: every
+// loop is stored once, in the cell of its lower corner, and a query scans the
+// cells [cell(lo_a) - 2, cell(hi_a)] per axis (floor((x - o) / c) is monotone
+// in x; the extra cell absorbs the rounding of lo_a - c).  A pair is emitted
+// only from its smaller index, into per-row slots sorted at compaction, so the
+// output is the PairList order without a global sort.
+
+constexpr int kRowSlots = 16;
+
+struct GridParams {
+    double o[3];
+    double c;
+    int dims[3];
+    int pad;
+};
+
+// One block: origin, cell size and dims with dims product <= max_cells.
+__global__ void grid_params_kernel(const double *__restrict__ lbox, int64_t L, int64_t max_cells,
+                                   GridParams *__restrict__ gp) {
+    __shared__ double red[7][32];
+    double v[7] = {CUDART_INF, CUDART_INF, CUDART_INF, -CUDART_INF, -CUDART_INF, -CUDART_INF, 0.0};
+    for (int64_t l = threadIdx.x; l < L; l += blockDim.x) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const double lo = lbox[d * L + l], hi = lbox[(3 + d) * L + l];
+            v[d] = fmin(v[d], lo);
+            v[3 + d] = fmax(v[3 + d], hi);
+            v[6] = fmax(v[6], hi - lo);
+        }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            v[d] = fmin(v[d], __shfl_xor_sync(0xffffffffu, v[d], off));
+            v[3 + d] = fmax(v[3 + d], __shfl_xor_sync(0xffffffffu, v[3 + d], off));
+        }
+        v[6] = fmax(v[6], __shfl_xor_sync(0xffffffffu, v[6], off));
+    }
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if ((threadIdx.x & 31) == 0)
+        for (int d = 0; d < 7; ++d) red[d][w] = v[d];
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    for (int k = 1; k < nw; ++k) {
+        for (int d = 0; d < 3; ++d) {
+            red[d][0] = fmin(red[d][0], red[d][k]);
+            red[3 + d][0] = fmax(red[3 + d][0], red[3 + d][k]);
+        }
+        red[6][0] = fmax(red[6][0], red[6][k]);
+    }
+    double span[3], c = red[6][0];
+    for (int d = 0; d < 3; ++d) {
+        gp->o[d] = red[d][0];
+        span[d] = red[3 + d][0] - red[d][0];
+    }
+    const double smax = fmax(span[0], fmax(span[1], span[2]));
+    if (!(c > 0.0)) c = smax > 0.0 ? smax * 1e-6 : 1.0;
+    for (;;) {
+        double prod = 1.0;
+        for (int d = 0; d < 3; ++d) prod *= floor(span[d] / c) + 1.0;
+        if (prod <= (double)max_cells) break;
+        c *= 1.25;
+    }
+    gp->c = c;
+    for (int d = 0; d < 3; ++d) gp->dims[d] = (int)(floor(span[d] / c) + 1.0);
+}
+
+__device__ __forceinline__ int cell_coord(double x, double o, double c, int dim) {
+    const double f = floor((x - o) / c);
+    return f < 0.0 ? 0 : (f >= (double)dim ? dim - 1 : (int)f);
+}
+
+__device__ __forceinline__ int64_t owner_cell(const double *__restrict__ lbox, int64_t L, int64_t l,
+                                              const GridParams &g) {
+    const int cx = cell_coord(lbox[l], g.o[0], g.c, g.dims[0]);
+    const int cy = cell_coord(lbox[L + l], g.o[1], g.c, g.dims[1]);
+    const int cz = cell_coord(lbox[2 * L + l], g.o[2], g.c, g.dims[2]);
+    return ((int64_t)cz * g.dims[1] + cy) * g.dims[0] + cx;
+}
+
+__global__ void cell_count_kernel(const double *__restrict__ lbox, int64_t L, const GridParams *__restrict__ gp,
+                                  int64_t *__restrict__ count) {
+    const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (l >= L) return;
+    const GridParams g = *gp;
+    atomicAdd((unsigned long long *)(count + owner_cell(lbox, L, l, g)), 1ULL);
+}
+
+__global__ void cell_scatter_kernel(const double *__restrict__ lbox, int64_t L, const GridParams *__restrict__ gp,
+                                    int64_t *__restrict__ cursor, int32_t *__restrict__ cell_loops) {
+    const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (l >= L) return;
+    const GridParams g = *gp;
+    const int64_t pos = (int64_t)atomicAdd((unsigned long long *)(cursor + owner_cell(lbox, L, l, g)), 1ULL);
+    cell_loops[pos] = (int32_t)l;
+}
+
+// Thread per loop a: every b > a with an overlapping closed box (bvh.py:93-98),
+// minus excluded keys.  SLOTS: count all, store up to kRowSlots per row;
+// !SLOTS: write keys at offs[a] (two-pass fallback, sorted afterwards).
+template <bool SLOTS>
+__global__ void grid_query_kernel(const double *__restrict__ lbox, int64_t L, const GridParams *__restrict__ gp,
+                                  const int64_t *__restrict__ cell_off, const int32_t *__restrict__ cell_loops,
+                                  const uint64_t *__restrict__ excl, int64_t n_excl, int *__restrict__ row_count,
+                                  int32_t *__restrict__ slots, const int64_t *__restrict__ offs,
+                                  uint64_t *__restrict__ keys) {
+    const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (a >= L) return;
+    const GridParams g = *gp;
+    double al[3], ah[3];
+    int c0[3], c1[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        al[d] = lbox[d * L + a];
+        ah[d] = lbox[(3 + d) * L + a];
+        c0[d] = max(cell_coord(al[d], g.o[d], g.c, g.dims[d]) - 2, 0);
+        c1[d] = cell_coord(ah[d], g.o[d], g.c, g.dims[d]);
+    }
+    int n = 0;
+    int64_t w = SLOTS ? 0 : offs[a];
+    for (int cz = c0[2]; cz <= c1[2]; ++cz)
+        for (int cy = c0[1]; cy <= c1[1]; ++cy) {
+            const int64_t row = ((int64_t)cz * g.dims[1] + cy) * g.dims[0];
+            const int64_t kb = cell_off[row + c0[0]], ke = cell_off[row + c1[0] + 1];
+            for (int64_t k = kb; k < ke; ++k) {
+                const int64_t b = cell_loops[k];
+                if (b <= a) continue;
+                bool ov = true;
+#pragma unroll
+                for (int d = 0; d < 3; ++d)
+                    if (al[d] > lbox[(3 + d) * L + b] || lbox[d * L + b] > ah[d]) ov = false;
+                if (!ov) continue;
+                const uint64_t key = ((uint64_t)a << 32) | (uint64_t)b;
+                if (n_excl && is_excluded(excl, n_excl, key)) continue;
+                if (SLOTS) {
+                    if (n < kRowSlots) slots[a * kRowSlots + n] = (int32_t)b;
+                } else {
+                    keys[w++] = key;
+                }
+                ++n;
+            }
+        }
+    if (SLOTS) row_count[a] = n;
+}
+
+// Warp per loop a (enough warps to hide the gather latency at L ~ 1e4):
+// lanes share a's candidate cells; hits are ranked with a ballot.
+template <bool SLOTS>
+__global__ void grid_query_warp_kernel(const double *__restrict__ lbox, int64_t L, const GridParams *__restrict__ gp,
+                                       const int64_t *__restrict__ cell_off, const int32_t *__restrict__ cell_loops,
+                                       const uint64_t *__restrict__ excl, int64_t n_excl, int *__restrict__ row_count,
+                                       int32_t *__restrict__ slots, const int64_t *__restrict__ offs,
+                                       uint64_t *__restrict__ keys) {
+    const int lane = threadIdx.x & 31;
+    const int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (a >= L) return;
+    const GridParams g = *gp;
+    double al[3], ah[3];
+    int c0[3], c1[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        al[d] = lbox[d * L + a];
+        ah[d] = lbox[(3 + d) * L + a];
+        c0[d] = max(cell_coord(al[d], g.o[d], g.c, g.dims[d]) - 2, 0);
+        c1[d] = cell_coord(ah[d], g.o[d], g.c, g.dims[d]);
+    }
+    int n = 0;
+    const int64_t w0 = SLOTS ? 0 : offs[a];
+    for (int cz = c0[2]; cz <= c1[2]; ++cz)
+        for (int cy = c0[1]; cy <= c1[1]; ++cy) {
+            const int64_t row = ((int64_t)cz * g.dims[1] + cy) * g.dims[0];
+            const int64_t kb = cell_off[row + c0[0]], ke = cell_off[row + c1[0] + 1];
+            for (int64_t k0 = kb; k0 < ke; k0 += 32) {
+                const int64_t k = k0 + lane;
+                bool hit = false;
+                int64_t b = 0;
+                if (k < ke) {
+                    b = cell_loops[k];
+                    if (b > a) {
+                        hit = true;
+#pragma unroll
+                        for (int d = 0; d < 3; ++d)
+                            if (al[d] > lbox[(3 + d) * L + b] || lbox[d * L + b] > ah[d]) hit = false;
+                        if (hit && n_excl && is_excluded(excl, n_excl, ((uint64_t)a << 32) | (uint64_t)b)) hit = false;
+                    }
+                }
+                const unsigned bal = __ballot_sync(0xffffffffu, hit);
+                if (hit) {
+                    const int r = n + __popc(bal & ((1u << lane) - 1u));
+                    if (SLOTS) {
+                        if (r < kRowSlots) slots[a * kRowSlots + r] = (int32_t)b;
+                    } else {
+                        keys[w0 + r] = ((uint64_t)a << 32) | (uint64_t)b;
+                    }
+                }
+                n += __popc(bal);
+            }
+        }
+    if (SLOTS && lane == 0) row_count[a] = n;
+}
+
+// Ordered-integer images of doubles (monotone): min/max through integer atomics.
+__device__ __forceinline__ unsigned long long ord_key(double x) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+__device__ __forceinline__ double ord_val(unsigned long long k) {
+    return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffULL) : ~k));
+}
+
+// Stage 1 (many blocks): acc[0..2] = min lo, acc[3..5] = max hi, acc[6] = max extent (ordered keys).
+__global__ void grid_reduce_kernel(const double *__restrict__ lbox, int64_t L, unsigned long long *__restrict__ acc) {
+    double v[7] = {CUDART_INF, CUDART_INF, CUDART_INF, -CUDART_INF, -CUDART_INF, -CUDART_INF, 0.0};
+    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < L; l += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const double lo = lbox[d * L + l], hi = lbox[(3 + d) * L + l];
+            v[d] = fmin(v[d], lo);
+            v[3 + d] = fmax(v[3 + d], hi);
+            v[6] = fmax(v[6], hi - lo);
+        }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            v[d] = fmin(v[d], __shfl_xor_sync(0xffffffffu, v[d], off));
+            v[3 + d] = fmax(v[3 + d], __shfl_xor_sync(0xffffffffu, v[3 + d], off));
+        }
+        v[6] = fmax(v[6], __shfl_xor_sync(0xffffffffu, v[6], off));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        for (int d = 0; d < 3; ++d) {
+            atomicMin(acc + d, ord_key(v[d]));
+            atomicMax(acc + 3 + d, ord_key(v[3 + d]));
+        }
+        atomicMax(acc + 6, ord_key(v[6]));
+    }
+}
+
+// Stage 2 (one thread): origin, cell size >= max extent, dims with product <= max_cells.
+__global__ void grid_finalize_kernel(const unsigned long long *__restrict__ acc, int64_t max_cells,
+                                     GridParams *__restrict__ gp) {
+    double span[3], c = ord_val(acc[6]);
+    for (int d = 0; d < 3; ++d) {
+        gp->o[d] = ord_val(acc[d]);
+        span[d] = ord_val(acc[3 + d]) - gp->o[d];
+    }
+    const double smax = fmax(span[0], fmax(span[1], span[2]));
+    if (!(c > 0.0)) c = smax > 0.0 ? smax * 1e-6 : 1.0;
+    for (;;) {
+        double prod = 1.0;
+        for (int d = 0; d < 3; ++d) prod *= floor(span[d] / c) + 1.0;
+        if (prod <= (double)max_cells) break;
+        c *= 1.25;
+    }
+    gp->c = c;
+    for (int d = 0; d < 3; ++d) gp->dims[d] = (int)(floor(span[d] / c) + 1.0);
+}
+
+// Row i's slots sorted by j -> pairs[off[i] ...] (insertion sort, <= kRowSlots).
+__global__ void slots_compact_kernel(const int *__restrict__ row_count, const int64_t *__restrict__ off, int64_t L,
+                                     const int32_t *__restrict__ slots, int32_t *__restrict__ pairs) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= L) return;
+    const int n = row_count[i];
+    int32_t v[kRowSlots];
+#pragma unroll
+    for (int k = 0; k < kRowSlots; ++k) v[k] = k < n ? slots[i * kRowSlots + k] : INT_MAX;
+#pragma unroll
+    for (int a = 1; a < kRowSlots; ++a)
+#pragma unroll
+        for (int b = a; b > 0; --b)
+            if (v[b] < v[b - 1]) {
+                const int32_t t = v[b];
+                v[b] = v[b - 1];
+                v[b - 1] = t;
+            }
+    const int64_t o = off[i];
+#pragma unroll
+    for (int k = 0; k < kRowSlots; ++k)
+        if (k < n) {
+            pairs[2 * (o + k)] = (int32_t)i;
+            pairs[2 * (o + k) + 1] = v[k];
+        }
+}
+
+__global__ void row_counts_i64_kernel(const int *__restrict__ row_count, int64_t L, int64_t *__restrict__ out,
+                                      int *__restrict__ max_count) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < L) {
+        out[i] = row_count[i];
+        atomicMax(max_count, row_count[i]);
+    } else if (i == L) {
+        out[L] = 0;
+    }
+}
 __global__ void unpack_pairs_kernel(const uint64_t *__restrict__ keys, int64_t P, int32_t *__restrict__ pairs) {
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p >= P) return;
@@ -174,12 +517,13 @@ __global__ void unpack_pairs_kernel(const uint64_t *__restrict__ keys, int64_t P
 }  // namespace
 
 void launch_seg_boxes(const double *coeffs, const double *t, const int64_t *loff, int64_t L, int64_t M,
-                      double min_diam, double *seg_box, int32_t *seg_loop, int *zero_loop, cudaStream_t s) {
-    const int init = INT_MAX;
-    LC_CUDA(cudaMemcpyAsync(zero_loop, &init, sizeof(int), cudaMemcpyHostToDevice, s));
+                      double *seg_box, int32_t *seg_loop, unsigned long long *loop_min_diag, int *max_exp,
+                      cudaStream_t s) {
+    if (loop_min_diag) LC_CUDA(cudaMemsetAsync(loop_min_diag, 0xff, sizeof(unsigned long long) * (L > 0 ? L : 1), s));
+    if (max_exp) LC_CUDA(cudaMemsetAsync(max_exp, 0, sizeof(int), s));
     if (M == 0) return;
-    seg_boxes_kernel<<<(unsigned)ceil_div(M, 128), 128, 0, s>>>(coeffs, t, loff, L, M, min_diam, seg_box,
-                                                                   seg_loop, zero_loop);
+    seg_boxes_kernel<<<(unsigned)ceil_div(M, 128), 128, 0, s>>>(coeffs, t, loff, L, M, seg_box, seg_loop,
+                                                                   loop_min_diag, max_exp);
     LC_CHECK_LAUNCH();
 }
 
@@ -191,59 +535,141 @@ void launch_loop_boxes(const double *seg_box, int64_t M, const int64_t *loff, in
 }
 
 int64_t run_pls(const double *loop_box, int64_t L, const uint64_t *h_excl, int64_t n_excl, PlsScratch &sc,
-                DevBuf &pairs, cudaStream_t s) {
+                DevBuf &pairs, cudaStream_t s, bool force_sweep) {
     if (L < 2) return 0;
+    sc.excl.reserve(sizeof(uint64_t) * (n_excl > 0 ? n_excl : 1), s);
+    if (n_excl > 0)
+        LC_CUDA(cudaMemcpyAsync(sc.excl.ptr, h_excl, sizeof(uint64_t) * n_excl, cudaMemcpyHostToDevice, s));
+    if (!force_sweep) {
+        const int64_t max_cells = 4 * L + 64;
+        sc.axis.reserve(sizeof(GridParams), s);
+        sc.keys.reserve(sizeof(int64_t) * (max_cells + 1), s);         // cell counts
+        sc.keys_sorted.reserve(sizeof(int64_t) * (max_cells + 1), s);  // cell offsets
+        sc.sbox.reserve(sizeof(int64_t) * (max_cells + 1), s);         // scatter cursors
+        sc.perm.reserve(sizeof(int32_t) * L, s);                       // loops in cell order
+        sc.idx.reserve(sizeof(int) * L, s);                            // row counts
+        sc.pair_keys.reserve(sizeof(int32_t) * kRowSlots * L, s);      // slots
+        sc.counts.reserve(sizeof(int64_t) * (L + 1), s);
+        sc.offs.reserve(sizeof(int64_t) * (L + 1), s);
+        sc.counter.reserve(sizeof(unsigned long long), s);
+        GridParams *gp = sc.axis.as<GridParams>();
+        int64_t *cnt = sc.keys.as<int64_t>(), *coff = sc.keys_sorted.as<int64_t>(), *cur = sc.sbox.as<int64_t>();
+        int *row_count = sc.idx.as<int>(), *max_count = sc.counter.as<int>();
+        sc.counts.reserve(sizeof(int64_t) * (L + 8 > 8 ? L + 8 : 8), s);
+        unsigned long long *acc = (unsigned long long *)sc.counts.ptr;   // 7 ordered keys, reused below
+        LC_CUDA(cudaMemsetAsync(acc, 0xff, 3 * sizeof(unsigned long long), s));
+        LC_CUDA(cudaMemsetAsync(acc + 3, 0, 4 * sizeof(unsigned long long), s));
+        grid_reduce_kernel<<<(unsigned)(ceil_div(L, 256) < 148 ? ceil_div(L, 256) : 148), 256, 0, s>>>(loop_box, L, acc);
+        LC_CHECK_LAUNCH();
+        grid_finalize_kernel<<<1, 1, 0, s>>>(acc, max_cells, gp);
+        LC_CHECK_LAUNCH();
+        LC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (max_cells + 1), s));
+        const unsigned gl = (unsigned)ceil_div(L, 256);
+        cell_count_kernel<<<gl, 256, 0, s>>>(loop_box, L, gp, cnt);
+        LC_CHECK_LAUNCH();
+        size_t b = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, b, (int64_t *)nullptr, (int64_t *)nullptr, (int)(max_cells + 1));
+        size_t b2 = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, b2, (int64_t *)nullptr, (int64_t *)nullptr, (int)(L + 1));
+        sc.cub_tmp.reserve(b > b2 ? b : b2, s);
+        b = sc.cub_tmp.bytes;
+        LC_CUB(cub::DeviceScan::ExclusiveSum(sc.cub_tmp.ptr, b, cnt, coff, (int)(max_cells + 1), s));
+        LC_CUDA(cudaMemcpyAsync(cur, coff, sizeof(int64_t) * (max_cells + 1), cudaMemcpyDeviceToDevice, s));
+        cell_scatter_kernel<<<gl, 256, 0, s>>>(loop_box, L, gp, cur, sc.perm.as<int32_t>());
+        LC_CHECK_LAUNCH();
+        LC_CUDA(cudaMemsetAsync(max_count, 0, sizeof(int), s));
+        grid_query_warp_kernel<true><<<(unsigned)ceil_div(L * 32, 256), 256, 0, s>>>(loop_box, L, gp, coff, sc.perm.as<int32_t>(),
+                                                   sc.excl.as<uint64_t>(), n_excl, row_count,
+                                                   sc.pair_keys.as<int32_t>(), nullptr, nullptr);
+        LC_CHECK_LAUNCH();
+        row_counts_i64_kernel<<<(unsigned)ceil_div(L + 1, 256), 256, 0, s>>>(row_count, L, sc.counts.as<int64_t>(),
+                                                                               max_count);
+        LC_CHECK_LAUNCH();
+        b = sc.cub_tmp.bytes;
+        LC_CUB(cub::DeviceScan::ExclusiveSum(sc.cub_tmp.ptr, b, sc.counts.as<int64_t>(), sc.offs.as<int64_t>(),
+                                             (int)(L + 1), s));
+        int64_t P = 0;
+        int mx = 0;
+        LC_CUDA(cudaMemcpyAsync(&P, sc.offs.as<int64_t>() + L, sizeof P, cudaMemcpyDeviceToHost, s));
+        LC_CUDA(cudaMemcpyAsync(&mx, max_count, sizeof mx, cudaMemcpyDeviceToHost, s));
+        LC_CUDA(cudaStreamSynchronize(s));
+        if (P == 0) return 0;
+        pairs.reserve(sizeof(int32_t) * 2 * P, s);
+        if (mx <= kRowSlots) {
+            slots_compact_kernel<<<gl, 256, 0, s>>>(row_count, sc.offs.as<int64_t>(), L, sc.pair_keys.as<int32_t>(),
+                                                     pairs.as<int32_t>());
+            LC_CHECK_LAUNCH();
+            return P;
+        }
+        // some loop overlaps more than kRowSlots later loops: write keys at exact offsets, sort
+        sc.pair_keys.reserve(sizeof(uint64_t) * P, s);
+        sc.pair_keys_sorted.reserve(sizeof(uint64_t) * P, s);
+        grid_query_warp_kernel<false><<<(unsigned)ceil_div(L * 32, 256), 256, 0, s>>>(loop_box, L, gp, coff, sc.perm.as<int32_t>(),
+                                                    sc.excl.as<uint64_t>(), n_excl, nullptr, nullptr,
+                                                    sc.offs.as<int64_t>(), sc.pair_keys.as<uint64_t>());
+        LC_CHECK_LAUNCH();
+        size_t b3 = 0;
+        cub::DeviceRadixSort::SortKeys(nullptr, b3, (uint64_t *)nullptr, (uint64_t *)nullptr, (int)P);
+        sc.cub_tmp.reserve(b3, s);
+        b3 = sc.cub_tmp.bytes;
+        LC_CUB(cub::DeviceRadixSort::SortKeys(sc.cub_tmp.ptr, b3, sc.pair_keys.as<uint64_t>(),
+                                              sc.pair_keys_sorted.as<uint64_t>(), (int)P, 0, 64, s));
+        unpack_pairs_kernel<<<(unsigned)ceil_div(P, 256), 256, 0, s>>>(sc.pair_keys_sorted.as<uint64_t>(), P,
+                                                                        pairs.as<int32_t>());
+        LC_CHECK_LAUNCH();
+        return P;
+    }
+    // sort-and-sweep on the axis of largest extent (LINKCERT_PLS_SWEEP=1)
     sc.keys.reserve(sizeof(double) * L, s);
     sc.keys_sorted.reserve(sizeof(double) * L, s);
     sc.idx.reserve(sizeof(int32_t) * L, s);
     sc.perm.reserve(sizeof(int32_t) * L, s);
-    sc.counts.reserve(sizeof(int64_t) * (L + 1), s);
-    sc.offs.reserve(sizeof(int64_t) * (L + 1), s);
+    sc.sbox.reserve(sizeof(double) * 6 * L, s);
     sc.axis.reserve(sizeof(int), s);
-    sc.excl.reserve(sizeof(uint64_t) * (n_excl > 0 ? n_excl : 1), s);
-    if (n_excl > 0)
-        LC_CUDA(cudaMemcpyAsync(sc.excl.ptr, h_excl, sizeof(uint64_t) * n_excl, cudaMemcpyHostToDevice, s));
+    sc.counter.reserve(sizeof(unsigned long long), s);
 
     sweep_axis_kernel<<<1, 1024, 0, s>>>(loop_box, L, sc.axis.as<int>(), sc.keys.as<double>(), sc.idx.as<int32_t>());
     LC_CHECK_LAUNCH();
-    size_t b1 = 0, b2 = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, b1, (double *)nullptr, (double *)nullptr, (int32_t *)nullptr,
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (double *)nullptr, (double *)nullptr, (int32_t *)nullptr,
                                     (int32_t *)nullptr, (int)L);
-    cub::DeviceScan::ExclusiveSum(nullptr, b2, (int64_t *)nullptr, (int64_t *)nullptr, (int)(L + 1));
-    sc.cub_tmp.reserve(b1 > b2 ? b1 : b2, s);
-    size_t bytes = sc.cub_tmp.bytes;
-    LC_CUB(cub::DeviceRadixSort::SortPairs(sc.cub_tmp.ptr, bytes, sc.keys.as<double>(), sc.keys_sorted.as<double>(),
-                                            sc.idx.as<int32_t>(), sc.perm.as<int32_t>(), (int)L, 0, 64, s));
-    const unsigned grid = (unsigned)ceil_div(L, 128);
-    LC_CUDA(cudaMemsetAsync(sc.counts.as<int64_t>() + L, 0, sizeof(int64_t), s));
-    sweep_kernel<false><<<grid, 128, 0, s>>>(loop_box, L, sc.axis.as<int>(), sc.keys_sorted.as<double>(),
-                                             sc.perm.as<int32_t>(), sc.excl.as<uint64_t>(), n_excl,
-                                             sc.counts.as<int64_t>(), nullptr, nullptr);
-    LC_CHECK_LAUNCH();
+    sc.cub_tmp.reserve(bytes, s);
     bytes = sc.cub_tmp.bytes;
-    LC_CUB(cub::DeviceScan::ExclusiveSum(sc.cub_tmp.ptr, bytes, sc.counts.as<int64_t>(), sc.offs.as<int64_t>(),
-                                          (int)(L + 1), s));
-    int64_t P = 0;
-    LC_CUDA(cudaMemcpyAsync(&P, sc.offs.as<int64_t>() + L, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    LC_CUDA(cudaStreamSynchronize(s));
-    if (P == 0) return 0;
-    sc.pair_keys.reserve(sizeof(uint64_t) * P, s);
-    sc.pair_keys_sorted.reserve(sizeof(uint64_t) * P, s);
-    sweep_kernel<true><<<grid, 128, 0, s>>>(loop_box, L, sc.axis.as<int>(), sc.keys_sorted.as<double>(),
-                                            sc.perm.as<int32_t>(), sc.excl.as<uint64_t>(), n_excl, nullptr,
-                                            sc.offs.as<int64_t>(), sc.pair_keys.as<uint64_t>());
+    LC_CUB(cub::DeviceRadixSort::SortPairs(sc.cub_tmp.ptr, bytes, sc.keys.as<double>(), sc.keys_sorted.as<double>(),
+                                           sc.idx.as<int32_t>(), sc.perm.as<int32_t>(), (int)L, 0, 64, s));
+    gather_boxes_kernel<<<(unsigned)ceil_div(L, 256), 256, 0, s>>>(loop_box, sc.perm.as<int32_t>(), L,
+                                                                    sc.sbox.as<double>());
     LC_CHECK_LAUNCH();
+
+    int64_t cap = sc.cap > 0 ? sc.cap : 16 * L + 1024;
+    unsigned long long P = 0;
+    for (;;) {
+        sc.pair_keys.reserve(sizeof(uint64_t) * cap, s);
+        LC_CUDA(cudaMemsetAsync(sc.counter.ptr, 0, sizeof(unsigned long long), s));
+        const int64_t warps = L < 148 * 64 ? L : 148 * 64;
+        sweep_warp_kernel<<<(unsigned)ceil_div(warps * 32, 256), 256, 0, s>>>(
+            sc.sbox.as<double>(), sc.perm.as<int32_t>(), L, sc.axis.as<int>(), sc.excl.as<uint64_t>(), n_excl,
+            sc.counter.as<unsigned long long>(), sc.pair_keys.as<uint64_t>(), cap);
+        LC_CHECK_LAUNCH();
+        LC_CUDA(cudaMemcpyAsync(&P, sc.counter.ptr, sizeof P, cudaMemcpyDeviceToHost, s));
+        LC_CUDA(cudaStreamSynchronize(s));
+        if ((int64_t)P <= cap) break;
+        cap = (int64_t)P + P / 4 + 1024;   // rare: grow and sweep again
+    }
+    sc.cap = cap;
+    if (P == 0) return 0;
+    sc.pair_keys_sorted.reserve(sizeof(uint64_t) * P, s);
     size_t b3 = 0;
     cub::DeviceRadixSort::SortKeys(nullptr, b3, (uint64_t *)nullptr, (uint64_t *)nullptr, (int)P);
     sc.cub_tmp.reserve(b3, s);
     bytes = sc.cub_tmp.bytes;
     LC_CUB(cub::DeviceRadixSort::SortKeys(sc.cub_tmp.ptr, bytes, sc.pair_keys.as<uint64_t>(),
-                                           sc.pair_keys_sorted.as<uint64_t>(), (int)P, 0, 64, s));
+                                          sc.pair_keys_sorted.as<uint64_t>(), (int)P, 0, 64, s));
     pairs.reserve(sizeof(int32_t) * 2 * P, s);
-    unpack_pairs_kernel<<<(unsigned)ceil_div(P, 256), 256, 0, s>>>(sc.pair_keys_sorted.as<uint64_t>(), P,
-                                                                     pairs.as<int32_t>());
+    unpack_pairs_kernel<<<(unsigned)ceil_div((int64_t)P, 256), 256, 0, s>>>(sc.pair_keys_sorted.as<uint64_t>(),
+                                                                              (int64_t)P, pairs.as<int32_t>());
     LC_CHECK_LAUNCH();
-    return P;
+    return (int64_t)P;
 }
 
 }  // namespace lc

@@ -7,25 +7,33 @@ namespace lc {
 
 // Boxes are SoA: box[0*n..] lo_x, [1*n] lo_y, [2*n] lo_z, [3*n] hi_x, [4*n] hi_y, [5*n] hi_z.
 
-// Per-segment tight boxes over each segment's own domain; seg_loop[m] = loop
-// of segment m; zero-length check (discretize.py:124-129): *zero_loop =
-// min loop index with a segment box diagonal < min_diam (INT_MAX if none).
+// Per-segment tight boxes over each segment's own domain (geometry.py:113-152);
+// seg_loop[m] = loop of segment m.  Optional outputs: loop_min_diag[l] =
+// bit pattern of the smallest segment-box diagonal of loop l (ZeroLengthInput,
+// discretize.py:124-129); *max_exp = largest exponent field of any box
+// coordinate (the exact power-of-two scale of the Gauss-sum input).
 void launch_seg_boxes(const double *coeffs, const double *t, const int64_t *loff, int64_t L, int64_t M,
-                      double min_diam, double *seg_box, int32_t *seg_loop, int *zero_loop, cudaStream_t s);
+                      double *seg_box, int32_t *seg_loop, unsigned long long *loop_min_diag, int *max_exp,
+                      cudaStream_t s);
 
 // Loop AABB = union of its segment boxes (pls.py:48-56).
 void launch_loop_boxes(const double *seg_box, int64_t M, const int64_t *loff, int64_t L, double *loop_box,
                        cudaStream_t s);
 
 struct PlsScratch {
-    DevBuf keys, keys_sorted, idx, perm, counts, offs, cub_tmp, pair_keys, pair_keys_sorted, axis, excl;
+    DevBuf keys, keys_sorted, idx, perm, sbox, counter, cub_tmp, pair_keys, pair_keys_sorted, axis, excl, counts,
+        offs;
+    int64_t cap = 0;
 };
 
-// Sort-and-sweep over loop boxes on the axis of largest extent, closed
-// intervals (bvh.py:93-98), i<j, minus the excluded keys (sorted uint64
-// (i<<32|j)), sorted lexicographically.  Writes int32 (P,2) into *pairs
-// (grown as needed) and returns P (one host sync for the count).
+// All (i<j) loop pairs with overlapping closed boxes (bvh.py:93-98) minus the
+// excluded keys (sorted uint64 (i<<32|j)), sorted lexicographically.
+// Default: exact uniform-grid culling (cells >= the largest loop extent, each
+// loop stored in the cell of its lower corner, pairs emitted from the
+// smaller index into per-row slots sorted at compaction — no global sort).
+// force_sweep: sort-and-sweep on the axis of largest extent + radix sort.
+// Writes int32 (P,2) into *pairs (grown as needed) and returns P (one sync).
 int64_t run_pls(const double *loop_box, int64_t L, const uint64_t *h_excl, int64_t n_excl, PlsScratch &sc,
-                DevBuf &pairs, cudaStream_t s);
+                DevBuf &pairs, cudaStream_t s, bool force_sweep = false);
 
 }  // namespace lc

@@ -312,7 +312,28 @@ class CurveModel:
         np.cumsum(counts, out=off[1:])
         packed = (coeffs, t, off)
         self.__dict__["_packed_cache"] = (key, packed)
+        self.__dict__.pop("_polyline_cache", None)
         return packed
+
+    def polyline_vertices(self):
+        """(verts (M, 3), loop_off) when every loop is a plain closed polyline whose
+        arrays are exactly LoopGeometry.from_polyline's (a1 = next - start bitwise,
+        a2 = a3 = 0, t = [0, 1]) — then only the vertices need to reach the GPU.
+        None otherwise.  Cached with the packed arrays."""
+        coeffs, t, off = self.packed()
+        cache = self.__dict__.get("_polyline_cache")
+        if cache is not None and cache[0] is coeffs:
+            return cache[1]
+        result = None
+        if len(off) > 1 and all(lp.closed for lp in self.loops) and np.all(np.diff(off) >= 1):
+            nxt = np.arange(len(coeffs), dtype=np.int64) + 1
+            nxt[off[1:] - 1] = off[:-1]
+            a0 = coeffs[:, 0]
+            if (not np.any(coeffs[:, 2:]) and np.all(t[:, 0] == 0.0) and np.all(t[:, 1] == 1.0)
+                    and np.array_equal((a0[nxt] - a0).view(np.int64), coeffs[:, 1].view(np.int64))):
+                result = (np.ascontiguousarray(a0), off)
+        self.__dict__["_polyline_cache"] = (coeffs, result)
+        return result
 
     @classmethod
     def from_polyline_arrays(cls, verts, offsets, closed=True):
@@ -364,6 +385,7 @@ class CurveModel:
         xi = total / (3 * len(verts)) if len(verts) else 0.0
         model = cls(loops, xi=xi)
         model.__dict__["_packed_cache"] = (tuple(map(id, loops)), (coeffs, t, off))
+        model.__dict__["_polyline_cache"] = (coeffs, (verts, off))
         return model
 
 

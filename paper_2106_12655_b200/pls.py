@@ -87,8 +87,12 @@ def excluded_keys(excluded):
 def upload(model: CurveModel, ctx=None):
     """Stage the model's packed arrays on the device (segment + loop boxes)."""
     ctx = ctx or _native.context()
-    coeffs, t, off = model.packed()
-    ctx.upload_model(coeffs, t, off)
+    poly = model.polyline_vertices()
+    if poly is not None:            # 24 B/segment instead of 112 B/segment over PCIe
+        ctx.upload_model_polylines(*poly)
+    else:
+        coeffs, t, off = model.packed()
+        ctx.upload_model(coeffs, t, off)
     return ctx
 
 

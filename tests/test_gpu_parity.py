@@ -66,6 +66,45 @@ def test_pls_pairs_exact(golden, golden_arrays, cert_models, name):
     assert np.array_equal(pl.array, golden_arrays[f"{name}__pairs"])
 
 
+@pytest.mark.parametrize("n_loops,spread", [(300, 3.0), (2000, 40.0), (40000, 400.0)])
+def test_pls_dense_and_large_vs_oracle(oracle, n_loops, spread):
+    """Crowded boxes (> 16 later overlaps per loop: two-pass fallback) and L > 32768 (sweep path)."""
+    rng = np.random.default_rng(n_loops)
+    ex, ey, ez = np.eye(3)
+    centers = rng.uniform(0, spread, size=(n_loops, 3))
+    pts = np.stack([cases.circ(6, c, ex, ey if k % 2 else ez, 0.5 + 0.5 * rng.random())
+                    for k, c in enumerate(centers)])
+    off = np.arange(n_loops + 1, dtype=np.int64) * 6
+    m = lc.CurveModel.from_polyline_arrays(pts.reshape(-1, 3), off)
+    coeffs, t, o = m.packed()
+    want = oracle.pls(coeffs, t, o) if n_loops <= 2000 else None
+    got = lc.potential_link_search(m).array
+    if want is not None:
+        assert np.array_equal(got, want)
+    else:   # large L: check soundness/completeness on a random sample of rows against brute force
+        lo, hi = oracle.loop_boxes(coeffs, t, o)
+        for i in rng.choice(n_loops, 50, replace=False):
+            ov = np.all((lo[i] <= hi) & (lo <= hi[i]), axis=1)
+            ov[: i + 1] = False
+            assert np.array_equal(np.nonzero(ov)[0], got[got[:, 0] == i, 1])
+
+
+def test_pls_sweep_path_exact(golden_arrays):
+    """The sort-and-sweep PLS (used for L > 32768) gives the same pair sets."""
+    import subprocess
+    import sys
+
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, 'tests'); import cases, paper_2106_12655_b200 as lc\n"
+        "g = np.load('tests/golden/golden_arrays.npz')\n"
+        "for name, m in cases.cert_models(full=True).items():\n"
+        "    assert np.array_equal(lc.potential_link_search(m).array, g[name + '__pairs']), name\n"
+        "print('sweep ok')\n")
+    env = dict(__import__("os").environ, LINKCERT_PLS_SWEEP="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "sweep ok" in out.stdout, out.stderr[-2000:]
+
+
 @pytest.mark.parametrize("name", ALL_CERTS)
 def test_discretize_bitwise(golden, golden_arrays, cert_models, name):
     m = cert_models[name]
