@@ -314,10 +314,31 @@ struct Sha256 {
 
 struct Chunk {
     int64_t l0, l1;                  // loops [l0, l1)
-    std::unique_ptr<char[]> data;
+    char *data = nullptr;            // points into the persistent chunk pool
     size_t size = 0;
     std::atomic<bool> ready{false};
 };
+
+// Persistent per-chunk output buffers: reused across calls so the formatting
+// threads do not page-fault fresh allocations every time (one digest at a time).
+std::mutex g_pool_mu;
+std::vector<std::unique_ptr<char[]>> g_pool;
+std::vector<size_t> g_pool_cap;
+
+char *pool_buffer(size_t k, size_t bound) {
+    if (g_pool_cap[k] < bound) {
+        g_pool[k].reset(new char[bound + bound / 4]);
+        g_pool_cap[k] = bound + bound / 4;
+    }
+    return g_pool[k].get();
+}
+
+void pool_reserve(size_t n) {
+    if (g_pool.size() < n) {
+        g_pool.resize(n);
+        g_pool_cap.resize(n, 0);
+    }
+}
 
 struct Job {
     const double *coeffs, *t;
@@ -336,14 +357,14 @@ struct Job {
             poly[l - c.l0] = loop_is_polyline(coeffs + 12 * off[l], t + 2 * off[l], m);
             bound += loop_bound(m, poly[l - c.l0]) + 1;
         }
-        c.data.reset(new char[bound]);
-        char *p = c.data.get();
+        c.data = pool_buffer((size_t)(&c - chunks.data()), bound);
+        char *p = c.data;
         for (int64_t l = c.l0; l < c.l1; ++l) {
             if (l) *p++ = ',';
             p = put_loop(p, coeffs + 12 * off[l], t + 2 * off[l], off[l + 1] - off[l], closed ? closed[l] != 0 : true,
                          poly[l - c.l0]);
         }
-        c.size = (size_t)(p - c.data.get());
+        c.size = (size_t)(p - c.data);
         {
             std::lock_guard<std::mutex> g(mu);
             c.ready.store(true, std::memory_order_release);
@@ -411,7 +432,9 @@ LC_API int64_t lc_model_json(const double *coeffs, const double *t, const int64_
     const int64_t M = L > 0 ? loop_off[L] : 0;
     if (!all_finite(coeffs, 12 * M)) return -1;
     Job job{coeffs, t, loop_off, closed};
+    std::lock_guard<std::mutex> pool_lock(g_pool_mu);
     make_chunks(job, L, M, 16384);
+    pool_reserve(job.chunks.size());
     std::vector<std::thread> th;
     for (int k = 0; k < resolve_threads(nthreads) - 1; ++k) th.emplace_back([&] { job.worker(); });
     job.worker();
@@ -424,7 +447,7 @@ LC_API int64_t lc_model_json(const double *coeffs, const double *t, const int64_
     std::memcpy(out, head, sizeof head - 1);
     n += sizeof head - 1;
     for (auto &c : job.chunks) {
-        std::memcpy(out + n, c.data.get(), c.size);
+        std::memcpy(out + n, c.data, c.size);
         n += (int64_t)c.size;
     }
     std::memcpy(out + n, tail, sizeof tail - 1);
@@ -436,16 +459,18 @@ LC_API int lc_model_digest(const double *coeffs, const double *t, const int64_t 
     const int64_t M = L > 0 ? loop_off[L] : 0;
     if (!all_finite(coeffs, 12 * M)) return -1;
     Job job{coeffs, t, loop_off, closed};
+    std::lock_guard<std::mutex> pool_lock(g_pool_mu);
     make_chunks(job, L, M, 4096);
+    pool_reserve(job.chunks.size());
     const int nt = resolve_threads(nthreads);
     std::vector<std::thread> th;
-    for (int k = 0; k < nt; ++k) th.emplace_back([&] { job.worker(); });
+    // the calling thread hashes: nt - 1 formatting workers keep it on its own core
+    for (int k = 0; k < (nt > 1 ? nt - 1 : 1); ++k) th.emplace_back([&] { job.worker(); });
     Sha256 h;
     h.update("{\"loops\":[", 10);
     for (auto &c : job.chunks) {
         job.wait(c);
-        h.update(c.data.get(), c.size);
-        c.data.reset();
+        h.update(c.data, c.size);
     }
     h.update("]}", 2);
     for (auto &x : th) x.join();
