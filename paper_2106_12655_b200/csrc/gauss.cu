@@ -52,17 +52,23 @@ __device__ __forceinline__ void cmul_w(double ax, double ay, double bx, double b
 // sqrt(x) for x >= 0 without the libdevice special-case branch: MUFU rsqrt
 // seed + 2 Newton steps, s = x * y (~2 ulp; the norms only enter the d1/d2
 // denominators).  LC_SQRT_HERON adds a Heron correction (<= 1 ulp).
+template <bool ZERO_SAFE = true>
 __device__ __forceinline__ double sqrt_nb(double x) {
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-    const double h = 0.5 * x;
-    y = fma(y, fma(-h * y, y, 0.5), y);
-    y = fma(y, fma(-h * y, y, 0.5), y);
-    double s = x * y;
+    // coupled (Goldschmidt) iteration: g -> sqrt(x), hh -> 1/(2 sqrt(x)); 7 FP64 ops
+    double g = x * y, hh = 0.5 * y;
+    double r = fma(-g, hh, 0.5);
+    g = fma(g, r, g);
+    hh = fma(hh, r, hh);
+    r = fma(-g, hh, 0.5);
+    g = fma(g, r, g);
 #ifdef LC_SQRT_HERON
-    s = fma(fma(-s, s, x), 0.5 * y, s);
+    g = fma(fma(-g, g, x), hh, g);
 #endif
-    return x > 0.0 ? s : 0.0;
+    // x == 0 (coincident vertices) gives NaN without the select; the phase fast
+    // path omits it and re-evaluates such (degenerate) strips exactly.
+    return ZERO_SAFE ? (x > 0.0 ? g : 0.0) : g;
 }
 
 // Reference _pair_lambda with the IEEE operation sequence of the numba
@@ -104,14 +110,41 @@ struct Col {   // one column: r(c, m) = l_c - k_m, |r(c, m)|, v[m] = r(c,m).r(c,
     double x[R + 1], y[R + 1], z[R + 1], n[R + 1], v[R];
 };
 
-__device__ __forceinline__ void col_fill(Col &B, double lx, double ly, double lz, const double *kx, const double *ky,
-                                         const double *kz) {
+// Row vertices k_m of a lane: in registers (KReg) or in shared memory (KSm,
+// re-read every column step with volatile loads to free 30 registers).
+struct KReg {
+    double x[R + 1], y[R + 1], z[R + 1];
+    __device__ __forceinline__ double X(int m) const { return x[m]; }
+    __device__ __forceinline__ double Y(int m) const { return y[m]; }
+    __device__ __forceinline__ double Z(int m) const { return z[m]; }
+    __device__ __forceinline__ void set(int m, double a, double b, double c) { x[m] = a; y[m] = b; z[m] = c; }
+};
+constexpr int kCtaThreads = 128;
+struct KSm {
+    double *p;   // this thread's column of a [3*(R+1)][kCtaThreads] shared array
+    __device__ __forceinline__ static double ld(const double *q) {
+        double v;
+        asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(v) : "l"(__cvta_generic_to_shared(q)));
+        return v;
+    }
+    __device__ __forceinline__ double X(int m) const { return ld(p + m * kCtaThreads); }
+    __device__ __forceinline__ double Y(int m) const { return ld(p + (R + 1 + m) * kCtaThreads); }
+    __device__ __forceinline__ double Z(int m) const { return ld(p + (2 * R + 2 + m) * kCtaThreads); }
+    __device__ __forceinline__ void set(int m, double a, double b, double c) {
+        p[m * kCtaThreads] = a;
+        p[(R + 1 + m) * kCtaThreads] = b;
+        p[(2 * R + 2 + m) * kCtaThreads] = c;
+    }
+};
+
+template <bool ZERO_SAFE, class K>
+__device__ __forceinline__ void col_fill(Col &B, double lx, double ly, double lz, const K &k) {
 #pragma unroll
     for (int m = 0; m <= R; ++m) {
-        B.x[m] = lx - kx[m];
-        B.y[m] = ly - ky[m];
-        B.z[m] = lz - kz[m];
-        B.n[m] = sqrt_nb(fma(B.z[m], B.z[m], fma(B.y[m], B.y[m], B.x[m] * B.x[m])));
+        B.x[m] = lx - k.X(m);
+        B.y[m] = ly - k.Y(m);
+        B.z[m] = lz - k.Z(m);
+        B.n[m] = sqrt_nb<ZERO_SAFE>(fma(B.z[m], B.z[m], fma(B.y[m], B.y[m], B.x[m] * B.x[m])));
     }
 #pragma unroll
     for (int m = 0; m < R; ++m) B.v[m] = fma(B.z[m], B.z[m + 1], fma(B.y[m], B.y[m + 1], B.x[m] * B.x[m + 1]));
@@ -123,6 +156,7 @@ __device__ __forceinline__ void col_fill(Col &B, double lx, double ly, double lz
 // Returns w = (d1 + i p)(d2 + i p) = (xp, yp); its wrap (z1, z2 share the sign
 // bit of p) goes to `turns`.  A degenerate w == 0 (p = 0 and d1 or d2 = 0)
 // contributes the exact atan2(+-0, d) half turns instead and w := 1.
+template <bool FAST>
 __device__ __forceinline__ void pair_w(const Col &A, const Col &B, const double *h, int m, double &wx, double &wy,
                                        int &turns, int &halves) {
     const double ax = A.x[m], ay = A.y[m], az = A.z[m];
@@ -138,6 +172,12 @@ __device__ __forceinline__ void pair_w(const Col &A, const Col &B, const double 
     const double d2 = fma(dn, t1, fma(cn, ad, an * dc));
     const double xp = fma(d1, d2, -p * p);
     const double yp = p * (d1 + d2);
+    if (FAST) {   // degenerate w == 0 is caught by the strip's zero/NaN check instead
+        turns += sbit(yp) - sbit(p);
+        wx = xp;
+        wy = yp;
+        return;
+    }
     const bool deg = (xp == 0.0) & (yp == 0.0);
     const int sp = sbit(p);
     turns += deg ? 0 : (sbit(yp) - sp);
@@ -151,12 +191,14 @@ struct Acc {
     double sx = 1.0, sy = 0.0;   // GAUSS_PHASE: phase product
     double ang = 0.0;            // GAUSS_ATAN: sum of fused angles (radians)
     int turns = 0, halves = 0;
+    int bad = 0;                 // GAUSS_PHASE: re-evaluate the strip exactly
 };
 
-template <int MODE, bool FULL>
-__device__ __forceinline__ void col_step(const Col &A, Col &B, double lx, double ly, double lz, const double *kx,
-                                         const double *ky, const double *kz, const bool *rv, Acc &acc) {
-    col_fill(B, lx, ly, lz, kx, ky, kz);
+template <int MODE, bool FULL, bool RENORM, class K>
+__device__ __forceinline__ void col_step(const Col &A, Col &B, double lx, double ly, double lz, const K &k,
+                                         const bool *rv, Acc &acc) {
+    constexpr bool FAST = MODE == GAUSS_PHASE;
+    col_fill<!FAST>(B, lx, ly, lz, k);
     double h[R + 1];
 #pragma unroll
     for (int m = 0; m <= R; ++m) h[m] = fma(A.z[m], B.z[m], fma(A.y[m], B.y[m], A.x[m] * B.x[m]));
@@ -164,7 +206,7 @@ __device__ __forceinline__ void col_step(const Col &A, Col &B, double lx, double
 #pragma unroll
     for (int m = 0; m < R; ++m) {
         int t = 0, hv = 0;
-        pair_w(A, B, h, m, wx[m], wy[m], t, hv);
+        pair_w<FAST>(A, B, h, m, wx[m], wy[m], t, hv);
         if (!FULL && !rv[m]) {
             wx[m] = 1.0;
             wy[m] = 0.0;
@@ -183,41 +225,47 @@ __device__ __forceinline__ void col_step(const Col &A, Col &B, double lx, double
         cmul_w(wx[2], wy[2], wx[3], wy[3], bx, by, acc.turns);
         cmul_w(ax, ay, bx, by, ux, uy, acc.turns);
         cmul_w(acc.sx, acc.sy, ux, uy, nx, ny, acc.turns);
-        const int ex = __double2hiint(nx) & 0x7ff00000, ey = __double2hiint(ny) & 0x7ff00000;
-        const double scale = __hiloint2double(0x7fe00000 - (ex > ey ? ex : ey), 0);
-        acc.sx = nx * scale;
-        acc.sy = ny * scale;
+        if (RENORM) {   // every second step: exact power-of-two rescale of S
+            const int ex = __double2hiint(nx) & 0x7ff00000, ey = __double2hiint(ny) & 0x7ff00000;
+            const int e = ex > ey ? ex : ey;
+            acc.bad |= (e == 0) | (e == 0x7ff00000);   // S underflowed / degenerate / NaN
+            const double scale = __hiloint2double(0x7fe00000 - e, 0);
+            nx *= scale;
+            ny *= scale;
+        }
+        acc.sx = nx;
+        acc.sy = ny;
     }
 }
 
 // Sum over rows [row0, row0+R) x columns [c0, c1) of one pair, in turns.
-template <int MODE, bool FULL>
+template <int MODE, bool FULL, class K>
 __device__ double lane_strip(const double *__restrict__ X, const double *__restrict__ Y,
                              const double *__restrict__ Z, int64_t row_off, int nrows, int64_t col_off, int row0,
-                             int c0, int c1) {
-    double kx[R + 1], ky[R + 1], kz[R + 1];
+                             int c0, int c1, K &kv) {
     bool rv[R];
 #pragma unroll
     for (int m = 0; m <= R; ++m) {
         const int v = FULL ? row0 + m : min(row0 + m, nrows);   // closing vertex sits at index nrows
-        kx[m] = __ldg(X + row_off + v);
-        ky[m] = __ldg(Y + row_off + v);
-        kz[m] = __ldg(Z + row_off + v);
+        kv.set(m, __ldg(X + row_off + v), __ldg(Y + row_off + v), __ldg(Z + row_off + v));
     }
 #pragma unroll
     for (int m = 0; m < R; ++m) rv[m] = FULL || row0 + m < nrows;
     const double *px = X + col_off, *py = Y + col_off, *pz = Z + col_off;
     Col A, B;
-    col_fill(A, __ldg(px + c0), __ldg(py + c0), __ldg(pz + c0), kx, ky, kz);
+    col_fill<MODE != GAUSS_PHASE>(A, __ldg(px + c0), __ldg(py + c0), __ldg(pz + c0), kv);
     Acc acc;
     int c = c0;
     for (; c + 2 <= c1; c += 2) {
         const double l1x = __ldg(px + c + 1), l1y = __ldg(py + c + 1), l1z = __ldg(pz + c + 1);
         const double l2x = __ldg(px + c + 2), l2y = __ldg(py + c + 2), l2z = __ldg(pz + c + 2);
-        col_step<MODE, FULL>(A, B, l1x, l1y, l1z, kx, ky, kz, rv, acc);
-        col_step<MODE, FULL>(B, A, l2x, l2y, l2z, kx, ky, kz, rv, acc);
+        col_step<MODE, FULL, false>(A, B, l1x, l1y, l1z, kv, rv, acc);
+        col_step<MODE, FULL, true>(B, A, l2x, l2y, l2z, kv, rv, acc);
     }
-    if (c < c1) col_step<MODE, FULL>(A, B, __ldg(px + c + 1), __ldg(py + c + 1), __ldg(pz + c + 1), kx, ky, kz, rv, acc);
+    if (c < c1) col_step<MODE, FULL, true>(A, B, __ldg(px + c + 1), __ldg(py + c + 1), __ldg(pz + c + 1), kv, rv, acc);
+    if (MODE == GAUSS_PHASE && (acc.bad || !isfinite(acc.sx) || !isfinite(acc.sy)))
+        // coincident vertices, w == 0, underflow or NaN input: the exact per-pair path
+        return lane_strip<GAUSS_ATAN, FULL>(X, Y, Z, row_off, nrows, col_off, row0, c0, c1, kv);
     const double frac = MODE == GAUSS_ATAN ? acc.ang * kInvTwoPi : atan2(acc.sy, acc.sx) * kInvTwoPi;
     return (double)acc.turns + 0.5 * (double)acc.halves + frac;
 }
@@ -261,12 +309,13 @@ __device__ __forceinline__ int64_t find_pair(const int64_t *__restrict__ item_of
     return lo;
 }
 
-template <int MODE, int MINB>
-__global__ void __launch_bounds__(128, MINB) gauss_items_kernel(
+template <int MODE, int MINB, bool KSM = false>
+__global__ void __launch_bounds__(kCtaThreads, MINB) gauss_items_kernel(
     const double *__restrict__ X, const double *__restrict__ Y, const double *__restrict__ Z,
     const PairGeom *__restrict__ pg, const int64_t *__restrict__ item_off, const int32_t *__restrict__ item_pair,
     int64_t P, int64_t item_begin, int64_t item_end, unsigned long long *__restrict__ counter,
     double *__restrict__ partials) {
+    __shared__ double ksh[KSM ? 3 * (R + 1) * kCtaThreads : 1];
     const int lane = threadIdx.x & 31;
     for (;;) {
         unsigned long long k = 0;
@@ -288,10 +337,16 @@ __global__ void __launch_bounds__(128, MINB) gauss_items_kernel(
         if (row0 < g.nrows && c0 < c1) {
             if (MODE == GAUSS_REF) {
                 val = lane_strip_ref(X, Y, Z, g.row_off, g.nrows, g.col_off, row0, c0, c1);
-            } else if (row0 + R <= g.nrows) {
-                val = lane_strip<MODE, true>(X, Y, Z, g.row_off, g.nrows, g.col_off, row0, c0, c1);
+            } else if (KSM) {
+                KSm kv{ksh + threadIdx.x};
+                val = row0 + R <= g.nrows
+                          ? lane_strip<MODE, true>(X, Y, Z, g.row_off, g.nrows, g.col_off, row0, c0, c1, kv)
+                          : lane_strip<MODE, false>(X, Y, Z, g.row_off, g.nrows, g.col_off, row0, c0, c1, kv);
             } else {
-                val = lane_strip<MODE, false>(X, Y, Z, g.row_off, g.nrows, g.col_off, row0, c0, c1);
+                KReg kv;
+                val = row0 + R <= g.nrows
+                          ? lane_strip<MODE, true>(X, Y, Z, g.row_off, g.nrows, g.col_off, row0, c0, c1, kv)
+                          : lane_strip<MODE, false>(X, Y, Z, g.row_off, g.nrows, g.col_off, row0, c0, c1, kv);
             }
         }
 #pragma unroll
@@ -466,10 +521,12 @@ void launch_gauss_items(int mode, const double *X, const double *Y, const double
     LC_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s));
     using Kern = void (*)(const double *, const double *, const double *, const PairGeom *, const int64_t *,
                           const int32_t *, int64_t, int64_t, int64_t, unsigned long long *, double *);
-    // GAUSS_PHASE_OCC3/4: the phase kernel compiled for 3 / 4 resident CTAs (A/B variants)
-    static const Kern table[] = {gauss_items_kernel<GAUSS_PHASE, 1>, gauss_items_kernel<GAUSS_ATAN, 1>,
-                                 gauss_items_kernel<GAUSS_REF, 1>, gauss_items_kernel<GAUSS_PHASE, 3>,
-                                 gauss_items_kernel<GAUSS_PHASE, 4>};
+    // default phase kernel: 3 resident CTAs/SM (168 regs); modes 3-6 are A/B variants
+    // (1 CTA/SM with 232 regs; 4 CTAs; row vertices in shared memory)
+    static const Kern table[] = {gauss_items_kernel<GAUSS_PHASE, 3>, gauss_items_kernel<GAUSS_ATAN, 1>,
+                                 gauss_items_kernel<GAUSS_REF, 1>, gauss_items_kernel<GAUSS_PHASE, 1>,
+                                 gauss_items_kernel<GAUSS_PHASE, 4>, gauss_items_kernel<GAUSS_PHASE, 4, true>,
+                                 gauss_items_kernel<GAUSS_PHASE, 3, true>};
     if (mode < 0 || mode >= (int)(sizeof table / sizeof table[0])) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
     const Kern fn = table[mode];
     int per_sm = 0;

@@ -258,7 +258,7 @@ void Pipeline::build_gauss_items() {
 
 void Pipeline::run_gauss(int mode, int64_t item_begin, int64_t item_end, double *partials_ext,
                          cudaEvent_t ev0, cudaEvent_t ev1) {
-    if (mode < GAUSS_PHASE || mode > GAUSS_PHASE_OCC4) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
+    if (mode < GAUSS_PHASE || mode > 6) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
     double *out = partials_ext ? partials_ext : d_partials.as<double>();
     LC_CUDA(cudaEventRecord(ev0 ? ev0 : ev[EV_GAUSS0], s));
     launch_gauss_items(mode, gX, gY, gZ, d_pg.as<PairGeom>(), d_item_off.as<int64_t>(), d_item_pair.as<int32_t>(), P,
