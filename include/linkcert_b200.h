@@ -160,6 +160,10 @@ LC_API int lc_run_pipeline(lc_ctx *ctx, const uint64_t *excluded_keys, int64_t n
                            double epsilon, int max_passes, int64_t max_subsegments, int mode,
                            int64_t *n_pairs);
 LC_API int lc_get_results(lc_ctx *ctx, double *raw, int64_t *lk, uint8_t *flags);
+/* Zero-copy views of the last lc_run_pipeline results in library-owned pinned
+ * memory: pairs int32 (P,2), raw f64 (P), lk int64 (P), flags u8 (P).  Valid
+ * until the next pipeline call on this context. */
+LC_API int lc_result_views(lc_ctx *ctx, void **pairs, void **raw, void **lk, void **flags, int64_t *n_pairs);
 /* Device times (ms) of the last pipeline: [PLS, discretize, Gauss kernel, reduce]. */
 LC_API int lc_stage_times(lc_ctx *ctx, float *ms);
 

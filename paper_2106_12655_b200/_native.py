@@ -74,6 +74,8 @@ SIGNATURES = {
     "lc_run_pipeline": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_int,
                                         ctypes.c_int64, ctypes.c_int, _c_int64_p]),
     "lc_get_results": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    "lc_result_views": (ctypes.c_int, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                                        ctypes.POINTER(_vp), _c_int64_p]),
     "lc_stage_times": (ctypes.c_int, [_vp, _c_float_p]),
     "lc_model_json_bound": (ctypes.c_int64, [_vp, ctypes.c_int64]),
     "lc_model_json": (ctypes.c_int64, [_vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, ctypes.c_int64]),
@@ -424,6 +426,23 @@ class Context:
         with self.lock:
             _check(self.lib.lc_get_results(self.handle, _ptr(raw), _ptr(lk), _ptr(flags)))
         return raw, lk, flags
+
+    def result_views(self):
+        """(pairs (P,2) int32, raw, lk, flags) views into the library's pinned result
+        buffer — valid until the next pipeline call; copy what must be kept."""
+        ptrs = [_vp() for _ in range(4)]
+        n = ctypes.c_int64(0)
+        with self.lock:
+            _check(self.lib.lc_result_views(self.handle, *[ctypes.byref(p) for p in ptrs], ctypes.byref(n)))
+        P = n.value
+        if P == 0:
+            return (np.zeros((0, 2), np.int32), np.zeros(0), np.zeros(0, np.int64), np.zeros(0, np.uint8))
+
+        def view(p, ctype, shape):
+            return np.ctypeslib.as_array(ctypes.cast(p, ctypes.POINTER(ctype)), shape=shape)
+
+        return (view(ptrs[0], ctypes.c_int32, (P, 2)), view(ptrs[1], ctypes.c_double, (P,)),
+                view(ptrs[2], ctypes.c_int64, (P,)), view(ptrs[3], ctypes.c_uint8, (P,)))
 
     def stage_times(self):
         ms = (ctypes.c_float * 4)()

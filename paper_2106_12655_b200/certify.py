@@ -248,8 +248,7 @@ def device_step(ctx, xi, excl_keys, params, mode=None, timings=None):
             ctx.run_pipeline(excl_keys, xi, params.epsilon, params.max_passes, params.max_subsegments, mode)
         except _native.DiscretizeFailure as fail:
             raise_for_failure(fail, params)
-        pairs = ctx.get_pairs()
-        raw, lk, flags = ctx.get_results()
+        pairs, raw, lk, flags = ctx.result_views()   # pinned, valid until the next pipeline call
         if timings is not None:
             st = ctx.stage_times()
             timings["pls"] = timings.get("upload", 0.0) + 1e-3 * st["pls"]

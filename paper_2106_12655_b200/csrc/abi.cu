@@ -337,6 +337,21 @@ int lc_run_pipeline(lc_ctx *ctx, const uint64_t *excluded_keys, int64_t n_excl, 
         ctx->pipe.build_gauss_items();
         ctx->pipe.run_gauss(mode, 0, ctx->pipe.n_items, nullptr, nullptr, nullptr);
         ctx->pipe.reduce_pairs(nullptr);
+        ctx->pipe.download_results_pinned();
+    });
+}
+
+int lc_result_views(lc_ctx *ctx, void **pairs, void **raw, void **lk, void **flags, int64_t *n_pairs) {
+    return guarded(ctx, [&] {
+        Pipeline &p = ctx->pipe;
+        if (p.h_res_P < 0) throw Error(LC_ERR_STATE, "no pipeline results");
+        char *h = static_cast<char *>(p.h_res.ptr);
+        const size_t n = (size_t)p.h_res_P;
+        *pairs = h;
+        *raw = h + 8 * n;
+        *lk = h + 16 * n;
+        *flags = h + 24 * n;
+        *n_pairs = p.h_res_P;
     });
 }
 

@@ -67,6 +67,24 @@ struct DevBuf {
     template <class T> T *as() const { return static_cast<T *>(ptr); }
 };
 
+// Grow-only pinned host buffer (fast D2H of results; exposed to callers as views).
+struct PinnedBuf {
+    void *ptr = nullptr;
+    size_t bytes = 0;
+    void reserve(size_t n) {
+        if (n <= bytes) return;
+        if (ptr) cudaFreeHost(ptr);
+        const size_t want = n < 4096 ? 4096 : n + n / 4;
+        LC_CUDA(cudaHostAlloc(&ptr, want, cudaHostAllocDefault));
+        bytes = want;
+    }
+    void release() {
+        if (ptr) cudaFreeHost(ptr);
+        ptr = nullptr;
+        bytes = 0;
+    }
+};
+
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 }  // namespace lc

@@ -643,6 +643,24 @@ bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc,
         pre_loops_kernel<<<grid_for(L), 256, 0, s>>>(in.loop_min_diag, sc.paired.as<uint8_t>(), L, min_diam, ctr);
         LC_CHECK_LAUNCH();
     }
+    // Pass-1 small-pair detection is launched before the first sync (identity
+    // view: entry e == segment e, union boxes == loop boxes), so one read-back
+    // returns the pre-checks and the pass-1 mark count together.
+    const int nsm = 148;
+    sc.mark.reserve(sizeof(uint32_t) * (M > 0 ? M : 1), s);
+    sc.first_pair.reserve(sizeof(int32_t) * (M > 0 ? M : 1), s);
+    if (M > 0) {
+        LC_CUDA(cudaMemsetAsync(sc.mark.ptr, 0, sizeof(uint32_t) * M, s));
+        LC_CUDA(cudaMemsetAsync(sc.first_pair.ptr, 0x7f, sizeof(int32_t) * M, s));
+    }
+    const ActView view0{nullptr, in.seg_loop, in.t, in.t + 1, 2, in.seg_box, M > 0 ? M : 1, in.loff};
+    if (P > 0) {
+        const int64_t blocks = ceil_div(P, kBruteWarps) < nsm * 16 ? ceil_div(P, kBruteWarps) : nsm * 16;
+        brute_kernel<<<(unsigned)blocks, 32 * kBruteWarps, 0, s>>>(view0, in.loop_box, L, in.pairs, P,
+                                                                   sc.mark.as<uint32_t>(), sc.first_pair.as<int32_t>(),
+                                                                   &ctr->marked);
+        LC_CHECK_LAUNCH();
+    }
     const PreCounters pc = d2h<PreCounters>(sc.prectr.ptr, s);
     if (pc.zero_loop != INT_MAX) {   // ZeroLengthInput, first loop in order (:124-129)
         err->kind = DISC_ZERO_LENGTH;
@@ -700,7 +718,7 @@ bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc,
     // unpaired loops belong to no pair, so nothing marks them, and with no mark
     // at all the chords are the segment start points of every loop.
     n_act = M;
-    view = ActView{nullptr, in.seg_loop, in.t, in.t + 1, 2, in.seg_box, M > 0 ? M : 1, in.loff};
+    view = view0;
     bool is_identity = true;
     const double *ubox = in.loop_box;   // union boxes of the active subsegments per loop
     sc.ubox.reserve(sizeof(double) * 6 * (L > 0 ? L : 1), s);
@@ -708,18 +726,19 @@ bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc,
     int64_t n_done = 0;
     sc.bad_first.reserve(sizeof(int32_t) * (L > 0 ? L : 1), s);
     sc.sweep_off.reserve(sizeof(int64_t) * (P + 1), s);
-    const int nsm = 148;
     for (int pass = 0; pass < prm.max_passes; ++pass) {
         if (n_act == 0) break;
         out.passes = pass + 1;
-        sc.mark.reserve(sizeof(uint32_t) * n_act, s);
-        sc.first_pair.reserve(sizeof(int32_t) * n_act, s);
-        LC_CUDA(cudaMemsetAsync(sc.mark.ptr, 0, sizeof(uint32_t) * n_act, s));
-        LC_CUDA(cudaMemsetAsync(sc.first_pair.ptr, 0x7f, sizeof(int32_t) * n_act, s));
-        LC_CUDA(cudaMemsetAsync(&ctr->marked, 0, sizeof(unsigned long long), s));
         unsigned long long *marked_ctr = &ctr->marked;
+        if (pass > 0) {
+            sc.mark.reserve(sizeof(uint32_t) * n_act, s);
+            sc.first_pair.reserve(sizeof(int32_t) * n_act, s);
+            LC_CUDA(cudaMemsetAsync(sc.mark.ptr, 0, sizeof(uint32_t) * n_act, s));
+            LC_CUDA(cudaMemsetAsync(sc.first_pair.ptr, 0x7f, sizeof(int32_t) * n_act, s));
+            LC_CUDA(cudaMemsetAsync(marked_ctr, 0, sizeof(unsigned long long), s));
+        }
         if (P > 0) {
-            // small pairs: brute force in shared memory
+            // small pairs: brute force with union-box prefilter (pass 1 already launched above)
             const int64_t blocks = ceil_div(P, kBruteWarps) < nsm * 16 ? ceil_div(P, kBruteWarps) : nsm * 16;
             if (!is_identity) {
                 union_boxes_kernel<<<grid_for(L * 32), 256, 0, s>>>(view.box, view.bstride, view.off, L,
@@ -727,10 +746,12 @@ bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc,
                 LC_CHECK_LAUNCH();
                 ubox = sc.ubox.as<double>();
             }
-            brute_kernel<<<(unsigned)blocks, 32 * kBruteWarps, 0, s>>>(view, ubox, L, in.pairs, P,
-                                                                       sc.mark.as<uint32_t>(),
-                                                                       sc.first_pair.as<int32_t>(), marked_ctr);
-            LC_CHECK_LAUNCH();
+            if (pass > 0) {
+                brute_kernel<<<(unsigned)blocks, 32 * kBruteWarps, 0, s>>>(view, ubox, L, in.pairs, P,
+                                                                           sc.mark.as<uint32_t>(),
+                                                                           sc.first_pair.as<int32_t>(), marked_ctr);
+                LC_CHECK_LAUNCH();
+            }
             // large pairs: segmented sorts + sweep (pass 1: count known; later passes: recount)
             sc.counters.reserve(sizeof(int64_t) * (P + 1), s);
             if (pass > 0) {
@@ -776,7 +797,8 @@ bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc,
                 LC_CHECK_LAUNCH();
             }
         }
-        const int64_t marked = (int64_t)d2h<unsigned long long>(marked_ctr, s);
+        const int64_t marked = (pass == 0 && n_large == 0) ? (int64_t)pc.marked
+                                                           : (int64_t)d2h<unsigned long long>(marked_ctr, s);
         if (marked == 0 && out.splits == 0) {   // nothing was ever refined: every segment is a chord
             n_act = 0;
             break;

@@ -58,6 +58,7 @@ void Pipeline::release() {
                     &d.prectr};
     for (DevBuf *b : db) b->release(s);
     if (s) cudaStreamSynchronize(s);
+    h_res.release();
     for (auto &e : ev)
         if (e) cudaEventDestroy(e);
 }
@@ -280,6 +281,20 @@ void Pipeline::download_results(double *raw, int64_t *lk, uint8_t *flags) {
         if (flags) LC_CUDA(cudaMemcpyAsync(flags, d_flags.ptr, (size_t)P, cudaMemcpyDeviceToHost, s));
     }
     LC_CUDA(cudaStreamSynchronize(s));
+}
+
+void Pipeline::download_results_pinned() {
+    const size_t n = (size_t)(P > 0 ? P : 0);
+    h_res.reserve(n * (8 + 8 + 8 + 1) + 64);
+    char *h = static_cast<char *>(h_res.ptr);
+    if (n > 0) {
+        LC_CUDA(cudaMemcpyAsync(h, d_pairs.ptr, 8 * n, cudaMemcpyDeviceToHost, s));
+        LC_CUDA(cudaMemcpyAsync(h + 8 * n, d_raw.ptr, 8 * n, cudaMemcpyDeviceToHost, s));
+        LC_CUDA(cudaMemcpyAsync(h + 16 * n, d_lk.ptr, 8 * n, cudaMemcpyDeviceToHost, s));
+        LC_CUDA(cudaMemcpyAsync(h + 24 * n, d_flags.ptr, n, cudaMemcpyDeviceToHost, s));
+    }
+    LC_CUDA(cudaStreamSynchronize(s));
+    h_res_P = (int64_t)n;
 }
 
 void Pipeline::segment_pair_lambda(const double *quads, int64_t n, double *out) {

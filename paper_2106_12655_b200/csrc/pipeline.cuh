@@ -65,6 +65,10 @@ struct Pipeline {
                    cudaEvent_t ev1);
     void reduce_pairs(const double *partials_ext);
     void download_results(double *raw, int64_t *lk, uint8_t *flags);
+    // pairs | raw | lk | flags of the last reduce into pinned host memory (one sync)
+    void download_results_pinned();
+    PinnedBuf h_res;
+    int64_t h_res_P = -1;
     void segment_pair_lambda(const double *quads, int64_t n, double *out);
 
     float stage_ms(int e0, int e1);

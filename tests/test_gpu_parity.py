@@ -240,6 +240,22 @@ def test_edge_cases(gpu):
     assert raw.shape == (0,)
 
 
+@pytest.mark.parametrize("mode", MODES)
+def test_degenerate_shared_vertices_vs_oracle(gpu, oracle, mode):
+    """Coincident vertices (|r| = 0, w = 0): the phase fast path must fall back to the
+    exact per-pair evaluation and agree with the reference's atan2(+-0, +-0) semantics."""
+    ex, ey, ez = np.eye(3)
+    a = cases.circ(24, (0, 0, 0), ex, ey)
+    b = cases.circ(24, (1.0, 0, 0), ez, ex)
+    b[5] = a[0]                                  # a shared vertex
+    c = a.copy()
+    c[3] = c[4]                                  # duplicate vertex inside one loop (zero-length segment)
+    for x, y in ((a, b), (c, b), (a, a + 1e-300), (a, a)):
+        want = oracle.link_direct(x, y)
+        got = gpu.link_direct(x, y, mode)
+        assert (np.isnan(want) and np.isnan(got)) or abs(got - want) < RAW_TOL, (want, got)
+
+
 def test_env_mode_selection(monkeypatch):
     ex, ey, ez = np.eye(3)
     a = cases.circ(100, (0, 0, 0), ex, ey)
