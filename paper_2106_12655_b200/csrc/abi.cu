@@ -268,7 +268,7 @@ int lc_set_pairs(lc_ctx *ctx, const int32_t *pairs, int64_t P) {
 }
 
 static int run_discretize_abi(lc_ctx *ctx, double xi, double epsilon, int max_passes, int64_t max_subsegments,
-                              int64_t *n_vertices, int *passes) {
+                              int64_t *n_vertices, int *passes, bool defer_validation = false) {
     int rc = LC_OK;
     int g = guarded(ctx, [&] {
         DiscParams prm;
@@ -276,6 +276,7 @@ static int run_discretize_abi(lc_ctx *ctx, double xi, double epsilon, int max_pa
         prm.epsilon = epsilon;
         prm.max_passes = max_passes;
         prm.max_subsegments = max_subsegments;
+        prm.defer_validation = defer_validation;
         const bool ok = ctx->pipe.discretize(prm);
         if (passes) *passes = ctx->pipe.dout.passes;
         if (!ok) {
@@ -331,10 +332,16 @@ int lc_run_pipeline(lc_ctx *ctx, const uint64_t *excluded_keys, int64_t n_excl, 
     if (rc != LC_OK) return rc;
     int64_t nv = 0;
     int passes = 0;
-    rc = run_discretize_abi(ctx, xi, epsilon, max_passes, max_subsegments, &nv, &passes);
+    rc = run_discretize_abi(ctx, xi, epsilon, max_passes, max_subsegments, &nv, &passes, true);
     if (rc != LC_OK) return rc;
+    bool valid = true;
+    rc = guarded(ctx, [&] { valid = ctx->pipe.build_gauss_items_checked(); });
+    if (rc != LC_OK) return rc;
+    if (!valid) {   // deferred PolylineLoop validation failed (read back with n_items)
+        g_last_error = "discretization failed (see lc_discretize_error)";
+        return LC_ERR_VALIDATION;
+    }
     return guarded(ctx, [&] {
-        ctx->pipe.build_gauss_items();
         ctx->pipe.run_gauss(mode, 0, ctx->pipe.n_items, nullptr, nullptr, nullptr);
         ctx->pipe.reduce_pairs(nullptr);
         ctx->pipe.download_results_pinned();

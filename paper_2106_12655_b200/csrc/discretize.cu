@@ -572,6 +572,19 @@ __global__ void unpack_kernel(const double *__restrict__ X, const double *__rest
     aos[3 * o + 2] = Z[k] * inv;
 }
 
+// First invalid loop per class: err[0] over unpaired loops, err[1] over paired loops.
+__global__ void validate_loops2_kernel(const int64_t *__restrict__ off, int64_t L, const uint8_t *__restrict__ paired,
+                                       const unsigned *__restrict__ flags, int *__restrict__ err) {
+    const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (l >= L) return;
+    const int64_t n = off[l + 1] - off[l];
+    int kind = PL_OK;
+    if (n < 3) kind = PL_TOO_FEW;
+    else if (flags[l] & 1) kind = PL_NONFINITE;
+    else if (flags[l] & 2) kind = PL_ZERO_SEGMENT;
+    if (kind) atomicMin(err + (paired[l] ? 1 : 0), (int)(l * 4 + kind));
+}
+
 inline unsigned grid_for(int64_t n, int threads = 256) { return (unsigned)(n > 0 ? ceil_div(n, threads) : 1); }
 
 template <class T> T d2h(const void *p, cudaStream_t s) {
@@ -616,8 +629,14 @@ void unpack_polylines(const DiscOutput &out, int64_t L, const int *max_exp, doub
     LC_CHECK_LAUNCH();
 }
 
+bool validation_error(const int val_err[2], DiscError *err) {
+    return polyline_error(val_err[0], err) || polyline_error(val_err[1], err);
+}
+
 bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc, DiscOutput &out, DiscError *err,
                     cudaStream_t s) {
+    out.validation_pending = false;
+    out.d_val_err = nullptr;
     const int64_t L = in.L, M = in.M, P = in.P;
     const double min_diam = prm.epsilon * prm.xi;      // discretize.py:122
     const double poly_thr = kMachineEps * prm.xi;       // PolylineLoop(xi_hint=xi), geometry.py:338-340
@@ -667,8 +686,11 @@ bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc,
         err->loops = {pc.zero_loop};
         return false;
     }
-    // ---- (2) unpaired loops are control chords, validated before any pass (:131-142)
-    if (pc.n_unpaired > 0 && M > 0) {
+    // ---- (2) unpaired loops are control chords, validated before any pass (:131-142).
+    // Only a refinement pass can raise an error that must come after this check;
+    // without one, the check is folded into the final chord validation.
+    const bool unpaired_first = pc.n_unpaired > 0 && (pc.marked > 0 || pc.n_large > 0);
+    if (unpaired_first && M > 0) {
         sc.tmp_aos.reserve(sizeof(double) * 3 * M, s);
         write_unpaired_kernel<<<grid_for(M), 256, 0, s>>>(M, in.seg_loop, sc.paired.as<uint8_t>(), in.loff, in.coeffs,
                                                           in.t, nullptr, in.max_exp, nullptr, nullptr, nullptr,
@@ -935,9 +957,22 @@ bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc,
                                                          out.Z.as<double>(), sc.val_flags.as<unsigned>());
             LC_CHECK_LAUNCH();
         }
-        // unpaired loops were validated in (2): check paired loops (or all, when every loop is paired)
-        const int ve = finish_validation(sc, in.loff, L, 0, identity ? nullptr : sc.paired.as<uint8_t>(), 1, s);
-        return !polyline_error(ve, err);
+        // unpaired (control-chord) loops rank before paired ones (:131-142 vs :189-191)
+        sc.val_err2.reserve(2 * sizeof(int), s);
+        const int init2[2] = {INT_MAX, INT_MAX};
+        LC_CUDA(cudaMemcpyAsync(sc.val_err2.ptr, init2, sizeof init2, cudaMemcpyHostToDevice, s));
+        validate_loops2_kernel<<<grid_for(L), 256, 0, s>>>(in.loff, L, sc.paired.as<uint8_t>(),
+                                                           sc.val_flags.as<unsigned>(), sc.val_err2.as<int>());
+        LC_CHECK_LAUNCH();
+        out.d_val_err = sc.val_err2.as<int>();
+        if (prm.defer_validation) {
+            out.validation_pending = true;
+            return true;
+        }
+        int ve[2];
+        LC_CUDA(cudaMemcpyAsync(ve, sc.val_err2.ptr, sizeof ve, cudaMemcpyDeviceToHost, s));
+        LC_CUDA(cudaStreamSynchronize(s));
+        return !validation_error(ve, err);
     }
     // general path: done entries sorted by (seg, tlo) (the lexsort of :104)
     const int32_t *seg_sorted = sc.done_seg.as<int32_t>();

@@ -28,13 +28,14 @@ struct DiscParams {
     double epsilon = 2.220446049250313e-16;   // discretize.py:27 (MACHINE_EPS)
     int max_passes = 64;
     int64_t max_subsegments = int64_t(1) << 22;
+    bool defer_validation = false;   // leave the PolylineLoop check result on the device (DiscOutput)
 };
 
 struct DiscScratch {
     DevBuf paired, act_seg, act_loop, act_tlo, act_thi, act_off, nxt_seg, nxt_loop, nxt_tlo, nxt_thi, nxt_off,
         nxt_partner, box, nxt_box, skey[3], sperm[3], iota, pair_axis, sweep_off, mark, first_pair, mark_scan,
         done_seg, done_tlo, done_seg2, done_tlo2, sort_idx, sort_idx2, done_cnt, done_off, bad_first, counters,
-        cub_tmp, loop_err, val_flags, ucnt, tmp_aos, prectr, ubox, mark2, fp2;
+        cub_tmp, loop_err, val_flags, ucnt, tmp_aos, prectr, ubox, mark2, fp2, val_err2;
     int64_t cap_done = 0;
 };
 
@@ -60,7 +61,14 @@ struct DiscOutput {
     int64_t V = 0, Vc = 0;
     int passes = 0;
     int64_t splits = 0;
+    // defer_validation: d_val_err[0] / [1] = first invalid unpaired / paired loop
+    // (loop*4 + PolylineInvalid, INT_MAX if none); the caller reads it back.
+    bool validation_pending = false;
+    const int *d_val_err = nullptr;
 };
+
+// Map a (deferred) validation read-back onto *err; true if it holds an error.
+bool validation_error(const int val_err[2], DiscError *err);
 
 // Returns false and fills *err on a reference error (nothing else is thrown
 // for input-dependent failures).

@@ -497,7 +497,7 @@ size_t build_items_scan_bytes(int64_t P) {
 }
 
 int64_t build_items(const int32_t *d_pairs, int64_t P, const int64_t *d_voff, PairGeom *d_pg,
-                    int64_t *d_item_off, void *d_scan_tmp, size_t scan_tmp_bytes, cudaStream_t s) {
+                    int64_t *d_item_off, void *d_scan_tmp, size_t scan_tmp_bytes, cudaStream_t s, bool read_back) {
     if (P == 0) {
         LC_CUDA(cudaMemsetAsync(d_item_off, 0, sizeof(int64_t), s));
         return 0;
@@ -508,6 +508,7 @@ int64_t build_items(const int32_t *d_pairs, int64_t P, const int64_t *d_voff, Pa
     LC_CHECK_LAUNCH();
     size_t bytes = scan_tmp_bytes;
     LC_CUB(cub::DeviceScan::ExclusiveSum(d_scan_tmp, bytes, d_item_off, d_item_off, (int)(P + 1), s));
+    if (!read_back) return -1;   // caller reads item_off[P] together with other results
     int64_t total = 0;
     LC_CUDA(cudaMemcpyAsync(&total, d_item_off + P, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     LC_CUDA(cudaStreamSynchronize(s));

@@ -34,7 +34,8 @@ struct PairGeom {
 // Builds PairGeom[P] and item_off[P+1] (exclusive prefix of items per pair).
 // voff: closed-loop SoA vertex offsets (L+1). Returns total item count (syncs).
 int64_t build_items(const int32_t *d_pairs, int64_t P, const int64_t *d_voff, PairGeom *d_pg,
-                    int64_t *d_item_off, void *d_scan_tmp, size_t scan_tmp_bytes, cudaStream_t s);
+                    int64_t *d_item_off, void *d_scan_tmp, size_t scan_tmp_bytes, cudaStream_t s,
+                    bool read_back = true);
 size_t build_items_scan_bytes(int64_t P);
 
 // Evaluates items [item_begin, item_end) into partials[item] (absolute index).

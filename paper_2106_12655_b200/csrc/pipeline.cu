@@ -1,4 +1,5 @@
 // Pipeline stage orchestration on one device/stream (host side of the C-ABI).
+#include <climits>
 #include <cstring>
 #include <vector>
 
@@ -249,6 +250,36 @@ void Pipeline::build_gauss_items() {
     d_counter.reserve(sizeof(unsigned long long), s);
     n_items = build_items(d_pairs.as<int32_t>(), P, gvoff, d_pg.as<PairGeom>(), d_item_off.as<int64_t>(), d_scan.ptr,
                           d_scan.bytes, s);
+    finish_items();
+}
+
+bool Pipeline::build_gauss_items_checked() {
+    if (!polylines_ready) throw Error(LC_ERR_STATE, "no polylines staged");
+    d_pg.reserve(sizeof(PairGeom) * (size_t)(P > 0 ? P : 1), s);
+    d_item_off.reserve(sizeof(int64_t) * (size_t)(P + 1), s);
+    const size_t scan_bytes = build_items_scan_bytes(P > 0 ? P : 1);
+    d_scan.reserve(scan_bytes, s);
+    d_counter.reserve(sizeof(unsigned long long), s);
+    build_items(d_pairs.as<int32_t>(), P, gvoff, d_pg.as<PairGeom>(), d_item_off.as<int64_t>(), d_scan.ptr,
+                d_scan.bytes, s, false);
+    int ve[2] = {INT_MAX, INT_MAX};
+    n_items = 0;
+    LC_CUDA(cudaMemcpyAsync(&n_items, d_item_off.as<int64_t>() + P, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    if (dout.validation_pending && dout.d_val_err)
+        LC_CUDA(cudaMemcpyAsync(ve, dout.d_val_err, sizeof ve, cudaMemcpyDeviceToHost, s));
+    LC_CUDA(cudaStreamSynchronize(s));
+    if (dout.validation_pending) {
+        dout.validation_pending = false;
+        if (validation_error(ve, &derr)) {
+            polylines_ready = false;
+            return false;
+        }
+    }
+    finish_items();
+    return true;
+}
+
+void Pipeline::finish_items() {
     d_partials.reserve(sizeof(double) * (size_t)(n_items > 0 ? n_items : 1), s);
     d_item_pair.reserve(sizeof(int32_t) * (size_t)(n_items > 0 ? n_items : 1), s);
     launch_item_pairs(d_item_off.as<int64_t>(), P, n_items, d_item_pair.as<int32_t>(), s);

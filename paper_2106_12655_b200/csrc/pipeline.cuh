@@ -61,6 +61,9 @@ struct Pipeline {
     void upload_pairs(const int32_t *pairs, int64_t npairs);
     void download_pairs(int32_t *pairs);
     void build_gauss_items();
+    // build items and read back n_items together with a deferred discretize
+    // validation result (one sync); false + derr on a ValidationError
+    bool build_gauss_items_checked();
     void run_gauss(int mode, int64_t item_begin, int64_t item_end, double *partials_ext, cudaEvent_t ev0,
                    cudaEvent_t ev1);
     void reduce_pairs(const double *partials_ext);
@@ -75,6 +78,7 @@ struct Pipeline {
 
   private:
     void model_boxes();
+    void finish_items();
 };
 
 }  // namespace lc
