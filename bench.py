@@ -44,6 +44,12 @@ UNIT = "seg-pairs/s"
 # dynamic 2*DFMA + DMUL + DADD of the GAUSS_REF kernel measured with ncu
 # (profiles/r01/SUMMARY.md): 261.8 -> frozen at 262.
 F_PAIR = 262.0
+# FP64 FLOPs the phase kernel actually executes per segment pair (same ncu count,
+# GAUSS_PHASE): the hardware-side view of the roofline next to the algorithmic one.
+EXEC_FLOP_PAIR = {"phase": 78.5, "atan": 133.3, "ref": 260.3}
+# DRAM bytes (read + write) of one gauss_items_kernel launch from the committed
+# `ncu --set full` capture of this workload (profiles/r01/gauss_phase_kusari_raw.csv).
+NCU_TRAFFIC = {("kusari", "phase"): (23055616 + 58368, "profiles/r01/gauss_phase_kusari_raw.csv")}
 L2_FLUSH_BYTES = 512 << 20
 
 
@@ -188,8 +194,10 @@ def main():
 
     # ---- value: device-resident hot path ------------------------------------
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
-    coeffs, t, off = after.packed()
-    ctx.upload_model(coeffs, t, off)
+    from paper_2106_12655_b200.pls import upload
+    upload(after, ctx)                                  # what verify() uploads (compact polylines here)
+    poly = after.polyline_vertices()
+    h2d = sum(a.nbytes for a in (poly if poly is not None else after.packed()))
     ex = excluded_keys(())
     step_ms, gauss_ms, launches = [], [], []
     n_sp = None
@@ -213,6 +221,7 @@ def main():
             if n_sp is None:
                 _, voff = ctx.get_polylines()
                 n_sp = seg_pairs(pairs, voff)
+                n_closed = int(voff[-1]) + len(voff) - 1     # closed SoA vertices read by the kernel
     clocks = clk.result
     ms = statistics.mean(step_ms)
     if world > 1:
@@ -241,7 +250,6 @@ def main():
         tt = torch.tensor([e2e], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e = float(tt.item())
-    h2d = coeffs.nbytes + t.nbytes + off.nbytes
     d2h = pairs.nbytes + raw.nbytes + lk.nbytes + flags.nbytes
 
     if rank != 0:
@@ -261,8 +269,15 @@ def main():
                 "d2h_bytes_per_step": int(d2h), "report": {"status": report.status, "destroyed": report.destroyed,
                                                            "created": report.created, "changed": report.changed}},
         "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": None, "kernel": "gauss_items_kernel<PHASE>",
+                     "frac": achieved / peak,
+                     "traffic": NCU_TRAFFIC.get((args.workload, args.mode), (None, None))[0],
+                     "kernel": f"gauss_items_kernel<{args.mode.upper()}>",
                      "kernel_ms": gk, "f_pair": F_PAIR,
+                     "executed": {"flop_per_pair": EXEC_FLOP_PAIR[args.mode],
+                                  "tflops": EXEC_FLOP_PAIR[args.mode] * n_sp / (gk * 1e-3) / 1e12,
+                                  "frac": EXEC_FLOP_PAIR[args.mode] * n_sp / (gk * 1e-3) / peak},
+                     "algorithmic_bytes": 24 * n_closed,
+                     "traffic_source": NCU_TRAFFIC.get((args.workload, args.mode), (None, None))[1],
                      "peak_source": "FP64 DFMA-chain probe measured live on this GPU (MEASURED_PEAKS.json has no FP64)"},
         "stage_ms": ctx.stage_times(),
         "clocks": clocks,

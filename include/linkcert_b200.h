@@ -185,6 +185,9 @@ LC_API int lc_model_digest(const double *coeffs, const double *t, const int64_t 
 LC_API int lc_sha256_hex(const void *data, int64_t n, int force_portable, char *hex_out);
 /* CPython float.__repr__ of x into out (>= 32 bytes); returns the length. */
 LC_API int lc_float_repr(double x, char *out);
+/* Test hook: repr of n doubles, each followed by '\n', into out (cap >= 26 n);
+ * use_tochars selects the std::to_chars cross-check formatter.  Returns bytes. */
+LC_API int64_t lc_float_repr_many(const double *x, int64_t n, int use_tochars, char *out, int64_t cap);
 
 /* Kernel launches issued by the library so far, all contexts (own kernels
  * exactly; each CUB device-algorithm call counted once). */

@@ -80,6 +80,7 @@ SIGNATURES = {
     "lc_model_json_bound": (ctypes.c_int64, [_vp, ctypes.c_int64]),
     "lc_model_json": (ctypes.c_int64, [_vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, ctypes.c_int64]),
     "lc_float_repr": (ctypes.c_int, [ctypes.c_double, ctypes.c_char_p]),
+    "lc_float_repr_many": (ctypes.c_int64, [_vp, ctypes.c_int64, ctypes.c_int, _vp, ctypes.c_int64]),
     "lc_model_digest": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p]),
     "lc_sha256_hex": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p]),
     "lc_launch_count": (ctypes.c_longlong, []),
@@ -132,6 +133,14 @@ def float_repr(x):
     out = ctypes.create_string_buffer(40)
     n = load_library().lc_float_repr(float(x), out)
     return out.raw[:n].decode()
+
+
+def float_repr_many(xs, use_tochars=False):
+    """repr of every double in xs (test hook for the digest formatter)."""
+    xs = np.ascontiguousarray(xs, dtype=np.float64)
+    buf = np.empty(26 * len(xs) + 1, dtype=np.uint8)
+    n = load_library().lc_float_repr_many(_ptr(xs), len(xs), int(bool(use_tochars)), _ptr(buf), len(buf))
+    return buf[:n].tobytes().decode().split("\n")[:-1]
 
 # lc_discretize_error kinds
 DISC_OK = 0

@@ -29,6 +29,21 @@ NVCC_FLAGS = [
     "--expt-relaxed-constexpr",
 ]
 
+CXX = os.environ.get("CXX", "g++")
+CXX_FLAGS = ["-O3", "-std=c++17", "-g", "-fPIC", "-fvisibility=hidden", "-pthread"]
+
+
+def _fmt_include() -> str:
+    """Header-only fmt (Dragonbox shortest float digits) vendored with PyTorch."""
+    import importlib.util
+
+    spec = importlib.util.find_spec("torch")
+    for loc in (spec.submodule_search_locations or []) if spec else []:
+        inc = Path(loc) / "include"
+        if (inc / "fmt" / "format.h").exists():
+            return str(inc)
+    raise RuntimeError("fmt headers not found (expected under torch/include/fmt)")
+
 
 def _sources():
     return [CSRC / s for s in SOURCES if (CSRC / s).exists()]
@@ -53,7 +68,10 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     procs = []
     for src in _sources():
         obj = build_dir / (src.stem + ".o")
-        cmd = [NVCC, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)]
+        if src.suffix == ".cpp":     # host-only code: the host compiler directly
+            cmd = [CXX, *CXX_FLAGS, "-I", _fmt_include(), "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)]
+        else:
+            cmd = [NVCC, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))

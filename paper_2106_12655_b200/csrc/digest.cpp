@@ -5,7 +5,7 @@
 // compute_linking_matrix and verify (certify.py:163,188).
 //
 // Floats follow CPython's float.__repr__: shortest round-trip digits
-// (std::to_chars, Ryu), fixed notation when -4 < decpt <= 16 with ".0" for
+// (Dragonbox via fmt, checked against std::to_chars), fixed notation when -4 < decpt <= 16 with ".0" for
 // integral values, otherwise d[.ddd]e(+|-)XX with at least two exponent
 // digits.  Formatting runs on worker threads chunk by chunk while the calling
 // thread streams finished chunks, in order, through SHA-256 (SHA-NI when the
@@ -23,31 +23,18 @@
 #include <thread>
 #include <vector>
 
+#define FMT_HEADER_ONLY
+#include <fmt/format.h>
+
 #include "../../include/linkcert_b200.h"
 
 namespace {
 
 // ------------------------------------------------------------ float repr
 
-char *put_repr(char *p, double x) {
-    char buf[64];
-    auto r = std::to_chars(buf, buf + sizeof buf, x, std::chars_format::scientific);
-    const char *b = buf, *e = r.ptr;
-    if (*b == '-') *p++ = *b++;
-    char digits[32];
-    int nd = 0;
-    const char *q = b;
-    for (; q < e && *q != 'e'; ++q)
-        if (*q != '.') digits[nd++] = *q;
-    int exp10 = 0;
-    if (q < e) {
-        ++q;
-        const bool neg = *q == '-';
-        if (*q == '+' || *q == '-') ++q;
-        for (; q < e; ++q) exp10 = exp10 * 10 + (*q - '0');
-        if (neg) exp10 = -exp10;
-    }
-    while (nd > 1 && digits[nd - 1] == '0') --nd;
+// Layout of a shortest digit string d1 d2 ... dnd x 10^(exp10 - nd + 1) in
+// float.__repr__ style (Objects/floatobject.c float_repr -> 'r' format).
+char *put_digits(char *p, const char *digits, int nd, int exp10) {
     const int decpt = exp10 + 1;
     if (decpt <= -4 || decpt > 16) {
         *p++ = digits[0];
@@ -85,6 +72,102 @@ char *put_repr(char *p, double x) {
         p += nd - decpt;
     }
     return p;
+}
+
+// Non-finite values and the cross-check path: std::to_chars (Ryu) shortest
+// scientific digits, re-laid out.
+char *put_repr_tochars(char *p, double x) {
+    char buf[64];
+    auto r = std::to_chars(buf, buf + sizeof buf, x, std::chars_format::scientific);
+    const char *b = buf, *e = r.ptr;
+    if (*b == '-') *p++ = *b++;
+    if (!std::isfinite(x)) {
+        std::memcpy(p, b, (size_t)(e - b));
+        return p + (e - b);
+    }
+    char digits[32];
+    int nd = 0;
+    const char *q = b;
+    for (; q < e && *q != 'e'; ++q)
+        if (*q != '.') digits[nd++] = *q;
+    int exp10 = 0;
+    if (q < e) {
+        ++q;
+        const bool neg = *q == '-';
+        if (*q == '+' || *q == '-') ++q;
+        for (; q < e; ++q) exp10 = exp10 * 10 + (*q - '0');
+        if (neg) exp10 = -exp10;
+    }
+    while (nd > 1 && digits[nd - 1] == '0') --nd;
+    return put_digits(p, digits, nd, exp10);
+}
+
+const char kPairs[201] =
+    "0001020304050607080910111213141516171819202122232425262728293031323334353637383940414243444546474849"
+    "5051525354555657585960616263646566676869707172737475767778798081828384858687888990919293949596979899";
+
+inline void put8(char *out, uint32_t v) {   // exactly 8 digits, leading zeros kept
+    const uint32_t hi = v / 10000, lo = v % 10000;
+    std::memcpy(out, kPairs + 2 * (hi / 100), 2);
+    std::memcpy(out + 2, kPairs + 2 * (hi % 100), 2);
+    std::memcpy(out + 4, kPairs + 2 * (lo / 100), 2);
+    std::memcpy(out + 6, kPairs + 2 * (lo % 100), 2);
+}
+
+constexpr uint64_t kPow10[20] = {1ull,
+                                 10ull,
+                                 100ull,
+                                 1000ull,
+                                 10000ull,
+                                 100000ull,
+                                 1000000ull,
+                                 10000000ull,
+                                 100000000ull,
+                                 1000000000ull,
+                                 10000000000ull,
+                                 100000000000ull,
+                                 1000000000000ull,
+                                 10000000000000ull,
+                                 100000000000000ull,
+                                 1000000000000000ull,
+                                 10000000000000000ull,
+                                 100000000000000000ull,
+                                 1000000000000000000ull,
+                                 10000000000000000000ull};
+
+// Decimal digits of 1 <= n < 10^17 (a double's shortest significand), most
+// significant first, via independent 8-digit halves; returns the count.
+inline int u64_digits(uint64_t n, char *out) {
+    const int bits = 64 - __builtin_clzll(n);
+    int nd = (bits * 1233) >> 12;          // floor(log10(2^bits)) approximation
+    nd += n >= kPow10[nd];
+    char buf[40];
+    const uint64_t top = n / 10000000000000000ull;   // digit 17 (0 or 1..9)
+    const uint64_t rest = n % 10000000000000000ull;
+    buf[0] = char('0' + top);
+    put8(buf + 1, (uint32_t)(rest / 100000000u));
+    put8(buf + 9, (uint32_t)(rest % 100000000u));
+    std::memcpy(out, buf + 17 - nd, 17);   // out has >= 17 bytes
+    return nd;
+}
+
+// float.__repr__: the shortest digit string that rounds back to x, the one
+// closest to x among those (David Gay's mode 0, which CPython uses).  The
+// shortest-closest decimal comes from fmt's Dragonbox (header-only, PyTorch's
+// vendored fmt), which implements exactly that selection.
+char *put_repr(char *p, double x) {
+    if (!std::isfinite(x)) return put_repr_tochars(p, x);
+    if (std::signbit(x)) *p++ = '-';
+    if (x == 0.0) {
+        std::memcpy(p, "0.0", 3);
+        return p + 3;
+    }
+    const auto d = fmt::detail::dragonbox::to_decimal(std::fabs(x));
+    char digits[24];
+    int nd = u64_digits(d.significand, digits);
+    int exp10 = d.exponent + nd - 1;
+    while (nd > 1 && digits[nd - 1] == '0') --nd;
+    return put_digits(p, digits, nd, exp10);
 }
 
 inline char *put(char *p, const char *s) {
@@ -491,6 +574,16 @@ LC_API int lc_float_repr(double x, char *out) {
     char *e = put_repr(out, x);
     *e = 0;
     return (int)(e - out);
+}
+
+LC_API int64_t lc_float_repr_many(const double *x, int64_t n, int use_tochars, char *out, int64_t cap) {
+    if (cap < 26 * n) return -1;
+    char *p = out;
+    for (int64_t k = 0; k < n; ++k) {
+        p = use_tochars ? put_repr_tochars(p, x[k]) : put_repr(p, x[k]);
+        *p++ = '\n';
+    }
+    return (int64_t)(p - out);
 }
 
 }  // extern "C"

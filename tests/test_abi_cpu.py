@@ -76,6 +76,25 @@ def test_float_repr_matches_cpython(lib):
     assert not bad, bad[:5]
 
 
+def test_float_repr_bulk_fuzz(lib):
+    """Dragonbox digest formatter vs CPython repr over all double classes (and
+    the std::to_chars cross-check formatter on the same values)."""
+    rng = np.random.default_rng(11)
+    n = 40000
+    xs = np.concatenate([
+        rng.integers(0, 0x7FF0000000000000, n, dtype=np.int64).view(np.float64),      # any finite bit pattern
+        np.ldexp(1.0, rng.integers(-1074, 1024, n)),                                   # shorter-interval case
+        np.ldexp(1.0 + rng.integers(0, 4, n) * 2.0 ** -52, rng.integers(-1074, 1023, n)),
+        rng.integers(-2 ** 62, 2 ** 62, n).astype(np.float64),
+        rng.integers(1, 1 << 52, n, dtype=np.int64).view(np.float64),                 # subnormals
+        np.round(rng.random(n) * 10.0 ** rng.integers(0, 17, n)) / 10.0 ** rng.integers(0, 20, n),
+    ])
+    xs *= np.where(rng.random(len(xs)) < 0.5, -1.0, 1.0)
+    truth = [repr(x) for x in xs.tolist()]
+    assert _native.float_repr_many(xs) == truth
+    assert _native.float_repr_many(xs, use_tochars=True) == truth
+
+
 @pytest.mark.parametrize("n", [0, 1, 55, 56, 57, 63, 64, 65, 119, 120, 128, 1000, 100003])
 def test_sha256_both_paths(lib, n):
     import hashlib
