@@ -11,6 +11,9 @@
 // thread streams finished chunks, in order, through SHA-256 (SHA-NI when the
 // CPU has it), so the digest costs ~max(format / threads, hash).
 #include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <charconv>
 #include <cmath>
 #include <condition_variable>
@@ -423,12 +426,20 @@ void pool_reserve(size_t n) {
     }
 }
 
+bool all_finite(const double *a, int64_t n) {
+    for (int64_t k = 0; k < n; ++k)
+        if (!std::isfinite(a[k])) return false;
+    return true;
+}
+
 struct Job {
     const double *coeffs, *t;
     const int64_t *off;
     const uint8_t *closed;
     std::vector<Chunk> chunks;
     std::atomic<int64_t> next{0};
+    bool check_finite = false;           // digest: validate the chunk's coefficients in the worker
+    std::atomic<bool> nonfinite{false};
     std::mutex mu;
     std::condition_variable cv;
 
@@ -440,6 +451,8 @@ struct Job {
             poly[l - c.l0] = loop_is_polyline(coeffs + 12 * off[l], t + 2 * off[l], m);
             bound += loop_bound(m, poly[l - c.l0]) + 1;
         }
+        if (check_finite && !all_finite(coeffs + 12 * off[c.l0], 12 * (off[c.l1] - off[c.l0])))
+            nonfinite.store(true);
         c.data = pool_buffer((size_t)(&c - chunks.data()), bound);
         char *p = c.data;
         for (int64_t l = c.l0; l < c.l1; ++l) {
@@ -469,12 +482,6 @@ struct Job {
         cv.wait(g, [&] { return c.ready.load(std::memory_order_acquire); });
     }
 };
-
-bool all_finite(const double *a, int64_t n) {
-    for (int64_t k = 0; k < n; ++k)
-        if (!std::isfinite(a[k])) return false;
-    return true;
-}
 
 // Split loops into chunks of ~target segments each.
 void make_chunks(Job &job, int64_t L, int64_t M, int64_t target) {
@@ -539,9 +546,15 @@ LC_API int64_t lc_model_json(const double *coeffs, const double *t, const int64_
 
 LC_API int lc_model_digest(const double *coeffs, const double *t, const int64_t *loop_off, const uint8_t *closed,
                            int64_t L, int nthreads, char *hex_out) {
+    static const bool stats = std::getenv("LC_DIGEST_STATS") != nullptr;
+    using clk = std::chrono::steady_clock;
+    const auto ms = [](clk::time_point a, clk::time_point b) {
+        return std::chrono::duration<double, std::milli>(b - a).count();
+    };
+    const auto t_begin = clk::now();
     const int64_t M = L > 0 ? loop_off[L] : 0;
-    if (!all_finite(coeffs, 12 * M)) return -1;
     Job job{coeffs, t, loop_off, closed};
+    job.check_finite = true;
     std::lock_guard<std::mutex> pool_lock(g_pool_mu);
     make_chunks(job, L, M, 4096);
     pool_reserve(job.chunks.size());
@@ -549,14 +562,33 @@ LC_API int lc_model_digest(const double *coeffs, const double *t, const int64_t 
     std::vector<std::thread> th;
     // the calling thread hashes: nt - 1 formatting workers keep it on its own core
     for (int k = 0; k < (nt > 1 ? nt - 1 : 1); ++k) th.emplace_back([&] { job.worker(); });
+    const auto t_spawned = clk::now();
     Sha256 h;
     h.update("{\"loops\":[", 10);
+    double t_wait = 0.0, t_hash = 0.0;
     for (auto &c : job.chunks) {
-        job.wait(c);
-        h.update(c.data, c.size);
+        if (stats) {
+            const auto t0 = clk::now();
+            job.wait(c);
+            const auto t1 = clk::now();
+            h.update(c.data, c.size);
+            t_wait += ms(t0, t1);
+            t_hash += ms(t1, clk::now());
+        } else {
+            job.wait(c);
+            h.update(c.data, c.size);
+        }
     }
     h.update("]}", 2);
+    const auto t_hashed = clk::now();
     for (auto &x : th) x.join();
+    const auto t_joined = clk::now();
+    if (stats)
+        std::fprintf(stderr,
+                     "lc_model_digest: threads %d chunks %zu setup %.2f wait %.2f hash %.2f join %.2f total %.2f ms\n",
+                     nt, job.chunks.size(), ms(t_begin, t_spawned), t_wait, t_hash, ms(t_hashed, t_joined),
+                     ms(t_begin, t_joined));
+    if (job.nonfinite.load()) return -1;
     h.hex(hex_out);
     return 0;
 }
