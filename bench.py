@@ -263,7 +263,7 @@ def main():
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": desc, "seg_pairs_per_step": n_sp, "pairs": int(len(pairs)),
-                   "gauss_mode": args.mode, "l2": f"flushed ({L2_FLUSH_BYTES >> 20} MiB write) between steps",
+                   "gauss_mode": args.mode, "device_path": ["staged", "fused", "fused (CUDA graph replay)"][ctx.last_run_fused()], "l2": f"flushed ({L2_FLUSH_BYTES >> 20} MiB write) between steps",
                    "parallelism": f"items sharded over {world} GPU(s), partials all-gathered" if world > 1 else "1 GPU"},
         "e2e": {"value": n_sp / (e2e * 1e-3), "unit": UNIT, "verify_ms": e2e, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "report": {"status": report.status, "destroyed": report.destroyed,

@@ -155,7 +155,10 @@ LC_API int lc_prepare_gauss(lc_ctx *ctx, int64_t *n_items);
 LC_API int lc_evaluate_staged(lc_ctx *ctx, int mode, double *raw, int64_t *lk, uint8_t *flags);
 /* Whole device path on the resident model: PLS -> discretize -> items ->
  * Gauss sum -> rounding (certify._prepare + _evaluate_pairs, certify.py:108-138).
- * Results stay on the device; lc_get_pairs / lc_get_results copy them out. */
+ * Results stay on the device; lc_get_pairs / lc_get_results copy them out,
+ * lc_result_views exposes them in pinned memory.  Runs the fused single-sync
+ * path first (no-refinement models) and the staged path otherwise;
+ * LINKCERT_FUSED=0 in the environment forces the staged path. */
 LC_API int lc_run_pipeline(lc_ctx *ctx, const uint64_t *excluded_keys, int64_t n_excl, double xi,
                            double epsilon, int max_passes, int64_t max_subsegments, int mode,
                            int64_t *n_pairs);
@@ -164,6 +167,9 @@ LC_API int lc_get_results(lc_ctx *ctx, double *raw, int64_t *lk, uint8_t *flags)
  * memory: pairs int32 (P,2), raw f64 (P), lk int64 (P), flags u8 (P).  Valid
  * until the next pipeline call on this context. */
 LC_API int lc_result_views(lc_ctx *ctx, void **pairs, void **raw, void **lk, void **flags, int64_t *n_pairs);
+/* Path of the last lc_run_pipeline: 0 staged, 1 fused, 2 fused replayed from
+ * the captured CUDA graph (same shape as the previous run, no reallocation). */
+LC_API int lc_last_run_fused(lc_ctx *ctx);
 /* Device times (ms) of the last pipeline: [PLS, discretize, Gauss kernel, reduce]. */
 LC_API int lc_stage_times(lc_ctx *ctx, float *ms);
 

@@ -80,6 +80,7 @@ SIGNATURES = {
     "lc_model_json_bound": (ctypes.c_int64, [_vp, ctypes.c_int64]),
     "lc_model_json": (ctypes.c_int64, [_vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, ctypes.c_int64]),
     "lc_float_repr": (ctypes.c_int, [ctypes.c_double, ctypes.c_char_p]),
+    "lc_last_run_fused": (ctypes.c_int, [_vp]),
     "lc_float_repr_many": (ctypes.c_int64, [_vp, ctypes.c_int64, ctypes.c_int, _vp, ctypes.c_int64]),
     "lc_model_digest": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p]),
     "lc_sha256_hex": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p]),
@@ -435,6 +436,11 @@ class Context:
         with self.lock:
             _check(self.lib.lc_get_results(self.handle, _ptr(raw), _ptr(lk), _ptr(flags)))
         return raw, lk, flags
+
+    def last_run_fused(self):
+        """Path of the last run_pipeline: 0 staged, 1 fused, 2 fused graph replay."""
+        with self.lock:
+            return int(self.lib.lc_last_run_fused(self.handle))
 
     def result_views(self):
         """(pairs (P,2) int32, raw, lk, flags) views into the library's pinned result

@@ -27,6 +27,7 @@ struct lc_ctx {
     Pipeline pipe;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     float last_gauss_ms = 0.f;
+    int last_fused = 0;   // last lc_run_pipeline: 0 staged, 1 fused, 2 fused replayed as a CUDA graph
     DevBuf tb_coeffs, tb_t, tb_box, tb_loop, tb_off, tb_flag;   // lc_tight_boxes scratch
 };
 
@@ -214,7 +215,7 @@ int lc_tight_boxes(lc_ctx *ctx, const double *coeffs, const double *t, int64_t m
         LC_CUDA(cudaMemcpyAsync(ctx->tb_coeffs.ptr, coeffs, sizeof(double) * 12 * m, cudaMemcpyHostToDevice, s));
         LC_CUDA(cudaMemcpyAsync(ctx->tb_t.ptr, t, sizeof(double) * 2 * m, cudaMemcpyHostToDevice, s));
         LC_CUDA(cudaMemcpyAsync(ctx->tb_off.ptr, off, sizeof off, cudaMemcpyHostToDevice, s));
-        launch_seg_boxes(ctx->tb_coeffs.as<double>(), ctx->tb_t.as<double>(), ctx->tb_off.as<int64_t>(), 1, m,
+        launch_seg_boxes(ctx->tb_coeffs.as<double>(), ctx->tb_t.as<double>(), nullptr, ctx->tb_off.as<int64_t>(), 1, m,
                          ctx->tb_box.as<double>(), ctx->tb_loop.as<int32_t>(), nullptr, nullptr, s);
         std::vector<double> b((size_t)6 * m);
         LC_CUDA(cudaMemcpyAsync(b.data(), ctx->tb_box.ptr, sizeof(double) * 6 * m, cudaMemcpyDeviceToHost, s));
@@ -247,13 +248,17 @@ int lc_loop_boxes(lc_ctx *ctx, double *lo, double *hi) {
     return guarded(ctx, [&] { ctx->pipe.download_loop_boxes(lo, hi); });
 }
 
-int lc_potential_link_search(lc_ctx *ctx, const uint64_t *excluded_keys, int64_t n_excl, int64_t *n_pairs) {
+static int pls_abi(lc_ctx *ctx, const uint64_t *excluded_keys, int64_t n_excl, int64_t *n_pairs, bool in_run) {
     return guarded(ctx, [&] {
         if (n_excl < 0 || (n_excl > 0 && !excluded_keys)) throw Error(LC_ERR_ARG, "bad excluded keys");
         for (int64_t k = 1; k < n_excl; ++k)
             if (excluded_keys[k] <= excluded_keys[k - 1]) throw Error(LC_ERR_ARG, "excluded keys must be sorted unique");
-        *n_pairs = ctx->pipe.potential_link_search(excluded_keys, n_excl);
+        *n_pairs = ctx->pipe.potential_link_search(excluded_keys, n_excl, in_run);
     });
+}
+
+int lc_potential_link_search(lc_ctx *ctx, const uint64_t *excluded_keys, int64_t n_excl, int64_t *n_pairs) {
+    return pls_abi(ctx, excluded_keys, n_excl, n_pairs, false);
 }
 
 int lc_get_pairs(lc_ctx *ctx, int32_t *pairs) {
@@ -328,7 +333,43 @@ int lc_evaluate_staged(lc_ctx *ctx, int mode, double *raw, int64_t *lk, uint8_t 
 
 int lc_run_pipeline(lc_ctx *ctx, const uint64_t *excluded_keys, int64_t n_excl, double xi, double epsilon,
                     int max_passes, int64_t max_subsegments, int mode, int64_t *n_pairs) {
-    int rc = lc_potential_link_search(ctx, excluded_keys, n_excl, n_pairs);
+    // Fused single-sync run first (LINKCERT_FUSED=0 disables it); it reports
+    // FAST_FALLBACK for the models it does not cover (refinement passes, the
+    // sweep path, PLS row overflow) and the staged pipeline below runs them.
+    const char *fz = getenv("LINKCERT_FUSED");
+    ctx->last_fused = 0;
+    ctx->pipe.derived_in_run = false;
+    const int gd = guarded(ctx, [&] {
+        if (n_excl < 0 || (n_excl > 0 && !excluded_keys)) throw Error(LC_ERR_ARG, "bad excluded keys");
+        for (int64_t k = 1; k < n_excl; ++k)
+            if (excluded_keys[k] <= excluded_keys[k - 1]) throw Error(LC_ERR_ARG, "excluded keys must be sorted unique");
+    });
+    if (gd != LC_OK) return gd;
+    if (!(fz && fz[0] == '0')) {
+        int fr = FAST_FALLBACK;
+        const int g = guarded(ctx, [&] {
+            DiscParams prm;
+            prm.xi = xi;
+            prm.epsilon = epsilon;
+            prm.max_passes = max_passes;
+            prm.max_subsegments = max_subsegments;
+            fr = ctx->pipe.run_fast(excluded_keys, n_excl, prm, mode);
+            if (n_pairs) *n_pairs = ctx->pipe.P;
+        });
+        if (g != LC_OK) return g;
+        ctx->last_fused = fr == FAST_FALLBACK ? 0 : (ctx->pipe.last_fast_graph ? 2 : 1);
+        if (fr == FAST_OK) return LC_OK;
+        if (fr == FAST_INVALID) {
+            g_last_error = "discretization failed (see lc_discretize_error)";
+            return LC_ERR_VALIDATION;
+        }
+    }
+    // staged path: derive the boxes unless the fused attempt just did
+    if (!ctx->pipe.derived_in_run) {
+        const int g2 = guarded(ctx, [&] { ctx->pipe.derive(); });
+        if (g2 != LC_OK) return g2;
+    }
+    int rc = pls_abi(ctx, excluded_keys, n_excl, n_pairs, true);
     if (rc != LC_OK) return rc;
     int64_t nv = 0;
     int passes = 0;
@@ -352,12 +393,10 @@ int lc_result_views(lc_ctx *ctx, void **pairs, void **raw, void **lk, void **fla
     return guarded(ctx, [&] {
         Pipeline &p = ctx->pipe;
         if (p.h_res_P < 0) throw Error(LC_ERR_STATE, "no pipeline results");
-        char *h = static_cast<char *>(p.h_res.ptr);
-        const size_t n = (size_t)p.h_res_P;
-        *pairs = h;
-        *raw = h + 8 * n;
-        *lk = h + 16 * n;
-        *flags = h + 24 * n;
+        *pairs = p.res_pairs;
+        *raw = p.res_raw;
+        *lk = p.res_lk;
+        *flags = p.res_flags;
         *n_pairs = p.h_res_P;
     });
 }
@@ -375,6 +414,8 @@ int lc_stage_times(lc_ctx *ctx, float *ms) {
         ms[3] = p.stage_ms(EV_GAUSS1, EV_END);
     });
 }
+
+int lc_last_run_fused(lc_ctx *ctx) { return ctx ? ctx->last_fused : 0; }
 
 long long lc_launch_count(void) { return launch_counter().load(); }
 

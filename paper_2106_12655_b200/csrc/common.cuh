@@ -48,18 +48,27 @@ inline std::atomic<long long> &launch_counter() {
         ::lc::check_cuda((x), #x, __FILE__, __LINE__);                               \
     } while (0)
 
+// Bumped by every (re)allocation of a DevBuf / PinnedBuf: a captured CUDA
+// graph bakes buffer addresses in, so it is reused only while this is unchanged.
+inline std::atomic<unsigned long long> &alloc_generation() {
+    static std::atomic<unsigned long long> g{0};
+    return g;
+}
+
 // Grow-only stream-ordered device buffer.
 struct DevBuf {
     void *ptr = nullptr;
     size_t bytes = 0;
     void reserve(size_t n, cudaStream_t s) {
         if (n <= bytes) return;
+        alloc_generation().fetch_add(1);
         if (ptr) LC_CUDA(cudaFreeAsync(ptr, s));
         size_t want = n < 256 ? 256 : n + n / 4;
         LC_CUDA(cudaMallocAsync(&ptr, want, s));
         bytes = want;
     }
     void release(cudaStream_t s) {
+        if (ptr) alloc_generation().fetch_add(1);
         if (ptr) cudaFreeAsync(ptr, s);
         ptr = nullptr;
         bytes = 0;
@@ -73,12 +82,14 @@ struct PinnedBuf {
     size_t bytes = 0;
     void reserve(size_t n) {
         if (n <= bytes) return;
+        alloc_generation().fetch_add(1);
         if (ptr) cudaFreeHost(ptr);
         const size_t want = n < 4096 ? 4096 : n + n / 4;
         LC_CUDA(cudaHostAlloc(&ptr, want, cudaHostAllocDefault));
         bytes = want;
     }
     void release() {
+        if (ptr) alloc_generation().fetch_add(1);
         if (ptr) cudaFreeHost(ptr);
         ptr = nullptr;
         bytes = 0;

@@ -43,15 +43,6 @@ constexpr int64_t kBruteLimit = 16384;         // bvh.py:224 BRUTE_FORCE_LIMIT
 constexpr int kBruteMaxSide = 256;             // shared-memory staging of loop j's boxes
 constexpr int kBruteWarps = 4;
 
-struct PreCounters {
-    int zero_loop;     // first loop with a zero-length segment box (INT_MAX: none)
-    int n_unpaired;
-    int n_large;       // pairs handled by the sweep path
-    int pad;
-    unsigned long long marked;
-    int err_loop;
-    int pad2;
-};
 
 // View of the active subsegment list: either the segment arrays themselves
 // (identity, pass 1 with every loop paired) or materialized SoA arrays.
@@ -86,16 +77,28 @@ __device__ __forceinline__ int64_t upper_index(const int64_t *__restrict__ off, 
 
 __device__ __forceinline__ void mark_entry(uint32_t *__restrict__ mark, int32_t *__restrict__ first_pair, int64_t e,
                                            int32_t p, unsigned long long *__restrict__ marked) {
+    if (!mark) {   // fused fast path: only "was anything marked" matters
+        atomicAdd(marked, 1ULL);
+        return;
+    }
     if (atomicOr(mark + e, 1u) == 0u) atomicAdd(marked, 1ULL);
     atomicMin(first_pair + e, p);
 }
 
 // ---------------------------------------------------------------- pre-pass
 
-__global__ void pre_pairs_kernel(const int32_t *__restrict__ pairs, int64_t P, const int64_t *__restrict__ loff,
-                                 const double *__restrict__ lbox, int64_t L, uint8_t *__restrict__ paired,
-                                 int8_t *__restrict__ axis, PreCounters *__restrict__ ctr) {
+__global__ void fast_init_kernel(PreCounters *__restrict__ ctr, int *__restrict__ val_err) {
+    *ctr = PreCounters{INT_MAX, 0, 0, 0, 0, INT_MAX, 0};
+    val_err[0] = INT_MAX;
+    val_err[1] = INT_MAX;
+}
+
+__global__ void pre_pairs_kernel(const int32_t *__restrict__ pairs, int64_t P, const int64_t *__restrict__ dP,
+                                 const int64_t *__restrict__ loff, const double *__restrict__ lbox, int64_t L,
+                                 uint8_t *__restrict__ paired, int8_t *__restrict__ axis,
+                                 PreCounters *__restrict__ ctr) {
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (dP && *dP < P) P = *dP;   // fused path: P on the device, grid sized by its capacity
     if (p >= P) return;
     const int i = pairs[2 * p], j = pairs[2 * p + 1];
     paired[i] = 1;
@@ -131,14 +134,25 @@ __device__ __forceinline__ bool box_overlap(const double *__restrict__ b, int64_
              lo[2] > b[5 * stride + e] || b[2 * stride + e] > hi[2]);
 }
 
+__device__ __forceinline__ bool box_overlap_f(const float *__restrict__ b, int64_t stride, int64_t e,
+                                              const float lo[3], const float hi[3]) {
+    return !(lo[0] > b[3 * stride + e] || b[e] > hi[0] || lo[1] > b[4 * stride + e] || b[stride + e] > hi[1] ||
+             lo[2] > b[5 * stride + e] || b[2 * stride + e] > hi[2]);
+}
+
 // Warp-wide compaction of the entries [b, b+n) whose box overlaps [lo, hi]
-// into list[]; returns the count (all lanes).
-__device__ __forceinline__ int filter_entries(const double *__restrict__ box, int64_t stride, int64_t b, int64_t n,
-                                              const double lo[3], const double hi[3], int32_t *list, int lane) {
+// into list[]; returns the count (all lanes).  fbox: test the outward-rounded
+// float boxes against [flo, fhi] (outward too) instead — a superset of the
+// exact hits, which is all a prefilter needs (half the bytes).
+__device__ __forceinline__ int filter_entries(const double *__restrict__ box, const float *__restrict__ fbox,
+                                              int64_t stride, int64_t b, int64_t n, const double lo[3],
+                                              const double hi[3], const float flo[3], const float fhi[3],
+                                              int32_t *list, int lane) {
     int cnt = 0;
     for (int64_t k0 = 0; k0 < n; k0 += 32) {
         const int64_t k = k0 + lane;
-        const bool in = k < n && box_overlap(box, stride, b + k, lo, hi);
+        const bool in = k < n && (fbox ? box_overlap_f(fbox, stride, b + k, flo, fhi)
+                                       : box_overlap(box, stride, b + k, lo, hi));
         const unsigned bal = __ballot_sync(0xffffffffu, in);
         if (in) list[cnt + __popc(bal & ((1u << lane) - 1u))] = (int32_t)(b + k);
         cnt += __popc(bal);
@@ -152,11 +166,14 @@ __device__ __forceinline__ int filter_entries(const double *__restrict__ box, in
 // versa), so both sides are first filtered against the other loop's union
 // box; the (usually tiny) filtered lists are then tested exhaustively.
 __global__ void __launch_bounds__(32 * kBruteWarps) brute_kernel(ActView v, const double *__restrict__ ubox,
+                                                                 const float *__restrict__ fbox,
                                                                  int64_t L, const int32_t *__restrict__ pairs,
-                                                                 int64_t P, uint32_t *__restrict__ mark,
+                                                                 int64_t P, const int64_t *__restrict__ dP,
+                                                                 uint32_t *__restrict__ mark,
                                                                  int32_t *__restrict__ first_pair,
                                                                  unsigned long long *__restrict__ marked) {
     __shared__ int32_t lists[kBruteWarps][2][kBruteMaxSide];
+    if (dP && *dP < P) P = *dP;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t nw = (int64_t)gridDim.x * kBruteWarps;
     for (int64_t p = blockIdx.x * (int64_t)kBruteWarps + w; p < P; p += nw) {
@@ -165,19 +182,33 @@ __global__ void __launch_bounds__(32 * kBruteWarps) brute_kernel(ActView v, cons
         const int64_t bj = v.off[j], nj = v.off[j + 1] - bj;
         if (ni == 0 || nj == 0 || !brute_pair(ni, nj)) continue;
         double ilo[3], ihi[3], jlo[3], jhi[3];
+        float filo[3], fihi[3], fjlo[3], fjhi[3];
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
             ilo[d] = ubox[d * L + i];
             ihi[d] = ubox[(3 + d) * L + i];
             jlo[d] = ubox[d * L + j];
             jhi[d] = ubox[(3 + d) * L + j];
+            filo[d] = __double2float_rd(ilo[d]);
+            fihi[d] = __double2float_ru(ihi[d]);
+            fjlo[d] = __double2float_rd(jlo[d]);
+            fjhi[d] = __double2float_ru(jhi[d]);
         }
         int32_t *si = lists[w][0], *tj = lists[w][1];
-        const int ns = filter_entries(v.box, v.bstride, bi, ni, jlo, jhi, si, lane);
-        const int nt = ns ? filter_entries(v.box, v.bstride, bj, nj, ilo, ihi, tj, lane) : 0;
+        const int ns = filter_entries(v.box, fbox, v.bstride, bi, ni, jlo, jhi, fjlo, fjhi, si, lane);
+        const int nt = ns ? filter_entries(v.box, fbox, v.bstride, bj, nj, ilo, ihi, filo, fihi, tj, lane) : 0;
         const int tot = ns * nt;
         for (int k = lane; k < tot; k += 32) {
             const int64_t es = si[k / nt], et = tj[k % nt];
+            if (fbox) {   // float prefilter of the pair test; exact double test on a float hit
+                float flo[3], fhi[3];
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    flo[d] = fbox[d * v.bstride + es];
+                    fhi[d] = fbox[(3 + d) * v.bstride + es];
+                }
+                if (!box_overlap_f(fbox, v.bstride, et, flo, fhi)) continue;
+            }
             double lo[3], hi[3];
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
@@ -447,24 +478,49 @@ __device__ __forceinline__ void put_closed(double *__restrict__ X, double *__res
 // No-split fast path: chord vertex m = start point of segment m for every loop
 // (paired loops keep all segments; unpaired loops are control chords, :108-109),
 // with the PolylineLoop checks fused (geometry.py:333-340).
+template <bool POLY>
 __global__ void write_all_kernel(int64_t M, const double *__restrict__ coeffs, const double *__restrict__ t,
-                                 const int32_t *__restrict__ seg_loop, const int64_t *__restrict__ loff,
-                                 const int *__restrict__ max_exp, double thr, double *__restrict__ X,
-                                 double *__restrict__ Y, double *__restrict__ Z, unsigned *__restrict__ flags) {
+                                 const double *__restrict__ verts, const int32_t *__restrict__ seg_loop,
+                                 const int64_t *__restrict__ loff, const int *__restrict__ max_exp, double thr,
+                                 double *__restrict__ X, double *__restrict__ Y, double *__restrict__ Z,
+                                 unsigned *__restrict__ flags) {
     const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (m >= M) return;
     const int l = seg_loop[m];
     const int64_t b = loff[l], n = loff[l + 1] - b, local = m - b;
     const int64_t nx = local + 1 < n ? m + 1 : b;
     double p[3], q[3];
-    eval_point(coeffs + 12 * m, t[2 * m], p);
-    eval_point(coeffs + 12 * nx, t[2 * nx], q);
+    if (POLY) {   // eval_cubics at t = 0 of the from_polyline coefficients (a1 = next - start, a2 = a3 = 0)
+        const int64_t nn = nx + 1 < b + n ? nx + 1 : b;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const double v0 = verts[3 * m + d], v1 = verts[3 * nx + d], v2 = verts[3 * nn + d];
+            p[d] = eval_axis(v0, v1 - v0, 0.0, 0.0, 0.0);
+            q[d] = eval_axis(v1, v2 - v1, 0.0, 0.0, 0.0);
+        }
+    } else {
+        eval_point(coeffs + 12 * m, t[2 * m], p);
+        eval_point(coeffs + 12 * nx, t[2 * nx], q);
+    }
     put_closed(X, Y, Z, b + l, local, n, p, scale_of(max_exp));
     unsigned f = 0;
     if (!(isfinite(p[0]) && isfinite(p[1]) && isfinite(p[2]))) f |= 1;
     const double dx = __dsub_rn(q[0], p[0]), dy = __dsub_rn(q[1], p[1]), dz = __dsub_rn(q[2], p[2]);
     if (__dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz))) <= thr) f |= 2;
     if (f) atomicOr(flags + l, f);
+}
+
+void launch_write_all(const DiscInput &in, double thr, DiscOutput &out, unsigned *flags, cudaStream_t s) {
+    if (in.M == 0) return;
+    if (in.verts)
+        write_all_kernel<true><<<(unsigned)ceil_div(in.M, 256), 256, 0, s>>>(in.M, nullptr, nullptr, in.verts, in.seg_loop, in.loff,
+                                                             in.max_exp, thr, out.X.as<double>(), out.Y.as<double>(),
+                                                             out.Z.as<double>(), flags);
+    else
+        write_all_kernel<false><<<(unsigned)ceil_div(in.M, 256), 256, 0, s>>>(in.M, in.coeffs, in.t, nullptr, in.seg_loop, in.loff,
+                                                              in.max_exp, thr, out.X.as<double>(), out.Y.as<double>(),
+                                                              out.Z.as<double>(), flags);
+    LC_CHECK_LAUNCH();
 }
 
 // General path: sorted done chords + unpaired control chords into the closed SoA.
@@ -654,8 +710,8 @@ bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc,
     LC_CUDA(cudaMemcpyAsync(sc.prectr.ptr, &pc0, sizeof pc0, cudaMemcpyHostToDevice, s));
     PreCounters *ctr = sc.prectr.as<PreCounters>();
     if (P > 0) {
-        pre_pairs_kernel<<<grid_for(P), 256, 0, s>>>(in.pairs, P, in.loff, in.loop_box, L, sc.paired.as<uint8_t>(),
-                                                     sc.pair_axis.as<int8_t>(), ctr);
+        pre_pairs_kernel<<<grid_for(P), 256, 0, s>>>(in.pairs, P, nullptr, in.loff, in.loop_box, L,
+                                                     sc.paired.as<uint8_t>(), sc.pair_axis.as<int8_t>(), ctr);
         LC_CHECK_LAUNCH();
     }
     if (L > 0) {
@@ -675,7 +731,7 @@ bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc,
     const ActView view0{nullptr, in.seg_loop, in.t, in.t + 1, 2, in.seg_box, M > 0 ? M : 1, in.loff};
     if (P > 0) {
         const int64_t blocks = ceil_div(P, kBruteWarps) < nsm * 16 ? ceil_div(P, kBruteWarps) : nsm * 16;
-        brute_kernel<<<(unsigned)blocks, 32 * kBruteWarps, 0, s>>>(view0, in.loop_box, L, in.pairs, P,
+        brute_kernel<<<(unsigned)blocks, 32 * kBruteWarps, 0, s>>>(view0, in.loop_box, in.seg_fbox, L, in.pairs, P, nullptr,
                                                                    sc.mark.as<uint32_t>(), sc.first_pair.as<int32_t>(),
                                                                    &ctr->marked);
         LC_CHECK_LAUNCH();
@@ -706,7 +762,6 @@ bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc,
 
     // ---- (3) passes
     // pass-1 list: the segment arrays themselves when every loop is paired
-    const bool identity = pc.n_unpaired == 0;
     int64_t n_act = 0, stride = 1;
     ActView view{};
     auto materialize = [&]() {
@@ -769,7 +824,7 @@ bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc,
                 ubox = sc.ubox.as<double>();
             }
             if (pass > 0) {
-                brute_kernel<<<(unsigned)blocks, 32 * kBruteWarps, 0, s>>>(view, ubox, L, in.pairs, P,
+                brute_kernel<<<(unsigned)blocks, 32 * kBruteWarps, 0, s>>>(view, ubox, nullptr, L, in.pairs, P, nullptr,
                                                                            sc.mark.as<uint32_t>(),
                                                                            sc.first_pair.as<int32_t>(), marked_ctr);
                 LC_CHECK_LAUNCH();
@@ -951,12 +1006,7 @@ bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc,
         out.X.reserve(sizeof(double) * (out.Vc + 1), s);
         out.Y.reserve(sizeof(double) * (out.Vc + 1), s);
         out.Z.reserve(sizeof(double) * (out.Vc + 1), s);
-        if (M > 0) {
-            write_all_kernel<<<grid_for(M), 256, 0, s>>>(M, in.coeffs, in.t, in.seg_loop, in.loff, in.max_exp,
-                                                         poly_thr, out.X.as<double>(), out.Y.as<double>(),
-                                                         out.Z.as<double>(), sc.val_flags.as<unsigned>());
-            LC_CHECK_LAUNCH();
-        }
+        launch_write_all(in, poly_thr, out, sc.val_flags.as<unsigned>(), s);
         // unpaired (control-chord) loops rank before paired ones (:131-142 vs :189-191)
         sc.val_err2.reserve(2 * sizeof(int), s);
         const int init2[2] = {INT_MAX, INT_MAX};
@@ -1050,6 +1100,63 @@ bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc,
     LC_CHECK_LAUNCH();
     const int ve = finish_validation(sc, out.voff.as<int64_t>(), L, 1, sc.paired.as<uint8_t>(), 1, s);
     return !polyline_error(ve, err);
+}
+
+// Fused pipeline, no-refinement case (see discretize.cuh).  Mirrors the
+// pass-1 + splits == 0 branch of run_discretize kernel for kernel.
+void launch_discretize_fast(const DiscInput &in, const int64_t *d_P, const DiscParams &prm, DiscScratch &sc,
+                            DiscOutput &out, cudaStream_t s, const PreCounters **d_ctr) {
+    const int64_t L = in.L, M = in.M, Pcap = in.P;
+    const double min_diam = prm.epsilon * prm.xi;
+    const double poly_thr = kMachineEps * prm.xi;
+    sc.paired.reserve(L > 0 ? L : 1, s);
+    sc.pair_axis.reserve(Pcap > 0 ? Pcap : 1, s);
+    sc.prectr.reserve(sizeof(PreCounters), s);
+    sc.val_flags.reserve(sizeof(unsigned) * (L > 0 ? L : 1), s);
+    sc.val_err2.reserve(2 * sizeof(int), s);
+    PreCounters *ctr = sc.prectr.as<PreCounters>();
+    LC_CUDA(cudaMemsetAsync(sc.paired.ptr, 0, L > 0 ? L : 1, s));
+    LC_CUDA(cudaMemsetAsync(sc.val_flags.ptr, 0, sizeof(unsigned) * (L > 0 ? L : 1), s));
+    fast_init_kernel<<<1, 1, 0, s>>>(ctr, sc.val_err2.as<int>());
+    LC_CHECK_LAUNCH();
+    if (Pcap > 0) {
+        pre_pairs_kernel<<<grid_for(Pcap), 256, 0, s>>>(in.pairs, Pcap, d_P, in.loff, in.loop_box, L,
+                                                        sc.paired.as<uint8_t>(), sc.pair_axis.as<int8_t>(), ctr);
+        LC_CHECK_LAUNCH();
+    }
+    if (L > 0) {
+        pre_loops_kernel<<<grid_for(L), 256, 0, s>>>(in.loop_min_diag, sc.paired.as<uint8_t>(), L, min_diam, ctr);
+        LC_CHECK_LAUNCH();
+    }
+    const ActView view0{nullptr, in.seg_loop, in.t, in.t + 1, 2, in.seg_box, M > 0 ? M : 1, in.loff};
+    if (Pcap > 0 && M > 0) {
+        const int64_t nsm = 148;
+        const int64_t blocks = ceil_div(Pcap, kBruteWarps) < nsm * 16 ? ceil_div(Pcap, kBruteWarps) : nsm * 16;
+        brute_kernel<<<(unsigned)blocks, 32 * kBruteWarps, 0, s>>>(view0, in.loop_box, in.seg_fbox, L, in.pairs, Pcap, d_P, nullptr,
+                                                                   nullptr, &ctr->marked);
+        LC_CHECK_LAUNCH();
+    }
+    out.passes = 1;
+    out.splits = 0;
+    out.V = M;
+    out.Vc = M + L;
+    out.vert_off.reserve(sizeof(int64_t) * (L + 1), s);
+    out.voff.reserve(sizeof(int64_t) * (L + 1), s);
+    out.X.reserve(sizeof(double) * (out.Vc + 1), s);
+    out.Y.reserve(sizeof(double) * (out.Vc + 1), s);
+    out.Z.reserve(sizeof(double) * (out.Vc + 1), s);
+    LC_CUDA(cudaMemcpyAsync(out.vert_off.ptr, in.loff, sizeof(int64_t) * (L + 1), cudaMemcpyDeviceToDevice, s));
+    closed_offsets_kernel<<<grid_for(L + 1), 256, 0, s>>>(in.loff, L, out.voff.as<int64_t>());
+    LC_CHECK_LAUNCH();
+    launch_write_all(in, poly_thr, out, sc.val_flags.as<unsigned>(), s);
+    if (L > 0) {
+        validate_loops2_kernel<<<grid_for(L), 256, 0, s>>>(in.loff, L, sc.paired.as<uint8_t>(),
+                                                           sc.val_flags.as<unsigned>(), sc.val_err2.as<int>());
+        LC_CHECK_LAUNCH();
+    }
+    out.d_val_err = sc.val_err2.as<int>();
+    out.validation_pending = true;
+    *d_ctr = ctr;
 }
 
 }  // namespace lc

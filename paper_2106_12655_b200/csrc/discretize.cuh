@@ -23,6 +23,17 @@ struct DiscError {
     std::vector<int64_t> loops;
 };
 
+// Pre-pass / pass counters on the device (read back together in one copy).
+struct PreCounters {
+    int zero_loop;     // first loop with a zero-length segment box (INT_MAX: none)
+    int n_unpaired;
+    int n_large;       // pairs handled by the sweep path
+    int pad;
+    unsigned long long marked;
+    int err_loop;
+    int pad2;
+};
+
 struct DiscParams {
     double xi = 1.0;
     double epsilon = 2.220446049250313e-16;   // discretize.py:27 (MACHINE_EPS)
@@ -51,6 +62,10 @@ struct DiscInput {
     int64_t L, M;
     const int32_t *pairs;                   // (P, 2), sorted PairList
     int64_t P;
+    const float *seg_fbox = nullptr;        // seg_box rounded outward to float (prefilter), optional
+    const double *verts = nullptr;          // closed-polyline model: vertices (M,3) (coeffs are then
+                                            // LoopGeometry.from_polyline's); lets the no-split chord
+                                            // write read 24 B instead of 112 B per segment
 };
 
 // Output: the chord polylines, already in the Gauss-sum layout — closed SoA
@@ -74,6 +89,17 @@ bool validation_error(const int val_err[2], DiscError *err);
 // for input-dependent failures).
 bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc, DiscOutput &out,
                     DiscError *err, cudaStream_t s);
+
+// Fused pipeline (no host sync): the discretization of the common case where
+// pass 1 marks nothing and every pair is a small (brute-force) pair — then
+// the chords are every segment's start point (run_discretize's splits == 0
+// branch).  in.P is the pair-buffer capacity, d_P the device pair count.
+// The result is the reference's iff, after the stream reaches it,
+// (*d_ctr)->zero_loop == INT_MAX, n_large == 0 and marked == 0; validation is
+// left pending in out.d_val_err like defer_validation.  Otherwise the caller
+// reruns run_discretize.
+void launch_discretize_fast(const DiscInput &in, const int64_t *d_P, const DiscParams &prm, DiscScratch &sc,
+                            DiscOutput &out, cudaStream_t s, const PreCounters **d_ctr);
 
 // Unscaled AoS (V, 3) vertices (no closing vertices) from a DiscOutput.
 void unpack_polylines(const DiscOutput &out, int64_t L, const int *max_exp, double *aos, cudaStream_t s);

@@ -314,9 +314,10 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) gauss_items_kernel(
     const double *__restrict__ X, const double *__restrict__ Y, const double *__restrict__ Z,
     const PairGeom *__restrict__ pg, const int64_t *__restrict__ item_off, const int32_t *__restrict__ item_pair,
     int64_t P, int64_t item_begin, int64_t item_end, unsigned long long *__restrict__ counter,
-    double *__restrict__ partials) {
+    double *__restrict__ partials, const int64_t *__restrict__ d_end) {
     __shared__ double ksh[KSM ? 3 * (R + 1) * kCtaThreads : 1];
     const int lane = threadIdx.x & 31;
+    if (d_end && *d_end < item_end) item_end = *d_end;   // fused path: item count on the device
     for (;;) {
         unsigned long long k = 0;
         if (lane == 0) k = atomicAdd(counter, 1ULL);
@@ -355,11 +356,15 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) gauss_items_kernel(
     }
 }
 
-__global__ void pair_geom_kernel(const int32_t *__restrict__ pairs, int64_t P,
+__global__ void pair_geom_kernel(const int32_t *__restrict__ pairs, int64_t P, const int64_t *__restrict__ dP,
                                  const int64_t *__restrict__ voff, PairGeom *__restrict__ pg,
                                  int64_t *__restrict__ nitems) {
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p >= P) return;
+    if (dP && p >= *dP) {   // fused path: capacity slots beyond the device pair count hold no items
+        nitems[p] = 0;
+        return;
+    }
     const int i = pairs[2 * p], j = pairs[2 * p + 1];
     PairGeom g;
     g.col_off = voff[i];
@@ -382,11 +387,12 @@ __global__ void pair_geom_kernel(const int32_t *__restrict__ pairs, int64_t P,
 }
 
 __global__ void reduce_pairs_kernel(const double *__restrict__ partials, const int64_t *__restrict__ item_off,
-                                    int64_t P, double *__restrict__ raw, int64_t *__restrict__ lk,
-                                    uint8_t *__restrict__ flags) {
-    const int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+                                    int64_t P, const int64_t *__restrict__ dP, double *__restrict__ raw,
+                                    int64_t *__restrict__ lk, uint8_t *__restrict__ flags) {
     const int lane = threadIdx.x & 31;
-    if (p >= P) return;
+    if (dP && *dP < P) P = *dP;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; p < P; p += nwarps) {
     const int64_t b = item_off[p], e = item_off[p + 1];
     double s = 0.0;
     for (int64_t k = b + lane; k < e; k += 32) s += partials[k];
@@ -405,6 +411,7 @@ __global__ void reduce_pairs_kernel(const double *__restrict__ partials, const i
         }
         lk[p] = r;
         flags[p] = f;
+    }
     }
 }
 
@@ -458,7 +465,28 @@ __global__ void item_pair_kernel(const int64_t *__restrict__ item_off, int64_t P
     if (it < n_items) item_pair[it] = (int32_t)find_pair(item_off, P, it);
 }
 
+// Fused path: warp per pair writes its item range (item count not known on the host).
+__global__ void item_pair_fill_kernel(const int64_t *__restrict__ item_off, int64_t P, const int64_t *__restrict__ dP,
+                                      int64_t cap_items, int32_t *__restrict__ item_pair) {
+    const int lane = threadIdx.x & 31;
+    if (*dP < P) P = *dP;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; p < P; p += nwarps) {
+        const int64_t b = item_off[p], e = item_off[p + 1] < cap_items ? item_off[p + 1] : cap_items;
+        for (int64_t it = b + lane; it < e; it += 32) item_pair[it] = (int32_t)p;
+    }
+}
+
 }  // namespace
+
+void launch_item_pairs_dev(const int64_t *item_off, int64_t P_cap, const int64_t *d_P, int64_t cap_items,
+                           int32_t *item_pair, cudaStream_t s) {
+    if (P_cap == 0) return;
+    int64_t blocks = ceil_div(P_cap * 32, 256);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    item_pair_fill_kernel<<<(unsigned)blocks, 256, 0, s>>>(item_off, P_cap, d_P, cap_items, item_pair);
+    LC_CHECK_LAUNCH();
+}
 
 void launch_item_pairs(const int64_t *item_off, int64_t P, int64_t n_items, int32_t *item_pair, cudaStream_t s) {
     if (n_items == 0) return;
@@ -497,14 +525,15 @@ size_t build_items_scan_bytes(int64_t P) {
 }
 
 int64_t build_items(const int32_t *d_pairs, int64_t P, const int64_t *d_voff, PairGeom *d_pg,
-                    int64_t *d_item_off, void *d_scan_tmp, size_t scan_tmp_bytes, cudaStream_t s, bool read_back) {
+                    int64_t *d_item_off, void *d_scan_tmp, size_t scan_tmp_bytes, cudaStream_t s, bool read_back,
+                    const int64_t *d_P) {
     if (P == 0) {
         LC_CUDA(cudaMemsetAsync(d_item_off, 0, sizeof(int64_t), s));
         return 0;
     }
     // nitems written into item_off[0..P), item_off[P] = 0, then in-place exclusive scan.
     LC_CUDA(cudaMemsetAsync(d_item_off + P, 0, sizeof(int64_t), s));
-    pair_geom_kernel<<<(unsigned)ceil_div(P, 256), 256, 0, s>>>(d_pairs, P, d_voff, d_pg, d_item_off);
+    pair_geom_kernel<<<(unsigned)ceil_div(P, 256), 256, 0, s>>>(d_pairs, P, d_P, d_voff, d_pg, d_item_off);
     LC_CHECK_LAUNCH();
     size_t bytes = scan_tmp_bytes;
     LC_CUB(cub::DeviceScan::ExclusiveSum(d_scan_tmp, bytes, d_item_off, d_item_off, (int)(P + 1), s));
@@ -517,11 +546,13 @@ int64_t build_items(const int32_t *d_pairs, int64_t P, const int64_t *d_voff, Pa
 
 void launch_gauss_items(int mode, const double *X, const double *Y, const double *Z, const PairGeom *pg,
                         const int64_t *item_off, const int32_t *item_pair, int64_t P, int64_t item_begin,
-                        int64_t item_end, unsigned long long *counter, double *partials, cudaStream_t s) {
+                        int64_t item_end, unsigned long long *counter, double *partials, cudaStream_t s,
+                        const int64_t *d_end) {
     if (item_end <= item_begin) return;
     LC_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s));
     using Kern = void (*)(const double *, const double *, const double *, const PairGeom *, const int64_t *,
-                          const int32_t *, int64_t, int64_t, int64_t, unsigned long long *, double *);
+                          const int32_t *, int64_t, int64_t, int64_t, unsigned long long *, double *,
+                          const int64_t *);
     // default phase kernel: 3 resident CTAs/SM (168 regs); modes 3-6 are A/B variants
     // (1 CTA/SM with 232 regs; 4 CTAs; row vertices in shared memory)
     static const Kern table[] = {gauss_items_kernel<GAUSS_PHASE, 3>, gauss_items_kernel<GAUSS_ATAN, 1>,
@@ -530,23 +561,30 @@ void launch_gauss_items(int mode, const double *X, const double *Y, const double
                                  gauss_items_kernel<GAUSS_PHASE, 3, true>};
     if (mode < 0 || mode >= (int)(sizeof table / sizeof table[0])) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
     const Kern fn = table[mode];
-    int per_sm = 0;
+    constexpr int kModes = (int)(sizeof table / sizeof table[0]);
+    static int occ[kModes] = {};   // resident CTAs per SM, queried once per mode
     const int threads = 128;
-    LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void *)fn, threads, 0));
-    if (per_sm < 1) per_sm = 1;
+    if (!occ[mode]) {
+        int per = 0;
+        LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void *)fn, threads, 0));
+        occ[mode] = per < 1 ? 1 : per;
+    }
+    const int per_sm = occ[mode];
     const int64_t warps_needed = item_end - item_begin;
     int64_t blocks = (int64_t)num_sms() * per_sm;
     const int64_t blocks_needed = ceil_div(warps_needed, threads / 32);
     if (blocks > blocks_needed) blocks = blocks_needed;
     fn<<<(unsigned)blocks, threads, 0, s>>>(X, Y, Z, pg, item_off, item_pair, P, item_begin, item_end, counter,
-                                            partials);
+                                            partials, d_end);
     LC_CHECK_LAUNCH();
 }
 
 void launch_reduce_pairs(const double *partials, const int64_t *item_off, int64_t P, double *raw, int64_t *lk,
-                         uint8_t *flags, cudaStream_t s) {
+                         uint8_t *flags, cudaStream_t s, const int64_t *d_P) {
     if (P == 0) return;
-    reduce_pairs_kernel<<<(unsigned)ceil_div(P * 32, 256), 256, 0, s>>>(partials, item_off, P, raw, lk, flags);
+    int64_t blocks = ceil_div(P * 32, 256);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    reduce_pairs_kernel<<<(unsigned)blocks, 256, 0, s>>>(partials, item_off, P, d_P, raw, lk, flags);
     LC_CHECK_LAUNCH();
 }
 

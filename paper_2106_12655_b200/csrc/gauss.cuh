@@ -33,24 +33,29 @@ struct PairGeom {
 
 // Builds PairGeom[P] and item_off[P+1] (exclusive prefix of items per pair).
 // voff: closed-loop SoA vertex offsets (L+1). Returns total item count (syncs).
+// d_P (fused path): P is the capacity, the device count *d_P <= P is used and
+// capacity slots past it get no items (item_off[P] is still the total).
 int64_t build_items(const int32_t *d_pairs, int64_t P, const int64_t *d_voff, PairGeom *d_pg,
                     int64_t *d_item_off, void *d_scan_tmp, size_t scan_tmp_bytes, cudaStream_t s,
-                    bool read_back = true);
+                    bool read_back = true, const int64_t *d_P = nullptr);
 size_t build_items_scan_bytes(int64_t P);
 
 // Evaluates items [item_begin, item_end) into partials[item] (absolute index).
 void launch_gauss_items(int mode, const double *X, const double *Y, const double *Z,
                         const PairGeom *pg, const int64_t *item_off, const int32_t *item_pair, int64_t P,
                         int64_t item_begin, int64_t item_end, unsigned long long *counter,
-                        double *partials, cudaStream_t s);
+                        double *partials, cudaStream_t s, const int64_t *d_end = nullptr);
 
 // item_pair[it] = pair of work item `it` (replaces a per-item binary search).
 void launch_item_pairs(const int64_t *item_off, int64_t P, int64_t n_items, int32_t *item_pair, cudaStream_t s);
+// Fused path: pair count on the device, item_pair capacity cap_items.
+void launch_item_pairs_dev(const int64_t *item_off, int64_t P_cap, const int64_t *d_P, int64_t cap_items,
+                           int32_t *item_pair, cudaStream_t s);
 
 // raw[p] = fixed-order sum of the pair's item partials; lk = rint(raw);
 // flags bit0 = NaN, bit1 = |raw - rint(raw)| > 0.25 (kernels.py:19-20,69-72).
 void launch_reduce_pairs(const double *partials, const int64_t *item_off, int64_t P, double *raw,
-                         int64_t *lk, uint8_t *flags, cudaStream_t s);
+                         int64_t *lk, uint8_t *flags, cudaStream_t s, const int64_t *d_P = nullptr);
 
 // Writes the closed SoA vertex arrays scaled by an exact power of two from
 // an AoS (n,3) buffer with per-loop offsets (no closing vertex in the input).

@@ -8,6 +8,16 @@
 
 namespace lc {
 
+// Device-written summary of a fused run (lives at the head of the pinned result buffer).
+struct FastStatus {
+    int64_t P, n_items;
+    int max_row, zero_loop, n_unpaired, n_large;
+    unsigned long long marked;
+    int val_err[2];
+};
+
+enum FastResult : int { FAST_OK = 0, FAST_FALLBACK = 1, FAST_INVALID = 2 };
+
 enum StageEvent : int { EV_BEGIN = 0, EV_PLS, EV_DISC, EV_GAUSS0, EV_GAUSS1, EV_END, EV_COUNT };
 
 struct Pipeline {
@@ -15,9 +25,13 @@ struct Pipeline {
     cudaEvent_t ev[EV_COUNT] = {};
 
     // Model: packed monomial cubics (linkcert LoopGeometry arrays, geometry.py:206-296).
-    DevBuf d_coeffs, d_t, d_loff, d_seg_box, d_seg_loop, d_loop_box, d_min_diag, d_model_exp, d_verts_in;
+    DevBuf d_coeffs, d_t, d_loff, d_seg_box, d_seg_fbox, d_seg_loop, d_loop_box, d_min_diag, d_model_exp, d_verts_in;
     int64_t L = 0, M = 0;
     bool model_ready = false;
+    bool model_poly = false;     // uploaded as closed-polyline vertices (d_verts_in)
+    bool coeffs_ready = false;   // d_coeffs/d_t hold the model (polyline models: formed on demand)
+    bool derived = false;        // segment/loop boxes of the current model
+    bool derived_in_run = false; // derive() ran during the current lc_run_pipeline
 
     PlsScratch pls_sc;
     DiscScratch disc_sc;
@@ -48,10 +62,18 @@ struct Pipeline {
     void release();
 
     // model + stages
+    // Segment boxes, loop boxes, min diagonals and the coordinate exponent from
+    // the resident model (records EV_BEGIN first).  Every lc_run_pipeline runs it.
+    void derive();
+    void ensure_derived() {
+        if (!derived) derive();
+    }
+    void ensure_coeffs();
     void upload_model(const double *coeffs, const double *t, const int64_t *loff, int64_t nloops);
     // closed polylines given as vertices only (a0 = v_k, a1 = v_k+1 - v_k, a2 = a3 = 0, t = [0, 1])
     void upload_model_polylines(const double *verts, const int64_t *loff, int64_t nloops);
-    int64_t potential_link_search(const uint64_t *excl_keys, int64_t n_excl);   // -> d_pairs, P
+    // -> d_pairs, P; in_run: EV_BEGIN already recorded by derive() of this run
+    int64_t potential_link_search(const uint64_t *excl_keys, int64_t n_excl, bool in_run = false);
     bool discretize(const DiscParams &prm);                                      // -> dout = gauss input
     void download_loop_boxes(double *lo, double *hi);
     void download_polylines(double *verts, int64_t *vert_off);
@@ -72,12 +94,41 @@ struct Pipeline {
     void download_results_pinned();
     PinnedBuf h_res;
     int64_t h_res_P = -1;
+    char *res_pairs = nullptr, *res_raw = nullptr, *res_lk = nullptr, *res_flags = nullptr;
+
+    // Fused pipeline: PLS -> discretize (no-refinement case) -> items -> Gauss
+    // sum -> rounding -> results into pinned memory with one host sync.  Sizes
+    // stay on the device (capacity-bounded grids); the summary decides whether
+    // the run was the reference's: FAST_OK (results in h_res), FAST_INVALID
+    // (PolylineLoop ValidationError in derr), FAST_FALLBACK (the model needs
+    // refinement / the sweep path / larger buffers: run the staged pipeline).
+    int run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscParams &prm, int mode);
+    int64_t items_cap = 0;
+    // The fused sequence is replayed as a CUDA graph once a run with the same
+    // shape (FastKey) and the same buffer generation has completed uncaptured.
+    struct FastKey {
+        int64_t L, M, pcap, icap, n_excl;
+        int mode, model_poly;
+        double min_diam, poly_thr;
+        unsigned long long gen;
+        bool operator==(const FastKey &o) const {
+            return L == o.L && M == o.M && pcap == o.pcap && icap == o.icap && n_excl == o.n_excl &&
+                   mode == o.mode && model_poly == o.model_poly && min_diam == o.min_diam &&
+                   poly_thr == o.poly_thr && gen == o.gen;
+        }
+    };
+    FastKey fast_seen{}, graph_key{};
+    bool fast_seen_valid = false;
+    cudaGraphExec_t graph_exec = nullptr;
+    long long graph_launches = 0;   // kernels inside the captured graph (lc_launch_count)
+    PinnedBuf h_excl;               // excluded keys staged for the graph's H2D copy
+    bool last_fast_graph = false;
     void segment_pair_lambda(const double *quads, int64_t n, double *out);
 
     float stage_ms(int e0, int e1);
+    void record(int e);
 
   private:
-    void model_boxes();
     void finish_items();
 };
 

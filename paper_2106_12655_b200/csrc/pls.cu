@@ -21,12 +21,20 @@ namespace {
 
 __device__ __forceinline__ int exp_field(double x) { return (__double2hiint(x) >> 20) & 0x7ff; }
 
+// POLY: the model is closed polylines given by their vertices (verts, (M,3));
+// segment m's coefficients are LoopGeometry.from_polyline's (a0 = v_m,
+// a1 = v_next - v_m, a2 = a3 = 0, t = [0, 1]), formed in registers.
+template <bool POLY>
 __global__ void seg_boxes_kernel(const double *__restrict__ coeffs, const double *__restrict__ t,
-                                 const int64_t *__restrict__ loff, int64_t L, int64_t M, double *__restrict__ box,
+                                 const double *__restrict__ verts, const int64_t *__restrict__ loff, int64_t L,
+                                 int64_t M, double *__restrict__ box, float *__restrict__ fbox,
                                  int32_t *__restrict__ seg_loop, unsigned long long *__restrict__ loop_min_diag,
                                  int *__restrict__ max_exp) {
     const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
     int e = 0;
+    int key = -1 - lane;                        // loop of this lane's segment (unique if none)
+    unsigned long long dg = ~0ULL;              // its box diagonal's bit pattern
     if (m < M) {
         int64_t lo = 0, hi = L;   // loop: largest l with loff[l] <= m
         while (hi - lo > 1) {
@@ -35,22 +43,53 @@ __global__ void seg_boxes_kernel(const double *__restrict__ coeffs, const double
         }
         seg_loop[m] = (int32_t)lo;
         double bl[3], bh[3];
-        tight_box(coeffs + 12 * m, t[2 * m], t[2 * m + 1], bl, bh);
+        if (POLY) {
+            // tight_box of (a0, a1, 0, 0) over [0, 1]: with a2 = a3 = +0 both root
+            // candidates are NaN (qa == 0; q == -0 or NaN), so they clip to t = 0
+            // and the box is np.min/np.max over (v(0), v(1), v(0), v(0)).
+            const int64_t nx = m + 1 < loff[lo + 1] ? m + 1 : loff[lo];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                const double a0 = verts[3 * m + d], a1 = verts[3 * nx + d] - a0;
+                const double v0 = eval_axis(a0, a1, 0.0, 0.0, 0.0), v1 = eval_axis(a0, a1, 0.0, 0.0, 1.0);
+                bl[d] = np_min(np_min(np_min(v0, v1), v0), v0);
+                bh[d] = np_max(np_max(np_max(v0, v1), v0), v0);
+            }
+        } else {
+            tight_box(coeffs + 12 * m, t[2 * m], t[2 * m + 1], bl, bh);
+        }
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
             box[d * M + m] = bl[d];
             box[(3 + d) * M + m] = bh[d];
+            if (fbox) {   // outward-rounded float copy: a conservative prefilter box
+                fbox[d * M + m] = __double2float_rd(bl[d]);
+                fbox[(3 + d) * M + m] = __double2float_ru(bh[d]);
+            }
             const int a = exp_field(bl[d]), b = exp_field(bh[d]);
             e = max(e, max(a, b));
         }
-        // per-loop minimum box diagonal (ZeroLengthInput, discretize.py:124-129);
+        key = (int)lo;
         // non-negative doubles order like their bit patterns
-        if (loop_min_diag) atomicMin(loop_min_diag + lo, (unsigned long long)__double_as_longlong(diag_norm(bl, bh)));
+        dg = (unsigned long long)__double_as_longlong(diag_norm(bl, bh));
+    }
+    // per-loop minimum box diagonal (ZeroLengthInput, discretize.py:124-129):
+    // a loop's segments are contiguous, so a segmented suffix-min over the warp
+    // leaves each loop's warp-local minimum in its first lane (one atomic per loop per warp)
+    if (loop_min_diag) {
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const unsigned long long o = __shfl_down_sync(0xffffffffu, dg, off);
+            const int ok = __shfl_down_sync(0xffffffffu, key, off);
+            if (lane + off < 32 && ok == key && o < dg) dg = o;
+        }
+        const int prev = __shfl_up_sync(0xffffffffu, key, 1);
+        if (key >= 0 && (lane == 0 || prev != key)) atomicMin(loop_min_diag + key, dg);
     }
     if (max_exp) {
 #pragma unroll
         for (int off = 16; off; off >>= 1) e = max(e, __shfl_xor_sync(0xffffffffu, e, off));
-        if ((threadIdx.x & 31) == 0 && e > 0) atomicMax(max_exp, e);
+        if (lane == 0 && e > 0) atomicMax(max_exp, e);
     }
 }
 
@@ -65,11 +104,20 @@ __global__ void loop_boxes_kernel(const double *__restrict__ box, int64_t M, con
         v[d] = CUDART_INF;
         v[3 + d] = -CUDART_INF;
     }
-    for (int64_t m = loff[l] + lane; m < loff[l + 1]; m += 32) {
+    // two entries per lane per round: 12 independent loads in flight
+    const int64_t end = loff[l + 1];
+    for (int64_t m = loff[l] + lane; m < end; m += 64) {
+        const bool two = m + 32 < end;
+        double a[6], b[6];
+#pragma unroll
+        for (int d = 0; d < 6; ++d) {
+            a[d] = box[d * M + m];
+            b[d] = two ? box[d * M + m + 32] : a[d];
+        }
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-            v[d] = np_min(v[d], box[d * M + m]);
-            v[3 + d] = np_max(v[3 + d], box[(3 + d) * M + m]);
+            v[d] = np_min(np_min(v[d], a[d]), b[d]);
+            v[3 + d] = np_max(np_max(v[3 + d], a[3 + d]), b[3 + d]);
         }
     }
 #pragma unroll
@@ -215,7 +263,6 @@ __global__ void sweep_warp_kernel(const double *__restrict__ sbox, const int32_t
 // only from its smaller index, into per-row slots sorted at compaction, so the
 // output is the PairList order without a global sort.
 
-constexpr int kRowSlots = 16;
 
 struct GridParams {
     double o[3];
@@ -223,58 +270,6 @@ struct GridParams {
     int dims[3];
     int pad;
 };
-
-// One block: origin, cell size and dims with dims product <= max_cells.
-__global__ void grid_params_kernel(const double *__restrict__ lbox, int64_t L, int64_t max_cells,
-                                   GridParams *__restrict__ gp) {
-    __shared__ double red[7][32];
-    double v[7] = {CUDART_INF, CUDART_INF, CUDART_INF, -CUDART_INF, -CUDART_INF, -CUDART_INF, 0.0};
-    for (int64_t l = threadIdx.x; l < L; l += blockDim.x) {
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-            const double lo = lbox[d * L + l], hi = lbox[(3 + d) * L + l];
-            v[d] = fmin(v[d], lo);
-            v[3 + d] = fmax(v[3 + d], hi);
-            v[6] = fmax(v[6], hi - lo);
-        }
-    }
-#pragma unroll
-    for (int off = 16; off; off >>= 1) {
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-            v[d] = fmin(v[d], __shfl_xor_sync(0xffffffffu, v[d], off));
-            v[3 + d] = fmax(v[3 + d], __shfl_xor_sync(0xffffffffu, v[3 + d], off));
-        }
-        v[6] = fmax(v[6], __shfl_xor_sync(0xffffffffu, v[6], off));
-    }
-    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    if ((threadIdx.x & 31) == 0)
-        for (int d = 0; d < 7; ++d) red[d][w] = v[d];
-    __syncthreads();
-    if (threadIdx.x != 0) return;
-    for (int k = 1; k < nw; ++k) {
-        for (int d = 0; d < 3; ++d) {
-            red[d][0] = fmin(red[d][0], red[d][k]);
-            red[3 + d][0] = fmax(red[3 + d][0], red[3 + d][k]);
-        }
-        red[6][0] = fmax(red[6][0], red[6][k]);
-    }
-    double span[3], c = red[6][0];
-    for (int d = 0; d < 3; ++d) {
-        gp->o[d] = red[d][0];
-        span[d] = red[3 + d][0] - red[d][0];
-    }
-    const double smax = fmax(span[0], fmax(span[1], span[2]));
-    if (!(c > 0.0)) c = smax > 0.0 ? smax * 1e-6 : 1.0;
-    for (;;) {
-        double prod = 1.0;
-        for (int d = 0; d < 3; ++d) prod *= floor(span[d] / c) + 1.0;
-        if (prod <= (double)max_cells) break;
-        c *= 1.25;
-    }
-    gp->c = c;
-    for (int d = 0; d < 3; ++d) gp->dims[d] = (int)(floor(span[d] / c) + 1.0);
-}
 
 __device__ __forceinline__ int cell_coord(double x, double o, double c, int dim) {
     const double f = floor((x - o) / c);
@@ -304,54 +299,6 @@ __global__ void cell_scatter_kernel(const double *__restrict__ lbox, int64_t L, 
     const GridParams g = *gp;
     const int64_t pos = (int64_t)atomicAdd((unsigned long long *)(cursor + owner_cell(lbox, L, l, g)), 1ULL);
     cell_loops[pos] = (int32_t)l;
-}
-
-// Thread per loop a: every b > a with an overlapping closed box (bvh.py:93-98),
-// minus excluded keys.  SLOTS: count all, store up to kRowSlots per row;
-// !SLOTS: write keys at offs[a] (two-pass fallback, sorted afterwards).
-template <bool SLOTS>
-__global__ void grid_query_kernel(const double *__restrict__ lbox, int64_t L, const GridParams *__restrict__ gp,
-                                  const int64_t *__restrict__ cell_off, const int32_t *__restrict__ cell_loops,
-                                  const uint64_t *__restrict__ excl, int64_t n_excl, int *__restrict__ row_count,
-                                  int32_t *__restrict__ slots, const int64_t *__restrict__ offs,
-                                  uint64_t *__restrict__ keys) {
-    const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (a >= L) return;
-    const GridParams g = *gp;
-    double al[3], ah[3];
-    int c0[3], c1[3];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-        al[d] = lbox[d * L + a];
-        ah[d] = lbox[(3 + d) * L + a];
-        c0[d] = max(cell_coord(al[d], g.o[d], g.c, g.dims[d]) - 2, 0);
-        c1[d] = cell_coord(ah[d], g.o[d], g.c, g.dims[d]);
-    }
-    int n = 0;
-    int64_t w = SLOTS ? 0 : offs[a];
-    for (int cz = c0[2]; cz <= c1[2]; ++cz)
-        for (int cy = c0[1]; cy <= c1[1]; ++cy) {
-            const int64_t row = ((int64_t)cz * g.dims[1] + cy) * g.dims[0];
-            const int64_t kb = cell_off[row + c0[0]], ke = cell_off[row + c1[0] + 1];
-            for (int64_t k = kb; k < ke; ++k) {
-                const int64_t b = cell_loops[k];
-                if (b <= a) continue;
-                bool ov = true;
-#pragma unroll
-                for (int d = 0; d < 3; ++d)
-                    if (al[d] > lbox[(3 + d) * L + b] || lbox[d * L + b] > ah[d]) ov = false;
-                if (!ov) continue;
-                const uint64_t key = ((uint64_t)a << 32) | (uint64_t)b;
-                if (n_excl && is_excluded(excl, n_excl, key)) continue;
-                if (SLOTS) {
-                    if (n < kRowSlots) slots[a * kRowSlots + n] = (int32_t)b;
-                } else {
-                    keys[w++] = key;
-                }
-                ++n;
-            }
-        }
-    if (SLOTS) row_count[a] = n;
 }
 
 // Warp per loop a (enough warps to hide the gather latency at L ~ 1e4):
@@ -471,10 +418,10 @@ __global__ void grid_finalize_kernel(const unsigned long long *__restrict__ acc,
 
 // Row i's slots sorted by j -> pairs[off[i] ...] (insertion sort, <= kRowSlots).
 __global__ void slots_compact_kernel(const int *__restrict__ row_count, const int64_t *__restrict__ off, int64_t L,
-                                     const int32_t *__restrict__ slots, int32_t *__restrict__ pairs) {
+                                     const int32_t *__restrict__ slots, int32_t *__restrict__ pairs, int64_t cap) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= L) return;
-    const int n = row_count[i];
+    const int n = row_count[i] < kRowSlots ? row_count[i] : kRowSlots;   // > kRowSlots: caller's fallback
     int32_t v[kRowSlots];
 #pragma unroll
     for (int k = 0; k < kRowSlots; ++k) v[k] = k < n ? slots[i * kRowSlots + k] : INT_MAX;
@@ -490,7 +437,7 @@ __global__ void slots_compact_kernel(const int *__restrict__ row_count, const in
     const int64_t o = off[i];
 #pragma unroll
     for (int k = 0; k < kRowSlots; ++k)
-        if (k < n) {
+        if (k < n && o + k < cap) {
             pairs[2 * (o + k)] = (int32_t)i;
             pairs[2 * (o + k) + 1] = v[k];
         }
@@ -516,14 +463,18 @@ __global__ void unpack_pairs_kernel(const uint64_t *__restrict__ keys, int64_t P
 
 }  // namespace
 
-void launch_seg_boxes(const double *coeffs, const double *t, const int64_t *loff, int64_t L, int64_t M,
-                      double *seg_box, int32_t *seg_loop, unsigned long long *loop_min_diag, int *max_exp,
-                      cudaStream_t s) {
+void launch_seg_boxes(const double *coeffs, const double *t, const double *verts, const int64_t *loff, int64_t L,
+                      int64_t M, double *seg_box, int32_t *seg_loop, unsigned long long *loop_min_diag, int *max_exp,
+                      cudaStream_t s, float *seg_fbox) {
     if (loop_min_diag) LC_CUDA(cudaMemsetAsync(loop_min_diag, 0xff, sizeof(unsigned long long) * (L > 0 ? L : 1), s));
     if (max_exp) LC_CUDA(cudaMemsetAsync(max_exp, 0, sizeof(int), s));
     if (M == 0) return;
-    seg_boxes_kernel<<<(unsigned)ceil_div(M, 128), 128, 0, s>>>(coeffs, t, loff, L, M, seg_box, seg_loop,
-                                                                   loop_min_diag, max_exp);
+    if (verts)
+        seg_boxes_kernel<true><<<(unsigned)ceil_div(M, 128), 128, 0, s>>>(nullptr, nullptr, verts, loff, L, M, seg_box,
+                                                                         seg_fbox, seg_loop, loop_min_diag, max_exp);
+    else
+        seg_boxes_kernel<false><<<(unsigned)ceil_div(M, 128), 128, 0, s>>>(coeffs, t, nullptr, loff, L, M, seg_box,
+                                                                          seg_fbox, seg_loop, loop_min_diag, max_exp);
     LC_CHECK_LAUNCH();
 }
 
@@ -534,6 +485,59 @@ void launch_loop_boxes(const double *seg_box, int64_t M, const int64_t *loff, in
     LC_CHECK_LAUNCH();
 }
 
+// Grid culling up to the per-row pair counts and their exclusive scan (no
+// host sync): sc.offs[L] = P, *sc.counter = largest row count, slots in
+// sc.pair_keys, row counts in sc.idx.  Excluded keys already in sc.excl.
+static void grid_prefix(const double *loop_box, int64_t L, int64_t n_excl, PlsScratch &sc, cudaStream_t s) {
+    const int64_t max_cells = 4 * L + 64;
+    sc.axis.reserve(sizeof(GridParams), s);
+    sc.keys.reserve(sizeof(int64_t) * (max_cells + 1), s);         // cell counts
+    sc.keys_sorted.reserve(sizeof(int64_t) * (max_cells + 1), s);  // cell offsets
+    sc.sbox.reserve(sizeof(int64_t) * (max_cells + 1), s);         // scatter cursors
+    sc.perm.reserve(sizeof(int32_t) * L, s);                       // loops in cell order
+    sc.idx.reserve(sizeof(int) * L, s);                            // row counts
+    sc.pair_keys.reserve(sizeof(int32_t) * kRowSlots * L, s);      // slots
+    sc.counts.reserve(sizeof(int64_t) * (L + 1), s);
+    sc.offs.reserve(sizeof(int64_t) * (L + 1), s);
+    sc.counter.reserve(sizeof(unsigned long long), s);
+    GridParams *gp = sc.axis.as<GridParams>();
+    int64_t *cnt = sc.keys.as<int64_t>(), *coff = sc.keys_sorted.as<int64_t>(), *cur = sc.sbox.as<int64_t>();
+    int *row_count = sc.idx.as<int>(), *max_count = sc.counter.as<int>();
+    sc.counts.reserve(sizeof(int64_t) * (L + 8 > 8 ? L + 8 : 8), s);
+    unsigned long long *acc = (unsigned long long *)sc.counts.ptr;   // 7 ordered keys, reused below
+    LC_CUDA(cudaMemsetAsync(acc, 0xff, 3 * sizeof(unsigned long long), s));
+    LC_CUDA(cudaMemsetAsync(acc + 3, 0, 4 * sizeof(unsigned long long), s));
+    grid_reduce_kernel<<<(unsigned)(ceil_div(L, 256) < 148 ? ceil_div(L, 256) : 148), 256, 0, s>>>(loop_box, L, acc);
+    LC_CHECK_LAUNCH();
+    grid_finalize_kernel<<<1, 1, 0, s>>>(acc, max_cells, gp);
+    LC_CHECK_LAUNCH();
+    LC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (max_cells + 1), s));
+    const unsigned gl = (unsigned)ceil_div(L, 256);
+    cell_count_kernel<<<gl, 256, 0, s>>>(loop_box, L, gp, cnt);
+    LC_CHECK_LAUNCH();
+    size_t b = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, b, (int64_t *)nullptr, (int64_t *)nullptr, (int)(max_cells + 1));
+    size_t b2 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, b2, (int64_t *)nullptr, (int64_t *)nullptr, (int)(L + 1));
+    sc.cub_tmp.reserve(b > b2 ? b : b2, s);
+    b = sc.cub_tmp.bytes;
+    LC_CUB(cub::DeviceScan::ExclusiveSum(sc.cub_tmp.ptr, b, cnt, coff, (int)(max_cells + 1), s));
+    LC_CUDA(cudaMemcpyAsync(cur, coff, sizeof(int64_t) * (max_cells + 1), cudaMemcpyDeviceToDevice, s));
+    cell_scatter_kernel<<<gl, 256, 0, s>>>(loop_box, L, gp, cur, sc.perm.as<int32_t>());
+    LC_CHECK_LAUNCH();
+    LC_CUDA(cudaMemsetAsync(max_count, 0, sizeof(int), s));
+    grid_query_warp_kernel<true><<<(unsigned)ceil_div(L * 32, 256), 256, 0, s>>>(loop_box, L, gp, coff, sc.perm.as<int32_t>(),
+                                               sc.excl.as<uint64_t>(), n_excl, row_count,
+                                               sc.pair_keys.as<int32_t>(), nullptr, nullptr);
+    LC_CHECK_LAUNCH();
+    row_counts_i64_kernel<<<(unsigned)ceil_div(L + 1, 256), 256, 0, s>>>(row_count, L, sc.counts.as<int64_t>(),
+                                                                           max_count);
+    LC_CHECK_LAUNCH();
+    b = sc.cub_tmp.bytes;
+    LC_CUB(cub::DeviceScan::ExclusiveSum(sc.cub_tmp.ptr, b, sc.counts.as<int64_t>(), sc.offs.as<int64_t>(),
+                                         (int)(L + 1), s));
+}
+
 int64_t run_pls(const double *loop_box, int64_t L, const uint64_t *h_excl, int64_t n_excl, PlsScratch &sc,
                 DevBuf &pairs, cudaStream_t s, bool force_sweep) {
     if (L < 2) return 0;
@@ -541,53 +545,11 @@ int64_t run_pls(const double *loop_box, int64_t L, const uint64_t *h_excl, int64
     if (n_excl > 0)
         LC_CUDA(cudaMemcpyAsync(sc.excl.ptr, h_excl, sizeof(uint64_t) * n_excl, cudaMemcpyHostToDevice, s));
     if (!force_sweep) {
-        const int64_t max_cells = 4 * L + 64;
-        sc.axis.reserve(sizeof(GridParams), s);
-        sc.keys.reserve(sizeof(int64_t) * (max_cells + 1), s);         // cell counts
-        sc.keys_sorted.reserve(sizeof(int64_t) * (max_cells + 1), s);  // cell offsets
-        sc.sbox.reserve(sizeof(int64_t) * (max_cells + 1), s);         // scatter cursors
-        sc.perm.reserve(sizeof(int32_t) * L, s);                       // loops in cell order
-        sc.idx.reserve(sizeof(int) * L, s);                            // row counts
-        sc.pair_keys.reserve(sizeof(int32_t) * kRowSlots * L, s);      // slots
-        sc.counts.reserve(sizeof(int64_t) * (L + 1), s);
-        sc.offs.reserve(sizeof(int64_t) * (L + 1), s);
-        sc.counter.reserve(sizeof(unsigned long long), s);
-        GridParams *gp = sc.axis.as<GridParams>();
-        int64_t *cnt = sc.keys.as<int64_t>(), *coff = sc.keys_sorted.as<int64_t>(), *cur = sc.sbox.as<int64_t>();
-        int *row_count = sc.idx.as<int>(), *max_count = sc.counter.as<int>();
-        sc.counts.reserve(sizeof(int64_t) * (L + 8 > 8 ? L + 8 : 8), s);
-        unsigned long long *acc = (unsigned long long *)sc.counts.ptr;   // 7 ordered keys, reused below
-        LC_CUDA(cudaMemsetAsync(acc, 0xff, 3 * sizeof(unsigned long long), s));
-        LC_CUDA(cudaMemsetAsync(acc + 3, 0, 4 * sizeof(unsigned long long), s));
-        grid_reduce_kernel<<<(unsigned)(ceil_div(L, 256) < 148 ? ceil_div(L, 256) : 148), 256, 0, s>>>(loop_box, L, acc);
-        LC_CHECK_LAUNCH();
-        grid_finalize_kernel<<<1, 1, 0, s>>>(acc, max_cells, gp);
-        LC_CHECK_LAUNCH();
-        LC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (max_cells + 1), s));
+        grid_prefix(loop_box, L, n_excl, sc, s);
         const unsigned gl = (unsigned)ceil_div(L, 256);
-        cell_count_kernel<<<gl, 256, 0, s>>>(loop_box, L, gp, cnt);
-        LC_CHECK_LAUNCH();
-        size_t b = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, b, (int64_t *)nullptr, (int64_t *)nullptr, (int)(max_cells + 1));
-        size_t b2 = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, b2, (int64_t *)nullptr, (int64_t *)nullptr, (int)(L + 1));
-        sc.cub_tmp.reserve(b > b2 ? b : b2, s);
-        b = sc.cub_tmp.bytes;
-        LC_CUB(cub::DeviceScan::ExclusiveSum(sc.cub_tmp.ptr, b, cnt, coff, (int)(max_cells + 1), s));
-        LC_CUDA(cudaMemcpyAsync(cur, coff, sizeof(int64_t) * (max_cells + 1), cudaMemcpyDeviceToDevice, s));
-        cell_scatter_kernel<<<gl, 256, 0, s>>>(loop_box, L, gp, cur, sc.perm.as<int32_t>());
-        LC_CHECK_LAUNCH();
-        LC_CUDA(cudaMemsetAsync(max_count, 0, sizeof(int), s));
-        grid_query_warp_kernel<true><<<(unsigned)ceil_div(L * 32, 256), 256, 0, s>>>(loop_box, L, gp, coff, sc.perm.as<int32_t>(),
-                                                   sc.excl.as<uint64_t>(), n_excl, row_count,
-                                                   sc.pair_keys.as<int32_t>(), nullptr, nullptr);
-        LC_CHECK_LAUNCH();
-        row_counts_i64_kernel<<<(unsigned)ceil_div(L + 1, 256), 256, 0, s>>>(row_count, L, sc.counts.as<int64_t>(),
-                                                                               max_count);
-        LC_CHECK_LAUNCH();
-        b = sc.cub_tmp.bytes;
-        LC_CUB(cub::DeviceScan::ExclusiveSum(sc.cub_tmp.ptr, b, sc.counts.as<int64_t>(), sc.offs.as<int64_t>(),
-                                             (int)(L + 1), s));
+        int *row_count = sc.idx.as<int>(), *max_count = sc.counter.as<int>();
+        const int64_t *coff = sc.keys_sorted.as<int64_t>();
+        const GridParams *gp = sc.axis.as<GridParams>();
         int64_t P = 0;
         int mx = 0;
         LC_CUDA(cudaMemcpyAsync(&P, sc.offs.as<int64_t>() + L, sizeof P, cudaMemcpyDeviceToHost, s));
@@ -597,7 +559,7 @@ int64_t run_pls(const double *loop_box, int64_t L, const uint64_t *h_excl, int64
         pairs.reserve(sizeof(int32_t) * 2 * P, s);
         if (mx <= kRowSlots) {
             slots_compact_kernel<<<gl, 256, 0, s>>>(row_count, sc.offs.as<int64_t>(), L, sc.pair_keys.as<int32_t>(),
-                                                     pairs.as<int32_t>());
+                                                     pairs.as<int32_t>(), INT64_MAX);
             LC_CHECK_LAUNCH();
             return P;
         }
@@ -670,6 +632,16 @@ int64_t run_pls(const double *loop_box, int64_t L, const uint64_t *h_excl, int64
                                                                               (int64_t)P, pairs.as<int32_t>());
     LC_CHECK_LAUNCH();
     return (int64_t)P;
+}
+
+void launch_pls_grid(const double *loop_box, int64_t L, int64_t n_excl, PlsScratch &sc, int32_t *pairs, int64_t cap,
+                     cudaStream_t s, const int64_t **d_P, const int **d_max_row) {
+    grid_prefix(loop_box, L, n_excl, sc, s);
+    slots_compact_kernel<<<(unsigned)ceil_div(L, 256), 256, 0, s>>>(sc.idx.as<int>(), sc.offs.as<int64_t>(), L,
+                                                                    sc.pair_keys.as<int32_t>(), pairs, cap);
+    LC_CHECK_LAUNCH();
+    *d_P = sc.offs.as<int64_t>() + L;
+    *d_max_row = sc.counter.as<int>();
 }
 
 }  // namespace lc

@@ -12,9 +12,13 @@ namespace lc {
 // bit pattern of the smallest segment-box diagonal of loop l (ZeroLengthInput,
 // discretize.py:124-129); *max_exp = largest exponent field of any box
 // coordinate (the exact power-of-two scale of the Gauss-sum input).
-void launch_seg_boxes(const double *coeffs, const double *t, const int64_t *loff, int64_t L, int64_t M,
-                      double *seg_box, int32_t *seg_loop, unsigned long long *loop_min_diag, int *max_exp,
-                      cudaStream_t s);
+// verts != nullptr: closed polylines given by their vertices (M,3) instead of
+// coeffs/t (the from_polyline arrays are formed in registers).  seg_fbox
+// (optional): the boxes rounded outward to float (SoA 6 x M), a conservative
+// copy for the discretization's overlap prefilter.
+void launch_seg_boxes(const double *coeffs, const double *t, const double *verts, const int64_t *loff, int64_t L,
+                      int64_t M, double *seg_box, int32_t *seg_loop, unsigned long long *loop_min_diag, int *max_exp,
+                      cudaStream_t s, float *seg_fbox = nullptr);
 
 // Loop AABB = union of its segment boxes (pls.py:48-56).
 void launch_loop_boxes(const double *seg_box, int64_t M, const int64_t *loff, int64_t L, double *loop_box,
@@ -35,5 +39,14 @@ struct PlsScratch {
 // Writes int32 (P,2) into *pairs (grown as needed) and returns P (one sync).
 int64_t run_pls(const double *loop_box, int64_t L, const uint64_t *h_excl, int64_t n_excl, PlsScratch &sc,
                 DevBuf &pairs, cudaStream_t s, bool force_sweep = false);
+
+// Grid-culling PLS without any host sync (the fused pipeline): the excluded
+// keys must already be in sc.excl (n_excl of them); pairs go to `pairs`
+// (capacity cap pairs, >= kRowSlots * L).  *d_P -> device P, *d_max_row ->
+// device largest per-row count; the result is exact iff max_row <= kRowSlots
+// (and then P <= kRowSlots * L).
+constexpr int kRowSlots = 16;
+void launch_pls_grid(const double *loop_box, int64_t L, int64_t n_excl, PlsScratch &sc, int32_t *pairs, int64_t cap,
+                     cudaStream_t s, const int64_t **d_P, const int **d_max_row);
 
 }  // namespace lc

@@ -275,3 +275,67 @@ def test_no_cpu_fallback_when_library_missing(monkeypatch, tmp_path):
     monkeypatch.setattr(_native, "_ctx", {})
     with pytest.raises(_native.NativeUnavailable):
         lc.link_direct(np.eye(3), np.eye(3) + 5)
+
+
+def _pipeline_outcome(model, excluded=(), params=None):
+    """(pairs, raw, lk, flags) bytes of the device pipeline, or the error it raises."""
+    from paper_2106_12655_b200.certify import run_device_pipeline
+
+    try:
+        pairs, raw, lk, flags, ctx = run_device_pipeline(model, excluded, params)
+        return ("ok", np.array(pairs).tobytes(), np.array(raw).tobytes(), np.array(lk).tobytes(),
+                np.array(flags).tobytes()), ctx.last_run_fused()
+    except (lc.DiscretizationError, lc.ValidationError) as e:
+        return (type(e).__name__, getattr(e, "kind", None), tuple(getattr(e, "loops", ()) or ()), str(e)), None
+
+
+def test_fused_matches_staged(monkeypatch, cert_models):
+    """The fused single-sync pipeline and the staged one give bitwise-identical
+    results and identical errors; the fused one runs wherever it applies."""
+    ex, ey, ez = np.eye(3)
+    runs = {name: (m, (), None) for name, m in cert_models.items()}
+    for name, (_, after) in cases.edit_cases().items():
+        runs["edit_" + name] = (after, (), None)
+    for name, (m, _, kw) in cases.disc_error_cases().items():
+        runs["disc_" + name] = (m, (), lc.DiscretizationParams(**kw))
+    a, b = cases.circ(16, (0, 0, 0), ex, ey), cases.circ(16, (1.0, 0, 0), ez, ex)
+    hopf = lc.CurveModel([lc.LoopGeometry.from_polyline(p) for p in (a, b)])
+    runs["hopf_excluded"] = (hopf, {(1, 0)}, None)
+    fused_names = []
+    for name, (m, excl, prm) in runs.items():
+        monkeypatch.setenv("LINKCERT_FUSED", "0")
+        staged, used = _pipeline_outcome(m, excl, prm)
+        assert not used
+        monkeypatch.setenv("LINKCERT_FUSED", "1")
+        fused, used = _pipeline_outcome(m, excl, prm)
+        assert fused == staged, name
+        if used:
+            fused_names.append(name)
+    # polyline models that need no refinement take the fused path
+    for name in ("grid6", "unlinked200", "e4in1_32x32", "kusari_small", "hopf_excluded"):
+        assert name in fused_names, (name, fused_names)
+
+
+def test_fused_graph_replay_bitwise(monkeypatch):
+    """Repeated runs of one model: plain fused run, capture, then graph replays —
+    all bitwise equal to the staged path; a reallocation forces a recapture."""
+    from paper_2106_12655_b200.certify import run_device_pipeline
+
+    monkeypatch.setenv("LINKCERT_FUSED", "0")
+    m = lc.generators.kusari_tube(n_around=12, rows=4, partial=5)
+    want = [np.array(a).copy() for a in run_device_pipeline(m)[:4]]
+    monkeypatch.setenv("LINKCERT_FUSED", "1")
+    # a fresh context: the first fused run sizes every buffer on the fly
+    *got, _ = run_device_pipeline(m, ctx=_native.Context())
+    for a, b in zip(want, got):
+        assert np.array_equal(a, np.asarray(b))
+    paths = []
+    for rep in range(5):
+        if rep == 3:   # a bigger model on the same context reallocates buffers
+            run_device_pipeline(lc.generators.kusari_tube(n_around=16, rows=6, partial=3))
+        *got, ctx = run_device_pipeline(m)
+        paths.append(ctx.last_run_fused())
+        assert all(v >= 0.0 for v in ctx.stage_times().values())   # events recorded inside the graph
+        for a, b in zip(want, got):
+            assert np.array_equal(a, np.asarray(b)) and np.asarray(b).dtype == a.dtype
+    assert paths[0] >= 1 and 2 in paths, paths
