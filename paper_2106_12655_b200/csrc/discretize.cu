@@ -121,7 +121,8 @@ __global__ void pre_loops_kernel(const unsigned long long *__restrict__ min_diag
                                  int64_t L, double min_diam, PreCounters *__restrict__ ctr) {
     const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (l >= L) return;
-    if (__longlong_as_double((long long)min_diag[l]) < min_diam) atomicMin(&ctr->zero_loop, (int)l);
+    // min over segments of sqrt(squared diagonal) == sqrt(min squared diagonal)
+    if (__dsqrt_rn(__longlong_as_double((long long)min_diag[l])) < min_diam) atomicMin(&ctr->zero_loop, (int)l);
     if (!paired[l]) atomicAdd(&ctr->n_unpaired, 1);
 }
 
@@ -220,6 +221,133 @@ __global__ void __launch_bounds__(32 * kBruteWarps) brute_kernel(ActView v, cons
                 mark_entry(mark, first_pair, et, (int32_t)p, marked);
             }
         }
+        __syncwarp();
+    }
+}
+
+// Fused-path pass-1 detection: does ANY pair of the (small) PLS pairs have two
+// overlapping segment boxes?  (Only "nothing marked" keeps the fused path;
+// otherwise the staged path recomputes the exact marks.)  Warp per pair: the
+// segments of both loops are filtered against the other loop's box in one
+// sweep over their outward-rounded float boxes (all loads in flight together),
+// survivors are staged in shared memory with their float boxes, tested
+// pairwise in float, and a float hit is confirmed with the exact closed-box
+// test on the double boxes (bvh.py:93-98).  Hits are counted into *marked.
+constexpr int kAnyWarps = 8;
+constexpr int kAnyCap = 64;   // staged survivors per side; beyond that the test reads global memory
+__global__ void __launch_bounds__(32 * kAnyWarps) brute_any_kernel(
+    const double *__restrict__ box, const float *__restrict__ fbox, int64_t M, const int64_t *__restrict__ loff,
+    const double *__restrict__ lbox, int64_t L, const int32_t *__restrict__ pairs, int64_t P,
+    const int64_t *__restrict__ dP, unsigned long long *__restrict__ marked) {
+    __shared__ int32_t sidx[kAnyWarps][2][kAnyCap];
+    __shared__ float sbox[kAnyWarps][2][6][kAnyCap];
+    if (dP && *dP < P) P = *dP;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * kAnyWarps;
+    for (int64_t p = blockIdx.x * (int64_t)kAnyWarps + w; p < P; p += nw) {
+        const int i = pairs[2 * p], j = pairs[2 * p + 1];
+        const int64_t bi = loff[i], ni = loff[i + 1] - bi;
+        const int64_t bj = loff[j], nj = loff[j + 1] - bj;
+        if (ni == 0 || nj == 0 || !brute_pair(ni, nj)) continue;
+        float fb[2][6];   // [0]: loop j's box (filters side i), [1]: loop i's box (filters side j)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            fb[0][d] = __double2float_rd(lbox[d * L + j]);
+            fb[0][3 + d] = __double2float_ru(lbox[(3 + d) * L + j]);
+            fb[1][d] = __double2float_rd(lbox[d * L + i]);
+            fb[1][3 + d] = __double2float_ru(lbox[(3 + d) * L + i]);
+        }
+        const int64_t ntot = ni + nj;
+        int cnt[2] = {0, 0};
+        for (int64_t e0 = 0; e0 < ntot; e0 += 128) {
+            float v[4][6];
+            int64_t seg[4];
+            bool ok[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {   // four chunks of 32 entries: 24 loads in flight
+                const int64_t e = e0 + 32 * c + lane;
+                ok[c] = e < ntot;
+                seg[c] = e < ni ? bi + e : bj + (e - ni);
+#pragma unroll
+                for (int d = 0; d < 6; ++d) v[c][d] = ok[c] ? fbox[d * M + seg[c]] : 0.f;
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int64_t e = e0 + 32 * c + lane;
+                const int side = e < ni ? 0 : 1;
+                const float *o = fb[side];
+                const bool in = ok[c] && !(o[0] > v[c][3] || v[c][0] > o[3] || o[1] > v[c][4] || v[c][1] > o[4] ||
+                                           o[2] > v[c][5] || v[c][2] > o[5]);
+#pragma unroll
+                for (int sd = 0; sd < 2; ++sd) {
+                    const unsigned bal = __ballot_sync(0xffffffffu, in && side == sd);
+                    if (in && side == sd) {
+                        const int r = cnt[sd] + __popc(bal & ((1u << lane) - 1u));
+                        if (r < kAnyCap) {
+                            sidx[w][sd][r] = (int32_t)seg[c];
+#pragma unroll
+                            for (int d = 0; d < 6; ++d) sbox[w][sd][d][r] = v[c][d];
+                        }
+                    }
+                    cnt[sd] += __popc(bal);
+                }
+            }
+        }
+        __syncwarp();
+        const int ns = cnt[0], nt = cnt[1];
+        const int tot = ns * nt;
+        int hits = 0;
+        for (int k = lane; k < tot; k += 32) {
+            const int a = k / nt, b = k % nt;
+            float x[6], y[6];
+            int64_t es, et;
+            if (ns <= kAnyCap && nt <= kAnyCap) {
+                es = sidx[w][0][a];
+                et = sidx[w][1][b];
+#pragma unroll
+                for (int d = 0; d < 6; ++d) {
+                    x[d] = sbox[w][0][d][a];
+                    y[d] = sbox[w][1][d][b];
+                }
+            } else {   // rare: more survivors than staged; re-filter from global memory
+                es = -1;
+                et = -1;
+                int c = 0;
+                for (int64_t q = 0; q < ni && es < 0; ++q) {
+                    const float *o = fb[0];
+                    float u[6];
+#pragma unroll
+                    for (int d = 0; d < 6; ++d) u[d] = fbox[d * M + bi + q];
+                    if (!(o[0] > u[3] || u[0] > o[3] || o[1] > u[4] || u[1] > o[4] || o[2] > u[5] || u[2] > o[5]) &&
+                        c++ == a)
+                        es = bi + q;
+                }
+                c = 0;
+                for (int64_t q = 0; q < nj && et < 0; ++q) {
+                    const float *o = fb[1];
+                    float u[6];
+#pragma unroll
+                    for (int d = 0; d < 6; ++d) u[d] = fbox[d * M + bj + q];
+                    if (!(o[0] > u[3] || u[0] > o[3] || o[1] > u[4] || u[1] > o[4] || o[2] > u[5] || u[2] > o[5]) &&
+                        c++ == b)
+                        et = bj + q;
+                }
+#pragma unroll
+                for (int d = 0; d < 6; ++d) {
+                    x[d] = fbox[d * M + es];
+                    y[d] = fbox[d * M + et];
+                }
+            }
+            if (x[0] > y[3] || y[0] > x[3] || x[1] > y[4] || y[1] > x[4] || x[2] > y[5] || y[2] > x[5]) continue;
+            double lo[3], hi[3];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                lo[d] = box[d * M + es];
+                hi[d] = box[(3 + d) * M + es];
+            }
+            if (box_overlap(box, M, et, lo, hi)) ++hits;
+        }
+        if (hits) atomicAdd(marked, (unsigned long long)hits);
         __syncwarp();
     }
 }
@@ -1130,10 +1258,10 @@ void launch_discretize_fast(const DiscInput &in, const int64_t *d_P, const DiscP
     }
     const ActView view0{nullptr, in.seg_loop, in.t, in.t + 1, 2, in.seg_box, M > 0 ? M : 1, in.loff};
     if (Pcap > 0 && M > 0) {
-        const int64_t nsm = 148;
-        const int64_t blocks = ceil_div(Pcap, kBruteWarps) < nsm * 16 ? ceil_div(Pcap, kBruteWarps) : nsm * 16;
-        brute_kernel<<<(unsigned)blocks, 32 * kBruteWarps, 0, s>>>(view0, in.loop_box, in.seg_fbox, L, in.pairs, Pcap, d_P, nullptr,
-                                                                   nullptr, &ctr->marked);
+        const int64_t blocks = ceil_div(Pcap, kAnyWarps) < 148 * 8 ? ceil_div(Pcap, kAnyWarps) : 148 * 8;
+        brute_any_kernel<<<(unsigned)blocks, 32 * kAnyWarps, 0, s>>>(in.seg_box, in.seg_fbox, M, in.loff,
+                                                                     in.loop_box, L, in.pairs, Pcap, d_P,
+                                                                     &ctr->marked);
         LC_CHECK_LAUNCH();
     }
     out.passes = 1;

@@ -57,7 +57,7 @@ struct DiscInput {
     const int32_t *seg_loop;                // (M)
     const double *seg_box;                  // SoA 6 x M
     const double *loop_box;                 // SoA 6 x L
-    const unsigned long long *loop_min_diag;// (L) bit patterns of min segment-box diagonals
+    const unsigned long long *loop_min_diag;// (L) bit patterns of min squared segment-box diagonals
     const int *max_exp;                     // exponent field of the largest |box coordinate|
     int64_t L, M;
     const int32_t *pairs;                   // (P, 2), sorted PairList

@@ -71,7 +71,7 @@ void Pipeline::init(cudaStream_t st) {
 }
 
 void Pipeline::release() {
-    DevBuf *bufs[] = {&d_coeffs, &d_t, &d_loff, &d_seg_box, &d_seg_fbox, &d_seg_loop, &d_loop_box, &d_min_diag, &d_model_exp,
+    DevBuf *bufs[] = {&d_coeffs, &d_t, &d_loff, &d_seg_box, &d_seg_fbox, &d_loop_keys, &d_seg_loop, &d_loop_box, &d_min_diag, &d_model_exp,
                       &d_verts_in, &d_aos, &d_in_off, &d_voff, &d_X, &d_Y, &d_Z, &d_exp, &d_tmp_aos, &d_pairs,
                       &d_pg, &d_item_off, &d_item_pair, &d_scan, &d_counter, &d_partials, &d_raw, &d_lk, &d_flags,
                       &d_quads, &d_qout, &dout.X, &dout.Y, &dout.Z, &dout.voff, &dout.vert_off};
@@ -127,11 +127,12 @@ void Pipeline::derive() {
     d_min_diag.reserve(sizeof(unsigned long long) * (L > 0 ? L : 1), s);
     d_model_exp.reserve(sizeof(int), s);
     // tight segment boxes, per-loop min diagonals, coordinate exponent, loop boxes
+    d_loop_keys.reserve(sizeof(unsigned long long) * 6 * (L > 0 ? L : 1), s);
     launch_seg_boxes(model_poly ? nullptr : d_coeffs.as<double>(), model_poly ? nullptr : d_t.as<double>(),
                      model_poly ? d_verts_in.as<double>() : nullptr, d_loff.as<int64_t>(), L, M,
                      d_seg_box.as<double>(), d_seg_loop.as<int32_t>(), d_min_diag.as<unsigned long long>(),
-                     d_model_exp.as<int>(), s, d_seg_fbox.as<float>());
-    launch_loop_boxes(d_seg_box.as<double>(), M, d_loff.as<int64_t>(), L, d_loop_box.as<double>(), s);
+                     d_model_exp.as<int>(), s, d_seg_fbox.as<float>(), d_loop_keys.as<unsigned long long>(),
+                     d_loop_box.as<double>());
     derived = true;
     derived_in_run = true;
 }

@@ -21,6 +21,42 @@ namespace {
 
 __device__ __forceinline__ int exp_field(double x) { return (__double2hiint(x) >> 20) & 0x7ff; }
 
+// Ordered 64-bit keys of doubles for atomicMin/atomicMax: monotone for
+// non-NaN values; NaN gets the extreme key of the reduction direction so it
+// propagates like np.min / np.max (min keys: 0, max keys: ~0).
+__device__ __forceinline__ unsigned long long min_key(double x) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    return x != x ? 0ULL : ((b >> 63) ? ~b : b ^ 0x8000000000000000ULL);
+}
+__device__ __forceinline__ unsigned long long max_key(double x) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    return x != x ? ~0ULL : ((b >> 63) ? ~b : b ^ 0x8000000000000000ULL);
+}
+__device__ __forceinline__ double key_value(unsigned long long k) {
+    return __longlong_as_double((long long)((k >> 63) ? (k ^ 0x8000000000000000ULL) : ~k));
+}
+
+// Group minimum of a 64-bit value over the lanes in `grp` (all lanes of a group
+// call with the same mask): high word first, then the low word among the
+// lanes holding the minimal high word.
+__device__ __forceinline__ unsigned long long group_min_u64(unsigned grp, unsigned long long v) {
+    const unsigned hi = __reduce_min_sync(grp, (unsigned)(v >> 32));
+    const unsigned lo = __reduce_min_sync(grp, (unsigned)(v >> 32) == hi ? (unsigned)v : 0xffffffffu);
+    return ((unsigned long long)hi << 32) | lo;
+}
+__device__ __forceinline__ unsigned long long group_max_u64(unsigned grp, unsigned long long v) {
+    const unsigned hi = __reduce_max_sync(grp, (unsigned)(v >> 32));
+    const unsigned lo = __reduce_max_sync(grp, (unsigned)(v >> 32) == hi ? (unsigned)v : 0u);
+    return ((unsigned long long)hi << 32) | lo;
+}
+
+// Tight per-segment boxes (geometry.py:113-152) plus, fused: seg_loop, the
+// outward-rounded float copy, the per-loop union boxes as ordered keys
+// (loop_keys: 3 x L min keys, then 3 x L max keys; decoded by
+// loop_keys_decode_kernel), the per-loop minimum squared box diagonal and the
+// coordinate exponent.  A loop's segments are contiguous, so the lanes of a
+// warp that share a loop form one group: group reductions, one atomic per
+// group and value.
 // POLY: the model is closed polylines given by their vertices (verts, (M,3));
 // segment m's coefficients are LoopGeometry.from_polyline's (a0 = v_m,
 // a1 = v_next - v_m, a2 = a3 = 0, t = [0, 1]), formed in registers.
@@ -28,32 +64,42 @@ template <bool POLY>
 __global__ void seg_boxes_kernel(const double *__restrict__ coeffs, const double *__restrict__ t,
                                  const double *__restrict__ verts, const int64_t *__restrict__ loff, int64_t L,
                                  int64_t M, double *__restrict__ box, float *__restrict__ fbox,
-                                 int32_t *__restrict__ seg_loop, unsigned long long *__restrict__ loop_min_diag,
-                                 int *__restrict__ max_exp) {
+                                 int32_t *__restrict__ seg_loop, unsigned long long *__restrict__ loop_min_diag2,
+                                 unsigned long long *__restrict__ loop_keys, int *__restrict__ max_exp) {
     const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
-    int e = 0;
-    int key = -1 - lane;                        // loop of this lane's segment (unique if none)
-    unsigned long long dg = ~0ULL;              // its box diagonal's bit pattern
-    if (m < M) {
-        int64_t lo = 0, hi = L;   // loop: largest l with loff[l] <= m
+    // loop of segment m: one binary search per warp (its first segment), then
+    // each lane walks forward (a warp spans few loops)
+    const int64_t m0 = m - lane;
+    int64_t l0 = 0;
+    if (lane == 0 && m0 < M) {
+        int64_t lo = 0, hi = L;   // largest l with loff[l] <= m0
         while (hi - lo > 1) {
             const int64_t mid = (lo + hi) >> 1;
-            if (loff[mid] <= m) lo = mid; else hi = mid;
+            if (loff[mid] <= m0) lo = mid; else hi = mid;
         }
+        l0 = lo;
+    }
+    l0 = __shfl_sync(0xffffffffu, l0, 0);
+    int e = 0;
+    int key = -1 - lane;   // unique when the lane has no segment
+    double bl[3] = {0, 0, 0}, bh[3] = {0, 0, 0};
+    unsigned long long dg = ~0ULL;
+    if (m < M) {
+        int64_t lo = l0;
+        while (loff[lo + 1] <= m) ++lo;
         seg_loop[m] = (int32_t)lo;
-        double bl[3], bh[3];
         if (POLY) {
             // tight_box of (a0, a1, 0, 0) over [0, 1]: with a2 = a3 = +0 both root
-            // candidates are NaN (qa == 0; q == -0 or NaN), so they clip to t = 0
-            // and the box is np.min/np.max over (v(0), v(1), v(0), v(0)).
+            // candidates are NaN (qa == 0; q == -0 or NaN), so they clip to t = 0 and
+            // the box is np.min/np.max over (v(0), v(1), v(0), v(0)) = over (v(0), v(1)).
             const int64_t nx = m + 1 < loff[lo + 1] ? m + 1 : loff[lo];
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
                 const double a0 = verts[3 * m + d], a1 = verts[3 * nx + d] - a0;
                 const double v0 = eval_axis(a0, a1, 0.0, 0.0, 0.0), v1 = eval_axis(a0, a1, 0.0, 0.0, 1.0);
-                bl[d] = np_min(np_min(np_min(v0, v1), v0), v0);
-                bh[d] = np_max(np_max(np_max(v0, v1), v0), v0);
+                bl[d] = np_min(v0, v1);
+                bh[d] = np_max(v0, v1);
             }
         } else {
             tight_box(coeffs + 12 * m, t[2 * m], t[2 * m + 1], bl, bh);
@@ -70,67 +116,49 @@ __global__ void seg_boxes_kernel(const double *__restrict__ coeffs, const double
             e = max(e, max(a, b));
         }
         key = (int)lo;
-        // non-negative doubles order like their bit patterns
-        dg = (unsigned long long)__double_as_longlong(diag_norm(bl, bh));
+        // squared diagonal ((dx*dx + dy*dy) + dz*dz); sqrt is monotone, so the
+        // loop minimum of the norms (discretize.py:124-129) is sqrt of this minimum.
+        // Non-negative doubles order like their bit patterns.
+        const double dx = __dsub_rn(bh[0], bl[0]), dy = __dsub_rn(bh[1], bl[1]), dz = __dsub_rn(bh[2], bl[2]);
+        dg = (unsigned long long)__double_as_longlong(
+            __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
     }
-    // per-loop minimum box diagonal (ZeroLengthInput, discretize.py:124-129):
-    // a loop's segments are contiguous, so a segmented suffix-min over the warp
-    // leaves each loop's warp-local minimum in its first lane (one atomic per loop per warp)
-    if (loop_min_diag) {
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const unsigned long long o = __shfl_down_sync(0xffffffffu, dg, off);
-            const int ok = __shfl_down_sync(0xffffffffu, key, off);
-            if (lane + off < 32 && ok == key && o < dg) dg = o;
+    if (loop_min_diag2 || loop_keys) {
+        const unsigned grp = __match_any_sync(0xffffffffu, key);
+        const bool head = lane == __ffs(grp) - 1 && key >= 0;
+        if (loop_min_diag2) {
+            const unsigned long long g = group_min_u64(grp, dg);
+            if (head) atomicMin(loop_min_diag2 + key, g);
         }
-        const int prev = __shfl_up_sync(0xffffffffu, key, 1);
-        if (key >= 0 && (lane == 0 || prev != key)) atomicMin(loop_min_diag + key, dg);
+        if (loop_keys) {
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                const unsigned long long kl = group_min_u64(grp, min_key(bl[d]));
+                const unsigned long long kh = group_max_u64(grp, max_key(bh[d]));
+                if (head) {
+                    atomicMin(loop_keys + d * L + key, kl);
+                    atomicMax(loop_keys + (3 + d) * L + key, kh);
+                }
+            }
+        }
     }
     if (max_exp) {
-#pragma unroll
-        for (int off = 16; off; off >>= 1) e = max(e, __shfl_xor_sync(0xffffffffu, e, off));
+        e = __reduce_max_sync(0xffffffffu, e);
         if (lane == 0 && e > 0) atomicMax(max_exp, e);
     }
 }
 
-__global__ void loop_boxes_kernel(const double *__restrict__ box, int64_t M, const int64_t *__restrict__ loff,
-                                  int64_t L, double *__restrict__ lbox) {
-    const int64_t l = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
+// Loop AABBs from the ordered keys (empty loop: [+inf, -inf], like the
+// reduction identity of loop_boxes_kernel).
+__global__ void loop_keys_decode_kernel(const unsigned long long *__restrict__ keys, int64_t L,
+                                        double *__restrict__ lbox) {
+    const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (l >= L) return;
-    double v[6];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-        v[d] = CUDART_INF;
-        v[3 + d] = -CUDART_INF;
-    }
-    // two entries per lane per round: 12 independent loads in flight
-    const int64_t end = loff[l + 1];
-    for (int64_t m = loff[l] + lane; m < end; m += 64) {
-        const bool two = m + 32 < end;
-        double a[6], b[6];
-#pragma unroll
-        for (int d = 0; d < 6; ++d) {
-            a[d] = box[d * M + m];
-            b[d] = two ? box[d * M + m + 32] : a[d];
-        }
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-            v[d] = np_min(np_min(v[d], a[d]), b[d]);
-            v[3 + d] = np_max(np_max(v[3 + d], a[3 + d]), b[3 + d]);
-        }
-    }
-#pragma unroll
-    for (int off = 16; off; off >>= 1) {
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-            v[d] = np_min(v[d], __shfl_xor_sync(0xffffffffu, v[d], off));
-            v[3 + d] = np_max(v[3 + d], __shfl_xor_sync(0xffffffffu, v[3 + d], off));
-        }
-    }
-    if (lane == 0) {
-#pragma unroll
-        for (int d = 0; d < 6; ++d) lbox[d * L + l] = v[d];
+        const unsigned long long kl = keys[d * L + l], kh = keys[(3 + d) * L + l];
+        lbox[d * L + l] = kl == 0ULL ? CUDART_NAN : (kl == ~0ULL ? CUDART_INF : key_value(kl));
+        lbox[(3 + d) * L + l] = kh == ~0ULL ? CUDART_NAN : (kh == 0ULL ? -CUDART_INF : key_value(kh));
     }
 }
 
@@ -284,31 +312,41 @@ __device__ __forceinline__ int64_t owner_cell(const double *__restrict__ lbox, i
     return ((int64_t)cz * g.dims[1] + cy) * g.dims[0] + cx;
 }
 
+// cell of each loop's lower corner and the loop's rank within that cell
 __global__ void cell_count_kernel(const double *__restrict__ lbox, int64_t L, const GridParams *__restrict__ gp,
-                                  int64_t *__restrict__ count) {
+                                  int64_t *__restrict__ count, int32_t *__restrict__ lcell, int32_t *__restrict__ lrank) {
     const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (l >= L) return;
     const GridParams g = *gp;
-    atomicAdd((unsigned long long *)(count + owner_cell(lbox, L, l, g)), 1ULL);
+    const int64_t c = owner_cell(lbox, L, l, g);
+    lcell[l] = (int32_t)c;
+    lrank[l] = (int32_t)atomicAdd((unsigned long long *)(count + c), 1ULL);
 }
 
-__global__ void cell_scatter_kernel(const double *__restrict__ lbox, int64_t L, const GridParams *__restrict__ gp,
-                                    int64_t *__restrict__ cursor, int32_t *__restrict__ cell_loops) {
+// loops in cell order with their boxes alongside (the query reads both at once)
+__global__ void cell_scatter_kernel(const double *__restrict__ lbox, int64_t L, const int64_t *__restrict__ cell_off,
+                                    const int32_t *__restrict__ lcell, const int32_t *__restrict__ lrank,
+                                    int32_t *__restrict__ cell_loops, double *__restrict__ cbox) {
     const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (l >= L) return;
-    const GridParams g = *gp;
-    const int64_t pos = (int64_t)atomicAdd((unsigned long long *)(cursor + owner_cell(lbox, L, l, g)), 1ULL);
+    const int64_t pos = cell_off[lcell[l]] + lrank[l];
     cell_loops[pos] = (int32_t)l;
+#pragma unroll
+    for (int d = 0; d < 6; ++d) cbox[d * L + pos] = lbox[d * L + l];
 }
 
-// Warp per loop a (enough warps to hide the gather latency at L ~ 1e4):
-// lanes share a's candidate cells; hits are ranked with a ballot.
+// Warp per loop a.  The candidate cells form up to 4 x 4 rows (z, y) of 4
+// consecutive x cells, i.e. up to 16 contiguous ranges of the cell-ordered
+// loop list: lanes fetch the row ranges at once, scan their lengths, and then
+// sweep the concatenated candidates 32 at a time (loop id + box read together),
+// so a query costs a few dependent memory round trips instead of ~3 per row.
+// Hits (b > a, closed-box overlap, not excluded) are ranked with a ballot.
 template <bool SLOTS>
 __global__ void grid_query_warp_kernel(const double *__restrict__ lbox, int64_t L, const GridParams *__restrict__ gp,
                                        const int64_t *__restrict__ cell_off, const int32_t *__restrict__ cell_loops,
-                                       const uint64_t *__restrict__ excl, int64_t n_excl, int *__restrict__ row_count,
-                                       int32_t *__restrict__ slots, const int64_t *__restrict__ offs,
-                                       uint64_t *__restrict__ keys) {
+                                       const double *__restrict__ cbox, const uint64_t *__restrict__ excl,
+                                       int64_t n_excl, int *__restrict__ row_count, int32_t *__restrict__ slots,
+                                       const int64_t *__restrict__ offs, uint64_t *__restrict__ keys) {
     const int lane = threadIdx.x & 31;
     const int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     if (a >= L) return;
@@ -322,38 +360,64 @@ __global__ void grid_query_warp_kernel(const double *__restrict__ lbox, int64_t 
         c0[d] = max(cell_coord(al[d], g.o[d], g.c, g.dims[d]) - 2, 0);
         c1[d] = cell_coord(ah[d], g.o[d], g.c, g.dims[d]);
     }
+    const int ny = c1[1] - c0[1] + 1, nrows_all = ny * (c1[2] - c0[2] + 1);   // <= 25 (cells >= any extent)
     int n = 0;
     const int64_t w0 = SLOTS ? 0 : offs[a];
-    for (int cz = c0[2]; cz <= c1[2]; ++cz)
-        for (int cy = c0[1]; cy <= c1[1]; ++cy) {
-            const int64_t row = ((int64_t)cz * g.dims[1] + cy) * g.dims[0];
-            const int64_t kb = cell_off[row + c0[0]], ke = cell_off[row + c1[0] + 1];
-            for (int64_t k0 = kb; k0 < ke; k0 += 32) {
-                const int64_t k = k0 + lane;
-                bool hit = false;
-                int64_t b = 0;
-                if (k < ke) {
-                    b = cell_loops[k];
-                    if (b > a) {
-                        hit = true;
+    for (int rb = 0; rb < nrows_all; rb += 32) {   // one batch unless the grid is degenerate
+    const int nrows = nrows_all - rb < 32 ? nrows_all - rb : 32;
+    int64_t kb = 0, len = 0;
+    if (lane < nrows) {
+        const int rr = rb + lane;
+        const int cz = c0[2] + rr / ny, cy = c0[1] + rr % ny;
+        const int64_t row = ((int64_t)cz * g.dims[1] + cy) * g.dims[0];
+        kb = cell_off[row + c0[0]];
+        len = cell_off[row + c1[0] + 1] - kb;
+    }
+    int64_t incl = len;   // inclusive scan of the row lengths
 #pragma unroll
-                        for (int d = 0; d < 3; ++d)
-                            if (al[d] > lbox[(3 + d) * L + b] || lbox[d * L + b] > ah[d]) hit = false;
-                        if (hit && n_excl && is_excluded(excl, n_excl, ((uint64_t)a << 32) | (uint64_t)b)) hit = false;
-                    }
-                }
-                const unsigned bal = __ballot_sync(0xffffffffu, hit);
-                if (hit) {
-                    const int r = n + __popc(bal & ((1u << lane) - 1u));
-                    if (SLOTS) {
-                        if (r < kRowSlots) slots[a * kRowSlots + r] = (int32_t)b;
-                    } else {
-                        keys[w0 + r] = ((uint64_t)a << 32) | (uint64_t)b;
-                    }
-                }
-                n += __popc(bal);
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const int64_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const int64_t excl_start = incl - len;
+    for (int64_t f0 = 0; f0 < total; f0 += 32) {
+        const int64_t f = f0 + lane;
+        // row of flat candidate f: the last row whose start is <= f (rows of length 0 skipped)
+        int r = 0;
+        for (int q = 1; q < nrows; ++q) {
+            const int64_t st = __shfl_sync(0xffffffffu, excl_start, q);
+            if (st <= f) r = q;
+        }
+        const int64_t kr = __shfl_sync(0xffffffffu, kb, r) + (f - __shfl_sync(0xffffffffu, excl_start, r));
+        bool hit = false;
+        int64_t b = 0;
+        if (f < total) {
+            b = cell_loops[kr];
+            double bl[3], bh[3];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                bl[d] = cbox[d * L + kr];
+                bh[d] = cbox[(3 + d) * L + kr];
+            }
+            hit = b > a;
+#pragma unroll
+            for (int d = 0; d < 3; ++d)
+                if (al[d] > bh[d] || bl[d] > ah[d]) hit = false;
+            if (hit && n_excl && is_excluded(excl, n_excl, ((uint64_t)a << 32) | (uint64_t)b)) hit = false;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
+            const int rk = n + __popc(bal & ((1u << lane) - 1u));
+            if (SLOTS) {
+                if (rk < kRowSlots) slots[a * kRowSlots + rk] = (int32_t)b;
+            } else {
+                keys[w0 + rk] = ((uint64_t)a << 32) | (uint64_t)b;
             }
         }
+        n += __popc(bal);
+    }
+    }
     if (SLOTS && lane == 0) row_count[a] = n;
 }
 
@@ -464,26 +528,30 @@ __global__ void unpack_pairs_kernel(const uint64_t *__restrict__ keys, int64_t P
 }  // namespace
 
 void launch_seg_boxes(const double *coeffs, const double *t, const double *verts, const int64_t *loff, int64_t L,
-                      int64_t M, double *seg_box, int32_t *seg_loop, unsigned long long *loop_min_diag, int *max_exp,
-                      cudaStream_t s, float *seg_fbox) {
-    if (loop_min_diag) LC_CUDA(cudaMemsetAsync(loop_min_diag, 0xff, sizeof(unsigned long long) * (L > 0 ? L : 1), s));
+                      int64_t M, double *seg_box, int32_t *seg_loop, unsigned long long *loop_min_diag2, int *max_exp,
+                      cudaStream_t s, float *seg_fbox, unsigned long long *loop_keys, double *loop_box) {
+    if (loop_min_diag2)
+        LC_CUDA(cudaMemsetAsync(loop_min_diag2, 0xff, sizeof(unsigned long long) * (L > 0 ? L : 1), s));
     if (max_exp) LC_CUDA(cudaMemsetAsync(max_exp, 0, sizeof(int), s));
-    if (M == 0) return;
-    if (verts)
-        seg_boxes_kernel<true><<<(unsigned)ceil_div(M, 128), 128, 0, s>>>(nullptr, nullptr, verts, loff, L, M, seg_box,
-                                                                         seg_fbox, seg_loop, loop_min_diag, max_exp);
-    else
-        seg_boxes_kernel<false><<<(unsigned)ceil_div(M, 128), 128, 0, s>>>(coeffs, t, nullptr, loff, L, M, seg_box,
-                                                                          seg_fbox, seg_loop, loop_min_diag, max_exp);
-    LC_CHECK_LAUNCH();
+    if (loop_keys && L > 0) {
+        LC_CUDA(cudaMemsetAsync(loop_keys, 0xff, sizeof(unsigned long long) * 3 * L, s));
+        LC_CUDA(cudaMemsetAsync(loop_keys + 3 * L, 0, sizeof(unsigned long long) * 3 * L, s));
+    }
+    if (M > 0) {
+        if (verts)
+            seg_boxes_kernel<true><<<(unsigned)ceil_div(M, 128), 128, 0, s>>>(
+                nullptr, nullptr, verts, loff, L, M, seg_box, seg_fbox, seg_loop, loop_min_diag2, loop_keys, max_exp);
+        else
+            seg_boxes_kernel<false><<<(unsigned)ceil_div(M, 128), 128, 0, s>>>(
+                coeffs, t, nullptr, loff, L, M, seg_box, seg_fbox, seg_loop, loop_min_diag2, loop_keys, max_exp);
+        LC_CHECK_LAUNCH();
+    }
+    if (loop_keys && loop_box && L > 0) {
+        loop_keys_decode_kernel<<<(unsigned)ceil_div(L, 256), 256, 0, s>>>(loop_keys, L, loop_box);
+        LC_CHECK_LAUNCH();
+    }
 }
 
-void launch_loop_boxes(const double *seg_box, int64_t M, const int64_t *loff, int64_t L, double *loop_box,
-                       cudaStream_t s) {
-    if (L == 0) return;
-    loop_boxes_kernel<<<(unsigned)ceil_div(L * 32, 256), 256, 0, s>>>(seg_box, M, loff, L, loop_box);
-    LC_CHECK_LAUNCH();
-}
 
 // Grid culling up to the per-row pair counts and their exclusive scan (no
 // host sync): sc.offs[L] = P, *sc.counter = largest row count, slots in
@@ -493,7 +561,9 @@ static void grid_prefix(const double *loop_box, int64_t L, int64_t n_excl, PlsSc
     sc.axis.reserve(sizeof(GridParams), s);
     sc.keys.reserve(sizeof(int64_t) * (max_cells + 1), s);         // cell counts
     sc.keys_sorted.reserve(sizeof(int64_t) * (max_cells + 1), s);  // cell offsets
-    sc.sbox.reserve(sizeof(int64_t) * (max_cells + 1), s);         // scatter cursors
+    sc.sbox.reserve(sizeof(double) * 6 * L, s);                      // loop boxes in cell order
+    sc.lcell.reserve(sizeof(int32_t) * L, s);
+    sc.lrank.reserve(sizeof(int32_t) * L, s);
     sc.perm.reserve(sizeof(int32_t) * L, s);                       // loops in cell order
     sc.idx.reserve(sizeof(int) * L, s);                            // row counts
     sc.pair_keys.reserve(sizeof(int32_t) * kRowSlots * L, s);      // slots
@@ -501,7 +571,7 @@ static void grid_prefix(const double *loop_box, int64_t L, int64_t n_excl, PlsSc
     sc.offs.reserve(sizeof(int64_t) * (L + 1), s);
     sc.counter.reserve(sizeof(unsigned long long), s);
     GridParams *gp = sc.axis.as<GridParams>();
-    int64_t *cnt = sc.keys.as<int64_t>(), *coff = sc.keys_sorted.as<int64_t>(), *cur = sc.sbox.as<int64_t>();
+    int64_t *cnt = sc.keys.as<int64_t>(), *coff = sc.keys_sorted.as<int64_t>();
     int *row_count = sc.idx.as<int>(), *max_count = sc.counter.as<int>();
     sc.counts.reserve(sizeof(int64_t) * (L + 8 > 8 ? L + 8 : 8), s);
     unsigned long long *acc = (unsigned long long *)sc.counts.ptr;   // 7 ordered keys, reused below
@@ -513,7 +583,7 @@ static void grid_prefix(const double *loop_box, int64_t L, int64_t n_excl, PlsSc
     LC_CHECK_LAUNCH();
     LC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (max_cells + 1), s));
     const unsigned gl = (unsigned)ceil_div(L, 256);
-    cell_count_kernel<<<gl, 256, 0, s>>>(loop_box, L, gp, cnt);
+    cell_count_kernel<<<gl, 256, 0, s>>>(loop_box, L, gp, cnt, sc.lcell.as<int32_t>(), sc.lrank.as<int32_t>());
     LC_CHECK_LAUNCH();
     size_t b = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, b, (int64_t *)nullptr, (int64_t *)nullptr, (int)(max_cells + 1));
@@ -522,12 +592,12 @@ static void grid_prefix(const double *loop_box, int64_t L, int64_t n_excl, PlsSc
     sc.cub_tmp.reserve(b > b2 ? b : b2, s);
     b = sc.cub_tmp.bytes;
     LC_CUB(cub::DeviceScan::ExclusiveSum(sc.cub_tmp.ptr, b, cnt, coff, (int)(max_cells + 1), s));
-    LC_CUDA(cudaMemcpyAsync(cur, coff, sizeof(int64_t) * (max_cells + 1), cudaMemcpyDeviceToDevice, s));
-    cell_scatter_kernel<<<gl, 256, 0, s>>>(loop_box, L, gp, cur, sc.perm.as<int32_t>());
+    cell_scatter_kernel<<<gl, 256, 0, s>>>(loop_box, L, coff, sc.lcell.as<int32_t>(), sc.lrank.as<int32_t>(),
+                                           sc.perm.as<int32_t>(), sc.sbox.as<double>());
     LC_CHECK_LAUNCH();
     LC_CUDA(cudaMemsetAsync(max_count, 0, sizeof(int), s));
     grid_query_warp_kernel<true><<<(unsigned)ceil_div(L * 32, 256), 256, 0, s>>>(loop_box, L, gp, coff, sc.perm.as<int32_t>(),
-                                               sc.excl.as<uint64_t>(), n_excl, row_count,
+                                               sc.sbox.as<double>(), sc.excl.as<uint64_t>(), n_excl, row_count,
                                                sc.pair_keys.as<int32_t>(), nullptr, nullptr);
     LC_CHECK_LAUNCH();
     row_counts_i64_kernel<<<(unsigned)ceil_div(L + 1, 256), 256, 0, s>>>(row_count, L, sc.counts.as<int64_t>(),
@@ -567,7 +637,7 @@ int64_t run_pls(const double *loop_box, int64_t L, const uint64_t *h_excl, int64
         sc.pair_keys.reserve(sizeof(uint64_t) * P, s);
         sc.pair_keys_sorted.reserve(sizeof(uint64_t) * P, s);
         grid_query_warp_kernel<false><<<(unsigned)ceil_div(L * 32, 256), 256, 0, s>>>(loop_box, L, gp, coff, sc.perm.as<int32_t>(),
-                                                    sc.excl.as<uint64_t>(), n_excl, nullptr, nullptr,
+                                                    sc.sbox.as<double>(), sc.excl.as<uint64_t>(), n_excl, nullptr, nullptr,
                                                     sc.offs.as<int64_t>(), sc.pair_keys.as<uint64_t>());
         LC_CHECK_LAUNCH();
         size_t b3 = 0;

@@ -8,25 +8,24 @@ namespace lc {
 // Boxes are SoA: box[0*n..] lo_x, [1*n] lo_y, [2*n] lo_z, [3*n] hi_x, [4*n] hi_y, [5*n] hi_z.
 
 // Per-segment tight boxes over each segment's own domain (geometry.py:113-152);
-// seg_loop[m] = loop of segment m.  Optional outputs: loop_min_diag[l] =
-// bit pattern of the smallest segment-box diagonal of loop l (ZeroLengthInput,
-// discretize.py:124-129); *max_exp = largest exponent field of any box
-// coordinate (the exact power-of-two scale of the Gauss-sum input).
+// seg_loop[m] = loop of segment m.  Optional outputs: loop_min_diag2[l] =
+// bit pattern of the smallest squared segment-box diagonal of loop l (its
+// sqrt is the ZeroLengthInput diagonal, discretize.py:124-129); *max_exp =
+// largest exponent field of any box coordinate (the exact power-of-two scale
+// of the Gauss-sum input); seg_fbox = the boxes rounded outward to float (SoA
+// 6 x M, the discretization's prefilter copy); loop_keys (6 x L scratch) +
+// loop_box: the loop AABBs (pls.py:48-56) reduced in the same pass.
 // verts != nullptr: closed polylines given by their vertices (M,3) instead of
-// coeffs/t (the from_polyline arrays are formed in registers).  seg_fbox
-// (optional): the boxes rounded outward to float (SoA 6 x M), a conservative
-// copy for the discretization's overlap prefilter.
+// coeffs/t (the from_polyline arrays are formed in registers).
 void launch_seg_boxes(const double *coeffs, const double *t, const double *verts, const int64_t *loff, int64_t L,
-                      int64_t M, double *seg_box, int32_t *seg_loop, unsigned long long *loop_min_diag, int *max_exp,
-                      cudaStream_t s, float *seg_fbox = nullptr);
+                      int64_t M, double *seg_box, int32_t *seg_loop, unsigned long long *loop_min_diag2, int *max_exp,
+                      cudaStream_t s, float *seg_fbox = nullptr, unsigned long long *loop_keys = nullptr,
+                      double *loop_box = nullptr);
 
-// Loop AABB = union of its segment boxes (pls.py:48-56).
-void launch_loop_boxes(const double *seg_box, int64_t M, const int64_t *loff, int64_t L, double *loop_box,
-                       cudaStream_t s);
 
 struct PlsScratch {
     DevBuf keys, keys_sorted, idx, perm, sbox, counter, cub_tmp, pair_keys, pair_keys_sorted, axis, excl, counts,
-        offs;
+        offs, lcell, lrank;
     int64_t cap = 0;
 };
 
