@@ -183,11 +183,12 @@ def load_library():
     with _lib_lock:
         if _lib is not None:
             return _lib
-        if not LIB_PATH.exists():
+        path = Path(os.environ.get("LINKCERT_LIB", LIB_PATH))   # A/B builds (tools/); default in-tree
+        if not path.exists():
             raise NativeUnavailable(
-                f"{LIB_PATH} is missing; build it with `python -m paper_2106_12655_b200.build`"
+                f"{path} is missing; build it with `python -m paper_2106_12655_b200.build`"
             )
-        lib = ctypes.CDLL(str(LIB_PATH))
+        lib = ctypes.CDLL(str(path))
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(lib, name)
             fn.restype = res

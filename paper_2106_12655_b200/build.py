@@ -59,11 +59,13 @@ def _stale() -> bool:
     return any(d.stat().st_mtime > mtime for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, variant: str = "", defines=()) -> Path:
+    """variant/defines: an A/B build (e.g. -DLC_ROWS=3) into _build_<variant>/, leaving the product .so alone."""
+    lib = PKG / f"_build_{variant}" / "liblinkcert_b200.so" if variant else LIB
+    if not variant and not force and not _stale():
         return LIB
     objs = []
-    build_dir = PKG / "_build"
+    build_dir = PKG / (f"_build_{variant}" if variant else "_build")
     build_dir.mkdir(exist_ok=True)
     procs = []
     for src in _sources():
@@ -71,7 +73,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         if src.suffix == ".cpp":     # host-only code: the host compiler directly
             cmd = [CXX, *CXX_FLAGS, "-I", _fmt_include(), "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)]
         else:
-            cmd = [NVCC, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)]
+            cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", str(ROOT / "include"), "-c", str(src),
+                   "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
@@ -86,14 +89,16 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if failed:
         msg = "\n".join(f"--- {s.name}\n{o}" for s, o in failed)
         raise RuntimeError(f"nvcc failed:\n{msg}")
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static",
            *map(str, objs), "-o", str(tmp)]
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    args = sys.argv[1:]
+    var = args[args.index("--variant") + 1] if "--variant" in args else ""
+    defs = [args[k + 1] for k, a in enumerate(args) if a == "-D"]
+    print(build(force="--force" in args, verbose="-v" in args, variant=var, defines=defs))

@@ -220,10 +220,23 @@ __device__ __forceinline__ void col_step(const Col &A, Col &B, double lx, double
         for (int m = 0; m < R; ++m) acc.ang += atan2(wy[m], wx[m]);
     } else {
         // product tree (w0 w1)(w2 w3), S *= W, then renormalize S by an exact power of two
-        double ax, ay, bx, by, ux, uy, nx, ny;
-        cmul_w(wx[0], wy[0], wx[1], wy[1], ax, ay, acc.turns);
-        cmul_w(wx[2], wy[2], wx[3], wy[3], bx, by, acc.turns);
-        cmul_w(ax, ay, bx, by, ux, uy, acc.turns);
+        double ux, uy, nx, ny;
+        if (R == 4) {
+            double ax, ay, bx, by;
+            cmul_w(wx[0], wy[0], wx[1], wy[1], ax, ay, acc.turns);
+            cmul_w(wx[2], wy[2], wx[3], wy[3], bx, by, acc.turns);
+            cmul_w(ax, ay, bx, by, ux, uy, acc.turns);
+        } else {
+            ux = wx[0];
+            uy = wy[0];
+#pragma unroll
+            for (int m = 1; m < R; ++m) {
+                double tx, ty;
+                cmul_w(ux, uy, wx[m], wy[m], tx, ty, acc.turns);
+                ux = tx;
+                uy = ty;
+            }
+        }
         cmul_w(acc.sx, acc.sy, ux, uy, nx, ny, acc.turns);
         if (RENORM) {   // every second step: exact power-of-two rescale of S
             const int ex = __double2hiint(nx) & 0x7ff00000, ey = __double2hiint(ny) & 0x7ff00000;

@@ -16,7 +16,10 @@ namespace lc {
 //                 freeze F_pair and as a numerics cross-check.
 enum GaussMode : int { GAUSS_PHASE = 0, GAUSS_ATAN = 1, GAUSS_REF = 2, GAUSS_PHASE_OCC3 = 3, GAUSS_PHASE_OCC4 = 4 };
 
-constexpr int kRowsPerLane = 4;     // outer-loop (k) segments held per lane
+#ifndef LC_ROWS
+#define LC_ROWS 4
+#endif
+constexpr int kRowsPerLane = LC_ROWS;   // outer-loop (k) segments held per lane (A/B builds: -DLC_ROWS=n)
 constexpr int kMaxColsPerLane = 2048;
 
 // Per loop-pair tiling, built on the device from the pair list.

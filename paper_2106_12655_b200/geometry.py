@@ -315,6 +315,16 @@ class CurveModel:
         self.__dict__.pop("_polyline_cache", None)
         return packed
 
+    def closed_flags(self):
+        """(L,) uint8 closedness of every loop, cached with the packed arrays."""
+        coeffs, _, _ = self.packed()
+        cache = self.__dict__.get("_closed_cache")
+        if cache is not None and cache[0] is coeffs:
+            return cache[1]
+        flags = np.fromiter((lp.closed for lp in self.loops), dtype=np.uint8, count=len(self.loops))
+        self.__dict__["_closed_cache"] = (coeffs, flags)
+        return flags
+
     def polyline_vertices(self):
         """(verts (M, 3), loop_off) when every loop is a plain closed polyline whose
         arrays are exactly LoopGeometry.from_polyline's (a1 = next - start bitwise,
@@ -386,6 +396,7 @@ class CurveModel:
         model = cls(loops, xi=xi)
         model.__dict__["_packed_cache"] = (tuple(map(id, loops)), (coeffs, t, off))
         model.__dict__["_polyline_cache"] = (coeffs, (verts, off))
+        model.__dict__["_closed_cache"] = (coeffs, np.ones(L, dtype=np.uint8))
         return model
 
 

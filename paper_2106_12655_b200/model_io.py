@@ -60,7 +60,7 @@ def canonical_json(model: CurveModel):
     """Bytes of json.dumps(model_to_dict(model), sort_keys=True, separators=(",", ":")),
     formatted by the library's multithreaded writer (csrc/digest.cpp)."""
     coeffs, t, off = model.packed()
-    closed = np.fromiter((lp.closed for lp in model.loops), dtype=np.uint8, count=model.num_loops)
+    closed = model.closed_flags()
     blob = _native.model_json(coeffs, t, off, None if closed.all() else closed)
     if blob is None:
         raise ValidationError("cannot serialize non-finite coordinate")
@@ -74,7 +74,7 @@ def model_digest(model: CurveModel) -> str:
     cores with the GIL released, so callers can overlap it with GPU work.
     """
     coeffs, t, off = model.packed()
-    closed = np.fromiter((lp.closed for lp in model.loops), dtype=np.uint8, count=model.num_loops)
+    closed = model.closed_flags()
     digest = _native.model_digest(coeffs, t, off, None if closed.all() else closed)
     if digest is None:
         raise ValidationError("cannot serialize non-finite coordinate")
