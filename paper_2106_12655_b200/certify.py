@@ -272,11 +272,11 @@ def device_step(ctx, xi, excl_keys, params, mode=None, timings=None):
     return pairs, raw, lk, flags
 
 
-def run_device_pipeline(model: CurveModel, excluded=(), params=None, timings=None, ctx=None):
+def run_device_pipeline(model: CurveModel, excluded=(), params=None, timings=None, ctx=None, snapshot=None):
     """Upload the packed model, then device_step.  Returns (pairs, raw, lk, flags, ctx)."""
     params = params or DiscretizationParams()
     t0 = time.perf_counter()
-    ctx = upload(model, ctx)
+    ctx = upload(model, ctx, snapshot)
     if timings is not None:
         timings["upload"] = time.perf_counter() - t0
     pairs, raw, lk, flags = device_step(ctx, model.xi, excluded_keys(excluded), params, timings=timings)
@@ -288,14 +288,14 @@ def run_device_pipeline(model: CurveModel, excluded=(), params=None, timings=Non
 _digest_pool = None
 
 
-def _digest_async(model):
+def _digest_async(model, snapshot=None):
     """model_digest on a helper thread (native, GIL released) to overlap it with the GPU."""
     global _digest_pool
     if _digest_pool is None:
         from concurrent.futures import ThreadPoolExecutor
 
         _digest_pool = ThreadPoolExecutor(max_workers=1, thread_name_prefix="linkcert-digest")
-    return _digest_pool.submit(model_digest, model)
+    return _digest_pool.submit(model_digest, model, snapshot)
 
 
 def _raise_for_flags(raw, flags, order=None):
@@ -362,9 +362,10 @@ def compute_linking_matrix(
             timings.update(pls=0.0, discretize=0.0, kernel=0.0)
         digest = model_digest(model)
     else:
-        fut = _digest_async(model)
+        snap = model.snapshot()
+        fut = _digest_async(model, snap)
         try:
-            pairs, raw, lk, flags, _ = run_device_pipeline(model, excluded, params, timings)
+            pairs, raw, lk, flags, _ = run_device_pipeline(model, excluded, params, timings, snapshot=snap)
             _raise_for_flags(raw, flags)
         except Exception:
             fut.result()          # a serialization error would have surfaced last in the reference
@@ -397,7 +398,8 @@ def verify(
         )
     # the digest (host, native) overlaps the device pipeline; its check and
     # warning come first, as in the reference (certify.py:188-193)
-    fut = _digest_async(model)
+    snap = model.snapshot()
+    fut = _digest_async(model, snap)
     try:
         if model.num_loops < 1:
             raise ValidationError("model has no loops")
@@ -407,7 +409,7 @@ def verify(
             lk = np.zeros(0, dtype=np.int64)
             flags = np.zeros(0, dtype=np.uint8)
         else:
-            pairs, raw, lk, flags, _ = run_device_pipeline(model, excluded, params)
+            pairs, raw, lk, flags, _ = run_device_pipeline(model, excluded, params, snapshot=snap)
     except Exception:
         _warn_digest(fut.result(), reference)
         raise

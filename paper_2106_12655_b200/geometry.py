@@ -317,7 +317,9 @@ class CurveModel:
 
     def closed_flags(self):
         """(L,) uint8 closedness of every loop, cached with the packed arrays."""
-        coeffs, _, _ = self.packed()
+        return self._closed_of(self.packed()[0])
+
+    def _closed_of(self, coeffs):
         cache = self.__dict__.get("_closed_cache")
         if cache is not None and cache[0] is coeffs:
             return cache[1]
@@ -330,7 +332,9 @@ class CurveModel:
         arrays are exactly LoopGeometry.from_polyline's (a1 = next - start bitwise,
         a2 = a3 = 0, t = [0, 1]) — then only the vertices need to reach the GPU.
         None otherwise.  Cached with the packed arrays."""
-        coeffs, t, off = self.packed()
+        return self._poly_of(*self.packed())
+
+    def _poly_of(self, coeffs, t, off):
         cache = self.__dict__.get("_polyline_cache")
         if cache is not None and cache[0] is coeffs:
             return cache[1]
@@ -344,6 +348,13 @@ class CurveModel:
                 result = (np.ascontiguousarray(a0), off)
         self.__dict__["_polyline_cache"] = (coeffs, result)
         return result
+
+    def snapshot(self):
+        """(coeffs, t, loop_off, closed, polyline) of the current loops after a single
+        cache check — what one verify / certificate call hands to the digest
+        thread and to the device upload."""
+        coeffs, t, off = self.packed()
+        return coeffs, t, off, self._closed_of(coeffs), self._poly_of(coeffs, t, off)
 
     @classmethod
     def from_polyline_arrays(cls, verts, offsets, closed=True):

@@ -67,14 +67,13 @@ def canonical_json(model: CurveModel):
     return blob
 
 
-def model_digest(model: CurveModel) -> str:
+def model_digest(model: CurveModel, snapshot=None) -> str:
     """SHA-256 hex digest of the canonical json-curves serialization (model_io.py:169-172).
 
     Formatting and hashing run in the library (csrc/digest.cpp) on all host
     cores with the GIL released, so callers can overlap it with GPU work.
     """
-    coeffs, t, off = model.packed()
-    closed = model.closed_flags()
+    coeffs, t, off, closed, _ = snapshot if snapshot is not None else model.snapshot()
     digest = _native.model_digest(coeffs, t, off, None if closed.all() else closed)
     if digest is None:
         raise ValidationError("cannot serialize non-finite coordinate")

@@ -84,14 +84,13 @@ def excluded_keys(excluded):
     return np.unique((arr[:, 0] << np.uint64(32)) | arr[:, 1])
 
 
-def upload(model: CurveModel, ctx=None):
-    """Stage the model's packed arrays on the device (segment + loop boxes)."""
+def upload(model: CurveModel, ctx=None, snapshot=None):
+    """Stage the model's packed arrays on the device (boxes are derived per run)."""
     ctx = ctx or _native.context()
-    poly = model.polyline_vertices()
+    coeffs, t, off, _, poly = snapshot if snapshot is not None else model.snapshot()
     if poly is not None:            # 24 B/segment instead of 112 B/segment over PCIe
         ctx.upload_model_polylines(*poly)
     else:
-        coeffs, t, off = model.packed()
         ctx.upload_model(coeffs, t, off)
     return ctx
 
