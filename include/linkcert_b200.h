@@ -170,7 +170,8 @@ LC_API int lc_result_views(lc_ctx *ctx, void **pairs, void **raw, void **lk, voi
 /* Path of the last lc_run_pipeline: 0 staged, 1 fused, 2 fused replayed from
  * the captured CUDA graph (same shape as the previous run, no reallocation). */
 LC_API int lc_last_run_fused(lc_ctx *ctx);
-/* Device times (ms) of the last pipeline: [PLS, discretize, Gauss kernel, reduce]. */
+/* Device times (ms) of the last pipeline: [derive + PLS, discretize, Gauss kernel, reduce,
+ * first stage start -> reduce end] (ms must hold 5 floats). */
 LC_API int lc_stage_times(lc_ctx *ctx, float *ms);
 
 /* ---- Canonical model serialization (host, multithreaded) ----

@@ -412,6 +412,7 @@ int lc_stage_times(lc_ctx *ctx, float *ms) {
         ms[1] = p.stage_ms(EV_PLS, EV_DISC);
         ms[2] = p.stage_ms(EV_GAUSS0, EV_GAUSS1);
         ms[3] = p.stage_ms(EV_GAUSS1, EV_END);
+        ms[4] = p.stage_ms(EV_BEGIN, EV_END);
     });
 }
 

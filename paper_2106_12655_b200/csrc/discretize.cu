@@ -1232,19 +1232,41 @@ bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc,
 
 // Fused pipeline, no-refinement case (see discretize.cuh).  Mirrors the
 // pass-1 + splits == 0 branch of run_discretize kernel for kernel.
-void launch_discretize_fast(const DiscInput &in, const int64_t *d_P, const DiscParams &prm, DiscScratch &sc,
-                            DiscOutput &out, cudaStream_t s, const PreCounters **d_ctr) {
+void reserve_discretize_fast(const DiscInput &in, DiscScratch &sc, DiscOutput &out, cudaStream_t s) {
     const int64_t L = in.L, M = in.M, Pcap = in.P;
-    const double min_diam = prm.epsilon * prm.xi;
-    const double poly_thr = kMachineEps * prm.xi;
     sc.paired.reserve(L > 0 ? L : 1, s);
     sc.pair_axis.reserve(Pcap > 0 ? Pcap : 1, s);
     sc.prectr.reserve(sizeof(PreCounters), s);
     sc.val_flags.reserve(sizeof(unsigned) * (L > 0 ? L : 1), s);
     sc.val_err2.reserve(2 * sizeof(int), s);
+    out.vert_off.reserve(sizeof(int64_t) * (L + 1), s);
+    out.voff.reserve(sizeof(int64_t) * (L + 1), s);
+    out.X.reserve(sizeof(double) * (M + L + 1), s);
+    out.Y.reserve(sizeof(double) * (M + L + 1), s);
+    out.Z.reserve(sizeof(double) * (M + L + 1), s);
+}
+
+void launch_discretize_chords(const DiscInput &in, const DiscParams &prm, DiscScratch &sc, DiscOutput &out,
+                              cudaStream_t s) {
+    const int64_t L = in.L, M = in.M;
+    const double poly_thr = kMachineEps * prm.xi;
+    out.passes = 1;
+    out.splits = 0;
+    out.V = M;
+    out.Vc = M + L;
+    LC_CUDA(cudaMemcpyAsync(out.vert_off.ptr, in.loff, sizeof(int64_t) * (L + 1), cudaMemcpyDeviceToDevice, s));
+    closed_offsets_kernel<<<grid_for(L + 1), 256, 0, s>>>(in.loff, L, out.voff.as<int64_t>());
+    LC_CHECK_LAUNCH();
+    LC_CUDA(cudaMemsetAsync(sc.val_flags.ptr, 0, sizeof(unsigned) * (L > 0 ? L : 1), s));
+    launch_write_all(in, poly_thr, out, sc.val_flags.as<unsigned>(), s);
+}
+
+void launch_discretize_checks(const DiscInput &in, const int64_t *d_P, const DiscParams &prm, DiscScratch &sc,
+                              DiscOutput &out, cudaStream_t s, cudaEvent_t chords_done, const PreCounters **d_ctr) {
+    const int64_t L = in.L, M = in.M, Pcap = in.P;
+    const double min_diam = prm.epsilon * prm.xi;
     PreCounters *ctr = sc.prectr.as<PreCounters>();
     LC_CUDA(cudaMemsetAsync(sc.paired.ptr, 0, L > 0 ? L : 1, s));
-    LC_CUDA(cudaMemsetAsync(sc.val_flags.ptr, 0, sizeof(unsigned) * (L > 0 ? L : 1), s));
     fast_init_kernel<<<1, 1, 0, s>>>(ctr, sc.val_err2.as<int>());
     LC_CHECK_LAUNCH();
     if (Pcap > 0) {
@@ -1256,7 +1278,6 @@ void launch_discretize_fast(const DiscInput &in, const int64_t *d_P, const DiscP
         pre_loops_kernel<<<grid_for(L), 256, 0, s>>>(in.loop_min_diag, sc.paired.as<uint8_t>(), L, min_diam, ctr);
         LC_CHECK_LAUNCH();
     }
-    const ActView view0{nullptr, in.seg_loop, in.t, in.t + 1, 2, in.seg_box, M > 0 ? M : 1, in.loff};
     if (Pcap > 0 && M > 0) {
         const int64_t blocks = ceil_div(Pcap, kAnyWarps) < 148 * 8 ? ceil_div(Pcap, kAnyWarps) : 148 * 8;
         brute_any_kernel<<<(unsigned)blocks, 32 * kAnyWarps, 0, s>>>(in.seg_box, in.seg_fbox, M, in.loff,
@@ -1264,19 +1285,7 @@ void launch_discretize_fast(const DiscInput &in, const int64_t *d_P, const DiscP
                                                                      &ctr->marked);
         LC_CHECK_LAUNCH();
     }
-    out.passes = 1;
-    out.splits = 0;
-    out.V = M;
-    out.Vc = M + L;
-    out.vert_off.reserve(sizeof(int64_t) * (L + 1), s);
-    out.voff.reserve(sizeof(int64_t) * (L + 1), s);
-    out.X.reserve(sizeof(double) * (out.Vc + 1), s);
-    out.Y.reserve(sizeof(double) * (out.Vc + 1), s);
-    out.Z.reserve(sizeof(double) * (out.Vc + 1), s);
-    LC_CUDA(cudaMemcpyAsync(out.vert_off.ptr, in.loff, sizeof(int64_t) * (L + 1), cudaMemcpyDeviceToDevice, s));
-    closed_offsets_kernel<<<grid_for(L + 1), 256, 0, s>>>(in.loff, L, out.voff.as<int64_t>());
-    LC_CHECK_LAUNCH();
-    launch_write_all(in, poly_thr, out, sc.val_flags.as<unsigned>(), s);
+    if (chords_done) LC_CUDA(cudaStreamWaitEvent(s, chords_done, 0));   // validation reads the chord flags
     if (L > 0) {
         validate_loops2_kernel<<<grid_for(L), 256, 0, s>>>(in.loff, L, sc.paired.as<uint8_t>(),
                                                            sc.val_flags.as<unsigned>(), sc.val_err2.as<int>());
@@ -1285,6 +1294,13 @@ void launch_discretize_fast(const DiscInput &in, const int64_t *d_P, const DiscP
     out.d_val_err = sc.val_err2.as<int>();
     out.validation_pending = true;
     *d_ctr = ctr;
+}
+
+void launch_discretize_fast(const DiscInput &in, const int64_t *d_P, const DiscParams &prm, DiscScratch &sc,
+                            DiscOutput &out, cudaStream_t s, const PreCounters **d_ctr) {
+    reserve_discretize_fast(in, sc, out, s);
+    launch_discretize_chords(in, prm, sc, out, s);
+    launch_discretize_checks(in, d_P, prm, sc, out, s, nullptr, d_ctr);
 }
 
 }  // namespace lc

@@ -100,6 +100,15 @@ bool run_discretize(const DiscInput &in, const DiscParams &prm, DiscScratch &sc,
 // reruns run_discretize.
 void launch_discretize_fast(const DiscInput &in, const int64_t *d_P, const DiscParams &prm, DiscScratch &sc,
                             DiscOutput &out, cudaStream_t s, const PreCounters **d_ctr);
+// The same as two independent branches (no allocation inside; reserve first):
+// chords (needs only the model: closed offsets, chord write + PolylineLoop
+// flags) and checks (needs the pairs: pre-pass, pass-1 detection, then —
+// after `chords_done` — the validation ranking).
+void reserve_discretize_fast(const DiscInput &in, DiscScratch &sc, DiscOutput &out, cudaStream_t s);
+void launch_discretize_chords(const DiscInput &in, const DiscParams &prm, DiscScratch &sc, DiscOutput &out,
+                              cudaStream_t s);
+void launch_discretize_checks(const DiscInput &in, const int64_t *d_P, const DiscParams &prm, DiscScratch &sc,
+                              DiscOutput &out, cudaStream_t s, cudaEvent_t chords_done, const PreCounters **d_ctr);
 
 // Unscaled AoS (V, 3) vertices (no closing vertices) from a DiscOutput.
 void unpack_polylines(const DiscOutput &out, int64_t L, const int *max_exp, double *aos, cudaStream_t s);

@@ -269,12 +269,31 @@ __device__ double lane_strip(const double *__restrict__ X, const double *__restr
     col_fill<MODE != GAUSS_PHASE>(A, __ldg(px + c0), __ldg(py + c0), __ldg(pz + c0), kv);
     Acc acc;
     int c = c0;
+#ifdef LC_PREFETCH_COLS
+    // column vertices of the next double step loaded one iteration ahead
+    // (clamped index: the closing vertex at ncols always exists)
+    double n1x = __ldg(px + min(c + 1, c1)), n1y = __ldg(py + min(c + 1, c1)), n1z = __ldg(pz + min(c + 1, c1));
+    double n2x = __ldg(px + min(c + 2, c1)), n2y = __ldg(py + min(c + 2, c1)), n2z = __ldg(pz + min(c + 2, c1));
+    for (; c + 2 <= c1; c += 2) {
+        const double l1x = n1x, l1y = n1y, l1z = n1z, l2x = n2x, l2y = n2y, l2z = n2z;
+        const int q1 = min(c + 3, c1), q2 = min(c + 4, c1);
+        n1x = __ldg(px + q1);
+        n1y = __ldg(py + q1);
+        n1z = __ldg(pz + q1);
+        n2x = __ldg(px + q2);
+        n2y = __ldg(py + q2);
+        n2z = __ldg(pz + q2);
+        col_step<MODE, FULL, false>(A, B, l1x, l1y, l1z, kv, rv, acc);
+        col_step<MODE, FULL, true>(B, A, l2x, l2y, l2z, kv, rv, acc);
+    }
+#else
     for (; c + 2 <= c1; c += 2) {
         const double l1x = __ldg(px + c + 1), l1y = __ldg(py + c + 1), l1z = __ldg(pz + c + 1);
         const double l2x = __ldg(px + c + 2), l2y = __ldg(py + c + 2), l2z = __ldg(pz + c + 2);
         col_step<MODE, FULL, false>(A, B, l1x, l1y, l1z, kv, rv, acc);
         col_step<MODE, FULL, true>(B, A, l2x, l2y, l2z, kv, rv, acc);
     }
+#endif
     if (c < c1) col_step<MODE, FULL, true>(A, B, __ldg(px + c + 1), __ldg(py + c + 1), __ldg(pz + c + 1), kv, rv, acc);
     if (MODE == GAUSS_PHASE && (acc.bad || !isfinite(acc.sx) || !isfinite(acc.sy)))
         // coincident vertices, w == 0, underflow or NaN input: the exact per-pair path
@@ -331,10 +350,20 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) gauss_items_kernel(
     __shared__ double ksh[KSM ? 3 * (R + 1) * kCtaThreads : 1];
     const int lane = threadIdx.x & 31;
     if (d_end && *d_end < item_end) item_end = *d_end;   // fused path: item count on the device
+#ifdef LC_PREFETCH_ITEM
+    // the next item index is claimed while the current one is evaluated
+    unsigned long long k_next = 0;
+    if (lane == 0) k_next = atomicAdd(counter, 1ULL);
+#endif
     for (;;) {
         unsigned long long k = 0;
+#ifdef LC_PREFETCH_ITEM
+        k = __shfl_sync(0xffffffffu, k_next, 0);
+        if (lane == 0 && item_begin + (int64_t)k < item_end) k_next = atomicAdd(counter, 1ULL);
+#else
         if (lane == 0) k = atomicAdd(counter, 1ULL);
         k = __shfl_sync(0xffffffffu, k, 0);
+#endif
         const int64_t it = item_begin + (int64_t)k;
         if (it >= item_end) break;
         const int64_t p = item_pair ? (int64_t)__ldg(item_pair + it) : find_pair(item_off, P, it);

@@ -68,6 +68,9 @@ __global__ void export_results_kernel(const int64_t *__restrict__ dP, int64_t ca
 void Pipeline::init(cudaStream_t st) {
     s = st;
     for (auto &e : ev) LC_CUDA(cudaEventCreate(&e));
+    for (auto &x : side) LC_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+    for (cudaEvent_t *e : {&ev_fork, &ev_chords, &ev_pairs, &ev_checks})
+        LC_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
 }
 
 void Pipeline::release() {
@@ -95,17 +98,22 @@ void Pipeline::release() {
     graph_exec = nullptr;
     for (auto &e : ev)
         if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : {ev_fork, ev_chords, ev_pairs, ev_checks})
+        if (e) cudaEventDestroy(e);
+    for (auto &x : side)
+        if (x) cudaStreamDestroy(x);
 }
 
 // Stage event on the stream; inside a stream capture it must become an
 // external event-record node to stay usable for timing after graph replays.
-void Pipeline::record(int e) {
+void Pipeline::record(int e, cudaStream_t st) {
+    if (!st) st = s;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    LC_CUDA(cudaStreamIsCapturing(s, &cs));
+    LC_CUDA(cudaStreamIsCapturing(st, &cs));
     if (cs == cudaStreamCaptureStatusActive)
-        LC_CUDA(cudaEventRecordWithFlags(ev[e], s, cudaEventRecordExternal));
+        LC_CUDA(cudaEventRecordWithFlags(ev[e], st, cudaEventRecordExternal));
     else
-        LC_CUDA(cudaEventRecord(ev[e], s));
+        LC_CUDA(cudaEventRecord(ev[e], st));
 }
 
 float Pipeline::stage_ms(int e0, int e1) {
@@ -407,7 +415,10 @@ void Pipeline::download_results_pinned() {
 int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscParams &prm, int mode) {
     if (!model_ready || L < 2 || M == 0 || prm.max_passes < 1) return FAST_FALLBACK;
     if (mode < GAUSS_PHASE || mode > 6) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
-    const int64_t pcap = (int64_t)kRowSlots * L;
+    // pair capacity: the grid PLS bound (16 per row) until a run has shown the
+    // model's pair count; then that plus headroom (smaller grids and scans)
+    int64_t pcap = (int64_t)kRowSlots * L;
+    if (pairs_seen > 0 && pairs_seen + pairs_seen / 4 + 1024 < pcap) pcap = pairs_seen + pairs_seen / 4 + 1024;
     const int64_t icap = items_cap > pcap ? items_cap : pcap;
     h_res_P = -1;
     polylines_ready = false;
@@ -441,6 +452,12 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
                      d_model_exp.as<int>(), L, M, d_pairs.as<int32_t>(), pcap};
         in.verts = model_poly ? d_verts_in.as<double>() : nullptr;
         in.seg_fbox = d_seg_fbox.as<float>();
+        reserve_discretize_fast(in, disc_sc, dout, s);
+        // branch 1: the chords need only the model — they run beside the PLS
+        LC_CUDA(cudaEventRecord(ev_fork, s));
+        LC_CUDA(cudaStreamWaitEvent(side[0], ev_fork, 0));
+        launch_discretize_chords(in, prm, disc_sc, dout, side[0]);
+        LC_CUDA(cudaEventRecord(ev_chords, side[0]));
         if (n_excl > 0)
             LC_CUDA(cudaMemcpyAsync(pls_sc.excl.ptr, h_excl.ptr, sizeof(uint64_t) * n_excl, cudaMemcpyHostToDevice,
                                     s));
@@ -448,8 +465,14 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
         const int *dmx = nullptr;
         launch_pls_grid(d_loop_box.as<double>(), L, n_excl, pls_sc, d_pairs.as<int32_t>(), pcap, s, &dP, &dmx);
         record(EV_PLS);
-        launch_discretize_fast(in, dP, prm, disc_sc, dout, s, &ctr);
-        record(EV_DISC);
+        // branch 2: pass-1 detection + validation only feed the status — they run
+        // beside the work items and the Gauss sum
+        LC_CUDA(cudaEventRecord(ev_pairs, s));
+        LC_CUDA(cudaStreamWaitEvent(side[1], ev_pairs, 0));
+        launch_discretize_checks(in, dP, prm, disc_sc, dout, side[1], ev_chords, &ctr);
+        record(EV_DISC, side[1]);
+        LC_CUDA(cudaEventRecord(ev_checks, side[1]));
+        LC_CUDA(cudaStreamWaitEvent(s, ev_chords, 0));   // items read the closed offsets, the sum the chords
         build_items(d_pairs.as<int32_t>(), pcap, dout.voff.as<int64_t>(), d_pg.as<PairGeom>(),
                     d_item_off.as<int64_t>(), d_scan.ptr, d_scan.bytes, s, false, dP);
         const int64_t *d_items = d_item_off.as<int64_t>() + pcap;
@@ -462,6 +485,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
         launch_reduce_pairs(d_partials.as<double>(), d_item_off.as<int64_t>(), pcap, d_raw.as<double>(),
                             d_lk.as<int64_t>(), d_flags.as<uint8_t>(), s, dP);
         record(EV_END);
+        LC_CUDA(cudaStreamWaitEvent(s, ev_checks, 0));
         export_results_kernel<<<148, 256, 0, s>>>(dP, pcap, d_items, dmx, ctr, dout.d_val_err, d_pairs.as<int2>(),
                                                   d_raw.as<double>(), d_lk.as<int64_t>(), d_flags.as<uint8_t>(), st,
                                                   reinterpret_cast<int2 *>(hp), reinterpret_cast<double *>(hr),
@@ -531,7 +555,9 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
 
     const FastStatus f = *st;
     if (f.n_items > items_cap) items_cap = f.n_items;
-    if (f.max_row > kRowSlots || f.zero_loop != INT_MAX || f.n_large != 0 || f.marked != 0 || f.n_items > icap)
+    if (f.P > pairs_seen) pairs_seen = f.P;
+    if (f.max_row > kRowSlots || f.P > pcap || f.zero_loop != INT_MAX || f.n_large != 0 || f.marked != 0 ||
+        f.n_items > icap)
         return FAST_FALLBACK;
     // the run was the reference's: adopt its sizes as the pipeline state
     P = f.P;

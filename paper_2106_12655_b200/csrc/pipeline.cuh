@@ -23,6 +23,9 @@ enum StageEvent : int { EV_BEGIN = 0, EV_PLS, EV_DISC, EV_GAUSS0, EV_GAUSS1, EV_
 struct Pipeline {
     cudaStream_t s = nullptr;
     cudaEvent_t ev[EV_COUNT] = {};
+    // fused run: side branches (chord write || PLS; pass-1 checks || items + Gauss sum)
+    cudaStream_t side[2] = {};
+    cudaEvent_t ev_fork = nullptr, ev_chords = nullptr, ev_pairs = nullptr, ev_checks = nullptr;
 
     // Model: packed monomial cubics (linkcert LoopGeometry arrays, geometry.py:206-296).
     DevBuf d_coeffs, d_t, d_loff, d_seg_box, d_seg_fbox, d_loop_keys, d_seg_loop, d_loop_box, d_min_diag, d_model_exp, d_verts_in;
@@ -104,6 +107,7 @@ struct Pipeline {
     // refinement / the sweep path / larger buffers: run the staged pipeline).
     int run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscParams &prm, int mode);
     int64_t items_cap = 0;
+    int64_t pairs_seen = 0;   // largest pair count of a fused run (sizes the next run's capacity)
     // The fused sequence is replayed as a CUDA graph once a run with the same
     // shape (FastKey) and the same buffer generation has completed uncaptured.
     struct FastKey {
@@ -126,7 +130,7 @@ struct Pipeline {
     void segment_pair_lambda(const double *quads, int64_t n, double *out);
 
     float stage_ms(int e0, int e1);
-    void record(int e);
+    void record(int e, cudaStream_t st = nullptr);
 
   private:
     void finish_items();

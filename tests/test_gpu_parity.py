@@ -339,3 +339,25 @@ def test_fused_graph_replay_bitwise(monkeypatch):
         for a, b in zip(want, got):
             assert np.array_equal(a, np.asarray(b)) and np.asarray(b).dtype == a.dtype
     assert paths[0] >= 1 and 2 in paths, paths
+
+
+def test_fused_pair_capacity_growth(monkeypatch, cert_models):
+    """The pair capacity follows the largest pair count seen on a context: a model
+    with more pairs than that overflows it once (staged fallback, same results),
+    and the next fused run is sized for it."""
+    from paper_2106_12655_b200.certify import run_device_pipeline
+
+    big = cert_models["e4in1_32x32"]    # 2,945 pairs > the capacity a 6x6 grid leaves
+    monkeypatch.setenv("LINKCERT_FUSED", "0")
+    want = [np.array(a).copy() for a in run_device_pipeline(big)[:4]]
+    monkeypatch.setenv("LINKCERT_FUSED", "1")
+    ctx = _native.Context()
+    run_device_pipeline(cert_models["grid6"], ctx=ctx)
+    assert ctx.last_run_fused() == 1
+    paths = []
+    for _ in range(3):
+        *got, _ = run_device_pipeline(big, ctx=ctx)
+        paths.append(ctx.last_run_fused())
+        for a, b in zip(want, got):
+            assert np.array_equal(a, np.asarray(b))
+    assert paths[0] == 0 and paths[1] >= 1, paths
