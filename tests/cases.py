@@ -99,3 +99,27 @@ def disc_error_cases():
         "tight_budget": (tight, [(0, 1)], {"max_subsegments": 1}),
         "zero_length": (zero, [(0, 1)], {}),
     }
+
+
+def _returning_loop(off):
+    """Closed 4-segment cubic loop whose first segment returns to its start
+    point (non-degenerate tight box, zero-length chord)."""
+    p0, p1, p2 = (np.array(v, dtype=np.float64) + off for v in ([0, 0, 0], [4, 0, 0], [2, 3, 0]))
+    c = np.zeros((4, 4, 3))
+    c[0, 0], c[0, 1], c[0, 2], c[0, 3] = p0, [3, 0, 1], [-3, 3, 0], [0, -3, -1]
+    c[1, 0], c[1, 1] = p0, p1 - p0
+    c[2, 0], c[2, 1] = p1, p2 - p1
+    c[3, 0], c[3, 1] = p2, p0 - p2
+    return LoopGeometry(c)
+
+
+def validation_cases():
+    """name -> model whose chords fail PolylineLoop validation with no refinement
+    pass (compute_linking_matrix raises ValidationError): unpaired and paired."""
+    def tri(off, s=1.0):
+        return LoopGeometry.from_polyline(np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0.0]]) * s + np.asarray(off))
+
+    return {
+        "returning_unpaired": CurveModel([_returning_loop(np.zeros(3)), tri([50.0, 0.0, 0.0])]),
+        "returning_paired": CurveModel([_returning_loop(np.zeros(3)), tri([1.5, 1.0, 0.1], 0.3)]),
+    }

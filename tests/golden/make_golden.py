@@ -152,6 +152,20 @@ def main(full=False):
         print(name, errs[name], flush=True)
     out_json["discretize"] = errs
 
+    # 6. chord validation errors through the whole pipeline
+    vals = {}
+    for name, m in cases.validation_cases().items():
+        rm = to_ref(m)
+        try:
+            ref.compute_linking_matrix(rm)
+            vals[name] = {"ok": True}
+        except ref.ValidationError as e:
+            vals[name] = {"ok": False, "message": str(e)}
+        vals[name]["fingerprint"] = fingerprint(m)
+        vals[name]["pairs"] = [list(p) for p in ref.potential_link_search(rm)]
+        print(name, vals[name], flush=True)
+    out_json["validation"] = vals
+
     with open(HERE / "golden.json", "w") as f:
         json.dump(out_json, f, indent=1, sort_keys=True)
     np.savez_compressed(HERE / "golden_arrays.npz", **arrays)

@@ -298,6 +298,8 @@ def test_fused_matches_staged(monkeypatch, cert_models):
         runs["edit_" + name] = (after, (), None)
     for name, (m, _, kw) in cases.disc_error_cases().items():
         runs["disc_" + name] = (m, (), lc.DiscretizationParams(**kw))
+    for name, m in cases.validation_cases().items():
+        runs["val_" + name] = (m, (), None)
     a, b = cases.circ(16, (0, 0, 0), ex, ey), cases.circ(16, (1.0, 0, 0), ez, ex)
     hopf = lc.CurveModel([lc.LoopGeometry.from_polyline(p) for p in (a, b)])
     runs["hopf_excluded"] = (hopf, {(1, 0)}, None)
@@ -361,3 +363,20 @@ def test_fused_pair_capacity_growth(monkeypatch, cert_models):
         for a, b in zip(want, got):
             assert np.array_equal(a, np.asarray(b))
     assert paths[0] == 0 and paths[1] >= 1, paths
+
+
+@pytest.mark.parametrize("name", list(cases.validation_cases()))
+def test_pipeline_validation_errors(golden, monkeypatch, name):
+    """A chord PolylineLoop failure through the whole pipeline raises the reference's
+    ValidationError on the fused path (read back with the run's status) and on the
+    staged path alike."""
+    g = golden["validation"][name]
+    m = cases.validation_cases()[name]
+    assert cases.fingerprint(m) == g["fingerprint"]
+    assert [list(p) for p in lc.potential_link_search(m)] == g["pairs"]
+    for fused in ("1", "0"):
+        monkeypatch.setenv("LINKCERT_FUSED", fused)
+        with pytest.raises(lc.ValidationError) as e:
+            lc.compute_linking_matrix(m)
+        assert str(e.value) == g["message"]
+        assert _native.context().last_run_fused() == (1 if fused == "1" else 0)

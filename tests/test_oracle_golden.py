@@ -93,3 +93,16 @@ def test_verify_lists(oracle, golden, golden_arrays, name):
     assert [list(p) for p in destroyed] == g["full"]["destroyed"]
     assert [list(p) for p in created] == g["full"]["created"]
     assert [list(p) for p in changed] == g["full"]["changed"]
+
+
+@pytest.mark.parametrize("name", list(cases.validation_cases()))
+def test_chord_validation_errors(oracle, golden, name):
+    """Chords that fail PolylineLoop validation without refinement (golden from the reference)."""
+    g = golden["validation"][name]
+    m = cases.validation_cases()[name]
+    assert cases.fingerprint(m) == g["fingerprint"]
+    coeffs, t, off = m.packed()
+    assert [list(p) for p in oracle.pls(coeffs, t, off)] == g["pairs"]
+    with pytest.raises(oracle.OracleValidationError) as e:
+        oracle.discretize(coeffs, t, off, m.xi, [tuple(p) for p in g["pairs"]])
+    assert not g["ok"] and str(e.value) == g["message"]
