@@ -217,7 +217,8 @@ def main():
             if k >= args.warmup:
                 launches.append(_native.launch_count() - n0)
                 step_ms.append(e0.elapsed_time(e1))
-                gauss_ms.append(ctx.stage_times()["gauss"] if world == 1 else ctx.gauss_event_ms())
+                gauss_ms.append(ctx.stage_times()["gauss"] if (world == 1 or ctx.last_run_fused())
+                                else ctx.gauss_event_ms())
             if n_sp is None:
                 _, voff = ctx.get_polylines()
                 n_sp = seg_pairs(pairs, voff)

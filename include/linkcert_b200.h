@@ -167,6 +167,19 @@ LC_API int lc_get_results(lc_ctx *ctx, double *raw, int64_t *lk, uint8_t *flags)
  * memory: pairs int32 (P,2), raw f64 (P), lk int64 (P), flags u8 (P).  Valid
  * until the next pipeline call on this context. */
 LC_API int lc_result_views(lc_ctx *ctx, void **pairs, void **raw, void **lk, void **flags, int64_t *n_pairs);
+/* Sharded fused run (one process per GPU, all ranks on the same model):
+ * as lc_run_pipeline, but the Gauss kernel evaluates only item slice `shard`
+ * (ceil(n_items / shards) items) into the library's device partials buffer
+ * (*partials_dev, indexed by absolute item id).  The caller all-gathers the
+ * slices (NCCL) into one array and calls lc_shard_reduce; results then come
+ * from lc_result_views.  *n_items = -1: the model needs the staged path
+ * (lc_potential_link_search / lc_discretize / lc_prepare_gauss / lc_gauss_run). */
+LC_API int lc_run_pipeline_shard(lc_ctx *ctx, const uint64_t *excluded_keys, int64_t n_excl, double xi,
+                                 double epsilon, int max_passes, int64_t max_subsegments, int mode, int shard,
+                                 int shards, int64_t *n_pairs, int64_t *n_items, double **partials_dev);
+/* Fixed-order per-pair reduction of the gathered partials of a sharded run
+ * (bitwise the single-GPU sums) + results into pinned memory. */
+LC_API int lc_shard_reduce(lc_ctx *ctx, const double *partials_all_dev);
 /* Path of the last lc_run_pipeline: 0 staged, 1 fused, 2 fused replayed from
  * the captured CUDA graph (same shape as the previous run, no reallocation). */
 LC_API int lc_last_run_fused(lc_ctx *ctx);

@@ -81,6 +81,11 @@ SIGNATURES = {
     "lc_model_json": (ctypes.c_int64, [_vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, ctypes.c_int64]),
     "lc_float_repr": (ctypes.c_int, [ctypes.c_double, ctypes.c_char_p]),
     "lc_last_run_fused": (ctypes.c_int, [_vp]),
+    "lc_run_pipeline_shard": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                                             ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                             ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
+                                             ctypes.POINTER(_vp)]),
+    "lc_shard_reduce": (ctypes.c_int, [_vp, _vp]),
     "lc_float_repr_many": (ctypes.c_int64, [_vp, ctypes.c_int64, ctypes.c_int, _vp, ctypes.c_int64]),
     "lc_model_digest": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p]),
     "lc_sha256_hex": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p]),
@@ -437,6 +442,25 @@ class Context:
         with self.lock:
             _check(self.lib.lc_get_results(self.handle, _ptr(raw), _ptr(lk), _ptr(flags)))
         return raw, lk, flags
+
+    def run_pipeline_shard(self, excluded_keys, xi, epsilon, max_passes, max_subsegments, mode, shard, shards):
+        """Fused run evaluating Gauss-sum item slice `shard` of `shards`; returns
+        (n_items, device pointer of the partials) or None when the staged path must run."""
+        ex = np.ascontiguousarray(excluded_keys if excluded_keys is not None else [], dtype=np.uint64)
+        n_pairs, n_items, ptr = ctypes.c_int64(0), ctypes.c_int64(-1), _vp()
+        with self.lock:
+            rc = self.lib.lc_run_pipeline_shard(self.handle, _ptr(ex), ex.size, float(xi), float(epsilon),
+                                                int(max_passes), int(max_subsegments), int(mode), int(shard),
+                                                int(shards), ctypes.byref(n_pairs), ctypes.byref(n_items),
+                                                ctypes.byref(ptr))
+            if rc in (LC_ERR_DISCRETIZE, LC_ERR_VALIDATION):
+                raise self._disc_error()
+            _check(rc)
+        return None if n_items.value < 0 else (n_items.value, ptr.value)
+
+    def shard_reduce(self, partials_all_ptr):
+        with self.lock:
+            _check(self.lib.lc_shard_reduce(self.handle, _vp(partials_all_ptr)))
 
     def last_run_fused(self):
         """Path of the last run_pipeline: 0 staged, 1 fused, 2 fused graph replay."""

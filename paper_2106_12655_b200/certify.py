@@ -9,16 +9,18 @@ pair on the device and then replays the reference's evaluation order on
 the host, which yields the identical report because the per-pair integers
 are identical.
 
-Multi-GPU: when torch.distributed is initialized with world_size > 1, the
-Gauss-sum work items are split into contiguous per-rank ranges and the
-per-item partial sums are all-gathered (NCCL over NVLink on GPUs, gloo in
-CPU tests) before the fixed-order per-pair reduction, so raw sums are
+Multi-GPU: when torch.distributed is initialized with world_size > 1, every
+rank runs the fused single-sync pipeline with the Gauss kernel restricted to
+its contiguous slice of the work items (sized on the device), the per-item
+partial sums are all-gathered (NCCL over NVLink; gloo in CPU tests of the
+staged fallback) and every rank reduces them in fixed order, so raw sums are
 bitwise identical for any number of ranks.
 """
 
 from __future__ import annotations
 
 import json
+import os
 import time
 import warnings
 
@@ -186,8 +188,10 @@ def _dist():
         import torch.distributed as dist
     except Exception:  # pragma: no cover - torch is part of the image
         return None
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
-        return dist
+    if dist.is_available() and dist.is_initialized():
+        # LINKCERT_FORCE_SHARDED=1 exercises the sharded code path at world size 1 (tests)
+        if dist.get_world_size() > 1 or os.environ.get("LINKCERT_FORCE_SHARDED") == "1":
+            return dist
     return None
 
 
@@ -196,6 +200,45 @@ def item_range(n_items, rank, world):
     per = -(-n_items // world) if world else n_items
     b = min(n_items, rank * per)
     return b, min(n_items, b + per), per
+
+
+class _DeviceArray:
+    """Zero-copy handle on a library-owned device buffer (torch.as_tensor reads
+    __cuda_array_interface__)."""
+
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": "<f8", "data": (int(ptr), False),
+                                         "version": 3}
+
+
+_gather_out = {}
+
+
+def _fused_sharded_step(ctx, xi, excl_keys, params, mode, dist):
+    """Multi-GPU hot path: every rank runs the fused single-sync pipeline on the
+    same model with the Gauss kernel restricted to its item slice; the slices
+    are all-gathered with NCCL into one partial array, which every rank reduces
+    in fixed order (bitwise the single-GPU sums).  None: the model needs the
+    staged path."""
+    import torch
+
+    world, rank = dist.get_world_size(), dist.get_rank()
+    got = ctx.run_pipeline_shard(excl_keys, xi, params.epsilon, params.max_passes, params.max_subsegments, mode,
+                                 rank, world)
+    if got is None:
+        return None
+    n_items, ptr = got
+    dev = torch.device("cuda", ctx.device)
+    per = -(-n_items // world)
+    out = _gather_out.get((dev, per * world))
+    if out is None:
+        out = _gather_out[(dev, per * world)] = torch.empty(per * world, dtype=torch.float64, device=dev)
+    if per:
+        mine = torch.as_tensor(_DeviceArray(ptr, per * world), device=dev)[rank * per:(rank + 1) * per]
+        dist.all_gather_into_tensor(out, mine)
+        torch.cuda.synchronize(dev)
+    ctx.shard_reduce(out.data_ptr())
+    return ctx.result_views()
 
 
 def _sharded_gauss(ctx, mode, dist):
@@ -255,6 +298,18 @@ def device_step(ctx, xi, excl_keys, params, mode=None, timings=None):
             timings["discretize"] = 1e-3 * st["discretize"]
             timings["kernel"] = 1e-3 * (st["gauss"] + st["reduce"])
         return pairs, raw, lk, flags
+    if dist.get_backend() == "nccl":
+        try:
+            res = _fused_sharded_step(ctx, xi, excl_keys, params, mode, dist)
+        except _native.DiscretizeFailure as fail:
+            raise_for_failure(fail, params)
+        if res is not None:
+            if timings is not None:
+                st = ctx.stage_times()
+                timings["pls"] = timings.get("upload", 0.0) + 1e-3 * st["pls"]
+                timings["discretize"] = 1e-3 * st["discretize"]
+                timings["kernel"] = 1e-3 * st["gauss"]
+            return res
     t0 = time.perf_counter()
     ctx.potential_link_search(excl_keys)
     t1 = time.perf_counter()

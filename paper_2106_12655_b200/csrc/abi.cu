@@ -389,6 +389,42 @@ int lc_run_pipeline(lc_ctx *ctx, const uint64_t *excluded_keys, int64_t n_excl, 
     });
 }
 
+int lc_run_pipeline_shard(lc_ctx *ctx, const uint64_t *excluded_keys, int64_t n_excl, double xi, double epsilon,
+                          int max_passes, int64_t max_subsegments, int mode, int shard, int shards, int64_t *n_pairs,
+                          int64_t *n_items, double **partials_dev) {
+    *n_items = -1;
+    ctx->last_fused = 0;
+    ctx->pipe.derived_in_run = false;
+    int fr = FAST_FALLBACK;
+    const int g = guarded(ctx, [&] {
+        if (n_excl < 0 || (n_excl > 0 && !excluded_keys)) throw Error(LC_ERR_ARG, "bad excluded keys");
+        for (int64_t k = 1; k < n_excl; ++k)
+            if (excluded_keys[k] <= excluded_keys[k - 1]) throw Error(LC_ERR_ARG, "excluded keys must be sorted unique");
+        DiscParams prm;
+        prm.xi = xi;
+        prm.epsilon = epsilon;
+        prm.max_passes = max_passes;
+        prm.max_subsegments = max_subsegments;
+        fr = ctx->pipe.run_fast(excluded_keys, n_excl, prm, mode, shard, shards);
+        if (n_pairs) *n_pairs = ctx->pipe.P;
+        if (fr == FAST_OK) {
+            *n_items = ctx->pipe.n_items;
+            *partials_dev = ctx->pipe.d_partials.as<double>();
+        }
+    });
+    if (g != LC_OK) return g;
+    ctx->last_fused = fr == FAST_FALLBACK ? 0 : (ctx->pipe.last_fast_graph ? 2 : 1);
+    if (fr == FAST_INVALID) {
+        g_last_error = "discretization failed (see lc_discretize_error)";
+        return LC_ERR_VALIDATION;
+    }
+    return LC_OK;
+}
+
+int lc_shard_reduce(lc_ctx *ctx, const double *partials_all_dev) {
+    return guarded(ctx, [&] { ctx->pipe.shard_reduce(partials_all_dev); });
+}
+
 int lc_result_views(lc_ctx *ctx, void **pairs, void **raw, void **lk, void **flags, int64_t *n_pairs) {
     return guarded(ctx, [&] {
         Pipeline &p = ctx->pipe;

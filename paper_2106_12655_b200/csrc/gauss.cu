@@ -346,10 +346,19 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) gauss_items_kernel(
     const double *__restrict__ X, const double *__restrict__ Y, const double *__restrict__ Z,
     const PairGeom *__restrict__ pg, const int64_t *__restrict__ item_off, const int32_t *__restrict__ item_pair,
     int64_t P, int64_t item_begin, int64_t item_end, unsigned long long *__restrict__ counter,
-    double *__restrict__ partials, const int64_t *__restrict__ d_end) {
+    double *__restrict__ partials, const int64_t *__restrict__ d_end, int shard, int shards) {
     __shared__ double ksh[KSM ? 3 * (R + 1) * kCtaThreads : 1];
     const int lane = threadIdx.x & 31;
-    if (d_end && *d_end < item_end) item_end = *d_end;   // fused path: item count on the device
+    if (d_end) {   // fused path: item count on the device; a shard takes its contiguous slice
+        const int64_t n = *d_end;
+        if (shards > 1) {
+            const int64_t per = (n + shards - 1) / shards;
+            item_begin = (int64_t)shard * per < n ? (int64_t)shard * per : n;
+            item_end = item_begin + per < n ? item_begin + per : n;
+        } else if (n < item_end) {
+            item_end = n;
+        }
+    }
 #ifdef LC_PREFETCH_ITEM
     // the next item index is claimed while the current one is evaluated
     unsigned long long k_next = 0;
@@ -589,12 +598,12 @@ int64_t build_items(const int32_t *d_pairs, int64_t P, const int64_t *d_voff, Pa
 void launch_gauss_items(int mode, const double *X, const double *Y, const double *Z, const PairGeom *pg,
                         const int64_t *item_off, const int32_t *item_pair, int64_t P, int64_t item_begin,
                         int64_t item_end, unsigned long long *counter, double *partials, cudaStream_t s,
-                        const int64_t *d_end) {
+                        const int64_t *d_end, int shard, int shards) {
     if (item_end <= item_begin) return;
     LC_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s));
     using Kern = void (*)(const double *, const double *, const double *, const PairGeom *, const int64_t *,
                           const int32_t *, int64_t, int64_t, int64_t, unsigned long long *, double *,
-                          const int64_t *);
+                          const int64_t *, int, int);
     // default phase kernel: 3 resident CTAs/SM (168 regs); modes 3-6 are A/B variants
     // (1 CTA/SM with 232 regs; 4 CTAs; row vertices in shared memory)
     static const Kern table[] = {gauss_items_kernel<GAUSS_PHASE, 3>, gauss_items_kernel<GAUSS_ATAN, 1>,
@@ -617,7 +626,7 @@ void launch_gauss_items(int mode, const double *X, const double *Y, const double
     const int64_t blocks_needed = ceil_div(warps_needed, threads / 32);
     if (blocks > blocks_needed) blocks = blocks_needed;
     fn<<<(unsigned)blocks, threads, 0, s>>>(X, Y, Z, pg, item_off, item_pair, P, item_begin, item_end, counter,
-                                            partials, d_end);
+                                            partials, d_end, shard, shards);
     LC_CHECK_LAUNCH();
 }
 

@@ -44,9 +44,11 @@ __global__ void export_results_kernel(const int64_t *__restrict__ dP, int64_t ca
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += stride) {
         h_pairs[i] = pairs[i];
-        h_raw[i] = raw[i];
-        h_lk[i] = lk[i];
-        h_flags[i] = flags[i];
+        if (raw) {   // sharded runs export the sums after the partials exchange
+            h_raw[i] = raw[i];
+            h_lk[i] = lk[i];
+            h_flags[i] = flags[i];
+        }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         FastStatus f;
@@ -412,7 +414,9 @@ void Pipeline::download_results_pinned() {
     h_res_P = (int64_t)n;
 }
 
-int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscParams &prm, int mode) {
+int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscParams &prm, int mode, int shard,
+                       int shards) {
+    if (shards < 1 || shard < 0 || shard >= shards) throw Error(LC_ERR_ARG, "bad shard");
     if (!model_ready || L < 2 || M == 0 || prm.max_passes < 1) return FAST_FALLBACK;
     if (mode < GAUSS_PHASE || mode > 6) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
     // pair capacity: the grid PLS bound (16 per row) until a run has shown the
@@ -430,7 +434,8 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
     d_item_off.reserve(sizeof(int64_t) * (pcap + 1), s);
     d_scan.reserve(build_items_scan_bytes(pcap), s);
     d_counter.reserve(sizeof(unsigned long long), s);
-    d_partials.reserve(sizeof(double) * icap, s);
+    const int64_t part_cap = ceil_div(icap, shards) * shards;   // every shard's slice fits at shard * per
+    d_partials.reserve(sizeof(double) * part_cap, s);
     d_item_pair.reserve(sizeof(int32_t) * icap, s);
     d_raw.reserve(sizeof(double) * pcap, s);
     d_lk.reserve(sizeof(int64_t) * pcap, s);
@@ -480,14 +485,16 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
         record(EV_GAUSS0);
         launch_gauss_items(mode, dout.X.as<double>(), dout.Y.as<double>(), dout.Z.as<double>(), d_pg.as<PairGeom>(),
                            d_item_off.as<int64_t>(), d_item_pair.as<int32_t>(), pcap, 0, icap,
-                           d_counter.as<unsigned long long>(), d_partials.as<double>(), s, d_items);
+                           d_counter.as<unsigned long long>(), d_partials.as<double>(), s, d_items, shard, shards);
         record(EV_GAUSS1);
-        launch_reduce_pairs(d_partials.as<double>(), d_item_off.as<int64_t>(), pcap, d_raw.as<double>(),
-                            d_lk.as<int64_t>(), d_flags.as<uint8_t>(), s, dP);
+        if (shards == 1)
+            launch_reduce_pairs(d_partials.as<double>(), d_item_off.as<int64_t>(), pcap, d_raw.as<double>(),
+                                d_lk.as<int64_t>(), d_flags.as<uint8_t>(), s, dP);
         record(EV_END);
         LC_CUDA(cudaStreamWaitEvent(s, ev_checks, 0));
         export_results_kernel<<<148, 256, 0, s>>>(dP, pcap, d_items, dmx, ctr, dout.d_val_err, d_pairs.as<int2>(),
-                                                  d_raw.as<double>(), d_lk.as<int64_t>(), d_flags.as<uint8_t>(), st,
+                                                  shards == 1 ? d_raw.as<double>() : nullptr, d_lk.as<int64_t>(),
+                                                  d_flags.as<uint8_t>(), st,
                                                   reinterpret_cast<int2 *>(hp), reinterpret_cast<double *>(hr),
                                                   reinterpret_cast<int64_t *>(hl), reinterpret_cast<uint8_t *>(hf));
         LC_CHECK_LAUNCH();
@@ -497,8 +504,8 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
         const char *e = getenv("LINKCERT_NO_GRAPH");
         return e && e[0] == '1';
     }();
-    FastKey key{L, M, pcap, icap, n_excl, mode, model_poly ? 1 : 0, prm.epsilon * prm.xi, 2.220446049250313e-16 * prm.xi,
-                alloc_generation().load()};
+    FastKey key{L, M, pcap, icap, n_excl, mode, model_poly ? 1 : 0, shard, shards, prm.epsilon * prm.xi,
+                2.220446049250313e-16 * prm.xi, alloc_generation().load()};
     last_fast_graph = false;
     if (!no_graph && graph_exec && key == graph_key) {
         LC_CUDA(cudaGraphLaunch(graph_exec, s));
@@ -577,8 +584,17 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
     res_raw = hr;
     res_lk = hl;
     res_flags = hf;
-    h_res_P = P;
+    h_res_P = shards == 1 ? P : -1;   // sharded: lc_shard_reduce completes the results
     return FAST_OK;
+}
+
+// After a sharded fused run and the all-gather of the item partials: the
+// fixed-order per-pair reduction and the results into pinned memory.
+void Pipeline::shard_reduce(const double *partials_all) {
+    if (!polylines_ready) throw Error(LC_ERR_STATE, "no sharded run to reduce");
+    launch_reduce_pairs(partials_all, d_item_off.as<int64_t>(), P, d_raw.as<double>(), d_lk.as<int64_t>(),
+                        d_flags.as<uint8_t>(), s);
+    download_results_pinned();
 }
 
 void Pipeline::segment_pair_lambda(const double *quads, int64_t n, double *out) {

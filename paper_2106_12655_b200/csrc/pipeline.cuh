@@ -105,20 +105,24 @@ struct Pipeline {
     // the run was the reference's: FAST_OK (results in h_res), FAST_INVALID
     // (PolylineLoop ValidationError in derr), FAST_FALLBACK (the model needs
     // refinement / the sweep path / larger buffers: run the staged pipeline).
-    int run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscParams &prm, int mode);
+    // shards > 1: the Gauss kernel evaluates only item slice `shard` (of ceil(n/shards))
+    // into d_partials at absolute item ids and the sums wait for shard_reduce().
+    int run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscParams &prm, int mode, int shard = 0,
+                 int shards = 1);
+    void shard_reduce(const double *partials_all);
     int64_t items_cap = 0;
     int64_t pairs_seen = 0;   // largest pair count of a fused run (sizes the next run's capacity)
     // The fused sequence is replayed as a CUDA graph once a run with the same
     // shape (FastKey) and the same buffer generation has completed uncaptured.
     struct FastKey {
         int64_t L, M, pcap, icap, n_excl;
-        int mode, model_poly;
+        int mode, model_poly, shard, shards;
         double min_diam, poly_thr;
         unsigned long long gen;
         bool operator==(const FastKey &o) const {
             return L == o.L && M == o.M && pcap == o.pcap && icap == o.icap && n_excl == o.n_excl &&
-                   mode == o.mode && model_poly == o.model_poly && min_diam == o.min_diam &&
-                   poly_thr == o.poly_thr && gen == o.gen;
+                   mode == o.mode && model_poly == o.model_poly && shard == o.shard && shards == o.shards &&
+                   min_diam == o.min_diam && poly_thr == o.poly_thr && gen == o.gen;
         }
     };
     FastKey fast_seen{}, graph_key{};
