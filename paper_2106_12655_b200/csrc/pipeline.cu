@@ -43,14 +43,14 @@ __global__ void export_results_kernel(const int64_t *__restrict__ dP, int64_t ca
     const int64_t P = *dP < cap ? *dP : cap;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += stride) {
-        h_pairs[i] = pairs[i];
+        if (pairs) h_pairs[i] = pairs[i];
         if (raw) {   // sharded runs export the sums after the partials exchange
             h_raw[i] = raw[i];
             h_lk[i] = lk[i];
             h_flags[i] = flags[i];
         }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (st && blockIdx.x == 0 && threadIdx.x == 0) {
         FastStatus f;
         f.P = *dP;
         f.n_items = *d_items;
@@ -142,7 +142,7 @@ void Pipeline::derive() {
                      model_poly ? d_verts_in.as<double>() : nullptr, d_loff.as<int64_t>(), L, M,
                      d_seg_box.as<double>(), d_seg_loop.as<int32_t>(), d_min_diag.as<unsigned long long>(),
                      d_model_exp.as<int>(), s, d_seg_fbox.as<float>(), d_loop_keys.as<unsigned long long>(),
-                     d_loop_box.as<double>());
+                     d_loop_box.as<double>(), max_loop);
     derived = true;
     derived_in_run = true;
 }
@@ -165,8 +165,11 @@ void Pipeline::upload_model(const double *coeffs, const double *t, const int64_t
     L = nloops;
     M = L > 0 ? loff[L] : 0;
     if (L > 0 && loff[0] != 0) throw Error(LC_ERR_ARG, "loop offsets must start at 0");
-    for (int64_t l = 0; l < L; ++l)
+    max_loop = 0;
+    for (int64_t l = 0; l < L; ++l) {
         if (loff[l + 1] < loff[l]) throw Error(LC_ERR_ARG, "loop offsets must be non-decreasing");
+        if (loff[l + 1] - loff[l] > max_loop) max_loop = loff[l + 1] - loff[l];
+    }
     d_coeffs.reserve(sizeof(double) * 12 * (M > 0 ? M : 1), s);
     d_t.reserve(sizeof(double) * 2 * (M > 0 ? M : 1), s);
     d_loff.reserve(sizeof(int64_t) * (L + 1), s);
@@ -188,8 +191,11 @@ void Pipeline::upload_model_polylines(const double *verts, const int64_t *loff, 
     L = nloops;
     M = L > 0 ? loff[L] : 0;
     if (L > 0 && loff[0] != 0) throw Error(LC_ERR_ARG, "loop offsets must start at 0");
-    for (int64_t l = 0; l < L; ++l)
+    max_loop = 0;
+    for (int64_t l = 0; l < L; ++l) {
         if (loff[l + 1] - loff[l] < 1) throw Error(LC_ERR_ARG, "every loop needs at least one vertex");
+        if (loff[l + 1] - loff[l] > max_loop) max_loop = loff[l + 1] - loff[l];
+    }
     d_loff.reserve(sizeof(int64_t) * (L + 1), s);
     d_verts_in.reserve(sizeof(double) * 3 * (M > 0 ? M : 1), s);
     if (M > 0) LC_CUDA(cudaMemcpyAsync(d_verts_in.ptr, verts, sizeof(double) * 3 * M, cudaMemcpyHostToDevice, s));
@@ -476,6 +482,11 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
         LC_CUDA(cudaStreamWaitEvent(side[1], ev_pairs, 0));
         launch_discretize_checks(in, dP, prm, disc_sc, dout, side[1], ev_chords, &ctr);
         record(EV_DISC, side[1]);
+        // the pair list is final: copy it out while the sums run
+        export_results_kernel<<<148, 256, 0, side[1]>>>(dP, pcap, nullptr, nullptr, nullptr, nullptr, d_pairs.as<int2>(),
+                                                        nullptr, nullptr, nullptr, nullptr,
+                                                        reinterpret_cast<int2 *>(hp), nullptr, nullptr, nullptr);
+        LC_CHECK_LAUNCH();
         LC_CUDA(cudaEventRecord(ev_checks, side[1]));
         LC_CUDA(cudaStreamWaitEvent(s, ev_chords, 0));   // items read the closed offsets, the sum the chords
         build_items(d_pairs.as<int32_t>(), pcap, dout.voff.as<int64_t>(), d_pg.as<PairGeom>(),
@@ -492,7 +503,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
                                 d_lk.as<int64_t>(), d_flags.as<uint8_t>(), s, dP);
         record(EV_END);
         LC_CUDA(cudaStreamWaitEvent(s, ev_checks, 0));
-        export_results_kernel<<<148, 256, 0, s>>>(dP, pcap, d_items, dmx, ctr, dout.d_val_err, d_pairs.as<int2>(),
+        export_results_kernel<<<148, 256, 0, s>>>(dP, pcap, d_items, dmx, ctr, dout.d_val_err, nullptr,
                                                   shards == 1 ? d_raw.as<double>() : nullptr, d_lk.as<int64_t>(),
                                                   d_flags.as<uint8_t>(), st,
                                                   reinterpret_cast<int2 *>(hp), reinterpret_cast<double *>(hr),

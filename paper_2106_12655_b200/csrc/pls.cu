@@ -148,6 +148,74 @@ __global__ void seg_boxes_kernel(const double *__restrict__ coeffs, const double
     }
 }
 
+// The same outputs for models whose loops are all short (<= kLoopWarpMax
+// segments, e.g. chainmail rings): warp per loop, lanes over its segments —
+// no loop lookup, plain warp reductions, direct stores of the loop box and
+// minimum diagonal (no keys, no atomics but the exponent).
+constexpr int64_t kLoopWarpMax = 1024;
+template <bool POLY>
+__global__ void seg_boxes_loop_kernel(const double *__restrict__ coeffs, const double *__restrict__ t,
+                                      const double *__restrict__ verts, const int64_t *__restrict__ loff, int64_t L,
+                                      int64_t M, double *__restrict__ box, float *__restrict__ fbox,
+                                      int32_t *__restrict__ seg_loop, unsigned long long *__restrict__ loop_min_diag2,
+                                      double *__restrict__ lbox, int *__restrict__ max_exp) {
+    const int lane = threadIdx.x & 31;
+    const int64_t l = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (l >= L) return;   // the whole warp
+    const int64_t b = loff[l], e = loff[l + 1];
+    double v[6] = {CUDART_INF, CUDART_INF, CUDART_INF, -CUDART_INF, -CUDART_INF, -CUDART_INF};
+    unsigned long long dg = ~0ULL;
+    int ex = 0;
+    for (int64_t m = b + lane; m < e; m += 32) {
+        double bl[3], bh[3];
+        if (POLY) {   // see seg_boxes_kernel: the box of a from_polyline segment
+            const int64_t nx = m + 1 < e ? m + 1 : b;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                const double a0 = verts[3 * m + d], a1 = verts[3 * nx + d] - a0;
+                const double v0 = eval_axis(a0, a1, 0.0, 0.0, 0.0), v1 = eval_axis(a0, a1, 0.0, 0.0, 1.0);
+                bl[d] = np_min(v0, v1);
+                bh[d] = np_max(v0, v1);
+            }
+        } else {
+            tight_box(coeffs + 12 * m, t[2 * m], t[2 * m + 1], bl, bh);
+        }
+        seg_loop[m] = (int32_t)l;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            box[d * M + m] = bl[d];
+            box[(3 + d) * M + m] = bh[d];
+            if (fbox) {
+                fbox[d * M + m] = __double2float_rd(bl[d]);
+                fbox[(3 + d) * M + m] = __double2float_ru(bh[d]);
+            }
+            ex = max(ex, max(exp_field(bl[d]), exp_field(bh[d])));
+            v[d] = np_min(v[d], bl[d]);
+            v[3 + d] = np_max(v[3 + d], bh[d]);
+        }
+        const double dx = __dsub_rn(bh[0], bl[0]), dy = __dsub_rn(bh[1], bl[1]), dz = __dsub_rn(bh[2], bl[2]);
+        const unsigned long long q = (unsigned long long)__double_as_longlong(
+            __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+        dg = q < dg ? q : dg;
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            v[d] = np_min(v[d], __shfl_xor_sync(0xffffffffu, v[d], off));
+            v[3 + d] = np_max(v[3 + d], __shfl_xor_sync(0xffffffffu, v[3 + d], off));
+        }
+    }
+    dg = group_min_u64(0xffffffffu, dg);
+    ex = __reduce_max_sync(0xffffffffu, ex);
+    if (lane == 0) {
+#pragma unroll
+        for (int d = 0; d < 6; ++d) lbox[d * L + l] = v[d];
+        if (loop_min_diag2) loop_min_diag2[l] = dg;
+        if (max_exp && ex > 0) atomicMax(max_exp, ex);
+    }
+}
+
 // Loop AABBs from the ordered keys (empty loop: [+inf, -inf], like the
 // reduction identity of loop_boxes_kernel).
 __global__ void loop_keys_decode_kernel(const unsigned long long *__restrict__ keys, int64_t L,
@@ -346,7 +414,8 @@ __global__ void grid_query_warp_kernel(const double *__restrict__ lbox, int64_t 
                                        const int64_t *__restrict__ cell_off, const int32_t *__restrict__ cell_loops,
                                        const double *__restrict__ cbox, const uint64_t *__restrict__ excl,
                                        int64_t n_excl, int *__restrict__ row_count, int32_t *__restrict__ slots,
-                                       const int64_t *__restrict__ offs, uint64_t *__restrict__ keys) {
+                                       const int64_t *__restrict__ offs, uint64_t *__restrict__ keys,
+                                       int64_t *__restrict__ counts64, int *__restrict__ overflow) {
     const int lane = threadIdx.x & 31;
     const int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     if (a >= L) return;
@@ -418,7 +487,12 @@ __global__ void grid_query_warp_kernel(const double *__restrict__ lbox, int64_t 
         n += __popc(bal);
     }
     }
-    if (SLOTS && lane == 0) row_count[a] = n;
+    if (SLOTS && lane == 0) {
+        row_count[a] = n;
+        counts64[a] = n;                      // scanned into the pair offsets
+        if (a == L - 1) counts64[L] = 0;
+        if (n > kRowSlots) atomicMax(overflow, n);   // rare: the two-pass variant takes over
+    }
 }
 
 // Ordered-integer images of doubles (monotone): min/max through integer atomics.
@@ -430,8 +504,29 @@ __device__ __forceinline__ double ord_val(unsigned long long k) {
     return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffULL) : ~k));
 }
 
+// Stage 2 (one thread): origin, cell size >= max extent, dims with product <= max_cells.
+__device__ void grid_finalize(const unsigned long long *acc, int64_t max_cells, GridParams *__restrict__ gp) {
+    double span[3], c = ord_val(acc[6]);
+    for (int d = 0; d < 3; ++d) {
+        gp->o[d] = ord_val(acc[d]);
+        span[d] = ord_val(acc[3 + d]) - gp->o[d];
+    }
+    const double smax = fmax(span[0], fmax(span[1], span[2]));
+    if (!(c > 0.0)) c = smax > 0.0 ? smax * 1e-6 : 1.0;
+    for (;;) {
+        double prod = 1.0;
+        for (int d = 0; d < 3; ++d) prod *= floor(span[d] / c) + 1.0;
+        if (prod <= (double)max_cells) break;
+        c *= 1.25;
+    }
+    gp->c = c;
+    for (int d = 0; d < 3; ++d) gp->dims[d] = (int)(floor(span[d] / c) + 1.0);
+}
+
 // Stage 1 (many blocks): acc[0..2] = min lo, acc[3..5] = max hi, acc[6] = max extent (ordered keys).
-__global__ void grid_reduce_kernel(const double *__restrict__ lbox, int64_t L, unsigned long long *__restrict__ acc) {
+// The last block to finish also derives the grid parameters (no second launch).
+__global__ void grid_reduce_kernel(const double *__restrict__ lbox, int64_t L, unsigned long long *__restrict__ acc,
+                                   unsigned *__restrict__ done, int64_t max_cells, GridParams *__restrict__ gp) {
     double v[7] = {CUDART_INF, CUDART_INF, CUDART_INF, -CUDART_INF, -CUDART_INF, -CUDART_INF, 0.0};
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < L; l += (int64_t)gridDim.x * blockDim.x) {
 #pragma unroll
@@ -458,27 +553,20 @@ __global__ void grid_reduce_kernel(const double *__restrict__ lbox, int64_t L, u
         }
         atomicMax(acc + 6, ord_key(v[6]));
     }
+    __threadfence();
+    __syncthreads();
+    __shared__ bool last;
+    if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        unsigned long long a[7];
+        for (int k = 0; k < 7; ++k) a[k] = atomicAdd(acc + k, 0ULL);   // L2-coherent reads
+        grid_finalize(a, max_cells, gp);
+        *done = 0;   // ready for the next run
+    }
 }
 
-// Stage 2 (one thread): origin, cell size >= max extent, dims with product <= max_cells.
-__global__ void grid_finalize_kernel(const unsigned long long *__restrict__ acc, int64_t max_cells,
-                                     GridParams *__restrict__ gp) {
-    double span[3], c = ord_val(acc[6]);
-    for (int d = 0; d < 3; ++d) {
-        gp->o[d] = ord_val(acc[d]);
-        span[d] = ord_val(acc[3 + d]) - gp->o[d];
-    }
-    const double smax = fmax(span[0], fmax(span[1], span[2]));
-    if (!(c > 0.0)) c = smax > 0.0 ? smax * 1e-6 : 1.0;
-    for (;;) {
-        double prod = 1.0;
-        for (int d = 0; d < 3; ++d) prod *= floor(span[d] / c) + 1.0;
-        if (prod <= (double)max_cells) break;
-        c *= 1.25;
-    }
-    gp->c = c;
-    for (int d = 0; d < 3; ++d) gp->dims[d] = (int)(floor(span[d] / c) + 1.0);
-}
 
 // Row i's slots sorted by j -> pairs[off[i] ...] (insertion sort, <= kRowSlots).
 __global__ void slots_compact_kernel(const int *__restrict__ row_count, const int64_t *__restrict__ off, int64_t L,
@@ -507,16 +595,6 @@ __global__ void slots_compact_kernel(const int *__restrict__ row_count, const in
         }
 }
 
-__global__ void row_counts_i64_kernel(const int *__restrict__ row_count, int64_t L, int64_t *__restrict__ out,
-                                      int *__restrict__ max_count) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < L) {
-        out[i] = row_count[i];
-        atomicMax(max_count, row_count[i]);
-    } else if (i == L) {
-        out[L] = 0;
-    }
-}
 __global__ void unpack_pairs_kernel(const uint64_t *__restrict__ keys, int64_t P, int32_t *__restrict__ pairs) {
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p >= P) return;
@@ -529,7 +607,20 @@ __global__ void unpack_pairs_kernel(const uint64_t *__restrict__ keys, int64_t P
 
 void launch_seg_boxes(const double *coeffs, const double *t, const double *verts, const int64_t *loff, int64_t L,
                       int64_t M, double *seg_box, int32_t *seg_loop, unsigned long long *loop_min_diag2, int *max_exp,
-                      cudaStream_t s, float *seg_fbox, unsigned long long *loop_keys, double *loop_box) {
+                      cudaStream_t s, float *seg_fbox, unsigned long long *loop_keys, double *loop_box,
+                      int64_t max_loop_segments) {
+    if (loop_box && L > 0 && max_loop_segments >= 0 && max_loop_segments <= kLoopWarpMax) {
+        if (max_exp) LC_CUDA(cudaMemsetAsync(max_exp, 0, sizeof(int), s));
+        const unsigned blocks = (unsigned)ceil_div(L * 32, 128);
+        if (verts)
+            seg_boxes_loop_kernel<true><<<blocks, 128, 0, s>>>(nullptr, nullptr, verts, loff, L, M, seg_box, seg_fbox,
+                                                               seg_loop, loop_min_diag2, loop_box, max_exp);
+        else
+            seg_boxes_loop_kernel<false><<<blocks, 128, 0, s>>>(coeffs, t, nullptr, loff, L, M, seg_box, seg_fbox,
+                                                                seg_loop, loop_min_diag2, loop_box, max_exp);
+        LC_CHECK_LAUNCH();
+        return;
+    }
     if (loop_min_diag2)
         LC_CUDA(cudaMemsetAsync(loop_min_diag2, 0xff, sizeof(unsigned long long) * (L > 0 ? L : 1), s));
     if (max_exp) LC_CUDA(cudaMemsetAsync(max_exp, 0, sizeof(int), s));
@@ -576,10 +667,9 @@ static void grid_prefix(const double *loop_box, int64_t L, int64_t n_excl, PlsSc
     sc.counts.reserve(sizeof(int64_t) * (L + 8 > 8 ? L + 8 : 8), s);
     unsigned long long *acc = (unsigned long long *)sc.counts.ptr;   // 7 ordered keys, reused below
     LC_CUDA(cudaMemsetAsync(acc, 0xff, 3 * sizeof(unsigned long long), s));
-    LC_CUDA(cudaMemsetAsync(acc + 3, 0, 4 * sizeof(unsigned long long), s));
-    grid_reduce_kernel<<<(unsigned)(ceil_div(L, 256) < 148 ? ceil_div(L, 256) : 148), 256, 0, s>>>(loop_box, L, acc);
-    LC_CHECK_LAUNCH();
-    grid_finalize_kernel<<<1, 1, 0, s>>>(acc, max_cells, gp);
+    LC_CUDA(cudaMemsetAsync(acc + 3, 0, 5 * sizeof(unsigned long long), s));   // + the block counter
+    grid_reduce_kernel<<<(unsigned)(ceil_div(L, 256) < 148 ? ceil_div(L, 256) : 148), 256, 0, s>>>(
+        loop_box, L, acc, reinterpret_cast<unsigned *>(acc + 7), max_cells, gp);
     LC_CHECK_LAUNCH();
     LC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (max_cells + 1), s));
     const unsigned gl = (unsigned)ceil_div(L, 256);
@@ -598,10 +688,8 @@ static void grid_prefix(const double *loop_box, int64_t L, int64_t n_excl, PlsSc
     LC_CUDA(cudaMemsetAsync(max_count, 0, sizeof(int), s));
     grid_query_warp_kernel<true><<<(unsigned)ceil_div(L * 32, 256), 256, 0, s>>>(loop_box, L, gp, coff, sc.perm.as<int32_t>(),
                                                sc.sbox.as<double>(), sc.excl.as<uint64_t>(), n_excl, row_count,
-                                               sc.pair_keys.as<int32_t>(), nullptr, nullptr);
-    LC_CHECK_LAUNCH();
-    row_counts_i64_kernel<<<(unsigned)ceil_div(L + 1, 256), 256, 0, s>>>(row_count, L, sc.counts.as<int64_t>(),
-                                                                           max_count);
+                                               sc.pair_keys.as<int32_t>(), nullptr, nullptr,
+                                               sc.counts.as<int64_t>(), max_count);
     LC_CHECK_LAUNCH();
     b = sc.cub_tmp.bytes;
     LC_CUB(cub::DeviceScan::ExclusiveSum(sc.cub_tmp.ptr, b, sc.counts.as<int64_t>(), sc.offs.as<int64_t>(),
@@ -638,7 +726,8 @@ int64_t run_pls(const double *loop_box, int64_t L, const uint64_t *h_excl, int64
         sc.pair_keys_sorted.reserve(sizeof(uint64_t) * P, s);
         grid_query_warp_kernel<false><<<(unsigned)ceil_div(L * 32, 256), 256, 0, s>>>(loop_box, L, gp, coff, sc.perm.as<int32_t>(),
                                                     sc.sbox.as<double>(), sc.excl.as<uint64_t>(), n_excl, nullptr, nullptr,
-                                                    sc.offs.as<int64_t>(), sc.pair_keys.as<uint64_t>());
+                                                    sc.offs.as<int64_t>(), sc.pair_keys.as<uint64_t>(), nullptr,
+                                                    nullptr);
         LC_CHECK_LAUNCH();
         size_t b3 = 0;
         cub::DeviceRadixSort::SortKeys(nullptr, b3, (uint64_t *)nullptr, (uint64_t *)nullptr, (int)P);

@@ -17,10 +17,12 @@ namespace lc {
 // loop_box: the loop AABBs (pls.py:48-56) reduced in the same pass.
 // verts != nullptr: closed polylines given by their vertices (M,3) instead of
 // coeffs/t (the from_polyline arrays are formed in registers).
+// max_loop_segments (host-known, >= 0) <= 1024 with loop_box: warp-per-loop
+// variant (no loop lookup, no keys); otherwise thread per segment + keys.
 void launch_seg_boxes(const double *coeffs, const double *t, const double *verts, const int64_t *loff, int64_t L,
                       int64_t M, double *seg_box, int32_t *seg_loop, unsigned long long *loop_min_diag2, int *max_exp,
                       cudaStream_t s, float *seg_fbox = nullptr, unsigned long long *loop_keys = nullptr,
-                      double *loop_box = nullptr);
+                      double *loop_box = nullptr, int64_t max_loop_segments = -1);
 
 
 struct PlsScratch {

@@ -2,7 +2,7 @@
 
 usage: python tools/step_table.py launches.csv [first_kernel_regex]
 The step is taken as the kernels from the last occurrence of the first-kernel
-pattern (default: seg_boxes) through the following export/reduce kernel.
+pattern (default: seg_boxes) to the end of the list.
 """
 import collections
 import csv
@@ -22,13 +22,8 @@ for r in rows:
         name = re.sub(r"\(.*", "", d["Kernel Name"])[:80]
         recs.append((name, float(d["Metric Value"].replace(",", "")) / 1000.0))
 starts = [i for i, (k, _) in enumerate(recs) if first.search(k)]
-start = starts[-1]
-end = len(recs)
-for i in range(start, len(recs)):
-    if "export_results" in recs[i][0] or (i > start and first.search(recs[i][0])):
-        end = i + 1 if "export_results" in recs[i][0] else i
-        break
-step = recs[start:end]
+start = starts[-1]            # the last step in the list runs to its end
+step = recs[start:]
 tot = sum(v for _, v in step)
 agg = collections.OrderedDict()
 for k, v in step:
