@@ -203,6 +203,40 @@ __device__ __forceinline__ void col_step(const Col &A, Col &B, double lx, double
 #pragma unroll
     for (int m = 0; m <= R; ++m) h[m] = fma(A.z[m], B.z[m], fma(A.y[m], B.y[m], A.x[m] * B.x[m]));
     double wx[R], wy[R];
+#if !defined(LC_UNSTAGED_PAIRS)
+    if (FAST) {   // the R pair terms stage by stage: independent chains side by side (+2% over pair_w order)
+        double ca[R], p[R], t1[R], d1[R], d2[R];
+#pragma unroll
+        for (int m = 0; m < R; ++m)
+            ca[m] = fma(B.z[m + 1], A.z[m], fma(B.y[m + 1], A.y[m], B.x[m + 1] * A.x[m]));
+#pragma unroll
+        for (int m = 0; m < R; ++m) {
+            const double ax = A.x[m], ay = A.y[m], az = A.z[m];
+            const double bx = A.x[m + 1], by = A.y[m + 1], bz = A.z[m + 1];
+            const double cx = B.x[m + 1], cy = B.y[m + 1], cz = B.z[m + 1];
+            p[m] = fma(az, fma(bx, cy, -by * cx), fma(ay, fma(bz, cx, -bx * cz), ax * fma(by, cz, -bz * cy)));
+        }
+#pragma unroll
+        for (int m = 0; m < R; ++m) t1[m] = fma(A.n[m], B.n[m + 1], ca[m]);
+#pragma unroll
+        for (int m = 0; m < R; ++m) {
+            d1[m] = fma(A.n[m + 1], t1[m], fma(B.n[m + 1], A.v[m], A.n[m] * h[m + 1]));
+            d2[m] = fma(B.n[m], t1[m], fma(B.n[m + 1], h[m], A.n[m] * B.v[m]));
+        }
+#pragma unroll
+        for (int m = 0; m < R; ++m) {
+            wx[m] = fma(d1[m], d2[m], -p[m] * p[m]);
+            wy[m] = p[m] * (d1[m] + d2[m]);
+            int t = sbit(wy[m]) - sbit(p[m]);
+            if (!FULL && !rv[m]) {
+                wx[m] = 1.0;
+                wy[m] = 0.0;
+                t = 0;
+            }
+            acc.turns += t;
+        }
+    } else
+#endif
 #pragma unroll
     for (int m = 0; m < R; ++m) {
         int t = 0, hv = 0;
@@ -609,7 +643,7 @@ void launch_gauss_items(int mode, const double *X, const double *Y, const double
     static const Kern table[] = {gauss_items_kernel<GAUSS_PHASE, 3>, gauss_items_kernel<GAUSS_ATAN, 1>,
                                  gauss_items_kernel<GAUSS_REF, 1>, gauss_items_kernel<GAUSS_PHASE, 1>,
                                  gauss_items_kernel<GAUSS_PHASE, 4>, gauss_items_kernel<GAUSS_PHASE, 4, true>,
-                                 gauss_items_kernel<GAUSS_PHASE, 3, true>};
+                                 gauss_items_kernel<GAUSS_PHASE, 3, true>, gauss_items_kernel<GAUSS_PHASE, 2>};
     if (mode < 0 || mode >= (int)(sizeof table / sizeof table[0])) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
     const Kern fn = table[mode];
     constexpr int kModes = (int)(sizeof table / sizeof table[0]);

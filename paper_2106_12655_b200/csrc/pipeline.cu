@@ -378,7 +378,7 @@ void Pipeline::finish_items() {
 
 void Pipeline::run_gauss(int mode, int64_t item_begin, int64_t item_end, double *partials_ext,
                          cudaEvent_t ev0, cudaEvent_t ev1) {
-    if (mode < GAUSS_PHASE || mode > 6) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
+    if (mode < GAUSS_PHASE || mode > 7) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
     double *out = partials_ext ? partials_ext : d_partials.as<double>();
     LC_CUDA(cudaEventRecord(ev0 ? ev0 : ev[EV_GAUSS0], s));
     launch_gauss_items(mode, gX, gY, gZ, d_pg.as<PairGeom>(), d_item_off.as<int64_t>(), d_item_pair.as<int32_t>(), P,
@@ -424,7 +424,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
                        int shards) {
     if (shards < 1 || shard < 0 || shard >= shards) throw Error(LC_ERR_ARG, "bad shard");
     if (!model_ready || L < 2 || M == 0 || prm.max_passes < 1) return FAST_FALLBACK;
-    if (mode < GAUSS_PHASE || mode > 6) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
+    if (mode < GAUSS_PHASE || mode > 7) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
     // pair capacity: the grid PLS bound (16 per row) until a run has shown the
     // model's pair count; then that plus headroom (smaller grids and scans)
     int64_t pcap = (int64_t)kRowSlots * L;
