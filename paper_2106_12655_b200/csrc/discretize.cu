@@ -114,7 +114,10 @@ __global__ void pre_pairs_kernel(const int32_t *__restrict__ pairs, int64_t P, c
         }
     }
     axis[p] = (int8_t)a;
-    if (!brute_pair(loff[i + 1] - loff[i], loff[j + 1] - loff[j])) atomicAdd(&ctr->n_large, 1);
+    if (!brute_pair(loff[i + 1] - loff[i], loff[j + 1] - loff[j])) {
+        atomicAdd(&ctr->n_large, 1);
+        ctr->abort = 1;
+    }
 }
 
 __global__ void pre_loops_kernel(const unsigned long long *__restrict__ min_diag, const uint8_t *__restrict__ paired,
@@ -122,7 +125,10 @@ __global__ void pre_loops_kernel(const unsigned long long *__restrict__ min_diag
     const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (l >= L) return;
     // min over segments of sqrt(squared diagonal) == sqrt(min squared diagonal)
-    if (__dsqrt_rn(__longlong_as_double((long long)min_diag[l])) < min_diam) atomicMin(&ctr->zero_loop, (int)l);
+    if (__dsqrt_rn(__longlong_as_double((long long)min_diag[l])) < min_diam) {
+        atomicMin(&ctr->zero_loop, (int)l);
+        ctr->abort = 1;
+    }
     if (!paired[l]) atomicAdd(&ctr->n_unpaired, 1);
 }
 
@@ -238,7 +244,7 @@ constexpr int kAnyCap = 64;   // staged survivors per side; beyond that the test
 __global__ void __launch_bounds__(32 * kAnyWarps) brute_any_kernel(
     const double *__restrict__ box, const float *__restrict__ fbox, int64_t M, const int64_t *__restrict__ loff,
     const double *__restrict__ lbox, int64_t L, const int32_t *__restrict__ pairs, int64_t P,
-    const int64_t *__restrict__ dP, unsigned long long *__restrict__ marked) {
+    const int64_t *__restrict__ dP, unsigned long long *__restrict__ marked, int *__restrict__ abort) {
     __shared__ int32_t sidx[kAnyWarps][2][kAnyCap];
     __shared__ float sbox[kAnyWarps][2][6][kAnyCap];
     if (dP && *dP < P) P = *dP;
@@ -347,7 +353,10 @@ __global__ void __launch_bounds__(32 * kAnyWarps) brute_any_kernel(
             }
             if (box_overlap(box, M, et, lo, hi)) ++hits;
         }
-        if (hits) atomicAdd(marked, (unsigned long long)hits);
+        if (hits) {
+            atomicAdd(marked, (unsigned long long)hits);
+            if (abort) *abort = 1;
+        }
         __syncwarp();
     }
 }
@@ -1267,8 +1276,6 @@ void launch_discretize_checks(const DiscInput &in, const int64_t *d_P, const Dis
     const double min_diam = prm.epsilon * prm.xi;
     PreCounters *ctr = sc.prectr.as<PreCounters>();
     LC_CUDA(cudaMemsetAsync(sc.paired.ptr, 0, L > 0 ? L : 1, s));
-    fast_init_kernel<<<1, 1, 0, s>>>(ctr, sc.val_err2.as<int>());
-    LC_CHECK_LAUNCH();
     if (Pcap > 0) {
         pre_pairs_kernel<<<grid_for(Pcap), 256, 0, s>>>(in.pairs, Pcap, d_P, in.loff, in.loop_box, L,
                                                         sc.paired.as<uint8_t>(), sc.pair_axis.as<int8_t>(), ctr);
@@ -1282,7 +1289,7 @@ void launch_discretize_checks(const DiscInput &in, const int64_t *d_P, const Dis
         const int64_t blocks = ceil_div(Pcap, kAnyWarps) < 148 * 8 ? ceil_div(Pcap, kAnyWarps) : 148 * 8;
         brute_any_kernel<<<(unsigned)blocks, 32 * kAnyWarps, 0, s>>>(in.seg_box, in.seg_fbox, M, in.loff,
                                                                      in.loop_box, L, in.pairs, Pcap, d_P,
-                                                                     &ctr->marked);
+                                                                     &ctr->marked, &ctr->abort);
         LC_CHECK_LAUNCH();
     }
     if (chords_done) LC_CUDA(cudaStreamWaitEvent(s, chords_done, 0));   // validation reads the chord flags
@@ -1296,9 +1303,15 @@ void launch_discretize_checks(const DiscInput &in, const int64_t *d_P, const Dis
     *d_ctr = ctr;
 }
 
+void launch_discretize_init(DiscScratch &sc, cudaStream_t s) {
+    fast_init_kernel<<<1, 1, 0, s>>>(sc.prectr.as<PreCounters>(), sc.val_err2.as<int>());
+    LC_CHECK_LAUNCH();
+}
+
 void launch_discretize_fast(const DiscInput &in, const int64_t *d_P, const DiscParams &prm, DiscScratch &sc,
                             DiscOutput &out, cudaStream_t s, const PreCounters **d_ctr) {
     reserve_discretize_fast(in, sc, out, s);
+    launch_discretize_init(sc, s);
     launch_discretize_chords(in, prm, sc, out, s);
     launch_discretize_checks(in, d_P, prm, sc, out, s, nullptr, d_ctr);
 }

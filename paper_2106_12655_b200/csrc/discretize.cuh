@@ -28,7 +28,7 @@ struct PreCounters {
     int zero_loop;     // first loop with a zero-length segment box (INT_MAX: none)
     int n_unpaired;
     int n_large;       // pairs handled by the sweep path
-    int pad;
+    int abort;         // fused path: set with any of the above / a pass-1 hit (the Gauss sum stops early)
     unsigned long long marked;
     int err_loop;
     int pad2;
@@ -109,6 +109,9 @@ void launch_discretize_chords(const DiscInput &in, const DiscParams &prm, DiscSc
                               cudaStream_t s);
 void launch_discretize_checks(const DiscInput &in, const int64_t *d_P, const DiscParams &prm, DiscScratch &sc,
                               DiscOutput &out, cudaStream_t s, cudaEvent_t chords_done, const PreCounters **d_ctr);
+// Resets the counters (incl. the abort flag the Gauss kernel polls) — on the
+// stream every branch forks from, before the fork.
+void launch_discretize_init(DiscScratch &sc, cudaStream_t s);
 
 // Unscaled AoS (V, 3) vertices (no closing vertices) from a DiscOutput.
 void unpack_polylines(const DiscOutput &out, int64_t L, const int *max_exp, double *aos, cudaStream_t s);

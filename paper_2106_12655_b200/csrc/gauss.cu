@@ -380,7 +380,8 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) gauss_items_kernel(
     const double *__restrict__ X, const double *__restrict__ Y, const double *__restrict__ Z,
     const PairGeom *__restrict__ pg, const int64_t *__restrict__ item_off, const int32_t *__restrict__ item_pair,
     int64_t P, int64_t item_begin, int64_t item_end, unsigned long long *__restrict__ counter,
-    double *__restrict__ partials, const int64_t *__restrict__ d_end, int shard, int shards) {
+    double *__restrict__ partials, const int64_t *__restrict__ d_end, int shard, int shards,
+    const int *__restrict__ abort) {
     __shared__ double ksh[KSM ? 3 * (R + 1) * kCtaThreads : 1];
     const int lane = threadIdx.x & 31;
     if (d_end) {   // fused path: item count on the device; a shard takes its contiguous slice
@@ -409,6 +410,13 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) gauss_items_kernel(
 #endif
         const int64_t it = item_begin + (int64_t)k;
         if (it >= item_end) break;
+        // fused path: the concurrent pass-1 checks found the run unusable (staged rerun
+        // follows); lane 0 reads the flag so the whole warp leaves together
+        if (abort) {
+            int ab = 0;
+            if (lane == 0) ab = *(volatile const int *)abort;
+            if (__shfl_sync(0xffffffffu, ab, 0)) break;
+        }
         const int64_t p = item_pair ? (int64_t)__ldg(item_pair + it) : find_pair(item_off, P, it);
         const PairGeom g = pg[p];
         const int64_t local = it - __ldg(item_off + p);
@@ -632,12 +640,12 @@ int64_t build_items(const int32_t *d_pairs, int64_t P, const int64_t *d_voff, Pa
 void launch_gauss_items(int mode, const double *X, const double *Y, const double *Z, const PairGeom *pg,
                         const int64_t *item_off, const int32_t *item_pair, int64_t P, int64_t item_begin,
                         int64_t item_end, unsigned long long *counter, double *partials, cudaStream_t s,
-                        const int64_t *d_end, int shard, int shards) {
+                        const int64_t *d_end, int shard, int shards, const int *abort) {
     if (item_end <= item_begin) return;
     LC_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s));
     using Kern = void (*)(const double *, const double *, const double *, const PairGeom *, const int64_t *,
                           const int32_t *, int64_t, int64_t, int64_t, unsigned long long *, double *,
-                          const int64_t *, int, int);
+                          const int64_t *, int, int, const int *);
     // default phase kernel: 3 resident CTAs/SM (168 regs); modes 3-6 are A/B variants
     // (1 CTA/SM with 232 regs; 4 CTAs; row vertices in shared memory)
     static const Kern table[] = {gauss_items_kernel<GAUSS_PHASE, 3>, gauss_items_kernel<GAUSS_ATAN, 1>,
@@ -660,7 +668,7 @@ void launch_gauss_items(int mode, const double *X, const double *Y, const double
     const int64_t blocks_needed = ceil_div(warps_needed, threads / 32);
     if (blocks > blocks_needed) blocks = blocks_needed;
     fn<<<(unsigned)blocks, threads, 0, s>>>(X, Y, Z, pg, item_off, item_pair, P, item_begin, item_end, counter,
-                                            partials, d_end, shard, shards);
+                                            partials, d_end, shard, shards, abort);
     LC_CHECK_LAUNCH();
 }
 

@@ -46,11 +46,12 @@ size_t build_items_scan_bytes(int64_t P);
 // Evaluates items [item_begin, item_end) into partials[item] (absolute index).
 // d_end (fused path): the item count n on the device bounds the range; with
 // shards > 1 the kernel takes slice `shard` of ceil(n / shards) items instead.
+// abort (fused path): polled per item; nonzero stops the sum (the run is redone).
 void launch_gauss_items(int mode, const double *X, const double *Y, const double *Z,
                         const PairGeom *pg, const int64_t *item_off, const int32_t *item_pair, int64_t P,
                         int64_t item_begin, int64_t item_end, unsigned long long *counter,
                         double *partials, cudaStream_t s, const int64_t *d_end = nullptr, int shard = 0,
-                        int shards = 1);
+                        int shards = 1, const int *abort = nullptr);
 
 // item_pair[it] = pair of work item `it` (replaces a per-item binary search).
 void launch_item_pairs(const int64_t *item_off, int64_t P, int64_t n_items, int32_t *item_pair, cudaStream_t s);

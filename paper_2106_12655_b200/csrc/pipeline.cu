@@ -423,7 +423,9 @@ void Pipeline::download_results_pinned() {
 int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscParams &prm, int mode, int shard,
                        int shards) {
     if (shards < 1 || shard < 0 || shard >= shards) throw Error(LC_ERR_ARG, "bad shard");
-    if (!model_ready || L < 2 || M == 0 || prm.max_passes < 1) return FAST_FALLBACK;
+    // loops longer than the brute-force side limit make every pair they are in a
+    // large (sweep) pair: the staged path handles those models directly
+    if (!model_ready || L < 2 || M == 0 || prm.max_passes < 1 || max_loop > 256) return FAST_FALLBACK;
     if (mode < GAUSS_PHASE || mode > 7) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
     // pair capacity: the grid PLS bound (16 per row) until a run has shown the
     // model's pair count; then that plus headroom (smaller grids and scans)
@@ -464,6 +466,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
         in.verts = model_poly ? d_verts_in.as<double>() : nullptr;
         in.seg_fbox = d_seg_fbox.as<float>();
         reserve_discretize_fast(in, disc_sc, dout, s);
+        launch_discretize_init(disc_sc, s);   // counters + abort flag, before any branch reads them
         // branch 1: the chords need only the model — they run beside the PLS
         LC_CUDA(cudaEventRecord(ev_fork, s));
         LC_CUDA(cudaStreamWaitEvent(side[0], ev_fork, 0));
@@ -496,7 +499,8 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
         record(EV_GAUSS0);
         launch_gauss_items(mode, dout.X.as<double>(), dout.Y.as<double>(), dout.Z.as<double>(), d_pg.as<PairGeom>(),
                            d_item_off.as<int64_t>(), d_item_pair.as<int32_t>(), pcap, 0, icap,
-                           d_counter.as<unsigned long long>(), d_partials.as<double>(), s, d_items, shard, shards);
+                           d_counter.as<unsigned long long>(), d_partials.as<double>(), s, d_items, shard, shards,
+                           &disc_sc.prectr.as<PreCounters>()->abort);
         record(EV_GAUSS1);
         if (shards == 1)
             launch_reduce_pairs(d_partials.as<double>(), d_item_off.as<int64_t>(), pcap, d_raw.as<double>(),
