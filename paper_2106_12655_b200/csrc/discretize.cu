@@ -32,6 +32,7 @@
 #include <cub/device/device_segmented_sort.cuh>
 
 #include "discretize.cuh"
+#include "scan.cuh"
 #include "geom.cuh"
 
 namespace lc {
@@ -788,11 +789,8 @@ template <class T> T d2h(const void *p, cudaStream_t s) {
 }
 
 void scan_i64(const int64_t *in, int64_t *out, int64_t n, DiscScratch &sc, cudaStream_t s) {
-    size_t bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, (int)n);
-    sc.cub_tmp.reserve(bytes, s);
-    bytes = sc.cub_tmp.bytes;
-    LC_CUB(cub::DeviceScan::ExclusiveSum(sc.cub_tmp.ptr, bytes, in, out, (int)n, s));
+    sc.cub_tmp.reserve(exclusive_scan_i64_tmp_bytes(n) + 16, s);
+    exclusive_scan_i64(in, out, n, sc.cub_tmp.ptr, sc.cub_tmp.bytes, s);
 }
 
 int finish_validation(DiscScratch &sc, const int64_t *off, int64_t L, int closed_layout, const uint8_t *paired,

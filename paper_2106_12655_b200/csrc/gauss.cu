@@ -23,7 +23,7 @@
 // the item range across GPUs.
 #include "gauss.cuh"
 
-#include <cub/device/device_scan.cuh>
+#include "scan.cuh"
 
 namespace lc {
 
@@ -611,11 +611,7 @@ int num_sms() {
     return n;
 }
 
-size_t build_items_scan_bytes(int64_t P) {
-    size_t bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, bytes, (int64_t *)nullptr, (int64_t *)nullptr, (int)(P + 1));
-    return bytes;
-}
+size_t build_items_scan_bytes(int64_t P) { return exclusive_scan_i64_tmp_bytes(P + 1) + 16; }
 
 int64_t build_items(const int32_t *d_pairs, int64_t P, const int64_t *d_voff, PairGeom *d_pg,
                     int64_t *d_item_off, void *d_scan_tmp, size_t scan_tmp_bytes, cudaStream_t s, bool read_back,
@@ -628,8 +624,7 @@ int64_t build_items(const int32_t *d_pairs, int64_t P, const int64_t *d_voff, Pa
     LC_CUDA(cudaMemsetAsync(d_item_off + P, 0, sizeof(int64_t), s));
     pair_geom_kernel<<<(unsigned)ceil_div(P, 256), 256, 0, s>>>(d_pairs, P, d_P, d_voff, d_pg, d_item_off);
     LC_CHECK_LAUNCH();
-    size_t bytes = scan_tmp_bytes;
-    LC_CUB(cub::DeviceScan::ExclusiveSum(d_scan_tmp, bytes, d_item_off, d_item_off, (int)(P + 1), s));
+    exclusive_scan_i64(d_item_off, d_item_off, P + 1, d_scan_tmp, scan_tmp_bytes, s);
     if (!read_back) return -1;   // caller reads item_off[P] together with other results
     int64_t total = 0;
     LC_CUDA(cudaMemcpyAsync(&total, d_item_off + P, sizeof(int64_t), cudaMemcpyDeviceToHost, s));

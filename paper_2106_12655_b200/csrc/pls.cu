@@ -15,6 +15,7 @@
 
 #include "geom.cuh"
 #include "pls.cuh"
+#include "scan.cuh"
 
 namespace lc {
 namespace {
@@ -675,13 +676,9 @@ static void grid_prefix(const double *loop_box, int64_t L, int64_t n_excl, PlsSc
     const unsigned gl = (unsigned)ceil_div(L, 256);
     cell_count_kernel<<<gl, 256, 0, s>>>(loop_box, L, gp, cnt, sc.lcell.as<int32_t>(), sc.lrank.as<int32_t>());
     LC_CHECK_LAUNCH();
-    size_t b = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, b, (int64_t *)nullptr, (int64_t *)nullptr, (int)(max_cells + 1));
-    size_t b2 = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, b2, (int64_t *)nullptr, (int64_t *)nullptr, (int)(L + 1));
-    sc.cub_tmp.reserve(b > b2 ? b : b2, s);
-    b = sc.cub_tmp.bytes;
-    LC_CUB(cub::DeviceScan::ExclusiveSum(sc.cub_tmp.ptr, b, cnt, coff, (int)(max_cells + 1), s));
+    const size_t b = exclusive_scan_i64_tmp_bytes(max_cells + 1), b2 = exclusive_scan_i64_tmp_bytes(L + 1);
+    sc.cub_tmp.reserve((b > b2 ? b : b2) + 16, s);
+    exclusive_scan_i64(cnt, coff, max_cells + 1, sc.cub_tmp.ptr, sc.cub_tmp.bytes, s);
     cell_scatter_kernel<<<gl, 256, 0, s>>>(loop_box, L, coff, sc.lcell.as<int32_t>(), sc.lrank.as<int32_t>(),
                                            sc.perm.as<int32_t>(), sc.sbox.as<double>());
     LC_CHECK_LAUNCH();
@@ -691,9 +688,7 @@ static void grid_prefix(const double *loop_box, int64_t L, int64_t n_excl, PlsSc
                                                sc.pair_keys.as<int32_t>(), nullptr, nullptr,
                                                sc.counts.as<int64_t>(), max_count);
     LC_CHECK_LAUNCH();
-    b = sc.cub_tmp.bytes;
-    LC_CUB(cub::DeviceScan::ExclusiveSum(sc.cub_tmp.ptr, b, sc.counts.as<int64_t>(), sc.offs.as<int64_t>(),
-                                         (int)(L + 1), s));
+    exclusive_scan_i64(sc.counts.as<int64_t>(), sc.offs.as<int64_t>(), L + 1, sc.cub_tmp.ptr, sc.cub_tmp.bytes, s);
 }
 
 int64_t run_pls(const double *loop_box, int64_t L, const uint64_t *h_excl, int64_t n_excl, PlsScratch &sc,
