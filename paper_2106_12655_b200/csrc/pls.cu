@@ -649,7 +649,7 @@ void launch_seg_boxes(const double *coeffs, const double *t, const double *verts
 // host sync): sc.offs[L] = P, *sc.counter = largest row count, slots in
 // sc.pair_keys, row counts in sc.idx.  Excluded keys already in sc.excl.
 static void grid_prefix(const double *loop_box, int64_t L, int64_t n_excl, PlsScratch &sc, cudaStream_t s) {
-    const int64_t max_cells = 4 * L + 64;
+    const int64_t max_cells = 32 * L + 64;   // cells ~ the largest loop extent for surface-like models (tube: 7x fewer candidates than 4L)
     sc.axis.reserve(sizeof(GridParams), s);
     sc.keys.reserve(sizeof(int64_t) * (max_cells + 1), s);         // cell counts
     sc.keys_sorted.reserve(sizeof(int64_t) * (max_cells + 1), s);  // cell offsets
