@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(32 * kBruteWarps) brute_kernel(ActView v, cons
 // test on the double boxes (bvh.py:93-98).  Hits are counted into *marked.
 constexpr int kAnyWarps = 8;
 constexpr int kAnyCap = 64;   // staged survivors per side; beyond that the test reads global memory
-__global__ void __launch_bounds__(32 * kAnyWarps) brute_any_kernel(
+__global__ void __launch_bounds__(32 * kAnyWarps, 3) brute_any_kernel(
     const double *__restrict__ box, const float *__restrict__ fbox, int64_t M, const int64_t *__restrict__ loff,
     const double *__restrict__ lbox, int64_t L, const int32_t *__restrict__ pairs, int64_t P,
     const int64_t *__restrict__ dP, unsigned long long *__restrict__ marked, int *__restrict__ abort) {
@@ -302,23 +302,42 @@ __global__ void __launch_bounds__(32 * kAnyWarps) brute_any_kernel(
         }
         __syncwarp();
         const int ns = cnt[0], nt = cnt[1];
-        const int tot = ns * nt;
         int hits = 0;
-        for (int k = lane; k < tot; k += 32) {
-            const int a = k / nt, b = k % nt;
-            float x[6], y[6];
-            int64_t es, et;
-            if (ns <= kAnyCap && nt <= kAnyCap) {
-                es = sidx[w][0][a];
-                et = sidx[w][1][b];
+        if (ns && nt && ns <= kAnyCap && nt <= kAnyCap) {
+            // lanes take the larger survivor list (its float box in registers), the smaller
+            // one is read from shared memory as a broadcast: ~n_small iterations, no division
+            const int sl = ns >= nt ? 0 : 1, nl = sl ? nt : ns, nq = sl ? ns : nt;
+            for (int base = 0; base < nl; base += 32) {
+                const int l = base + lane;
+                float x[6];
+                int64_t el = -1;
+                if (l < nl) {
+                    el = sidx[w][sl][l];
 #pragma unroll
-                for (int d = 0; d < 6; ++d) {
-                    x[d] = sbox[w][0][d][a];
-                    y[d] = sbox[w][1][d][b];
+                    for (int d = 0; d < 6; ++d) x[d] = sbox[w][sl][d][l];
                 }
-            } else {   // rare: more survivors than staged; re-filter from global memory
-                es = -1;
-                et = -1;
+                for (int q = 0; q < nq; ++q) {
+                    float y[6];
+#pragma unroll
+                    for (int d = 0; d < 6; ++d) y[d] = sbox[w][sl ^ 1][d][q];
+                    if (el < 0 || x[0] > y[3] || y[0] > x[3] || x[1] > y[4] || y[1] > x[4] || x[2] > y[5] ||
+                        y[2] > x[5])
+                        continue;
+                    // a float hit: the exact closed test on the double boxes (bvh.py:93-98)
+                    const int64_t eq = sidx[w][sl ^ 1][q];
+                    double lo[3], hi[3];
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) {
+                        lo[d] = box[d * M + el];
+                        hi[d] = box[(3 + d) * M + el];
+                    }
+                    if (box_overlap(box, M, eq, lo, hi)) ++hits;
+                }
+            }
+        } else if (ns && nt) {   // rare: more survivors than staged — every combination from global memory
+            for (int k = lane; k < ns * nt; k += 32) {
+                const int a = k / nt, b = k % nt;
+                int64_t es = -1, et = -1;
                 int c = 0;
                 for (int64_t q = 0; q < ni && es < 0; ++q) {
                     const float *o = fb[0];
@@ -339,20 +358,14 @@ __global__ void __launch_bounds__(32 * kAnyWarps) brute_any_kernel(
                         c++ == b)
                         et = bj + q;
                 }
+                double lo[3], hi[3];
 #pragma unroll
-                for (int d = 0; d < 6; ++d) {
-                    x[d] = fbox[d * M + es];
-                    y[d] = fbox[d * M + et];
+                for (int d = 0; d < 3; ++d) {
+                    lo[d] = box[d * M + es];
+                    hi[d] = box[(3 + d) * M + es];
                 }
+                if (box_overlap(box, M, et, lo, hi)) ++hits;
             }
-            if (x[0] > y[3] || y[0] > x[3] || x[1] > y[4] || y[1] > x[4] || x[2] > y[5] || y[2] > x[5]) continue;
-            double lo[3], hi[3];
-#pragma unroll
-            for (int d = 0; d < 3; ++d) {
-                lo[d] = box[d * M + es];
-                hi[d] = box[(3 + d) * M + es];
-            }
-            if (box_overlap(box, M, et, lo, hi)) ++hits;
         }
         if (hits) {
             atomicAdd(marked, (unsigned long long)hits);
