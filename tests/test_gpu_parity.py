@@ -430,3 +430,36 @@ def test_sharded_nccl_path_world1():
                           os.path.join(root, "tools", "sharded_smoke.py")],
                          capture_output=True, text=True, timeout=600, cwd=root)
     assert out.returncode == 0 and "sharded smoke ok" in out.stdout, (out.stdout[-2000:], out.stderr[-2000:])
+
+
+def _ring_soup(seed, count=400, n=24, size=12.0, spline=False):
+    rng = np.random.default_rng(seed)
+    th = 2 * np.pi * np.arange(n) / n
+    loops = []
+    for c in rng.uniform(0.0, size, size=(count, 3)):
+        u = rng.normal(size=3)
+        u /= np.linalg.norm(u)
+        v = np.cross(u, rng.normal(size=3))
+        v /= np.linalg.norm(v)
+        pts = c + np.outer(np.cos(th), u) + np.outer(np.sin(th), v)
+        loops.append(lc.LoopGeometry.from_catmull_rom(pts) if spline else lc.LoopGeometry.from_polyline(pts))
+    return lc.CurveModel(loops)
+
+
+@pytest.mark.parametrize("spline", [False, True])
+@pytest.mark.parametrize("seed,count,size", [(1, 400, 12.0), (2, 400, 12.0), (5, 150, 3.0)])
+def test_random_ring_soup_vs_oracle(oracle, seed, count, size, spline):
+    """Random overlapping rings (polyline or spline; near contacts need refinement
+    passes; the dense soup has ~90 partners per PLS row, past the 16 row slots):
+    the device certificate — PLS, discretization, Gauss sums, rounding — equals
+    the oracle's, integers and pair lists exactly, raw sums within RAW_TOL."""
+    from paper_2106_12655_b200.certify import run_device_pipeline
+
+    m = _ring_soup(seed, count=count, size=size, spline=spline)
+    coeffs, t, off = m.packed()
+    want, pairs, raw = oracle.link_matrix(coeffs, t, off, m.xi)
+    got = lc.compute_linking_matrix(m)
+    assert np.array_equal(got.array, want)
+    p2, r2, _, _, ctx = run_device_pipeline(m)
+    assert np.array_equal(np.asarray(p2), pairs)
+    assert np.max(np.abs(np.asarray(r2) - raw)) < RAW_TOL
