@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(32 * kBruteWarps) brute_kernel(ActView v, cons
 // test on the double boxes (bvh.py:93-98).  Hits are counted into *marked.
 constexpr int kAnyWarps = 8;
 constexpr int kAnyCap = 64;   // staged survivors per side; beyond that the test reads global memory
-__global__ void __launch_bounds__(32 * kAnyWarps, 3) brute_any_kernel(
+__global__ void __launch_bounds__(32 * kAnyWarps, 4) brute_any_kernel(
     const double *__restrict__ box, const float *__restrict__ fbox, int64_t M, const int64_t *__restrict__ loff,
     const double *__restrict__ lbox, int64_t L, const int32_t *__restrict__ pairs, int64_t P,
     const int64_t *__restrict__ dP, unsigned long long *__restrict__ marked, int *__restrict__ abort) {
@@ -264,40 +264,33 @@ __global__ void __launch_bounds__(32 * kAnyWarps, 3) brute_any_kernel(
             fb[1][d] = __double2float_rd(lbox[d * L + i]);
             fb[1][3 + d] = __double2float_ru(lbox[(3 + d) * L + i]);
         }
-        const int64_t ntot = ni + nj;
+        // side 0: loop i's segments vs loop j's box; side 1 only if side 0 kept any
         int cnt[2] = {0, 0};
-        for (int64_t e0 = 0; e0 < ntot; e0 += 128) {
-            float v[4][6];
-            int64_t seg[4];
-            bool ok[4];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {   // four chunks of 32 entries: 24 loads in flight
-                const int64_t e = e0 + 32 * c + lane;
-                ok[c] = e < ntot;
-                seg[c] = e < ni ? bi + e : bj + (e - ni);
+        for (int sd = 0; sd < 2; ++sd) {
+            if (sd == 1 && cnt[0] == 0) break;   // no survivor on one side: no hit possible
+            const float *o = fb[sd];
+            const int64_t base = sd ? bj : bi;
+            const int n = (int)(sd ? nj : ni);
+#pragma unroll 2
+            for (int k0 = 0; k0 < n; k0 += 32) {
+                const int k = k0 + lane;
+                const int64_t e = base + k;
+                float v[6];
 #pragma unroll
-                for (int d = 0; d < 6; ++d) v[c][d] = ok[c] ? fbox[d * M + seg[c]] : 0.f;
-            }
+                for (int d = 0; d < 6; ++d) v[d] = k < n ? fbox[d * M + e] : 0.f;
+                const bool in = k < n && !(o[0] > v[3] || v[0] > o[3] || o[1] > v[4] || v[1] > o[4] ||
+                                           o[2] > v[5] || v[2] > o[5]);
+                const unsigned bal = __ballot_sync(0xffffffffu, in);
+                if (in) {
+                    const int r = cnt[sd] + __popc(bal & ((1u << lane) - 1u));
+                    if (r < kAnyCap) {
+                        sidx[w][sd][r] = (int32_t)e;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const int64_t e = e0 + 32 * c + lane;
-                const int side = e < ni ? 0 : 1;
-                const float *o = fb[side];
-                const bool in = ok[c] && !(o[0] > v[c][3] || v[c][0] > o[3] || o[1] > v[c][4] || v[c][1] > o[4] ||
-                                           o[2] > v[c][5] || v[c][2] > o[5]);
-#pragma unroll
-                for (int sd = 0; sd < 2; ++sd) {
-                    const unsigned bal = __ballot_sync(0xffffffffu, in && side == sd);
-                    if (in && side == sd) {
-                        const int r = cnt[sd] + __popc(bal & ((1u << lane) - 1u));
-                        if (r < kAnyCap) {
-                            sidx[w][sd][r] = (int32_t)seg[c];
-#pragma unroll
-                            for (int d = 0; d < 6; ++d) sbox[w][sd][d][r] = v[c][d];
-                        }
+                        for (int d = 0; d < 6; ++d) sbox[w][sd][d][r] = v[d];
                     }
-                    cnt[sd] += __popc(bal);
                 }
+                cnt[sd] += __popc(bal);
             }
         }
         __syncwarp();

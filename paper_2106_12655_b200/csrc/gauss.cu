@@ -459,22 +459,7 @@ __global__ void pair_geom_kernel(const int32_t *__restrict__ pairs, int64_t P, c
         return;
     }
     const int i = pairs[2 * p], j = pairs[2 * p + 1];
-    PairGeom g;
-    g.col_off = voff[i];
-    g.row_off = voff[j];
-    g.ncols = (int)(voff[i + 1] - voff[i] - 1);
-    g.nrows = (int)(voff[j + 1] - voff[j] - 1);
-    const int nb = (g.nrows + R - 1) / R;
-    int rbl = 0;
-    while ((1 << rbl) < nb && rbl < 5) ++rbl;
-    g.rb_log2 = rbl;
-    const int cs = 32 >> rbl;
-    const int cl = (g.ncols + cs - 1) / cs;
-    g.cl = cl < kMaxColsPerLane ? (cl > 0 ? cl : 1) : kMaxColsPerLane;
-    g.items_r = (g.nrows + (R << rbl) - 1) / (R << rbl);
-    const int64_t span = (int64_t)cs * g.cl;
-    g.items_c = (int)((g.ncols + span - 1) / span);
-    if (g.nrows <= 0 || g.ncols <= 0) g.items_r = g.items_c = 0;
+    const PairGeom g = make_pair_geom(voff[i], voff[j], (int)(voff[i + 1] - voff[i] - 1), (int)(voff[j + 1] - voff[j] - 1));
     pg[p] = g;
     nitems[p] = (int64_t)g.items_r * g.items_c;
 }

@@ -34,6 +34,28 @@ struct PairGeom {
     int32_t items_c;
 };
 
+// Tiling of pair (column loop i, row loop j) from the two loops' closed-vertex
+// offsets and segment counts (one definition for every path that builds items).
+__host__ __device__ inline PairGeom make_pair_geom(int64_t col_off, int64_t row_off, int ncols, int nrows) {
+    PairGeom g;
+    g.col_off = col_off;
+    g.row_off = row_off;
+    g.ncols = ncols;
+    g.nrows = nrows;
+    const int nb = (nrows + kRowsPerLane - 1) / kRowsPerLane;
+    int rbl = 0;
+    while ((1 << rbl) < nb && rbl < 5) ++rbl;
+    g.rb_log2 = rbl;
+    const int cs = 32 >> rbl;
+    const int cl = (ncols + cs - 1) / cs;
+    g.cl = cl < kMaxColsPerLane ? (cl > 0 ? cl : 1) : kMaxColsPerLane;
+    g.items_r = (nrows + (kRowsPerLane << rbl) - 1) / (kRowsPerLane << rbl);
+    const int64_t span = (int64_t)cs * g.cl;
+    g.items_c = (int)((ncols + span - 1) / span);
+    if (nrows <= 0 || ncols <= 0) g.items_r = g.items_c = 0;
+    return g;
+}
+
 // Builds PairGeom[P] and item_off[P+1] (exclusive prefix of items per pair).
 // voff: closed-loop SoA vertex offsets (L+1). Returns total item count (syncs).
 // d_P (fused path): P is the capacity, the device count *d_P <= P is used and

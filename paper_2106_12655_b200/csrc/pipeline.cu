@@ -52,8 +52,8 @@ __global__ void export_results_kernel(const int64_t *__restrict__ dP, int64_t ca
     }
     if (st && blockIdx.x == 0 && threadIdx.x == 0) {
         FastStatus f;
-        f.P = *dP;
-        f.n_items = *d_items;
+        f.P = dP[2];          // the real counts (dP[0], dP[1] are 0 for an unusable run)
+        f.n_items = dP[3];
         f.max_row = *d_max_row;
         f.zero_loop = ctr->zero_loop;
         f.n_unpaired = ctr->n_unpaired;
@@ -70,13 +70,18 @@ __global__ void export_results_kernel(const int64_t *__restrict__ dP, int64_t ca
 void Pipeline::init(cudaStream_t st) {
     s = st;
     for (auto &e : ev) LC_CUDA(cudaEventCreate(&e));
-    for (auto &x : side) LC_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+    // the checks branch runs at the highest priority: its blocks are dispatched ahead
+    // of the Gauss kernel's persistent CTAs when both become ready after the PLS
+    int prio_lo = 0, prio_hi = 0;
+    LC_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    LC_CUDA(cudaStreamCreateWithPriority(&side[0], cudaStreamNonBlocking, prio_lo));
+    LC_CUDA(cudaStreamCreateWithPriority(&side[1], cudaStreamNonBlocking, prio_hi));
     for (cudaEvent_t *e : {&ev_fork, &ev_chords, &ev_pairs, &ev_checks})
         LC_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
 }
 
 void Pipeline::release() {
-    DevBuf *bufs[] = {&d_coeffs, &d_t, &d_loff, &d_seg_box, &d_seg_fbox, &d_loop_keys, &d_seg_loop, &d_loop_box, &d_min_diag, &d_model_exp,
+    DevBuf *bufs[] = {&d_tot, &d_coeffs, &d_t, &d_loff, &d_seg_box, &d_seg_fbox, &d_loop_keys, &d_seg_loop, &d_loop_box, &d_min_diag, &d_model_exp,
                       &d_verts_in, &d_aos, &d_in_off, &d_voff, &d_X, &d_Y, &d_Z, &d_exp, &d_tmp_aos, &d_pairs,
                       &d_pg, &d_item_off, &d_item_pair, &d_scan, &d_counter, &d_partials, &d_raw, &d_lk, &d_flags,
                       &d_quads, &d_qout, &dout.X, &dout.Y, &dout.Z, &dout.voff, &dout.vert_off};
@@ -425,7 +430,9 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
     if (shards < 1 || shard < 0 || shard >= shards) throw Error(LC_ERR_ARG, "bad shard");
     // loops longer than the brute-force side limit make every pair they are in a
     // large (sweep) pair: the staged path handles those models directly
-    if (!model_ready || L < 2 || M == 0 || prm.max_passes < 1 || max_loop > 256) return FAST_FALLBACK;
+    if (!model_ready || L < 2 || M == 0 || prm.max_passes < 1 || max_loop > 256 ||
+        (int64_t)kRowSlots * L >= (int64_t(1) << 24))   // the packed row scan holds P in 24 bits
+        return FAST_FALLBACK;
     if (mode < GAUSS_PHASE || mode > 7) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
     // pair capacity: the grid PLS bound (16 per row) until a run has shown the
     // model's pair count; then that plus headroom (smaller grids and scans)
@@ -442,6 +449,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
     d_item_off.reserve(sizeof(int64_t) * (pcap + 1), s);
     d_scan.reserve(build_items_scan_bytes(pcap), s);
     d_counter.reserve(sizeof(unsigned long long), s);
+    d_tot.reserve(4 * sizeof(int64_t), s);
     const int64_t part_cap = ceil_div(icap, shards) * shards;   // every shard's slice fits at shard * per
     d_partials.reserve(sizeof(double) * part_cap, s);
     d_item_pair.reserve(sizeof(int32_t) * icap, s);
@@ -475,9 +483,10 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
         if (n_excl > 0)
             LC_CUDA(cudaMemcpyAsync(pls_sc.excl.ptr, h_excl.ptr, sizeof(uint64_t) * n_excl, cudaMemcpyHostToDevice,
                                     s));
-        const int64_t *dP = nullptr;
         const int *dmx = nullptr;
-        launch_pls_grid(d_loop_box.as<double>(), L, n_excl, pls_sc, d_pairs.as<int32_t>(), pcap, s, &dP, &dmx);
+        launch_pls_grid(d_loop_box.as<double>(), L, n_excl, pls_sc, d_pairs.as<int32_t>(), pcap, d_loff.as<int64_t>(),
+                        d_pg.as<PairGeom>(), d_item_off.as<int64_t>(), d_tot.as<int64_t>(), icap, s, &dmx);
+        const int64_t *dP = d_tot.as<int64_t>(), *d_items = d_tot.as<int64_t>() + 1;
         record(EV_PLS);
         // branch 2: pass-1 detection + validation only feed the status — they run
         // beside the work items and the Gauss sum
@@ -491,11 +500,8 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
                                                         reinterpret_cast<int2 *>(hp), nullptr, nullptr, nullptr);
         LC_CHECK_LAUNCH();
         LC_CUDA(cudaEventRecord(ev_checks, side[1]));
-        LC_CUDA(cudaStreamWaitEvent(s, ev_chords, 0));   // items read the closed offsets, the sum the chords
-        build_items(d_pairs.as<int32_t>(), pcap, dout.voff.as<int64_t>(), d_pg.as<PairGeom>(),
-                    d_item_off.as<int64_t>(), d_scan.ptr, d_scan.bytes, s, false, dP);
-        const int64_t *d_items = d_item_off.as<int64_t>() + pcap;
         launch_item_pairs_dev(d_item_off.as<int64_t>(), pcap, dP, icap, d_item_pair.as<int32_t>(), s);
+        LC_CUDA(cudaStreamWaitEvent(s, ev_chords, 0));   // the sum reads the chords
         record(EV_GAUSS0);
         launch_gauss_items(mode, dout.X.as<double>(), dout.Y.as<double>(), dout.Z.as<double>(), d_pg.as<PairGeom>(),
                            d_item_off.as<int64_t>(), d_item_pair.as<int32_t>(), pcap, 0, icap,

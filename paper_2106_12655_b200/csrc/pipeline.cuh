@@ -58,7 +58,7 @@ struct Pipeline {
     int64_t P = 0;
 
     // Work items and results.
-    DevBuf d_pg, d_item_off, d_item_pair, d_scan, d_counter, d_partials, d_raw, d_lk, d_flags, d_quads, d_qout;
+    DevBuf d_tot, d_pg, d_item_off, d_item_pair, d_scan, d_counter, d_partials, d_raw, d_lk, d_flags, d_quads, d_qout;
     int64_t n_items = 0;
 
     void init(cudaStream_t st);

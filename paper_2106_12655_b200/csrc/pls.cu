@@ -14,11 +14,14 @@
 #include <cub/device/device_scan.cuh>
 
 #include "geom.cuh"
+#include "gauss.cuh"
 #include "pls.cuh"
 #include "scan.cuh"
 
 namespace lc {
 namespace {
+
+constexpr int kPackShift = 24;   // fused-path row scan: pair count in the low 24 bits, items above
 
 __device__ __forceinline__ int exp_field(double x) { return (__double2hiint(x) >> 20) & 0x7ff; }
 
@@ -416,7 +419,8 @@ __global__ void grid_query_warp_kernel(const double *__restrict__ lbox, int64_t 
                                        const double *__restrict__ cbox, const uint64_t *__restrict__ excl,
                                        int64_t n_excl, int *__restrict__ row_count, int32_t *__restrict__ slots,
                                        const int64_t *__restrict__ offs, uint64_t *__restrict__ keys,
-                                       int64_t *__restrict__ counts64, int *__restrict__ overflow) {
+                                       int64_t *__restrict__ counts64, int *__restrict__ overflow,
+                                       const int64_t *__restrict__ item_loff) {
     const int lane = threadIdx.x & 31;
     const int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     if (a >= L) return;
@@ -432,7 +436,9 @@ __global__ void grid_query_warp_kernel(const double *__restrict__ lbox, int64_t 
     }
     const int ny = c1[1] - c0[1] + 1, nrows_all = ny * (c1[2] - c0[2] + 1);   // <= 25 (cells >= any extent)
     int n = 0;
+    int64_t row_items = 0;   // fused path: work items of this row's pairs (the loops' segment counts)
     const int64_t w0 = SLOTS ? 0 : offs[a];
+    const int ncols_a = item_loff ? (int)(item_loff[a + 1] - item_loff[a]) : 0;
     for (int rb = 0; rb < nrows_all; rb += 32) {   // one batch unless the grid is degenerate
     const int nrows = nrows_all - rb < 32 ? nrows_all - rb : 32;
     int64_t kb = 0, len = 0;
@@ -477,6 +483,10 @@ __global__ void grid_query_warp_kernel(const double *__restrict__ lbox, int64_t 
             if (hit && n_excl && is_excluded(excl, n_excl, ((uint64_t)a << 32) | (uint64_t)b)) hit = false;
         }
         const unsigned bal = __ballot_sync(0xffffffffu, hit);
+        if (SLOTS && item_loff && hit) {
+            const PairGeom pgm = make_pair_geom(0, 0, ncols_a, (int)(item_loff[b + 1] - item_loff[b]));
+            row_items += (int64_t)pgm.items_r * pgm.items_c;
+        }
         if (hit) {
             const int rk = n + __popc(bal & ((1u << lane) - 1u));
             if (SLOTS) {
@@ -488,9 +498,14 @@ __global__ void grid_query_warp_kernel(const double *__restrict__ lbox, int64_t 
         n += __popc(bal);
     }
     }
+    if (SLOTS && item_loff) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) row_items += __shfl_xor_sync(0xffffffffu, row_items, o);
+    }
     if (SLOTS && lane == 0) {
         row_count[a] = n;
-        counts64[a] = n;                      // scanned into the pair offsets
+        // scanned into the pair offsets (fused path: items << kPackShift | pairs, one scan for both)
+        counts64[a] = item_loff ? (row_items << kPackShift) | (int64_t)n : (int64_t)n;
         if (a == L - 1) counts64[L] = 0;
         if (n > kRowSlots) atomicMax(overflow, n);   // rare: the two-pass variant takes over
     }
@@ -596,6 +611,62 @@ __global__ void slots_compact_kernel(const int *__restrict__ row_count, const in
         }
 }
 
+// Fused path: compaction that also lays out the work items — PairGeom and the
+// exclusive item offset of every pair — from the packed (items, pairs) row scan;
+// the last row stores P and the item total (d_tot[0], d_tot[1]) and item_off[P].
+__global__ void slots_compact_items_kernel(const int *__restrict__ row_count, const int64_t *__restrict__ offs,
+                                           int64_t L, const int32_t *__restrict__ slots, int32_t *__restrict__ pairs,
+                                           int64_t cap, const int64_t *__restrict__ loff, PairGeom *__restrict__ pg,
+                                           int64_t *__restrict__ item_off, int64_t *__restrict__ d_tot,
+                                           const int *__restrict__ overflow, int64_t item_cap) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= L) return;
+    const int64_t mask = (int64_t(1) << kPackShift) - 1;
+    const int n = row_count[i] < kRowSlots ? row_count[i] : kRowSlots;
+    int32_t v[kRowSlots];
+#pragma unroll
+    for (int k = 0; k < kRowSlots; ++k) v[k] = k < n ? slots[i * kRowSlots + k] : INT_MAX;
+#pragma unroll
+    for (int a = 1; a < kRowSlots; ++a)
+#pragma unroll
+        for (int b = a; b > 0; --b)
+            if (v[b] < v[b - 1]) {
+                const int32_t t = v[b];
+                v[b] = v[b - 1];
+                v[b - 1] = t;
+            }
+    const int64_t packed = offs[i], o = packed & mask;
+    int64_t it = packed >> kPackShift;
+    const int64_t ci = loff[i] + i;   // closed-vertex offset of loop i (vertex 0 repeated per loop)
+    const int ncols = (int)(loff[i + 1] - loff[i]);
+#pragma unroll
+    for (int k = 0; k < kRowSlots; ++k)
+        if (k < n) {
+            const int32_t j = v[k];
+            const PairGeom g = make_pair_geom(ci, loff[j] + j, ncols, (int)(loff[j + 1] - loff[j]));
+            if (o + k < cap) {
+                pairs[2 * (o + k)] = (int32_t)i;
+                pairs[2 * (o + k) + 1] = j;
+                pg[o + k] = g;
+                item_off[o + k] = it;
+            }
+            it += (int64_t)g.items_r * g.items_c;
+        }
+    if (i == L - 1) {
+        const int64_t tot = offs[L], P = tot & mask, items = tot >> kPackShift;
+        // a run that cannot be the reference's (row slots overflowed, or more pairs /
+        // items than the capacities) hands 0 pairs to everything downstream; the
+        // status reports the real counts and the caller reruns on the staged path
+        const bool usable = P <= cap && items <= item_cap && *overflow <= kRowSlots;
+        d_tot[0] = usable ? P : 0;
+        d_tot[1] = usable ? items : 0;
+        d_tot[2] = P;
+        d_tot[3] = items;
+        if (usable) item_off[P] = items;
+        else item_off[0] = 0;
+    }
+}
+
 __global__ void unpack_pairs_kernel(const uint64_t *__restrict__ keys, int64_t P, int32_t *__restrict__ pairs) {
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p >= P) return;
@@ -648,7 +719,8 @@ void launch_seg_boxes(const double *coeffs, const double *t, const double *verts
 // Grid culling up to the per-row pair counts and their exclusive scan (no
 // host sync): sc.offs[L] = P, *sc.counter = largest row count, slots in
 // sc.pair_keys, row counts in sc.idx.  Excluded keys already in sc.excl.
-static void grid_prefix(const double *loop_box, int64_t L, int64_t n_excl, PlsScratch &sc, cudaStream_t s) {
+static void grid_prefix(const double *loop_box, int64_t L, int64_t n_excl, PlsScratch &sc, cudaStream_t s,
+                        const int64_t *item_loff = nullptr) {
     const int64_t max_cells = 32 * L + 64;   // cells ~ the largest loop extent for surface-like models (tube: 7x fewer candidates than 4L)
     sc.axis.reserve(sizeof(GridParams), s);
     sc.keys.reserve(sizeof(int64_t) * (max_cells + 1), s);         // cell counts
@@ -686,7 +758,7 @@ static void grid_prefix(const double *loop_box, int64_t L, int64_t n_excl, PlsSc
     grid_query_warp_kernel<true><<<(unsigned)ceil_div(L * 32, 256), 256, 0, s>>>(loop_box, L, gp, coff, sc.perm.as<int32_t>(),
                                                sc.sbox.as<double>(), sc.excl.as<uint64_t>(), n_excl, row_count,
                                                sc.pair_keys.as<int32_t>(), nullptr, nullptr,
-                                               sc.counts.as<int64_t>(), max_count);
+                                               sc.counts.as<int64_t>(), max_count, item_loff);
     LC_CHECK_LAUNCH();
     exclusive_scan_i64(sc.counts.as<int64_t>(), sc.offs.as<int64_t>(), L + 1, sc.cub_tmp.ptr, sc.cub_tmp.bytes, s);
 }
@@ -722,7 +794,7 @@ int64_t run_pls(const double *loop_box, int64_t L, const uint64_t *h_excl, int64
         grid_query_warp_kernel<false><<<(unsigned)ceil_div(L * 32, 256), 256, 0, s>>>(loop_box, L, gp, coff, sc.perm.as<int32_t>(),
                                                     sc.sbox.as<double>(), sc.excl.as<uint64_t>(), n_excl, nullptr, nullptr,
                                                     sc.offs.as<int64_t>(), sc.pair_keys.as<uint64_t>(), nullptr,
-                                                    nullptr);
+                                                    nullptr, nullptr);
         LC_CHECK_LAUNCH();
         size_t b3 = 0;
         cub::DeviceRadixSort::SortKeys(nullptr, b3, (uint64_t *)nullptr, (uint64_t *)nullptr, (int)P);
@@ -789,12 +861,14 @@ int64_t run_pls(const double *loop_box, int64_t L, const uint64_t *h_excl, int64
 }
 
 void launch_pls_grid(const double *loop_box, int64_t L, int64_t n_excl, PlsScratch &sc, int32_t *pairs, int64_t cap,
-                     cudaStream_t s, const int64_t **d_P, const int **d_max_row) {
-    grid_prefix(loop_box, L, n_excl, sc, s);
-    slots_compact_kernel<<<(unsigned)ceil_div(L, 256), 256, 0, s>>>(sc.idx.as<int>(), sc.offs.as<int64_t>(), L,
-                                                                    sc.pair_keys.as<int32_t>(), pairs, cap);
+                     const int64_t *loff, PairGeom *pg, int64_t *item_off, int64_t *d_tot, int64_t item_cap,
+                     cudaStream_t s, const int **d_max_row) {
+    grid_prefix(loop_box, L, n_excl, sc, s, loff);
+    slots_compact_items_kernel<<<(unsigned)ceil_div(L, 256), 256, 0, s>>>(sc.idx.as<int>(), sc.offs.as<int64_t>(), L,
+                                                                          sc.pair_keys.as<int32_t>(), pairs, cap, loff,
+                                                                          pg, item_off, d_tot, sc.counter.as<int>(),
+                                                                          item_cap);
     LC_CHECK_LAUNCH();
-    *d_P = sc.offs.as<int64_t>() + L;
     *d_max_row = sc.counter.as<int>();
 }
 

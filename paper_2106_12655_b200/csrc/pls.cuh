@@ -41,13 +41,21 @@ struct PlsScratch {
 int64_t run_pls(const double *loop_box, int64_t L, const uint64_t *h_excl, int64_t n_excl, PlsScratch &sc,
                 DevBuf &pairs, cudaStream_t s, bool force_sweep = false);
 
-// Grid-culling PLS without any host sync (the fused pipeline): the excluded
-// keys must already be in sc.excl (n_excl of them); pairs go to `pairs`
-// (capacity cap pairs, >= kRowSlots * L).  *d_P -> device P, *d_max_row ->
-// device largest per-row count; the result is exact iff max_row <= kRowSlots
-// (and then P <= kRowSlots * L).
+// Grid-culling PLS without any host sync (the fused pipeline), which also lays
+// out the Gauss-sum work items of the no-refinement case (chords = segment
+// start points, so a pair's tiling follows from the loops' segment counts):
+// the excluded keys must already be in sc.excl (n_excl of them); pairs go to
+// `pairs` (capacity cap), PairGeom to pg, exclusive item offsets to item_off
+// (item_off[P] = total), d_tot[0] = P and d_tot[1] = item total on the device
+// — both 0 when the run cannot be exact (row overflow, P > cap, items >
+// item_cap: nothing downstream then reads past the capacities) — and
+// d_tot[2], d_tot[3] = the real P and item total for the status.
+// *d_max_row -> device flag > kRowSlots when some row overflowed its slots
+// (then the result is not exact and the caller falls back).  Needs 16 L < 2^24.
 constexpr int kRowSlots = 16;
+struct PairGeom;
 void launch_pls_grid(const double *loop_box, int64_t L, int64_t n_excl, PlsScratch &sc, int32_t *pairs, int64_t cap,
-                     cudaStream_t s, const int64_t **d_P, const int **d_max_row);
+                     const int64_t *loff, PairGeom *pg, int64_t *item_off, int64_t *d_tot, int64_t item_cap,
+                     cudaStream_t s, const int **d_max_row);
 
 }  // namespace lc
