@@ -242,20 +242,23 @@ __global__ void __launch_bounds__(32 * kBruteWarps) brute_kernel(ActView v, cons
 // test on the double boxes (bvh.py:93-98).  Hits are counted into *marked.
 constexpr int kAnyWarps = 8;
 constexpr int kAnyCap = 64;   // staged survivors per side; beyond that the test reads global memory
-__global__ void __launch_bounds__(32 * kAnyWarps, 4) brute_any_kernel(
-    const double *__restrict__ box, const float *__restrict__ fbox, int64_t M, const int64_t *__restrict__ loff,
-    const double *__restrict__ lbox, int64_t L, const int32_t *__restrict__ pairs, int64_t P,
-    const int64_t *__restrict__ dP, unsigned long long *__restrict__ marked, int *__restrict__ abort) {
-    __shared__ int32_t sidx[kAnyWarps][2][kAnyCap];
-    __shared__ float sbox[kAnyWarps][2][6][kAnyCap];
-    if (dP && *dP < P) P = *dP;
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t nw = (int64_t)gridDim.x * kAnyWarps;
-    for (int64_t p = blockIdx.x * (int64_t)kAnyWarps + w; p < P; p += nw) {
+
+// One pair: the warp's share of the pass-1 detection (see brute_any_kernel).
+__device__ __forceinline__ void brute_any_pair(int64_t p, const double *__restrict__ box, const float *__restrict__ fbox,
+                                               int64_t M, const int64_t *__restrict__ loff,
+                                               const double *__restrict__ lbox, int64_t L,
+                                               const int32_t *__restrict__ pairs, int32_t *sidx0, int32_t *sidx1,
+                                               float *sbox0, float *sbox1, int lane,
+                                               unsigned long long *__restrict__ marked, int *__restrict__ abort) {
+    int32_t *sidx_[2] = {sidx0, sidx1};
+    float *sbox_[2] = {sbox0, sbox1};
+#define sidx_at(sd, r) sidx_[sd][r]
+#define sbox_at(sd, d, r) sbox_[sd][(d) * kAnyCap + (r)]
+
         const int i = pairs[2 * p], j = pairs[2 * p + 1];
         const int64_t bi = loff[i], ni = loff[i + 1] - bi;
         const int64_t bj = loff[j], nj = loff[j + 1] - bj;
-        if (ni == 0 || nj == 0 || !brute_pair(ni, nj)) continue;
+        if (ni == 0 || nj == 0 || !brute_pair(ni, nj)) return;
         float fb[2][6];   // [0]: loop j's box (filters side i), [1]: loop i's box (filters side j)
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
@@ -285,9 +288,9 @@ __global__ void __launch_bounds__(32 * kAnyWarps, 4) brute_any_kernel(
                 if (in) {
                     const int r = cnt[sd] + __popc(bal & ((1u << lane) - 1u));
                     if (r < kAnyCap) {
-                        sidx[w][sd][r] = (int32_t)e;
+                        sidx_at(sd, r) = (int32_t)e;
 #pragma unroll
-                        for (int d = 0; d < 6; ++d) sbox[w][sd][d][r] = v[d];
+                        for (int d = 0; d < 6; ++d) sbox_at(sd, d, r) = v[d];
                     }
                 }
                 cnt[sd] += __popc(bal);
@@ -305,19 +308,19 @@ __global__ void __launch_bounds__(32 * kAnyWarps, 4) brute_any_kernel(
                 float x[6];
                 int64_t el = -1;
                 if (l < nl) {
-                    el = sidx[w][sl][l];
+                    el = sidx_at(sl, l);
 #pragma unroll
-                    for (int d = 0; d < 6; ++d) x[d] = sbox[w][sl][d][l];
+                    for (int d = 0; d < 6; ++d) x[d] = sbox_at(sl, d, l);
                 }
                 for (int q = 0; q < nq; ++q) {
                     float y[6];
 #pragma unroll
-                    for (int d = 0; d < 6; ++d) y[d] = sbox[w][sl ^ 1][d][q];
+                    for (int d = 0; d < 6; ++d) y[d] = sbox_at(sl ^ 1, d, q);
                     if (el < 0 || x[0] > y[3] || y[0] > x[3] || x[1] > y[4] || y[1] > x[4] || x[2] > y[5] ||
                         y[2] > x[5])
                         continue;
                     // a float hit: the exact closed test on the double boxes (bvh.py:93-98)
-                    const int64_t eq = sidx[w][sl ^ 1][q];
+                    const int64_t eq = sidx_at(sl ^ 1, q);
                     double lo[3], hi[3];
 #pragma unroll
                     for (int d = 0; d < 3; ++d) {
@@ -365,7 +368,40 @@ __global__ void __launch_bounds__(32 * kAnyWarps, 4) brute_any_kernel(
             if (abort) *abort = 1;
         }
         __syncwarp();
-    }
+    #undef sidx_at
+#undef sbox_at
+}
+
+__global__ void __launch_bounds__(32 * kAnyWarps, 4) brute_any_kernel(
+    const double *__restrict__ box, const float *__restrict__ fbox, int64_t M, const int64_t *__restrict__ loff,
+    const double *__restrict__ lbox, int64_t L, const int32_t *__restrict__ pairs, int64_t P,
+    const int64_t *__restrict__ dP, unsigned long long *__restrict__ marked, int *__restrict__ abort) {
+    __shared__ int32_t sidx[kAnyWarps][2][kAnyCap];
+    __shared__ float sbox[kAnyWarps][2][6 * kAnyCap];
+    if (dP && *dP < P) P = *dP;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * kAnyWarps;
+    for (int64_t p = blockIdx.x * (int64_t)kAnyWarps + w; p < P; p += nw)
+        brute_any_pair(p, box, fbox, M, loff, lbox, L, pairs, sidx[w][0], sidx[w][1], sbox[w][0], sbox[w][1], lane,
+                       marked, abort);
+}
+
+// The same as single-warp blocks of kAnyLitePairs pairs capped at 32 registers:
+// a block fits beside the Gauss kernel's three 168-register CTAs on an SM
+// (1024 registers left), so the checks use the issue slots the FP64-bound sum
+// leaves free instead of taking SMs from it.
+constexpr int kAnyLitePairs = 4;
+__global__ void __maxnreg__(32) brute_any_lite_kernel(
+    const double *__restrict__ box, const float *__restrict__ fbox, int64_t M, const int64_t *__restrict__ loff,
+    const double *__restrict__ lbox, int64_t L, const int32_t *__restrict__ pairs, int64_t P,
+    const int64_t *__restrict__ dP, unsigned long long *__restrict__ marked, int *__restrict__ abort) {
+    __shared__ int32_t sidx[2][kAnyCap];
+    __shared__ float sbox[2][6 * kAnyCap];
+    if (dP && *dP < P) P = *dP;
+    const int lane = threadIdx.x & 31;
+    const int64_t p0 = (int64_t)blockIdx.x * kAnyLitePairs;
+    for (int64_t p = p0; p < p0 + kAnyLitePairs && p < P; ++p)
+        brute_any_pair(p, box, fbox, M, loff, lbox, L, pairs, sidx[0], sidx[1], sbox[0], sbox[1], lane, marked, abort);
 }
 
 // Union box of every loop's active subsegments (warp per loop).
@@ -1290,10 +1326,19 @@ void launch_discretize_checks(const DiscInput &in, const int64_t *d_P, const Dis
         LC_CHECK_LAUNCH();
     }
     if (Pcap > 0 && M > 0) {
-        const int64_t blocks = ceil_div(Pcap, kAnyWarps) < 148 * 8 ? ceil_div(Pcap, kAnyWarps) : 148 * 8;
-        brute_any_kernel<<<(unsigned)blocks, 32 * kAnyWarps, 0, s>>>(in.seg_box, in.seg_fbox, M, in.loff,
-                                                                     in.loop_box, L, in.pairs, Pcap, d_P,
-                                                                     &ctr->marked, &ctr->abort);
+        static const bool lite = [] {
+            const char *e = getenv("LINKCERT_BRUTE_LITE");
+            return !(e && e[0] == '0');
+        }();
+        if (lite) {
+            brute_any_lite_kernel<<<(unsigned)ceil_div(Pcap, kAnyLitePairs), 32, 0, s>>>(
+                in.seg_box, in.seg_fbox, M, in.loff, in.loop_box, L, in.pairs, Pcap, d_P, &ctr->marked, &ctr->abort);
+        } else {
+            const int64_t blocks = ceil_div(Pcap, kAnyWarps) < 148 * 8 ? ceil_div(Pcap, kAnyWarps) : 148 * 8;
+            brute_any_kernel<<<(unsigned)blocks, 32 * kAnyWarps, 0, s>>>(in.seg_box, in.seg_fbox, M, in.loff,
+                                                                         in.loop_box, L, in.pairs, Pcap, d_P,
+                                                                         &ctr->marked, &ctr->abort);
+        }
         LC_CHECK_LAUNCH();
     }
     if (chords_done) LC_CUDA(cudaStreamWaitEvent(s, chords_done, 0));   // validation reads the chord flags

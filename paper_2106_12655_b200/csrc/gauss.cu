@@ -378,8 +378,7 @@ __device__ __forceinline__ int64_t find_pair(const int64_t *__restrict__ item_of
 template <int MODE, int MINB, bool KSM = false>
 __global__ void __launch_bounds__(kCtaThreads, MINB) gauss_items_kernel(
     const double *__restrict__ X, const double *__restrict__ Y, const double *__restrict__ Z,
-    const PairGeom *__restrict__ pg, const int64_t *__restrict__ item_off, const int32_t *__restrict__ item_pair,
-    int64_t P, int64_t item_begin, int64_t item_end, unsigned long long *__restrict__ counter,
+    const ItemRec *__restrict__ items, int64_t item_begin, int64_t item_end, unsigned long long *__restrict__ counter,
     double *__restrict__ partials, const int64_t *__restrict__ d_end, int shard, int shards,
     const int *__restrict__ abort) {
     __shared__ double ksh[KSM ? 3 * (R + 1) * kCtaThreads : 1];
@@ -405,22 +404,22 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) gauss_items_kernel(
         k = __shfl_sync(0xffffffffu, k_next, 0);
         if (lane == 0 && item_begin + (int64_t)k < item_end) k_next = atomicAdd(counter, 1ULL);
 #else
-        if (lane == 0) k = atomicAdd(counter, 1ULL);
+        // fused path: the abort flag (the concurrent pass-1 checks found the run
+        // unusable; a staged rerun follows) is read with the item claim, so both
+        // round trips overlap; lane 0 reads it so the whole warp leaves together
+        int ab = 0;
+        if (lane == 0) {
+            k = atomicAdd(counter, 1ULL);
+            if (abort) ab = *(volatile const int *)abort;
+        }
         k = __shfl_sync(0xffffffffu, k, 0);
+        if (__shfl_sync(0xffffffffu, ab, 0)) break;
 #endif
         const int64_t it = item_begin + (int64_t)k;
         if (it >= item_end) break;
-        // fused path: the concurrent pass-1 checks found the run unusable (staged rerun
-        // follows); lane 0 reads the flag so the whole warp leaves together
-        if (abort) {
-            int ab = 0;
-            if (lane == 0) ab = *(volatile const int *)abort;
-            if (__shfl_sync(0xffffffffu, ab, 0)) break;
-        }
-        const int64_t p = item_pair ? (int64_t)__ldg(item_pair + it) : find_pair(item_off, P, it);
-        const PairGeom g = pg[p];
-        const int64_t local = it - __ldg(item_off + p);
-        const int ir = (int)(local / g.items_c), ic = (int)(local % g.items_c);
+        const ItemRec rec = items[it];
+        const PairGeom &g = rec.g;
+        const int ir = rec.ir, ic = rec.ic;
         const int rbm = (1 << g.rb_log2) - 1;
         const int my_rb = lane & rbm, my_cs = lane >> g.rb_log2;
         const int row0 = ((ir << g.rb_log2) + my_rb) * R;
@@ -537,38 +536,50 @@ __global__ void segment_pairs_kernel(const double *__restrict__ q, int64_t n, do
     out[k] = ref_pair_lambda(a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7], a[8], a[9], a[10], a[11]);
 }
 
-__global__ void item_pair_kernel(const int64_t *__restrict__ item_off, int64_t P, int64_t n_items,
-                                 int32_t *__restrict__ item_pair) {
+__device__ __forceinline__ ItemRec make_item(const PairGeom &g, int64_t local) {
+    ItemRec r;
+    r.g = g;
+    r.ir = (int32_t)(local / g.items_c);
+    r.ic = (int32_t)(local % g.items_c);
+    return r;
+}
+
+__global__ void item_pair_kernel(const int64_t *__restrict__ item_off, const PairGeom *__restrict__ pg, int64_t P,
+                                 int64_t n_items, ItemRec *__restrict__ items) {
     const int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (it < n_items) item_pair[it] = (int32_t)find_pair(item_off, P, it);
+    if (it >= n_items) return;
+    const int64_t p = find_pair(item_off, P, it);
+    items[it] = make_item(pg[p], it - item_off[p]);
 }
 
 // Fused path: warp per pair writes its item range (item count not known on the host).
-__global__ void item_pair_fill_kernel(const int64_t *__restrict__ item_off, int64_t P, const int64_t *__restrict__ dP,
-                                      int64_t cap_items, int32_t *__restrict__ item_pair) {
+__global__ void item_pair_fill_kernel(const int64_t *__restrict__ item_off, const PairGeom *__restrict__ pg, int64_t P,
+                                      const int64_t *__restrict__ dP, int64_t cap_items, ItemRec *__restrict__ items) {
     const int lane = threadIdx.x & 31;
     if (*dP < P) P = *dP;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; p < P; p += nwarps) {
         const int64_t b = item_off[p], e = item_off[p + 1] < cap_items ? item_off[p + 1] : cap_items;
-        for (int64_t it = b + lane; it < e; it += 32) item_pair[it] = (int32_t)p;
+        const PairGeom g = pg[p];
+        for (int64_t it = b + lane; it < e; it += 32) items[it] = make_item(g, it - b);
     }
 }
 
 }  // namespace
 
-void launch_item_pairs_dev(const int64_t *item_off, int64_t P_cap, const int64_t *d_P, int64_t cap_items,
-                           int32_t *item_pair, cudaStream_t s) {
+void launch_item_pairs_dev(const int64_t *item_off, const PairGeom *pg, int64_t P_cap, const int64_t *d_P,
+                           int64_t cap_items, ItemRec *items, cudaStream_t s) {
     if (P_cap == 0) return;
     int64_t blocks = ceil_div(P_cap * 32, 256);
     if (blocks > 148 * 8) blocks = 148 * 8;
-    item_pair_fill_kernel<<<(unsigned)blocks, 256, 0, s>>>(item_off, P_cap, d_P, cap_items, item_pair);
+    item_pair_fill_kernel<<<(unsigned)blocks, 256, 0, s>>>(item_off, pg, P_cap, d_P, cap_items, items);
     LC_CHECK_LAUNCH();
 }
 
-void launch_item_pairs(const int64_t *item_off, int64_t P, int64_t n_items, int32_t *item_pair, cudaStream_t s) {
+void launch_item_pairs(const int64_t *item_off, const PairGeom *pg, int64_t P, int64_t n_items, ItemRec *items,
+                       cudaStream_t s) {
     if (n_items == 0) return;
-    item_pair_kernel<<<(unsigned)ceil_div(n_items, 256), 256, 0, s>>>(item_off, P, n_items, item_pair);
+    item_pair_kernel<<<(unsigned)ceil_div(n_items, 256), 256, 0, s>>>(item_off, pg, P, n_items, items);
     LC_CHECK_LAUNCH();
 }
 
@@ -617,15 +628,14 @@ int64_t build_items(const int32_t *d_pairs, int64_t P, const int64_t *d_voff, Pa
     return total;
 }
 
-void launch_gauss_items(int mode, const double *X, const double *Y, const double *Z, const PairGeom *pg,
-                        const int64_t *item_off, const int32_t *item_pair, int64_t P, int64_t item_begin,
+void launch_gauss_items(int mode, const double *X, const double *Y, const double *Z, const ItemRec *items,
+                        int64_t item_begin,
                         int64_t item_end, unsigned long long *counter, double *partials, cudaStream_t s,
                         const int64_t *d_end, int shard, int shards, const int *abort) {
     if (item_end <= item_begin) return;
     LC_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s));
-    using Kern = void (*)(const double *, const double *, const double *, const PairGeom *, const int64_t *,
-                          const int32_t *, int64_t, int64_t, int64_t, unsigned long long *, double *,
-                          const int64_t *, int, int, const int *);
+    using Kern = void (*)(const double *, const double *, const double *, const ItemRec *, int64_t, int64_t,
+                          unsigned long long *, double *, const int64_t *, int, int, const int *);
     // default phase kernel: 3 resident CTAs/SM (168 regs); modes 3-6 are A/B variants
     // (1 CTA/SM with 232 regs; 4 CTAs; row vertices in shared memory)
     static const Kern table[] = {gauss_items_kernel<GAUSS_PHASE, 3>, gauss_items_kernel<GAUSS_ATAN, 1>,
@@ -647,8 +657,8 @@ void launch_gauss_items(int mode, const double *X, const double *Y, const double
     int64_t blocks = (int64_t)num_sms() * per_sm;
     const int64_t blocks_needed = ceil_div(warps_needed, threads / 32);
     if (blocks > blocks_needed) blocks = blocks_needed;
-    fn<<<(unsigned)blocks, threads, 0, s>>>(X, Y, Z, pg, item_off, item_pair, P, item_begin, item_end, counter,
-                                            partials, d_end, shard, shards, abort);
+    fn<<<(unsigned)blocks, threads, 0, s>>>(X, Y, Z, items, item_begin, item_end, counter, partials, d_end, shard,
+                                            shards, abort);
     LC_CHECK_LAUNCH();
 }
 

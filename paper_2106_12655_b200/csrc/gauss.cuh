@@ -34,6 +34,13 @@ struct PairGeom {
     int32_t items_c;
 };
 
+// One work item, self-contained: the pair's tiling and the item's place in it
+// (the Gauss kernel's item prologue is one 48-byte load after the claim).
+struct ItemRec {
+    PairGeom g;
+    int32_t ir, ic;   // row-block group and column-strip group of the item
+};
+
 // Tiling of pair (column loop i, row loop j) from the two loops' closed-vertex
 // offsets and segment counts (one definition for every path that builds items).
 __host__ __device__ inline PairGeom make_pair_geom(int64_t col_off, int64_t row_off, int ncols, int nrows) {
@@ -69,17 +76,17 @@ size_t build_items_scan_bytes(int64_t P);
 // d_end (fused path): the item count n on the device bounds the range; with
 // shards > 1 the kernel takes slice `shard` of ceil(n / shards) items instead.
 // abort (fused path): polled per item; nonzero stops the sum (the run is redone).
-void launch_gauss_items(int mode, const double *X, const double *Y, const double *Z,
-                        const PairGeom *pg, const int64_t *item_off, const int32_t *item_pair, int64_t P,
+void launch_gauss_items(int mode, const double *X, const double *Y, const double *Z, const ItemRec *items,
                         int64_t item_begin, int64_t item_end, unsigned long long *counter,
                         double *partials, cudaStream_t s, const int64_t *d_end = nullptr, int shard = 0,
                         int shards = 1, const int *abort = nullptr);
 
-// item_pair[it] = pair of work item `it` (replaces a per-item binary search).
-void launch_item_pairs(const int64_t *item_off, int64_t P, int64_t n_items, int32_t *item_pair, cudaStream_t s);
+// items[it] = the record of work item `it` (pair tiling + the item's place in it).
+void launch_item_pairs(const int64_t *item_off, const PairGeom *pg, int64_t P, int64_t n_items, ItemRec *items,
+                       cudaStream_t s);
 // Fused path: pair count on the device, item_pair capacity cap_items.
-void launch_item_pairs_dev(const int64_t *item_off, int64_t P_cap, const int64_t *d_P, int64_t cap_items,
-                           int32_t *item_pair, cudaStream_t s);
+void launch_item_pairs_dev(const int64_t *item_off, const PairGeom *pg, int64_t P_cap, const int64_t *d_P,
+                           int64_t cap_items, ItemRec *items, cudaStream_t s);
 
 // raw[p] = fixed-order sum of the pair's item partials; lk = rint(raw);
 // flags bit0 = NaN, bit1 = |raw - rint(raw)| > 0.25 (kernels.py:19-20,69-72).

@@ -374,8 +374,8 @@ bool Pipeline::build_gauss_items_checked() {
 
 void Pipeline::finish_items() {
     d_partials.reserve(sizeof(double) * (size_t)(n_items > 0 ? n_items : 1), s);
-    d_item_pair.reserve(sizeof(int32_t) * (size_t)(n_items > 0 ? n_items : 1), s);
-    launch_item_pairs(d_item_off.as<int64_t>(), P, n_items, d_item_pair.as<int32_t>(), s);
+    d_item_pair.reserve(sizeof(ItemRec) * (size_t)(n_items > 0 ? n_items : 1), s);
+    launch_item_pairs(d_item_off.as<int64_t>(), d_pg.as<PairGeom>(), P, n_items, d_item_pair.as<ItemRec>(), s);
     d_raw.reserve(sizeof(double) * (size_t)(P > 0 ? P : 1), s);
     d_lk.reserve(sizeof(int64_t) * (size_t)(P > 0 ? P : 1), s);
     d_flags.reserve((size_t)(P > 0 ? P : 1), s);
@@ -386,7 +386,7 @@ void Pipeline::run_gauss(int mode, int64_t item_begin, int64_t item_end, double 
     if (mode < GAUSS_PHASE || mode > 7) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
     double *out = partials_ext ? partials_ext : d_partials.as<double>();
     LC_CUDA(cudaEventRecord(ev0 ? ev0 : ev[EV_GAUSS0], s));
-    launch_gauss_items(mode, gX, gY, gZ, d_pg.as<PairGeom>(), d_item_off.as<int64_t>(), d_item_pair.as<int32_t>(), P,
+    launch_gauss_items(mode, gX, gY, gZ, d_item_pair.as<ItemRec>(),
                        item_begin, item_end, d_counter.as<unsigned long long>(), out, s);
     LC_CUDA(cudaEventRecord(ev1 ? ev1 : ev[EV_GAUSS1], s));
 }
@@ -452,7 +452,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
     d_tot.reserve(4 * sizeof(int64_t), s);
     const int64_t part_cap = ceil_div(icap, shards) * shards;   // every shard's slice fits at shard * per
     d_partials.reserve(sizeof(double) * part_cap, s);
-    d_item_pair.reserve(sizeof(int32_t) * icap, s);
+    d_item_pair.reserve(sizeof(ItemRec) * icap, s);
     d_raw.reserve(sizeof(double) * pcap, s);
     d_lk.reserve(sizeof(int64_t) * pcap, s);
     d_flags.reserve((size_t)pcap, s);
@@ -492,6 +492,8 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
         // beside the work items and the Gauss sum
         LC_CUDA(cudaEventRecord(ev_pairs, s));
         LC_CUDA(cudaStreamWaitEvent(side[1], ev_pairs, 0));
+        static const bool exp_serial = getenv("LINKCERT_EXP_SERIAL_CHECKS") != nullptr;   // A/B experiment
+        if (exp_serial) LC_CUDA(cudaStreamWaitEvent(side[1], ev_chords, 0));
         launch_discretize_checks(in, dP, prm, disc_sc, dout, side[1], ev_chords, &ctr);
         record(EV_DISC, side[1]);
         // the pair list is final: copy it out while the sums run
@@ -500,11 +502,13 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
                                                         reinterpret_cast<int2 *>(hp), nullptr, nullptr, nullptr);
         LC_CHECK_LAUNCH();
         LC_CUDA(cudaEventRecord(ev_checks, side[1]));
-        launch_item_pairs_dev(d_item_off.as<int64_t>(), pcap, dP, icap, d_item_pair.as<int32_t>(), s);
+        if (exp_serial) LC_CUDA(cudaStreamWaitEvent(s, ev_checks, 0));
+        launch_item_pairs_dev(d_item_off.as<int64_t>(), d_pg.as<PairGeom>(), pcap, dP, icap, d_item_pair.as<ItemRec>(),
+                              s);
         LC_CUDA(cudaStreamWaitEvent(s, ev_chords, 0));   // the sum reads the chords
         record(EV_GAUSS0);
-        launch_gauss_items(mode, dout.X.as<double>(), dout.Y.as<double>(), dout.Z.as<double>(), d_pg.as<PairGeom>(),
-                           d_item_off.as<int64_t>(), d_item_pair.as<int32_t>(), pcap, 0, icap,
+        launch_gauss_items(mode, dout.X.as<double>(), dout.Y.as<double>(), dout.Z.as<double>(), d_item_pair.as<ItemRec>(),
+                           0, icap,
                            d_counter.as<unsigned long long>(), d_partials.as<double>(), s, d_items, shard, shards,
                            &disc_sc.prectr.as<PreCounters>()->abort);
         record(EV_GAUSS1);
