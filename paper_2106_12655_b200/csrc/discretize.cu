@@ -1317,12 +1317,13 @@ void launch_discretize_checks(const DiscInput &in, const int64_t *d_P, const Dis
     PreCounters *ctr = sc.prectr.as<PreCounters>();
     LC_CUDA(cudaMemsetAsync(sc.paired.ptr, 0, L > 0 ? L : 1, s));
     if (Pcap > 0) {
-        pre_pairs_kernel<<<grid_for(Pcap), 256, 0, s>>>(in.pairs, Pcap, d_P, in.loff, in.loop_box, L,
+        // single-warp blocks: they fit beside the Gauss kernel's CTAs (this branch runs under it)
+        pre_pairs_kernel<<<grid_for(Pcap, 32), 32, 0, s>>>(in.pairs, Pcap, d_P, in.loff, in.loop_box, L,
                                                         sc.paired.as<uint8_t>(), sc.pair_axis.as<int8_t>(), ctr);
         LC_CHECK_LAUNCH();
     }
     if (L > 0) {
-        pre_loops_kernel<<<grid_for(L), 256, 0, s>>>(in.loop_min_diag, sc.paired.as<uint8_t>(), L, min_diam, ctr);
+        pre_loops_kernel<<<grid_for(L, 32), 32, 0, s>>>(in.loop_min_diag, sc.paired.as<uint8_t>(), L, min_diam, ctr);
         LC_CHECK_LAUNCH();
     }
     if (Pcap > 0 && M > 0) {
@@ -1343,7 +1344,7 @@ void launch_discretize_checks(const DiscInput &in, const int64_t *d_P, const Dis
     }
     if (chords_done) LC_CUDA(cudaStreamWaitEvent(s, chords_done, 0));   // validation reads the chord flags
     if (L > 0) {
-        validate_loops2_kernel<<<grid_for(L), 256, 0, s>>>(in.loff, L, sc.paired.as<uint8_t>(),
+        validate_loops2_kernel<<<grid_for(L, 32), 32, 0, s>>>(in.loff, L, sc.paired.as<uint8_t>(),
                                                            sc.val_flags.as<unsigned>(), sc.val_err2.as<int>());
         LC_CHECK_LAUNCH();
     }
