@@ -560,8 +560,11 @@ LC_API int lc_model_digest(const double *coeffs, const double *t, const int64_t 
     pool_reserve(job.chunks.size());
     const int nt = resolve_threads(nthreads);
     std::vector<std::thread> th;
-    // the calling thread hashes: nt - 1 formatting workers keep it on its own core
-    for (int k = 0; k < (nt > 1 ? nt - 1 : 1); ++k) th.emplace_back([&] { job.worker(); });
+    // the calling thread hashes; by default two cores stay free of formatting
+    // workers — the hasher's and the one driving the GPU pipeline beside it
+    // (formatting needs a fraction of the hash time on the remaining cores)
+    const int workers = nthreads > 0 ? (nt > 1 ? nt - 1 : 1) : (nt > 3 ? nt - 2 : 1);
+    for (int k = 0; k < workers; ++k) th.emplace_back([&] { job.worker(); });
     const auto t_spawned = clk::now();
     Sha256 h;
     h.update("{\"loops\":[", 10);
