@@ -468,8 +468,16 @@ def verify(
     except Exception:
         _warn_digest(fut.result(), reference)
         raise
+    # the diff runs while the digest finishes; its outcome (report or error) is
+    # delivered after the digest warning, the reference's order
+    try:
+        report, err = diff_arrays(reference.array, pairs, raw, lk, flags, early_exit), None
+    except Exception as exc:  # noqa: BLE001 - re-raised below, after the warning
+        report, err = None, exc
     _warn_digest(fut.result(), reference)
-    return diff_arrays(reference.array, pairs, raw, lk, flags, early_exit)
+    if err is not None:
+        raise err
+    return report
 
 
 def _warn_digest(digest, reference):

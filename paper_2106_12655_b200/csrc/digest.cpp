@@ -488,8 +488,10 @@ void make_chunks(Job &job, int64_t L, int64_t M, int64_t target) {
     int64_t l = 0;
     std::vector<std::pair<int64_t, int64_t>> r;
     while (l < L) {
+        // the first chunks are small so the in-order hasher starts almost at once
+        const int64_t want = r.size() < 4 ? target / 8 : target;
         int64_t e = l + 1;
-        while (e < L && job.off[e] - job.off[l] < target) ++e;
+        while (e < L && job.off[e] - job.off[l] < want) ++e;
         r.emplace_back(l, e);
         l = e;
     }
