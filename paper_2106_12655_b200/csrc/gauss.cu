@@ -203,7 +203,6 @@ __device__ __forceinline__ void col_step(const Col &A, Col &B, double lx, double
 #pragma unroll
     for (int m = 0; m <= R; ++m) h[m] = fma(A.z[m], B.z[m], fma(A.y[m], B.y[m], A.x[m] * B.x[m]));
     double wx[R], wy[R];
-#if !defined(LC_UNSTAGED_PAIRS)
     if (FAST) {   // the R pair terms stage by stage: independent chains side by side (+2% over pair_w order)
         double ca[R], p[R], t1[R], d1[R], d2[R];
 #pragma unroll
@@ -236,7 +235,6 @@ __device__ __forceinline__ void col_step(const Col &A, Col &B, double lx, double
             acc.turns += t;
         }
     } else
-#endif
 #pragma unroll
     for (int m = 0; m < R; ++m) {
         int t = 0, hv = 0;
@@ -303,31 +301,12 @@ __device__ double lane_strip(const double *__restrict__ X, const double *__restr
     col_fill<MODE != GAUSS_PHASE>(A, __ldg(px + c0), __ldg(py + c0), __ldg(pz + c0), kv);
     Acc acc;
     int c = c0;
-#ifdef LC_PREFETCH_COLS
-    // column vertices of the next double step loaded one iteration ahead
-    // (clamped index: the closing vertex at ncols always exists)
-    double n1x = __ldg(px + min(c + 1, c1)), n1y = __ldg(py + min(c + 1, c1)), n1z = __ldg(pz + min(c + 1, c1));
-    double n2x = __ldg(px + min(c + 2, c1)), n2y = __ldg(py + min(c + 2, c1)), n2z = __ldg(pz + min(c + 2, c1));
-    for (; c + 2 <= c1; c += 2) {
-        const double l1x = n1x, l1y = n1y, l1z = n1z, l2x = n2x, l2y = n2y, l2z = n2z;
-        const int q1 = min(c + 3, c1), q2 = min(c + 4, c1);
-        n1x = __ldg(px + q1);
-        n1y = __ldg(py + q1);
-        n1z = __ldg(pz + q1);
-        n2x = __ldg(px + q2);
-        n2y = __ldg(py + q2);
-        n2z = __ldg(pz + q2);
-        col_step<MODE, FULL, false>(A, B, l1x, l1y, l1z, kv, rv, acc);
-        col_step<MODE, FULL, true>(B, A, l2x, l2y, l2z, kv, rv, acc);
-    }
-#else
     for (; c + 2 <= c1; c += 2) {
         const double l1x = __ldg(px + c + 1), l1y = __ldg(py + c + 1), l1z = __ldg(pz + c + 1);
         const double l2x = __ldg(px + c + 2), l2y = __ldg(py + c + 2), l2z = __ldg(pz + c + 2);
         col_step<MODE, FULL, false>(A, B, l1x, l1y, l1z, kv, rv, acc);
         col_step<MODE, FULL, true>(B, A, l2x, l2y, l2z, kv, rv, acc);
     }
-#endif
     if (c < c1) col_step<MODE, FULL, true>(A, B, __ldg(px + c + 1), __ldg(py + c + 1), __ldg(pz + c + 1), kv, rv, acc);
     if (MODE == GAUSS_PHASE && (acc.bad || !isfinite(acc.sx) || !isfinite(acc.sy)))
         // coincident vertices, w == 0, underflow or NaN input: the exact per-pair path
@@ -393,17 +372,8 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) gauss_items_kernel(
             item_end = n;
         }
     }
-#ifdef LC_PREFETCH_ITEM
-    // the next item index is claimed while the current one is evaluated
-    unsigned long long k_next = 0;
-    if (lane == 0) k_next = atomicAdd(counter, 1ULL);
-#endif
     for (;;) {
         unsigned long long k = 0;
-#ifdef LC_PREFETCH_ITEM
-        k = __shfl_sync(0xffffffffu, k_next, 0);
-        if (lane == 0 && item_begin + (int64_t)k < item_end) k_next = atomicAdd(counter, 1ULL);
-#else
         // fused path: the abort flag (the concurrent pass-1 checks found the run
         // unusable; a staged rerun follows) is read with the item claim, so both
         // round trips overlap; lane 0 reads it so the whole warp leaves together
@@ -414,7 +384,6 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) gauss_items_kernel(
         }
         k = __shfl_sync(0xffffffffu, k, 0);
         if (__shfl_sync(0xffffffffu, ab, 0)) break;
-#endif
         const int64_t it = item_begin + (int64_t)k;
         if (it >= item_end) break;
         const ItemRec rec = items[it];
@@ -636,8 +605,8 @@ void launch_gauss_items(int mode, const double *X, const double *Y, const double
     LC_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s));
     using Kern = void (*)(const double *, const double *, const double *, const ItemRec *, int64_t, int64_t,
                           unsigned long long *, double *, const int64_t *, int, int, const int *);
-    // default phase kernel: 3 resident CTAs/SM (168 regs); modes 3-6 are A/B variants
-    // (1 CTA/SM with 232 regs; 4 CTAs; row vertices in shared memory)
+    // default phase kernel: 3 resident CTAs/SM (168 regs); modes 3-7 are A/B variants
+    // (1 CTA/SM with 232 regs; 4 CTAs; row vertices in shared memory; 2 CTAs/SM)
     static const Kern table[] = {gauss_items_kernel<GAUSS_PHASE, 3>, gauss_items_kernel<GAUSS_ATAN, 1>,
                                  gauss_items_kernel<GAUSS_REF, 1>, gauss_items_kernel<GAUSS_PHASE, 1>,
                                  gauss_items_kernel<GAUSS_PHASE, 4>, gauss_items_kernel<GAUSS_PHASE, 4, true>,

@@ -492,15 +492,12 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
         // beside the work items and the Gauss sum
         LC_CUDA(cudaEventRecord(ev_pairs, s));
         LC_CUDA(cudaStreamWaitEvent(side[1], ev_pairs, 0));
-        static const bool exp_serial = getenv("LINKCERT_EXP_SERIAL_CHECKS") != nullptr;   // A/B experiment
-        if (exp_serial) LC_CUDA(cudaStreamWaitEvent(side[1], ev_chords, 0));
         launch_discretize_checks(in, dP, prm, disc_sc, dout, side[1], ev_chords, &ctr);
         record(EV_DISC, side[1]);
         // the pair list is final: the copy engine moves the whole capacity to pinned
         // memory while the sums run (no SM time; the host reads the first P)
         LC_CUDA(cudaMemcpyAsync(hp, d_pairs.ptr, sizeof(int32_t) * 2 * pcap, cudaMemcpyDeviceToHost, side[1]));
         LC_CUDA(cudaEventRecord(ev_checks, side[1]));
-        if (exp_serial) LC_CUDA(cudaStreamWaitEvent(s, ev_checks, 0));
         launch_item_pairs_dev(d_item_off.as<int64_t>(), d_pg.as<PairGeom>(), pcap, dP, icap, d_item_pair.as<ItemRec>(),
                               s);
         LC_CUDA(cudaStreamWaitEvent(s, ev_chords, 0));   // the sum reads the chords
