@@ -143,7 +143,7 @@ def cpu_reference_step(model, threads):
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    desc, before, after = build_workload(args.workload)
+    desc, _, after = build_workload(args.workload)
     threads = os.cpu_count()
     vals = []
     for k in range(args.warmup + args.steps):
@@ -158,8 +158,9 @@ def run_reference(args, rank, world):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": desc},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": "full workload per step: oracle PLS (numpy) + discretize (numpy) + Gauss sum (C, "
-                                   f"{threads} threads); the reference itself is numba on 1 effective core (GIL)"},
+                         "sample": "per step: the full workload; oracle PLS (numpy sweep) + discretize (numpy) + "
+                                   f"Gauss sum (C, {threads} threads); the reference itself is numba on 1 effective "
+                                   "core (GIL)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
