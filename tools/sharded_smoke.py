@@ -12,8 +12,11 @@ torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
 dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0"))))
 import paper_2106_12655_b200 as lc
 from paper_2106_12655_b200 import _native, generators as gen
-for name, (before, after) in {"kusari_small": (gen.kusari_tube(n_around=12, rows=4, partial=5),
-                                               gen.kusari_tube(n_around=12, rows=4, partial=5))}.items():
+cases = {"kusari_small": (gen.kusari_tube(n_around=12, rows=4, partial=5),
+                          gen.kusari_tube(n_around=12, rows=4, partial=5)),
+         # long loops: the staged sharded path (gauss_run item ranges + all-gather)
+         "knit_4x2000": (gen.knit_tube(courses=4, n=2000, W=10), gen.knit_tube(courses=4, n=2000, W=10))}
+for name, (before, after) in cases.items():
     cert = lc.compute_linking_matrix(before)
     path = _native.context().last_run_fused()
     os.environ["LINKCERT_FORCE_SHARDED"] = "0"
