@@ -463,3 +463,47 @@ def test_random_ring_soup_vs_oracle(oracle, seed, count, size, spline):
     p2, r2, _, _, ctx = run_device_pipeline(m)
     assert np.array_equal(np.asarray(p2), pairs)
     assert np.max(np.abs(np.asarray(r2) - raw)) < RAW_TOL
+
+
+def _edge_models():
+    ex, ey, ez = np.eye(3)
+    rng = np.random.default_rng(9)
+    far = lc.CurveModel([lc.LoopGeometry.from_polyline(cases.circ(8, (0, 0, 0), ex, ey)),
+                         lc.LoopGeometry.from_polyline(cases.circ(8, (50, 0, 0), ex, ey))])
+    tris = []
+    for c in rng.uniform(0, 4, size=(300, 3)):
+        pts = c + rng.normal(size=(3, 3)) * 0.6
+        tris.append(lc.LoopGeometry.from_polyline(pts))
+    tri_soup = lc.CurveModel(tris)
+    # chains of alternately oriented rings (a Hopf link between neighbours)
+    shifted = lc.CurveModel([lc.LoopGeometry.from_polyline(
+        cases.circ(32, (1e6 + 1.2 * k, 0, 0), ex, ey) if k % 2 else cases.circ(32, (1e6 + 1.2 * k, 0, 0), ez, ex))
+        for k in range(6)])
+    tiny = lc.CurveModel([lc.LoopGeometry.from_polyline(
+        cases.circ(16, (1.2e-6 * k, 0, 0), ex, ey, radius=1e-6) if k % 2 else
+        cases.circ(16, (1.2e-6 * k, 0, 0), ez, ex, radius=1e-6)) for k in range(4)])
+    # loops of 256 and 257 segments: either side of the fused path's loop-length limit
+    long_loops = {n: lc.CurveModel([lc.LoopGeometry.from_polyline(cases.circ(n, (0, 0, 0), ex, ey)),
+                                    lc.LoopGeometry.from_polyline(cases.circ(n, (1.0, 0, 0), ez, ex))])
+                  for n in (256, 257)}
+    mixed = lc.CurveModel([lc.LoopGeometry.from_polyline(cases.circ(16, (0, 0, 0), ex, ey)),
+                           lc.LoopGeometry.from_catmull_rom(cases.circ(12, (1.0, 0, 0), ez, ex))])
+    return {"far": far, "tri_soup": tri_soup, "shifted_1e6": shifted, "tiny_1e-6": tiny,
+            "loops_256": long_loops[256], "loops_257": long_loops[257], "mixed_poly_spline": mixed}
+
+
+@pytest.mark.parametrize("name", list(_edge_models()))
+def test_edge_models_vs_oracle(oracle, name):
+    """Edge geometry through the whole device path (fused and staged) vs the oracle:
+    no pairs, 3-segment loops, large offsets, tiny scales, the fused path's
+    loop-length limit, polyline + spline mixes."""
+    from paper_2106_12655_b200.certify import run_device_pipeline
+
+    m = _edge_models()[name]
+    coeffs, t, off = m.packed()
+    want, pairs, raw = oracle.link_matrix(coeffs, t, off, m.xi)
+    assert np.array_equal(lc.compute_linking_matrix(m).array, want)
+    p2, r2, _, _, ctx = run_device_pipeline(m)
+    assert np.array_equal(np.asarray(p2).reshape(-1, 2), pairs.reshape(-1, 2))
+    if len(raw):
+        assert np.max(np.abs(np.asarray(r2) - raw)) < RAW_TOL
