@@ -203,6 +203,10 @@ LC_API int lc_model_digest(const double *coeffs, const double *t, const int64_t 
                            const uint8_t *closed, int64_t L, int nthreads, char *hex_out);
 /* SHA-256 hex of a buffer (test hook; force_portable skips SHA-NI); returns 1 if SHA-NI exists. */
 LC_API int lc_sha256_hex(const void *data, int64_t n, int force_portable, char *hex_out);
+/* Page-locked host memory for model arrays (the per-call H2D copies of verify
+ * then run at DMA speed).  NULL when no CUDA device is usable. */
+LC_API void *lc_host_alloc(int64_t bytes);
+LC_API void lc_host_free(void *p);
 /* CPython float.__repr__ of x into out (>= 32 bytes); returns the length. */
 LC_API int lc_float_repr(double x, char *out);
 /* Test hook: repr of n doubles, each followed by '\n', into out (cap >= 26 n);

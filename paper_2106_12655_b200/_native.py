@@ -81,6 +81,8 @@ SIGNATURES = {
     "lc_model_json": (ctypes.c_int64, [_vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, ctypes.c_int64]),
     "lc_float_repr": (ctypes.c_int, [ctypes.c_double, ctypes.c_char_p]),
     "lc_last_run_fused": (ctypes.c_int, [_vp]),
+    "lc_host_alloc": (_vp, [ctypes.c_int64]),
+    "lc_host_free": (None, [_vp]),
     "lc_run_pipeline_shard": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_int,
                                              ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                              ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
@@ -133,6 +135,37 @@ def model_json(coeffs, t, loop_off, closed=None, nthreads=0):
     if n < 0:
         raise NativeError(LC_ERR_STATE, "lc_model_json: buffer too small")
     return memoryview(buf)[:n]
+
+
+_pinned_ok = None
+
+
+def pinned_empty(shape, dtype=np.float64):
+    """numpy array in page-locked host memory (freed with the array); plain numpy
+    memory when no device is usable (the arrays are storage, not a compute path)."""
+    global _pinned_ok
+    dtype = np.dtype(dtype)
+    n = int(np.prod(shape)) * dtype.itemsize
+    if n > 0 and _pinned_ok is not False:
+        try:
+            lib = load_library()
+            ptr = lib.lc_host_alloc(n)
+        except NativeUnavailable:
+            ptr = None
+        _pinned_ok = bool(ptr)
+        if ptr:
+            raw = (ctypes.c_char * n).from_address(ptr)
+            import weakref
+
+            weakref.finalize(raw, lib.lc_host_free, ptr)
+            return np.frombuffer(raw, dtype=dtype).reshape(shape)
+    return np.empty(shape, dtype=dtype)
+
+
+def pinned_copy(a):
+    out = pinned_empty(a.shape, a.dtype)
+    np.copyto(out, a)
+    return out
 
 
 def float_repr(x):

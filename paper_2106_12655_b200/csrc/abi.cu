@@ -452,6 +452,19 @@ int lc_stage_times(lc_ctx *ctx, float *ms) {
     });
 }
 
+void *lc_host_alloc(int64_t bytes) {
+    void *p = nullptr;
+    if (bytes <= 0 || cudaHostAlloc(&p, (size_t)bytes, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();   // clear the sticky-free error of a failed allocation
+        return nullptr;
+    }
+    return p;
+}
+
+void lc_host_free(void *p) {
+    if (p) cudaFreeHost(p);
+}
+
 int lc_last_run_fused(lc_ctx *ctx) { return ctx ? ctx->last_fused : 0; }
 
 long long lc_launch_count(void) { return launch_counter().load(); }

@@ -301,9 +301,14 @@ class CurveModel:
         if cache is not None and cache[0] == key:
             return cache[1]
         if self.loops:
+            from . import _native
+
             counts = np.fromiter((lp.coeffs.shape[0] for lp in self.loops), dtype=np.int64, count=len(self.loops))
-            coeffs = np.ascontiguousarray(np.concatenate([lp.coeffs for lp in self.loops]))
-            t = np.ascontiguousarray(np.concatenate([lp.t for lp in self.loops]))
+            # page-locked: verify copies these to the device on every call
+            coeffs = _native.pinned_empty((int(counts.sum()), 4, 3))
+            np.concatenate([lp.coeffs for lp in self.loops], out=coeffs)
+            t = _native.pinned_empty((int(counts.sum()), 2))
+            np.concatenate([lp.t for lp in self.loops], out=t)
         else:
             counts = np.zeros(0, dtype=np.int64)
             coeffs = np.zeros((0, 4, 3))
@@ -345,7 +350,9 @@ class CurveModel:
             a0 = coeffs[:, 0]
             if (not np.any(coeffs[:, 2:]) and np.all(t[:, 0] == 0.0) and np.all(t[:, 1] == 1.0)
                     and np.array_equal((a0[nxt] - a0).view(np.int64), coeffs[:, 1].view(np.int64))):
-                result = (np.ascontiguousarray(a0), off)
+                from . import _native
+
+                result = (_native.pinned_copy(a0), off)   # page-locked upload source
         self.__dict__["_polyline_cache"] = (coeffs, result)
         return result
 
@@ -406,7 +413,9 @@ class CurveModel:
         xi = total / (3 * len(verts)) if len(verts) else 0.0
         model = cls(loops, xi=xi)
         model.__dict__["_packed_cache"] = (tuple(map(id, loops)), (coeffs, t, off))
-        model.__dict__["_polyline_cache"] = (coeffs, (verts, off))
+        from . import _native
+
+        model.__dict__["_polyline_cache"] = (coeffs, (_native.pinned_copy(verts), off))   # page-locked upload source
         model.__dict__["_closed_cache"] = (coeffs, np.ones(L, dtype=np.uint8))
         return model
 
