@@ -269,6 +269,9 @@ class Context:
         self.handle = ctypes.c_void_p(h)
         self.lib = lib
         self.lock = threading.Lock()
+        # held across upload -> pipeline -> use of the result views by one caller, so
+        # concurrent callers on this context cannot interleave models or overwrite views
+        self.session = threading.RLock()
 
     def __del__(self):
         h = getattr(self, "handle", None)

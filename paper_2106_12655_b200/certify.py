@@ -330,13 +330,15 @@ def device_step(ctx, xi, excl_keys, params, mode=None, timings=None):
 def run_device_pipeline(model: CurveModel, excluded=(), params=None, timings=None, ctx=None, snapshot=None):
     """Upload the packed model, then device_step.  Returns (pairs, raw, lk, flags, ctx)."""
     params = params or DiscretizationParams()
-    t0 = time.perf_counter()
-    ctx = upload(model, ctx, snapshot)
-    if timings is not None:
-        timings["upload"] = time.perf_counter() - t0
-    pairs, raw, lk, flags = device_step(ctx, model.xi, excluded_keys(excluded), params, timings=timings)
-    if timings is not None:
-        timings.pop("upload", None)
+    ctx = ctx or _native.context()
+    with ctx.session:
+        t0 = time.perf_counter()
+        upload(model, ctx, snapshot)
+        if timings is not None:
+            timings["upload"] = time.perf_counter() - t0
+        pairs, raw, lk, flags = device_step(ctx, model.xi, excluded_keys(excluded), params, timings=timings)
+        if timings is not None:
+            timings.pop("upload", None)
     return pairs, raw, lk, flags, ctx
 
 
@@ -419,16 +421,19 @@ def compute_linking_matrix(
     else:
         snap = model.snapshot()
         fut = _digest_async(model, snap)
+        ctx = _native.context()
         try:
-            pairs, raw, lk, flags, _ = run_device_pipeline(model, excluded, params, timings, snapshot=snap)
-            _raise_for_flags(raw, flags)
+            with ctx.session:   # the result views stay ours until copied into arr
+                pairs, raw, lk, flags, _ = run_device_pipeline(model, excluded, params, timings, ctx=ctx,
+                                                               snapshot=snap)
+                _raise_for_flags(raw, flags)
+                keep = lk != 0
+                arr = np.empty((int(keep.sum()), 3), dtype=np.int64)
+                arr[:, :2] = pairs[keep]
+                arr[:, 2] = lk[keep]
         except Exception:
             fut.result()          # a serialization error would have surfaced last in the reference
             raise
-        keep = lk != 0
-        arr = np.empty((int(keep.sum()), 3), dtype=np.int64)
-        arr[:, :2] = pairs[keep]
-        arr[:, 2] = lk[keep]
         digest = fut.result()
     return LinkMatrix._from_array(model.num_loops, arr, digest, choice.tag, {})
 
@@ -455,6 +460,7 @@ def verify(
     # warning come first, as in the reference (certify.py:188-193)
     snap = model.snapshot()
     fut = _digest_async(model, snap)
+    ctx = None
     try:
         if model.num_loops < 1:
             raise ValidationError("model has no loops")
@@ -464,7 +470,13 @@ def verify(
             lk = np.zeros(0, dtype=np.int64)
             flags = np.zeros(0, dtype=np.uint8)
         else:
-            pairs, raw, lk, flags, _ = run_device_pipeline(model, excluded, params, snapshot=snap)
+            ctx = _native.context()
+            ctx.session.acquire()   # the result views stay ours through the diff
+            try:
+                pairs, raw, lk, flags, _ = run_device_pipeline(model, excluded, params, ctx=ctx, snapshot=snap)
+            except Exception:
+                ctx.session.release()
+                raise
     except Exception:
         _warn_digest(fut.result(), reference)
         raise
@@ -474,6 +486,9 @@ def verify(
         report, err = diff_arrays(reference.array, pairs, raw, lk, flags, early_exit), None
     except Exception as exc:  # noqa: BLE001 - re-raised below, after the warning
         report, err = None, exc
+    finally:
+        if ctx is not None:
+            ctx.session.release()
     _warn_digest(fut.result(), reference)
     if err is not None:
         raise err

@@ -125,3 +125,30 @@ def test_pls_degenerate_models():
     hopf = lc.CurveModel([lc.LoopGeometry.from_polyline(a), lc.LoopGeometry.from_polyline(b)])
     assert list(lc.potential_link_search(hopf)) == [(0, 1)]
     assert list(lc.potential_link_search(hopf, excluded={(1, 0)})) == []
+
+
+def test_concurrent_callers_share_the_context_safely():
+    """Two threads certifying different models on the one device context: the
+    session lock keeps upload -> pipeline -> result views of a call together."""
+    import threading
+
+    models = [lc.generators.european_4in1(8, 8), lc.generators.square_link_grid(6)[0]]
+    want = [lc.compute_linking_matrix(m) for m in models]
+    errors = []
+
+    def worker(k):
+        try:
+            for _ in range(20):
+                assert lc.compute_linking_matrix(models[k]) == want[k]
+                with warnings.catch_warnings():
+                    warnings.simplefilter("ignore")
+                    assert lc.verify(models[k], want[k]).status == PASS
+        except Exception as exc:  # noqa: BLE001
+            errors.append(exc)
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in (0, 1)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
