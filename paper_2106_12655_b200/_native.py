@@ -268,10 +268,11 @@ class Context:
             raise NativeUnavailable(f"lc_create({self.device}) failed: {lib.lc_last_error().decode()}")
         self.handle = ctypes.c_void_p(h)
         self.lib = lib
-        self.lock = threading.Lock()
-        # held across upload -> pipeline -> use of the result views by one caller, so
-        # concurrent callers on this context cannot interleave models or overwrite views
-        self.session = threading.RLock()
+        # one re-entrant lock: every call takes it, and a caller holds it (as `session`)
+        # across upload -> pipeline -> use of the result views, so concurrent callers on
+        # this context can neither interleave models nor overwrite each other's views
+        self.lock = threading.RLock()
+        self.session = self.lock
 
     def __del__(self):
         h = getattr(self, "handle", None)
