@@ -363,6 +363,23 @@ class CurveModel:
         coeffs, t, off = self.packed()
         return coeffs, t, off, self._closed_of(coeffs), self._poly_of(coeffs, t, off)
 
+    def snapshot_hint(self):
+        """The cached snapshot if a cheap O(1) check (loop count, first and last loop
+        identity) says the loops are unchanged, else None.  Only a head start: the
+        caller still runs snapshot() and must discard work done on a stale hint."""
+        cache = self.__dict__.get("_packed_cache")
+        loops = self.loops
+        if cache is None or not loops:
+            return None
+        key, (coeffs, t, off) = cache
+        if len(key) != len(loops) or key[0] != id(loops[0]) or key[-1] != id(loops[-1]):
+            return None
+        closed = self.__dict__.get("_closed_cache")
+        poly = self.__dict__.get("_polyline_cache")
+        if closed is None or closed[0] is not coeffs or poly is None or poly[0] is not coeffs:
+            return None
+        return coeffs, t, off, closed[1], poly[1]
+
     @classmethod
     def from_polyline_arrays(cls, verts, offsets, closed=True):
         """Bulk constructor for closed polylines given as one (V,3) array + offsets.

@@ -327,3 +327,20 @@ def test_multirank_gather_is_bitwise(world, n_items):
     for p in procs:
         p.join(timeout=60)
     assert sorted(res) == [(r, True) for r in range(world)]
+
+
+def test_snapshot_hint_tracks_the_loops():
+    """The O(1) snapshot hint matches the full snapshot and turns None when the loop
+    list changes (verify then discards the digest started on it)."""
+    import numpy as np
+
+    from paper_2106_12655_b200 import generators as gen
+
+    m = gen.kusari_tube(n_around=12, rows=4, partial=5)
+    assert m.snapshot_hint() is None or all(a is b for a, b in zip(m.snapshot_hint(), m.snapshot()))
+    snap = m.snapshot()
+    assert all(a is b for a, b in zip(m.snapshot_hint(), snap))
+    m.loops.append(m.loops[0])          # the last loop's identity changes
+    assert m.snapshot_hint() is None
+    assert m.snapshot()[2][-1] == snap[2][-1] + m.loops[0].coeffs.shape[0]
+    assert np.array_equal(m.snapshot()[0][:len(snap[0])], snap[0])
