@@ -440,6 +440,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
     if (pairs_seen > 0 && pairs_seen + pairs_seen / 4 + 1024 < pcap) pcap = pairs_seen + pairs_seen / 4 + 1024;
     const int64_t icap = items_cap > pcap ? items_cap : pcap;
     h_res_P = -1;
+    fused_shard_pending = false;
     polylines_ready = false;
     // every buffer sized up front from host-known capacities
     pls_sc.excl.reserve(sizeof(uint64_t) * (n_excl > 0 ? n_excl : 1), s);
@@ -605,6 +606,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
     res_lk = hl;
     res_flags = hf;
     h_res_P = shards == 1 ? P : -1;   // sharded: lc_shard_reduce completes the results
+    fused_shard_pending = shards > 1;
     return FAST_OK;
 }
 
@@ -614,6 +616,20 @@ void Pipeline::shard_reduce(const double *partials_all) {
     if (!polylines_ready) throw Error(LC_ERR_STATE, "no sharded run to reduce");
     launch_reduce_pairs(partials_all, d_item_off.as<int64_t>(), P, d_raw.as<double>(), d_lk.as<int64_t>(),
                         d_flags.as<uint8_t>(), s);
+    if (fused_shard_pending) {
+        fused_shard_pending = false;
+        // after a fused sharded run the pair list is already in pinned memory: one
+        // kernel writes the sums next to it (no per-array copies)
+        export_results_kernel<<<148, 256, 0, s>>>(d_tot.as<int64_t>(), P, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                                  d_raw.as<double>(), d_lk.as<int64_t>(), d_flags.as<uint8_t>(),
+                                                  nullptr, nullptr, reinterpret_cast<double *>(res_raw),
+                                                  reinterpret_cast<int64_t *>(res_lk),
+                                                  reinterpret_cast<uint8_t *>(res_flags));
+        LC_CHECK_LAUNCH();
+        LC_CUDA(cudaStreamSynchronize(s));
+        h_res_P = P;
+        return;
+    }
     download_results_pinned();
 }
 

@@ -98,6 +98,7 @@ struct Pipeline {
     void download_results_pinned();
     PinnedBuf h_res;
     int64_t h_res_P = -1;
+    bool fused_shard_pending = false;   // run_fast(shards > 1) left res_* for shard_reduce to fill
     char *res_pairs = nullptr, *res_raw = nullptr, *res_lk = nullptr, *res_flags = nullptr;
 
     // Fused pipeline: PLS -> discretize (no-refinement case) -> items -> Gauss

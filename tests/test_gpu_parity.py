@@ -311,6 +311,9 @@ def test_fused_matches_staged(monkeypatch, cert_models):
         monkeypatch.setenv("LINKCERT_FUSED", "1")
         fused, used = _pipeline_outcome(m, excl, prm)
         assert fused == staged, name
+        if not used:   # a first run past the item capacity falls back and sizes it
+            fused, used = _pipeline_outcome(m, excl, prm)
+            assert fused == staged, name
         if used:
             fused_names.append(name)
     # polyline models that need no refinement take the fused path
@@ -407,6 +410,7 @@ def test_fused_shards_reassemble_bitwise(shards):
             buf = torch.as_tensor(_DeviceArray(ptr, per * shards), device="cuda")
             slices.append(buf[r * per:(r + 1) * per].clone())
         gathered = torch.cat(slices)
+        torch.cuda.synchronize()   # the library reduces on its own stream
         ctx.shard_reduce(gathered.data_ptr())
         got = ctx.result_views()
         for a, b in zip(want, got):
