@@ -217,6 +217,37 @@ LC_API int64_t lc_float_repr_many(const double *x, int64_t n, int use_tochars, c
  * exactly; each CUB device-algorithm call counted once). */
 LC_API long long lc_launch_count(void);
 
+/* ---- Barnes-Hut (reference: linkcert/barneshut.py, tree: linkcert/bvh.py) ----
+ * A forest is the moment trees (leaf size 1, the reference's median split and
+ * node numbering) of L closed polylines, device-resident, owned by ctx.
+ * lc_bh_forest_build replaces MomentTree.__init__ (barneshut.py:298-312):
+ *   verts (M, 3) row-major, loop t = rows [loop_off[t], loop_off[t+1]), closed
+ *   implicitly (segment i ends at the next vertex of its loop, np.roll).
+ * lc_bh_forest_sizes: trees, segments, nodes, levels (max depth + 1).
+ * lc_bh_forest_nodes copies node data to the host in the reference's per-tree
+ *   numbering (bvh.BvhTree fields + barneshut moment arrays; any pointer may be
+ *   NULL): node_off (L+1), left/right (-1 = leaf), start/end, prim_order (M),
+ *   node_lo/node_hi/center (N,3), radius (N), cm (N,3), cd (N,3,3), cq (N,3,3,3),
+ *   ncm/ncd/ncq (N).  Node ids / positions are relative to each tree.
+ * lc_bh_far_field replaces barneshut._far_field via far_field_eval
+ *   (barneshut.py:330-345); node ids are forest-global (node_off[t] + local).
+ * lc_bh_eval replaces barneshut._dual_eval (barneshut.py:175-240) for P tree
+ *   pairs at once: pairs (P, 2) = (tree in a, tree in b), beta (P) opening
+ *   parameters; lam/e_est (P) out; visits = node pairs visited (may be NULL). */
+typedef struct lc_bh_forest lc_bh_forest;
+LC_API int lc_bh_forest_build(lc_ctx *ctx, const double *verts, const int64_t *loop_off, int64_t L,
+                              lc_bh_forest **out);
+LC_API int lc_bh_forest_free(lc_ctx *ctx, lc_bh_forest *f);
+LC_API int lc_bh_forest_sizes(const lc_bh_forest *f, int64_t *L, int64_t *M, int64_t *N, int *levels);
+LC_API int lc_bh_forest_nodes(lc_ctx *ctx, const lc_bh_forest *f, int64_t *node_off, int64_t *left, int64_t *right,
+                              int64_t *start, int64_t *end, int64_t *prim_order, double *node_lo, double *node_hi,
+                              double *center, double *radius, double *cm, double *cd, double *cq, double *ncm,
+                              double *ncd, double *ncq);
+LC_API int lc_bh_far_field(lc_ctx *ctx, const lc_bh_forest *a, int64_t node_a, const lc_bh_forest *b, int64_t node_b,
+                           int quadrupole, double *out);
+LC_API int lc_bh_eval(lc_ctx *ctx, const lc_bh_forest *a, const lc_bh_forest *b, const int32_t *pairs, int64_t P,
+                      const double *beta, int quadrupole, double k_const, double *lam, double *e_est, int64_t *visits);
+
 /* FP64 DFMA-chain throughput probe (roofline denominator), FLOP/s. */
 LC_API int lc_probe_fp64_peak(lc_ctx *ctx, double *flops, float *ms);
 

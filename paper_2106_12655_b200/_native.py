@@ -92,6 +92,13 @@ SIGNATURES = {
     "lc_model_digest": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p]),
     "lc_sha256_hex": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p]),
     "lc_launch_count": (ctypes.c_longlong, []),
+    "lc_bh_forest_build": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.POINTER(_vp)]),
+    "lc_bh_forest_free": (ctypes.c_int, [_vp, _vp]),
+    "lc_bh_forest_sizes": (ctypes.c_int, [_vp, _c_int64_p, _c_int64_p, _c_int64_p, ctypes.POINTER(ctypes.c_int)]),
+    "lc_bh_forest_nodes": (ctypes.c_int, [_vp] * 18),
+    "lc_bh_far_field": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64, ctypes.c_int, _c_double_p]),
+    "lc_bh_eval": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int64, _vp, ctypes.c_int, ctypes.c_double, _vp, _vp,
+                                   _c_int64_p]),
 }
 
 
@@ -533,11 +540,81 @@ class Context:
             _check(self.lib.lc_stage_times(self.handle, ms))
         return {"pls": ms[0], "discretize": ms[1], "gauss": ms[2], "reduce": ms[3], "begin_to_reduce": ms[4]}
 
+    def bh_forest(self, verts, loop_off):
+        """Moment trees of closed polylines on this device (Barnes-Hut)."""
+        return MomentForest(self, verts, loop_off)
+
     def probe_fp64_peak(self):
         flops = ctypes.c_double(0.0)
         ms = ctypes.c_float(0.0)
         _check(self.lib.lc_probe_fp64_peak(self.handle, ctypes.byref(flops), ctypes.byref(ms)))
         return flops.value, ms.value
+
+
+class MomentForest:
+    """Device-resident moment trees of L closed polylines (lc_bh_forest_*):
+    the Barnes-Hut trees of linkcert/barneshut.py:295-323, built on the GPU."""
+
+    FIELDS = ("node_off", "left", "right", "start", "end", "prim_order", "node_lo", "node_hi", "center", "radius",
+              "cm", "cd", "cq", "ncm", "ncd", "ncq")
+
+    def __init__(self, ctx, verts, loop_off):
+        verts = np.ascontiguousarray(verts, dtype=np.float64).reshape(-1, 3)
+        loop_off = np.ascontiguousarray(loop_off, dtype=np.int64)
+        h = _vp()
+        with ctx.lock:
+            _check(ctx.lib.lc_bh_forest_build(ctx.handle, _ptr(verts), _ptr(loop_off), len(loop_off) - 1,
+                                              ctypes.byref(h)))
+        self.ctx, self.handle = ctx, h
+        L, M, N, lv = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()
+        _check(ctx.lib.lc_bh_forest_sizes(h, ctypes.byref(L), ctypes.byref(M), ctypes.byref(N), ctypes.byref(lv)))
+        self.num_trees, self.num_segments, self.num_nodes, self.levels = L.value, M.value, N.value, lv.value
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                with self.ctx.lock:
+                    self.ctx.lib.lc_bh_forest_free(self.ctx.handle, h)
+            except Exception:
+                pass
+            self.handle = None
+
+    def nodes(self, fields=FIELDS):
+        """Host copies of node data, per-tree (reference) numbering."""
+        L, M, N = self.num_trees, self.num_segments, self.num_nodes
+        shapes = {"node_off": ((L + 1,), np.int64), "prim_order": ((M,), np.int64), "left": ((N,), np.int64),
+                  "right": ((N,), np.int64), "start": ((N,), np.int64), "end": ((N,), np.int64),
+                  "node_lo": ((N, 3), np.float64), "node_hi": ((N, 3), np.float64), "center": ((N, 3), np.float64),
+                  "radius": ((N,), np.float64), "cm": ((N, 3), np.float64), "cd": ((N, 3, 3), np.float64),
+                  "cq": ((N, 3, 3, 3), np.float64), "ncm": ((N,), np.float64), "ncd": ((N,), np.float64),
+                  "ncq": ((N,), np.float64)}
+        out = {f: np.empty(*shapes[f]) for f in fields}
+        args = [_ptr(out.get(f)) for f in self.FIELDS]
+        with self.ctx.lock:
+            _check(self.ctx.lib.lc_bh_forest_nodes(self.ctx.handle, self.handle, *args))
+        return out
+
+    def far_field(self, node, other, other_node, quadrupole=True):
+        out = ctypes.c_double(0.0)
+        with self.ctx.lock:
+            _check(self.ctx.lib.lc_bh_far_field(self.ctx.handle, self.handle, int(node), other.handle,
+                                                int(other_node), int(bool(quadrupole)), ctypes.byref(out)))
+        return out.value
+
+    def eval(self, other, pairs, beta, quadrupole=True, k_const=1.0 / (4.0 * np.pi)):
+        """Dual-tree Barnes-Hut sums for tree pairs (i in self, j in other): lam, e_est, visits."""
+        pairs = np.ascontiguousarray(pairs, dtype=np.int32).reshape(-1, 2)
+        P = pairs.shape[0]
+        beta = np.ascontiguousarray(np.broadcast_to(np.asarray(beta, dtype=np.float64), (P,)))
+        lam = np.empty(P, dtype=np.float64)
+        est = np.empty(P, dtype=np.float64)
+        visits = ctypes.c_int64(0)
+        with self.ctx.lock:
+            _check(self.ctx.lib.lc_bh_eval(self.ctx.handle, self.handle, other.handle, _ptr(pairs), P, _ptr(beta),
+                                           int(bool(quadrupole)), float(k_const), _ptr(lam), _ptr(est),
+                                           ctypes.byref(visits)))
+        return lam, est, visits.value
 
 
 _ctx = {}

@@ -14,8 +14,10 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "liblinkcert_b200.so"
-SOURCES = ["abi.cu", "pipeline.cu", "gauss.cu", "pls.cu", "discretize.cu", "probe.cu", "digest.cpp"]
-HEADERS = ["common.cuh", "gauss.cuh", "pipeline.cuh", "pls.cuh", "discretize.cuh", "geom.cuh", "scan.cuh"]
+SOURCES = ["abi.cu", "pipeline.cu", "gauss.cu", "pls.cu", "discretize.cu", "bh.cu", "probe.cu", "digest.cpp"]
+# bh.cu reproduces the reference numba arithmetic (no FMA contraction) operation by operation
+EXTRA_FLAGS = {"bh.cu": ["-fmad=false"]}
+HEADERS = ["common.cuh", "gauss.cuh", "pipeline.cuh", "pls.cuh", "discretize.cuh", "geom.cuh", "scan.cuh", "bh.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 NVCC_FLAGS = [
@@ -73,7 +75,7 @@ def build(force: bool = False, verbose: bool = False, variant: str = "", defines
         if src.suffix == ".cpp":     # host-only code: the host compiler directly
             cmd = [CXX, *CXX_FLAGS, "-I", _fmt_include(), "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)]
         else:
-            cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", str(ROOT / "include"), "-c", str(src),
+            cmd = [NVCC, *NVCC_FLAGS, *EXTRA_FLAGS.get(src.name, []), *[f"-D{d}" for d in defines], "-I", str(ROOT / "include"), "-c", str(src),
                    "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)

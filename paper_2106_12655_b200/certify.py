@@ -30,7 +30,9 @@ from . import _native
 from .direct import gauss_mode
 from .discretize import DiscretizationParams, raise_for_failure, split_polylines
 from .geometry import CurveModel, ValidationError
-from .kernels import AmbiguousLinkError, KernelChoice, ROUNDING_THRESHOLD, require_ds
+from . import barneshut
+from .kernels import (BARNES_HUT, AmbiguousLinkError, KernelChoice, ROUNDING_THRESHOLD, require_ds,
+                      require_gpu_kernel)
 from .model_io import ParseError, model_digest
 from .pls import PairList, excluded_keys, upload
 
@@ -400,6 +402,34 @@ def _prepare(model, choice, excluded, params, timings=None):
     return pair_list, split_polylines(verts, off)
 
 
+def _round_array(raw):
+    """Python round() (half-to-even) per value plus the NaN / ambiguity flags (kernels.py:68-73)."""
+    raw = np.asarray(raw, dtype=np.float64)
+    nan = np.isnan(raw)
+    r = np.rint(np.where(nan, 0.0, raw))
+    flags = np.where(nan, _native.FLAG_NAN, 0).astype(np.uint8)
+    flags[~nan & (np.abs(raw - r) > ROUNDING_THRESHOLD)] |= _native.FLAG_AMBIGUOUS
+    return r.astype(np.int64), flags
+
+
+def _bh_evaluate(model, choice, excluded, params, timings=None):
+    """Barnes-Hut certificate values: PLS + discretization on the device, then
+    every candidate pair through one batched moment-forest traversal."""
+    pair_list, polylines = _prepare(model, choice, excluded, params, timings)
+    pairs = np.asarray(list(pair_list), dtype=np.int64).reshape(-1, 2)
+    tick = time.perf_counter()
+    raw, est, beta_used, reran = barneshut.evaluate_pairs(polylines, pairs, choice.bh)
+    lk, flags = _round_array(raw)
+    if timings is not None:
+        timings["kernel"] = time.perf_counter() - tick
+    # diagnostics of the reran pairs, keys in compute_link's order (kernels.py:60-67)
+    diagnostics = {(int(pairs[k, 0]), int(pairs[k, 1])): {"e_estimate": float(est[k]),
+                                                          "beta_used": float(beta_used[k]),
+                                                          "reran": True, "raw": float(raw[k])}
+                   for k in np.nonzero(reran)[0]}
+    return pairs, raw, lk, flags, diagnostics
+
+
 def compute_linking_matrix(
     model: CurveModel,
     choice: KernelChoice | None = None,
@@ -410,9 +440,15 @@ def compute_linking_matrix(
 ) -> LinkMatrix:
     """Full pipeline: potential link search, discretization, kernel per pair (certify.py:141-166)."""
     choice = choice or KernelChoice()
-    require_ds(choice)
+    require_gpu_kernel(choice)
     if model.num_loops < 1:
         raise ValidationError("model has no loops")
+    if choice.method == BARNES_HUT:
+        pairs, raw, lk, flags, diagnostics = _bh_evaluate(model, choice, excluded, params, timings)
+        _raise_for_flags(raw, flags)
+        keep = lk != 0
+        arr = np.concatenate([pairs[keep], lk[keep, None]], axis=1) if len(pairs) else np.zeros((0, 3), np.int64)
+        return LinkMatrix._from_array(model.num_loops, arr, model_digest(model), choice.tag, diagnostics)
     if model.num_loops == 1:
         arr = np.zeros((0, 3), dtype=np.int64)
         if timings is not None:
@@ -449,13 +485,19 @@ def verify(
 ) -> VerificationReport:
     """Recompute pairwise links and diff against a reference certificate (certify.py:169-221)."""
     choice = choice or KernelChoice()
-    require_ds(choice)
+    require_gpu_kernel(choice)
     if model.num_loops != reference.num_loops:
         return VerificationReport(
             FAIL,
             message=(f"loop count mismatch: model has {model.num_loops}, "
                      f"certificate has {reference.num_loops}"),
         )
+    if choice.method == BARNES_HUT:
+        _warn_digest(model_digest(model), reference)
+        if model.num_loops < 1:
+            raise ValidationError("model has no loops")
+        pairs, raw, lk, flags, _ = _bh_evaluate(model, choice, excluded, params)
+        return diff_arrays(reference.array, pairs, raw, lk, flags, early_exit)
     # the digest (host, native) overlaps the device pipeline; its check and
     # warning come first, as in the reference (certify.py:188-193).  It starts on
     # the cached arrays before the full cache check; a stale hint is redone.

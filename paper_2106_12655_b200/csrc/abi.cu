@@ -8,6 +8,7 @@
 #include <string>
 #include <vector>
 
+#include "bh.cuh"
 #include "gauss.cuh"
 #include "pipeline.cuh"
 
@@ -29,6 +30,12 @@ struct lc_ctx {
     float last_gauss_ms = 0.f;
     int last_fused = 0;   // last lc_run_pipeline: 0 staged, 1 fused, 2 fused replayed as a CUDA graph
     DevBuf tb_coeffs, tb_t, tb_box, tb_loop, tb_off, tb_flag;   // lc_tight_boxes scratch
+    BhScratch bh;                                                // Barnes-Hut traversal scratch
+};
+
+struct lc_bh_forest {
+    lc::BhForest f;
+    lc_ctx *owner = nullptr;
 };
 
 template <class F>
@@ -468,6 +475,74 @@ void lc_host_free(void *p) {
 int lc_last_run_fused(lc_ctx *ctx) { return ctx ? ctx->last_fused : 0; }
 
 long long lc_launch_count(void) { return launch_counter().load(); }
+
+int lc_bh_forest_build(lc_ctx *ctx, const double *verts, const int64_t *loop_off, int64_t L, lc_bh_forest **out) {
+    if (out) *out = nullptr;
+    return guarded(ctx, [&] {
+        if (!out || !loop_off || L < 1 || (!verts && loop_off[L] > 0)) throw Error(LC_ERR_ARG, "lc_bh_forest_build: bad arguments");
+        for (int64_t t = 0; t < L; ++t)
+            if (loop_off[t + 1] <= loop_off[t]) throw Error(LC_ERR_ARG, "lc_bh_forest_build: empty loop or bad offsets");
+        auto *h = new lc_bh_forest;
+        h->owner = ctx;
+        try {
+            bh_build(h->f, verts, loop_off, L, ctx->stream);
+        } catch (...) {
+            h->f.release(ctx->stream);
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int lc_bh_forest_free(lc_ctx *ctx, lc_bh_forest *f) {
+    if (!f) return LC_OK;
+    return guarded(ctx, [&] {
+        if (f->owner != ctx) throw Error(LC_ERR_ARG, "forest belongs to another context");
+        f->f.release(ctx->stream);
+        delete f;
+    });
+}
+
+int lc_bh_forest_sizes(const lc_bh_forest *f, int64_t *L, int64_t *M, int64_t *N, int *levels) {
+    if (!f) {
+        g_last_error = "null forest";
+        return LC_ERR_ARG;
+    }
+    if (L) *L = f->f.L;
+    if (M) *M = f->f.M;
+    if (N) *N = f->f.N;
+    if (levels) *levels = f->f.levels;
+    return LC_OK;
+}
+
+int lc_bh_forest_nodes(lc_ctx *ctx, const lc_bh_forest *f, int64_t *node_off, int64_t *left, int64_t *right,
+                       int64_t *start, int64_t *end, int64_t *prim_order, double *node_lo, double *node_hi,
+                       double *center, double *radius, double *cm, double *cd, double *cq, double *ncm, double *ncd,
+                       double *ncq) {
+    return guarded(ctx, [&] {
+        if (!f || f->owner != ctx) throw Error(LC_ERR_ARG, "lc_bh_forest_nodes: bad forest");
+        bh_download(f->f, node_off, left, right, start, end, prim_order, node_lo, node_hi, center, radius, cm, cd, cq,
+                    ncm, ncd, ncq, ctx->stream);
+    });
+}
+
+int lc_bh_far_field(lc_ctx *ctx, const lc_bh_forest *a, int64_t node_a, const lc_bh_forest *b, int64_t node_b,
+                    int quadrupole, double *out) {
+    return guarded(ctx, [&] {
+        if (!a || !b || !out || a->owner != ctx || b->owner != ctx) throw Error(LC_ERR_ARG, "lc_bh_far_field: bad arguments");
+        *out = bh_far_field(a->f, node_a, b->f, node_b, quadrupole != 0, ctx->bh, ctx->stream);
+    });
+}
+
+int lc_bh_eval(lc_ctx *ctx, const lc_bh_forest *a, const lc_bh_forest *b, const int32_t *pairs, int64_t P,
+               const double *beta, int quadrupole, double k_const, double *lam, double *e_est, int64_t *visits) {
+    return guarded(ctx, [&] {
+        if (!a || !b || a->owner != ctx || b->owner != ctx || P < 0 || (P > 0 && (!pairs || !beta)))
+            throw Error(LC_ERR_ARG, "lc_bh_eval: bad arguments");
+        bh_eval(a->f, b->f, pairs, P, beta, quadrupole != 0, k_const, lam, e_est, visits, ctx->bh, ctx->stream);
+    });
+}
 
 int lc_probe_fp64_peak(lc_ctx *ctx, double *flops, float *ms) {
     return guarded(ctx, [&] { *flops = probe_dfma_flops(ctx->stream, ms); });

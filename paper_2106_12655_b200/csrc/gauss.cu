@@ -22,6 +22,7 @@
 // fixed order, so raw sums are identical run to run and for any split of
 // the item range across GPUs.
 #include "gauss.cuh"
+#include "geom.cuh"
 
 #include "scan.cuh"
 
@@ -29,7 +30,6 @@ namespace lc {
 
 namespace {
 
-constexpr double kTwoPi = 6.283185307179586;          // 2.0 * math.pi (direct.py:16)
 constexpr double kInvTwoPi = 0.15915494309189535;     // 1 / (2 pi), correctly rounded
 
 __device__ __forceinline__ int sbit(double x) { return (int)((unsigned)__double2hiint(x) >> 31); }
@@ -69,37 +69,6 @@ __device__ __forceinline__ double sqrt_nb(double x) {
     // x == 0 (coincident vertices) gives NaN without the select; the phase fast
     // path omits it and re-evaluates such (degenerate) strips exactly.
     return ZERO_SAFE ? (x > 0.0 ? g : 0.0) : g;
-}
-
-// Reference _pair_lambda with the IEEE operation sequence of the numba
-// kernel (fastmath=False: no contraction): explicit _rn intrinsics.
-__device__ __forceinline__ double ref_pair_lambda(double ljx, double ljy, double ljz, double lj1x,
-                                                  double lj1y, double lj1z, double kix, double kiy,
-                                                  double kiz, double ki1x, double ki1y, double ki1z) {
-#define S_(a, b) __dsub_rn(a, b)
-#define A_(a, b) __dadd_rn(a, b)
-#define M_(a, b) __dmul_rn(a, b)
-    const double ax = S_(ljx, kix), ay = S_(ljy, kiy), az = S_(ljz, kiz);
-    const double bx = S_(ljx, ki1x), by = S_(ljy, ki1y), bz = S_(ljz, ki1z);
-    const double cx = S_(lj1x, ki1x), cy = S_(lj1y, ki1y), cz = S_(lj1z, ki1z);
-    const double dx = S_(lj1x, kix), dy = S_(lj1y, kiy), dz = S_(lj1z, kiz);
-    const double an = __dsqrt_rn(A_(A_(M_(ax, ax), M_(ay, ay)), M_(az, az)));
-    const double bn = __dsqrt_rn(A_(A_(M_(bx, bx), M_(by, by)), M_(bz, bz)));
-    const double cn = __dsqrt_rn(A_(A_(M_(cx, cx), M_(cy, cy)), M_(cz, cz)));
-    const double dn = __dsqrt_rn(A_(A_(M_(dx, dx), M_(dy, dy)), M_(dz, dz)));
-    const double p = A_(A_(M_(ax, S_(M_(by, cz), M_(bz, cy))), M_(ay, S_(M_(bz, cx), M_(bx, cz)))),
-                        M_(az, S_(M_(bx, cy), M_(by, cx))));
-    const double ab = A_(A_(M_(ax, bx), M_(ay, by)), M_(az, bz));
-    const double bc = A_(A_(M_(bx, cx), M_(by, cy)), M_(bz, cz));
-    const double ca = A_(A_(M_(cx, ax), M_(cy, ay)), M_(cz, az));
-    const double ad = A_(A_(M_(ax, dx), M_(ay, dy)), M_(az, dz));
-    const double dc = A_(A_(M_(dx, cx), M_(dy, cy)), M_(dz, cz));
-    const double d1 = A_(A_(A_(M_(M_(an, bn), cn), M_(ab, cn)), M_(bc, an)), M_(ca, bn));
-    const double d2 = A_(A_(A_(M_(M_(an, dn), cn), M_(ad, cn)), M_(dc, an)), M_(ca, dn));
-    return __ddiv_rn(A_(atan2(p, d1), atan2(p, d2)), kTwoPi);
-#undef S_
-#undef A_
-#undef M_
 }
 
 // ------------------------------------------------------------ lane strip

@@ -72,3 +72,22 @@ def gpu():
     from paper_2106_12655_b200 import _native
 
     return _native.context()
+
+
+@pytest.fixture(scope="session")
+def bh_golden():
+    with open(GOLDEN / "bh_golden.json") as f:
+        return json.load(f)
+
+
+@pytest.fixture(scope="session")
+def bh_arrays():
+    with np.load(GOLDEN / "bh_golden.npz") as z:
+        return {k: z[k] for k in z.files}
+
+
+@pytest.fixture(scope="session")
+def bh_oracle():
+    import bh_oracle
+
+    return bh_oracle
