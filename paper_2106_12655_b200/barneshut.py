@@ -137,11 +137,10 @@ class MomentTree:
     def __init__(self, loop):
         verts = loop.vertices if hasattr(loop, "vertices") else np.asarray(loop, float)
         self.seg_a = np.ascontiguousarray(verts)
-        self.seg_b = np.ascontiguousarray(np.roll(verts, -1, axis=0))
         if self.seg_a.ndim != 2 or self.seg_a.shape[1:] != (3,) or self.seg_a.shape[0] == 0:
             raise ValueError("expected matching (m, 3) box corner arrays, m >= 1")
+        # the device derives segment ends itself; seg_b / loop_length are host views made on first use
         self._forest = _native.context().bh_forest(self.seg_a, np.array([0, len(self.seg_a)], dtype=np.int64))
-        self.loop_length = float(np.sum(np.linalg.norm(self.seg_b - self.seg_a, axis=1)))
         self._nodes = None
 
     def _host(self):
@@ -152,6 +151,12 @@ class MomentTree:
     def __getattr__(self, name):
         if name in MomentTree._HOST:
             return self._host()[name]
+        if name == "seg_b":
+            self.__dict__["seg_b"] = np.ascontiguousarray(np.roll(self.seg_a, -1, axis=0))
+            return self.seg_b
+        if name == "loop_length":
+            self.__dict__["loop_length"] = float(np.sum(np.linalg.norm(self.seg_b - self.seg_a, axis=1)))
+            return self.loop_length
         if name == "bvh":
             lo = np.minimum(self.seg_a, self.seg_b)
             hi = np.maximum(self.seg_a, self.seg_b)

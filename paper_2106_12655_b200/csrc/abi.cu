@@ -81,6 +81,12 @@ lc_ctx *lc_create(int device) {
     ctx->device = device;
     try {
         LC_CUDA(cudaSetDevice(device));
+        // stream-ordered frees stay in the device pool (no OS round trip when a
+        // moment forest or a scratch buffer is rebuilt at the same size)
+        cudaMemPool_t pool;
+        LC_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t keep = ~0ull;
+        LC_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
         LC_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         ctx->own_stream = true;
         LC_CUDA(cudaEventCreate(&ctx->ev0));

@@ -9,8 +9,8 @@
 //
 // Tree build (bvh._build, bvh.py:17-90, leaf_size 1).  The node ranges of a
 // median-split tree depend only on the loop length m, so the node table
-// (numbering, start/end, children, depth) is generated once per m on the host
-// in the reference's DFS order.  The geometry only decides the permutation:
+// (numbering, start/end, children, depth) is computed in closed form on the
+// device (bh_table_kernel, the reference's DFS numbering).  The geometry only decides the permutation:
 // level by level, every node's primitives are ordered by (center on the
 // node's longest axis, input index).  On the device that is one radix sort of
 // all primitives per level with the key (node start, rank of the primitive on
@@ -33,8 +33,8 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
-#include <map>
-#include <mutex>
+#include <chrono>
+#include <cstdlib>
 
 #include "bh.cuh"
 #include "geom.cuh"
@@ -463,58 +463,87 @@ struct Add2 {
 
 // ------------------------------------------------------------------ node tables
 
-struct Table {
-    std::vector<int32_t> left, right, start, end, depth;
-    int levels = 0;
-};
-
-const Table &table_for(int64_t m) {
-    static std::mutex mu;
-    static std::map<int64_t, Table> cache;
-    std::lock_guard<std::mutex> g(mu);
-    auto it = cache.find(m);
-    if (it != cache.end()) return it->second;
-    Table t;
-    const int64_t n = 2 * m - 1;
-    t.left.assign(n, -1);
-    t.right.assign(n, -1);
-    t.start.assign(n, 0);
-    t.end.assign(n, 0);
-    t.depth.assign(n, 0);
-    struct Item { int64_t node, s, e; int d; };
-    std::vector<Item> stack{{0, 0, m, 0}};
-    int64_t n_nodes = 1;
-    while (!stack.empty()) {   // bvh.py:31-80: pop, set range, split at the middle
-        const Item it2 = stack.back();
-        stack.pop_back();
-        t.start[it2.node] = (int32_t)it2.s;
-        t.end[it2.node] = (int32_t)it2.e;
-        t.depth[it2.node] = it2.d;
-        t.levels = std::max(t.levels, it2.d + 1);
-        if (it2.e - it2.s <= 1) continue;
-        const int64_t mid = it2.s + (it2.e - it2.s) / 2;
-        const int64_t lc = n_nodes, rc = n_nodes + 1;
-        n_nodes += 2;
-        t.left[it2.node] = (int32_t)lc;
-        t.right[it2.node] = (int32_t)rc;
-        stack.push_back({lc, it2.s, mid, it2.d + 1});
-        stack.push_back({rc, mid, it2.e, it2.d + 1});
+// Node table of every tree in the reference numbering (bvh.py:31-80), one
+// thread per position walking root -> leaf.  The reference pops a LIFO stack,
+// so internal nodes are numbered in a right-first preorder: the k-th popped
+// internal node allocates children 2k+1 (left) and 2k+2 (right).  With leaf
+// size 1 a subtree of n primitives has n-1 internal nodes, hence
+// k(right) = k + 1 and k(left) = k + size(right).  A node is written by the
+// thread of its first position.
+__global__ void bh_table_kernel(const int64_t *__restrict__ loff, const int64_t *__restrict__ noff, int64_t L,
+                                int64_t M, int *__restrict__ left, int *__restrict__ right, int *__restrict__ start,
+                                int *__restrict__ end, int *__restrict__ depth) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= M) return;
+    int64_t lo_t = 0, hi_t = L;
+    while (hi_t - lo_t > 1) {
+        const int64_t mid = (lo_t + hi_t) >> 1;
+        if (loff[mid] <= p) lo_t = mid; else hi_t = mid;
     }
-    return cache.emplace(m, std::move(t)).first->second;
+    const int64_t po = loff[lo_t], no = noff[lo_t];
+    const int64_t q = p - po;
+    int64_t s = 0, e = loff[lo_t + 1] - po, id = 0, k = 0;
+    for (int d = 0;; ++d) {
+        const bool mine = q == s;
+        if (mine) {
+            start[no + id] = (int)(s + po);
+            end[no + id] = (int)(e + po);
+            depth[no + id] = d;
+        }
+        if (e - s <= 1) {
+            if (mine) left[no + id] = right[no + id] = -1;
+            break;
+        }
+        const int64_t mid = s + (e - s) / 2, lc = 2 * k + 1, rc = 2 * k + 2;
+        if (mine) {
+            left[no + id] = (int)(no + lc);
+            right[no + id] = (int)(no + rc);
+        }
+        if (q < mid) {
+            id = lc;
+            k += e - mid;
+            e = mid;
+        } else {
+            id = rc;
+            k += 1;
+            s = mid;
+        }
+    }
 }
 
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)ceil_div(n > 0 ? n : 1, t); }
 
 }  // namespace
 
+namespace {
+// LC_BH_STATS=1: per-phase wall times of bh_build on stderr (stream synced per phase)
+struct PhaseClock {
+    bool on = false;
+    cudaStream_t s;
+    std::chrono::steady_clock::time_point t0;
+    explicit PhaseClock(cudaStream_t st) : s(st) {
+        const char *e = getenv("LC_BH_STATS");
+        on = e && e[0] == '1';
+        t0 = std::chrono::steady_clock::now();
+    }
+    void mark(const char *what) {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        const auto t1 = std::chrono::steady_clock::now();
+        fprintf(stderr, "bh_build %-10s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+        t0 = t1;
+    }
+};
+}  // namespace
+
 void bh_build(BhForest &f, const double *verts, const int64_t *loop_off, int64_t L, cudaStream_t s) {
+    PhaseClock clk(s);
     if (L < 1) throw Error(LC_ERR_ARG, "moment forest needs at least one loop");
     if (loop_off[0] != 0) throw Error(LC_ERR_ARG, "loop offsets must start at 0");
     f.L = L;
     f.loop_off.assign(loop_off, loop_off + L + 1);
     f.node_off.assign(L + 1, 0);
     int64_t M = 0, N = 0;
-    int levels = 0;
     for (int64_t t = 0; t < L; ++t) {
         const int64_t m = loop_off[t + 1] - loop_off[t];
         if (m < 1) throw Error(LC_ERR_ARG, "every loop needs at least one vertex");
@@ -526,24 +555,12 @@ void bh_build(BhForest &f, const double *verts, const int64_t *loop_off, int64_t
     if (M >= (int64_t(1) << 30)) throw Error(LC_ERR_ARG, "moment forest too large (2^30 segments)");
     f.M = M;
     f.N = N;
-    // host node table in the reference numbering, offset per tree
-    std::vector<int32_t> hl(N), hr(N), hs(N), he(N), hd(N);
-    std::vector<char> internal_at(1, 0);
-    for (int64_t t = 0; t < L; ++t) {
-        const Table &tb = table_for(loop_off[t + 1] - loop_off[t]);
-        levels = std::max(levels, tb.levels);
-        if ((int)internal_at.size() < levels) internal_at.resize(levels, 0);
-        const int64_t no = f.node_off[t], po = loop_off[t];
-        for (size_t v = 0; v < tb.left.size(); ++v) {
-            hl[no + v] = tb.left[v] < 0 ? -1 : (int32_t)(tb.left[v] + no);
-            hr[no + v] = tb.right[v] < 0 ? -1 : (int32_t)(tb.right[v] + no);
-            hs[no + v] = (int32_t)(tb.start[v] + po);
-            he[no + v] = (int32_t)(tb.end[v] + po);
-            hd[no + v] = tb.depth[v];
-            if (tb.left[v] >= 0) internal_at[tb.depth[v]] = 1;
-        }
-    }
+    int64_t max_m = 1;
+    for (int64_t t = 0; t < L; ++t) max_m = std::max(max_m, loop_off[t + 1] - loop_off[t]);
+    int levels = 1;   // leaves of a median split of m sit at depth <= ceil(log2 m)
+    while ((int64_t(1) << (levels - 1)) < max_m) ++levels;
     f.levels = levels;
+    clk.mark("table");
     const size_t i4 = sizeof(int32_t);
     f.seg.reserve(sizeof(double) * 6 * M, s);
     f.left.reserve(i4 * N, s);
@@ -574,14 +591,14 @@ void bh_build(BhForest &f, const double *verts, const int64_t *loop_off, int64_t
     LC_CUDA(cudaMemcpyAsync(d_verts.ptr, verts, sizeof(double) * 3 * M, cudaMemcpyHostToDevice, s));
     LC_CUDA(cudaMemcpyAsync(d_loff.ptr, loop_off, sizeof(int64_t) * (L + 1), cudaMemcpyHostToDevice, s));
     LC_CUDA(cudaMemcpyAsync(f.d_node_off.ptr, f.node_off.data(), sizeof(int64_t) * (L + 1), cudaMemcpyHostToDevice, s));
-    LC_CUDA(cudaMemcpyAsync(f.left.ptr, hl.data(), i4 * N, cudaMemcpyHostToDevice, s));
-    LC_CUDA(cudaMemcpyAsync(f.right.ptr, hr.data(), i4 * N, cudaMemcpyHostToDevice, s));
-    LC_CUDA(cudaMemcpyAsync(f.start.ptr, hs.data(), i4 * N, cudaMemcpyHostToDevice, s));
-    LC_CUDA(cudaMemcpyAsync(f.end.ptr, he.data(), i4 * N, cudaMemcpyHostToDevice, s));
-    LC_CUDA(cudaMemcpyAsync(f.depth.ptr, hd.data(), i4 * N, cudaMemcpyHostToDevice, s));
     LC_CUDA(cudaMemsetAsync(enc_lo.ptr, 0xFF, sizeof(unsigned long long) * 3 * N, s));
     LC_CUDA(cudaMemsetAsync(enc_hi.ptr, 0x00, sizeof(unsigned long long) * 3 * N, s));
+    clk.mark("alloc+h2d");
 
+    bh_table_kernel<<<blocks_for(M, 256), 256, 0, s>>>(d_loff.as<int64_t>(), f.d_node_off.as<int64_t>(), L, M,
+                                                       f.left.as<int>(), f.right.as<int>(), f.start.as<int>(),
+                                                       f.end.as<int>(), f.depth.as<int>());
+    LC_CHECK_LAUNCH();
     bh_prims_kernel<<<blocks_for(M, 256), 256, 0, s>>>(d_verts.as<double>(), d_loff.as<int64_t>(),
                                                        f.d_node_off.as<int64_t>(), L, M, f.seg.as<double>(),
                                                        ckey.as<unsigned long long>(), iota.as<int>(), f.order.as<int>(),
@@ -604,13 +621,14 @@ void bh_build(BhForest &f, const double *verts, const int64_t *loop_off, int64_t
         bh_rank_kernel<<<blocks_for(M, 256), 256, 0, s>>>(ids_out.as<int>(), M, rank.as<int>() + k * M);
         LC_CHECK_LAUNCH();
     }
+    clk.mark("ranks");
     int *ord = f.order.as<int>(), *ord_alt = order2.as<int>();
     for (int d = 0; d < levels; ++d) {
         bh_bbox_kernel<<<blocks_for(M, 256), 256, 0, s>>>(nodeid.as<int>(), ord, f.depth.as<int>(), d,
                                                           f.seg.as<double>(), M, enc_lo.as<unsigned long long>(),
                                                           enc_hi.as<unsigned long long>());
         LC_CHECK_LAUNCH();
-        if (!internal_at[d]) continue;
+        if (d == levels - 1) continue;   // leaves only
         bh_key_kernel<<<blocks_for(M, 256), 256, 0, s>>>(nodeid.as<int>(), ord, f.depth.as<int>(), f.left.as<int>(),
                                                          f.start.as<int>(), d, enc_lo.as<unsigned long long>(),
                                                          enc_hi.as<unsigned long long>(), rank.as<int>(), M, rank_bits,
@@ -628,6 +646,7 @@ void bh_build(BhForest &f, const double *verts, const int64_t *loop_off, int64_t
     }
     if (ord != f.order.as<int>())
         LC_CUDA(cudaMemcpyAsync(f.order.ptr, ord, i4 * M, cudaMemcpyDeviceToDevice, s));
+    clk.mark("levels");
     for (int d = levels - 1; d >= 0; --d) {
         bh_moments_kernel<<<blocks_for(N, 128), 128, 0, s>>>(
             f.depth.as<int>(), f.left.as<int>(), f.right.as<int>(), f.start.as<int>(), f.order.as<int>(),
@@ -635,10 +654,12 @@ void bh_build(BhForest &f, const double *verts, const int64_t *loop_off, int64_t
             f.box.as<double>(), f.rec.as<double>(), f.leaf_prim.as<int>());
         LC_CHECK_LAUNCH();
     }
+    clk.mark("moments");
     for (DevBuf *b : {&d_verts, &d_loff, &ckey, &ckey_out, &iota, &ids_out, &rank, &nodeid, &order2, &key, &key2,
                       &enc_lo, &enc_hi, &tmp})
         b->release(s);
     LC_CUDA(cudaStreamSynchronize(s));
+    clk.mark("release");
 }
 
 void bh_download(const BhForest &f, int64_t *node_off, int64_t *left, int64_t *right, int64_t *start, int64_t *end,
