@@ -219,6 +219,20 @@ def evaluate_pairs(polylines, pairs, params=None):
     adaptive rule reruns (each with its own beta, computed as the reference's
     barnes_hut_detailed does per pair).  Returns (value, e_estimate, beta_used,
     reran) arrays in pair order."""
+    pairs = np.asarray(pairs, dtype=np.int64).reshape(-1, 2)
+    if pairs.shape[0] == 0:
+        return evaluate_pairs_packed(np.zeros((0, 3)), np.zeros(1, dtype=np.int64), pairs, params)
+    used, tree_of = np.unique(pairs, return_inverse=True)
+    blocks = [np.asarray(polylines[int(i)].vertices if hasattr(polylines[int(i)], "vertices")
+                         else polylines[int(i)], dtype=np.float64) for i in used]
+    off = np.zeros(len(blocks) + 1, dtype=np.int64)
+    np.cumsum([len(b) for b in blocks], out=off[1:])
+    return evaluate_pairs_packed(np.concatenate(blocks), off, tree_of.reshape(-1, 2), params)
+
+
+def evaluate_pairs_packed(verts, loop_off, pairs, params=None):
+    """evaluate_pairs on packed loops: verts (M, 3), loop t = rows
+    [loop_off[t], loop_off[t+1]); pairs index the loops."""
     params = params or BarnesHutParams()
     pairs = np.asarray(pairs, dtype=np.int64).reshape(-1, 2)
     P = pairs.shape[0]
@@ -228,13 +242,8 @@ def evaluate_pairs(polylines, pairs, params=None):
     reran = np.zeros(P, dtype=bool)
     if P == 0:
         return value, est, beta_used, reran
-    used, tree_of = np.unique(pairs, return_inverse=True)
-    tree_pairs = tree_of.reshape(-1, 2).astype(np.int32)
-    blocks = [np.asarray(polylines[int(i)].vertices if hasattr(polylines[int(i)], "vertices")
-                         else polylines[int(i)], dtype=np.float64) for i in used]
-    off = np.zeros(len(blocks) + 1, dtype=np.int64)
-    np.cumsum([len(b) for b in blocks], out=off[1:])
-    forest = _native.context().bh_forest(np.concatenate(blocks), off)
+    tree_pairs = pairs.astype(np.int32)
+    forest = _native.context().bh_forest(verts, loop_off)
     quad = params.order == "quadrupole"
     value, est, _ = forest.eval(forest, tree_pairs, params.beta_init, quad, params.k_const)
     if params.adaptive:

@@ -383,7 +383,7 @@ def _evaluate_pairs(polylines, pair_items, choice, threads, diagnostics):
     return {(int(i), int(j)): int(v) for (i, j), v in zip(pairs.tolist(), lk.tolist())}
 
 
-def _prepare(model, choice, excluded, params, timings=None):
+def _prepare(model, choice, excluded, params, timings=None, packed=False):
     """PLS + discretization (certify.py:130-138); polylines copied back from the device."""
     params = params or DiscretizationParams()
     tick = time.perf_counter()
@@ -399,6 +399,8 @@ def _prepare(model, choice, excluded, params, timings=None):
     if timings is not None:
         timings["pls"] = tock - tick
         timings["discretize"] = time.perf_counter() - tock
+    if packed:
+        return pair_list, verts, off
     return pair_list, split_polylines(verts, off)
 
 
@@ -415,10 +417,10 @@ def _round_array(raw):
 def _bh_evaluate(model, choice, excluded, params, timings=None):
     """Barnes-Hut certificate values: PLS + discretization on the device, then
     every candidate pair through one batched moment-forest traversal."""
-    pair_list, polylines = _prepare(model, choice, excluded, params, timings)
-    pairs = np.asarray(list(pair_list), dtype=np.int64).reshape(-1, 2)
+    pair_list, verts, off = _prepare(model, choice, excluded, params, timings, packed=True)
+    pairs = pair_list.array.astype(np.int64).reshape(-1, 2)
     tick = time.perf_counter()
-    raw, est, beta_used, reran = barneshut.evaluate_pairs(polylines, pairs, choice.bh)
+    raw, est, beta_used, reran = barneshut.evaluate_pairs_packed(verts, off, pairs, choice.bh)
     lk, flags = _round_array(raw)
     if timings is not None:
         timings["kernel"] = time.perf_counter() - tick

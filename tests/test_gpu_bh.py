@@ -219,3 +219,54 @@ def test_empty_loop_rejected(gpu):
         lc.build_moment_tree(np.zeros((0, 3)))
     with pytest.raises(_native.NativeError):
         gpu.bh_forest(np.zeros((4, 3)), [0, 2, 2, 4])
+
+
+def _random_loops(seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    for k in range(12):
+        n = int(rng.integers(3, 300))
+        kind = k % 4
+        if kind == 0:      # random walk
+            v = np.cumsum(rng.normal(size=(n, 3)), axis=0)
+        elif kind == 1:    # integer lattice walk: many equal centers (tie breaking)
+            v = np.cumsum(rng.integers(-1, 2, size=(n, 3)), axis=0).astype(float)
+        elif kind == 2:    # repeated vertices (zero-length segments) and a flat loop
+            v = np.repeat(rng.normal(size=(n // 2 + 2, 3)), 2, axis=0)
+            v[:, 2] = 0.0
+        else:              # noisy circle with signed zeros
+            v = _circle(n, radius=float(rng.uniform(0.5, 5))) + 1e-3 * rng.normal(size=(n, 3))
+            v[::7, 1] = -0.0
+        out.append(np.ascontiguousarray(v))
+    return out
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_random_trees_bitwise_vs_oracle(gpu, bh_oracle, seed):
+    loops = _random_loops(seed)
+    off = np.zeros(len(loops) + 1, dtype=np.int64)
+    np.cumsum([len(v) for v in loops], out=off[1:])
+    nodes = gpu.bh_forest(np.concatenate(loops), off).nodes()
+    noff = nodes["node_off"]
+    for t, v in enumerate(loops):
+        o = bh_oracle.Tree(v)
+        sl = slice(noff[t], noff[t + 1])
+        for f in ("node_lo", "node_hi", "left", "right", "start", "end") + MOM:
+            assert np.array_equal(nodes[f][sl], getattr(o, f)), (seed, t, f)
+        assert np.array_equal(nodes["prim_order"][off[t]:off[t + 1]], o.prim_order)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_random_pairs_bh_vs_oracle(gpu, bh_oracle, seed):
+    loops = _random_loops(seed)[:6]
+    trees = [bh_oracle.Tree(v) for v in loops]
+    pairs = [(i, j) for i in range(len(loops)) for j in range(len(loops)) if (i + j) % 2 == 0]
+    for beta, quad in ((1.0, True), (2.0, False), (3.5, True)):
+        off = np.zeros(len(loops) + 1, dtype=np.int64)
+        np.cumsum([len(v) for v in loops], out=off[1:])
+        f = gpu.bh_forest(np.concatenate(loops), off)
+        lam, est, _ = f.eval(f, pairs, beta, quad)
+        for k, (i, j) in enumerate(pairs):
+            lo, eo, _, _ = bh_oracle.dual_eval(trees[i], trees[j], beta, quad)
+            assert abs(lam[k] - lo) <= 1e-12 * max(1.0, abs(lo)), (seed, i, j, beta)
+            assert est[k] == pytest.approx(eo, rel=1e-12, abs=1e-300)

@@ -16,3 +16,6 @@ done
 python tools/prof_gauss.py --case ribbon --n 100000 --mode phase --reps 1 > gpurun_out/plain_ribbon.log 2>&1 && \
 ncu --metrics $M --clock-control none --csv -k regex:gauss_items --log-file gpurun_out/counts_ribbon_phase.csv python tools/prof_gauss.py --case ribbon --n 100000 --mode phase --reps 1 > gpurun_out/ncu_ribbon.log 2>&1
 nvidia-smi --query-gpu=name,driver_version,clocks.max.sm --format=csv > gpurun_out/gpu.txt; lscpu > gpurun_out/lscpu.txt
+# Barnes-Hut (csrc/bh.cu): probe line + launch list of its kernels (forest build, traversal levels)
+python tools/bh_probe.py --sizes 1000000 --ds-max 0 > gpurun_out/bh_probe.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv -k regex:bh_ -c 400 --log-file gpurun_out/bh_launches.csv python tools/bh_probe.py --sizes 1000000 --ds-max 0 > gpurun_out/ncu_bh.log 2>&1
