@@ -19,7 +19,8 @@
 // reference's argsort-with-index-ties.  Node boxes are reduced with ordered
 // 64-bit atomics (min / max are order-free, hence exact and deterministic).
 //
-// Moments (barneshut._compute_moments) bottom-up, one launch per depth.
+// Moments (barneshut._compute_moments) bottom-up, one launch per depth over
+// the depth-ordered node list, one warp per node (coalesced 384 B records).
 //
 // Traversal (barneshut._dual_eval): breadth-first over node pairs.  Each
 // level's frontier is classified (far field / leaf pair / split); splits are
@@ -86,7 +87,7 @@ __global__ void bh_prims_kernel(const double *__restrict__ v, const int64_t *__r
 
 __global__ void bh_rank_kernel(const int *__restrict__ sorted_ids, int64_t M, int *__restrict__ rank) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < M) rank[sorted_ids[i]] = (int)i;
+    if (i < M) rank[sorted_ids ? sorted_ids[i] : i] = (int)i;   // no ids: iota
 }
 
 // Node boxes of depth d: union of the primitive boxes in the node's range.
@@ -206,109 +207,121 @@ __global__ void bh_descend_kernel(int *__restrict__ nodeid, const int *__restric
     nodeid[p] = p < mid ? left[node] : right[node];
 }
 
-// Moments of the depth-d nodes (barneshut.py:44-90), children first.
-__global__ void bh_moments_kernel(const int *__restrict__ depth, const int *__restrict__ left,
-                                  const int *__restrict__ right, const int *__restrict__ start,
-                                  const int *__restrict__ order, const double *__restrict__ seg,
-                                  const unsigned long long *__restrict__ enc_lo,
-                                  const unsigned long long *__restrict__ enc_hi, int d, int64_t N,
-                                  double *__restrict__ box, double *__restrict__ rec, int *__restrict__ leaf_prim) {
-    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (v >= N || depth[v] != d) return;
-    double lo[3], hi[3], c[3];
+// Moments of the depth-d nodes, one warp per node (the depth-ordered node
+// list gives the nodes of a level): the children's 384 B records are read
+// and the node's record written as whole coalesced rows through shared
+// memory; lane l computes moment components l and l + 32 (cm 0-2, cd 3-11,
+// cq 12-38), each in the reference's expression order; lane 0 forms the norms
+// in their sequential order (barneshut.py:93-112).
+__global__ void __launch_bounds__(256) bh_moments_warp_kernel(
+    const int *__restrict__ nodes, int64_t count, const int *__restrict__ left, const int *__restrict__ right,
+    const int *__restrict__ start, const int *__restrict__ order, const double *__restrict__ seg,
+    const unsigned long long *__restrict__ enc_lo, const unsigned long long *__restrict__ enc_hi,
+    double *__restrict__ box, double *__restrict__ rec, int *__restrict__ leaf_prim) {
+    __shared__ double sm[8][3][kBhRec];   // per warp: left child, right child, own record
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double *sL = sm[w][0], *sR = sm[w][1], *sO = sm[w][2];
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t q = blockIdx.x * (int64_t)(blockDim.x >> 5) + w; q < count; q += warps) {
+        const int v = nodes[q];
+        double lo[3], hi[3], c[3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        lo[k] = ord_val(enc_lo[3 * v + k]);
-        hi[k] = ord_val(enc_hi[3 * v + k]);
-        box[6 * v + k] = lo[k];
-        box[6 * v + 3 + k] = hi[k];
-        c[k] = 0.5 * (lo[k] + hi[k]);
-    }
-    double *R = rec + kBhRec * v;
-    const double dx = hi[0] - lo[0], dy = hi[1] - lo[1], dz = hi[2] - lo[2];
-    R[BH_CENTER + 0] = c[0];
-    R[BH_CENTER + 1] = c[1];
-    R[BH_CENTER + 2] = c[2];
-    R[BH_RADIUS] = 0.5 * sqrt(dx * dx + dy * dy + dz * dz);
-    double cm[3], cd[3][3], cq[3][3][3];
-    if (left[v] < 0) {
-        const int s = order[start[v]];
-        leaf_prim[v] = s;
-        const double *a = seg + 6 * (int64_t)s, *b = a + 3;
+        for (int k = 0; k < 3; ++k) {
+            lo[k] = ord_val(enc_lo[3 * (int64_t)v + k]);
+            hi[k] = ord_val(enc_hi[3 * (int64_t)v + k]);
+            c[k] = 0.5 * (lo[k] + hi[k]);
+        }
+        if (lane < 6) box[6 * (int64_t)v + lane] = lane < 3 ? lo[lane] : hi[lane - 3];
+        const int lv = left[v];
+        if (lv >= 0) {
+            const double *L = rec + kBhRec * (int64_t)lv, *R = rec + kBhRec * (int64_t)right[v];
+            sL[lane] = L[lane];
+            sR[lane] = R[lane];
+            if (lane < kBhRec - 32) {
+                sL[32 + lane] = L[32 + lane];
+                sR[32 + lane] = R[32 + lane];
+            }
+        }
+        __syncwarp();
         double dd[3], rl[3];
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            const double mid = 0.5 * (a[i] + b[i]);
-            dd[i] = b[i] - a[i];
-            rl[i] = mid - c[i];
-        }
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            cm[i] = dd[i];
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-                cd[i][j] = dd[i] * rl[j];
-#pragma unroll
-                for (int k = 0; k < 3; ++k) cq[i][j][k] = dd[i] * (dd[j] * dd[k] / 12.0 + rl[j] * rl[k]);
-            }
-        }
-    } else {
-        leaf_prim[v] = -1;
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            cm[i] = 0.0;
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-                cd[i][j] = 0.0;
-#pragma unroll
-                for (int k = 0; k < 3; ++k) cq[i][j][k] = 0.0;
-            }
-        }
-        const int kids[2] = {left[v], right[v]};
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            const double *C = rec + kBhRec * (int64_t)kids[q];
-            double rc[3];
-#pragma unroll
-            for (int i = 0; i < 3; ++i) rc[i] = C[BH_CENTER + i] - c[i];
+        if (lv < 0) {
+            const int sp = order[start[v]];
+            if (lane == 0) leaf_prim[v] = sp;
+            const double *a = seg + 6 * (int64_t)sp, *b = a + 3;
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
-                const double cmc = C[BH_CM + i];
-                cm[i] += cmc;
+                const double mid = 0.5 * (a[i] + b[i]);
+                dd[i] = b[i] - a[i];
+                rl[i] = mid - c[i];
+            }
+        } else if (lane == 0) {
+            leaf_prim[v] = -1;
+        }
 #pragma unroll
-                for (int j = 0; j < 3; ++j) {
-                    cd[i][j] += C[BH_CD + 3 * i + j] + cmc * rc[j];
+        for (int h = 0; h < 2; ++h) {
+            const int o = lane + 32 * h;
+            if (o >= 39) break;
+            double out;
+            if (lv < 0) {
+                if (o < 3) {
+                    out = dd[o];
+                } else if (o < 12) {
+                    const int i = (o - 3) / 3, j = (o - 3) % 3;
+                    out = dd[i] * rl[j];
+                } else {
+                    const int i = (o - 12) / 9, j = ((o - 12) / 3) % 3, k = (o - 12) % 3;
+                    out = dd[i] * (dd[j] * dd[k] / 12.0 + rl[j] * rl[k]);
+                }
+            } else {
+                out = 0.0;
 #pragma unroll
-                    for (int k = 0; k < 3; ++k)
-                        cq[i][j][k] += C[BH_CQ + 9 * i + 3 * j + k] + C[BH_CD + 3 * i + j] * rc[k] +
-                                       C[BH_CD + 3 * i + k] * rc[j] + cmc * rc[j] * rc[k];
+                for (int ch = 0; ch < 2; ++ch) {
+                    const double *C = ch ? sR : sL;
+                    const double rc0 = C[BH_CENTER + 0] - c[0], rc1 = C[BH_CENTER + 1] - c[1],
+                                 rc2 = C[BH_CENTER + 2] - c[2];
+                    const double rc[3] = {rc0, rc1, rc2};
+                    if (o < 3) {
+                        out += C[BH_CM + o];
+                    } else if (o < 12) {
+                        const int i = (o - 3) / 3, j = (o - 3) % 3;
+                        out += C[BH_CD + 3 * i + j] + C[BH_CM + i] * rc[j];
+                    } else {
+                        const int i = (o - 12) / 9, j = ((o - 12) / 3) % 3, k = (o - 12) % 3;
+                        out += C[BH_CQ + 9 * i + 3 * j + k] + C[BH_CD + 3 * i + j] * rc[k] +
+                               C[BH_CD + 3 * i + k] * rc[j] + C[BH_CM + i] * rc[j] * rc[k];
+                    }
                 }
             }
+            sO[BH_CM + o] = out;
         }
-    }
-    double s2 = 0.0, s3 = 0.0;
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-        R[BH_CM + i] = cm[i];
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-            R[BH_CD + 3 * i + j] = cd[i][j];
-            s2 += cd[i][j] * cd[i][j];
-#pragma unroll
-            for (int k = 0; k < 3; ++k) R[BH_CQ + 9 * i + 3 * j + k] = cq[i][j][k];
+        __syncwarp();
+        if (lane == 0) {
+            const double dx = hi[0] - lo[0], dy = hi[1] - lo[1], dz = hi[2] - lo[2];
+            sO[BH_CENTER + 0] = c[0];
+            sO[BH_CENTER + 1] = c[1];
+            sO[BH_CENTER + 2] = c[2];
+            sO[BH_RADIUS] = 0.5 * sqrt(dx * dx + dy * dy + dz * dz);
+            sO[BH_NCM] = sqrt(sO[BH_CM] * sO[BH_CM] + sO[BH_CM + 1] * sO[BH_CM + 1] + sO[BH_CM + 2] * sO[BH_CM + 2]);
+            double s2 = 0.0, s3 = 0.0;
+            for (int i = 0; i < 9; ++i) s2 += sO[BH_CD + i] * sO[BH_CD + i];
+            for (int i = 0; i < 27; ++i) s3 += sO[BH_CQ + i] * sO[BH_CQ + i];
+            sO[BH_NCD] = sqrt(s2);
+            sO[BH_NCQ] = sqrt(s3);
+            sO[46] = 0.0;
+            sO[47] = 0.0;
         }
+        __syncwarp();
+        double *Rv = rec + kBhRec * (int64_t)v;
+        Rv[lane] = sO[lane];
+        if (lane < kBhRec - 32) Rv[32 + lane] = sO[32 + lane];
+        __syncwarp();
     }
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j)
-#pragma unroll
-            for (int k = 0; k < 3; ++k) s3 += cq[i][j][k] * cq[i][j][k];
-    R[BH_NCM] = sqrt(cm[0] * cm[0] + cm[1] * cm[1] + cm[2] * cm[2]);
-    R[BH_NCD] = sqrt(s2);
-    R[BH_NCQ] = sqrt(s3);
-    R[46] = 0.0;
-    R[47] = 0.0;
+}
+
+// Depth-ordered node list: first node of each depth in the sorted key array.
+__global__ void bh_level_starts_kernel(const int *__restrict__ sorted_depth, int64_t N, int *__restrict__ starts) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < N && (i == 0 || sorted_depth[i] != sorted_depth[i - 1])) starts[sorted_depth[i]] = (int)i;
 }
 
 // ------------------------------------------------------------------ far field
@@ -647,12 +660,40 @@ void bh_build(BhForest &f, const double *verts, const int64_t *loop_off, int64_t
     if (ord != f.order.as<int>())
         LC_CUDA(cudaMemcpyAsync(f.order.ptr, ord, i4 * M, cudaMemcpyDeviceToDevice, s));
     clk.mark("levels");
-    for (int d = levels - 1; d >= 0; --d) {
-        bh_moments_kernel<<<blocks_for(N, 128), 128, 0, s>>>(
-            f.depth.as<int>(), f.left.as<int>(), f.right.as<int>(), f.start.as<int>(), f.order.as<int>(),
-            f.seg.as<double>(), enc_lo.as<unsigned long long>(), enc_hi.as<unsigned long long>(), d, N,
-            f.box.as<double>(), f.rec.as<double>(), f.leaf_prim.as<int>());
+    // nodes grouped by depth (stable radix sort of (depth, id)), then bottom-up
+    {
+        DevBuf nid, nid_sorted, dsorted, starts, tmp2;
+        nid.reserve(i4 * N, s);
+        nid_sorted.reserve(i4 * N, s);
+        dsorted.reserve(i4 * N, s);
+        starts.reserve(i4 * (levels + 1), s);
+        bh_rank_kernel<<<blocks_for(N, 256), 256, 0, s>>>(nullptr, N, nid.as<int>());   // iota
         LC_CHECK_LAUNCH();
+        int dbits = 1;
+        while ((1 << dbits) < levels) ++dbits;
+        size_t bt = 0;
+        LC_CUB(cub::DeviceRadixSort::SortPairs(nullptr, bt, (int *)nullptr, (int *)nullptr, (int *)nullptr,
+                                               (int *)nullptr, (int)N, 0, dbits));
+        tmp2.reserve(bt, s);
+        bt = tmp2.bytes;
+        LC_CUB(cub::DeviceRadixSort::SortPairs(tmp2.ptr, bt, f.depth.as<int>(), dsorted.as<int>(), nid.as<int>(),
+                                               nid_sorted.as<int>(), (int)N, 0, dbits, s));
+        bh_level_starts_kernel<<<blocks_for(N, 256), 256, 0, s>>>(dsorted.as<int>(), N, starts.as<int>());
+        LC_CHECK_LAUNCH();
+        std::vector<int> h_starts(levels + 1);
+        LC_CUDA(cudaMemcpyAsync(h_starts.data(), starts.ptr, i4 * levels, cudaMemcpyDeviceToHost, s));
+        LC_CUDA(cudaStreamSynchronize(s));
+        h_starts[levels] = (int)N;
+        for (int d = levels - 1; d >= 0; --d) {
+            const int64_t cnt = h_starts[d + 1] - h_starts[d];
+            const int64_t blocks = std::min<int64_t>(ceil_div(cnt, 8), 148 * 16);
+            bh_moments_warp_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(
+                nid_sorted.as<int>() + h_starts[d], cnt, f.left.as<int>(), f.right.as<int>(), f.start.as<int>(),
+                f.order.as<int>(), f.seg.as<double>(), enc_lo.as<unsigned long long>(),
+                enc_hi.as<unsigned long long>(), f.box.as<double>(), f.rec.as<double>(), f.leaf_prim.as<int>());
+            LC_CHECK_LAUNCH();
+        }
+        for (DevBuf *b : {&nid, &nid_sorted, &dsorted, &starts, &tmp2}) b->release(s);
     }
     clk.mark("moments");
     for (DevBuf *b : {&d_verts, &d_loff, &ckey, &ckey_out, &iota, &ids_out, &rank, &nodeid, &order2, &key, &key2,
