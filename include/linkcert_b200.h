@@ -179,6 +179,21 @@ LC_API int lc_run_pipeline_shard(lc_ctx *ctx, const uint64_t *excluded_keys, int
                                  int shards, int64_t *n_pairs, int64_t *n_items, double **partials_dev);
 /* Fixed-order per-pair reduction of the gathered partials of a sharded run
  * (bitwise the single-GPU sums) + results into pinned memory. */
+/* Multi-GPU without a host round trip between the sum and the exchange:
+ * lc_run_pipeline_shard_async enqueues the fused run of shard `shard` of
+ * `shards` (>= 1) on the context stream and returns at once with the library's
+ * item-partials buffer (*part_cap doubles; *part_cap = 0: the model needs the
+ * staged path).  Items of other shards hold the bits of -0.0, so an in-place
+ * int64 MAX all-reduce of that buffer over the ranks (NCCL, enqueued on the
+ * context stream: lc_get_stream) assembles every shard's partials bit-exactly.
+ * lc_shard_finish then enqueues the fixed-order reduction and the export and
+ * syncs once; *fused = 1: results ready (lc_result_views), 0: run the staged
+ * path; LC_ERR_VALIDATION as lc_run_pipeline. */
+LC_API int lc_run_pipeline_shard_async(lc_ctx *ctx, const uint64_t *excluded_keys, int64_t n_excl, double xi,
+                                       double epsilon, int max_passes, int64_t max_subsegments, int mode, int shard,
+                                       int shards, double **partials_dev, int64_t *part_cap);
+LC_API int lc_shard_finish(lc_ctx *ctx, int *fused);
+LC_API int lc_get_stream(lc_ctx *ctx, void **stream);
 LC_API int lc_shard_reduce(lc_ctx *ctx, const double *partials_all_dev);
 /* Path of the last lc_run_pipeline: 0 staged, 1 fused, 2 fused replayed from
  * the captured CUDA graph (same shape as the previous run, no reallocation). */

@@ -88,6 +88,11 @@ SIGNATURES = {
                                              ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
                                              ctypes.POINTER(_vp)]),
     "lc_shard_reduce": (ctypes.c_int, [_vp, _vp]),
+    "lc_run_pipeline_shard_async": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                                                   ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                                   ctypes.c_int, ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_int64)]),
+    "lc_shard_finish": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int)]),
+    "lc_get_stream": (ctypes.c_int, [_vp, ctypes.POINTER(_vp)]),
     "lc_float_repr_many": (ctypes.c_int64, [_vp, ctypes.c_int64, ctypes.c_int, _vp, ctypes.c_int64]),
     "lc_model_digest": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p]),
     "lc_sha256_hex": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p]),
@@ -501,6 +506,35 @@ class Context:
                 raise self._disc_error()
             _check(rc)
         return None if n_items.value < 0 else (n_items.value, ptr.value)
+
+    def run_pipeline_shard_async(self, excluded_keys, xi, epsilon, max_passes, max_subsegments, mode, shard,
+                                 shards):
+        """Enqueue the fused run of item shard `shard` of `shards` (>= 2) without a
+        host sync; returns (device pointer of the partials, entries) or None when
+        the staged path must run.  Complete with shard_finish()."""
+        ex = np.ascontiguousarray(excluded_keys if excluded_keys is not None else [], dtype=np.uint64)
+        ptr, cap = _vp(), ctypes.c_int64(0)
+        with self.lock:
+            _check(self.lib.lc_run_pipeline_shard_async(self.handle, _ptr(ex), ex.size, float(xi), float(epsilon),
+                                                        int(max_passes), int(max_subsegments), int(mode),
+                                                        int(shard), int(shards), ctypes.byref(ptr),
+                                                        ctypes.byref(cap)))
+        return None if cap.value <= 0 else (ptr.value, cap.value)
+
+    def shard_finish(self):
+        """Reduce + export + the one host sync of an async sharded run; True: results ready."""
+        fused = ctypes.c_int(0)
+        with self.lock:
+            rc = self.lib.lc_shard_finish(self.handle, ctypes.byref(fused))
+            if rc in (LC_ERR_DISCRETIZE, LC_ERR_VALIDATION):
+                raise self._disc_error()
+            _check(rc)
+        return bool(fused.value)
+
+    def stream_ptr(self):
+        out = _vp()
+        _check(self.lib.lc_get_stream(self.handle, ctypes.byref(out)))
+        return out.value or 0
 
     def shard_reduce(self, partials_all_ptr):
         with self.lock:

@@ -208,38 +208,34 @@ class _DeviceArray:
     """Zero-copy handle on a library-owned device buffer (torch.as_tensor reads
     __cuda_array_interface__)."""
 
-    def __init__(self, ptr, n):
-        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": "<f8", "data": (int(ptr), False),
+    def __init__(self, ptr, n, typestr="<f8"):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr, "data": (int(ptr), False),
                                          "version": 3}
 
 
-_gather_out = {}
-
-
 def _fused_sharded_step(ctx, xi, excl_keys, params, mode, dist):
-    """Multi-GPU hot path: every rank runs the fused single-sync pipeline on the
-    same model with the Gauss kernel restricted to its item slice; the slices
-    are all-gathered with NCCL into one partial array, which every rank reduces
-    in fixed order (bitwise the single-GPU sums).  None: the model needs the
-    staged path."""
+    """Multi-GPU hot path with one host sync per rank: every rank enqueues the
+    fused pipeline on the same model with the Gauss kernel restricted to its
+    item slice (lc_run_pipeline_shard_async), the partials are assembled by an
+    in-place NCCL int64 MAX all-reduce enqueued on the library stream (items
+    of other ranks hold the bits of -0.0, the MAX identity here), and
+    lc_shard_finish reduces every pair in fixed order (bitwise the single-GPU
+    sums), exports and syncs.  None: the model needs the staged path (every
+    rank decides alike: same model, deterministic device summary)."""
     import torch
 
     world, rank = dist.get_world_size(), dist.get_rank()
-    got = ctx.run_pipeline_shard(excl_keys, xi, params.epsilon, params.max_passes, params.max_subsegments, mode,
-                                 rank, world)
+    got = ctx.run_pipeline_shard_async(excl_keys, xi, params.epsilon, params.max_passes, params.max_subsegments,
+                                       mode, rank, world)
     if got is None:
         return None
-    n_items, ptr = got
+    ptr, cap = got
     dev = torch.device("cuda", ctx.device)
-    per = -(-n_items // world)
-    out = _gather_out.get((dev, per * world))
-    if out is None:
-        out = _gather_out[(dev, per * world)] = torch.empty(per * world, dtype=torch.float64, device=dev)
-    if per:
-        mine = torch.as_tensor(_DeviceArray(ptr, per * world), device=dev)[rank * per:(rank + 1) * per]
-        dist.all_gather_into_tensor(out, mine)
-        torch.cuda.synchronize(dev)
-    ctx.shard_reduce(out.data_ptr())
+    buf = torch.as_tensor(_DeviceArray(ptr, cap, "<i8"), device=dev)
+    with torch.cuda.stream(torch.cuda.ExternalStream(ctx.stream_ptr(), device=dev)):
+        dist.all_reduce(buf, op=dist.ReduceOp.MAX)
+    if not ctx.shard_finish():
+        return None
     return ctx.result_views()
 
 

@@ -434,6 +434,51 @@ int lc_run_pipeline_shard(lc_ctx *ctx, const uint64_t *excluded_keys, int64_t n_
     return LC_OK;
 }
 
+int lc_run_pipeline_shard_async(lc_ctx *ctx, const uint64_t *excluded_keys, int64_t n_excl, double xi,
+                                double epsilon, int max_passes, int64_t max_subsegments, int mode, int shard,
+                                int shards, double **partials_dev, int64_t *part_cap) {
+    if (part_cap) *part_cap = 0;
+    ctx->last_fused = 0;
+    ctx->pipe.derived_in_run = false;
+    return guarded(ctx, [&] {
+        if (!partials_dev || !part_cap || shards < 1) throw Error(LC_ERR_ARG, "lc_run_pipeline_shard_async: bad arguments");
+        if (n_excl < 0 || (n_excl > 0 && !excluded_keys)) throw Error(LC_ERR_ARG, "bad excluded keys");
+        for (int64_t k = 1; k < n_excl; ++k)
+            if (excluded_keys[k] <= excluded_keys[k - 1]) throw Error(LC_ERR_ARG, "excluded keys must be sorted unique");
+        DiscParams prm;
+        prm.xi = xi;
+        prm.epsilon = epsilon;
+        prm.max_passes = max_passes;
+        prm.max_subsegments = max_subsegments;
+        const int fr = ctx->pipe.run_fast(excluded_keys, n_excl, prm, mode, shard, shards, true);
+        if (fr == FAST_PENDING) {
+            *partials_dev = ctx->pipe.d_partials.as<double>();
+            *part_cap = ctx->pipe.part_cap;
+        }
+    });
+}
+
+int lc_shard_finish(lc_ctx *ctx, int *fused) {
+    if (fused) *fused = 0;
+    int fr = FAST_FALLBACK;
+    const int g = guarded(ctx, [&] { fr = ctx->pipe.shard_finish(); });
+    if (g != LC_OK) return g;
+    ctx->last_fused = fr == FAST_FALLBACK ? 0 : (ctx->pipe.last_fast_graph ? 2 : 1);
+    if (fused) *fused = fr == FAST_OK ? 1 : 0;
+    if (fr == FAST_INVALID) {
+        g_last_error = "discretization failed (see lc_discretize_error)";
+        return LC_ERR_VALIDATION;
+    }
+    return LC_OK;
+}
+
+int lc_get_stream(lc_ctx *ctx, void **stream) {
+    return guarded(ctx, [&] {
+        if (!stream) throw Error(LC_ERR_ARG, "null stream pointer");
+        *stream = (void *)ctx->stream;
+    });
+}
+
 int lc_shard_reduce(lc_ctx *ctx, const double *partials_all_dev) {
     return guarded(ctx, [&] { ctx->pipe.shard_reduce(partials_all_dev); });
 }

@@ -33,6 +33,11 @@ __global__ void polyline_coeffs_kernel(const double *__restrict__ v, const int64
     t[2 * m + 1] = 1.0;
 }
 
+__global__ void fill_bits_kernel(unsigned long long *__restrict__ p, int64_t n, unsigned long long v) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
 __global__ void export_results_kernel(const int64_t *__restrict__ dP, int64_t cap, const int64_t *__restrict__ d_items,
                                       const int *__restrict__ d_max_row, const PreCounters *__restrict__ ctr,
                                       const int *__restrict__ val_err, const int2 *__restrict__ pairs,
@@ -426,7 +431,8 @@ void Pipeline::download_results_pinned() {
 }
 
 int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscParams &prm, int mode, int shard,
-                       int shards) {
+                       int shards, bool async) {
+    pend.on = false;
     if (shards < 1 || shard < 0 || shard >= shards) throw Error(LC_ERR_ARG, "bad shard");
     // loops longer than the brute-force side limit make every pair they are in a
     // large (sweep) pair: the staged path handles those models directly
@@ -451,7 +457,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
     d_scan.reserve(build_items_scan_bytes(pcap), s);
     d_counter.reserve(sizeof(unsigned long long), s);
     d_tot.reserve(4 * sizeof(int64_t), s);
-    const int64_t part_cap = ceil_div(icap, shards) * shards;   // every shard's slice fits at shard * per
+    part_cap = ceil_div(icap, shards) * shards;   // every shard's slice fits at shard * per
     d_partials.reserve(sizeof(double) * part_cap, s);
     d_item_pair.reserve(sizeof(ItemRec) * icap, s);
     d_raw.reserve(sizeof(double) * pcap, s);
@@ -501,6 +507,11 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
         LC_CUDA(cudaEventRecord(ev_checks, side[1]));
         launch_item_pairs_dev(d_item_off.as<int64_t>(), d_pg.as<PairGeom>(), pcap, dP, icap, d_item_pair.as<ItemRec>(),
                               s);
+        if (shards > 1) {   // items of other shards: the bits of -0.0 (the int64 MAX all-reduce identity)
+            fill_bits_kernel<<<(unsigned)ceil_div(part_cap, 256), 256, 0, s>>>(
+                reinterpret_cast<unsigned long long *>(d_partials.ptr), part_cap, 0x8000000000000000ull);
+            LC_CHECK_LAUNCH();
+        }
         LC_CUDA(cudaStreamWaitEvent(s, ev_chords, 0));   // the sum reads the chords
         record(EV_GAUSS0);
         launch_gauss_items(mode, dout.X.as<double>(), dout.Y.as<double>(), dout.Z.as<double>(), d_item_pair.as<ItemRec>(),
@@ -576,12 +587,34 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
     } else {
         enqueue();
     }
+    pend.on = true;
+    pend.key = key;
+    pend.pcap = pcap;
+    pend.icap = icap;
+    pend.shards = shards;
+    pend.st = st;
+    pend.hp = hp;
+    pend.hr = hr;
+    pend.hl = hl;
+    pend.hf = hf;
+    if (async) return FAST_PENDING;
+    return finish_fast();
+}
+
+// Host side of a fused run: the one sync, then the device summary decides.
+int Pipeline::finish_fast() {
+    if (!pend.on) throw Error(LC_ERR_STATE, "no enqueued fused run");
+    pend.on = false;
+    const FastKey key = pend.key;
+    const int64_t pcap = pend.pcap, icap = pend.icap;
+    const int shards = pend.shards;
+    char *hp = pend.hp, *hr = pend.hr, *hl = pend.hl, *hf = pend.hf;
     LC_CUDA(cudaStreamSynchronize(s));
     fast_seen = key;
     fast_seen.gen = alloc_generation().load();
     fast_seen_valid = true;
 
-    const FastStatus f = *st;
+    const FastStatus f = *pend.st;
     if (f.n_items > items_cap) items_cap = f.n_items;
     if (f.P > pairs_seen) pairs_seen = f.P;
     if (f.max_row > kRowSlots || f.P > pcap || f.zero_loop != INT_MAX || f.n_large != 0 || f.marked != 0 ||
@@ -631,6 +664,28 @@ void Pipeline::shard_reduce(const double *partials_all) {
         return;
     }
     download_results_pinned();
+}
+
+// After an async sharded run and the in-place all-reduce of d_partials: the
+// fixed-order per-pair reduction and the results into pinned memory, sized on
+// the device (no host count needed), then the run's single host sync.
+int Pipeline::shard_finish() {
+    if (!pend.on) throw Error(LC_ERR_STATE, "no pending sharded run");
+    const int64_t *dP = d_tot.as<int64_t>();
+    launch_reduce_pairs(d_partials.as<double>(), d_item_off.as<int64_t>(), pend.pcap, d_raw.as<double>(),
+                        d_lk.as<int64_t>(), d_flags.as<uint8_t>(), s, dP);
+    export_results_kernel<<<148, 256, 0, s>>>(dP, pend.pcap, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                              d_raw.as<double>(), d_lk.as<int64_t>(), d_flags.as<uint8_t>(), nullptr,
+                                              nullptr, reinterpret_cast<double *>(pend.hr),
+                                              reinterpret_cast<int64_t *>(pend.hl),
+                                              reinterpret_cast<uint8_t *>(pend.hf));
+    LC_CHECK_LAUNCH();
+    const int r = finish_fast();
+    if (r == FAST_OK) {
+        h_res_P = P;
+        fused_shard_pending = false;
+    }
+    return r;
 }
 
 void Pipeline::segment_pair_lambda(const double *quads, int64_t n, double *out) {

@@ -16,7 +16,7 @@ struct FastStatus {
     int val_err[2];
 };
 
-enum FastResult : int { FAST_OK = 0, FAST_FALLBACK = 1, FAST_INVALID = 2 };
+enum FastResult : int { FAST_OK = 0, FAST_FALLBACK = 1, FAST_INVALID = 2, FAST_PENDING = 3 };
 
 enum StageEvent : int { EV_BEGIN = 0, EV_PLS, EV_DISC, EV_GAUSS0, EV_GAUSS1, EV_END, EV_COUNT };
 
@@ -109,9 +109,15 @@ struct Pipeline {
     // refinement / the sweep path / larger buffers: run the staged pipeline).
     // shards > 1: the Gauss kernel evaluates only item slice `shard` (of ceil(n/shards))
     // into d_partials at absolute item ids and the sums wait for shard_reduce().
+    // async: enqueue the run and return FAST_PENDING without a
+    // host sync; the item partials not owned by this shard hold the bits of -0.0
+    // (INT64_MIN), so an int64 MAX all-reduce of d_partials assembles every
+    // shard's items exactly; shard_finish() then reduces, exports and syncs once.
     int run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscParams &prm, int mode, int shard = 0,
-                 int shards = 1);
+                 int shards = 1, bool async = false);
     void shard_reduce(const double *partials_all);
+    int shard_finish();
+    int64_t part_cap = 0;   // d_partials entries of the last run (shards x per-shard capacity)
     int64_t items_cap = 0;
     int64_t pairs_seen = 0;   // largest pair count of a fused run (sizes the next run's capacity)
     // The fused sequence is replayed as a CUDA graph once a run with the same
@@ -128,6 +134,16 @@ struct Pipeline {
         }
     };
     FastKey fast_seen{}, graph_key{};
+    // state of an enqueued fused run between run_fast and finish_fast
+    struct Pending {
+        bool on = false;
+        FastKey key{};
+        int64_t pcap = 0, icap = 0;
+        int shards = 1;
+        FastStatus *st = nullptr;
+        char *hp = nullptr, *hr = nullptr, *hl = nullptr, *hf = nullptr;
+    } pend;
+    int finish_fast();
     bool fast_seen_valid = false;
     cudaGraphExec_t graph_exec = nullptr;
     long long graph_launches = 0;   // kernels inside the captured graph (lc_launch_count)

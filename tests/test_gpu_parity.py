@@ -417,9 +417,46 @@ def test_fused_shards_reassemble_bitwise(shards):
             assert np.array_equal(a, np.asarray(b)), (rep, shards)
 
 
+@pytest.mark.parametrize("shards", [2, 3, 8])
+def test_async_shards_allreduce_max_bitwise(shards):
+    """The multi-GPU exchange emulated on one GPU: every shard's async fused run
+    leaves its items in the partials buffer and -0.0 bits elsewhere; the int64
+    MAX over the shards' buffers (what the NCCL all-reduce computes) handed to
+    the pending run's lc_shard_finish gives bitwise the single-GPU results."""
+    import torch
+
+    from paper_2106_12655_b200.certify import _DeviceArray, excluded_keys, run_device_pipeline
+    from paper_2106_12655_b200.pls import upload
+
+    m = lc.generators.kusari_tube(n_around=12, rows=4, partial=5)
+    want = [np.array(a).copy() for a in run_device_pipeline(m)[:4]]
+    ctx = _native.Context()
+    upload(m, ctx)
+    prm = lc.DiscretizationParams()
+    for rep in range(2):   # second round: graph replays
+        bufs = []
+        for r in range(shards):
+            got = ctx.run_pipeline_shard_async(excluded_keys(()), m.xi, prm.epsilon, prm.max_passes,
+                                               prm.max_subsegments, 0, r, shards)
+            assert got is not None
+            ptr, cap = got
+            ctx.synchronize()
+            bufs.append(torch.as_tensor(_DeviceArray(ptr, cap, "<i8"), device="cuda").clone())
+        owned = torch.stack(bufs) != torch.iinfo(torch.int64).min
+        assert int(owned.sum(dim=0).max()) <= 1            # every item has one owner
+        combined = torch.stack(bufs).max(dim=0).values
+        torch.as_tensor(_DeviceArray(ptr, cap, "<i8"), device="cuda").copy_(combined)
+        torch.cuda.synchronize()
+        assert ctx.shard_finish()
+        got = ctx.result_views()
+        for a, b in zip(want, got):
+            assert np.array_equal(a, np.asarray(b)), (rep, shards)
+
+
 def test_sharded_nccl_path_world1():
-    """The multi-GPU code path (fused shard run + NCCL all-gather + fixed-order
-    reduce) end to end under torchrun at world size 1 (LINKCERT_FORCE_SHARDED)."""
+    """The multi-GPU code path (async fused shard run + NCCL MAX all-reduce on
+    the library stream + fixed-order reduce) end to end under torchrun at world
+    size 1 (LINKCERT_FORCE_SHARDED)."""
     import os
     import socket
     import subprocess

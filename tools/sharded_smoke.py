@@ -1,7 +1,7 @@
 """Sharded (NCCL) device path at world size 1 under torchrun (GPU box):
     python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 \
         --master-port 29511 tools/sharded_smoke.py
-LINKCERT_FORCE_SHARDED=1 routes through the fused shard run + all-gather + reduce."""
+LINKCERT_FORCE_SHARDED=1 routes through the async fused shard run + NCCL MAX all-reduce + reduce."""
 import os, sys, warnings
 os.environ["LINKCERT_FORCE_SHARDED"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
