@@ -329,6 +329,55 @@ def test_multirank_gather_is_bitwise(world, n_items):
     assert sorted(res) == [(r, True) for r in range(world)]
 
 
+def _gloo_max_worker(rank, world, port, n_items, q):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2106_12655_b200.certify import item_range
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    vals = np.random.default_rng(7).normal(size=n_items) * 10.0 ** np.random.default_rng(8).integers(-300, 300, n_items)
+    vals[::5] = -0.0
+    vals[1::7] = 0.0
+    vals[2::11] = np.inf
+    vals[3::13] = -np.inf
+    vals[4::17] = 5e-324                            # subnormal
+    bits = vals.view(np.int64).copy()
+    bits[6::19] = 0x7FF8DEADBEEF0001                # NaN with a payload
+    cap = -(-n_items // world) * world + 3          # capacity > n_items, like the library buffer
+    buf = torch.full((cap,), torch.iinfo(torch.int64).min, dtype=torch.int64)   # bits of -0.0
+    b, e, _ = item_range(n_items, rank, world)
+    buf[b:e] = torch.from_numpy(bits[b:e])          # the items this rank's Gauss slice wrote
+    dist.all_reduce(buf, op=dist.ReduceOp.MAX)      # what _fused_sharded_step enqueues (NCCL)
+    ok = bool(np.array_equal(buf.numpy()[:n_items], bits))
+    q.put((rank, ok))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n_items", [(2, 18749), (3, 1000)])
+def test_multirank_max_allreduce_assembles_bits(world, n_items):
+    """The fused multi-GPU exchange on CPU (gloo): items of other ranks hold the
+    bits of -0.0 (INT64_MIN), so an int64 MAX all-reduce returns every item's bit
+    pattern unchanged (signed zeros, infinities, subnormals, NaN payloads)."""
+    import multiprocessing as mp
+    import random
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = random.randint(20000, 40000)
+    procs = [ctx.Process(target=_gloo_max_worker, args=(r, world, port, n_items, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(res) == [(r, True) for r in range(world)]
+
+
 def test_snapshot_hint_tracks_the_loops():
     """The O(1) snapshot hint matches the full snapshot and turns None when the loop
     list changes (verify then discards the digest started on it)."""
