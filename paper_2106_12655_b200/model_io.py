@@ -1,9 +1,14 @@
-"""Canonical model serialization and digest — drop-in subset of linkcert.model_io.
+"""Model files, canonical serialization and digest — drop-in for linkcert.model_io.
 
-Reference: linkcert/model_io.py:22-176.  Only what the verify path needs is
-in scope: ParseError, model_to_dict and model_digest (SHA-256 of the
-canonical json-curves document, called by compute_linking_matrix and
-verify, certify.py:163,188).  File loading/saving is out of scope.
+Reference: linkcert/model_io.py:1-176.  The digest (SHA-256 of the canonical
+json-curves document, called by compute_linking_matrix and verify,
+certify.py:163,188) is formatted and hashed by the library (csrc/digest.cpp);
+the file formats feeding the path are read and written here:
+
+* json-curves: {"loops": [{"type": "polyline" | "catmullrom" | "cubics",
+  "closed": bool, "points": [[x, y, z], ...]}]}; "cubics" loops carry
+  "segments": [{"coeffs": 4 x 3, "t": [lo, hi]}] instead of "points".
+* polyline-text: "v x y z" lines, a blank line closes a loop.
 """
 
 from __future__ import annotations
@@ -15,7 +20,7 @@ import math
 import numpy as np
 
 from . import _native
-from .geometry import CurveModel, ValidationError
+from .geometry import CurveModel, LoopGeometry, ValidationError, compute_xi
 
 
 class ParseError(ValueError):
@@ -84,3 +89,113 @@ def model_digest_python(model: CurveModel) -> str:
     """Straight json.dumps restatement (cross-check for canonical_json in the tests)."""
     blob = json.dumps(model_to_dict(model), sort_keys=True, separators=(",", ":"))
     return hashlib.sha256(blob.encode()).hexdigest()
+
+
+# ---- model files (model_io.py:29-119, 160-176) ------------------------------
+
+def load_model(path, format="json-curves") -> CurveModel:
+    readers = {"json-curves": load_json_curves, "polyline-text": load_polyline_text}
+    if format not in readers:
+        raise ParseError(f"unknown model format: {format!r}")
+    return readers[format](path)
+
+
+def load_json_curves(path) -> CurveModel:
+    with open(path) as f:
+        try:
+            doc = json.load(f)
+        except json.JSONDecodeError as exc:
+            raise ParseError(f"malformed JSON in {path}: {exc}") from None
+    return model_from_dict(doc)
+
+
+def model_from_dict(doc) -> CurveModel:
+    """CurveModel of a json-curves document; errors name the offending loop."""
+    if not isinstance(doc, dict) or "loops" not in doc:
+        raise ParseError("json-curves file must be an object with a 'loops' key")
+    loops = []
+    for idx, entry in enumerate(doc["loops"]):
+        try:
+            loops.append(_loop_from_entry(entry))
+        except ValidationError as exc:
+            raise ValidationError(f"loop {idx}: {exc}") from None
+        except (ParseError, KeyError, TypeError, ValueError) as exc:
+            raise ParseError(f"loop {idx}: {exc}") from None
+    return CurveModel(loops)
+
+
+def _xyz_rows(raw):
+    pts = np.asarray(raw, dtype=np.float64)
+    if pts.ndim != 2 or pts.shape[1] != 3:
+        raise ParseError("points must be a list of [x, y, z] triples")
+    if not np.isfinite(pts).all():
+        raise ValidationError("points contain NaN or Inf")
+    return pts
+
+
+def _loop_from_entry(entry):
+    kind = entry.get("type", "polyline")
+    closed = bool(entry.get("closed", True))
+    if kind == "polyline":
+        return LoopGeometry.from_polyline(_xyz_rows(entry["points"]), closed=closed)
+    if kind == "catmullrom":
+        if not closed:
+            raise ParseError("catmullrom loops must be closed")
+        return LoopGeometry.from_catmull_rom(_xyz_rows(entry["points"]))
+    if kind == "cubics":
+        segs = entry["segments"]
+        coeffs = [np.asarray(sg["coeffs"], dtype=np.float64) for sg in segs]
+        for c in coeffs:
+            if c.shape != (4, 3):
+                raise ParseError(f"cubic coeffs must be 4x3, got {c.shape}")
+        t = np.asarray([sg.get("t", [0.0, 1.0]) for sg in segs], dtype=np.float64)
+        return LoopGeometry(np.stack(coeffs), t, closed=closed)
+    raise ParseError(f"unknown loop type {kind!r}")
+
+
+def load_polyline_text(path) -> CurveModel:
+    loops, rows = [], []
+
+    def close_block(where):
+        pts = np.asarray(rows, dtype=np.float64)
+        if not np.isfinite(pts).all():
+            raise ValidationError(f"loop ending at line {where} has non-finite vertices")
+        loops.append(LoopGeometry.from_polyline(pts, closed=True))
+        rows.clear()
+
+    with open(path) as f:
+        for lineno, raw in enumerate(f, 1):
+            line = raw.strip()
+            if not line:
+                if rows:
+                    close_block(lineno)
+                continue
+            fields = line.split()
+            if len(fields) != 4 or fields[0] != "v":
+                raise ParseError(f"{path}:{lineno}: expected 'v x y z', got {line!r}")
+            try:
+                rows.append([float(x) for x in fields[1:]])
+            except ValueError:
+                raise ParseError(f"{path}:{lineno}: bad coordinate in {line!r}") from None
+    if rows:
+        close_block("eof")
+    return CurveModel(loops)
+
+
+def save_json_curves(model: CurveModel, path, extra=None):
+    """json.dump(model_to_dict(model, extra), sort_keys=True) plus a newline.  Without
+    `extra` the bytes come from the library's canonical writer with json.dump's
+    default separators restored (every ',' and ':' of that document is structural)."""
+    if extra:
+        with open(path, "w") as f:
+            json.dump(model_to_dict(model, extra=extra), f, sort_keys=True)
+            f.write("\n")
+        return
+    blob = bytes(canonical_json(model)).replace(b",", b", ").replace(b":", b": ")
+    with open(path, "wb") as f:
+        f.write(blob)
+        f.write(b"\n")
+
+
+def recompute_xi(model: CurveModel) -> float:
+    return compute_xi(model.loops)
