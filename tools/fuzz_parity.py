@@ -133,11 +133,14 @@ def main():
     ap.add_argument("--cases", type=int, default=200)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--verbose", action="store_true", help="one line per case (model, outcome, seconds)")
+    ap.add_argument("--budget", type=float, default=0.0, help="stop starting new cases after this many seconds")
     args = ap.parse_args()
     rng = np.random.default_rng(args.seed)
     t0 = time.time()
     stats = {"cases": 0, "agree": 0, "errors_agreed": 0, "mismatch": []}
     for k in range(args.cases):
+        if args.budget and time.time() - t0 > args.budget:
+            break
         m, desc, params = next_case(rng)
         t1 = time.time()
         try:
