@@ -408,25 +408,13 @@ __global__ void reduce_pairs_kernel(const double *__restrict__ partials, const i
     if (dP && *dP < P) P = *dP;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; p < P; p += nwarps) {
-    const int64_t b = item_off[p], e = item_off[p + 1];
-    double s = 0.0;
-    for (int64_t k = b + lane; k < e; k += 32) s += partials[k];
-#pragma unroll
-    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (lane == 0) {
-        raw[p] = s;
-        uint8_t f = 0;
-        int64_t r = 0;
-        if (isnan(s)) {
-            f = 1;
-        } else {
-            const double rr = rint(s);   // half-to-even, like Python round()
-            if (fabs(s - rr) > 0.25) f |= 2;
-            r = (int64_t)rr;
+        const double s = warp_pair_sum(partials, item_off[p], item_off[p + 1], lane);
+        if (lane == 0) {
+            raw[p] = s;
+            int64_t r;
+            flags[p] = round_link(s, r);
+            lk[p] = r;
         }
-        lk[p] = r;
-        flags[p] = f;
-    }
     }
 }
 

@@ -93,6 +93,31 @@ void launch_item_pairs_dev(const int64_t *item_off, const PairGeom *pg, int64_t 
 void launch_reduce_pairs(const double *partials, const int64_t *item_off, int64_t P, double *raw,
                          int64_t *lk, uint8_t *flags, cudaStream_t s, const int64_t *d_P = nullptr);
 
+#ifdef __CUDACC__
+// One warp: the fixed-order sum of items [b, e) (lane-strided partial sums, then
+// the xor butterfly) -- every reduction of pair sums goes through this, so the
+// staged, fused and sharded paths agree bitwise.  All lanes return the sum.
+__device__ __forceinline__ double warp_pair_sum(const double *__restrict__ partials, int64_t b, int64_t e, int lane) {
+    double s = 0.0;
+    for (int64_t k = b + lane; k < e; k += 32) s += partials[k];
+#pragma unroll
+    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    return s;
+}
+
+// lk = rint(raw) (half-to-even, like Python round()); flags bit0 = NaN, bit1 =
+// |raw - rint(raw)| > 0.25 (kernels.py:19-20,69-72).
+__device__ __forceinline__ uint8_t round_link(double s, int64_t &lk) {
+    if (isnan(s)) {
+        lk = 0;
+        return 1;
+    }
+    const double rr = rint(s);
+    lk = (int64_t)rr;
+    return fabs(s - rr) > 0.25 ? 2 : 0;
+}
+#endif
+
 // Writes the closed SoA vertex arrays scaled by an exact power of two from
 // an AoS (n,3) buffer with per-loop offsets (no closing vertex in the input).
 void launch_pack_closed_soa(const double *aos, const int64_t *in_off, const int64_t *voff, int64_t L,

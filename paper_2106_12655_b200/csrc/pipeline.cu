@@ -70,6 +70,69 @@ __global__ void export_results_kernel(const int64_t *__restrict__ dP, int64_t ca
     }
 }
 
+// The per-pair reduction (warp_pair_sum, the order of reduce_pairs_kernel) fused
+// with the export: each block sums 64 pairs into shared memory (8 warps x 8
+// pairs), then 64 threads write raw / lk / flags to pinned host memory in
+// coalesced runs; block 0 also writes the status record.
+constexpr int kExportChunk = 64;
+__global__ void __launch_bounds__(256) reduce_export_kernel(
+    const double *__restrict__ partials, const int64_t *__restrict__ item_off, const int64_t *__restrict__ dP,
+    int64_t cap, const int64_t *__restrict__ d_items, const int *__restrict__ d_max_row,
+    const PreCounters *__restrict__ ctr, const int *__restrict__ val_err, FastStatus *__restrict__ st,
+    double *__restrict__ raw, int64_t *__restrict__ lk, uint8_t *__restrict__ flags, double *__restrict__ h_raw,
+    int64_t *__restrict__ h_lk, uint8_t *__restrict__ h_flags) {
+    __shared__ double sraw[kExportChunk];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t P = *dP < cap ? *dP : cap;
+    for (int64_t c0 = (int64_t)blockIdx.x * kExportChunk; c0 < P; c0 += (int64_t)gridDim.x * kExportChunk) {
+        for (int k = warp; k < kExportChunk; k += 8) {
+            const int64_t p = c0 + k;
+            if (p < P) {
+                const double v = warp_pair_sum(partials, item_off[p], item_off[p + 1], lane);
+                if (lane == 0) sraw[k] = v;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < kExportChunk && c0 + threadIdx.x < P) {
+            const int64_t p = c0 + threadIdx.x;
+            const double v = sraw[threadIdx.x];
+            int64_t r;
+            const uint8_t f = round_link(v, r);
+            raw[p] = v;   // the device copies serve lc_get_results
+            lk[p] = r;
+            flags[p] = f;
+            h_raw[p] = v;
+            h_lk[p] = r;
+            h_flags[p] = f;
+        }
+        __syncthreads();
+    }
+    if (st && blockIdx.x == 0 && threadIdx.x == 0) {
+        FastStatus f;
+        f.P = dP[2];
+        f.n_items = dP[3];
+        f.max_row = *d_max_row;
+        f.zero_loop = ctr->zero_loop;
+        f.n_unpaired = ctr->n_unpaired;
+        f.n_large = ctr->n_large;
+        f.marked = ctr->marked;
+        f.val_err[0] = val_err[0];
+        f.val_err[1] = val_err[1];
+        *st = f;
+    }
+}
+
+void launch_reduce_export(const double *partials, const int64_t *item_off, const int64_t *dP, int64_t cap,
+                          const int64_t *d_items, const int *d_max_row, const PreCounters *ctr, const int *val_err,
+                          FastStatus *st, double *raw, int64_t *lk, uint8_t *flags, double *h_raw, int64_t *h_lk,
+                          uint8_t *h_flags, cudaStream_t s) {
+    int64_t blocks = ceil_div(cap > 0 ? cap : 1, kExportChunk);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    reduce_export_kernel<<<(unsigned)blocks, 256, 0, s>>>(partials, item_off, dP, cap, d_items, d_max_row, ctr,
+                                                          val_err, st, raw, lk, flags, h_raw, h_lk, h_flags);
+    LC_CHECK_LAUNCH();
+}
+
 }  // namespace
 
 void Pipeline::init(cudaStream_t st) {
@@ -519,17 +582,18 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
                            d_counter.as<unsigned long long>(), d_partials.as<double>(), s, d_items, shard, shards,
                            &disc_sc.prectr.as<PreCounters>()->abort);
         record(EV_GAUSS1);
-        if (shards == 1)
-            launch_reduce_pairs(d_partials.as<double>(), d_item_off.as<int64_t>(), pcap, d_raw.as<double>(),
-                                d_lk.as<int64_t>(), d_flags.as<uint8_t>(), s, dP);
-        record(EV_END);
         LC_CUDA(cudaStreamWaitEvent(s, ev_checks, 0));
-        export_results_kernel<<<148, 256, 0, s>>>(dP, pcap, d_items, dmx, ctr, dout.d_val_err, nullptr,
-                                                  shards == 1 ? d_raw.as<double>() : nullptr, d_lk.as<int64_t>(),
-                                                  d_flags.as<uint8_t>(), st,
-                                                  reinterpret_cast<int2 *>(hp), reinterpret_cast<double *>(hr),
-                                                  reinterpret_cast<int64_t *>(hl), reinterpret_cast<uint8_t *>(hf));
-        LC_CHECK_LAUNCH();
+        if (shards == 1) {   // per-pair sums straight into pinned memory, with the status
+            launch_reduce_export(d_partials.as<double>(), d_item_off.as<int64_t>(), dP, pcap, d_items, dmx, ctr,
+                                 dout.d_val_err, st, d_raw.as<double>(), d_lk.as<int64_t>(), d_flags.as<uint8_t>(),
+                                 reinterpret_cast<double *>(hr), reinterpret_cast<int64_t *>(hl),
+                                 reinterpret_cast<uint8_t *>(hf), s);
+        } else {   // sharded: the status only; lc_shard_finish reduces after the exchange
+            export_results_kernel<<<1, 32, 0, s>>>(dP, pcap, d_items, dmx, ctr, dout.d_val_err, nullptr, nullptr,
+                                                   nullptr, nullptr, st, nullptr, nullptr, nullptr, nullptr);
+            LC_CHECK_LAUNCH();
+        }
+        record(EV_END);   // "reduce" = Gauss end -> sums (and status) in pinned memory
     };
 
     static const bool no_graph = [] {
@@ -672,14 +736,10 @@ void Pipeline::shard_reduce(const double *partials_all) {
 int Pipeline::shard_finish() {
     if (!pend.on) throw Error(LC_ERR_STATE, "no pending sharded run");
     const int64_t *dP = d_tot.as<int64_t>();
-    launch_reduce_pairs(d_partials.as<double>(), d_item_off.as<int64_t>(), pend.pcap, d_raw.as<double>(),
-                        d_lk.as<int64_t>(), d_flags.as<uint8_t>(), s, dP);
-    export_results_kernel<<<148, 256, 0, s>>>(dP, pend.pcap, nullptr, nullptr, nullptr, nullptr, nullptr,
-                                              d_raw.as<double>(), d_lk.as<int64_t>(), d_flags.as<uint8_t>(), nullptr,
-                                              nullptr, reinterpret_cast<double *>(pend.hr),
-                                              reinterpret_cast<int64_t *>(pend.hl),
-                                              reinterpret_cast<uint8_t *>(pend.hf));
-    LC_CHECK_LAUNCH();
+    launch_reduce_export(d_partials.as<double>(), d_item_off.as<int64_t>(), dP, pend.pcap, nullptr, nullptr, nullptr,
+                         nullptr, nullptr, d_raw.as<double>(), d_lk.as<int64_t>(), d_flags.as<uint8_t>(),
+                         reinterpret_cast<double *>(pend.hr), reinterpret_cast<int64_t *>(pend.hl),
+                         reinterpret_cast<uint8_t *>(pend.hf), s);
     const int r = finish_fast();
     if (r == FAST_OK) {
         h_res_P = P;

@@ -170,6 +170,7 @@ __global__ void seg_boxes_loop_kernel(const double *__restrict__ coeffs, const d
     double v[6] = {CUDART_INF, CUDART_INF, CUDART_INF, -CUDART_INF, -CUDART_INF, -CUDART_INF};
     unsigned long long dg = ~0ULL;
     int ex = 0;
+#pragma unroll 2   // both segments' loads of a 64-segment loop in flight together
     for (int64_t m = b + lane; m < e; m += 32) {
         double bl[3], bh[3];
         if (POLY) {   // see seg_boxes_kernel: the box of a from_polyline segment

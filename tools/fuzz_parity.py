@@ -69,7 +69,11 @@ def with_contacts(rng):
     if kind == 0:
         k = int(rng.integers(0, len(loops)))
         loops.insert(int(rng.integers(0, len(loops) + 1)), loops[k])
-        desc += " +duplicate ring"
+        # every subsegment of the twins overlaps its copy, so the count doubles each
+        # pass: a budget of a few thousand ends it in ~6 passes (the default 4M takes
+        # the oracle -- and the reference -- many minutes of Python per pass)
+        params = lc.DiscretizationParams(max_subsegments=int(rng.integers(1024, 16384)))
+        desc += f" +duplicate ring subseg={params.max_subsegments}"
     elif kind == 1:
         k = int(rng.integers(0, len(loops)))
         v = loops[k].start_points()
