@@ -557,9 +557,9 @@ int64_t build_items(const int32_t *d_pairs, int64_t P, const int64_t *d_voff, Pa
 void launch_gauss_items(int mode, const double *X, const double *Y, const double *Z, const ItemRec *items,
                         int64_t item_begin,
                         int64_t item_end, unsigned long long *counter, double *partials, cudaStream_t s,
-                        const int64_t *d_end, int shard, int shards, const int *abort) {
+                        const int64_t *d_end, int shard, int shards, const int *abort, bool counter_zeroed) {
     if (item_end <= item_begin) return;
-    LC_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s));
+    if (!counter_zeroed) LC_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s));
     using Kern = void (*)(const double *, const double *, const double *, const ItemRec *, int64_t, int64_t,
                           unsigned long long *, double *, const int64_t *, int, int, const int *);
     // default phase kernel: 3 resident CTAs/SM (168 regs); modes 3-7 are A/B variants

@@ -79,7 +79,7 @@ size_t build_items_scan_bytes(int64_t P);
 void launch_gauss_items(int mode, const double *X, const double *Y, const double *Z, const ItemRec *items,
                         int64_t item_begin, int64_t item_end, unsigned long long *counter,
                         double *partials, cudaStream_t s, const int64_t *d_end = nullptr, int shard = 0,
-                        int shards = 1, const int *abort = nullptr);
+                        int shards = 1, const int *abort = nullptr, bool counter_zeroed = false);
 
 // items[it] = the record of work item `it` (pair tiling + the item's place in it).
 void launch_item_pairs(const int64_t *item_off, const PairGeom *pg, int64_t P, int64_t n_items, ItemRec *items,

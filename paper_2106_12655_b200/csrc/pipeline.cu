@@ -5,6 +5,8 @@
 
 #include "pipeline.cuh"
 
+#include <cstddef>
+
 namespace lc {
 
 namespace {
@@ -75,6 +77,7 @@ __global__ void export_results_kernel(const int64_t *__restrict__ dP, int64_t ca
 // pairs), then 64 threads write raw / lk / flags to pinned host memory in
 // coalesced runs; block 0 also writes the status record.
 constexpr int kExportChunk = 64;
+constexpr int kPairsPerWarp = kExportChunk / 8;
 __global__ void __launch_bounds__(256) reduce_export_kernel(
     const double *__restrict__ partials, const int64_t *__restrict__ item_off, const int64_t *__restrict__ dP,
     int64_t cap, const int64_t *__restrict__ d_items, const int *__restrict__ d_max_row,
@@ -85,12 +88,32 @@ __global__ void __launch_bounds__(256) reduce_export_kernel(
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t P = *dP < cap ? *dP : cap;
     for (int64_t c0 = (int64_t)blockIdx.x * kExportChunk; c0 < P; c0 += (int64_t)gridDim.x * kExportChunk) {
-        for (int k = warp; k < kExportChunk; k += 8) {
-            const int64_t p = c0 + k;
-            if (p < P) {
-                const double v = warp_pair_sum(partials, item_off[p], item_off[p + 1], lane);
-                if (lane == 0) sraw[k] = v;
-            }
+        // warp w sums pairs pb .. pb+7 in warp_pair_sum's order (lane strides,
+        // then the xor butterfly: bitwise equal to reduce_pairs_kernel), with the
+        // 9 offsets in one load and the pairs' first partials loaded side by side
+        const int64_t pb = c0 + warp * kPairsPerWarp;
+        const int64_t off = lane <= kPairsPerWarp && pb + lane <= P ? item_off[pb + lane] : 0;
+        double v[kPairsPerWarp];
+        int64_t b[kPairsPerWarp], e[kPairsPerWarp];
+#pragma unroll
+        for (int j = 0; j < kPairsPerWarp; ++j) {
+            b[j] = __shfl_sync(0xffffffffu, off, j);
+            e[j] = __shfl_sync(0xffffffffu, off, j + 1);
+            if (pb + j >= P) e[j] = b[j];
+        }
+#pragma unroll
+        for (int j = 0; j < kPairsPerWarp; ++j) {
+            v[j] = 0.0;
+            if (b[j] + lane < e[j]) v[j] += partials[b[j] + lane];
+        }
+#pragma unroll
+        for (int j = 0; j < kPairsPerWarp; ++j)   // pairs of more than 32 items
+            for (int64_t k = b[j] + lane + 32; k < e[j]; k += 32) v[j] += partials[k];
+#pragma unroll
+        for (int j = 0; j < kPairsPerWarp; ++j) {
+#pragma unroll
+            for (int o = 16; o; o >>= 1) v[j] += __shfl_xor_sync(0xffffffffu, v[j], o);
+            if (lane == 0) sraw[warp * kPairsPerWarp + j] = v[j];
         }
         __syncthreads();
         if (threadIdx.x < kExportChunk && c0 + threadIdx.x < P) {
@@ -519,6 +542,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
     d_item_off.reserve(sizeof(int64_t) * (pcap + 1), s);
     d_scan.reserve(build_items_scan_bytes(pcap), s);
     d_counter.reserve(sizeof(unsigned long long), s);
+    reserve_pls_grid(L, pls_sc, s);   // prezeroed by the run's first kernel
     d_tot.reserve(4 * sizeof(int64_t), s);
     part_cap = ceil_div(icap, shards) * shards;   // every shard's slice fits at shard * per
     d_partials.reserve(sizeof(double) * part_cap, s);
@@ -544,7 +568,24 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
         in.verts = model_poly ? d_verts_in.as<double>() : nullptr;
         in.seg_fbox = d_seg_fbox.as<float>();
         reserve_discretize_fast(in, disc_sc, dout, s);
-        launch_discretize_init(disc_sc, s);   // counters + abort flag, before any branch reads them
+        // one node for every initial value of the run: the pass-1 counters + abort
+        // flag and validation slots (launch_discretize_init's values, before any
+        // branch reads them), the grid PLS memsets and the Gauss item counter
+        {
+            static_assert(sizeof(PreCounters) == 32 && offsetof(PreCounters, marked) == 16 &&
+                              offsetof(PreCounters, err_loop) == 24,
+                          "prezero word layout of PreCounters");
+            unsigned *pc = disc_sc.prectr.as<unsigned>();
+            const ZeroRange extra[] = {
+                {pc, 1, (unsigned)INT_MAX},                   // zero_loop
+                {pc + 1, 5, 0u},                              // n_unpaired, n_large, abort, marked
+                {pc + 6, 1, (unsigned)INT_MAX},               // err_loop
+                {pc + 7, 1, 0u},                              // pad
+                {disc_sc.val_err2.ptr, 2, (unsigned)INT_MAX}, // validation: first bad loop / pair
+                {d_counter.ptr, 2, 0u},                       // Gauss item claim counter
+            };
+            launch_grid_prezero(L, pls_sc, extra, (int)(sizeof extra / sizeof extra[0]), s);
+        }
         // branch 1: the chords need only the model — they run beside the PLS
         LC_CUDA(cudaEventRecord(ev_fork, s));
         LC_CUDA(cudaStreamWaitEvent(side[0], ev_fork, 0));
@@ -555,7 +596,8 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
                                     s));
         const int *dmx = nullptr;
         launch_pls_grid(d_loop_box.as<double>(), L, n_excl, pls_sc, d_pairs.as<int32_t>(), pcap, d_loff.as<int64_t>(),
-                        d_pg.as<PairGeom>(), d_item_off.as<int64_t>(), d_tot.as<int64_t>(), icap, s, &dmx);
+                        d_pg.as<PairGeom>(), d_item_off.as<int64_t>(), d_tot.as<int64_t>(), icap, s, &dmx,
+                        /*prezeroed=*/true);
         const int64_t *dP = d_tot.as<int64_t>(), *d_items = d_tot.as<int64_t>() + 1;
         record(EV_PLS);
         // branch 2: pass-1 detection + validation only feed the status — they run
@@ -580,7 +622,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
         launch_gauss_items(mode, dout.X.as<double>(), dout.Y.as<double>(), dout.Z.as<double>(), d_item_pair.as<ItemRec>(),
                            0, icap,
                            d_counter.as<unsigned long long>(), d_partials.as<double>(), s, d_items, shard, shards,
-                           &disc_sc.prectr.as<PreCounters>()->abort);
+                           &disc_sc.prectr.as<PreCounters>()->abort, /*counter_zeroed=*/true);
         record(EV_GAUSS1);
         LC_CUDA(cudaStreamWaitEvent(s, ev_checks, 0));
         if (shards == 1) {   // per-pair sums straight into pinned memory, with the status

@@ -717,12 +717,56 @@ void launch_seg_boxes(const double *coeffs, const double *t, const double *verts
 }
 
 
+namespace {
+constexpr int kMaxZeroRanges = 12;
+struct ZeroList {
+    ZeroRange r[kMaxZeroRanges];
+    int n;
+};
+__global__ void prezero_kernel(ZeroList zl) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (int k = 0; k < zl.n; ++k) {
+        unsigned *p = static_cast<unsigned *>(zl.r[k].ptr);
+        const unsigned v = zl.r[k].value;
+        for (int64_t i = t0; i < zl.r[k].words; i += stride) p[i] = v;
+    }
+}
+}  // namespace
+
+int64_t pls_grid_max_cells(int64_t L) {
+    return 32 * L + 64;   // cells ~ the largest loop extent for surface-like models (tube: 7x fewer candidates than 4L)
+}
+
+void reserve_pls_grid(int64_t L, PlsScratch &sc, cudaStream_t s) {
+    const int64_t max_cells = pls_grid_max_cells(L);
+    sc.keys.reserve(sizeof(int64_t) * (max_cells + 1), s);
+    sc.counter.reserve(sizeof(unsigned long long), s);
+    sc.counts.reserve(sizeof(int64_t) * (L + 8 > 8 ? L + 8 : 8), s);
+}
+
+void launch_grid_prezero(int64_t L, PlsScratch &sc, const ZeroRange *extra, int n_extra, cudaStream_t s) {
+    const int64_t max_cells = pls_grid_max_cells(L);
+    reserve_pls_grid(L, sc, s);
+    if (n_extra < 0 || n_extra > kMaxZeroRanges - 4) throw Error(LC_ERR_ARG, "too many prezero ranges");
+    ZeroList zl{};
+    // the memsets of grid_prefix: 3 min keys (all ones), 4 max keys + block counter, cell counts, largest row count
+    zl.r[0] = ZeroRange{sc.counts.ptr, 6, 0xffffffffu};
+    zl.r[1] = ZeroRange{static_cast<unsigned long long *>(sc.counts.ptr) + 3, 10, 0u};
+    zl.r[2] = ZeroRange{sc.keys.ptr, 2 * (max_cells + 1), 0u};
+    zl.r[3] = ZeroRange{sc.counter.ptr, 1, 0u};
+    zl.n = 4;
+    for (int k = 0; k < n_extra; ++k) zl.r[zl.n++] = extra[k];
+    prezero_kernel<<<2 * 148, 256, 0, s>>>(zl);
+    LC_CHECK_LAUNCH();
+}
+
 // Grid culling up to the per-row pair counts and their exclusive scan (no
 // host sync): sc.offs[L] = P, *sc.counter = largest row count, slots in
 // sc.pair_keys, row counts in sc.idx.  Excluded keys already in sc.excl.
 static void grid_prefix(const double *loop_box, int64_t L, int64_t n_excl, PlsScratch &sc, cudaStream_t s,
-                        const int64_t *item_loff = nullptr) {
-    const int64_t max_cells = 32 * L + 64;   // cells ~ the largest loop extent for surface-like models (tube: 7x fewer candidates than 4L)
+                        const int64_t *item_loff = nullptr, bool prezeroed = false) {
+    const int64_t max_cells = pls_grid_max_cells(L);
     sc.axis.reserve(sizeof(GridParams), s);
     sc.keys.reserve(sizeof(int64_t) * (max_cells + 1), s);         // cell counts
     sc.keys_sorted.reserve(sizeof(int64_t) * (max_cells + 1), s);  // cell offsets
@@ -740,12 +784,14 @@ static void grid_prefix(const double *loop_box, int64_t L, int64_t n_excl, PlsSc
     int *row_count = sc.idx.as<int>(), *max_count = sc.counter.as<int>();
     sc.counts.reserve(sizeof(int64_t) * (L + 8 > 8 ? L + 8 : 8), s);
     unsigned long long *acc = (unsigned long long *)sc.counts.ptr;   // 7 ordered keys, reused below
-    LC_CUDA(cudaMemsetAsync(acc, 0xff, 3 * sizeof(unsigned long long), s));
-    LC_CUDA(cudaMemsetAsync(acc + 3, 0, 5 * sizeof(unsigned long long), s));   // + the block counter
+    if (!prezeroed) {   // else done by the caller's init kernel (launch_grid_prezero)
+        LC_CUDA(cudaMemsetAsync(acc, 0xff, 3 * sizeof(unsigned long long), s));
+        LC_CUDA(cudaMemsetAsync(acc + 3, 0, 5 * sizeof(unsigned long long), s));   // + the block counter
+    }
     grid_reduce_kernel<<<(unsigned)(ceil_div(L, 256) < 148 ? ceil_div(L, 256) : 148), 256, 0, s>>>(
         loop_box, L, acc, reinterpret_cast<unsigned *>(acc + 7), max_cells, gp);
     LC_CHECK_LAUNCH();
-    LC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (max_cells + 1), s));
+    if (!prezeroed) LC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (max_cells + 1), s));
     const unsigned gl = (unsigned)ceil_div(L, 256);
     cell_count_kernel<<<gl, 256, 0, s>>>(loop_box, L, gp, cnt, sc.lcell.as<int32_t>(), sc.lrank.as<int32_t>());
     LC_CHECK_LAUNCH();
@@ -755,7 +801,7 @@ static void grid_prefix(const double *loop_box, int64_t L, int64_t n_excl, PlsSc
     cell_scatter_kernel<<<gl, 256, 0, s>>>(loop_box, L, coff, sc.lcell.as<int32_t>(), sc.lrank.as<int32_t>(),
                                            sc.perm.as<int32_t>(), sc.sbox.as<double>());
     LC_CHECK_LAUNCH();
-    LC_CUDA(cudaMemsetAsync(max_count, 0, sizeof(int), s));
+    if (!prezeroed) LC_CUDA(cudaMemsetAsync(max_count, 0, sizeof(int), s));
     grid_query_warp_kernel<true><<<(unsigned)ceil_div(L * 32, 256), 256, 0, s>>>(loop_box, L, gp, coff, sc.perm.as<int32_t>(),
                                                sc.sbox.as<double>(), sc.excl.as<uint64_t>(), n_excl, row_count,
                                                sc.pair_keys.as<int32_t>(), nullptr, nullptr,
@@ -863,8 +909,8 @@ int64_t run_pls(const double *loop_box, int64_t L, const uint64_t *h_excl, int64
 
 void launch_pls_grid(const double *loop_box, int64_t L, int64_t n_excl, PlsScratch &sc, int32_t *pairs, int64_t cap,
                      const int64_t *loff, PairGeom *pg, int64_t *item_off, int64_t *d_tot, int64_t item_cap,
-                     cudaStream_t s, const int **d_max_row) {
-    grid_prefix(loop_box, L, n_excl, sc, s, loff);
+                     cudaStream_t s, const int **d_max_row, bool prezeroed) {
+    grid_prefix(loop_box, L, n_excl, sc, s, loff, prezeroed);
     slots_compact_items_kernel<<<(unsigned)ceil_div(L, 256), 256, 0, s>>>(sc.idx.as<int>(), sc.offs.as<int64_t>(), L,
                                                                           sc.pair_keys.as<int32_t>(), pairs, cap, loff,
                                                                           pg, item_off, d_tot, sc.counter.as<int>(),

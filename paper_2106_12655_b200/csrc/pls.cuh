@@ -56,6 +56,19 @@ constexpr int kRowSlots = 16;
 struct PairGeom;
 void launch_pls_grid(const double *loop_box, int64_t L, int64_t n_excl, PlsScratch &sc, int32_t *pairs, int64_t cap,
                      const int64_t *loff, PairGeom *pg, int64_t *item_off, int64_t *d_tot, int64_t item_cap,
-                     cudaStream_t s, const int **d_max_row);
+                     cudaStream_t s, const int **d_max_row, bool prezeroed = false);
+
+// Scratch sizes of launch_pls_grid, and one kernel doing the memsets it issues
+// (grid-reduce keys, cell counts, largest row count) plus `extra` int ranges —
+// the fused pipeline folds its initial memsets into this single graph node and
+// passes prezeroed = true.
+int64_t pls_grid_max_cells(int64_t L);
+void reserve_pls_grid(int64_t L, PlsScratch &sc, cudaStream_t s);
+struct ZeroRange {
+    void *ptr;
+    int64_t words;      // 32-bit words
+    unsigned value;     // word pattern
+};
+void launch_grid_prezero(int64_t L, PlsScratch &sc, const ZeroRange *extra, int n_extra, cudaStream_t s);
 
 }  // namespace lc
