@@ -76,7 +76,10 @@ __global__ void export_results_kernel(const int64_t *__restrict__ dP, int64_t ca
 // with the export: each block sums 64 pairs into shared memory (8 warps x 8
 // pairs), then 64 threads write raw / lk / flags to pinned host memory in
 // coalesced runs; block 0 also writes the status record.
-constexpr int kExportChunk = 64;
+#ifndef LC_EXPORT_CHUNK
+#define LC_EXPORT_CHUNK 64   // pairs per block (A/B builds: -DLC_EXPORT_CHUNK=n, a multiple of 8)
+#endif
+constexpr int kExportChunk = LC_EXPORT_CHUNK;
 constexpr int kPairsPerWarp = kExportChunk / 8;
 __global__ void __launch_bounds__(256) reduce_export_kernel(
     const double *__restrict__ partials, const int64_t *__restrict__ item_off, const int64_t *__restrict__ dP,
