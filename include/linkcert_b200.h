@@ -114,6 +114,14 @@ LC_API int lc_model_upload(lc_ctx *ctx, const double *coeffs, const double *t, c
  * geometry.py:269-283): only the vertices (M, 3) travel; the device builds
  * a0 = v_k, a1 = v_{k+1} - v_k, a2 = a3 = 0, t = [0, 1] (bitwise the host arrays). */
 LC_API int lc_model_upload_polylines(lc_ctx *ctx, const double *verts, const int64_t *loop_off, int64_t L);
+/* Same model from one vertex array per loop (loop_verts[l] -> (n_l, 3) rows,
+ * n_l = loop_off[l+1] - loop_off[l]) — the arrays of L separate
+ * LoopGeometry.from_polyline loops, no host-side packing by the caller: the
+ * library gathers them on host threads into its own pinned staging buffer and
+ * copies asynchronously (returns before the copy ends; the caller's arrays are
+ * no longer read after return). */
+LC_API int lc_model_upload_polyline_ptrs(lc_ctx *ctx, const double *const *loop_verts, const int64_t *loop_off,
+                                         int64_t L);
 /* Drop-in for geometry.tight_boxes (geometry.py:113-152): coeffs (m,4,3),
  * t (m,2) domains -> lo, hi (m,3).  Independent of the uploaded model. */
 LC_API int lc_tight_boxes(lc_ctx *ctx, const double *coeffs, const double *t, int64_t m, double *lo,
@@ -216,6 +224,12 @@ LC_API int64_t lc_model_json(const double *coeffs, const double *t, const int64_
  * hashed in stream order (SHA-NI when available).  -1: non-finite coordinate. */
 LC_API int lc_model_digest(const double *coeffs, const double *t, const int64_t *loop_off,
                            const uint8_t *closed, int64_t L, int nthreads, char *hex_out);
+/* model_digest of a model whose loops are all closed LoopGeometry.from_polyline
+ * loops, from one vertex array per loop (as lc_model_upload_polyline_ptrs):
+ * the canonical "points" are the vertices (model_io.py:126-133), so no packed
+ * coefficient array is needed.  -1: non-finite coordinate, -2: null pointer. */
+LC_API int lc_model_digest_polylines(const double *const *loop_verts, const int64_t *loop_off, int64_t L,
+                                     int nthreads, char *hex_out);
 /* SHA-256 hex of a buffer (test hook; force_portable skips SHA-NI); returns 1 if SHA-NI exists. */
 LC_API int lc_sha256_hex(const void *data, int64_t n, int force_portable, char *hex_out);
 /* Page-locked host memory for model arrays (the per-call H2D copies of verify
@@ -265,6 +279,9 @@ LC_API int lc_bh_eval(lc_ctx *ctx, const lc_bh_forest *a, const lc_bh_forest *b,
 
 /* FP64 DFMA-chain throughput probe (roofline denominator), FLOP/s. */
 LC_API int lc_probe_fp64_peak(lc_ctx *ctx, double *flops, float *ms);
+/* FP64 tensor-core (mma.sync m8n8k4 f64) throughput probe, FLOP/s: the FP64
+ * datapath's other peak (DFMA and DMMA share it; the roofline takes the max). */
+LC_API int lc_probe_fp64_dmma_peak(lc_ctx *ctx, double *flops, float *ms);
 
 #ifdef __cplusplus
 }

@@ -57,8 +57,11 @@ SIGNATURES = {
     "lc_gauss_reduce": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "lc_gauss_event_ms": (ctypes.c_int, [_vp, _c_float_p]),
     "lc_probe_fp64_peak": (ctypes.c_int, [_vp, _c_double_p, _c_float_p]),
+    "lc_probe_fp64_dmma_peak": (ctypes.c_int, [_vp, _c_double_p, _c_float_p]),
     "lc_model_upload": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int64]),
     "lc_model_upload_polylines": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64]),
+    "lc_model_upload_polyline_ptrs": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64]),
+    "lc_model_digest_polylines": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p]),
     "lc_tight_boxes": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, _vp, _vp]),
     "lc_loop_boxes": (ctypes.c_int, [_vp, _vp, _vp]),
     "lc_potential_link_search": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _c_int64_p]),
@@ -120,6 +123,19 @@ def model_digest(coeffs, t, loop_off, closed=None, nthreads=0):
     cl = None if closed is None else np.ascontiguousarray(closed, dtype=np.uint8)
     out = ctypes.create_string_buffer(65)
     rc = lib.lc_model_digest(_ptr(coeffs), _ptr(t), _ptr(loop_off), _ptr(cl), len(loop_off) - 1, int(nthreads), out)
+    return None if rc != 0 else out.value.decode()
+
+
+def model_digest_polylines(vptrs, loop_off, nthreads=0):
+    """model_digest of closed from_polyline loops given by their vertex-array
+    addresses (vptrs uint64 (L)); None if a coordinate is non-finite."""
+    lib = load_library()
+    vptrs = np.ascontiguousarray(vptrs, dtype=np.uint64)
+    loop_off = np.ascontiguousarray(loop_off, dtype=np.int64)
+    out = ctypes.create_string_buffer(65)
+    rc = lib.lc_model_digest_polylines(_ptr(vptrs), _ptr(loop_off), len(loop_off) - 1, int(nthreads), out)
+    if rc == -2:
+        raise NativeError(LC_ERR_ARG, "lc_model_digest_polylines: null loop pointer")
     return None if rc != 0 else out.value.decode()
 
 
@@ -396,6 +412,16 @@ class Context:
             _check(self.lib.lc_model_upload_polylines(self.handle, _ptr(verts), _ptr(loop_off), len(loop_off) - 1))
         self._L = len(loop_off) - 1
 
+    def upload_model_polyline_ptrs(self, vptrs, loop_off):
+        """Closed polylines from one vertex array per loop (addresses in vptrs); the
+        library gathers them into its pinned staging buffer, the copy runs async."""
+        vptrs = np.ascontiguousarray(vptrs, dtype=np.uint64)
+        loop_off = np.ascontiguousarray(loop_off, dtype=np.int64)
+        with self.lock:
+            _check(self.lib.lc_model_upload_polyline_ptrs(self.handle, _ptr(vptrs), _ptr(loop_off),
+                                                          len(loop_off) - 1))
+        self._L = len(loop_off) - 1
+
     def loop_boxes(self):
         lo = np.empty((self._L, 3))
         hi = np.empty((self._L, 3))
@@ -578,10 +604,13 @@ class Context:
         """Moment trees of closed polylines on this device (Barnes-Hut)."""
         return MomentForest(self, verts, loop_off)
 
-    def probe_fp64_peak(self):
+    def probe_fp64_peak(self, dmma=False):
+        """FP64 FLOP/s of the DFMA-chain probe (dmma=True: the FP64 tensor-core probe)."""
         flops = ctypes.c_double(0.0)
         ms = ctypes.c_float(0.0)
-        _check(self.lib.lc_probe_fp64_peak(self.handle, ctypes.byref(flops), ctypes.byref(ms)))
+        fn = self.lib.lc_probe_fp64_dmma_peak if dmma else self.lib.lc_probe_fp64_peak
+        with self.lock:
+            _check(fn(self.handle, ctypes.byref(flops), ctypes.byref(ms)))
         return flops.value, ms.value
 
 

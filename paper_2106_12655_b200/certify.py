@@ -497,15 +497,9 @@ def verify(
         pairs, raw, lk, flags, _ = _bh_evaluate(model, choice, excluded, params)
         return diff_arrays(reference.array, pairs, raw, lk, flags, early_exit)
     # the digest (host, native) overlaps the device pipeline; its check and
-    # warning come first, as in the reference (certify.py:188-193).  It starts on
-    # the cached arrays before the full cache check; a stale hint is redone.
-    hint = model.snapshot_hint()
-    fut = _digest_async(model, hint) if hint is not None else None
+    # warning come first, as in the reference (certify.py:188-193)
     snap = model.snapshot()
-    if fut is None or any(a is not b for a, b in zip(hint, snap)):
-        if fut is not None:
-            fut.exception()   # wait for the stale digest; its outcome is discarded
-        fut = _digest_async(model, snap)
+    fut = _digest_async(model, snap)
     ctx = None
     try:
         if model.num_loops < 1:

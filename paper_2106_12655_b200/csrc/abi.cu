@@ -14,6 +14,7 @@
 
 namespace lc {
 double probe_dfma_flops(cudaStream_t s, float *elapsed_ms);
+double probe_dmma_flops(cudaStream_t s, float *elapsed_ms);
 }
 
 using namespace lc;
@@ -254,6 +255,15 @@ int lc_model_upload_polylines(lc_ctx *ctx, const double *verts, const int64_t *l
         if (L < 0 || !loop_off || (L > 0 && loop_off[L] > 0 && !verts))
             throw Error(LC_ERR_ARG, "lc_model_upload_polylines: bad arguments");
         ctx->pipe.upload_model_polylines(verts, loop_off, L);
+    });
+}
+
+int lc_model_upload_polyline_ptrs(lc_ctx *ctx, const double *const *loop_verts, const int64_t *loop_off,
+                                  int64_t L) {
+    return guarded(ctx, [&] {
+        if (L < 0 || !loop_off || (L > 0 && !loop_verts))
+            throw Error(LC_ERR_ARG, "lc_model_upload_polyline_ptrs: bad arguments");
+        ctx->pipe.upload_model_polyline_ptrs(loop_verts, loop_off, L);
     });
 }
 
@@ -597,6 +607,13 @@ int lc_bh_eval(lc_ctx *ctx, const lc_bh_forest *a, const lc_bh_forest *b, const 
 
 int lc_probe_fp64_peak(lc_ctx *ctx, double *flops, float *ms) {
     return guarded(ctx, [&] { *flops = probe_dfma_flops(ctx->stream, ms); });
+}
+
+int lc_probe_fp64_dmma_peak(lc_ctx *ctx, double *flops, float *ms) {
+    return guarded(ctx, [&] {
+        const double f = probe_dmma_flops(ctx->stream, ms);
+        if (flops) *flops = f;
+    });
 }
 
 }  // extern "C"

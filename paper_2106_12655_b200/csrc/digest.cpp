@@ -246,6 +246,17 @@ char *put_loop(char *p, const double *coeffs, const double *t, int64_t m, bool c
     return p;
 }
 
+// A closed from_polyline loop given by its vertex rows (n, 3): the "points" of
+// model_to_dict are coeffs[:, 0] = the vertices (model_io.py:126-133).
+char *put_loop_vertices(char *p, const double *v, int64_t m) {
+    p = put(p, "{\"closed\":true,\"points\":[");
+    for (int64_t k = 0; k < m; ++k) {
+        if (k) *p++ = ',';
+        p = put_triple(p, v + 3 * k);
+    }
+    return put(p, "],\"type\":\"polyline\"}");
+}
+
 // --------------------------------------------------------------- SHA-256
 
 const uint32_t K256[64] = {
@@ -436,6 +447,7 @@ struct Job {
     const double *coeffs, *t;
     const int64_t *off;
     const uint8_t *closed;
+    const double *const *vptr = nullptr;  // per-loop vertex rows of closed polylines (coeffs/t unused)
     std::vector<Chunk> chunks;
     std::atomic<int64_t> next{0};
     bool check_finite = false;           // digest: validate the chunk's coefficients in the worker
@@ -444,6 +456,10 @@ struct Job {
     std::condition_variable cv;
 
     void format(Chunk &c) {
+        if (vptr) {
+            format_vertices(c);
+            return;
+        }
         size_t bound = 1;
         std::vector<uint8_t> poly((size_t)(c.l1 - c.l0));
         for (int64_t l = c.l0; l < c.l1; ++l) {
@@ -459,6 +475,27 @@ struct Job {
             if (l) *p++ = ',';
             p = put_loop(p, coeffs + 12 * off[l], t + 2 * off[l], off[l + 1] - off[l], closed ? closed[l] != 0 : true,
                          poly[l - c.l0]);
+        }
+        c.size = (size_t)(p - c.data);
+        {
+            std::lock_guard<std::mutex> g(mu);
+            c.ready.store(true, std::memory_order_release);
+        }
+        cv.notify_all();
+    }
+
+    void format_vertices(Chunk &c) {
+        size_t bound = 1;
+        for (int64_t l = c.l0; l < c.l1; ++l) bound += loop_bound(off[l + 1] - off[l], true) + 1;
+        bool fin = true;
+        if (check_finite)
+            for (int64_t l = c.l0; l < c.l1 && fin; ++l) fin = all_finite(vptr[l], 3 * (off[l + 1] - off[l]));
+        if (!fin) nonfinite.store(true);
+        c.data = pool_buffer((size_t)(&c - chunks.data()), bound);
+        char *p = c.data;
+        for (int64_t l = c.l0; l < c.l1; ++l) {
+            if (l) *p++ = ',';
+            p = put_loop_vertices(p, vptr[l], off[l + 1] - off[l]);
         }
         c.size = (size_t)(p - c.data);
         {
@@ -546,16 +583,14 @@ LC_API int64_t lc_model_json(const double *coeffs, const double *t, const int64_
     return n + (int64_t)sizeof tail - 1;
 }
 
-LC_API int lc_model_digest(const double *coeffs, const double *t, const int64_t *loop_off, const uint8_t *closed,
-                           int64_t L, int nthreads, char *hex_out) {
+static int digest_job(Job &job, int64_t L, int nthreads, char *hex_out) {
     static const bool stats = std::getenv("LC_DIGEST_STATS") != nullptr;
     using clk = std::chrono::steady_clock;
     const auto ms = [](clk::time_point a, clk::time_point b) {
         return std::chrono::duration<double, std::milli>(b - a).count();
     };
     const auto t_begin = clk::now();
-    const int64_t M = L > 0 ? loop_off[L] : 0;
-    Job job{coeffs, t, loop_off, closed};
+    const int64_t M = L > 0 ? job.off[L] : 0;
     job.check_finite = true;
     std::lock_guard<std::mutex> pool_lock(g_pool_mu);
     make_chunks(job, L, M, 4096);
@@ -596,6 +631,21 @@ LC_API int lc_model_digest(const double *coeffs, const double *t, const int64_t 
     if (job.nonfinite.load()) return -1;
     h.hex(hex_out);
     return 0;
+}
+
+LC_API int lc_model_digest(const double *coeffs, const double *t, const int64_t *loop_off, const uint8_t *closed,
+                           int64_t L, int nthreads, char *hex_out) {
+    Job job{coeffs, t, loop_off, closed};
+    return digest_job(job, L, nthreads, hex_out);
+}
+
+LC_API int lc_model_digest_polylines(const double *const *loop_verts, const int64_t *loop_off, int64_t L,
+                                     int nthreads, char *hex_out) {
+    for (int64_t l = 0; l < L; ++l)
+        if (loop_off[l + 1] > loop_off[l] && !loop_verts[l]) return -2;
+    Job job{nullptr, nullptr, loop_off, nullptr};
+    job.vptr = loop_verts;
+    return digest_job(job, L, nthreads, hex_out);
 }
 
 LC_API int lc_sha256_hex(const void *data, int64_t n, int force_portable, char *hex_out) {

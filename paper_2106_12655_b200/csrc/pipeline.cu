@@ -1,6 +1,8 @@
 // Pipeline stage orchestration on one device/stream (host side of the C-ABI).
+#include <algorithm>
 #include <climits>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 #include "pipeline.cuh"
@@ -170,7 +172,7 @@ void Pipeline::init(cudaStream_t st) {
     LC_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     LC_CUDA(cudaStreamCreateWithPriority(&side[0], cudaStreamNonBlocking, prio_lo));
     LC_CUDA(cudaStreamCreateWithPriority(&side[1], cudaStreamNonBlocking, prio_hi));
-    for (cudaEvent_t *e : {&ev_fork, &ev_chords, &ev_pairs, &ev_checks})
+    for (cudaEvent_t *e : {&ev_fork, &ev_chords, &ev_pairs, &ev_checks, &ev_stage})
         LC_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
 }
 
@@ -195,11 +197,12 @@ void Pipeline::release() {
     if (s) cudaStreamSynchronize(s);
     h_res.release();
     h_excl.release();
+    h_stage.release();
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
     graph_exec = nullptr;
     for (auto &e : ev)
         if (e) cudaEventDestroy(e);
-    for (cudaEvent_t e : {ev_fork, ev_chords, ev_pairs, ev_checks})
+    for (cudaEvent_t e : {ev_fork, ev_chords, ev_pairs, ev_checks, ev_stage})
         if (e) cudaEventDestroy(e);
     for (auto &x : side)
         if (x) cudaStreamDestroy(x);
@@ -306,6 +309,71 @@ void Pipeline::upload_model_polylines(const double *verts, const int64_t *loff, 
     polylines_ready = false;
     P = 0;
     LC_CUDA(cudaStreamSynchronize(s));
+}
+
+namespace {
+
+// Copy loop rows [l0, l1) of a per-loop pointer table into dst (row_bytes each).
+void gather_loops(char *dst, const double *const *src, const int64_t *loff, int64_t l0, int64_t l1,
+                  size_t row_bytes) {
+    for (int64_t l = l0; l < l1; ++l) {
+        const int64_t m = loff[l + 1] - loff[l];
+        if (m > 0) std::memcpy(dst + (size_t)loff[l] * row_bytes, src[l], (size_t)m * row_bytes);
+    }
+}
+
+}  // namespace
+
+void Pipeline::upload_model_polyline_ptrs(const double *const *loop_verts, const int64_t *loff, int64_t nloops) {
+    if (nloops > 0 && loff[0] != 0) throw Error(LC_ERR_ARG, "loop offsets must start at 0");
+    int64_t mx = 0;
+    for (int64_t l = 0; l < nloops; ++l) {
+        const int64_t m = loff[l + 1] - loff[l];
+        if (m < 1) throw Error(LC_ERR_ARG, "every loop needs at least one vertex");
+        if (!loop_verts[l]) throw Error(LC_ERR_ARG, "null loop vertex pointer");
+        if (m > mx) mx = m;
+    }
+    const int64_t nM = nloops > 0 ? loff[nloops] : 0;
+    const size_t vbytes = sizeof(double) * 3 * (size_t)nM, obytes = sizeof(int64_t) * (size_t)(nloops + 1);
+    if (stage_pending) {   // the previous upload's copy still reads the staging buffer
+        LC_CUDA(cudaEventSynchronize(ev_stage));
+        stage_pending = false;
+    }
+    h_stage.reserve(vbytes + obytes);
+    char *st = static_cast<char *>(h_stage.ptr);
+    // loops split into ~equal-byte ranges, one per thread (the caller's thread takes the first)
+    const int64_t per_thread = 1 << 18;   // rows (6 MiB) per thread at least
+    int nt = (int)std::min<int64_t>(8, std::max<int64_t>(1, nM / per_thread));
+    const unsigned hw = std::thread::hardware_concurrency();
+    if (hw > 0 && (unsigned)nt > hw / 2) nt = std::max(1, (int)hw / 2);
+    std::vector<int64_t> cut(nt + 1, nloops);
+    cut[0] = 0;
+    for (int k = 1, l = 0; k < nt; ++k) {
+        const int64_t want = nM * k / nt;
+        while (l < nloops && loff[l] < want) ++l;
+        cut[k] = l;
+    }
+    std::vector<std::thread> th;
+    for (int k = 1; k < nt; ++k)
+        th.emplace_back(gather_loops, st, loop_verts, loff, cut[k], cut[k + 1], sizeof(double) * 3);
+    gather_loops(st, loop_verts, loff, cut[0], cut[1], sizeof(double) * 3);
+    std::memcpy(st + vbytes, loff, obytes);
+    for (auto &x : th) x.join();
+    L = nloops;
+    M = nM;
+    max_loop = mx;
+    d_loff.reserve(obytes, s);
+    d_verts_in.reserve(sizeof(double) * 3 * (M > 0 ? M : 1), s);
+    if (M > 0) LC_CUDA(cudaMemcpyAsync(d_verts_in.ptr, st, vbytes, cudaMemcpyHostToDevice, s));
+    LC_CUDA(cudaMemcpyAsync(d_loff.ptr, st + vbytes, obytes, cudaMemcpyHostToDevice, s));
+    LC_CUDA(cudaEventRecord(ev_stage, s));
+    stage_pending = true;
+    model_ready = true;
+    model_poly = true;
+    coeffs_ready = false;
+    derived = false;
+    polylines_ready = false;
+    P = 0;
 }
 
 int64_t Pipeline::potential_link_search(const uint64_t *excl_keys, int64_t n_excl, bool in_run) {

@@ -76,6 +76,13 @@ struct Pipeline {
     void upload_model(const double *coeffs, const double *t, const int64_t *loff, int64_t nloops);
     // closed polylines given as vertices only (a0 = v_k, a1 = v_k+1 - v_k, a2 = a3 = 0, t = [0, 1])
     void upload_model_polylines(const double *verts, const int64_t *loff, int64_t nloops);
+    // the same from one vertex array per loop: gathered on host threads into a
+    // library-owned pinned staging buffer and copied asynchronously (no host sync;
+    // the next gather waits only for the previous copy)
+    void upload_model_polyline_ptrs(const double *const *loop_verts, const int64_t *loff, int64_t nloops);
+    PinnedBuf h_stage;
+    cudaEvent_t ev_stage = nullptr;
+    bool stage_pending = false;
     // -> d_pairs, P; in_run: EV_BEGIN already recorded by derive() of this run
     int64_t potential_link_search(const uint64_t *excl_keys, int64_t n_excl, bool in_run = false);
     bool discretize(const DiscParams &prm);                                      // -> dout = gauss input

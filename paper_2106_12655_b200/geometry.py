@@ -5,9 +5,10 @@ reference (linkcert/geometry.py:14-360).  Everything numeric on the hot path
 (tight boxes, PLS, discretization, Gauss sums) runs on the GPU through the
 C-ABI; the host types here only hold float64 arrays.
 
-B200-first addition: a CurveModel keeps one packed copy of all its loops
-(coeffs (M, 4, 3), t (M, 2), loop offsets (L+1)) — the layout the device
-pipeline consumes — built once and cached.
+B200-first addition: a CurveModel hands the device pipeline and the digest a
+ModelSnapshot of its loops — the loops' own vertex arrays (closed
+from_polyline loops) or a packed copy (coeffs (M, 4, 3), t (M, 2), loop
+offsets (L+1)) — cached while the loops are unchanged.
 """
 
 from __future__ import annotations
@@ -164,29 +165,80 @@ def catmull_rom_to_cubics(control_points) -> list[CubicSegment]:
     return [CubicSegment(c) for c in catmull_rom_coeffs(pts)]
 
 
+_EPOCH = [0]   # bumped by every attribute assignment on any LoopGeometry (model snapshot validity)
+
+
+def _owned(a, frozen=True):
+    """Owned, C-contiguous float64 copy of `a`, read-only: a loop's arrays cannot
+    change under a cached model snapshot (in-place edits raise; reassignment of
+    the attribute is seen by the loop's stamp)."""
+    out = np.array(a, dtype=np.float64, order="C")
+    if frozen:
+        out.setflags(write=False)
+    return out
+
+
+def _loop_attr(name, conv):
+    def get(self):
+        return self.__dict__[name]
+
+    def put(self, value):
+        d = self.__dict__
+        d[name] = conv(value)
+        d["_pv"] = None                 # no longer known to be a plain from_polyline loop
+        _EPOCH[0] += 1
+        d["_stamp"] = _EPOCH[0]
+
+    return property(get, put)
+
+
 class LoopGeometry:
-    """Ordered chain of cubic segments, optionally closed (geometry.py:206-296)."""
+    """Ordered chain of cubic segments, optionally closed (geometry.py:206-296).
+
+    B200-first ownership: the loop keeps owned, read-only copies of its arrays
+    (the reference aliases the caller's arrays, geometry.py:225-230), so a
+    CurveModel can cache what it uploads and hashes.  Reassigning an attribute
+    (loop.coeffs = ...) is tracked; editing an array in place raises ValueError.
+    A closed loop built by from_polyline remembers its vertex array: a model of
+    such loops reaches the GPU and the digest as vertices only (24 B/segment).
+    """
+
+    coeffs = _loop_attr("_coeffs", _owned)
+    t = _loop_attr("_t", _owned)
+    control_points = _loop_attr("_cp", _owned)
+    closed = _loop_attr("_closed", bool)
 
     def __init__(self, coeffs, t=None, closed=True, control_points=None, xi_hint=None):
-        coeffs = np.asarray(coeffs, dtype=np.float64)
+        coeffs = _owned(coeffs, frozen=False)
+        t = None if t is None else _owned(t, frozen=False)
+        cp = None if control_points is None else _owned(control_points, frozen=False)
+        self._setup(coeffs, t, closed, cp, xi_hint)
+
+    def _setup(self, coeffs, t, closed, cp, xi_hint, pv=None):
+        """Validate (geometry.py:216-240) and take ownership of already-owned arrays."""
         if coeffs.ndim != 3 or coeffs.shape[1:] != (4, 3):
             raise ValidationError("loop coeffs must be (m, 4, 3)")
         if not np.all(np.isfinite(coeffs)):
             raise ValidationError("loop has non-finite coefficients")
         m = coeffs.shape[0]
-        t = np.tile(np.array([0.0, 1.0]), (m, 1)) if t is None else np.asarray(t, dtype=np.float64)
+        if t is None:
+            t = np.empty((m, 2))
+            t[:, 0] = 0.0
+            t[:, 1] = 1.0
         if t.shape != (m, 2) or np.any(t[:, 0] >= t[:, 1]):
             raise ValidationError("bad segment parameter domains")
-        self.coeffs = coeffs
-        self.t = t
-        self.closed = bool(closed)
-        self.control_points = np.asarray(
-            self.start_points() if control_points is None else control_points, dtype=np.float64
-        )
+        if cp is None:
+            cp = eval_cubics(coeffs, t[:, 0])
+        for a in (coeffs, t, cp):
+            a.setflags(write=False)
+        d = self.__dict__
+        d["_coeffs"], d["_t"], d["_closed"], d["_cp"] = coeffs, t, bool(closed), cp
+        d["_pv"] = pv
+        d["_stamp"] = 0
         if closed and m < 3:
             raise ValidationError(f"closed loop needs >= 3 segments, got {m}")
         if xi_hint is None:
-            xi_hint = float(np.mean(np.abs(self.control_points))) or 1.0
+            xi_hint = float(np.mean(np.abs(cp))) or 1.0
         starts, ends = self.start_points(), self.end_points()
         nxt = np.roll(starts, -1, axis=0) if closed else starts[1:]
         gaps = np.linalg.norm((ends if closed else ends[:-1]) - nxt, axis=1)
@@ -194,30 +246,30 @@ class LoopGeometry:
             raise ValidationError(f"consecutive segments do not share endpoints (max gap {gaps.max():.3e})")
 
     @classmethod
-    def _trusted(cls, coeffs, t, closed, control_points):
-        """Construct without re-validation (arrays already validated in bulk)."""
+    def _view(cls, coeffs, t, verts, ptr):
+        """A closed from_polyline loop over views of a validated read-only block."""
         self = cls.__new__(cls)
-        self.coeffs = coeffs
-        self.t = t
-        self.closed = closed
-        self.control_points = control_points
+        d = self.__dict__
+        d["_coeffs"], d["_t"], d["_closed"], d["_cp"] = coeffs, t, True, verts
+        d["_pv"] = (verts, ptr)
+        d["_stamp"] = 0
         return self
 
     def __len__(self):
-        return self.coeffs.shape[0]
+        return self._coeffs.shape[0]
 
     def start_points(self):
-        return eval_cubics(self.coeffs, self.t[:, 0])
+        return eval_cubics(self._coeffs, self._t[:, 0])
 
     def end_points(self):
-        return eval_cubics(self.coeffs, self.t[:, 1])
+        return eval_cubics(self._coeffs, self._t[:, 1])
 
     @property
     def is_polyline(self):
-        return not np.any(self.coeffs[:, 2:])
+        return not np.any(self._coeffs[:, 2:])
 
     def boxes(self):
-        return tight_boxes(self.coeffs, self.t[:, 0], self.t[:, 1])
+        return tight_boxes(self._coeffs, self._t[:, 0], self._t[:, 1])
 
     def aabb(self) -> Aabb:
         lo, hi = self.boxes()
@@ -230,12 +282,16 @@ class LoopGeometry:
             raise ValidationError("polyline vertices must be (n, 3)")
         if not np.all(np.isfinite(verts)):
             raise ValidationError("polyline has non-finite vertices")
+        verts = _owned(verts, frozen=False)
         starts = verts if closed else verts[:-1]
         ends = np.roll(verts, -1, axis=0) if closed else verts[1:]
         coeffs = np.zeros((len(starts), 4, 3))
         coeffs[:, 0] = starts
         coeffs[:, 1] = ends - starts
-        return LoopGeometry(coeffs, closed=closed, control_points=verts)
+        loop = LoopGeometry.__new__(LoopGeometry)
+        pv = (verts, verts.ctypes.data) if closed and len(verts) else None
+        loop._setup(coeffs, None, closed, verts, None, pv)
+        return loop
 
     @staticmethod
     def from_segments(segments, closed=True):
@@ -276,6 +332,68 @@ def compute_xi(loops):
     return total / count if count else 0.0
 
 
+class ModelSnapshot:
+    """What one certificate / verify call hands to the digest thread and to the
+    device upload, taken after one validity check of the model's loops.
+
+    poly: every loop is a closed from_polyline loop -> `vptrs` (L) addresses of
+    the loops' own vertex arrays (kept alive by `vrefs`) and `off` (L+1) reach
+    the library directly (lc_model_upload_polyline_ptrs / lc_model_digest_polylines:
+    no host-side packing).  Otherwise `packed()` = (coeffs (M,4,3), t (M,2), off)
+    in page-locked memory.
+    """
+
+    __slots__ = ("key", "epoch", "poly", "off", "closed", "vptrs", "vrefs", "_packed")
+
+    def __init__(self, loops, epoch):
+        self.key = tuple(loops)
+        self.epoch = epoch
+        self._packed = None
+        L = len(self.key)
+        pv = [lp._pv for lp in self.key]
+        self.poly = L > 0 and None not in pv
+        self.off = np.zeros(L + 1, dtype=np.int64)
+        if self.poly:
+            self.vrefs = [p[0] for p in pv]
+            self.vptrs = np.fromiter((p[1] for p in pv), dtype=np.uint64, count=L)
+            np.cumsum(np.fromiter((len(v) for v in self.vrefs), dtype=np.int64, count=L), out=self.off[1:])
+            self.closed = np.ones(L, dtype=np.uint8)
+        else:
+            self.vrefs = self.vptrs = None
+            if L:
+                np.cumsum(np.fromiter((len(lp) for lp in self.key), dtype=np.int64, count=L), out=self.off[1:])
+            self.closed = np.fromiter((lp.closed for lp in self.key), dtype=np.uint8, count=L)
+
+    def valid_for(self, loops, epoch):
+        if self.key != tuple(loops):          # identity per element (LoopGeometry has no __eq__)
+            return False
+        if self.epoch != epoch:
+            if any(lp._stamp > self.epoch for lp in self.key):
+                return False
+            self.epoch = epoch
+        return True
+
+    def packed(self):
+        """(coeffs (M,4,3), t (M,2), loop_off (L+1)), page-locked, built on first use."""
+        if self._packed is None:
+            M = int(self.off[-1])
+            if M:
+                from . import _native
+
+                coeffs = _native.pinned_empty((M, 4, 3))
+                np.concatenate([lp.coeffs for lp in self.key], out=coeffs)
+                t = _native.pinned_empty((M, 2))
+                np.concatenate([lp.t for lp in self.key], out=t)
+            else:
+                coeffs, t = np.zeros((0, 4, 3)), np.zeros((0, 2))
+            self._packed = (coeffs, t, self.off)
+        return self._packed
+
+    def vertices(self):
+        """Packed (M, 3) vertices of a poly snapshot (a host copy; tests / tools)."""
+        return np.concatenate(self.vrefs) if self.vrefs else np.zeros((0, 3))
+
+
 @dataclass
 class CurveModel:
     """A collection of loops plus the model coordinate scale xi (geometry.py:299-312)."""
@@ -293,92 +411,32 @@ class CurveModel:
     def num_loops(self):
         return len(self.loops)
 
-    # ---- B200 packed layout -------------------------------------------------
-    def packed(self):
-        """(coeffs (M,4,3), t (M,2), loop_off (L+1)) float64/int64, cached."""
-        key = tuple(map(id, self.loops))
-        cache = self.__dict__.get("_packed_cache")
-        if cache is not None and cache[0] == key:
-            return cache[1]
-        if self.loops:
-            from . import _native
+    # ---- B200 snapshot of the loops -------------------------------------------
+    def snapshot(self) -> ModelSnapshot:
+        """The loops as the device upload and the digest consume them.  Cached
+        while the loop list holds the same objects and none of them had an
+        attribute reassigned (their arrays are read-only); O(L) to check."""
+        epoch = _EPOCH[0]
+        snap = self.__dict__.get("_snapshot")
+        if snap is not None and snap.valid_for(self.loops, epoch):
+            return snap
+        snap = ModelSnapshot(self.loops, epoch)
+        self.__dict__["_snapshot"] = snap
+        return snap
 
-            counts = np.fromiter((lp.coeffs.shape[0] for lp in self.loops), dtype=np.int64, count=len(self.loops))
-            # page-locked: verify copies these to the device on every call
-            coeffs = _native.pinned_empty((int(counts.sum()), 4, 3))
-            np.concatenate([lp.coeffs for lp in self.loops], out=coeffs)
-            t = _native.pinned_empty((int(counts.sum()), 2))
-            np.concatenate([lp.t for lp in self.loops], out=t)
-        else:
-            counts = np.zeros(0, dtype=np.int64)
-            coeffs = np.zeros((0, 4, 3))
-            t = np.zeros((0, 2))
-        off = np.zeros(len(counts) + 1, dtype=np.int64)
-        np.cumsum(counts, out=off[1:])
-        packed = (coeffs, t, off)
-        self.__dict__["_packed_cache"] = (key, packed)
-        self.__dict__.pop("_polyline_cache", None)
-        return packed
+    def packed(self):
+        """(coeffs (M,4,3), t (M,2), loop_off (L+1)) float64/int64 of the current loops."""
+        return self.snapshot().packed()
 
     def closed_flags(self):
-        """(L,) uint8 closedness of every loop, cached with the packed arrays."""
-        return self._closed_of(self.packed()[0])
-
-    def _closed_of(self, coeffs):
-        cache = self.__dict__.get("_closed_cache")
-        if cache is not None and cache[0] is coeffs:
-            return cache[1]
-        flags = np.fromiter((lp.closed for lp in self.loops), dtype=np.uint8, count=len(self.loops))
-        self.__dict__["_closed_cache"] = (coeffs, flags)
-        return flags
+        """(L,) uint8 closedness of every loop."""
+        return self.snapshot().closed
 
     def polyline_vertices(self):
-        """(verts (M, 3), loop_off) when every loop is a plain closed polyline whose
-        arrays are exactly LoopGeometry.from_polyline's (a1 = next - start bitwise,
-        a2 = a3 = 0, t = [0, 1]) — then only the vertices need to reach the GPU.
-        None otherwise.  Cached with the packed arrays."""
-        return self._poly_of(*self.packed())
-
-    def _poly_of(self, coeffs, t, off):
-        cache = self.__dict__.get("_polyline_cache")
-        if cache is not None and cache[0] is coeffs:
-            return cache[1]
-        result = None
-        if len(off) > 1 and all(lp.closed for lp in self.loops) and np.all(np.diff(off) >= 1):
-            nxt = np.arange(len(coeffs), dtype=np.int64) + 1
-            nxt[off[1:] - 1] = off[:-1]
-            a0 = coeffs[:, 0]
-            if (not np.any(coeffs[:, 2:]) and np.all(t[:, 0] == 0.0) and np.all(t[:, 1] == 1.0)
-                    and np.array_equal((a0[nxt] - a0).view(np.int64), coeffs[:, 1].view(np.int64))):
-                from . import _native
-
-                result = (_native.pinned_copy(a0), off)   # page-locked upload source
-        self.__dict__["_polyline_cache"] = (coeffs, result)
-        return result
-
-    def snapshot(self):
-        """(coeffs, t, loop_off, closed, polyline) of the current loops after a single
-        cache check — what one verify / certificate call hands to the digest
-        thread and to the device upload."""
-        coeffs, t, off = self.packed()
-        return coeffs, t, off, self._closed_of(coeffs), self._poly_of(coeffs, t, off)
-
-    def snapshot_hint(self):
-        """The cached snapshot if a cheap O(1) check (loop count, first and last loop
-        identity) says the loops are unchanged, else None.  Only a head start: the
-        caller still runs snapshot() and must discard work done on a stale hint."""
-        cache = self.__dict__.get("_packed_cache")
-        loops = self.loops
-        if cache is None or not loops:
-            return None
-        key, (coeffs, t, off) = cache
-        if len(key) != len(loops) or key[0] != id(loops[0]) or key[-1] != id(loops[-1]):
-            return None
-        closed = self.__dict__.get("_closed_cache")
-        poly = self.__dict__.get("_polyline_cache")
-        if closed is None or closed[0] is not coeffs or poly is None or poly[0] is not coeffs:
-            return None
-        return coeffs, t, off, closed[1], poly[1]
+        """(verts (M, 3), loop_off) when every loop is a closed from_polyline loop
+        (only the vertices reach the GPU), else None."""
+        snap = self.snapshot()
+        return (snap.vertices(), snap.off) if snap.poly else None
 
     @classmethod
     def from_polyline_arrays(cls, verts, offsets, closed=True):
@@ -386,9 +444,10 @@ class CurveModel:
 
         Equivalent to CurveModel([LoopGeometry.from_polyline(v) for v in
         split(verts)]) — same validation, same arrays, same xi — but checks
-        every loop in one vectorized pass and fills the packed cache.
+        every loop in one vectorized pass; the loops are read-only views of one
+        owned block.
         """
-        verts = np.ascontiguousarray(verts, dtype=np.float64)
+        verts = np.asarray(verts, dtype=np.float64)
         off = np.ascontiguousarray(offsets, dtype=np.int64)
         if verts.ndim != 2 or verts.shape[1] != 3:
             raise ValidationError("polyline vertices must be (n, 3)")
@@ -396,6 +455,7 @@ class CurveModel:
             raise ValidationError("bulk constructor supports closed loops only")
         if not np.all(np.isfinite(verts)):
             raise ValidationError("polyline has non-finite vertices")
+        verts = _owned(verts, frozen=False)
         L = len(off) - 1
         counts = np.diff(off)
         if np.any(counts < 3):
@@ -419,22 +479,19 @@ class CurveModel:
         gmax = np.maximum.reduceat(gaps, off[:-1]) if L else np.zeros(0)
         if np.any(gmax > CONTINUITY_TOL * hint):
             raise ValidationError("consecutive segments do not share endpoints")
-        loops = [
-            LoopGeometry._trusted(coeffs[off[k]:off[k + 1]], t[off[k]:off[k + 1]], True, verts[off[k]:off[k + 1]])
-            for k in range(L)
-        ]
+        for a in (verts, coeffs, t):
+            a.setflags(write=False)
+        base = verts.ctypes.data
+        ptrs = (base + 24 * off[:-1]).tolist()
+        loops = [LoopGeometry._view(coeffs[off[k]:off[k + 1]], t[off[k]:off[k + 1]], verts[off[k]:off[k + 1]],
+                                    ptrs[k])
+                 for k in range(L)]
         # xi exactly as compute_xi: sequential float accumulation of per-loop sums
         total = 0.0
         for s in sums.tolist():
             total += s
         xi = total / (3 * len(verts)) if len(verts) else 0.0
-        model = cls(loops, xi=xi)
-        model.__dict__["_packed_cache"] = (tuple(map(id, loops)), (coeffs, t, off))
-        from . import _native
-
-        model.__dict__["_polyline_cache"] = (coeffs, (_native.pinned_copy(verts), off))   # page-locked upload source
-        model.__dict__["_closed_cache"] = (coeffs, np.ones(L, dtype=np.uint8))
-        return model
+        return cls(loops, xi=xi)
 
 
 class PolylineLoop:
@@ -479,7 +536,8 @@ class PolylineLoop:
 
 
 __all__ = [
-    "Aabb", "CONTINUITY_TOL", "CubicSegment", "CurveModel", "LoopGeometry", "MACHINE_EPS", "PolylineLoop",
+    "Aabb", "CONTINUITY_TOL", "CubicSegment", "CurveModel", "LoopGeometry", "MACHINE_EPS", "ModelSnapshot",
+    "PolylineLoop",
     "ValidationError", "catmull_rom_coeffs", "catmull_rom_to_cubics", "compute_xi", "eval_cubics",
     "split_cubic", "tight_aabb_of_cubic", "tight_boxes",
 ]

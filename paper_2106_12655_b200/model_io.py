@@ -64,22 +64,28 @@ def model_to_dict(model: CurveModel, extra=None) -> dict:
 def canonical_json(model: CurveModel):
     """Bytes of json.dumps(model_to_dict(model), sort_keys=True, separators=(",", ":")),
     formatted by the library's multithreaded writer (csrc/digest.cpp)."""
-    coeffs, t, off = model.packed()
-    closed = model.closed_flags()
+    snap = model.snapshot()
+    coeffs, t, off = snap.packed()
+    closed = snap.closed
     blob = _native.model_json(coeffs, t, off, None if closed.all() else closed)
     if blob is None:
         raise ValidationError("cannot serialize non-finite coordinate")
     return blob
 
 
-def model_digest(model: CurveModel, snapshot=None) -> str:
+def model_digest(model: CurveModel, snapshot=None, nthreads=0) -> str:
     """SHA-256 hex digest of the canonical json-curves serialization (model_io.py:169-172).
 
     Formatting and hashing run in the library (csrc/digest.cpp) on all host
     cores with the GIL released, so callers can overlap it with GPU work.
     """
-    coeffs, t, off, closed, _ = snapshot if snapshot is not None else model.snapshot()
-    digest = _native.model_digest(coeffs, t, off, None if closed.all() else closed)
+    snap = snapshot if snapshot is not None else model.snapshot()
+    if snap.poly:     # closed from_polyline loops: straight from their vertex arrays
+        digest = _native.model_digest_polylines(snap.vptrs, snap.off, nthreads)
+    else:
+        coeffs, t, off = snap.packed()
+        closed = snap.closed
+        digest = _native.model_digest(coeffs, t, off, None if closed.all() else closed, nthreads)
     if digest is None:
         raise ValidationError("cannot serialize non-finite coordinate")
     return digest

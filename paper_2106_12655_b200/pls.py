@@ -87,11 +87,11 @@ def excluded_keys(excluded):
 def upload(model: CurveModel, ctx=None, snapshot=None):
     """Stage the model's packed arrays on the device (boxes are derived per run)."""
     ctx = ctx or _native.context()
-    coeffs, t, off, _, poly = snapshot if snapshot is not None else model.snapshot()
-    if poly is not None:            # 24 B/segment instead of 112 B/segment over PCIe
-        ctx.upload_model_polylines(*poly)
+    snap = snapshot if snapshot is not None else model.snapshot()
+    if snap.poly:       # the loops' own vertex arrays: 24 B/segment, gathered by the library
+        ctx.upload_model_polyline_ptrs(snap.vptrs, snap.off)
     else:
-        ctx.upload_model(coeffs, t, off)
+        ctx.upload_model(*snap.packed())
     return ctx
 
 

@@ -378,18 +378,61 @@ def test_multirank_max_allreduce_assembles_bits(world, n_items):
     assert sorted(res) == [(r, True) for r in range(world)]
 
 
-def test_snapshot_hint_tracks_the_loops():
-    """The O(1) snapshot hint matches the full snapshot and turns None when the loop
-    list changes (verify then discards the digest started on it)."""
+def test_snapshot_tracks_the_loops():
+    """The model snapshot (what verify uploads and hashes) is reused only while the
+    loop list holds the same objects and no loop had an attribute reassigned."""
     import numpy as np
 
     from paper_2106_12655_b200 import generators as gen
 
     m = gen.kusari_tube(n_around=12, rows=4, partial=5)
-    assert m.snapshot_hint() is None or all(a is b for a, b in zip(m.snapshot_hint(), m.snapshot()))
     snap = m.snapshot()
-    assert all(a is b for a, b in zip(m.snapshot_hint(), snap))
-    m.loops.append(m.loops[0])          # the last loop's identity changes
-    assert m.snapshot_hint() is None
-    assert m.snapshot()[2][-1] == snap[2][-1] + m.loops[0].coeffs.shape[0]
-    assert np.array_equal(m.snapshot()[0][:len(snap[0])], snap[0])
+    assert snap.poly and m.snapshot() is snap
+    assert np.array_equal(snap.vertices(), np.concatenate([lp.control_points for lp in m.loops]))
+    m.loops.append(m.loops[0])                      # list changed -> new snapshot
+    s2 = m.snapshot()
+    assert s2 is not snap and s2.off[-1] == snap.off[-1] + len(m.loops[0])
+    assert np.array_equal(s2.packed()[0][:len(snap.packed()[0])], snap.packed()[0])
+    m.loops.pop()
+    s3 = m.snapshot()
+    fresh = lc.CurveModel(list(m.loops), xi=m.xi)   # a fresh model of the same loops
+    assert fresh.snapshot() is not s3 and np.array_equal(fresh.snapshot().vptrs, s3.vptrs)
+
+
+def test_loop_arrays_are_owned_and_read_only():
+    """an in-place edit cannot leave a cached snapshot stale —
+    the loop owns read-only copies; reassignment invalidates the snapshot and
+    drops the vertex-only fast path for that loop."""
+    import numpy as np
+
+    pts = circle_points(16)
+    loop = lc.LoopGeometry.from_polyline(pts)
+    pts[0, 0] += 1.0                                # the caller's array is not aliased
+    assert loop.control_points[0, 0] != pts[0, 0]
+    with pytest.raises(ValueError):
+        loop.coeffs[0, 0, 2] += 3.0
+    with pytest.raises(ValueError):
+        loop.control_points[0] = 0.0
+    m = lc.CurveModel([loop, lc.LoopGeometry.from_polyline(circle_points(16, center=(5, 0, 0)))])
+    s1 = m.snapshot()
+    assert s1.poly
+    c = loop.coeffs.copy()
+    c[:, 0, 2] += 3.0
+    loop.coeffs = c                                  # reassignment: tracked
+    s2 = m.snapshot()
+    assert s2 is not s1 and not s2.poly
+    assert np.array_equal(s2.packed()[0][:16], c)
+    assert m.snapshot() is s2                        # and cached again
+
+
+def test_snapshot_poly_only_for_closed_from_polyline_loops():
+    import numpy as np
+
+    closed = lc.LoopGeometry.from_polyline(circle_points(8))
+    generic = lc.LoopGeometry(closed.coeffs, closed.t)          # polyline-shaped, but generic
+    assert lc.CurveModel([closed, closed]).snapshot().poly
+    assert not lc.CurveModel([closed, generic]).snapshot().poly
+    opened = lc.LoopGeometry.from_polyline(circle_points(8), closed=False)
+    assert not lc.CurveModel([closed, opened]).snapshot().poly
+    a, b = lc.CurveModel([closed, generic]).packed(), lc.CurveModel([closed, closed]).packed()
+    assert all(np.array_equal(x, y) for x, y in zip(a, b))
