@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define LC_ABI_VERSION 1
+#define LC_ABI_VERSION 2
 
 enum {
     LC_OK = 0,
@@ -49,7 +49,11 @@ enum {
 enum {
     LC_GAUSS_PHASE = 0, /* default: shared corner terms + turn-counted phase product */
     LC_GAUSS_ATAN = 1,  /* shared corner terms + one fused atan2 per segment pair   */
-    LC_GAUSS_REF = 2    /* reference formula per pair, no FMA, two atan2            */
+    LC_GAUSS_REF = 2,   /* reference formula per pair, no FMA, two atan2            */
+    LC_GAUSS_ANGLESUM = 3 /* the reference's "anglesum" variant (direct.py:75-134):
+                             lane per outer segment, phase product over the inner
+                             segments in order, one atan2 per outer segment;
+                             its work items differ (lc_prepare_gauss(mode))      */
 };
 
 /* Per-pair result flags (lc_evaluate_pairs flags_out). */
@@ -97,7 +101,7 @@ LC_API int lc_last_gauss_ms(lc_ctx *ctx, float *ms);
  * lc_gauss_reduce reduces all n_items partials per pair in fixed order and
  * copies raw/lk/flags (P each; any may be NULL) to the host. */
 LC_API int lc_stage_polylines(lc_ctx *ctx, const double *verts, const int64_t *vert_off, int64_t L,
-                       const int32_t *pairs, int64_t P, int64_t *n_items);
+                       const int32_t *pairs, int64_t P, int mode, int64_t *n_items);
 LC_API int lc_gauss_run(lc_ctx *ctx, int mode, int64_t item_begin, int64_t item_end, double *partials_dev);
 LC_API int lc_gauss_reduce(lc_ctx *ctx, const double *partials_dev, double *raw, int64_t *lk, uint8_t *flags);
 /* Duration of the last lc_gauss_run kernel (waits for it). */
@@ -157,8 +161,8 @@ LC_API int lc_discretize(lc_ctx *ctx, double xi, double epsilon, int max_passes,
 LC_API int lc_discretize_error(lc_ctx *ctx, int *kind, int *detail, int64_t *loops, int64_t cap,
                                int64_t *n_loops);
 LC_API int lc_get_polylines(lc_ctx *ctx, double *verts, int64_t *vert_off);
-/* Build the Gauss-sum work items for the device polylines + pair list. */
-LC_API int lc_prepare_gauss(lc_ctx *ctx, int64_t *n_items);
+/* Build the Gauss-sum work items of Gauss mode `mode` for the device polylines + pair list. */
+LC_API int lc_prepare_gauss(lc_ctx *ctx, int mode, int64_t *n_items);
 /* Gauss sum over the device polylines and pair list; results to the host. */
 LC_API int lc_evaluate_staged(lc_ctx *ctx, int mode, double *raw, int64_t *lk, uint8_t *flags);
 /* Whole device path on the resident model: PLS -> discretize -> items ->

@@ -26,7 +26,8 @@ LC_ERR_VALIDATION = 5
 GAUSS_PHASE = 0
 GAUSS_ATAN = 1
 GAUSS_REF = 2
-GAUSS_MODES = {"phase": GAUSS_PHASE, "atan": GAUSS_ATAN, "ref": GAUSS_REF}
+GAUSS_ANGLESUM = 3
+GAUSS_MODES = {"phase": GAUSS_PHASE, "atan": GAUSS_ATAN, "ref": GAUSS_REF}   # arithmetic forms of the "atan" variant
 
 FLAG_NAN = 1
 FLAG_AMBIGUOUS = 2
@@ -52,7 +53,8 @@ SIGNATURES = {
     "lc_link_direct": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64, ctypes.c_int, _vp]),
     "lc_segment_pair_lambda": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp]),
     "lc_last_gauss_ms": (ctypes.c_int, [_vp, _c_float_p]),
-    "lc_stage_polylines": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64, _c_int64_p]),
+    "lc_stage_polylines": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64, ctypes.c_int,
+                                           _c_int64_p]),
     "lc_gauss_run": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, _vp]),
     "lc_gauss_reduce": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "lc_gauss_event_ms": (ctypes.c_int, [_vp, _c_float_p]),
@@ -72,7 +74,7 @@ SIGNATURES = {
     "lc_discretize_error": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
                                             _vp, ctypes.c_int64, _c_int64_p]),
     "lc_get_polylines": (ctypes.c_int, [_vp, _vp, _vp]),
-    "lc_prepare_gauss": (ctypes.c_int, [_vp, _c_int64_p]),
+    "lc_prepare_gauss": (ctypes.c_int, [_vp, ctypes.c_int, _c_int64_p]),
     "lc_evaluate_staged": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, _vp]),
     "lc_run_pipeline": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_int,
                                         ctypes.c_int64, ctypes.c_int, _c_int64_p]),
@@ -346,14 +348,14 @@ class Context:
         _check(self.lib.lc_last_gauss_ms(self.handle, ctypes.byref(ms)))
         return ms.value
 
-    def stage_polylines(self, verts, vert_off, pairs):
+    def stage_polylines(self, verts, vert_off, pairs, mode=GAUSS_PHASE):
         verts = np.ascontiguousarray(verts, dtype=np.float64)
         vert_off = np.ascontiguousarray(vert_off, dtype=np.int64)
         pairs = np.ascontiguousarray(pairs, dtype=np.int32).reshape(-1, 2)
         n = ctypes.c_int64(0)
         with self.lock:
             _check(self.lib.lc_stage_polylines(self.handle, _ptr(verts), _ptr(vert_off), len(vert_off) - 1,
-                                               _ptr(pairs), pairs.shape[0], ctypes.byref(n)))
+                                               _ptr(pairs), pairs.shape[0], int(mode), ctypes.byref(n)))
         self._staged_pairs = pairs.shape[0]
         return n.value
 
@@ -490,10 +492,10 @@ class Context:
             _check(self.lib.lc_evaluate_staged(self.handle, int(mode), _ptr(raw), _ptr(lk), _ptr(flags)))
         return raw, lk, flags
 
-    def prepare_gauss(self):
+    def prepare_gauss(self, mode=GAUSS_PHASE):
         n = ctypes.c_int64(0)
         with self.lock:
-            _check(self.lib.lc_prepare_gauss(self.handle, ctypes.byref(n)))
+            _check(self.lib.lc_prepare_gauss(self.handle, int(mode), ctypes.byref(n)))
         return n.value
 
     def run_pipeline(self, excluded_keys, xi, epsilon, max_passes, max_subsegments, mode=GAUSS_PHASE):

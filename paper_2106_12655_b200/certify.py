@@ -27,7 +27,7 @@ import warnings
 import numpy as np
 
 from . import _native
-from .direct import gauss_mode
+from .direct import ds_mode, gauss_mode
 from .discretize import DiscretizationParams, raise_for_failure, split_polylines
 from .geometry import CurveModel, ValidationError
 from . import barneshut
@@ -243,7 +243,7 @@ def _sharded_gauss(ctx, mode, dist):
     """Gauss sum over this rank's item range + all-gather of partials + fixed-order reduce."""
     import torch
 
-    n_items = ctx.prepare_gauss()
+    n_items = ctx.prepare_gauss(mode)
     world, rank = dist.get_world_size(), dist.get_rank()
     b, e, per = item_range(n_items, rank, world)
     if dist.get_backend() != "nccl":
@@ -325,8 +325,9 @@ def device_step(ctx, xi, excl_keys, params, mode=None, timings=None):
     return pairs, raw, lk, flags
 
 
-def run_device_pipeline(model: CurveModel, excluded=(), params=None, timings=None, ctx=None, snapshot=None):
-    """Upload the packed model, then device_step.  Returns (pairs, raw, lk, flags, ctx)."""
+def run_device_pipeline(model: CurveModel, excluded=(), params=None, timings=None, ctx=None, snapshot=None,
+                        mode=None):
+    """Upload the model snapshot, then device_step.  Returns (pairs, raw, lk, flags, ctx)."""
     params = params or DiscretizationParams()
     ctx = ctx or _native.context()
     with ctx.session:
@@ -334,7 +335,8 @@ def run_device_pipeline(model: CurveModel, excluded=(), params=None, timings=Non
         upload(model, ctx, snapshot)
         if timings is not None:
             timings["upload"] = time.perf_counter() - t0
-        pairs, raw, lk, flags = device_step(ctx, model.xi, excluded_keys(excluded), params, timings=timings)
+        pairs, raw, lk, flags = device_step(ctx, model.xi, excluded_keys(excluded), params, mode=mode,
+                                            timings=timings)
         if timings is not None:
             timings.pop("upload", None)
     return pairs, raw, lk, flags, ctx
@@ -374,7 +376,7 @@ def _evaluate_pairs(polylines, pair_items, choice, threads, diagnostics):
     np.cumsum(counts, out=off[1:])
     verts = np.concatenate([p.vertices if hasattr(p, "vertices") else np.asarray(p, float) for p in polylines])
     pairs = np.asarray(sorted(pair_items), dtype=np.int32).reshape(-1, 2)
-    raw, lk, flags = _native.context().evaluate_pairs(verts, off, pairs, gauss_mode())
+    raw, lk, flags = _native.context().evaluate_pairs(verts, off, pairs, ds_mode((choice or KernelChoice()).ds_variant))
     _raise_for_flags(raw, flags)
     return {(int(i), int(j)): int(v) for (i, j), v in zip(pairs.tolist(), lk.tolist())}
 
@@ -459,7 +461,7 @@ def compute_linking_matrix(
         try:
             with ctx.session:   # the result views stay ours until copied into arr
                 pairs, raw, lk, flags, _ = run_device_pipeline(model, excluded, params, timings, ctx=ctx,
-                                                               snapshot=snap)
+                                                               snapshot=snap, mode=ds_mode(choice.ds_variant))
                 _raise_for_flags(raw, flags)
                 keep = lk != 0
                 arr = np.empty((int(keep.sum()), 3), dtype=np.int64)
@@ -513,7 +515,8 @@ def verify(
             ctx = _native.context()
             ctx.session.acquire()   # the result views stay ours through the diff
             try:
-                pairs, raw, lk, flags, _ = run_device_pipeline(model, excluded, params, ctx=ctx, snapshot=snap)
+                pairs, raw, lk, flags, _ = run_device_pipeline(model, excluded, params, ctx=ctx, snapshot=snap,
+                                                               mode=ds_mode(choice.ds_variant))
             except Exception:
                 ctx.session.release()
                 raise

@@ -139,7 +139,7 @@ int lc_evaluate_pairs(lc_ctx *ctx, const double *verts, const int64_t *vert_off,
             throw Error(LC_ERR_ARG, "lc_evaluate_pairs: bad arguments");
         ctx->pipe.upload_polylines(verts, vert_off, L);
         ctx->pipe.upload_pairs(pairs, P);
-        ctx->pipe.build_gauss_items();
+        ctx->pipe.build_gauss_items(mode);
         ctx->pipe.run_gauss(mode, 0, ctx->pipe.n_items, nullptr, ctx->ev0, ctx->ev1);
         ctx->pipe.reduce_pairs(nullptr);
         ctx->pipe.download_results(raw, lk, flags);
@@ -160,7 +160,7 @@ int lc_link_direct(lc_ctx *ctx, const double *loop1, int64_t n1, const double *l
         uint8_t fl = 0;
         ctx->pipe.upload_polylines(v.data(), off, 2);
         ctx->pipe.upload_pairs(pr, 1);
-        ctx->pipe.build_gauss_items();
+        ctx->pipe.build_gauss_items(mode);
         ctx->pipe.run_gauss(mode, 0, ctx->pipe.n_items, nullptr, ctx->ev0, ctx->ev1);
         ctx->pipe.reduce_pairs(nullptr);
         ctx->pipe.download_results(raw, &lk, &fl);
@@ -181,11 +181,11 @@ int lc_last_gauss_ms(lc_ctx *ctx, float *ms) {
 
 // Device-resident staging (bench / multi-GPU): upload once, run many times.
 int lc_stage_polylines(lc_ctx *ctx, const double *verts, const int64_t *vert_off, int64_t L,
-                       const int32_t *pairs, int64_t P, int64_t *n_items) {
+                       const int32_t *pairs, int64_t P, int mode, int64_t *n_items) {
     return guarded(ctx, [&] {
         ctx->pipe.upload_polylines(verts, vert_off, L);
         ctx->pipe.upload_pairs(pairs, P);
-        ctx->pipe.build_gauss_items();
+        ctx->pipe.build_gauss_items(mode);
         *n_items = ctx->pipe.n_items;
     });
 }
@@ -337,16 +337,16 @@ int lc_get_polylines(lc_ctx *ctx, double *verts, int64_t *vert_off) {
     return guarded(ctx, [&] { ctx->pipe.download_polylines(verts, vert_off); });
 }
 
-int lc_prepare_gauss(lc_ctx *ctx, int64_t *n_items) {
+int lc_prepare_gauss(lc_ctx *ctx, int mode, int64_t *n_items) {
     return guarded(ctx, [&] {
-        ctx->pipe.build_gauss_items();
+        ctx->pipe.build_gauss_items(mode);
         *n_items = ctx->pipe.n_items;
     });
 }
 
 int lc_evaluate_staged(lc_ctx *ctx, int mode, double *raw, int64_t *lk, uint8_t *flags) {
     return guarded(ctx, [&] {
-        ctx->pipe.build_gauss_items();
+        ctx->pipe.build_gauss_items(mode);
         ctx->pipe.run_gauss(mode, 0, ctx->pipe.n_items, nullptr, nullptr, nullptr);
         ctx->pipe.reduce_pairs(nullptr);
         ctx->pipe.download_results(raw, lk, flags);
@@ -399,7 +399,7 @@ int lc_run_pipeline(lc_ctx *ctx, const uint64_t *excluded_keys, int64_t n_excl, 
     rc = run_discretize_abi(ctx, xi, epsilon, max_passes, max_subsegments, &nv, &passes, true);
     if (rc != LC_OK) return rc;
     bool valid = true;
-    rc = guarded(ctx, [&] { valid = ctx->pipe.build_gauss_items_checked(); });
+    rc = guarded(ctx, [&] { valid = ctx->pipe.build_gauss_items_checked(mode); });
     if (rc != LC_OK) return rc;
     if (!valid) {   // deferred PolylineLoop validation failed (read back with n_items)
         g_last_error = "discretization failed (see lc_discretize_error)";

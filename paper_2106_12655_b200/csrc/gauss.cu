@@ -313,6 +313,68 @@ __device__ double lane_strip_ref(const double *__restrict__ X, const double *__r
     return acc;
 }
 
+// GAUSS_ANGLESUM: outer segment `row` of _link_angle_sum (direct.py:75-134) over
+// all inner segments in order, in the reference's operation order (explicit _rn:
+// no contraction, like numba fastmath=False).  The coordinates are scaled by an
+// exact power of two, which every operation here carries exactly (the crossing
+// decisions and the normalized phase are bitwise the unscaled ones).
+__device__ __forceinline__ double sgn_rs(double x, double y) {   // _sgn (direct.py:68-72)
+    return (y > 0.0 || (y == 0.0 && x < 0.0)) ? 1.0 : -1.0;
+}
+
+__device__ double lane_anglesum(const double *__restrict__ X, const double *__restrict__ Y,
+                                const double *__restrict__ Z, int64_t row_off, int row, int64_t col_off, int ncols) {
+#define S_(a, b) __dsub_rn(a, b)
+#define A_(a, b) __dadd_rn(a, b)
+#define M_(a, b) __dmul_rn(a, b)
+    const double kix = __ldg(X + row_off + row), kiy = __ldg(Y + row_off + row), kiz = __ldg(Z + row_off + row);
+    const double ki1x = __ldg(X + row_off + row + 1), ki1y = __ldg(Y + row_off + row + 1),
+                 ki1z = __ldg(Z + row_off + row + 1);
+    double xs = 1.0, ys = 0.0, s_prev = -1.0, lam = 0.0;
+    double ljx = __ldg(X + col_off), ljy = __ldg(Y + col_off), ljz = __ldg(Z + col_off);
+    for (int j = 0; j < ncols; ++j) {
+        const double lj1x = __ldg(X + col_off + j + 1), lj1y = __ldg(Y + col_off + j + 1),
+                     lj1z = __ldg(Z + col_off + j + 1);
+        const double ax = S_(ljx, kix), ay = S_(ljy, kiy), az = S_(ljz, kiz);
+        const double bx = S_(ljx, ki1x), by = S_(ljy, ki1y), bz = S_(ljz, ki1z);
+        const double cx = S_(lj1x, ki1x), cy = S_(lj1y, ki1y), cz = S_(lj1z, ki1z);
+        const double dx = S_(lj1x, kix), dy = S_(lj1y, kiy), dz = S_(lj1z, kiz);
+        const double an = __dsqrt_rn(A_(A_(M_(ax, ax), M_(ay, ay)), M_(az, az)));
+        const double bn = __dsqrt_rn(A_(A_(M_(bx, bx), M_(by, by)), M_(bz, bz)));
+        const double cn = __dsqrt_rn(A_(A_(M_(cx, cx), M_(cy, cy)), M_(cz, cz)));
+        const double dn = __dsqrt_rn(A_(A_(M_(dx, dx), M_(dy, dy)), M_(dz, dz)));
+        const double p = A_(A_(M_(ax, S_(M_(by, cz), M_(bz, cy))), M_(ay, S_(M_(bz, cx), M_(bx, cz)))),
+                            M_(az, S_(M_(bx, cy), M_(by, cx))));
+        const double ab = A_(A_(M_(ax, bx), M_(ay, by)), M_(az, bz));
+        const double bc = A_(A_(M_(bx, cx), M_(by, cy)), M_(bz, cz));
+        const double ca = A_(A_(M_(cx, ax), M_(cy, ay)), M_(cz, az));
+        const double ad = A_(A_(M_(ax, dx), M_(ay, dy)), M_(az, dz));
+        const double dc = A_(A_(M_(dx, cx), M_(dy, cy)), M_(dz, cz));
+        const double d1 = A_(A_(A_(M_(M_(an, bn), cn), M_(ab, cn)), M_(bc, an)), M_(ca, bn));
+        const double d2 = A_(A_(A_(M_(M_(an, dn), cn), M_(ad, cn)), M_(dc, an)), M_(ca, dn));
+        const double xp = S_(M_(d1, d2), M_(p, p));
+        const double yp = M_(p, A_(d1, d2));
+        const double s1 = sgn_rs(d1, p), sw = sgn_rs(xp, yp);
+        if (s1 * sgn_rs(d2, p) > 0.0 && s1 * sw < 0.0) lam = A_(lam, s1);
+        const double xpp = S_(M_(xs, xp), M_(ys, yp));
+        const double ypp = A_(M_(xs, yp), M_(ys, xp));
+        const double sn = sgn_rs(xpp, ypp);
+        if (sw * s_prev > 0.0 && sn * s_prev < 0.0) lam = A_(lam, s_prev);
+        s_prev = sn;
+        const double axp = fabs(xpp), ayp = fabs(ypp);
+        const double nrm = ayp > axp ? ayp : axp;   // Python max(a, b): b only if b > a
+        xs = __ddiv_rn(xpp, nrm);
+        ys = __ddiv_rn(ypp, nrm);
+        ljx = lj1x;
+        ljy = lj1y;
+        ljz = lj1z;
+    }
+    return A_(lam, __ddiv_rn(atan2(ys, xs), kTwoPi));
+#undef S_
+#undef A_
+#undef M_
+}
+
 __device__ __forceinline__ int64_t find_pair(const int64_t *__restrict__ item_off, int64_t P, int64_t it) {
     // largest p with item_off[p] <= it
     int64_t lo = 0, hi = P;   // item_off[P] > it
@@ -365,7 +427,10 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) gauss_items_kernel(
         const int c0 = (int)(c0l < g.ncols ? c0l : g.ncols);
         const int c1 = min(c0 + g.cl, g.ncols);
         double val = 0.0;
-        if (row0 < g.nrows && c0 < c1) {
+        if constexpr (MODE == GAUSS_ANGLESUM) {   // items of 32 whole rows: lane = row
+            const int row = (ir << 5) + lane;
+            if (row < g.nrows) val = lane_anglesum(X, Y, Z, g.row_off, row, g.col_off, g.ncols);
+        } else if (row0 < g.nrows && c0 < c1) {
             if (MODE == GAUSS_REF) {
                 val = lane_strip_ref(X, Y, Z, g.row_off, g.nrows, g.col_off, row0, c0, c1);
             } else if (KSM) {
@@ -388,7 +453,7 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) gauss_items_kernel(
 
 __global__ void pair_geom_kernel(const int32_t *__restrict__ pairs, int64_t P, const int64_t *__restrict__ dP,
                                  const int64_t *__restrict__ voff, PairGeom *__restrict__ pg,
-                                 int64_t *__restrict__ nitems) {
+                                 int64_t *__restrict__ nitems, bool seq) {
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p >= P) return;
     if (dP && p >= *dP) {   // fused path: capacity slots beyond the device pair count hold no items
@@ -396,7 +461,8 @@ __global__ void pair_geom_kernel(const int32_t *__restrict__ pairs, int64_t P, c
         return;
     }
     const int i = pairs[2 * p], j = pairs[2 * p + 1];
-    const PairGeom g = make_pair_geom(voff[i], voff[j], (int)(voff[i + 1] - voff[i] - 1), (int)(voff[j + 1] - voff[j] - 1));
+    const PairGeom g = make_pair_geom(voff[i], voff[j], (int)(voff[i + 1] - voff[i] - 1),
+                                      (int)(voff[j + 1] - voff[j] - 1), seq);
     pg[p] = g;
     nitems[p] = (int64_t)g.items_r * g.items_c;
 }
@@ -537,14 +603,14 @@ size_t build_items_scan_bytes(int64_t P) { return exclusive_scan_i64_tmp_bytes(P
 
 int64_t build_items(const int32_t *d_pairs, int64_t P, const int64_t *d_voff, PairGeom *d_pg,
                     int64_t *d_item_off, void *d_scan_tmp, size_t scan_tmp_bytes, cudaStream_t s, bool read_back,
-                    const int64_t *d_P) {
+                    const int64_t *d_P, bool seq) {
     if (P == 0) {
         LC_CUDA(cudaMemsetAsync(d_item_off, 0, sizeof(int64_t), s));
         return 0;
     }
     // nitems written into item_off[0..P), item_off[P] = 0, then in-place exclusive scan.
     LC_CUDA(cudaMemsetAsync(d_item_off + P, 0, sizeof(int64_t), s));
-    pair_geom_kernel<<<(unsigned)ceil_div(P, 256), 256, 0, s>>>(d_pairs, P, d_P, d_voff, d_pg, d_item_off);
+    pair_geom_kernel<<<(unsigned)ceil_div(P, 256), 256, 0, s>>>(d_pairs, P, d_P, d_voff, d_pg, d_item_off, seq);
     LC_CHECK_LAUNCH();
     exclusive_scan_i64(d_item_off, d_item_off, P + 1, d_scan_tmp, scan_tmp_bytes, s);
     if (!read_back) return -1;   // caller reads item_off[P] together with other results
@@ -562,23 +628,25 @@ void launch_gauss_items(int mode, const double *X, const double *Y, const double
     if (!counter_zeroed) LC_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s));
     using Kern = void (*)(const double *, const double *, const double *, const ItemRec *, int64_t, int64_t,
                           unsigned long long *, double *, const int64_t *, int, int, const int *);
-    // default phase kernel: 3 resident CTAs/SM (168 regs); modes 3-7 are A/B variants
+    // default phase kernel: 3 resident CTAs/SM (168 regs); modes 16-20 are A/B variants
     // (1 CTA/SM with 232 regs; 4 CTAs; row vertices in shared memory; 2 CTAs/SM)
-    static const Kern table[] = {gauss_items_kernel<GAUSS_PHASE, 3>, gauss_items_kernel<GAUSS_ATAN, 1>,
-                                 gauss_items_kernel<GAUSS_REF, 1>, gauss_items_kernel<GAUSS_PHASE, 1>,
-                                 gauss_items_kernel<GAUSS_PHASE, 4>, gauss_items_kernel<GAUSS_PHASE, 4, true>,
-                                 gauss_items_kernel<GAUSS_PHASE, 3, true>, gauss_items_kernel<GAUSS_PHASE, 2>};
-    if (mode < 0 || mode >= (int)(sizeof table / sizeof table[0])) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
-    const Kern fn = table[mode];
+    static const Kern table[] = {gauss_items_kernel<GAUSS_PHASE, 3>,       gauss_items_kernel<GAUSS_ATAN, 1>,
+                                 gauss_items_kernel<GAUSS_REF, 1>,         gauss_items_kernel<GAUSS_ANGLESUM, 4>,
+                                 gauss_items_kernel<GAUSS_PHASE, 1>,       gauss_items_kernel<GAUSS_PHASE, 4>,
+                                 gauss_items_kernel<GAUSS_PHASE, 4, true>, gauss_items_kernel<GAUSS_PHASE, 3, true>,
+                                 gauss_items_kernel<GAUSS_PHASE, 2>};
+    if (!gauss_mode_valid(mode)) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
+    const int slot = mode < GAUSS_AB_FIRST ? mode : mode - GAUSS_AB_FIRST + 4;
+    const Kern fn = table[slot];
     constexpr int kModes = (int)(sizeof table / sizeof table[0]);
     static int occ[kModes] = {};   // resident CTAs per SM, queried once per mode
     const int threads = 128;
-    if (!occ[mode]) {
+    if (!occ[slot]) {
         int per = 0;
         LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void *)fn, threads, 0));
-        occ[mode] = per < 1 ? 1 : per;
+        occ[slot] = per < 1 ? 1 : per;
     }
-    const int per_sm = occ[mode];
+    const int per_sm = occ[slot];
     const int64_t warps_needed = item_end - item_begin;
     int64_t blocks = (int64_t)num_sms() * per_sm;
     const int64_t blocks_needed = ceil_div(warps_needed, threads / 32);

@@ -14,7 +14,21 @@ namespace lc {
 //   GAUSS_REF   : the reference formula evaluated per pair from scratch with
 //                 no FMA contraction and two atan2 (direct.py:19-46); used to
 //                 freeze F_pair and as a numerics cross-check.
-enum GaussMode : int { GAUSS_PHASE = 0, GAUSS_ATAN = 1, GAUSS_REF = 2, GAUSS_PHASE_OCC3 = 3, GAUSS_PHASE_OCC4 = 4 };
+//   GAUSS_ANGLESUM : the reference's "anglesum" variant (_link_angle_sum,
+//                 direct.py:75-134): one lane per outer segment walks every
+//                 inner segment in order, accumulating the normalized phase
+//                 product with its half-plane crossing counts, one atan2 per
+//                 outer segment; reference operation order, no contraction.
+//   16..20      : A/B builds of the phase kernel (occupancy / shared-memory
+//                 variants; tools/kbench.py), not part of the ABI.
+enum GaussMode : int { GAUSS_PHASE = 0, GAUSS_ATAN = 1, GAUSS_REF = 2, GAUSS_ANGLESUM = 3, GAUSS_AB_FIRST = 16,
+                       GAUSS_AB_LAST = 20 };
+
+inline bool gauss_mode_valid(int mode) {
+    return (mode >= GAUSS_PHASE && mode <= GAUSS_ANGLESUM) || (mode >= GAUSS_AB_FIRST && mode <= GAUSS_AB_LAST);
+}
+// Modes whose work items are whole outer segments (32 per item, all inner segments in order).
+inline bool gauss_mode_sequential(int mode) { return mode == GAUSS_ANGLESUM; }
 
 #ifndef LC_ROWS
 #define LC_ROWS 4
@@ -43,12 +57,22 @@ struct ItemRec {
 
 // Tiling of pair (column loop i, row loop j) from the two loops' closed-vertex
 // offsets and segment counts (one definition for every path that builds items).
-__host__ __device__ inline PairGeom make_pair_geom(int64_t col_off, int64_t row_off, int ncols, int nrows) {
+// seq: items of the sequential (anglesum) modes — 32 whole rows per item, one per lane.
+__host__ __device__ inline PairGeom make_pair_geom(int64_t col_off, int64_t row_off, int ncols, int nrows,
+                                                   bool seq = false) {
     PairGeom g;
     g.col_off = col_off;
     g.row_off = row_off;
     g.ncols = ncols;
     g.nrows = nrows;
+    if (seq) {
+        g.rb_log2 = 5;
+        g.cl = ncols > 0 ? ncols : 1;
+        g.items_r = (nrows + 31) / 32;
+        g.items_c = 1;
+        if (nrows <= 0 || ncols <= 0) g.items_r = g.items_c = 0;
+        return g;
+    }
     const int nb = (nrows + kRowsPerLane - 1) / kRowsPerLane;
     int rbl = 0;
     while ((1 << rbl) < nb && rbl < 5) ++rbl;
@@ -69,7 +93,7 @@ __host__ __device__ inline PairGeom make_pair_geom(int64_t col_off, int64_t row_
 // capacity slots past it get no items (item_off[P] is still the total).
 int64_t build_items(const int32_t *d_pairs, int64_t P, const int64_t *d_voff, PairGeom *d_pg,
                     int64_t *d_item_off, void *d_scan_tmp, size_t scan_tmp_bytes, cudaStream_t s,
-                    bool read_back = true, const int64_t *d_P = nullptr);
+                    bool read_back = true, const int64_t *d_P = nullptr, bool seq = false);
 size_t build_items_scan_bytes(int64_t P);
 
 // Evaluates items [item_begin, item_end) into partials[item] (absolute index).

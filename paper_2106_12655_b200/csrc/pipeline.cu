@@ -496,27 +496,31 @@ void Pipeline::download_pairs(int32_t *pairs) {
     LC_CUDA(cudaStreamSynchronize(s));
 }
 
-void Pipeline::build_gauss_items() {
+void Pipeline::build_gauss_items(int mode) {
     if (!polylines_ready) throw Error(LC_ERR_STATE, "no polylines staged");
+    if (!gauss_mode_valid(mode)) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
+    items_seq = gauss_mode_sequential(mode);
     d_pg.reserve(sizeof(PairGeom) * (size_t)(P > 0 ? P : 1), s);
     d_item_off.reserve(sizeof(int64_t) * (size_t)(P + 1), s);
     const size_t scan_bytes = build_items_scan_bytes(P > 0 ? P : 1);
     d_scan.reserve(scan_bytes, s);
     d_counter.reserve(sizeof(unsigned long long), s);
     n_items = build_items(d_pairs.as<int32_t>(), P, gvoff, d_pg.as<PairGeom>(), d_item_off.as<int64_t>(), d_scan.ptr,
-                          d_scan.bytes, s);
+                          d_scan.bytes, s, true, nullptr, items_seq);
     finish_items();
 }
 
-bool Pipeline::build_gauss_items_checked() {
+bool Pipeline::build_gauss_items_checked(int mode) {
     if (!polylines_ready) throw Error(LC_ERR_STATE, "no polylines staged");
+    if (!gauss_mode_valid(mode)) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
+    items_seq = gauss_mode_sequential(mode);
     d_pg.reserve(sizeof(PairGeom) * (size_t)(P > 0 ? P : 1), s);
     d_item_off.reserve(sizeof(int64_t) * (size_t)(P + 1), s);
     const size_t scan_bytes = build_items_scan_bytes(P > 0 ? P : 1);
     d_scan.reserve(scan_bytes, s);
     d_counter.reserve(sizeof(unsigned long long), s);
     build_items(d_pairs.as<int32_t>(), P, gvoff, d_pg.as<PairGeom>(), d_item_off.as<int64_t>(), d_scan.ptr,
-                d_scan.bytes, s, false);
+                d_scan.bytes, s, false, nullptr, items_seq);
     int ve[2] = {INT_MAX, INT_MAX};
     n_items = 0;
     LC_CUDA(cudaMemcpyAsync(&n_items, d_item_off.as<int64_t>() + P, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -545,7 +549,9 @@ void Pipeline::finish_items() {
 
 void Pipeline::run_gauss(int mode, int64_t item_begin, int64_t item_end, double *partials_ext,
                          cudaEvent_t ev0, cudaEvent_t ev1) {
-    if (mode < GAUSS_PHASE || mode > 7) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
+    if (!gauss_mode_valid(mode)) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
+    if (gauss_mode_sequential(mode) != items_seq)
+        throw Error(LC_ERR_STATE, "the work items were built for another Gauss-sum mode");
     double *out = partials_ext ? partials_ext : d_partials.as<double>();
     LC_CUDA(cudaEventRecord(ev0 ? ev0 : ev[EV_GAUSS0], s));
     launch_gauss_items(mode, gX, gY, gZ, d_item_pair.as<ItemRec>(),
@@ -596,7 +602,8 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
     if (!model_ready || L < 2 || M == 0 || prm.max_passes < 1 || max_loop > 256 ||
         (int64_t)kRowSlots * L >= (int64_t(1) << 24))   // the packed row scan holds P in 24 bits
         return FAST_FALLBACK;
-    if (mode < GAUSS_PHASE || mode > 7) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
+    if (!gauss_mode_valid(mode)) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
+    if (gauss_mode_sequential(mode)) return FAST_FALLBACK;   // the anglesum variant: staged path (own item tiling)
     // pair capacity: the grid PLS bound (16 per row) until a run has shown the
     // model's pair count; then that plus headroom (smaller grids and scans)
     int64_t pcap = (int64_t)kRowSlots * L;
@@ -800,6 +807,7 @@ int Pipeline::finish_fast() {
     // the run was the reference's: adopt its sizes as the pipeline state
     P = f.P;
     n_items = f.n_items;
+    items_seq = false;
     V = dout.V;
     Vc = dout.Vc;
     gX = dout.X.as<double>();

@@ -93,10 +93,12 @@ struct Pipeline {
     void upload_polylines(const double *verts, const int64_t *vert_off, int64_t nloops);
     void upload_pairs(const int32_t *pairs, int64_t npairs);
     void download_pairs(int32_t *pairs);
-    void build_gauss_items();
+    // items for Gauss mode `mode` (the sequential anglesum mode has its own tiling)
+    void build_gauss_items(int mode = GAUSS_PHASE);
     // build items and read back n_items together with a deferred discretize
     // validation result (one sync); false + derr on a ValidationError
-    bool build_gauss_items_checked();
+    bool build_gauss_items_checked(int mode = GAUSS_PHASE);
+    bool items_seq = false;   // the current items are whole-row (sequential-mode) items
     void run_gauss(int mode, int64_t item_begin, int64_t item_end, double *partials_ext, cudaEvent_t ev0,
                    cudaEvent_t ev1);
     void reduce_pairs(const double *partials_ext);

@@ -1,11 +1,14 @@
 """Gauss linking integral by exact segment-pair summation — on the GPU.
 
-Drop-in for linkcert.direct (direct.py:137-166).  Both reference variants
-("atan": one signed-solid-angle arctangent pair per segment pair;
-"anglesum": accumulated phase products) compute the same real number; here
-both run on the sm_100a Gauss-sum kernel (csrc/gauss.cu).  The kernel's
-arithmetic form is selected by LINKCERT_GAUSS_MODE (phase | atan | ref,
-default phase); all three agree with the reference to ~1e-14.
+Drop-in for linkcert.direct (direct.py:137-166).  Both reference variants run
+on the sm_100a Gauss-sum kernel (csrc/gauss.cu):
+* "atan" (one signed-solid-angle arctangent pair per segment pair,
+  direct.py:19-65) in the arithmetic form selected by LINKCERT_GAUSS_MODE
+  (phase | atan | ref, default phase); all three agree with the reference to
+  ~1e-14;
+* "anglesum" (_link_angle_sum, direct.py:68-134) as the reference computes it:
+  GAUSS_ANGLESUM, one lane per outer segment walking the inner segments in
+  order with the reference's normalized phase product and crossing counts.
 """
 
 from __future__ import annotations
@@ -27,6 +30,15 @@ def gauss_mode():
         raise ValueError(f"LINKCERT_GAUSS_MODE must be one of {sorted(_native.GAUSS_MODES)}, got {name!r}") from None
 
 
+def ds_mode(variant="atan"):
+    """Gauss-kernel mode of a direct-summation variant (KernelChoice.ds_variant)."""
+    if variant == "anglesum":
+        return _native.GAUSS_ANGLESUM
+    if variant != "atan":
+        raise ValueError(f"unknown direct-summation variant {variant!r}")
+    return gauss_mode()
+
+
 def _vertices(loop):
     verts = loop.vertices if hasattr(loop, "vertices") else np.asarray(loop, dtype=np.float64)
     return np.ascontiguousarray(verts, dtype=np.float64)
@@ -40,6 +52,5 @@ def segment_pair_lambda(l_j, l_j1, k_i, k_i1) -> float:
 
 def link_direct(loop1, loop2, variant="atan") -> float:
     """Real-valued linking number of two closed polylines (direct.py:149-161)."""
-    if variant not in VARIANTS:
-        raise ValueError(f"unknown direct-summation variant {variant!r}")
-    return float(_native.context().link_direct(_vertices(loop1), _vertices(loop2), gauss_mode()))
+    mode = ds_mode(variant)
+    return float(_native.context().link_direct(_vertices(loop1), _vertices(loop2), mode))

@@ -41,7 +41,7 @@ def test_ctypes_table_matches_header():
 
 
 def test_abi_version(lib):
-    assert lib.lc_abi_version() == 1
+    assert lib.lc_abi_version() == 2
 
 
 def test_no_device_means_loud_failure():
