@@ -179,34 +179,50 @@ LC_API int lc_get_results(lc_ctx *ctx, double *raw, int64_t *lk, uint8_t *flags)
  * memory: pairs int32 (P,2), raw f64 (P), lk int64 (P), flags u8 (P).  Valid
  * until the next pipeline call on this context. */
 LC_API int lc_result_views(lc_ctx *ctx, void **pairs, void **raw, void **lk, void **flags, int64_t *n_pairs);
-/* Sharded fused run (one process per GPU, all ranks on the same model):
- * as lc_run_pipeline, but the Gauss kernel evaluates only item slice `shard`
- * (ceil(n_items / shards) items) into the library's device partials buffer
- * (*partials_dev, indexed by absolute item id).  The caller all-gathers the
- * slices (NCCL) into one array and calls lc_shard_reduce; results then come
- * from lc_result_views.  *n_items = -1: the model needs the staged path
- * (lc_potential_link_search / lc_discretize / lc_prepare_gauss / lc_gauss_run). */
-LC_API int lc_run_pipeline_shard(lc_ctx *ctx, const uint64_t *excluded_keys, int64_t n_excl, double xi,
-                                 double epsilon, int max_passes, int64_t max_subsegments, int mode, int shard,
-                                 int shards, int64_t *n_pairs, int64_t *n_items, double **partials_dev);
-/* Fixed-order per-pair reduction of the gathered partials of a sharded run
- * (bitwise the single-GPU sums) + results into pinned memory. */
-/* Multi-GPU without a host round trip between the sum and the exchange:
+/* ---- Multi-GPU: one process per GPU, all ranks on the same model ----
+ * The reference has no distribution (certify.py:117-119 fans pairs over a
+ * GIL-bound thread pool); this is the B200 replacement of that fan-out, the
+ * multi-device contract of SURVEY §8(b)/(e).  The work-item list is split by
+ * COST (segment pairs, lc_shard_bounds) over the ranks; the small per-item
+ * partials vector is exchanged in place by an NCCL int64 MAX all-reduce (items
+ * of other ranks hold the bits of -0.0) and reduced per pair in a fixed order,
+ * so results are bitwise those of one GPU for any world size.
+ *
+ * Library-owned communicator (no torch.distributed needed):
+ *   rank 0: lc_comm_unique_id(id)  -> move the 128 bytes to every rank
+ *   every rank: lc_comm_init(ctx, id, world, rank) on its own device's context
+ *   every step: lc_model_upload* + lc_run_pipeline_sharded -> lc_result_views
+ * NCCL is loaded at run time (the copy already in the process, else
+ * libnccl.so.2).  lc_nccl_version: the loaded NCCL's version code, 0 if none. */
+LC_API int lc_nccl_version(void);
+LC_API int lc_comm_unique_id(char *id_out /* 128 bytes */);
+LC_API int lc_comm_init(lc_ctx *ctx, const char *id /* 128 bytes */, int world, int rank);
+LC_API int lc_comm_destroy(lc_ctx *ctx);
+/* lc_run_pipeline over the communicator: fused single-sync run of this rank's
+ * item range with the exchange enqueued behind it on the context stream, or
+ * (refinement / sweep PLS / anglesum) the staged path with the same split.
+ * Every rank gets the full results (lc_result_views); same return codes. */
+LC_API int lc_run_pipeline_sharded(lc_ctx *ctx, const uint64_t *excluded_keys, int64_t n_excl, double xi,
+                                   double epsilon, int max_passes, int64_t max_subsegments, int mode,
+                                   int64_t *n_pairs);
+/* Cost-balanced item ranges of the current work items (after lc_prepare_gauss /
+ * lc_stage_polylines): bounds[0..shards], rank r owns [bounds[r], bounds[r+1]),
+ * each range's segment-pair cost within one item of total / shards. */
+LC_API int lc_shard_bounds(lc_ctx *ctx, int shards, int64_t *bounds);
+/* The same exchange with a caller-owned collective (e.g. torch.distributed):
  * lc_run_pipeline_shard_async enqueues the fused run of shard `shard` of
- * `shards` (>= 1) on the context stream and returns at once with the library's
- * item-partials buffer (*part_cap doubles; *part_cap = 0: the model needs the
- * staged path).  Items of other shards hold the bits of -0.0, so an in-place
- * int64 MAX all-reduce of that buffer over the ranks (NCCL, enqueued on the
- * context stream: lc_get_stream) assembles every shard's partials bit-exactly.
- * lc_shard_finish then enqueues the fixed-order reduction and the export and
- * syncs once; *fused = 1: results ready (lc_result_views), 0: run the staged
- * path; LC_ERR_VALIDATION as lc_run_pipeline. */
+ * `shards` (>= 1, cost-balanced ranges) on the context stream and returns at
+ * once with the library's item-partials buffer (*part_cap int64 words;
+ * *part_cap = 0: the model needs the staged path).  The caller enqueues an
+ * in-place int64 MAX all-reduce of that buffer on the context stream
+ * (lc_get_stream); lc_shard_finish then enqueues the fixed-order reduction and
+ * the export and syncs once; *fused = 1: results ready (lc_result_views), 0:
+ * run the staged path; LC_ERR_VALIDATION as lc_run_pipeline. */
 LC_API int lc_run_pipeline_shard_async(lc_ctx *ctx, const uint64_t *excluded_keys, int64_t n_excl, double xi,
                                        double epsilon, int max_passes, int64_t max_subsegments, int mode, int shard,
                                        int shards, double **partials_dev, int64_t *part_cap);
 LC_API int lc_shard_finish(lc_ctx *ctx, int *fused);
 LC_API int lc_get_stream(lc_ctx *ctx, void **stream);
-LC_API int lc_shard_reduce(lc_ctx *ctx, const double *partials_all_dev);
 /* Path of the last lc_run_pipeline: 0 staged, 1 fused, 2 fused replayed from
  * the captured CUDA graph (same shape as the previous run, no reallocation). */
 LC_API int lc_last_run_fused(lc_ctx *ctx);

@@ -88,15 +88,17 @@ SIGNATURES = {
     "lc_last_run_fused": (ctypes.c_int, [_vp]),
     "lc_host_alloc": (_vp, [ctypes.c_int64]),
     "lc_host_free": (None, [_vp]),
-    "lc_run_pipeline_shard": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_int,
-                                             ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
-                                             ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
-                                             ctypes.POINTER(_vp)]),
-    "lc_shard_reduce": (ctypes.c_int, [_vp, _vp]),
     "lc_run_pipeline_shard_async": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
                                                    ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                                    ctypes.c_int, ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_int64)]),
     "lc_shard_finish": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int)]),
+    "lc_nccl_version": (ctypes.c_int, []),
+    "lc_comm_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
+    "lc_comm_init": (ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_int, ctypes.c_int]),
+    "lc_comm_destroy": (ctypes.c_int, [_vp]),
+    "lc_run_pipeline_sharded": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                                                ctypes.c_int, ctypes.c_int64, ctypes.c_int, _c_int64_p]),
+    "lc_shard_bounds": (ctypes.c_int, [_vp, ctypes.c_int, _vp]),
     "lc_get_stream": (ctypes.c_int, [_vp, ctypes.POINTER(_vp)]),
     "lc_float_repr_many": (ctypes.c_int64, [_vp, ctypes.c_int64, ctypes.c_int, _vp, ctypes.c_int64]),
     "lc_model_digest": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p]),
@@ -139,6 +141,19 @@ def model_digest_polylines(vptrs, loop_off, nthreads=0):
     if rc == -2:
         raise NativeError(LC_ERR_ARG, "lc_model_digest_polylines: null loop pointer")
     return None if rc != 0 else out.value.decode()
+
+
+def comm_unique_id():
+    """128-byte NCCL unique id for a new library communicator (call on rank 0)."""
+    out = ctypes.create_string_buffer(128)
+    rc = load_library().lc_comm_unique_id(out)
+    if rc != LC_OK:
+        raise NativeError(rc, load_library().lc_last_error().decode(errors="replace"))
+    return out.raw
+
+
+def nccl_version():
+    return int(load_library().lc_nccl_version())
 
 
 def sha256_hex(data, force_portable=False):
@@ -520,21 +535,6 @@ class Context:
             _check(self.lib.lc_get_results(self.handle, _ptr(raw), _ptr(lk), _ptr(flags)))
         return raw, lk, flags
 
-    def run_pipeline_shard(self, excluded_keys, xi, epsilon, max_passes, max_subsegments, mode, shard, shards):
-        """Fused run evaluating Gauss-sum item slice `shard` of `shards`; returns
-        (n_items, device pointer of the partials) or None when the staged path must run."""
-        ex = np.ascontiguousarray(excluded_keys if excluded_keys is not None else [], dtype=np.uint64)
-        n_pairs, n_items, ptr = ctypes.c_int64(0), ctypes.c_int64(-1), _vp()
-        with self.lock:
-            rc = self.lib.lc_run_pipeline_shard(self.handle, _ptr(ex), ex.size, float(xi), float(epsilon),
-                                                int(max_passes), int(max_subsegments), int(mode), int(shard),
-                                                int(shards), ctypes.byref(n_pairs), ctypes.byref(n_items),
-                                                ctypes.byref(ptr))
-            if rc in (LC_ERR_DISCRETIZE, LC_ERR_VALIDATION):
-                raise self._disc_error()
-            _check(rc)
-        return None if n_items.value < 0 else (n_items.value, ptr.value)
-
     def run_pipeline_shard_async(self, excluded_keys, xi, epsilon, max_passes, max_subsegments, mode, shard,
                                  shards):
         """Enqueue the fused run of item shard `shard` of `shards` (>= 2) without a
@@ -559,14 +559,43 @@ class Context:
             _check(rc)
         return bool(fused.value)
 
+    # ---- multi-GPU (library-owned NCCL communicator) ------------------------
+    def comm_init(self, unique_id, world, rank):
+        """Join the communicator `unique_id` (128 bytes from comm_unique_id() on rank 0)."""
+        with self.lock:
+            _check(self.lib.lc_comm_init(self.handle, bytes(unique_id), int(world), int(rank)))
+        self.comm = (int(world), int(rank))
+
+    def comm_destroy(self):
+        with self.lock:
+            _check(self.lib.lc_comm_destroy(self.handle))
+        self.comm = None
+
+    def run_pipeline_sharded(self, excluded_keys, xi, epsilon, max_passes, max_subsegments, mode=GAUSS_PHASE):
+        """run_pipeline over the communicator: this rank's cost-balanced share of the
+        Gauss sum, partials exchanged in the library; full results on every rank."""
+        ex = np.ascontiguousarray(excluded_keys if excluded_keys is not None else [], dtype=np.uint64)
+        n = ctypes.c_int64(0)
+        with self.lock:
+            rc = self.lib.lc_run_pipeline_sharded(self.handle, _ptr(ex), ex.size, float(xi), float(epsilon),
+                                                  int(max_passes), int(max_subsegments), int(mode), ctypes.byref(n))
+            if rc in (LC_ERR_DISCRETIZE, LC_ERR_VALIDATION):
+                raise self._disc_error()
+            _check(rc)
+        self._staged_pairs = n.value
+        return n.value
+
+    def shard_bounds(self, shards):
+        """Cost-balanced item ranges of the current work items: bounds (shards + 1)."""
+        out = np.zeros(int(shards) + 1, dtype=np.int64)
+        with self.lock:
+            _check(self.lib.lc_shard_bounds(self.handle, int(shards), _ptr(out)))
+        return out
+
     def stream_ptr(self):
         out = _vp()
         _check(self.lib.lc_get_stream(self.handle, ctypes.byref(out)))
         return out.value or 0
-
-    def shard_reduce(self, partials_all_ptr):
-        with self.lock:
-            _check(self.lib.lc_shard_reduce(self.handle, _vp(partials_all_ptr)))
 
     def last_run_fused(self):
         """Path of the last run_pipeline: 0 staged, 1 fused, 2 fused graph replay."""

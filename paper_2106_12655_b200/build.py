@@ -14,10 +14,11 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "liblinkcert_b200.so"
-SOURCES = ["abi.cu", "pipeline.cu", "gauss.cu", "pls.cu", "discretize.cu", "bh.cu", "probe.cu", "digest.cpp"]
+SOURCES = ["abi.cu", "pipeline.cu", "gauss.cu", "pls.cu", "discretize.cu", "bh.cu", "probe.cu", "comm.cu", "digest.cpp"]
 # bh.cu reproduces the reference numba arithmetic (no FMA contraction) operation by operation
 EXTRA_FLAGS = {"bh.cu": ["-fmad=false"]}
-HEADERS = ["common.cuh", "gauss.cuh", "pipeline.cuh", "pls.cuh", "discretize.cuh", "geom.cuh", "scan.cuh", "bh.cuh"]
+HEADERS = ["common.cuh", "gauss.cuh", "pipeline.cuh", "pls.cuh", "discretize.cuh", "geom.cuh", "scan.cuh", "bh.cuh",
+           "comm.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 NVCC_FLAGS = [
@@ -93,7 +94,7 @@ def build(force: bool = False, verbose: bool = False, variant: str = "", defines
         raise RuntimeError(f"nvcc failed:\n{msg}")
     tmp = lib.with_suffix(".so.tmp")
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static",
-           *map(str, objs), "-o", str(tmp)]
+           *map(str, objs), "-ldl", "-o", str(tmp)]
     subprocess.run(cmd, check=True)
     os.replace(tmp, lib)
     return lib

@@ -9,12 +9,14 @@ pair on the device and then replays the reference's evaluation order on
 the host, which yields the identical report because the per-pair integers
 are identical.
 
-Multi-GPU: when torch.distributed is initialized with world_size > 1, every
-rank runs the fused single-sync pipeline with the Gauss kernel restricted to
-its contiguous slice of the work items (sized on the device), the per-item
-partial sums are all-gathered (NCCL over NVLink; gloo in CPU tests of the
-staged fallback) and every rank reduces them in fixed order, so raw sums are
-bitwise identical for any number of ranks.
+Multi-GPU: when torch.distributed is initialized with world_size > 1 (NCCL),
+every rank runs the pipeline with the Gauss kernel restricted to its
+cost-balanced range of the work items (computed on the device); the per-item
+partials are exchanged over the library's own NCCL communicator (an in-place
+int64 MAX all-reduce enqueued behind the kernels) and every rank reduces them
+in fixed order, so raw sums are bitwise identical for any number of ranks.
+torch.distributed only carries the communicator's unique id and the model
+digest, which rank 0 alone computes.
 """
 
 from __future__ import annotations
@@ -197,131 +199,70 @@ def _dist():
     return None
 
 
-def item_range(n_items, rank, world):
-    """Contiguous, balanced split of the global work-item list (items are near-equal cost)."""
-    per = -(-n_items // world) if world else n_items
-    b = min(n_items, rank * per)
-    return b, min(n_items, b + per), per
-
-
-class _DeviceArray:
-    """Zero-copy handle on a library-owned device buffer (torch.as_tensor reads
-    __cuda_array_interface__)."""
-
-    def __init__(self, ptr, n, typestr="<f8"):
-        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr, "data": (int(ptr), False),
-                                         "version": 3}
-
-
-def _fused_sharded_step(ctx, xi, excl_keys, params, mode, dist):
-    """Multi-GPU hot path with one host sync per rank: every rank enqueues the
-    fused pipeline on the same model with the Gauss kernel restricted to its
-    item slice (lc_run_pipeline_shard_async), the partials are assembled by an
-    in-place NCCL int64 MAX all-reduce enqueued on the library stream (items
-    of other ranks hold the bits of -0.0, the MAX identity here), and
-    lc_shard_finish reduces every pair in fixed order (bitwise the single-GPU
-    sums), exports and syncs.  None: the model needs the staged path (every
-    rank decides alike: same model, deterministic device summary)."""
-    import torch
-
+def ensure_comm(ctx, dist):
+    """The library's own NCCL communicator for this process group (created once):
+    rank 0 makes the unique id, torch.distributed only carries those 128 bytes."""
     world, rank = dist.get_world_size(), dist.get_rank()
-    got = ctx.run_pipeline_shard_async(excl_keys, xi, params.epsilon, params.max_passes, params.max_subsegments,
-                                       mode, rank, world)
-    if got is None:
-        return None
-    ptr, cap = got
-    dev = torch.device("cuda", ctx.device)
-    buf = torch.as_tensor(_DeviceArray(ptr, cap, "<i8"), device=dev)
-    with torch.cuda.stream(torch.cuda.ExternalStream(ctx.stream_ptr(), device=dev)):
-        dist.all_reduce(buf, op=dist.ReduceOp.MAX)
-    if not ctx.shard_finish():
-        return None
-    return ctx.result_views()
+    if getattr(ctx, "comm", None) == (world, rank):
+        return
+    obj = [_native.comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    ctx.comm_init(obj[0], world, rank)
 
 
-def _sharded_gauss(ctx, mode, dist):
-    """Gauss sum over this rank's item range + all-gather of partials + fixed-order reduce."""
-    import torch
+def digest_on_rank0(model, snapshot, dist):
+    """model_digest computed once per job: rank 0 hashes (helper thread, overlapped
+    with the GPU), the other ranks receive the string.  Returns a callable giving
+    the digest (or raising the digest's error) on every rank."""
+    if dist is None or dist.get_rank() == 0:
+        world = 1 if dist is None else dist.get_world_size()
+        fut = _digest_async(model, snapshot, nthreads=0 if world == 1 else max(2, (os.cpu_count() or 2) - world))
+    else:
+        fut = None
 
-    n_items = ctx.prepare_gauss(mode)
-    world, rank = dist.get_world_size(), dist.get_rank()
-    b, e, per = item_range(n_items, rank, world)
-    if dist.get_backend() != "nccl":
-        raise _native.NativeUnavailable("sharded Gauss sum needs the NCCL backend on CUDA devices")
-    dev = torch.device("cuda", ctx.device)
-    # the kernel writes partials[item] at absolute item ids: this rank's slice of `full`
-    full = torch.zeros(per * world, dtype=torch.float64, device=dev)
-    ctx.gauss_run(mode, b, e, full.data_ptr())
-    ctx.synchronize()
-    gathered = gather_item_partials(dist, full, rank, per)
-    torch.cuda.synchronize(dev)
-    return ctx.gauss_reduce(gathered.data_ptr())
+    def result():
+        if dist is None:
+            return fut.result()
+        obj = [None]
+        if fut is not None:
+            try:
+                obj[0] = ("ok", fut.result())
+            except Exception as exc:  # noqa: BLE001 - re-raised on every rank below
+                obj[0] = ("err", exc)
+        dist.broadcast_object_list(obj, src=0)
+        kind, val = obj[0]
+        if kind == "err":
+            raise val
+        return val
 
-
-def gather_item_partials(dist, full, rank, per):
-    """All ranks' contiguous item slices -> one array indexed by absolute item id.
-
-    `full` holds this rank's partials at [rank*per, (rank+1)*per); the result
-    is bitwise the single-GPU partial array (no arithmetic on the values), so
-    the fixed-order per-pair reduction that follows is world-size independent.
-    """
-    import torch
-
-    mine = full[rank * per:(rank + 1) * per].contiguous()
-    if dist.get_backend() == "nccl":
-        out = torch.empty_like(full)
-        dist.all_gather_into_tensor(out, mine)
-        return out
-    parts = [torch.empty_like(mine) for _ in range(dist.get_world_size())]
-    dist.all_gather(parts, mine)
-    return torch.cat(parts)
+    return result
 
 
 def device_step(ctx, xi, excl_keys, params, mode=None, timings=None):
     """One pass of the hot path over the model resident on `ctx`:
-    PLS -> discretize -> Gauss sum (sharded + all-gathered under torch.distributed).
-    Returns (pairs int32 (P,2), raw, lk, flags) on the host."""
+    PLS -> discretize -> Gauss sum -> rounding.  Under torch.distributed (NCCL,
+    world > 1) every rank evaluates its cost-balanced share of the work items
+    and the library exchanges the partials over its own NCCL communicator.
+    Returns (pairs int32 (P,2), raw, lk, flags) views in pinned host memory."""
     mode = gauss_mode() if mode is None else mode
     dist = _dist()
-    if dist is None:
-        # one C-ABI call for the whole device path; stage times from CUDA events
-        try:
-            ctx.run_pipeline(excl_keys, xi, params.epsilon, params.max_passes, params.max_subsegments, mode)
-        except _native.DiscretizeFailure as fail:
-            raise_for_failure(fail, params)
-        pairs, raw, lk, flags = ctx.result_views()   # pinned, valid until the next pipeline call
-        if timings is not None:
-            st = ctx.stage_times()
-            timings["pls"] = timings.get("upload", 0.0) + 1e-3 * st["pls"]
-            timings["discretize"] = 1e-3 * st["discretize"]
-            timings["kernel"] = 1e-3 * (st["gauss"] + st["reduce"])
-        return pairs, raw, lk, flags
-    if dist.get_backend() == "nccl":
-        try:
-            res = _fused_sharded_step(ctx, xi, excl_keys, params, mode, dist)
-        except _native.DiscretizeFailure as fail:
-            raise_for_failure(fail, params)
-        if res is not None:
-            if timings is not None:
-                st = ctx.stage_times()
-                timings["pls"] = timings.get("upload", 0.0) + 1e-3 * st["pls"]
-                timings["discretize"] = 1e-3 * st["discretize"]
-                timings["kernel"] = 1e-3 * st["gauss"]
-            return res
-    t0 = time.perf_counter()
-    ctx.potential_link_search(excl_keys)
-    t1 = time.perf_counter()
+    args = (excl_keys, xi, params.epsilon, params.max_passes, params.max_subsegments, mode)
+    if dist is not None and dist.get_backend() != "nccl":
+        raise _native.NativeUnavailable("the multi-GPU path needs the NCCL backend on CUDA devices")
     try:
-        ctx.discretize(xi, params.epsilon, params.max_passes, params.max_subsegments)
+        if dist is None:
+            ctx.run_pipeline(*args)          # one C-ABI call for the whole device path
+        else:
+            ensure_comm(ctx, dist)
+            ctx.run_pipeline_sharded(*args)
     except _native.DiscretizeFailure as fail:
         raise_for_failure(fail, params)
-    t2 = time.perf_counter()
-    raw, lk, flags = _sharded_gauss(ctx, mode, dist)
-    pairs = ctx.get_pairs()
+    pairs, raw, lk, flags = ctx.result_views()   # pinned, valid until the next pipeline call
     if timings is not None:
-        timings["pls"] = timings.get("upload", 0.0) + (t1 - t0)
-        timings["discretize"] = t2 - t1
-        timings["kernel"] = time.perf_counter() - t2
+        st = ctx.stage_times()
+        timings["pls"] = timings.get("upload", 0.0) + 1e-3 * st["pls"]
+        timings["discretize"] = 1e-3 * st["discretize"]
+        timings["kernel"] = 1e-3 * (st["gauss"] + st["reduce"])
     return pairs, raw, lk, flags
 
 
@@ -345,14 +286,14 @@ def run_device_pipeline(model: CurveModel, excluded=(), params=None, timings=Non
 _digest_pool = None
 
 
-def _digest_async(model, snapshot=None):
+def _digest_async(model, snapshot=None, nthreads=0):
     """model_digest on a helper thread (native, GIL released) to overlap it with the GPU."""
     global _digest_pool
     if _digest_pool is None:
         from concurrent.futures import ThreadPoolExecutor
 
         _digest_pool = ThreadPoolExecutor(max_workers=1, thread_name_prefix="linkcert-digest")
-    return _digest_pool.submit(model_digest, model, snapshot)
+    return _digest_pool.submit(model_digest, model, snapshot, nthreads)
 
 
 def _raise_for_flags(raw, flags, order=None):
@@ -456,7 +397,7 @@ def compute_linking_matrix(
         digest = model_digest(model)
     else:
         snap = model.snapshot()
-        fut = _digest_async(model, snap)
+        digest_of = digest_on_rank0(model, snap, _dist())
         ctx = _native.context()
         try:
             with ctx.session:   # the result views stay ours until copied into arr
@@ -468,9 +409,9 @@ def compute_linking_matrix(
                 arr[:, :2] = pairs[keep]
                 arr[:, 2] = lk[keep]
         except Exception:
-            fut.result()          # a serialization error would have surfaced last in the reference
+            digest_of()           # a serialization error would have surfaced last in the reference
             raise
-        digest = fut.result()
+        digest = digest_of()
     return LinkMatrix._from_array(model.num_loops, arr, digest, choice.tag, {})
 
 
@@ -501,7 +442,7 @@ def verify(
     # the digest (host, native) overlaps the device pipeline; its check and
     # warning come first, as in the reference (certify.py:188-193)
     snap = model.snapshot()
-    fut = _digest_async(model, snap)
+    digest_of = digest_on_rank0(model, snap, _dist())
     ctx = None
     try:
         if model.num_loops < 1:
@@ -521,7 +462,7 @@ def verify(
                 ctx.session.release()
                 raise
     except Exception:
-        _warn_digest(fut.result(), reference)
+        _warn_digest(digest_of(), reference)
         raise
     # the diff runs while the digest finishes; its outcome (report or error) is
     # delivered after the digest warning, the reference's order
@@ -532,7 +473,7 @@ def verify(
     finally:
         if ctx is not None:
             ctx.session.release()
-    _warn_digest(fut.result(), reference)
+    _warn_digest(digest_of(), reference)
     if err is not None:
         raise err
     return report

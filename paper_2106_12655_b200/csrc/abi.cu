@@ -4,11 +4,13 @@
 // crosses the ABI.  The library owns device buffers (grow-only, cached in the
 // context); callers own every host buffer they pass.  Calls on one context
 // are serialized by its mutex.
+#include <cstring>
 #include <mutex>
 #include <string>
 #include <vector>
 
 #include "bh.cuh"
+#include "comm.cuh"
 #include "gauss.cuh"
 #include "pipeline.cuh"
 
@@ -32,6 +34,7 @@ struct lc_ctx {
     int last_fused = 0;   // last lc_run_pipeline: 0 staged, 1 fused, 2 fused replayed as a CUDA graph
     DevBuf tb_coeffs, tb_t, tb_box, tb_loop, tb_off, tb_flag;   // lc_tight_boxes scratch
     BhScratch bh;                                                // Barnes-Hut traversal scratch
+    Comm comm;                                                   // multi-GPU communicator (lc_comm_init)
 };
 
 struct lc_bh_forest {
@@ -412,38 +415,6 @@ int lc_run_pipeline(lc_ctx *ctx, const uint64_t *excluded_keys, int64_t n_excl, 
     });
 }
 
-int lc_run_pipeline_shard(lc_ctx *ctx, const uint64_t *excluded_keys, int64_t n_excl, double xi, double epsilon,
-                          int max_passes, int64_t max_subsegments, int mode, int shard, int shards, int64_t *n_pairs,
-                          int64_t *n_items, double **partials_dev) {
-    *n_items = -1;
-    ctx->last_fused = 0;
-    ctx->pipe.derived_in_run = false;
-    int fr = FAST_FALLBACK;
-    const int g = guarded(ctx, [&] {
-        if (n_excl < 0 || (n_excl > 0 && !excluded_keys)) throw Error(LC_ERR_ARG, "bad excluded keys");
-        for (int64_t k = 1; k < n_excl; ++k)
-            if (excluded_keys[k] <= excluded_keys[k - 1]) throw Error(LC_ERR_ARG, "excluded keys must be sorted unique");
-        DiscParams prm;
-        prm.xi = xi;
-        prm.epsilon = epsilon;
-        prm.max_passes = max_passes;
-        prm.max_subsegments = max_subsegments;
-        fr = ctx->pipe.run_fast(excluded_keys, n_excl, prm, mode, shard, shards);
-        if (n_pairs) *n_pairs = ctx->pipe.P;
-        if (fr == FAST_OK) {
-            *n_items = ctx->pipe.n_items;
-            *partials_dev = ctx->pipe.d_partials.as<double>();
-        }
-    });
-    if (g != LC_OK) return g;
-    ctx->last_fused = fr == FAST_FALLBACK ? 0 : (ctx->pipe.last_fast_graph ? 2 : 1);
-    if (fr == FAST_INVALID) {
-        g_last_error = "discretization failed (see lc_discretize_error)";
-        return LC_ERR_VALIDATION;
-    }
-    return LC_OK;
-}
-
 int lc_run_pipeline_shard_async(lc_ctx *ctx, const uint64_t *excluded_keys, int64_t n_excl, double xi,
                                 double epsilon, int max_passes, int64_t max_subsegments, int mode, int shard,
                                 int shards, double **partials_dev, int64_t *part_cap) {
@@ -468,6 +439,119 @@ int lc_run_pipeline_shard_async(lc_ctx *ctx, const uint64_t *excluded_keys, int6
     });
 }
 
+// ---------------------------------------------------- multi-GPU (NCCL)
+
+int lc_nccl_version(void) { return nccl_version(); }
+
+int lc_comm_unique_id(char *id_out) {
+    try {
+        if (!id_out) throw Error(LC_ERR_ARG, "null id buffer");
+        ncclUniqueId id;
+        comm_unique_id(&id);
+        std::memcpy(id_out, id.internal, sizeof id.internal);
+        return LC_OK;
+    } catch (const Error &e) {
+        g_last_error = e.what();
+        return e.code;
+    }
+}
+
+int lc_comm_init(lc_ctx *ctx, const char *id, int world, int rank) {
+    return guarded(ctx, [&] {
+        if (!id) throw Error(LC_ERR_ARG, "null id");
+        ncclUniqueId u;
+        std::memcpy(u.internal, id, sizeof u.internal);
+        comm_init(ctx->comm, u, world, rank);
+        ctx->pipe.gather_share = world;
+    });
+}
+
+int lc_comm_destroy(lc_ctx *ctx) {
+    return guarded(ctx, [&] {
+        comm_destroy(ctx->comm);
+        ctx->pipe.gather_share = 1;
+    });
+}
+
+int lc_shard_bounds(lc_ctx *ctx, int shards, int64_t *bounds) {
+    return guarded(ctx, [&] {
+        if (!bounds) throw Error(LC_ERR_ARG, "null bounds");
+        ctx->pipe.shard_bounds(shards, bounds);
+    });
+}
+
+int lc_run_pipeline_sharded(lc_ctx *ctx, const uint64_t *excluded_keys, int64_t n_excl, double xi, double epsilon,
+                            int max_passes, int64_t max_subsegments, int mode, int64_t *n_pairs) {
+    ctx->last_fused = 0;
+    ctx->pipe.derived_in_run = false;
+    int world = 1, rank = 0;
+    const int gd = guarded(ctx, [&] {
+        if (!ctx->comm.ready()) throw Error(LC_ERR_STATE, "lc_run_pipeline_sharded needs lc_comm_init");
+        if (n_excl < 0 || (n_excl > 0 && !excluded_keys)) throw Error(LC_ERR_ARG, "bad excluded keys");
+        for (int64_t k = 1; k < n_excl; ++k)
+            if (excluded_keys[k] <= excluded_keys[k - 1]) throw Error(LC_ERR_ARG, "excluded keys must be sorted unique");
+        world = ctx->comm.world;
+        rank = ctx->comm.rank;
+    });
+    if (gd != LC_OK) return gd;
+    // fused single-sync run, this rank's cost-balanced item range; the partials
+    // exchange is enqueued right behind it on the same stream (no host round trip)
+    const char *fz = getenv("LINKCERT_FUSED");
+    if (!(fz && fz[0] == '0')) {
+        int fr = FAST_FALLBACK;
+        const int g = guarded(ctx, [&] {
+            DiscParams prm;
+            prm.xi = xi;
+            prm.epsilon = epsilon;
+            prm.max_passes = max_passes;
+            prm.max_subsegments = max_subsegments;
+            fr = ctx->pipe.run_fast(excluded_keys, n_excl, prm, mode, rank, world, true, true);
+            if (fr == FAST_PENDING) {
+                comm_allreduce_max_i64(ctx->comm, ctx->pipe.d_partials.ptr, (size_t)ctx->pipe.part_cap,
+                                       ctx->stream);
+                fr = ctx->pipe.shard_finish();
+            }
+            if (n_pairs) *n_pairs = ctx->pipe.P;
+        });
+        if (g != LC_OK) return g;
+        ctx->last_fused = fr == FAST_FALLBACK ? 0 : (ctx->pipe.last_fast_graph ? 2 : 1);
+        if (fr == FAST_OK) return LC_OK;
+        if (fr == FAST_INVALID) {
+            g_last_error = "discretization failed (see lc_discretize_error)";
+            return LC_ERR_VALIDATION;
+        }
+    }
+    // staged path (refinement, the sweep PLS, anglesum): every rank runs the same
+    // front end; the Gauss sum covers this rank's cost-balanced item range
+    if (!ctx->pipe.derived_in_run) {
+        const int g2 = guarded(ctx, [&] { ctx->pipe.derive(); });
+        if (g2 != LC_OK) return g2;
+    }
+    int rc = pls_abi(ctx, excluded_keys, n_excl, n_pairs, true);
+    if (rc != LC_OK) return rc;
+    int64_t nv = 0;
+    int passes = 0;
+    rc = run_discretize_abi(ctx, xi, epsilon, max_passes, max_subsegments, &nv, &passes, true);
+    if (rc != LC_OK) return rc;
+    bool valid = true;
+    rc = guarded(ctx, [&] { valid = ctx->pipe.build_gauss_items_checked(mode); });
+    if (rc != LC_OK) return rc;
+    if (!valid) {
+        g_last_error = "discretization failed (see lc_discretize_error)";
+        return LC_ERR_VALIDATION;
+    }
+    return guarded(ctx, [&] {
+        Pipeline &p = ctx->pipe;
+        std::vector<int64_t> b((size_t)world + 1);
+        p.shard_bounds(world, b.data());
+        p.prefill_partials_neg_zero(p.n_items);
+        p.run_gauss(mode, b[rank], b[rank + 1], nullptr, nullptr, nullptr);
+        comm_allreduce_max_i64(ctx->comm, p.d_partials.ptr, (size_t)p.n_items, ctx->stream);
+        p.reduce_pairs(nullptr);
+        p.download_results_pinned();
+    });
+}
+
 int lc_shard_finish(lc_ctx *ctx, int *fused) {
     if (fused) *fused = 0;
     int fr = FAST_FALLBACK;
@@ -489,9 +573,6 @@ int lc_get_stream(lc_ctx *ctx, void **stream) {
     });
 }
 
-int lc_shard_reduce(lc_ctx *ctx, const double *partials_all_dev) {
-    return guarded(ctx, [&] { ctx->pipe.shard_reduce(partials_all_dev); });
-}
 
 int lc_result_views(lc_ctx *ctx, void **pairs, void **raw, void **lk, void **flags, int64_t *n_pairs) {
     return guarded(ctx, [&] {

@@ -390,18 +390,15 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) gauss_items_kernel(
     const double *__restrict__ X, const double *__restrict__ Y, const double *__restrict__ Z,
     const ItemRec *__restrict__ items, int64_t item_begin, int64_t item_end, unsigned long long *__restrict__ counter,
     double *__restrict__ partials, const int64_t *__restrict__ d_end, int shard, int shards,
-    const int *__restrict__ abort) {
+    const int *__restrict__ abort, const int64_t *__restrict__ d_bounds) {
     __shared__ double ksh[KSM ? 3 * (R + 1) * kCtaThreads : 1];
     const int lane = threadIdx.x & 31;
-    if (d_end) {   // fused path: item count on the device; a shard takes its contiguous slice
+    if (d_bounds) {   // sharded fused path: this shard's cost-balanced item range (shard_bounds_kernel)
+        item_begin = d_bounds[shard];
+        item_end = d_bounds[shard + 1];
+    } else if (d_end) {   // fused path: item count on the device
         const int64_t n = *d_end;
-        if (shards > 1) {
-            const int64_t per = (n + shards - 1) / shards;
-            item_begin = (int64_t)shard * per < n ? (int64_t)shard * per : n;
-            item_end = item_begin + per < n ? item_begin + per : n;
-        } else if (n < item_end) {
-            item_end = n;
-        }
+        if (n < item_end) item_end = n;
     }
     for (;;) {
         unsigned long long k = 0;
@@ -557,7 +554,73 @@ __global__ void item_pair_fill_kernel(const int64_t *__restrict__ item_off, cons
     }
 }
 
+// Cost-balanced split of the item list over `shards` ranks: the cost
+// of pair p is nrows x ncols segment pairs; boundary k sits where the running
+// cost crosses floor(k * total / shards), inside pair p at item
+// item_off[p] + ceil((t_k - C_p) * items_p / cost_p) (items of a pair are
+// near-equal).  One block; bounds[0] = 0, bounds[shards] = the item count.
+__global__ void __launch_bounds__(1024) shard_bounds_kernel(const PairGeom *__restrict__ pg,
+                                                            const int64_t *__restrict__ item_off, int64_t Pcap,
+                                                            const int64_t *__restrict__ dP, int shards,
+                                                            int64_t *__restrict__ bounds) {
+    __shared__ int64_t wsum[32];
+    __shared__ int64_t s_total, s_carry;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    const int64_t P = dP && *dP < Pcap ? *dP : Pcap;
+    int64_t part = 0;
+    for (int64_t p = tid; p < P; p += blockDim.x) part += (int64_t)pg[p].nrows * pg[p].ncols;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (lane == 0) wsum[warp] = part;
+    __syncthreads();
+    if (tid == 0) {
+        int64_t t = 0;
+        for (int w = 0; w < nw; ++w) t += wsum[w];
+        s_total = t;
+        s_carry = 0;
+        const int64_t n = P > 0 ? item_off[P] : 0;
+        bounds[0] = 0;
+        for (int k = 1; k <= shards; ++k) bounds[k] = n;
+    }
+    __syncthreads();
+    const int64_t total = s_total;
+    for (int64_t base = 0; base < P; base += blockDim.x) {
+        const int64_t p = base + tid;
+        const int64_t c = p < P ? (int64_t)pg[p].nrows * pg[p].ncols : 0;
+        int64_t incl = c;   // inclusive block scan of the pair costs
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        __syncthreads();
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        int64_t before = 0;
+        for (int w = 0; w < warp; ++w) before += wsum[w];
+        const int64_t excl = s_carry + before + incl - c;
+        if (p < P && c > 0)
+            for (int k = 1; k < shards; ++k) {
+                const int64_t t = (int64_t)((__int128)total * k / shards);
+                if (excl <= t && t < excl + c) {
+                    const int64_t items_p = item_off[p + 1] - item_off[p];
+                    int64_t local = (int64_t)(((__int128)(t - excl) * items_p + c - 1) / c);
+                    bounds[k] = item_off[p] + (local < items_p ? local : items_p);
+                }
+            }
+        __syncthreads();
+        if (tid == blockDim.x - 1) s_carry += before + incl;
+        __syncthreads();
+    }
+}
+
 }  // namespace
+
+void launch_shard_bounds(const PairGeom *pg, const int64_t *item_off, int64_t Pcap, const int64_t *d_P, int shards,
+                         int64_t *bounds, cudaStream_t s) {
+    shard_bounds_kernel<<<1, 1024, 0, s>>>(pg, item_off, Pcap, d_P, shards, bounds);
+    LC_CHECK_LAUNCH();
+}
 
 void launch_item_pairs_dev(const int64_t *item_off, const PairGeom *pg, int64_t P_cap, const int64_t *d_P,
                            int64_t cap_items, ItemRec *items, cudaStream_t s) {
@@ -623,11 +686,12 @@ int64_t build_items(const int32_t *d_pairs, int64_t P, const int64_t *d_voff, Pa
 void launch_gauss_items(int mode, const double *X, const double *Y, const double *Z, const ItemRec *items,
                         int64_t item_begin,
                         int64_t item_end, unsigned long long *counter, double *partials, cudaStream_t s,
-                        const int64_t *d_end, int shard, int shards, const int *abort, bool counter_zeroed) {
+                        const int64_t *d_end, int shard, int shards, const int *abort, bool counter_zeroed,
+                        const int64_t *d_bounds) {
     if (item_end <= item_begin) return;
     if (!counter_zeroed) LC_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s));
     using Kern = void (*)(const double *, const double *, const double *, const ItemRec *, int64_t, int64_t,
-                          unsigned long long *, double *, const int64_t *, int, int, const int *);
+                          unsigned long long *, double *, const int64_t *, int, int, const int *, const int64_t *);
     // default phase kernel: 3 resident CTAs/SM (168 regs); modes 16-20 are A/B variants
     // (1 CTA/SM with 232 regs; 4 CTAs; row vertices in shared memory; 2 CTAs/SM)
     static const Kern table[] = {gauss_items_kernel<GAUSS_PHASE, 3>,       gauss_items_kernel<GAUSS_ATAN, 1>,
@@ -652,7 +716,7 @@ void launch_gauss_items(int mode, const double *X, const double *Y, const double
     const int64_t blocks_needed = ceil_div(warps_needed, threads / 32);
     if (blocks > blocks_needed) blocks = blocks_needed;
     fn<<<(unsigned)blocks, threads, 0, s>>>(X, Y, Z, items, item_begin, item_end, counter, partials, d_end, shard,
-                                            shards, abort);
+                                            shards, abort, d_bounds);
     LC_CHECK_LAUNCH();
 }
 

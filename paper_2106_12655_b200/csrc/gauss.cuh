@@ -97,13 +97,21 @@ int64_t build_items(const int32_t *d_pairs, int64_t P, const int64_t *d_voff, Pa
 size_t build_items_scan_bytes(int64_t P);
 
 // Evaluates items [item_begin, item_end) into partials[item] (absolute index).
-// d_end (fused path): the item count n on the device bounds the range; with
-// shards > 1 the kernel takes slice `shard` of ceil(n / shards) items instead.
-// abort (fused path): polled per item; nonzero stops the sum (the run is redone).
+// d_end (fused path): the item count n on the device bounds the range.
+// d_bounds (sharded fused path): the kernel takes items [d_bounds[shard], d_bounds[shard+1])
+// instead (launch_shard_bounds).  abort (fused path): polled per item; nonzero
+// stops the sum (the run is redone).
 void launch_gauss_items(int mode, const double *X, const double *Y, const double *Z, const ItemRec *items,
                         int64_t item_begin, int64_t item_end, unsigned long long *counter,
                         double *partials, cudaStream_t s, const int64_t *d_end = nullptr, int shard = 0,
-                        int shards = 1, const int *abort = nullptr, bool counter_zeroed = false);
+                        int shards = 1, const int *abort = nullptr, bool counter_zeroed = false,
+                        const int64_t *d_bounds = nullptr);
+
+// Cost-balanced shard boundaries of the item list: bounds[0..shards] (device),
+// shard r owns items [bounds[r], bounds[r+1]); each shard's segment-pair cost is
+// within one item of total / shards.  d_P: device pair count (<= Pcap) or null.
+void launch_shard_bounds(const PairGeom *pg, const int64_t *item_off, int64_t Pcap, const int64_t *d_P, int shards,
+                         int64_t *bounds, cudaStream_t s);
 
 // items[it] = the record of work item `it` (pair tiling + the item's place in it).
 void launch_item_pairs(const int64_t *item_off, const PairGeom *pg, int64_t P, int64_t n_items, ItemRec *items,

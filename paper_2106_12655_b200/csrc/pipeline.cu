@@ -177,7 +177,7 @@ void Pipeline::init(cudaStream_t st) {
 }
 
 void Pipeline::release() {
-    DevBuf *bufs[] = {&d_tot, &d_coeffs, &d_t, &d_loff, &d_seg_box, &d_seg_fbox, &d_loop_keys, &d_seg_loop, &d_loop_box, &d_min_diag, &d_model_exp,
+    DevBuf *bufs[] = {&d_bounds, &d_tot, &d_coeffs, &d_t, &d_loff, &d_seg_box, &d_seg_fbox, &d_loop_keys, &d_seg_loop, &d_loop_box, &d_min_diag, &d_model_exp,
                       &d_verts_in, &d_aos, &d_in_off, &d_voff, &d_X, &d_Y, &d_Z, &d_exp, &d_tmp_aos, &d_pairs,
                       &d_pg, &d_item_off, &d_item_pair, &d_scan, &d_counter, &d_partials, &d_raw, &d_lk, &d_flags,
                       &d_quads, &d_qout, &dout.X, &dout.Y, &dout.Z, &dout.voff, &dout.vert_off};
@@ -345,7 +345,8 @@ void Pipeline::upload_model_polyline_ptrs(const double *const *loop_verts, const
     const int64_t per_thread = 1 << 18;   // rows (6 MiB) per thread at least
     int nt = (int)std::min<int64_t>(8, std::max<int64_t>(1, nM / per_thread));
     const unsigned hw = std::thread::hardware_concurrency();
-    if (hw > 0 && (unsigned)nt > hw / 2) nt = std::max(1, (int)hw / 2);
+    const int share = gather_share > 1 ? gather_share : 1;   // ranks of one host split its cores
+    if (hw > 0 && (unsigned)nt > hw / (2 * share)) nt = std::max(1, (int)hw / (2 * share));
     std::vector<int64_t> cut(nt + 1, nloops);
     cut[0] = 0;
     for (int k = 1, l = 0; k < nt; ++k) {
@@ -594,9 +595,12 @@ void Pipeline::download_results_pinned() {
 }
 
 int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscParams &prm, int mode, int shard,
-                       int shards, bool async) {
+                       int shards, bool async, bool force_sharded) {
     pend.on = false;
     if (shards < 1 || shard < 0 || shard >= shards) throw Error(LC_ERR_ARG, "bad shard");
+    // sharded: the partials are exchanged (all-reduce) before the per-pair sums —
+    // every run of a multi-GPU communicator, including world size 1
+    const bool sharded = shards > 1 || force_sharded;
     // loops longer than the brute-force side limit make every pair they are in a
     // large (sweep) pair: the staged path handles those models directly
     if (!model_ready || L < 2 || M == 0 || prm.max_passes < 1 || max_loop > 256 ||
@@ -622,8 +626,9 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
     d_counter.reserve(sizeof(unsigned long long), s);
     reserve_pls_grid(L, pls_sc, s);   // prezeroed by the run's first kernel
     d_tot.reserve(4 * sizeof(int64_t), s);
-    part_cap = ceil_div(icap, shards) * shards;   // every shard's slice fits at shard * per
+    part_cap = icap;   // partials at absolute item ids; a shard writes only its cost-balanced range
     d_partials.reserve(sizeof(double) * part_cap, s);
+    d_bounds.reserve(sizeof(int64_t) * (shards + 1), s);
     d_item_pair.reserve(sizeof(ItemRec) * icap, s);
     d_raw.reserve(sizeof(double) * pcap, s);
     d_lk.reserve(sizeof(int64_t) * pcap, s);
@@ -690,20 +695,23 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
         LC_CUDA(cudaEventRecord(ev_checks, side[1]));
         launch_item_pairs_dev(d_item_off.as<int64_t>(), d_pg.as<PairGeom>(), pcap, dP, icap, d_item_pair.as<ItemRec>(),
                               s);
-        if (shards > 1) {   // items of other shards: the bits of -0.0 (the int64 MAX all-reduce identity)
+        if (sharded) {   // items of other shards: the bits of -0.0 (the int64 MAX all-reduce identity)
             fill_bits_kernel<<<(unsigned)ceil_div(part_cap, 256), 256, 0, s>>>(
                 reinterpret_cast<unsigned long long *>(d_partials.ptr), part_cap, 0x8000000000000000ull);
             LC_CHECK_LAUNCH();
+            launch_shard_bounds(d_pg.as<PairGeom>(), d_item_off.as<int64_t>(), pcap, dP, shards,
+                                d_bounds.as<int64_t>(), s);
         }
         LC_CUDA(cudaStreamWaitEvent(s, ev_chords, 0));   // the sum reads the chords
         record(EV_GAUSS0);
         launch_gauss_items(mode, dout.X.as<double>(), dout.Y.as<double>(), dout.Z.as<double>(), d_item_pair.as<ItemRec>(),
                            0, icap,
                            d_counter.as<unsigned long long>(), d_partials.as<double>(), s, d_items, shard, shards,
-                           &disc_sc.prectr.as<PreCounters>()->abort, /*counter_zeroed=*/true);
+                           &disc_sc.prectr.as<PreCounters>()->abort, /*counter_zeroed=*/true,
+                           sharded ? d_bounds.as<int64_t>() : nullptr);
         record(EV_GAUSS1);
         LC_CUDA(cudaStreamWaitEvent(s, ev_checks, 0));
-        if (shards == 1) {   // per-pair sums straight into pinned memory, with the status
+        if (!sharded) {   // per-pair sums straight into pinned memory, with the status
             launch_reduce_export(d_partials.as<double>(), d_item_off.as<int64_t>(), dP, pcap, d_items, dmx, ctr,
                                  dout.d_val_err, st, d_raw.as<double>(), d_lk.as<int64_t>(), d_flags.as<uint8_t>(),
                                  reinterpret_cast<double *>(hr), reinterpret_cast<int64_t *>(hl),
@@ -720,7 +728,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
         const char *e = getenv("LINKCERT_NO_GRAPH");
         return e && e[0] == '1';
     }();
-    FastKey key{L, M, pcap, icap, n_excl, mode, model_poly ? 1 : 0, shard, shards, prm.epsilon * prm.xi,
+    FastKey key{L, M, pcap, icap, n_excl, mode, model_poly ? 1 : 0, shard, sharded ? shards : 0, prm.epsilon * prm.xi,
                 2.220446049250313e-16 * prm.xi, alloc_generation().load()};
     last_fast_graph = false;
     if (!no_graph && graph_exec && key == graph_key) {
@@ -776,6 +784,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
     pend.pcap = pcap;
     pend.icap = icap;
     pend.shards = shards;
+    pend.sharded = sharded;
     pend.st = st;
     pend.hp = hp;
     pend.hr = hr;
@@ -791,7 +800,7 @@ int Pipeline::finish_fast() {
     pend.on = false;
     const FastKey key = pend.key;
     const int64_t pcap = pend.pcap, icap = pend.icap;
-    const int shards = pend.shards;
+    const bool pend_sharded = pend.sharded;
     char *hp = pend.hp, *hr = pend.hr, *hl = pend.hl, *hf = pend.hf;
     LC_CUDA(cudaStreamSynchronize(s));
     fast_seen = key;
@@ -823,32 +832,9 @@ int Pipeline::finish_fast() {
     res_raw = hr;
     res_lk = hl;
     res_flags = hf;
-    h_res_P = shards == 1 ? P : -1;   // sharded: lc_shard_reduce completes the results
-    fused_shard_pending = shards > 1;
+    h_res_P = pend_sharded ? -1 : P;   // sharded: lc_shard_finish completes the results
+    fused_shard_pending = pend_sharded;
     return FAST_OK;
-}
-
-// After a sharded fused run and the all-gather of the item partials: the
-// fixed-order per-pair reduction and the results into pinned memory.
-void Pipeline::shard_reduce(const double *partials_all) {
-    if (!polylines_ready) throw Error(LC_ERR_STATE, "no sharded run to reduce");
-    launch_reduce_pairs(partials_all, d_item_off.as<int64_t>(), P, d_raw.as<double>(), d_lk.as<int64_t>(),
-                        d_flags.as<uint8_t>(), s);
-    if (fused_shard_pending) {
-        fused_shard_pending = false;
-        // after a fused sharded run the pair list is already in pinned memory: one
-        // kernel writes the sums next to it (no per-array copies)
-        export_results_kernel<<<148, 256, 0, s>>>(d_tot.as<int64_t>(), P, nullptr, nullptr, nullptr, nullptr, nullptr,
-                                                  d_raw.as<double>(), d_lk.as<int64_t>(), d_flags.as<uint8_t>(),
-                                                  nullptr, nullptr, reinterpret_cast<double *>(res_raw),
-                                                  reinterpret_cast<int64_t *>(res_lk),
-                                                  reinterpret_cast<uint8_t *>(res_flags));
-        LC_CHECK_LAUNCH();
-        LC_CUDA(cudaStreamSynchronize(s));
-        h_res_P = P;
-        return;
-    }
-    download_results_pinned();
 }
 
 // After an async sharded run and the in-place all-reduce of d_partials: the
@@ -867,6 +853,25 @@ int Pipeline::shard_finish() {
         fused_shard_pending = false;
     }
     return r;
+}
+
+void Pipeline::prefill_partials_neg_zero(int64_t n) {
+    d_partials.reserve(sizeof(double) * (size_t)(n > 0 ? n : 1), s);
+    if (n == 0) return;
+    fill_bits_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(reinterpret_cast<unsigned long long *>(d_partials.ptr),
+                                                                n, 0x8000000000000000ull);
+    LC_CHECK_LAUNCH();
+}
+
+void Pipeline::shard_bounds(int shards, int64_t *out) {
+    if (!polylines_ready) throw Error(LC_ERR_STATE, "no work items built");
+    if (shards < 1) throw Error(LC_ERR_ARG, "shards must be >= 1");
+    d_bounds.reserve(sizeof(int64_t) * (shards + 1), s);
+    launch_shard_bounds(d_pg.as<PairGeom>(), d_item_off.as<int64_t>(), P, nullptr, shards, d_bounds.as<int64_t>(), s);
+    if (out) {
+        LC_CUDA(cudaMemcpyAsync(out, d_bounds.ptr, sizeof(int64_t) * (shards + 1), cudaMemcpyDeviceToHost, s));
+        LC_CUDA(cudaStreamSynchronize(s));
+    }
 }
 
 void Pipeline::segment_pair_lambda(const double *quads, int64_t n, double *out) {

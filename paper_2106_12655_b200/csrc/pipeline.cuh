@@ -116,17 +116,22 @@ struct Pipeline {
     // the run was the reference's: FAST_OK (results in h_res), FAST_INVALID
     // (PolylineLoop ValidationError in derr), FAST_FALLBACK (the model needs
     // refinement / the sweep path / larger buffers: run the staged pipeline).
-    // shards > 1: the Gauss kernel evaluates only item slice `shard` (of ceil(n/shards))
-    // into d_partials at absolute item ids and the sums wait for shard_reduce().
+    // shards > 1 (or force_sharded): the Gauss kernel evaluates only the
+    // cost-balanced item range of `shard` (launch_shard_bounds) into d_partials at
+    // absolute item ids and the sums wait for the exchange + shard_finish().
     // async: enqueue the run and return FAST_PENDING without a
     // host sync; the item partials not owned by this shard hold the bits of -0.0
     // (INT64_MIN), so an int64 MAX all-reduce of d_partials assembles every
     // shard's items exactly; shard_finish() then reduces, exports and syncs once.
     int run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscParams &prm, int mode, int shard = 0,
-                 int shards = 1, bool async = false);
-    void shard_reduce(const double *partials_all);
+                 int shards = 1, bool async = false, bool force_sharded = false);
     int shard_finish();
-    int64_t part_cap = 0;   // d_partials entries of the last run (shards x per-shard capacity)
+    int gather_share = 1;         // ranks sharing this host (host gather threads / rank)
+    void prefill_partials_neg_zero(int64_t n);   // d_partials[0, n) <- bits of -0.0 (staged sharded path)
+    int64_t part_cap = 0;   // d_partials entries of the last run (item capacity)
+    DevBuf d_bounds;        // cost-balanced shard boundaries of the item list (shards + 1)
+    // staged path: cost-balanced bounds of the current items (device d_bounds; out: host copy, may be null)
+    void shard_bounds(int shards, int64_t *out);
     int64_t items_cap = 0;
     int64_t pairs_seen = 0;   // largest pair count of a fused run (sizes the next run's capacity)
     // The fused sequence is replayed as a CUDA graph once a run with the same
@@ -149,6 +154,7 @@ struct Pipeline {
         FastKey key{};
         int64_t pcap = 0, icap = 0;
         int shards = 1;
+        bool sharded = false;
         FastStatus *st = nullptr;
         char *hp = nullptr, *hr = nullptr, *hl = nullptr, *hf = nullptr;
     } pend;

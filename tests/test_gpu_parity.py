@@ -189,9 +189,9 @@ def test_deterministic_and_split_invariant(gpu):
     n = gpu.prepare_gauss()
     for world in (2, 3, 8):
         buf = torch.zeros(n, dtype=torch.float64, device="cuda")
+        bounds = gpu.shard_bounds(world)
         for r in range(world):
-            b, e, _ = lc.certify.item_range(n, r, world)
-            gpu.gauss_run(_native.GAUSS_PHASE, b, e, buf.data_ptr())
+            gpu.gauss_run(_native.GAUSS_PHASE, int(bounds[r]), int(bounds[r + 1]), buf.data_ptr())
         gpu.synchronize()
         raw2, lk2, _ = gpu.gauss_reduce(buf.data_ptr())
         assert np.array_equal(raw0.view(np.int64), raw2.view(np.int64))
@@ -385,36 +385,66 @@ def test_pipeline_validation_errors(golden, monkeypatch, name):
         assert _native.context().last_run_fused() == (1 if fused == "1" else 0)
 
 
+class _DeviceArray:
+    """Zero-copy torch view of a library-owned device buffer (__cuda_array_interface__)."""
+
+    def __init__(self, ptr, n, typestr="<f8"):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3}
+
+
+def _mixed_model():
+    """Kusari rings + knit courses of very different sizes: item costs vary ~60x."""
+    k = lc.generators.kusari_tube(n_around=12, rows=4, partial=5)
+    kv = k.snapshot()
+    knit = lc.generators.knit_tube(courses=4, n=3000, W=10)
+    kn = knit.snapshot()
+    shift = np.array([200.0, 0.0, 0.0])
+    verts = np.concatenate([kv.vertices(), kn.vertices() + shift])
+    off = np.concatenate([kv.off, kn.off[1:] + kv.off[-1]])
+    return lc.CurveModel.from_polyline_arrays(verts, off)
+
+
 @pytest.mark.parametrize("shards", [2, 3, 8])
-def test_fused_shards_reassemble_bitwise(shards):
-    """The sharded fused run, emulated on one GPU: each shard's item slice of the
-    partials, concatenated as the NCCL all-gather would, reduces to bitwise the
-    single-GPU results (what every rank of a multi-GPU run computes)."""
-    import torch
+def test_cost_balanced_shard_bounds(gpu, shards):
+    """lc_shard_bounds: the ranges partition the items, and each rank's segment-pair
+    cost is within one item of total / shards (north_star: split by estimated cost)."""
+    from paper_2106_12655_b200.certify import run_device_pipeline
 
-    from paper_2106_12655_b200.certify import _DeviceArray, excluded_keys, run_device_pipeline
-    from paper_2106_12655_b200.pls import upload
-
-    m = lc.generators.kusari_tube(n_around=12, rows=4, partial=5)
-    want = [np.array(a).copy() for a in run_device_pipeline(m)[:4]]
-    ctx = _native.Context()
-    upload(m, ctx)
-    prm = lc.DiscretizationParams()
-    slices = []
-    for rep in range(2):   # second round: graph replays of each shard's key
-        slices = []
-        for r in range(shards):
-            n_items, ptr = ctx.run_pipeline_shard(excluded_keys(()), m.xi, prm.epsilon, prm.max_passes,
-                                                  prm.max_subsegments, 0, r, shards)
-            per = -(-n_items // shards)
-            buf = torch.as_tensor(_DeviceArray(ptr, per * shards), device="cuda")
-            slices.append(buf[r * per:(r + 1) * per].clone())
-        gathered = torch.cat(slices)
-        torch.cuda.synchronize()   # the library reduces on its own stream
-        ctx.shard_reduce(gathered.data_ptr())
-        got = ctx.result_views()
-        for a, b in zip(want, got):
-            assert np.array_equal(a, np.asarray(b)), (rep, shards)
+    m = _mixed_model()
+    pairs, _, _, _, ctx = run_device_pipeline(m)
+    pairs = np.array(pairs)
+    ctx.prepare_gauss()
+    b = ctx.shard_bounds(shards)
+    assert b[0] == 0 and np.all(np.diff(b) >= 0)
+    # per-item cost on the host from the pair sizes (items of a pair tile it exactly)
+    _, voff = ctx.get_polylines()
+    nseg = np.diff(voff)
+    items = []
+    for i, j in pairs:
+        g_rows, g_cols = int(nseg[j]), int(nseg[i])
+        nb = -(-g_rows // 4)
+        rbl = 0
+        while (1 << rbl) < nb and rbl < 5:
+            rbl += 1
+        cs = 32 >> rbl
+        cl = min(max(-(-g_cols // cs), 1), 2048)
+        rows_per, span = 4 << rbl, cs * cl
+        for ir in range(-(-g_rows // rows_per)):
+            for ic in range(-(-g_cols // span)):
+                items.append(min(rows_per, g_rows - ir * rows_per) * min(span, g_cols - ic * span))
+    items = np.array(items, dtype=np.int64)
+    assert b[-1] == len(items)
+    total = items.sum()
+    cum = np.concatenate([[0], np.cumsum(items)])
+    assert total == int(np.sum(nseg[pairs[:, 0]] * nseg[pairs[:, 1]]))
+    for r in range(shards):
+        cost = cum[b[r + 1]] - cum[b[r]]
+        assert abs(cost - total / shards) <= 2 * items.max(), (r, cost, total / shards)
+    # the old equal-count split is far off on this model
+    per = -(-len(items) // shards)
+    counts = [cum[min(len(items), (r + 1) * per)] - cum[min(len(items), r * per)] for r in range(shards)]
+    assert max(counts) - min(counts) > 2 * items.max()
 
 
 @pytest.mark.parametrize("shards", [2, 3, 8])
@@ -425,7 +455,7 @@ def test_async_shards_allreduce_max_bitwise(shards):
     the pending run's lc_shard_finish gives bitwise the single-GPU results."""
     import torch
 
-    from paper_2106_12655_b200.certify import _DeviceArray, excluded_keys, run_device_pipeline
+    from paper_2106_12655_b200.certify import excluded_keys, run_device_pipeline
     from paper_2106_12655_b200.pls import upload
 
     m = lc.generators.kusari_tube(n_around=12, rows=4, partial=5)
@@ -454,9 +484,10 @@ def test_async_shards_allreduce_max_bitwise(shards):
 
 
 def test_sharded_nccl_path_world1():
-    """The multi-GPU code path (async fused shard run + NCCL MAX all-reduce on
-    the library stream + fixed-order reduce) end to end under torchrun at world
-    size 1 (LINKCERT_FORCE_SHARDED)."""
+    """The multi-GPU code path (the library's own NCCL communicator: fused shard
+    run + in-place MAX all-reduce on the library stream + fixed-order reduce, and
+    the staged sharded path) end to end under torchrun at world size 1
+    (LINKCERT_FORCE_SHARDED)."""
     import os
     import socket
     import subprocess

@@ -13,7 +13,7 @@ import cases
 import paper_2106_12655_b200 as lc
 from conftest import circle_points
 from paper_2106_12655_b200 import _native
-from paper_2106_12655_b200.certify import ABORTED, FAIL, PASS, diff_arrays, item_range
+from paper_2106_12655_b200.certify import ABORTED, FAIL, PASS, diff_arrays
 from paper_2106_12655_b200.geometry import compute_xi
 from paper_2106_12655_b200.model_io import model_digest_python
 
@@ -279,54 +279,72 @@ def test_digest_cubics_and_open_loops():
 
 # ------------------------------------------------------------- sharding
 
-@pytest.mark.parametrize("n", [0, 1, 7, 100, 18749, 1 << 20])
-@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
-def test_item_ranges_partition(n, world):
-    covered = []
-    for r in range(world):
-        b, e, per = item_range(n, r, world)
-        assert 0 <= b <= e <= n and e - b <= per
-        covered.extend(range(b, e))
-    assert covered == list(range(n))
-
-
-def _gloo_worker(rank, world, port, n_items, q):
+def _gloo_comm_worker(rank, world, port, q):
+    """ensure_comm + digest_on_rank0 host logic over gloo: one unique id and one
+    digest (rank 0's) reach every rank; a digest error reaches every rank too."""
     import os
 
-    import torch
     import torch.distributed as dist
 
-    from paper_2106_12655_b200.certify import gather_item_partials, item_range
+    from paper_2106_12655_b200 import _native, certify
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    partials = torch.from_numpy(np.random.default_rng(5).normal(size=n_items))   # "kernel output" per item id
-    b, e, per = item_range(n_items, rank, world)
-    full = torch.zeros(per * world, dtype=torch.float64)
-    full[b:e] = partials[b:e]                      # this rank computed only its own items
-    gathered = gather_item_partials(dist, full, rank, per)
-    ok = bool(torch.equal(gathered[:n_items], partials))
-    q.put((rank, ok))
+    _native.comm_unique_id = lambda: bytes([7]) * 128      # no NCCL on the CPU box: the exchange is the test
+
+    class Ctx:
+        comm = None
+
+        def comm_init(self, uid, w, r):
+            self.comm = (w, r)
+            self.uid = uid
+
+    ctx = Ctx()
+    certify.ensure_comm(ctx, dist)
+    certify.ensure_comm(ctx, dist)                          # idempotent: no second exchange
+    calls = []
+    certify._digest_async = lambda model, snap, nthreads=0: calls.append(nthreads) or _Done("d" + str(model))
+    got = certify.digest_on_rank0("M", None, dist)()
+    certify._digest_async = lambda model, snap, nthreads=0: _Done(exc=ValueError("cannot serialize"))
+    try:
+        certify.digest_on_rank0("M", None, dist)()
+        err = None
+    except ValueError as exc:
+        err = str(exc)
+    q.put((rank, ctx.comm == (world, rank) and ctx.uid == bytes([7]) * 128, got, len(calls), err))
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n_items", [(2, 18749), (2, 5), (3, 1000)])
-def test_multirank_gather_is_bitwise(world, n_items):
-    """world_size>1 path on CPU (gloo): item-slice all-gather reproduces the 1-GPU partial array bitwise."""
+class _Done:
+    def __init__(self, val=None, exc=None):
+        self.val, self.exc = val, exc
+
+    def result(self):
+        if self.exc is not None:
+            raise self.exc
+        return self.val
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_multirank_comm_and_digest_exchange(world):
+    """world_size > 1 host logic on CPU (gloo): the library communicator's unique id
+    and the model digest are made on rank 0 only and received by every rank."""
     import multiprocessing as mp
     import random
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = random.randint(20000, 40000)
-    procs = [ctx.Process(target=_gloo_worker, args=(r, world, port, n_items, q)) for r in range(world)]
+    procs = [ctx.Process(target=_gloo_comm_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=120) for _ in procs]
+    res = sorted(q.get(timeout=120) for _ in procs)
     for p in procs:
         p.join(timeout=60)
-    assert sorted(res) == [(r, True) for r in range(world)]
+    assert [r[0] for r in res] == list(range(world))
+    assert all(r[1] and r[2] == "dM" and r[4] == "cannot serialize" for r in res)
+    assert [r[3] for r in res] == [1] + [0] * (world - 1)      # only rank 0 hashed
 
 
 def _gloo_max_worker(rank, world, port, n_items, q):
@@ -334,8 +352,6 @@ def _gloo_max_worker(rank, world, port, n_items, q):
 
     import torch
     import torch.distributed as dist
-
-    from paper_2106_12655_b200.certify import item_range
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -350,9 +366,10 @@ def _gloo_max_worker(rank, world, port, n_items, q):
     bits[6::19] = 0x7FF8DEADBEEF0001                # NaN with a payload
     cap = -(-n_items // world) * world + 3          # capacity > n_items, like the library buffer
     buf = torch.full((cap,), torch.iinfo(torch.int64).min, dtype=torch.int64)   # bits of -0.0
-    b, e, _ = item_range(n_items, rank, world)
+    bounds = np.linspace(0, n_items, world + 1).astype(np.int64)   # any partition (the library's is by cost)
+    b, e = bounds[rank], bounds[rank + 1]
     buf[b:e] = torch.from_numpy(bits[b:e])          # the items this rank's Gauss slice wrote
-    dist.all_reduce(buf, op=dist.ReduceOp.MAX)      # what _fused_sharded_step enqueues (NCCL)
+    dist.all_reduce(buf, op=dist.ReduceOp.MAX)      # what lc_run_pipeline_sharded enqueues (NCCL)
     ok = bool(np.array_equal(buf.numpy()[:n_items], bits))
     q.put((rank, ok))
     dist.destroy_process_group()
