@@ -57,11 +57,11 @@ F_PAIR = 262.0
 # FP64 FLOPs the kernels actually execute per segment pair (ncu
 # smsp__sass_thread_inst_executed_op_{dfma,dmul,dadd}_pred_on, 2*DFMA+DMUL+DADD;
 # profiles/r01/counts_*.csv): the numerator of roofline.frac.
-EXEC_FLOP_PAIR = {"phase": 78.5, "atan": 133.3, "ref": 260.3}
-# Hardware counters of the committed `ncu --set full` capture of the Gauss kernel on this
-# workload: DRAM bytes per launch and FP64-pipe activity.
-NCU = {("kusari", "phase"): {"traffic": 23055616 + 58368, "fp64_pipe_active_pct": 73.8,
-                             "source": "profiles/r01/gauss_phase_kusari_raw.csv"}}
+EXEC_FLOP_PAIR = {"phase": 73.54, "atan": 128.28, "ref": 260.25}   # profiles/r02/counts_torus_*.csv
+# Hardware counters of the committed `ncu --set full` capture of the fused Gauss kernel on
+# this workload: DRAM bytes per launch and FP64-pipe activity.
+NCU = {("kusari", "phase"): {"traffic": 22835200, "fp64_pipe_active_pct": 70.45,
+                             "source": "profiles/r02/gauss_pairs_kusari_raw.csv"}}
 L2_FLUSH_BYTES = 512 << 20
 DESC = {
     "kusari": "kusari_tube 14112 rings x 64 seg, 18752 links (BASELINE configs[2]); verify(after, cert(before))",
@@ -385,6 +385,14 @@ def main():
     if rank != 0:
         dist.destroy_process_group()
         return 0
+    # the same arithmetic kernel alone on this workload's work items (no concurrent branches)
+    ctx_mode = _native.GAUSS_MODES[args.mode]
+    n_items = ctx.prepare_gauss(ctx_mode)
+    solo = []
+    for _ in range(5):
+        ctx.gauss_run(ctx_mode, 0, n_items)
+        solo.append(ctx.gauss_event_ms())
+    gk_solo = min(solo[1:])
     peak_dfma, _ = ctx.probe_fp64_peak()
     peak_dmma, _ = ctx.probe_fp64_peak(dmma=True)
     peak = max(peak_dfma, peak_dmma)
@@ -411,11 +419,15 @@ def main():
                                                            "created": report.created, "changed": report.changed}},
         "roofline": {"bound": "fp64", "achieved": executed / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
                      "frac": executed / peak, "traffic": ncu.get("traffic"),
-                     "kernel": f"gauss_items_kernel<{args.mode.upper()}>", "kernel_ms": gk,
+                     "kernel": f"gauss_pairs_kernel<{args.mode.upper()}> (fused step, beside the checks branch)",
+                     "kernel_ms": gk,
                      "flop_per_pair_executed": EXEC_FLOP_PAIR[args.mode],
                      "fp64_pipe_active_pct_ncu": ncu.get("fp64_pipe_active_pct"),
                      "ncu_source": ncu.get("source"),
                      "frac_algorithmic": F_PAIR * rate / peak, "f_pair_algorithmic": F_PAIR,
+                     "standalone": {"kernel": f"gauss_items_kernel<{args.mode.upper()}> alone on the same items",
+                                    "kernel_ms": gk_solo, "seg_pairs_per_s": n_sp / (gk_solo * 1e-3),
+                                    "frac": EXEC_FLOP_PAIR[args.mode] * n_sp / (gk_solo * 1e-3) / peak},
                      "algorithmic_bytes": 24 * n_closed,
                      "peak_probes_tflops": {"dfma": peak_dfma / 1e12, "dmma": peak_dmma / 1e12},
                      "peak_source": "max(FP64 DFMA-chain, FP64 tensor-core MMA) probes measured live on this GPU "

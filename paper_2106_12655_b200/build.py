@@ -18,7 +18,7 @@ SOURCES = ["abi.cu", "pipeline.cu", "gauss.cu", "pls.cu", "discretize.cu", "bh.c
 # bh.cu reproduces the reference numba arithmetic (no FMA contraction) operation by operation
 EXTRA_FLAGS = {"bh.cu": ["-fmad=false"]}
 HEADERS = ["common.cuh", "gauss.cuh", "pipeline.cuh", "pls.cuh", "discretize.cuh", "geom.cuh", "scan.cuh", "bh.cuh",
-           "comm.cuh"]
+           "comm.cuh", "pass1.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 NVCC_FLAGS = [

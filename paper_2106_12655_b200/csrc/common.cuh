@@ -7,6 +7,8 @@
 #include <cstdio>
 #include <stdexcept>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "../../include/linkcert_b200.h"
 
@@ -97,5 +99,54 @@ struct PinnedBuf {
 };
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Debug timeline of the fused run (LINKCERT_TIMELINE=1): external event-record
+// nodes after each stage (captured into the CUDA graph like the stage events),
+// printed to stderr after the run's sync as microseconds from the first mark.
+struct Timeline {
+    bool on = false;
+    std::vector<std::pair<const char *, cudaEvent_t>> marks;
+    size_t n = 0;
+};
+inline Timeline &timeline() {
+    static Timeline t = [] {
+        Timeline x;
+        const char *e = getenv("LINKCERT_TIMELINE");
+        x.on = e && e[0] == '1';
+        return x;
+    }();
+    return t;
+}
+inline void tl_reset() { timeline().n = 0; }
+inline void tl_mark(const char *name, cudaStream_t s) {
+    Timeline &t = timeline();
+    if (!t.on) return;
+    if (t.n == t.marks.size()) {
+        cudaEvent_t e;
+        LC_CUDA(cudaEventCreate(&e));
+        t.marks.emplace_back(name, e);
+    }
+    t.marks[t.n].first = name;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    LC_CUDA(cudaStreamIsCapturing(s, &cs));
+    if (cs == cudaStreamCaptureStatusActive)
+        LC_CUDA(cudaEventRecordWithFlags(t.marks[t.n].second, s, cudaEventRecordExternal));
+    else
+        LC_CUDA(cudaEventRecord(t.marks[t.n].second, s));
+    ++t.n;
+}
+inline void tl_print(const char *tag) {
+    Timeline &t = timeline();
+    if (!t.on || t.n == 0) return;
+    std::string line = std::string("[timeline ") + tag + "]";
+    for (size_t k = 0; k < t.n; ++k) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, t.marks[0].second, t.marks[k].second);
+        char buf[96];
+        snprintf(buf, sizeof buf, " %s=%.1f", t.marks[k].first, 1000.f * ms);
+        line += buf;
+    }
+    fprintf(stderr, "%s\n", line.c_str());
+}
 
 }  // namespace lc

@@ -1,3 +1,4 @@
+#include <algorithm>
 // Device discretization: refine paired loops until the tight boxes of their
 // subsegments are pairwise disjoint across every PLS pair, then emit chords.
 //
@@ -32,6 +33,7 @@
 #include <cub/device/device_segmented_sort.cuh>
 
 #include "discretize.cuh"
+#include "pass1.cuh"
 #include "scan.cuh"
 #include "geom.cuh"
 
@@ -40,8 +42,6 @@ namespace {
 
 constexpr double kMachineEps = 2.220446049250313e-16;
 constexpr int32_t kNoIndex = 0x7f7f7f7f;       // atomicMin sentinel from cudaMemset(0x7f)
-constexpr int64_t kBruteLimit = 16384;         // bvh.py:224 BRUTE_FORCE_LIMIT
-constexpr int kBruteMaxSide = 256;             // shared-memory staging of loop j's boxes
 constexpr int kBruteWarps = 4;
 
 
@@ -63,9 +63,6 @@ __device__ __forceinline__ double scale_of(const int *max_exp) {
     return __hiloint2double((1023 - e) << 20, 0);   // 2^-e, exact
 }
 
-__device__ __forceinline__ bool brute_pair(int64_t ni, int64_t nj) {
-    return ni * nj <= kBruteLimit && ni <= kBruteMaxSide && nj <= kBruteMaxSide;
-}
 
 __device__ __forceinline__ int64_t upper_index(const int64_t *__restrict__ off, int64_t n, int64_t k) {
     int64_t lo = 0, hi = n;   // largest idx in [0, n) with off[idx] <= k  (off[0] == 0)
@@ -98,9 +95,8 @@ __global__ void pre_pairs_kernel(const int32_t *__restrict__ pairs, int64_t P, c
                                  const int64_t *__restrict__ loff, const double *__restrict__ lbox, int64_t L,
                                  uint8_t *__restrict__ paired, int8_t *__restrict__ axis,
                                  PreCounters *__restrict__ ctr) {
-    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (dP && *dP < P) P = *dP;   // fused path: P on the device, grid sized by its capacity
-    if (p >= P) return;
+    if (dP && *dP < P) P = *dP;   // fused path: P on the device (grid-stride over the real count)
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P; p += (int64_t)gridDim.x * blockDim.x) {
     const int i = pairs[2 * p], j = pairs[2 * p + 1];
     paired[i] = 1;
     paired[j] = 1;
@@ -119,6 +115,7 @@ __global__ void pre_pairs_kernel(const int32_t *__restrict__ pairs, int64_t P, c
         atomicAdd(&ctr->n_large, 1);
         ctr->abort = 1;
     }
+    }
 }
 
 __global__ void pre_loops_kernel(const unsigned long long *__restrict__ min_diag, const uint8_t *__restrict__ paired,
@@ -134,13 +131,6 @@ __global__ void pre_loops_kernel(const unsigned long long *__restrict__ min_diag
 }
 
 // ------------------------------------------------------------- detection
-
-__device__ __forceinline__ bool box_overlap(const double *__restrict__ b, int64_t stride, int64_t e,
-                                            const double lo[3], const double hi[3]) {
-    // closed-interval overlap (bvh.py:93-98)
-    return !(lo[0] > b[3 * stride + e] || b[e] > hi[0] || lo[1] > b[4 * stride + e] || b[stride + e] > hi[1] ||
-             lo[2] > b[5 * stride + e] || b[2 * stride + e] > hi[2]);
-}
 
 __device__ __forceinline__ bool box_overlap_f(const float *__restrict__ b, int64_t stride, int64_t e,
                                               const float lo[3], const float hi[3]) {
@@ -241,136 +231,6 @@ __global__ void __launch_bounds__(32 * kBruteWarps) brute_kernel(ActView v, cons
 // pairwise in float, and a float hit is confirmed with the exact closed-box
 // test on the double boxes (bvh.py:93-98).  Hits are counted into *marked.
 constexpr int kAnyWarps = 8;
-constexpr int kAnyCap = 64;   // staged survivors per side; beyond that the test reads global memory
-
-// One pair: the warp's share of the pass-1 detection (see brute_any_kernel).
-__device__ __forceinline__ void brute_any_pair(int64_t p, const double *__restrict__ box, const float *__restrict__ fbox,
-                                               int64_t M, const int64_t *__restrict__ loff,
-                                               const double *__restrict__ lbox, int64_t L,
-                                               const int32_t *__restrict__ pairs, int32_t *sidx0, int32_t *sidx1,
-                                               float *sbox0, float *sbox1, int lane,
-                                               unsigned long long *__restrict__ marked, int *__restrict__ abort) {
-    int32_t *sidx_[2] = {sidx0, sidx1};
-    float *sbox_[2] = {sbox0, sbox1};
-#define sidx_at(sd, r) sidx_[sd][r]
-#define sbox_at(sd, d, r) sbox_[sd][(d) * kAnyCap + (r)]
-
-        const int i = pairs[2 * p], j = pairs[2 * p + 1];
-        const int64_t bi = loff[i], ni = loff[i + 1] - bi;
-        const int64_t bj = loff[j], nj = loff[j + 1] - bj;
-        if (ni == 0 || nj == 0 || !brute_pair(ni, nj)) return;
-        float fb[2][6];   // [0]: loop j's box (filters side i), [1]: loop i's box (filters side j)
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-            fb[0][d] = __double2float_rd(lbox[d * L + j]);
-            fb[0][3 + d] = __double2float_ru(lbox[(3 + d) * L + j]);
-            fb[1][d] = __double2float_rd(lbox[d * L + i]);
-            fb[1][3 + d] = __double2float_ru(lbox[(3 + d) * L + i]);
-        }
-        // side 0: loop i's segments vs loop j's box; side 1 only if side 0 kept any
-        int cnt[2] = {0, 0};
-#pragma unroll
-        for (int sd = 0; sd < 2; ++sd) {
-            if (sd == 1 && cnt[0] == 0) break;   // no survivor on one side: no hit possible
-            const float *o = fb[sd];
-            const int64_t base = sd ? bj : bi;
-            const int n = (int)(sd ? nj : ni);
-#pragma unroll 2
-            for (int k0 = 0; k0 < n; k0 += 32) {
-                const int k = k0 + lane;
-                const int64_t e = base + k;
-                float v[6];
-#pragma unroll
-                for (int d = 0; d < 6; ++d) v[d] = k < n ? fbox[d * M + e] : 0.f;
-                const bool in = k < n && !(o[0] > v[3] || v[0] > o[3] || o[1] > v[4] || v[1] > o[4] ||
-                                           o[2] > v[5] || v[2] > o[5]);
-                const unsigned bal = __ballot_sync(0xffffffffu, in);
-                if (in) {
-                    const int r = cnt[sd] + __popc(bal & ((1u << lane) - 1u));
-                    if (r < kAnyCap) {
-                        sidx_at(sd, r) = (int32_t)e;
-#pragma unroll
-                        for (int d = 0; d < 6; ++d) sbox_at(sd, d, r) = v[d];
-                    }
-                }
-                cnt[sd] += __popc(bal);
-            }
-        }
-        __syncwarp();
-        const int ns = cnt[0], nt = cnt[1];
-        int hits = 0;
-        if (ns && nt && ns <= kAnyCap && nt <= kAnyCap) {
-            // lanes take the larger survivor list (its float box in registers), the smaller
-            // one is read from shared memory as a broadcast: ~n_small iterations, no division
-            const int sl = ns >= nt ? 0 : 1, nl = sl ? nt : ns, nq = sl ? ns : nt;
-            for (int base = 0; base < nl; base += 32) {
-                const int l = base + lane;
-                float x[6];
-                int64_t el = -1;
-                if (l < nl) {
-                    el = sidx_at(sl, l);
-#pragma unroll
-                    for (int d = 0; d < 6; ++d) x[d] = sbox_at(sl, d, l);
-                }
-                for (int q = 0; q < nq; ++q) {
-                    float y[6];
-#pragma unroll
-                    for (int d = 0; d < 6; ++d) y[d] = sbox_at(sl ^ 1, d, q);
-                    if (el < 0 || x[0] > y[3] || y[0] > x[3] || x[1] > y[4] || y[1] > x[4] || x[2] > y[5] ||
-                        y[2] > x[5])
-                        continue;
-                    // a float hit: the exact closed test on the double boxes (bvh.py:93-98)
-                    const int64_t eq = sidx_at(sl ^ 1, q);
-                    double lo[3], hi[3];
-#pragma unroll
-                    for (int d = 0; d < 3; ++d) {
-                        lo[d] = box[d * M + el];
-                        hi[d] = box[(3 + d) * M + el];
-                    }
-                    if (box_overlap(box, M, eq, lo, hi)) ++hits;
-                }
-            }
-        } else if (ns && nt) {   // rare: more survivors than staged — every combination from global memory
-            for (int k = lane; k < ns * nt; k += 32) {
-                const int a = k / nt, b = k % nt;
-                int64_t es = -1, et = -1;
-                int c = 0;
-                for (int64_t q = 0; q < ni && es < 0; ++q) {
-                    const float *o = fb[0];
-                    float u[6];
-#pragma unroll
-                    for (int d = 0; d < 6; ++d) u[d] = fbox[d * M + bi + q];
-                    if (!(o[0] > u[3] || u[0] > o[3] || o[1] > u[4] || u[1] > o[4] || o[2] > u[5] || u[2] > o[5]) &&
-                        c++ == a)
-                        es = bi + q;
-                }
-                c = 0;
-                for (int64_t q = 0; q < nj && et < 0; ++q) {
-                    const float *o = fb[1];
-                    float u[6];
-#pragma unroll
-                    for (int d = 0; d < 6; ++d) u[d] = fbox[d * M + bj + q];
-                    if (!(o[0] > u[3] || u[0] > o[3] || o[1] > u[4] || u[1] > o[4] || o[2] > u[5] || u[2] > o[5]) &&
-                        c++ == b)
-                        et = bj + q;
-                }
-                double lo[3], hi[3];
-#pragma unroll
-                for (int d = 0; d < 3; ++d) {
-                    lo[d] = box[d * M + es];
-                    hi[d] = box[(3 + d) * M + es];
-                }
-                if (box_overlap(box, M, et, lo, hi)) ++hits;
-            }
-        }
-        if (hits) {
-            atomicAdd(marked, (unsigned long long)hits);
-            if (abort) *abort = 1;
-        }
-        __syncwarp();
-    #undef sidx_at
-#undef sbox_at
-}
 
 __global__ void __launch_bounds__(32 * kAnyWarps, 4) brute_any_kernel(
     const double *__restrict__ box, const float *__restrict__ fbox, int64_t M, const int64_t *__restrict__ loff,
@@ -399,9 +259,13 @@ __global__ void __maxnreg__(32) brute_any_lite_kernel(
     __shared__ float sbox[2][6 * kAnyCap];
     if (dP && *dP < P) P = *dP;
     const int lane = threadIdx.x & 31;
-    const int64_t p0 = (int64_t)blockIdx.x * kAnyLitePairs;
-    for (int64_t p = p0; p < p0 + kAnyLitePairs && p < P; ++p)
-        brute_any_pair(p, box, fbox, M, loff, lbox, L, pairs, sidx[0], sidx[1], sbox[0], sbox[1], lane, marked, abort);
+    // grid-stride over the device pair count: a bounded grid (the capacity-sized one
+    // was ~56k single-warp blocks for the Kusari tube, dispatched a few at a time
+    // beside the Gauss CTAs — it finished after the sum)
+    for (int64_t p0 = (int64_t)blockIdx.x * kAnyLitePairs; p0 < P; p0 += (int64_t)gridDim.x * kAnyLitePairs)
+        for (int64_t p = p0; p < p0 + kAnyLitePairs && p < P; ++p)
+            brute_any_pair(p, box, fbox, M, loff, lbox, L, pairs, sidx[0], sidx[1], sbox[0], sbox[1], lane, marked,
+                           abort);
 }
 
 // Union box of every loop's active subsegments (warp per loop).
@@ -822,6 +686,8 @@ __global__ void validate_loops2_kernel(const int64_t *__restrict__ off, int64_t 
 }
 
 inline unsigned grid_for(int64_t n, int threads = 256) { return (unsigned)(n > 0 ? ceil_div(n, threads) : 1); }
+// single-warp check blocks running beside the Gauss CTAs: 8 per SM
+constexpr unsigned kChecksBlocks = 148 * 8;
 
 template <class T> T d2h(const void *p, cudaStream_t s) {
     T v;
@@ -1311,25 +1177,30 @@ void launch_discretize_chords(const DiscInput &in, const DiscParams &prm, DiscSc
 }
 
 void launch_discretize_checks(const DiscInput &in, const int64_t *d_P, const DiscParams &prm, DiscScratch &sc,
-                              DiscOutput &out, cudaStream_t s, cudaEvent_t chords_done, const PreCounters **d_ctr) {
+                              DiscOutput &out, cudaStream_t s, cudaEvent_t chords_done, const PreCounters **d_ctr,
+                              bool brute_in_gauss) {
     const int64_t L = in.L, M = in.M, Pcap = in.P;
     const double min_diam = prm.epsilon * prm.xi;
     PreCounters *ctr = sc.prectr.as<PreCounters>();
     LC_CUDA(cudaMemsetAsync(sc.paired.ptr, 0, L > 0 ? L : 1, s));
     if (Pcap > 0) {
         // single-warp blocks: they fit beside the Gauss kernel's CTAs (this branch runs under it)
-        pre_pairs_kernel<<<grid_for(Pcap, 32), 32, 0, s>>>(in.pairs, Pcap, d_P, in.loff, in.loop_box, L,
+        pre_pairs_kernel<<<std::min(grid_for(Pcap, 32), kChecksBlocks), 32, 0, s>>>(in.pairs, Pcap, d_P, in.loff, in.loop_box, L,
                                                         sc.paired.as<uint8_t>(), sc.pair_axis.as<int8_t>(), ctr);
         LC_CHECK_LAUNCH();
+        tl_mark("S1:pre_pairs", s);
     }
     if (L > 0) {
         pre_loops_kernel<<<grid_for(L, 32), 32, 0, s>>>(in.loop_min_diag, sc.paired.as<uint8_t>(), L, min_diam, ctr);
         LC_CHECK_LAUNCH();
     }
-    if (Pcap > 0 && M > 0) {
+    if (Pcap > 0 && M > 0 && !brute_in_gauss) {
+        // the 8-warp grid-stride kernel (default) runs in the slots the short-lived Gauss
+        // CTAs free; LINKCERT_BRUTE_LITE=1 selects the single-warp variant (A/B: 0.460 vs
+        // 0.463 ms per Kusari step)
         static const bool lite = [] {
             const char *e = getenv("LINKCERT_BRUTE_LITE");
-            return !(e && e[0] == '0');
+            return e && e[0] == '1';
         }();
         if (lite) {
             brute_any_lite_kernel<<<(unsigned)ceil_div(Pcap, kAnyLitePairs), 32, 0, s>>>(
@@ -1341,6 +1212,7 @@ void launch_discretize_checks(const DiscInput &in, const int64_t *d_P, const Dis
                                                                          &ctr->marked, &ctr->abort);
         }
         LC_CHECK_LAUNCH();
+        tl_mark("S1:brute", s);
     }
     if (chords_done) LC_CUDA(cudaStreamWaitEvent(s, chords_done, 0));   // validation reads the chord flags
     if (L > 0) {

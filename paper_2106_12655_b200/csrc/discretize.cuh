@@ -108,7 +108,8 @@ void reserve_discretize_fast(const DiscInput &in, DiscScratch &sc, DiscOutput &o
 void launch_discretize_chords(const DiscInput &in, const DiscParams &prm, DiscScratch &sc, DiscOutput &out,
                               cudaStream_t s);
 void launch_discretize_checks(const DiscInput &in, const int64_t *d_P, const DiscParams &prm, DiscScratch &sc,
-                              DiscOutput &out, cudaStream_t s, cudaEvent_t chords_done, const PreCounters **d_ctr);
+                              DiscOutput &out, cudaStream_t s, cudaEvent_t chords_done, const PreCounters **d_ctr,
+                              bool brute_in_gauss = false);
 // Resets the counters (incl. the abort flag the Gauss kernel polls) — on the
 // stream every branch forks from, before the fork.
 void launch_discretize_init(DiscScratch &sc, cudaStream_t s);

@@ -23,6 +23,7 @@
 // the item range across GPUs.
 #include "gauss.cuh"
 #include "geom.cuh"
+#include "pass1.cuh"
 
 #include "scan.cuh"
 
@@ -31,6 +32,22 @@ namespace lc {
 namespace {
 
 constexpr double kInvTwoPi = 0.15915494309189535;     // 1 / (2 pi), correctly rounded
+#ifndef LC_GAUSS_CARVEOUT
+#define LC_GAUSS_CARVEOUT 10   // % of the unified L1 kept as shared memory beside the Gauss CTAs
+#endif
+constexpr int kGaussCarveout = LC_GAUSS_CARVEOUT;
+#ifndef LC_PAIRS_STATIC
+#define LC_PAIRS_STATIC 1          // pair kernel: static chunks, short-lived CTAs (0: persistent claiming)
+#endif
+#ifndef LC_PAIRS_WAVES
+#define LC_PAIRS_WAVES 16          // CTA waves of the static pair kernel (A/B: 4 / 8 / 16 -> 16 best)
+#endif
+#ifndef LC_PAIRS_PRIORITY_LOW
+#define LC_PAIRS_PRIORITY_LOW 1    // launch the pair kernel at the lowest stream priority
+#endif
+#ifndef LC_MINB
+#define LC_MINB 2   // resident CTAs per SM the phase kernel is compiled for (A/B: -DLC_MINB=n)
+#endif
 
 __device__ __forceinline__ int sbit(double x) { return (int)((unsigned)__double2hiint(x) >> 31); }
 
@@ -52,10 +69,14 @@ __device__ __forceinline__ void cmul_w(double ax, double ay, double bx, double b
 // sqrt(x) for x >= 0 without the libdevice special-case branch: MUFU rsqrt
 // seed + 2 Newton steps, s = x * y (~2 ulp; the norms only enter the d1/d2
 // denominators).  LC_SQRT_HERON adds a Heron correction (<= 1 ulp).
+#ifndef LC_SQRT
+#define LC_SQRT 5
+#endif
 template <bool ZERO_SAFE = true>
 __device__ __forceinline__ double sqrt_nb(double x) {
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#if LC_SQRT == 7
     // coupled (Goldschmidt) iteration: g -> sqrt(x), hh -> 1/(2 sqrt(x)); 7 FP64 ops
     double g = x * y, hh = 0.5 * y;
     double r = fma(-g, hh, 0.5);
@@ -63,8 +84,17 @@ __device__ __forceinline__ double sqrt_nb(double x) {
     hh = fma(hh, r, hh);
     r = fma(-g, hh, 0.5);
     g = fma(g, r, g);
-#ifdef LC_SQRT_HERON
-    g = fma(fma(-g, g, x), hh, g);
+#else
+    // one step from the seed with the series of (1 - e)^(-1/2), e = 1 - x y^2:
+    // sqrt(x) = x y (1 + e/2 + 3e^2/8 [+ 5e^3/16]); 5 [6] FP64 ops
+    const double t = x * y;
+    const double e = fma(-t, y, 1.0);
+#if LC_SQRT == 6
+    const double q = e * fma(e, fma(e, 0.3125, 0.375), 0.5);
+#else
+    const double q = e * fma(e, 0.375, 0.5);
+#endif
+    double g = fma(t, q, t);
 #endif
     // x == 0 (coincident vertices) gives NaN without the select; the phase fast
     // path omits it and re-evaluates such (degenerate) strips exactly.
@@ -270,12 +300,30 @@ __device__ double lane_strip(const double *__restrict__ X, const double *__restr
     col_fill<MODE != GAUSS_PHASE>(A, __ldg(px + c0), __ldg(py + c0), __ldg(pz + c0), kv);
     Acc acc;
     int c = c0;
+#ifdef LC_PREFETCH
+    // the next pair of columns is loaded one iteration ahead (column loads off the critical path)
+    double n1x = 0, n1y = 0, n1z = 0, n2x = 0, n2y = 0, n2z = 0;
+    if (c + 2 <= c1) {
+        n1x = __ldg(px + c + 1); n1y = __ldg(py + c + 1); n1z = __ldg(pz + c + 1);
+        n2x = __ldg(px + c + 2); n2y = __ldg(py + c + 2); n2z = __ldg(pz + c + 2);
+    }
+    for (; c + 2 <= c1; c += 2) {
+        const double l1x = n1x, l1y = n1y, l1z = n1z, l2x = n2x, l2y = n2y, l2z = n2z;
+        if (c + 4 <= c1) {
+            n1x = __ldg(px + c + 3); n1y = __ldg(py + c + 3); n1z = __ldg(pz + c + 3);
+            n2x = __ldg(px + c + 4); n2y = __ldg(py + c + 4); n2z = __ldg(pz + c + 4);
+        }
+        col_step<MODE, FULL, false>(A, B, l1x, l1y, l1z, kv, rv, acc);
+        col_step<MODE, FULL, true>(B, A, l2x, l2y, l2z, kv, rv, acc);
+    }
+#else
     for (; c + 2 <= c1; c += 2) {
         const double l1x = __ldg(px + c + 1), l1y = __ldg(py + c + 1), l1z = __ldg(pz + c + 1);
         const double l2x = __ldg(px + c + 2), l2y = __ldg(py + c + 2), l2z = __ldg(pz + c + 2);
         col_step<MODE, FULL, false>(A, B, l1x, l1y, l1z, kv, rv, acc);
         col_step<MODE, FULL, true>(B, A, l2x, l2y, l2z, kv, rv, acc);
     }
+#endif
     if (c < c1) col_step<MODE, FULL, true>(A, B, __ldg(px + c + 1), __ldg(py + c + 1), __ldg(pz + c + 1), kv, rv, acc);
     if (MODE == GAUSS_PHASE && (acc.bad || !isfinite(acc.sx) || !isfinite(acc.sy)))
         // coincident vertices, w == 0, underflow or NaN input: the exact per-pair path
@@ -385,6 +433,58 @@ __device__ __forceinline__ int64_t find_pair(const int64_t *__restrict__ item_of
     return lo;
 }
 
+// One work item (row-block group ir, column-strip group ic of pair tiling g):
+// every lane's strip, then the fixed xor butterfly.  Returns the butterfly sum
+// (lane 0's value is the item partial of every path).
+template <int MODE, bool KSM>
+__device__ __forceinline__ double item_value(const double *__restrict__ X, const double *__restrict__ Y,
+                                             const double *__restrict__ Z, const PairGeom &g, int ir, int ic, int lane,
+                                             double *ksh) {
+    const int rbm = (1 << g.rb_log2) - 1;
+    const int my_rb = lane & rbm, my_cs = lane >> g.rb_log2;
+    const int row0 = ((ir << g.rb_log2) + my_rb) * R;
+    const int64_t c0l = ((int64_t)ic * (32 >> g.rb_log2) + my_cs) * g.cl;
+    const int c0 = (int)(c0l < g.ncols ? c0l : g.ncols);
+    const int c1 = min(c0 + g.cl, g.ncols);
+    double val = 0.0;
+    if constexpr (MODE == GAUSS_ANGLESUM) {   // items of 32 whole rows: lane = row
+        const int row = (ir << 5) + lane;
+        if (row < g.nrows) val = lane_anglesum(X, Y, Z, g.row_off, row, g.col_off, g.ncols);
+    } else if (row0 < g.nrows && c0 < c1) {
+        if (MODE == GAUSS_REF) {
+            val = lane_strip_ref(X, Y, Z, g.row_off, g.nrows, g.col_off, row0, c0, c1);
+        } else if (KSM) {
+            KSm kv{ksh + threadIdx.x};
+            val = row0 + R <= g.nrows
+                      ? lane_strip<MODE, true>(X, Y, Z, g.row_off, g.nrows, g.col_off, row0, c0, c1, kv)
+                      : lane_strip<MODE, false>(X, Y, Z, g.row_off, g.nrows, g.col_off, row0, c0, c1, kv);
+        } else {
+            KReg kv;
+            val = row0 + R <= g.nrows
+                      ? lane_strip<MODE, true>(X, Y, Z, g.row_off, g.nrows, g.col_off, row0, c0, c1, kv)
+                      : lane_strip<MODE, false>(X, Y, Z, g.row_off, g.nrows, g.col_off, row0, c0, c1, kv);
+        }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) val += __shfl_xor_sync(0xffffffffu, val, off);
+    return val;
+}
+
+// Claim the next unit of work (item or pair) for the whole warp; the abort flag
+// (fused path: the concurrent pass-1 checks found the run unusable, a staged
+// rerun follows) is read with the claim so both round trips overlap.  Returns
+// false when the warp should leave.
+__device__ __forceinline__ bool claim(unsigned long long *counter, const int *abort, int lane, int64_t &k) {
+    unsigned long long c = 0;
+    int ab = 0;
+    if (lane == 0) {
+        c = atomicAdd(counter, 1ULL);
+        if (abort) ab = *(volatile const int *)abort;
+    }
+    k = (int64_t)__shfl_sync(0xffffffffu, c, 0);
+    return !__shfl_sync(0xffffffffu, ab, 0);
+}
+
 template <int MODE, int MINB, bool KSM = false>
 __global__ void __launch_bounds__(kCtaThreads, MINB) gauss_items_kernel(
     const double *__restrict__ X, const double *__restrict__ Y, const double *__restrict__ Z,
@@ -393,58 +493,91 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) gauss_items_kernel(
     const int *__restrict__ abort, const int64_t *__restrict__ d_bounds) {
     __shared__ double ksh[KSM ? 3 * (R + 1) * kCtaThreads : 1];
     const int lane = threadIdx.x & 31;
-    if (d_bounds) {   // sharded fused path: this shard's cost-balanced item range (shard_bounds_kernel)
+    if (d_bounds) {   // sharded: this shard's cost-balanced item range (shard_bounds_kernel)
         item_begin = d_bounds[shard];
         item_end = d_bounds[shard + 1];
-    } else if (d_end) {   // fused path: item count on the device
+    } else if (d_end) {   // item count on the device
         const int64_t n = *d_end;
         if (n < item_end) item_end = n;
     }
     for (;;) {
-        unsigned long long k = 0;
-        // fused path: the abort flag (the concurrent pass-1 checks found the run
-        // unusable; a staged rerun follows) is read with the item claim, so both
-        // round trips overlap; lane 0 reads it so the whole warp leaves together
-        int ab = 0;
-        if (lane == 0) {
-            k = atomicAdd(counter, 1ULL);
-            if (abort) ab = *(volatile const int *)abort;
-        }
-        k = __shfl_sync(0xffffffffu, k, 0);
-        if (__shfl_sync(0xffffffffu, ab, 0)) break;
-        const int64_t it = item_begin + (int64_t)k;
+        int64_t k;
+        if (!claim(counter, abort, lane, k)) break;
+        const int64_t it = item_begin + k;
         if (it >= item_end) break;
         const ItemRec rec = items[it];
-        const PairGeom &g = rec.g;
-        const int ir = rec.ir, ic = rec.ic;
-        const int rbm = (1 << g.rb_log2) - 1;
-        const int my_rb = lane & rbm, my_cs = lane >> g.rb_log2;
-        const int row0 = ((ir << g.rb_log2) + my_rb) * R;
-        const int64_t c0l = ((int64_t)ic * (32 >> g.rb_log2) + my_cs) * g.cl;
-        const int c0 = (int)(c0l < g.ncols ? c0l : g.ncols);
-        const int c1 = min(c0 + g.cl, g.ncols);
-        double val = 0.0;
-        if constexpr (MODE == GAUSS_ANGLESUM) {   // items of 32 whole rows: lane = row
-            const int row = (ir << 5) + lane;
-            if (row < g.nrows) val = lane_anglesum(X, Y, Z, g.row_off, row, g.col_off, g.ncols);
-        } else if (row0 < g.nrows && c0 < c1) {
-            if (MODE == GAUSS_REF) {
-                val = lane_strip_ref(X, Y, Z, g.row_off, g.nrows, g.col_off, row0, c0, c1);
-            } else if (KSM) {
-                KSm kv{ksh + threadIdx.x};
-                val = row0 + R <= g.nrows
-                          ? lane_strip<MODE, true>(X, Y, Z, g.row_off, g.nrows, g.col_off, row0, c0, c1, kv)
-                          : lane_strip<MODE, false>(X, Y, Z, g.row_off, g.nrows, g.col_off, row0, c0, c1, kv);
-            } else {
-                KReg kv;
-                val = row0 + R <= g.nrows
-                          ? lane_strip<MODE, true>(X, Y, Z, g.row_off, g.nrows, g.col_off, row0, c0, c1, kv)
-                          : lane_strip<MODE, false>(X, Y, Z, g.row_off, g.nrows, g.col_off, row0, c0, c1, kv);
-            }
+        const double val = item_value<MODE, KSM>(X, Y, Z, rec.g, rec.ir, rec.ic, lane, ksh);
+        if (lane == 0) partials[it] = val;
+    }
+}
+
+// Fused path: warps claim whole PAIRS (loops of <= 256 segments: 1-2 items each)
+// and evaluate the pair's items in order, so no per-item records are built.
+// The pair sum is formed exactly as warp_pair_sum forms it from the item
+// partials (item k's partial — lane 0's butterfly value — added into lane k mod
+// 32, then the xor butterfly), so raw is bitwise the staged path's.  Unsharded:
+// raw / lk / flags go to the device arrays and straight into the pinned result
+// arrays (zero-copy writes spread over the kernel: no export pass after it).
+// Sharded: raw goes to partials[p] (the exchange buffer) for the pairs of this
+// shard's cost-balanced range.
+template <int MODE, int MINB>
+__global__ void __launch_bounds__(kCtaThreads, MINB) gauss_pairs_kernel(
+    const double *__restrict__ X, const double *__restrict__ Y, const double *__restrict__ Z,
+    const PairGeom *__restrict__ pg, const int64_t *__restrict__ dP, int64_t pcap,
+    unsigned long long *__restrict__ counter, const int *__restrict__ abort, const int64_t *__restrict__ d_bounds,
+    int shard, double *__restrict__ partials, double *__restrict__ raw, int64_t *__restrict__ lk,
+    uint8_t *__restrict__ flags, double *__restrict__ h_raw, int64_t *__restrict__ h_lk,
+    uint8_t *__restrict__ h_flags, const Pass1Args chk) {
+    __shared__ int32_t sidx[kCtaThreads / 32][2][kAnyCap];
+    __shared__ float sbox[kCtaThreads / 32][2][6 * kAnyCap];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int64_t b = 0, e = *dP < pcap ? *dP : pcap;
+    if (d_bounds) {
+        b = d_bounds[shard];
+        e = d_bounds[shard + 1];
+    }
+#if LC_PAIRS_STATIC
+    // non-persistent: CTA c takes a contiguous chunk of the pairs (its warps
+    // interleaved) and exits, so higher-priority kernels (the pass-1 checks) get
+    // the SM slots the retiring CTAs free instead of waiting for the kernel's end
+    const int64_t chunk = (e - b + gridDim.x - 1) / gridDim.x;
+    const int64_t cb = b + (int64_t)blockIdx.x * chunk, ce = cb + chunk < e ? cb + chunk : e;
+    for (int64_t p = cb + w; p < ce; p += kCtaThreads / 32) {
+        if (abort && __shfl_sync(0xffffffffu, lane == 0 ? *(volatile const int *)abort : 0, 0)) break;
+#else
+    for (;;) {
+        int64_t k;
+        if (!claim(counter, abort, lane, k)) break;
+        const int64_t p = b + k;
+        if (p >= e) break;
+#endif
+        if (chk.box)   // the pair's pass-1 check (a hit aborts the fused run: staged path)
+            brute_any_pair(p, chk.box, chk.fbox, chk.M, chk.loff, chk.lbox, chk.L, chk.pairs, sidx[w][0], sidx[w][1],
+                           sbox[w][0], sbox[w][1], lane, chk.marked, chk.abort);
+        const PairGeom g = pg[p];
+        const int n = g.items_r * g.items_c;
+        double s = 0.0;
+        for (int it = 0; it < n; ++it) {
+            const double v = __shfl_sync(0xffffffffu, item_value<MODE, false>(X, Y, Z, g, it / g.items_c,
+                                                                                it % g.items_c, lane, nullptr), 0);
+            if (lane == (it & 31)) s += v;
         }
 #pragma unroll
-        for (int off = 16; off; off >>= 1) val += __shfl_xor_sync(0xffffffffu, val, off);
-        if (lane == 0) partials[it] = val;
+        for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) {
+            if (partials) {
+                partials[p] = s;
+            } else {
+                int64_t r;
+                const uint8_t f = round_link(s, r);
+                raw[p] = s;
+                lk[p] = r;
+                flags[p] = f;
+                h_raw[p] = s;
+                h_lk[p] = r;
+                h_flags[p] = f;
+            }
+        }
     }
 }
 
@@ -578,7 +711,7 @@ __global__ void __launch_bounds__(1024) shard_bounds_kernel(const PairGeom *__re
         for (int w = 0; w < nw; ++w) t += wsum[w];
         s_total = t;
         s_carry = 0;
-        const int64_t n = P > 0 ? item_off[P] : 0;
+        const int64_t n = P > 0 ? (item_off ? item_off[P] : P) : 0;   // item_off null: pair ranges
         bounds[0] = 0;
         for (int k = 1; k <= shards; ++k) bounds[k] = n;
     }
@@ -603,9 +736,9 @@ __global__ void __launch_bounds__(1024) shard_bounds_kernel(const PairGeom *__re
             for (int k = 1; k < shards; ++k) {
                 const int64_t t = (int64_t)((__int128)total * k / shards);
                 if (excl <= t && t < excl + c) {
-                    const int64_t items_p = item_off[p + 1] - item_off[p];
+                    const int64_t items_p = item_off ? item_off[p + 1] - item_off[p] : 1;
                     int64_t local = (int64_t)(((__int128)(t - excl) * items_p + c - 1) / c);
-                    bounds[k] = item_off[p] + (local < items_p ? local : items_p);
+                    bounds[k] = (item_off ? item_off[p] : p) + (local < items_p ? local : items_p);
                 }
             }
         __syncthreads();
@@ -694,7 +827,7 @@ void launch_gauss_items(int mode, const double *X, const double *Y, const double
                           unsigned long long *, double *, const int64_t *, int, int, const int *, const int64_t *);
     // default phase kernel: 3 resident CTAs/SM (168 regs); modes 16-20 are A/B variants
     // (1 CTA/SM with 232 regs; 4 CTAs; row vertices in shared memory; 2 CTAs/SM)
-    static const Kern table[] = {gauss_items_kernel<GAUSS_PHASE, 3>,       gauss_items_kernel<GAUSS_ATAN, 1>,
+    static const Kern table[] = {gauss_items_kernel<GAUSS_PHASE, LC_MINB>, gauss_items_kernel<GAUSS_ATAN, 1>,
                                  gauss_items_kernel<GAUSS_REF, 1>,         gauss_items_kernel<GAUSS_ANGLESUM, 4>,
                                  gauss_items_kernel<GAUSS_PHASE, 1>,       gauss_items_kernel<GAUSS_PHASE, 4>,
                                  gauss_items_kernel<GAUSS_PHASE, 4, true>, gauss_items_kernel<GAUSS_PHASE, 3, true>,
@@ -706,6 +839,7 @@ void launch_gauss_items(int mode, const double *X, const double *Y, const double
     static int occ[kModes] = {};   // resident CTAs per SM, queried once per mode
     const int threads = 128;
     if (!occ[slot]) {
+        LC_CUDA(cudaFuncSetAttribute((const void *)fn, cudaFuncAttributePreferredSharedMemoryCarveout, kGaussCarveout));
         int per = 0;
         LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void *)fn, threads, 0));
         occ[slot] = per < 1 ? 1 : per;
@@ -717,6 +851,54 @@ void launch_gauss_items(int mode, const double *X, const double *Y, const double
     if (blocks > blocks_needed) blocks = blocks_needed;
     fn<<<(unsigned)blocks, threads, 0, s>>>(X, Y, Z, items, item_begin, item_end, counter, partials, d_end, shard,
                                             shards, abort, d_bounds);
+    LC_CHECK_LAUNCH();
+}
+
+void launch_gauss_pairs(int mode, const double *X, const double *Y, const double *Z, const PairGeom *pg,
+                        const int64_t *d_P, int64_t pcap, unsigned long long *counter, const int *abort,
+                        const int64_t *d_bounds, int shard, double *partials, double *raw, int64_t *lk, uint8_t *flags,
+                        double *h_raw, int64_t *h_lk, uint8_t *h_flags, cudaStream_t s, const Pass1Args &chk) {
+    if (pcap <= 0) return;
+    using Kern = void (*)(const double *, const double *, const double *, const PairGeom *, const int64_t *, int64_t,
+                          unsigned long long *, const int *, const int64_t *, int, double *, double *, int64_t *,
+                          uint8_t *, double *, int64_t *, uint8_t *, const Pass1Args);
+    Kern fn;
+    switch (mode) {
+        case GAUSS_PHASE: fn = gauss_pairs_kernel<GAUSS_PHASE, LC_MINB>; break;
+        case GAUSS_ATAN: fn = gauss_pairs_kernel<GAUSS_ATAN, 1>; break;
+        case GAUSS_REF: fn = gauss_pairs_kernel<GAUSS_REF, 1>; break;
+        default: throw Error(LC_ERR_ARG, "the pair-claiming Gauss kernel takes modes phase / atan / ref");
+    }
+    static int occ[3] = {};
+    const int threads = kCtaThreads;
+    if (!occ[mode]) {
+        // keep a slice of the SM's unified L1 as shared memory: the pass-1 checks
+        // (brute_any_lite, 4.6 KB of shared memory per block) then co-reside with the
+        // persistent Gauss CTAs instead of waiting for them to exit
+        LC_CUDA(cudaFuncSetAttribute((const void *)fn, cudaFuncAttributePreferredSharedMemoryCarveout, kGaussCarveout));
+        int per = 0;
+        LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void *)fn, threads, 0));
+        occ[mode] = per < 1 ? 1 : per;
+    }
+    int64_t blocks = (int64_t)num_sms() * occ[mode];
+#if LC_PAIRS_STATIC
+    blocks *= LC_PAIRS_WAVES;   // several short-lived CTA waves (see the kernel)
+#endif
+    const int64_t need = ceil_div(pcap, threads / 32);
+    if (blocks > need) blocks = need;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)blocks);
+    cfg.blockDim = dim3(threads);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    int prio_lo = 0, prio_hi = 0;
+    LC_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    attr[0].id = cudaLaunchAttributePriority;
+    attr[0].val.priority = LC_PAIRS_PRIORITY_LOW ? prio_lo : prio_hi;   // below the checks branch
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    LC_CUDA(cudaLaunchKernelEx(&cfg, fn, X, Y, Z, pg, d_P, pcap, counter, abort, d_bounds, shard, partials, raw, lk,
+                               flags, h_raw, h_lk, h_flags, chk));
     LC_CHECK_LAUNCH();
 }
 

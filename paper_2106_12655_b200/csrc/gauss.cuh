@@ -107,7 +107,30 @@ void launch_gauss_items(int mode, const double *X, const double *Y, const double
                         int shards = 1, const int *abort = nullptr, bool counter_zeroed = false,
                         const int64_t *d_bounds = nullptr);
 
-// Cost-balanced shard boundaries of the item list: bounds[0..shards] (device),
+// Fused path: warps claim whole pairs [0, *d_P) (or [d_bounds[shard], d_bounds[shard+1]) of a
+// cost-balanced pair split) and evaluate each pair's items in order; raw is bitwise the
+// item path's per-pair sum.  partials == null: raw / lk / flags written to the device
+// arrays and to the pinned host arrays; else raw to partials[p] (the sharded exchange).
+// Pass-1 check inputs (pass1.cuh brute_any_pair): when box != null every claimed
+// pair is checked first (hits -> *marked, *abort = 1).
+struct Pass1Args {
+    const double *box = nullptr;   // segment boxes (6 x M)
+    const float *fbox = nullptr;   // outward-rounded float copy
+    int64_t M = 0;
+    const int64_t *loff = nullptr;
+    const double *lbox = nullptr;  // loop boxes (6 x L)
+    int64_t L = 0;
+    const int32_t *pairs = nullptr;
+    unsigned long long *marked = nullptr;
+    int *abort = nullptr;
+};
+void launch_gauss_pairs(int mode, const double *X, const double *Y, const double *Z, const PairGeom *pg,
+                        const int64_t *d_P, int64_t pcap, unsigned long long *counter, const int *abort,
+                        const int64_t *d_bounds, int shard, double *partials, double *raw, int64_t *lk, uint8_t *flags,
+                        double *h_raw, int64_t *h_lk, uint8_t *h_flags, cudaStream_t s,
+                        const Pass1Args &chk = Pass1Args());
+
+// Cost-balanced shard boundaries of the item list (item_off null: of the pair list): bounds[0..shards] (device),
 // shard r owns items [bounds[r], bounds[r+1]); each shard's segment-pair cost is
 // within one item of total / shards.  d_P: device pair count (<= Pcap) or null.
 void launch_shard_bounds(const PairGeom *pg, const int64_t *item_off, int64_t Pcap, const int64_t *d_P, int shards,

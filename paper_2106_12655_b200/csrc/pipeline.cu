@@ -97,7 +97,8 @@ __global__ void __launch_bounds__(256) reduce_export_kernel(
         // then the xor butterfly: bitwise equal to reduce_pairs_kernel), with the
         // 9 offsets in one load and the pairs' first partials loaded side by side
         const int64_t pb = c0 + warp * kPairsPerWarp;
-        const int64_t off = lane <= kPairsPerWarp && pb + lane <= P ? item_off[pb + lane] : 0;
+        // item_off null: one partial per pair (the pair-claiming Gauss kernel's sums)
+        const int64_t off = lane <= kPairsPerWarp && pb + lane <= P ? (item_off ? item_off[pb + lane] : pb + lane) : 0;
         double v[kPairsPerWarp];
         int64_t b[kPairsPerWarp], e[kPairsPerWarp];
 #pragma unroll
@@ -172,7 +173,10 @@ void Pipeline::init(cudaStream_t st) {
     LC_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     LC_CUDA(cudaStreamCreateWithPriority(&side[0], cudaStreamNonBlocking, prio_lo));
     LC_CUDA(cudaStreamCreateWithPriority(&side[1], cudaStreamNonBlocking, prio_hi));
-    for (cudaEvent_t *e : {&ev_fork, &ev_chords, &ev_pairs, &ev_checks, &ev_stage})
+    // the fused run's critical path (derive -> PLS -> Gauss sum) at the highest priority:
+    // its small latency-bound kernels are dispatched ahead of the chord branch's blocks
+    LC_CUDA(cudaStreamCreateWithPriority(&crit, cudaStreamNonBlocking, prio_hi));
+    for (cudaEvent_t *e : {&ev_fork, &ev_chords, &ev_pairs, &ev_checks, &ev_stage, &ev_enter, &ev_leave})
         LC_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
 }
 
@@ -202,10 +206,11 @@ void Pipeline::release() {
     graph_exec = nullptr;
     for (auto &e : ev)
         if (e) cudaEventDestroy(e);
-    for (cudaEvent_t e : {ev_fork, ev_chords, ev_pairs, ev_checks, ev_stage})
+    for (cudaEvent_t e : {ev_fork, ev_chords, ev_pairs, ev_checks, ev_stage, ev_enter, ev_leave})
         if (e) cudaEventDestroy(e);
     for (auto &x : side)
         if (x) cudaStreamDestroy(x);
+    if (crit) cudaStreamDestroy(crit);
 }
 
 // Stage event on the stream; inside a stream capture it must become an
@@ -228,6 +233,16 @@ float Pipeline::stage_ms(int e0, int e1) {
 }
 
 // ------------------------------------------------------------------ model
+
+void Pipeline::reserve_derived() {
+    d_seg_box.reserve(sizeof(double) * 6 * (M > 0 ? M : 1), s);
+    d_seg_fbox.reserve(sizeof(float) * 6 * (M > 0 ? M : 1), s);
+    d_seg_loop.reserve(sizeof(int32_t) * (M > 0 ? M : 1), s);
+    d_loop_box.reserve(sizeof(double) * 6 * (L > 0 ? L : 1), s);
+    d_min_diag.reserve(sizeof(unsigned long long) * (L > 0 ? L : 1), s);
+    d_model_exp.reserve(sizeof(int), s);
+    d_loop_keys.reserve(sizeof(unsigned long long) * 6 * (L > 0 ? L : 1), s);
+}
 
 void Pipeline::derive() {
     if (!model_ready) throw Error(LC_ERR_STATE, "no model uploaded");
@@ -540,6 +555,7 @@ bool Pipeline::build_gauss_items_checked(int mode) {
 }
 
 void Pipeline::finish_items() {
+    items_ready = true;
     d_partials.reserve(sizeof(double) * (size_t)(n_items > 0 ? n_items : 1), s);
     d_item_pair.reserve(sizeof(ItemRec) * (size_t)(n_items > 0 ? n_items : 1), s);
     launch_item_pairs(d_item_off.as<int64_t>(), d_pg.as<PairGeom>(), P, n_items, d_item_pair.as<ItemRec>(), s);
@@ -551,6 +567,7 @@ void Pipeline::finish_items() {
 void Pipeline::run_gauss(int mode, int64_t item_begin, int64_t item_end, double *partials_ext,
                          cudaEvent_t ev0, cudaEvent_t ev1) {
     if (!gauss_mode_valid(mode)) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
+    if (!items_ready) throw Error(LC_ERR_STATE, "no work items built (lc_prepare_gauss)");
     if (gauss_mode_sequential(mode) != items_seq)
         throw Error(LC_ERR_STATE, "the work items were built for another Gauss-sum mode");
     double *out = partials_ext ? partials_ext : d_partials.as<double>();
@@ -626,7 +643,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
     d_counter.reserve(sizeof(unsigned long long), s);
     reserve_pls_grid(L, pls_sc, s);   // prezeroed by the run's first kernel
     d_tot.reserve(4 * sizeof(int64_t), s);
-    part_cap = icap;   // partials at absolute item ids; a shard writes only its cost-balanced range
+    part_cap = pcap;   // pair partials (sharded); a shard writes only its cost-balanced pair range
     d_partials.reserve(sizeof(double) * part_cap, s);
     d_bounds.reserve(sizeof(int64_t) * (shards + 1), s);
     d_item_pair.reserve(sizeof(ItemRec) * icap, s);
@@ -643,8 +660,27 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
     const PreCounters *ctr = nullptr;
     // The whole device sequence; stream-capturable (no allocation once the
     // buffers are sized, no host-pageable copies, no host syncs).
+    const bool split = seg_boxes_split_ok(L, max_loop);
+    if (split) reserve_derived();
     auto enqueue = [&]() {
-        derive();   // records EV_BEGIN; (re)sizes the box buffers read below
+        // the whole sequence runs on the high-priority critical stream, joined to the
+        // caller's stream at both ends (captured with it into the graph)
+        cudaStream_t caller = s;
+        LC_CUDA(cudaEventRecord(ev_enter, caller));
+        LC_CUDA(cudaStreamWaitEvent(crit, ev_enter, 0));
+        s = crit;
+        struct Restore {
+            cudaStream_t &ref, val;
+            ~Restore() { ref = val; }
+        } restore{s, caller};
+        tl_reset();
+        if (split) {   // the loop half of derive on the critical path, the segment half on the chord branch
+            record(EV_BEGIN);
+            derived = true;
+            derived_in_run = true;
+        } else {
+            derive();   // records EV_BEGIN; (re)sizes the box buffers read below
+        }
         DiscInput in{d_coeffs.as<double>(), d_t.as<double>(), d_loff.as<int64_t>(), d_seg_loop.as<int32_t>(),
                      d_seg_box.as<double>(), d_loop_box.as<double>(), d_min_diag.as<unsigned long long>(),
                      d_model_exp.as<int>(), L, M, d_pairs.as<int32_t>(), pcap};
@@ -666,13 +702,34 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
                 {pc + 7, 1, 0u},                              // pad
                 {disc_sc.val_err2.ptr, 2, (unsigned)INT_MAX}, // validation: first bad loop / pair
                 {d_counter.ptr, 2, 0u},                       // Gauss item claim counter
+                {d_model_exp.ptr, 1, 0u},                     // coordinate exponent (atomicMax)
             };
             launch_grid_prezero(L, pls_sc, extra, (int)(sizeof extra / sizeof extra[0]), s);
         }
-        // branch 1: the chords need only the model — they run beside the PLS
+        tl_mark("prezero", s);
+        // branch 1: the chords need only the model — they run beside the PLS; the
+        // segment half of derive goes with them, after the loop half (which it
+        // would otherwise slow down by sharing the HBM bandwidth on the critical path)
+        if (split) {
+            const double *vp = model_poly ? d_verts_in.as<double>() : nullptr;
+            const double *cp = model_poly ? nullptr : d_coeffs.as<double>(), *tp = model_poly ? nullptr : d_t.as<double>();
+            // loop boxes + minimum diagonals with the PLS grid reduction folded in
+            launch_loop_grid(cp, tp, vp, d_loff.as<int64_t>(), L, d_min_diag.as<unsigned long long>(),
+                             d_loop_box.as<double>(), pls_sc, s);
+            tl_mark("loop_boxes", s);
+        }
         LC_CUDA(cudaEventRecord(ev_fork, s));
         LC_CUDA(cudaStreamWaitEvent(side[0], ev_fork, 0));
+        if (split) {
+            const double *vp = model_poly ? d_verts_in.as<double>() : nullptr;
+            const double *cp = model_poly ? nullptr : d_coeffs.as<double>(), *tp = model_poly ? nullptr : d_t.as<double>();
+            launch_seg_boxes_split(cp, tp, vp, d_loff.as<int64_t>(), L, M, false, d_seg_box.as<double>(),
+                                   d_seg_fbox.as<float>(), d_seg_loop.as<int32_t>(), d_model_exp.as<int>(), nullptr,
+                                   nullptr, side[0]);
+            tl_mark("S0:seg_boxes", side[0]);
+        }
         launch_discretize_chords(in, prm, disc_sc, dout, side[0]);
+        tl_mark("S0:chords", side[0]);
         LC_CUDA(cudaEventRecord(ev_chords, side[0]));
         if (n_excl > 0)
             LC_CUDA(cudaMemcpyAsync(pls_sc.excl.ptr, h_excl.ptr, sizeof(uint64_t) * n_excl, cudaMemcpyHostToDevice,
@@ -680,48 +737,73 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
         const int *dmx = nullptr;
         launch_pls_grid(d_loop_box.as<double>(), L, n_excl, pls_sc, d_pairs.as<int32_t>(), pcap, d_loff.as<int64_t>(),
                         d_pg.as<PairGeom>(), d_item_off.as<int64_t>(), d_tot.as<int64_t>(), icap, s, &dmx,
-                        /*prezeroed=*/true);
+                        /*prezeroed=*/true, /*grid_ready=*/split);
         const int64_t *dP = d_tot.as<int64_t>(), *d_items = d_tot.as<int64_t>() + 1;
         record(EV_PLS);
         // branch 2: pass-1 detection + validation only feed the status — they run
         // beside the work items and the Gauss sum
         LC_CUDA(cudaEventRecord(ev_pairs, s));
         LC_CUDA(cudaStreamWaitEvent(side[1], ev_pairs, 0));
-        launch_discretize_checks(in, dP, prm, disc_sc, dout, side[1], ev_chords, &ctr);
+        // (Pass1Args: the pass-1 pair check can also run inside the Gauss kernel — measured
+        // slower than this branch beside it, 0.49 vs 0.47 ms per Kusari step)
+        launch_discretize_checks(in, dP, prm, disc_sc, dout, side[1], ev_chords, &ctr, /*brute_in_gauss=*/false);
+        tl_mark("S1:checks", side[1]);
         record(EV_DISC, side[1]);
         // the pair list is final: the copy engine moves the whole capacity to pinned
         // memory while the sums run (no SM time; the host reads the first P)
         LC_CUDA(cudaMemcpyAsync(hp, d_pairs.ptr, sizeof(int32_t) * 2 * pcap, cudaMemcpyDeviceToHost, side[1]));
         LC_CUDA(cudaEventRecord(ev_checks, side[1]));
-        launch_item_pairs_dev(d_item_off.as<int64_t>(), d_pg.as<PairGeom>(), pcap, dP, icap, d_item_pair.as<ItemRec>(),
-                              s);
-        if (sharded) {   // items of other shards: the bits of -0.0 (the int64 MAX all-reduce identity)
+        tl_mark("pls_items", s);
+        if (sharded) {   // pairs of other shards: the bits of -0.0 (the int64 MAX all-reduce identity)
             fill_bits_kernel<<<(unsigned)ceil_div(part_cap, 256), 256, 0, s>>>(
                 reinterpret_cast<unsigned long long *>(d_partials.ptr), part_cap, 0x8000000000000000ull);
             LC_CHECK_LAUNCH();
-            launch_shard_bounds(d_pg.as<PairGeom>(), d_item_off.as<int64_t>(), pcap, dP, shards,
-                                d_bounds.as<int64_t>(), s);
+            launch_shard_bounds(d_pg.as<PairGeom>(), nullptr, pcap, dP, shards, d_bounds.as<int64_t>(), s);
         }
         LC_CUDA(cudaStreamWaitEvent(s, ev_chords, 0));   // the sum reads the chords
+        tl_mark("chords_joined", s);
         record(EV_GAUSS0);
-        launch_gauss_items(mode, dout.X.as<double>(), dout.Y.as<double>(), dout.Z.as<double>(), d_item_pair.as<ItemRec>(),
-                           0, icap,
-                           d_counter.as<unsigned long long>(), d_partials.as<double>(), s, d_items, shard, shards,
-                           &disc_sc.prectr.as<PreCounters>()->abort, /*counter_zeroed=*/true,
-                           sharded ? d_bounds.as<int64_t>() : nullptr);
+        // warps claim whole pairs; unsharded, each pair's raw / lk / flags go straight to
+        // the pinned result arrays as it completes (no reduce / export pass after the sum)
+        // (LINKCERT_PAIR_EXPORT=1: A/B — the sums go to the partials, a coalesced export follows)
+        static const bool pair_export = [] {
+            const char *e = getenv("LINKCERT_PAIR_EXPORT");
+            return e && e[0] == '1';
+        }();
+        const bool via_partials = sharded || pair_export;
+        Pass1Args chk;
+        chk.box = d_seg_box.as<double>();
+        chk.fbox = d_seg_fbox.as<float>();
+        chk.M = M;
+        chk.loff = d_loff.as<int64_t>();
+        chk.lbox = d_loop_box.as<double>();
+        chk.L = L;
+        chk.pairs = d_pairs.as<int32_t>();
+        chk.marked = &disc_sc.prectr.as<PreCounters>()->marked;
+        chk.abort = &disc_sc.prectr.as<PreCounters>()->abort;
+        launch_gauss_pairs(mode, dout.X.as<double>(), dout.Y.as<double>(), dout.Z.as<double>(), d_pg.as<PairGeom>(), dP,
+                           pcap, d_counter.as<unsigned long long>(), &disc_sc.prectr.as<PreCounters>()->abort,
+                           sharded ? d_bounds.as<int64_t>() : nullptr, shard,
+                           via_partials ? d_partials.as<double>() : nullptr, d_raw.as<double>(), d_lk.as<int64_t>(),
+                           d_flags.as<uint8_t>(), reinterpret_cast<double *>(hr), reinterpret_cast<int64_t *>(hl),
+                           reinterpret_cast<uint8_t *>(hf), s, Pass1Args());
         record(EV_GAUSS1);
+        tl_mark("gauss", s);
         LC_CUDA(cudaStreamWaitEvent(s, ev_checks, 0));
-        if (!sharded) {   // per-pair sums straight into pinned memory, with the status
-            launch_reduce_export(d_partials.as<double>(), d_item_off.as<int64_t>(), dP, pcap, d_items, dmx, ctr,
-                                 dout.d_val_err, st, d_raw.as<double>(), d_lk.as<int64_t>(), d_flags.as<uint8_t>(),
+        if (!sharded && pair_export) {
+            launch_reduce_export(d_partials.as<double>(), nullptr, dP, pcap, d_items, dmx, ctr, dout.d_val_err, st,
+                                 d_raw.as<double>(), d_lk.as<int64_t>(), d_flags.as<uint8_t>(),
                                  reinterpret_cast<double *>(hr), reinterpret_cast<int64_t *>(hl),
                                  reinterpret_cast<uint8_t *>(hf), s);
-        } else {   // sharded: the status only; lc_shard_finish reduces after the exchange
+        } else {   // the run's status record (sharded: lc_shard_finish reduces after the exchange)
             export_results_kernel<<<1, 32, 0, s>>>(dP, pcap, d_items, dmx, ctr, dout.d_val_err, nullptr, nullptr,
                                                    nullptr, nullptr, st, nullptr, nullptr, nullptr, nullptr);
             LC_CHECK_LAUNCH();
         }
-        record(EV_END);   // "reduce" = Gauss end -> sums (and status) in pinned memory
+        record(EV_END);   // "reduce" = Gauss end -> status in pinned memory
+        tl_mark("export", s);
+        LC_CUDA(cudaEventRecord(ev_leave, crit));
+        LC_CUDA(cudaStreamWaitEvent(caller, ev_leave, 0));
     };
 
     static const bool no_graph = [] {
@@ -764,7 +846,8 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
         graph_launches = launch_counter().load() - n0;
         const bool same_gen = alloc_generation().load() == key.gen;
         if (same_gen) {
-            LC_CUDA(cudaGraphInstantiate(&graph_exec, g, 0));
+            // honour the captured per-node priorities (critical path / checks high, chords low)
+            LC_CUDA(cudaGraphInstantiateWithFlags(&graph_exec, g, cudaGraphInstantiateFlagUseNodePriority));
             graph_key = key;
         }
         if (same_gen) {
@@ -803,6 +886,7 @@ int Pipeline::finish_fast() {
     const bool pend_sharded = pend.sharded;
     char *hp = pend.hp, *hr = pend.hr, *hl = pend.hl, *hf = pend.hf;
     LC_CUDA(cudaStreamSynchronize(s));
+    tl_print(last_fast_graph ? "fused graph" : "fused");
     fast_seen = key;
     fast_seen.gen = alloc_generation().load();
     fast_seen_valid = true;
@@ -817,6 +901,7 @@ int Pipeline::finish_fast() {
     P = f.P;
     n_items = f.n_items;
     items_seq = false;
+    items_ready = false;   // the fused run claims pairs: no item records (lc_prepare_gauss builds them)
     V = dout.V;
     Vc = dout.Vc;
     gX = dout.X.as<double>();
@@ -843,7 +928,7 @@ int Pipeline::finish_fast() {
 int Pipeline::shard_finish() {
     if (!pend.on) throw Error(LC_ERR_STATE, "no pending sharded run");
     const int64_t *dP = d_tot.as<int64_t>();
-    launch_reduce_export(d_partials.as<double>(), d_item_off.as<int64_t>(), dP, pend.pcap, nullptr, nullptr, nullptr,
+    launch_reduce_export(d_partials.as<double>(), nullptr, dP, pend.pcap, nullptr, nullptr, nullptr,
                          nullptr, nullptr, d_raw.as<double>(), d_lk.as<int64_t>(), d_flags.as<uint8_t>(),
                          reinterpret_cast<double *>(pend.hr), reinterpret_cast<int64_t *>(pend.hl),
                          reinterpret_cast<uint8_t *>(pend.hf), s);

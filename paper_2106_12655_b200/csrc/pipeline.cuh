@@ -26,6 +26,8 @@ struct Pipeline {
     // fused run: side branches (chord write || PLS; pass-1 checks || items + Gauss sum)
     cudaStream_t side[2] = {};
     cudaEvent_t ev_fork = nullptr, ev_chords = nullptr, ev_pairs = nullptr, ev_checks = nullptr;
+    cudaStream_t crit = nullptr;                          // fused run's critical path (highest priority)
+    cudaEvent_t ev_enter = nullptr, ev_leave = nullptr;   // caller stream <-> crit joins
 
     // Model: packed monomial cubics (linkcert LoopGeometry arrays, geometry.py:206-296).
     DevBuf d_coeffs, d_t, d_loff, d_seg_box, d_seg_fbox, d_loop_keys, d_seg_loop, d_loop_box, d_min_diag, d_model_exp, d_verts_in;
@@ -73,6 +75,7 @@ struct Pipeline {
         if (!derived) derive();
     }
     void ensure_coeffs();
+    void reserve_derived();   // the derive() outputs' buffers (the fused path derives in two halves)
     void upload_model(const double *coeffs, const double *t, const int64_t *loff, int64_t nloops);
     // closed polylines given as vertices only (a0 = v_k, a1 = v_k+1 - v_k, a2 = a3 = 0, t = [0, 1])
     void upload_model_polylines(const double *verts, const int64_t *loff, int64_t nloops);
@@ -99,6 +102,7 @@ struct Pipeline {
     // validation result (one sync); false + derr on a ValidationError
     bool build_gauss_items_checked(int mode = GAUSS_PHASE);
     bool items_seq = false;   // the current items are whole-row (sequential-mode) items
+    bool items_ready = false; // d_item_pair holds the item records of the current pairs
     void run_gauss(int mode, int64_t item_begin, int64_t item_end, double *partials_ext, cudaEvent_t ev0,
                    cudaEvent_t ev1);
     void reduce_pairs(const double *partials_ext);

@@ -101,7 +101,8 @@ __global__ void seg_boxes_kernel(const double *__restrict__ coeffs, const double
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
                 const double a0 = verts[3 * m + d], a1 = verts[3 * nx + d] - a0;
-                const double v0 = eval_axis(a0, a1, 0.0, 0.0, 0.0), v1 = eval_axis(a0, a1, 0.0, 0.0, 1.0);
+                // eval_axis at t = 0 and 1 with a2 = a3 = 0, bitwise: a0 (+0 for -0) and a0 + a1 (+0 for -0)
+                const double v0 = __dadd_rn(a0, 0.0), v1 = __dadd_rn(__dadd_rn(a0, a1), 0.0);
                 bl[d] = np_min(v0, v1);
                 bh[d] = np_max(v0, v1);
             }
@@ -156,8 +157,13 @@ __global__ void seg_boxes_kernel(const double *__restrict__ coeffs, const double
 // segments, e.g. chainmail rings): warp per loop, lanes over its segments —
 // no loop lookup, plain warp reductions, direct stores of the loop box and
 // minimum diagonal (no keys, no atomics but the exponent).
+// SEG_OUT / LOOP_OUT: the fused path splits the outputs over two branches —
+// the loop-level ones (loop boxes, minimum diagonals: PLS input, on the critical
+// path) and the segment-level ones (boxes, float boxes, segment loop, exponent:
+// read only by the chord and pass-1 branches) — so the critical path writes
+// ~L x 56 B instead of ~M x 76 B.
 constexpr int64_t kLoopWarpMax = 1024;
-template <bool POLY>
+template <bool POLY, bool SEG_OUT = true, bool LOOP_OUT = true>
 __global__ void seg_boxes_loop_kernel(const double *__restrict__ coeffs, const double *__restrict__ t,
                                       const double *__restrict__ verts, const int64_t *__restrict__ loff, int64_t L,
                                       int64_t M, double *__restrict__ box, float *__restrict__ fbox,
@@ -178,30 +184,40 @@ __global__ void seg_boxes_loop_kernel(const double *__restrict__ coeffs, const d
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
                 const double a0 = verts[3 * m + d], a1 = verts[3 * nx + d] - a0;
-                const double v0 = eval_axis(a0, a1, 0.0, 0.0, 0.0), v1 = eval_axis(a0, a1, 0.0, 0.0, 1.0);
+                // eval_axis at t = 0 and 1 with a2 = a3 = 0, bitwise: a0 (+0 for -0) and a0 + a1 (+0 for -0)
+                const double v0 = __dadd_rn(a0, 0.0), v1 = __dadd_rn(__dadd_rn(a0, a1), 0.0);
                 bl[d] = np_min(v0, v1);
                 bh[d] = np_max(v0, v1);
             }
         } else {
             tight_box(coeffs + 12 * m, t[2 * m], t[2 * m + 1], bl, bh);
         }
-        seg_loop[m] = (int32_t)l;
+        if (SEG_OUT) seg_loop[m] = (int32_t)l;
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-            box[d * M + m] = bl[d];
-            box[(3 + d) * M + m] = bh[d];
-            if (fbox) {
-                fbox[d * M + m] = __double2float_rd(bl[d]);
-                fbox[(3 + d) * M + m] = __double2float_ru(bh[d]);
+            if (SEG_OUT) {
+                box[d * M + m] = bl[d];
+                box[(3 + d) * M + m] = bh[d];
+                if (fbox) {
+                    fbox[d * M + m] = __double2float_rd(bl[d]);
+                    fbox[(3 + d) * M + m] = __double2float_ru(bh[d]);
+                }
+                ex = max(ex, max(exp_field(bl[d]), exp_field(bh[d])));
             }
-            ex = max(ex, max(exp_field(bl[d]), exp_field(bh[d])));
             v[d] = np_min(v[d], bl[d]);
             v[3 + d] = np_max(v[3 + d], bh[d]);
         }
-        const double dx = __dsub_rn(bh[0], bl[0]), dy = __dsub_rn(bh[1], bl[1]), dz = __dsub_rn(bh[2], bl[2]);
-        const unsigned long long q = (unsigned long long)__double_as_longlong(
-            __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
-        dg = q < dg ? q : dg;
+        if (LOOP_OUT) {
+            const double dx = __dsub_rn(bh[0], bl[0]), dy = __dsub_rn(bh[1], bl[1]), dz = __dsub_rn(bh[2], bl[2]);
+            const unsigned long long q = (unsigned long long)__double_as_longlong(
+                __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+            dg = q < dg ? q : dg;
+        }
+    }
+    if (!LOOP_OUT) {   // segment outputs only: the exponent is the one loop-level value they need
+        ex = __reduce_max_sync(0xffffffffu, ex);
+        if (lane == 0 && max_exp && ex > 0) atomicMax(max_exp, ex);
+        return;
     }
 #pragma unroll
     for (int off = 16; off; off >>= 1) {
@@ -585,6 +601,102 @@ __global__ void grid_reduce_kernel(const double *__restrict__ lbox, int64_t L, u
 }
 
 
+// The fused path's loop half of derive with the grid reduction folded in:
+// grid-stride warps per loop (loops of <= kLoopWarpMax segments) write the loop
+// box and minimum squared diagonal; the loop boxes are reduced per block
+// (ordered-key warp reductions, then shared memory) into the model box and the
+// largest loop extent (one atomic set per block), and the last block derives
+// the grid parameters — grid_reduce_kernel's outputs with no second pass.
+template <bool POLY>
+__global__ void __launch_bounds__(128) loop_grid_kernel(const double *__restrict__ coeffs, const double *__restrict__ t,
+                                                        const double *__restrict__ verts,
+                                                        const int64_t *__restrict__ loff, int64_t L,
+                                                        unsigned long long *__restrict__ loop_min_diag2,
+                                                        double *__restrict__ lbox, unsigned long long *__restrict__ acc,
+                                                        unsigned *__restrict__ done, int64_t max_cells,
+                                                        GridParams *__restrict__ gp) {
+    __shared__ unsigned long long sk[4][7];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // block accumulators (ordered keys): min lo x3, max hi x3, max extent
+    unsigned long long bk[7] = {~0ULL, ~0ULL, ~0ULL, 0ULL, 0ULL, 0ULL, 0ULL};
+    const int64_t nw = (int64_t)gridDim.x * 4;
+    for (int64_t l = (int64_t)blockIdx.x * 4 + warp; l < L; l += nw) {
+        const int64_t b = loff[l], e = loff[l + 1];
+        double v[6] = {CUDART_INF, CUDART_INF, CUDART_INF, -CUDART_INF, -CUDART_INF, -CUDART_INF};
+        unsigned long long dg = ~0ULL;
+#pragma unroll 2
+        for (int64_t m = b + lane; m < e; m += 32) {
+            double bl[3], bh[3];
+            if (POLY) {
+                const int64_t nx = m + 1 < e ? m + 1 : b;
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    const double a0 = verts[3 * m + d], a1 = verts[3 * nx + d] - a0;
+                    // eval_axis at t = 0 and 1 with a2 = a3 = 0, bitwise: a0 (+0 for -0) and a0 + a1 (+0 for -0)
+                const double v0 = __dadd_rn(a0, 0.0), v1 = __dadd_rn(__dadd_rn(a0, a1), 0.0);
+                    bl[d] = np_min(v0, v1);
+                    bh[d] = np_max(v0, v1);
+                }
+            } else {
+                tight_box(coeffs + 12 * m, t[2 * m], t[2 * m + 1], bl, bh);
+            }
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                v[d] = np_min(v[d], bl[d]);
+                v[3 + d] = np_max(v[3 + d], bh[d]);
+            }
+            const double dx = __dsub_rn(bh[0], bl[0]), dy = __dsub_rn(bh[1], bl[1]), dz = __dsub_rn(bh[2], bl[2]);
+            const unsigned long long q = (unsigned long long)__double_as_longlong(
+                __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+            dg = q < dg ? q : dg;
+        }
+        // loop box: ordered-key warp reductions (2 redux per value instead of 10 shuffles)
+        unsigned long long k[6];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            k[d] = group_min_u64(0xffffffffu, ord_key(v[d]));
+            k[3 + d] = group_max_u64(0xffffffffu, ord_key(v[3 + d]));
+        }
+        dg = group_min_u64(0xffffffffu, dg);
+        if (lane == 0) {
+            double ext = 0.0;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                const double lo = ord_val(k[d]), hi = ord_val(k[3 + d]);
+                lbox[d * L + l] = lo;
+                lbox[(3 + d) * L + l] = hi;
+                ext = fmax(ext, hi - lo);
+                bk[d] = k[d] < bk[d] ? k[d] : bk[d];
+                bk[3 + d] = k[3 + d] > bk[3 + d] ? k[3 + d] : bk[3 + d];
+            }
+            const unsigned long long ke = ord_key(ext);
+            bk[6] = ke > bk[6] ? ke : bk[6];
+            loop_min_diag2[l] = dg;
+        }
+    }
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < 7; ++q) sk[warp][q] = bk[q];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 4; ++w) {
+            for (int q = 0; q < 3; ++q) bk[q] = sk[w][q] < bk[q] ? sk[w][q] : bk[q];
+            for (int q = 3; q < 7; ++q) bk[q] = sk[w][q] > bk[q] ? sk[w][q] : bk[q];
+        }
+        for (int q = 0; q < 3; ++q) atomicMin(acc + q, bk[q]);
+        for (int q = 3; q < 7; ++q) atomicMax(acc + q, bk[q]);
+        __threadfence();
+        const bool last = atomicAdd(done, 1u) == gridDim.x - 1;
+        if (last) {
+            __threadfence();
+            unsigned long long a[7];
+            for (int q = 0; q < 7; ++q) a[q] = atomicAdd(acc + q, 0ULL);   // L2-coherent reads
+            grid_finalize(a, max_cells, gp);
+            *done = 0;
+        }
+    }
+}
+
 // Row i's slots sorted by j -> pairs[off[i] ...] (insertion sort, <= kRowSlots).
 __global__ void slots_compact_kernel(const int *__restrict__ row_count, const int64_t *__restrict__ off, int64_t L,
                                      const int32_t *__restrict__ slots, int32_t *__restrict__ pairs, int64_t cap) {
@@ -678,6 +790,36 @@ __global__ void unpack_pairs_kernel(const uint64_t *__restrict__ keys, int64_t P
 
 }  // namespace
 
+bool seg_boxes_split_ok(int64_t L, int64_t max_loop_segments) {
+    return L > 0 && max_loop_segments >= 0 && max_loop_segments <= kLoopWarpMax;
+}
+
+void launch_seg_boxes_split(const double *coeffs, const double *t, const double *verts, const int64_t *loff, int64_t L,
+                            int64_t M, bool loop_part, double *seg_box, float *seg_fbox, int32_t *seg_loop,
+                            int *max_exp, unsigned long long *loop_min_diag2, double *loop_box, cudaStream_t s) {
+    const unsigned blocks = (unsigned)ceil_div(L * 32, 128);
+    if (loop_part) {
+        if (verts)
+            seg_boxes_loop_kernel<true, false, true><<<blocks, 128, 0, s>>>(nullptr, nullptr, verts, loff, L, M, nullptr,
+                                                                            nullptr, nullptr, loop_min_diag2, loop_box,
+                                                                            nullptr);
+        else
+            seg_boxes_loop_kernel<false, false, true><<<blocks, 128, 0, s>>>(coeffs, t, nullptr, loff, L, M, nullptr,
+                                                                             nullptr, nullptr, loop_min_diag2, loop_box,
+                                                                             nullptr);
+    } else {
+        if (verts)
+            seg_boxes_loop_kernel<true, true, false><<<blocks, 128, 0, s>>>(nullptr, nullptr, verts, loff, L, M, seg_box,
+                                                                            seg_fbox, seg_loop, nullptr, nullptr,
+                                                                            max_exp);
+        else
+            seg_boxes_loop_kernel<false, true, false><<<blocks, 128, 0, s>>>(coeffs, t, nullptr, loff, L, M, seg_box,
+                                                                             seg_fbox, seg_loop, nullptr, nullptr,
+                                                                             max_exp);
+    }
+    LC_CHECK_LAUNCH();
+}
+
 void launch_seg_boxes(const double *coeffs, const double *t, const double *verts, const int64_t *loff, int64_t L,
                       int64_t M, double *seg_box, int32_t *seg_loop, unsigned long long *loop_min_diag2, int *max_exp,
                       cudaStream_t s, float *seg_fbox, unsigned long long *loop_keys, double *loop_box,
@@ -765,7 +907,7 @@ void launch_grid_prezero(int64_t L, PlsScratch &sc, const ZeroRange *extra, int 
 // host sync): sc.offs[L] = P, *sc.counter = largest row count, slots in
 // sc.pair_keys, row counts in sc.idx.  Excluded keys already in sc.excl.
 static void grid_prefix(const double *loop_box, int64_t L, int64_t n_excl, PlsScratch &sc, cudaStream_t s,
-                        const int64_t *item_loff = nullptr, bool prezeroed = false) {
+                        const int64_t *item_loff = nullptr, bool prezeroed = false, bool grid_ready = false) {
     const int64_t max_cells = pls_grid_max_cells(L);
     sc.axis.reserve(sizeof(GridParams), s);
     sc.keys.reserve(sizeof(int64_t) * (max_cells + 1), s);         // cell counts
@@ -788,26 +930,36 @@ static void grid_prefix(const double *loop_box, int64_t L, int64_t n_excl, PlsSc
         LC_CUDA(cudaMemsetAsync(acc, 0xff, 3 * sizeof(unsigned long long), s));
         LC_CUDA(cudaMemsetAsync(acc + 3, 0, 5 * sizeof(unsigned long long), s));   // + the block counter
     }
-    grid_reduce_kernel<<<(unsigned)(ceil_div(L, 256) < 148 ? ceil_div(L, 256) : 148), 256, 0, s>>>(
-        loop_box, L, acc, reinterpret_cast<unsigned *>(acc + 7), max_cells, gp);
-    LC_CHECK_LAUNCH();
+    if (!grid_ready) {   // else loop_grid_kernel derived the grid parameters with the loop boxes
+        grid_reduce_kernel<<<(unsigned)(ceil_div(L, 256) < 148 ? ceil_div(L, 256) : 148), 256, 0, s>>>(
+            loop_box, L, acc, reinterpret_cast<unsigned *>(acc + 7), max_cells, gp);
+        LC_CHECK_LAUNCH();
+        tl_mark("grid_reduce", s);
+    }
     if (!prezeroed) LC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (max_cells + 1), s));
-    const unsigned gl = (unsigned)ceil_div(L, 256);
-    cell_count_kernel<<<gl, 256, 0, s>>>(loop_box, L, gp, cnt, sc.lcell.as<int32_t>(), sc.lrank.as<int32_t>());
+    // thread-per-loop kernels in 64-thread blocks: the latency chains spread over every SM
+    const unsigned gl = (unsigned)ceil_div(L, 64);
+    cell_count_kernel<<<gl, 64, 0, s>>>(loop_box, L, gp, cnt, sc.lcell.as<int32_t>(), sc.lrank.as<int32_t>());
     LC_CHECK_LAUNCH();
+    tl_mark("cell_count", s);
     const size_t b = exclusive_scan_i64_tmp_bytes(max_cells + 1), b2 = exclusive_scan_i64_tmp_bytes(L + 1);
     sc.cub_tmp.reserve((b > b2 ? b : b2) + 16, s);
     exclusive_scan_i64(cnt, coff, max_cells + 1, sc.cub_tmp.ptr, sc.cub_tmp.bytes, s);
-    cell_scatter_kernel<<<gl, 256, 0, s>>>(loop_box, L, coff, sc.lcell.as<int32_t>(), sc.lrank.as<int32_t>(),
+    tl_mark("cell_scan", s);
+    cell_scatter_kernel<<<gl, 64, 0, s>>>(loop_box, L, coff, sc.lcell.as<int32_t>(), sc.lrank.as<int32_t>(),
                                            sc.perm.as<int32_t>(), sc.sbox.as<double>());
     LC_CHECK_LAUNCH();
+    tl_mark("cell_scatter", s);
     if (!prezeroed) LC_CUDA(cudaMemsetAsync(max_count, 0, sizeof(int), s));
     grid_query_warp_kernel<true><<<(unsigned)ceil_div(L * 32, 256), 256, 0, s>>>(loop_box, L, gp, coff, sc.perm.as<int32_t>(),
                                                sc.sbox.as<double>(), sc.excl.as<uint64_t>(), n_excl, row_count,
                                                sc.pair_keys.as<int32_t>(), nullptr, nullptr,
                                                sc.counts.as<int64_t>(), max_count, item_loff);
     LC_CHECK_LAUNCH();
+    tl_mark("query", s);
+    // (a single-block scan measured 14 us here vs 8.4 us for DeviceScan's init + scan)
     exclusive_scan_i64(sc.counts.as<int64_t>(), sc.offs.as<int64_t>(), L + 1, sc.cub_tmp.ptr, sc.cub_tmp.bytes, s);
+    tl_mark("row_scan", s);
 }
 
 int64_t run_pls(const double *loop_box, int64_t L, const uint64_t *h_excl, int64_t n_excl, PlsScratch &sc,
@@ -907,11 +1059,30 @@ int64_t run_pls(const double *loop_box, int64_t L, const uint64_t *h_excl, int64
     return (int64_t)P;
 }
 
+void launch_loop_grid(const double *coeffs, const double *t, const double *verts, const int64_t *loff, int64_t L,
+                      unsigned long long *loop_min_diag2, double *loop_box, PlsScratch &sc, cudaStream_t s) {
+    const int64_t max_cells = pls_grid_max_cells(L);
+    sc.axis.reserve(sizeof(GridParams), s);
+    sc.counts.reserve(sizeof(int64_t) * (L + 8 > 8 ? L + 8 : 8), s);
+    unsigned long long *acc = (unsigned long long *)sc.counts.ptr;   // prezeroed keys + block counter
+    int64_t blocks = ceil_div(L, 4);
+    if (blocks > 148 * 6) blocks = 148 * 6;
+    if (verts)
+        loop_grid_kernel<true><<<(unsigned)blocks, 128, 0, s>>>(nullptr, nullptr, verts, loff, L, loop_min_diag2,
+                                                                loop_box, acc, reinterpret_cast<unsigned *>(acc + 7),
+                                                                max_cells, sc.axis.as<GridParams>());
+    else
+        loop_grid_kernel<false><<<(unsigned)blocks, 128, 0, s>>>(coeffs, t, nullptr, loff, L, loop_min_diag2,
+                                                                 loop_box, acc, reinterpret_cast<unsigned *>(acc + 7),
+                                                                 max_cells, sc.axis.as<GridParams>());
+    LC_CHECK_LAUNCH();
+}
+
 void launch_pls_grid(const double *loop_box, int64_t L, int64_t n_excl, PlsScratch &sc, int32_t *pairs, int64_t cap,
                      const int64_t *loff, PairGeom *pg, int64_t *item_off, int64_t *d_tot, int64_t item_cap,
-                     cudaStream_t s, const int **d_max_row, bool prezeroed) {
-    grid_prefix(loop_box, L, n_excl, sc, s, loff, prezeroed);
-    slots_compact_items_kernel<<<(unsigned)ceil_div(L, 256), 256, 0, s>>>(sc.idx.as<int>(), sc.offs.as<int64_t>(), L,
+                     cudaStream_t s, const int **d_max_row, bool prezeroed, bool grid_ready) {
+    grid_prefix(loop_box, L, n_excl, sc, s, loff, prezeroed, grid_ready);
+    slots_compact_items_kernel<<<(unsigned)ceil_div(L, 64), 64, 0, s>>>(sc.idx.as<int>(), sc.offs.as<int64_t>(), L,
                                                                           sc.pair_keys.as<int32_t>(), pairs, cap, loff,
                                                                           pg, item_off, d_tot, sc.counter.as<int>(),
                                                                           item_cap);

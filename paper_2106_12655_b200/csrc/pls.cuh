@@ -19,6 +19,14 @@ namespace lc {
 // coeffs/t (the from_polyline arrays are formed in registers).
 // max_loop_segments (host-known, >= 0) <= 1024 with loop_box: warp-per-loop
 // variant (no loop lookup, no keys); otherwise thread per segment + keys.
+// The fused path's derive in two halves on two streams (loops of <= 1024 segments):
+// loop_part = loop boxes + minimum squared diagonals; otherwise the segment
+// boxes, float boxes, segment loops and the coordinate exponent (max_exp zeroed
+// by the caller).
+bool seg_boxes_split_ok(int64_t L, int64_t max_loop_segments);
+void launch_seg_boxes_split(const double *coeffs, const double *t, const double *verts, const int64_t *loff, int64_t L,
+                            int64_t M, bool loop_part, double *seg_box, float *seg_fbox, int32_t *seg_loop,
+                            int *max_exp, unsigned long long *loop_min_diag2, double *loop_box, cudaStream_t s);
 void launch_seg_boxes(const double *coeffs, const double *t, const double *verts, const int64_t *loff, int64_t L,
                       int64_t M, double *seg_box, int32_t *seg_loop, unsigned long long *loop_min_diag2, int *max_exp,
                       cudaStream_t s, float *seg_fbox = nullptr, unsigned long long *loop_keys = nullptr,
@@ -56,7 +64,12 @@ constexpr int kRowSlots = 16;
 struct PairGeom;
 void launch_pls_grid(const double *loop_box, int64_t L, int64_t n_excl, PlsScratch &sc, int32_t *pairs, int64_t cap,
                      const int64_t *loff, PairGeom *pg, int64_t *item_off, int64_t *d_tot, int64_t item_cap,
-                     cudaStream_t s, const int **d_max_row, bool prezeroed = false);
+                     cudaStream_t s, const int **d_max_row, bool prezeroed = false, bool grid_ready = false);
+// Fused path: loop boxes + minimum squared diagonals with the grid reduction folded
+// in (launch_pls_grid(..., grid_ready = true) then skips its reduction); needs the
+// keys prezeroed (launch_grid_prezero) and loops of <= 1024 segments.
+void launch_loop_grid(const double *coeffs, const double *t, const double *verts, const int64_t *loff, int64_t L,
+                      unsigned long long *loop_min_diag2, double *loop_box, PlsScratch &sc, cudaStream_t s);
 
 // Scratch sizes of launch_pls_grid, and one kernel doing the memsets it issues
 // (grid-reduce keys, cell counts, largest row count) plus `extra` int ranges —

@@ -14,6 +14,7 @@ offsets (L+1)) — cached while the loops are unchanged.
 from __future__ import annotations
 
 from dataclasses import dataclass, field
+from operator import attrgetter, itemgetter
 
 import numpy as np
 
@@ -199,8 +200,9 @@ class LoopGeometry:
     (the reference aliases the caller's arrays, geometry.py:225-230), so a
     CurveModel can cache what it uploads and hashes.  Reassigning an attribute
     (loop.coeffs = ...) is tracked; editing an array in place raises ValueError.
-    A closed loop built by from_polyline remembers its vertex array: a model of
-    such loops reaches the GPU and the digest as vertices only (24 B/segment).
+    A closed loop built by from_polyline remembers its vertex array (with its
+    address and row count, `_pv`): a model of such loops reaches the GPU and the
+    digest as vertices only (24 B/segment).
     """
 
     coeffs = _loop_attr("_coeffs", _owned)
@@ -251,7 +253,7 @@ class LoopGeometry:
         self = cls.__new__(cls)
         d = self.__dict__
         d["_coeffs"], d["_t"], d["_closed"], d["_cp"] = coeffs, t, True, verts
-        d["_pv"] = (verts, ptr)
+        d["_pv"] = (verts, ptr, verts.shape[0])
         d["_stamp"] = 0
         return self
 
@@ -289,7 +291,7 @@ class LoopGeometry:
         coeffs[:, 0] = starts
         coeffs[:, 1] = ends - starts
         loop = LoopGeometry.__new__(LoopGeometry)
-        pv = (verts, verts.ctypes.data) if closed and len(verts) else None
+        pv = (verts, verts.ctypes.data, len(verts)) if closed and len(verts) else None
         loop._setup(coeffs, None, closed, verts, None, pv)
         return loop
 
@@ -332,6 +334,9 @@ def compute_xi(loops):
     return total / count if count else 0.0
 
 
+_get_pv, _item0, _item1, _item2 = attrgetter("_pv"), itemgetter(0), itemgetter(1), itemgetter(2)
+
+
 class ModelSnapshot:
     """What one certificate / verify call hands to the digest thread and to the
     device upload, taken after one validity check of the model's loops.
@@ -350,13 +355,13 @@ class ModelSnapshot:
         self.epoch = epoch
         self._packed = None
         L = len(self.key)
-        pv = [lp._pv for lp in self.key]
+        pv = list(map(_get_pv, self.key))          # C-level iteration: ~0.05 us per loop
         self.poly = L > 0 and None not in pv
         self.off = np.zeros(L + 1, dtype=np.int64)
         if self.poly:
-            self.vrefs = [p[0] for p in pv]
-            self.vptrs = np.fromiter((p[1] for p in pv), dtype=np.uint64, count=L)
-            np.cumsum(np.fromiter((len(v) for v in self.vrefs), dtype=np.int64, count=L), out=self.off[1:])
+            self.vrefs = list(map(_item0, pv))
+            self.vptrs = np.fromiter(map(_item1, pv), dtype=np.uint64, count=L)
+            np.cumsum(np.fromiter(map(_item2, pv), dtype=np.int64, count=L), out=self.off[1:])
             self.closed = np.ones(L, dtype=np.uint8)
         else:
             self.vrefs = self.vptrs = None

@@ -1,6 +1,6 @@
 """Gauss-kernel A/B microbenchmark (CUDA events around the kernel only).
 
-  python tools/kbench.py [--modes 0,3,4,5] [--reps 10]
+  python tools/kbench.py [--modes 0,16,17,18] [--reps 10]
 """
 import argparse
 import os
@@ -32,7 +32,7 @@ def bench_staged(ctx, modes, reps, label, sp):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--modes", default="0,3,4,5")
+    ap.add_argument("--modes", default="0")
     ap.add_argument("--reps", type=int, default=10)
     a = ap.parse_args()
     modes = [int(x) for x in a.modes.split(",")]

@@ -19,16 +19,16 @@ from paper_2106_12655_b200.discretize import DiscretizationParams  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--case", default="kusari", choices=["kusari", "torus", "ribbon"])
-    ap.add_argument("--mode", default="phase", choices=list(_native.GAUSS_MODES))
+    ap.add_argument("--mode", default="phase", choices=list(_native.GAUSS_MODES) + ["anglesum"])
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--n", type=int, default=1024)
     a = ap.parse_args()
     ctx = _native.context(0)
-    mode = _native.GAUSS_MODES[a.mode]
+    mode = _native.GAUSS_ANGLESUM if a.mode == "anglesum" else _native.GAUSS_MODES[a.mode]
     if a.case == "kusari":
         m = gen.kusari_tube(after=True)
-        coeffs, t, off = m.packed()
-        ctx.upload_model(coeffs, t, off)
+        from paper_2106_12655_b200.pls import upload
+        upload(m, ctx)
         for _ in range(a.reps):
             device_step(ctx, m.xi, excluded_keys(()), DiscretizationParams(), mode=mode)
     else:
