@@ -223,6 +223,19 @@ LC_API int lc_run_pipeline_shard_async(lc_ctx *ctx, const uint64_t *excluded_key
                                        int shards, double **partials_dev, int64_t *part_cap);
 LC_API int lc_shard_finish(lc_ctx *ctx, int *fused);
 LC_API int lc_get_stream(lc_ctx *ctx, void **stream);
+/* Device early exit for verify(..., early_exit=True) (certify.py:195-216).
+ * lc_set_early_exit hands the library the reference certificate — keys
+ * (i << 32 | j) sorted unique, values lk (nonzero) — and, enable != 0, makes the
+ * next single-GPU fused runs evaluate the candidate pairs against it in the
+ * reference's order (certificate pairs, then the other candidates, each in key
+ * order): the first pair whose value differs (or is NaN / ambiguous) ends the
+ * evaluation and every pair after it in that order is cancelled.  Pairs before it
+ * are all evaluated, so the caller replays the reference's report from the
+ * results.  lc_early_exit_stats: that pair's place (-1: none) and the number of
+ * pairs evaluated (-1: the last run was not a device early-exit run). */
+LC_API int lc_set_early_exit(lc_ctx *ctx, const uint64_t *ref_keys, const int64_t *ref_lk, int64_t n_ref,
+                             int enable);
+LC_API int lc_early_exit_stats(lc_ctx *ctx, int64_t *first_fail_place, int64_t *n_evaluated);
 /* Path of the last lc_run_pipeline: 0 staged, 1 fused, 2 fused replayed from
  * the captured CUDA graph (same shape as the previous run, no reallocation). */
 LC_API int lc_last_run_fused(lc_ctx *ctx);

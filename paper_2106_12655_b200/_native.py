@@ -99,6 +99,8 @@ SIGNATURES = {
     "lc_run_pipeline_sharded": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
                                                 ctypes.c_int, ctypes.c_int64, ctypes.c_int, _c_int64_p]),
     "lc_shard_bounds": (ctypes.c_int, [_vp, ctypes.c_int, _vp]),
+    "lc_set_early_exit": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int]),
+    "lc_early_exit_stats": (ctypes.c_int, [_vp, _c_int64_p, _c_int64_p]),
     "lc_get_stream": (ctypes.c_int, [_vp, ctypes.POINTER(_vp)]),
     "lc_float_repr_many": (ctypes.c_int64, [_vp, ctypes.c_int64, ctypes.c_int, _vp, ctypes.c_int64]),
     "lc_model_digest": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p]),
@@ -591,6 +593,24 @@ class Context:
         with self.lock:
             _check(self.lib.lc_shard_bounds(self.handle, int(shards), _ptr(out)))
         return out
+
+    def set_early_exit(self, ref_keys=None, ref_lk=None):
+        """Arm (certificate keys / values) or disarm (None) the device early exit."""
+        if ref_keys is None:
+            with self.lock:
+                _check(self.lib.lc_set_early_exit(self.handle, None, None, 0, 0))
+            return
+        k = np.ascontiguousarray(ref_keys, dtype=np.uint64)
+        v = np.ascontiguousarray(ref_lk, dtype=np.int64)
+        with self.lock:
+            _check(self.lib.lc_set_early_exit(self.handle, _ptr(k), _ptr(v), k.size, 1))
+
+    def early_exit_stats(self):
+        """(place of the first failing pair or -1, pairs evaluated or -1) of the last fused run."""
+        f, n = ctypes.c_int64(0), ctypes.c_int64(0)
+        with self.lock:
+            _check(self.lib.lc_early_exit_stats(self.handle, ctypes.byref(f), ctypes.byref(n)))
+        return f.value, n.value
 
     def stream_ptr(self):
         out = _vp()

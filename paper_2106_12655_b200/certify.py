@@ -456,8 +456,15 @@ def verify(
             ctx = _native.context()
             ctx.session.acquire()   # the result views stay ours through the diff
             try:
-                pairs, raw, lk, flags, _ = run_device_pipeline(model, excluded, params, ctx=ctx, snapshot=snap,
-                                                               mode=ds_mode(choice.ds_variant))
+                if early_exit:   # single GPU: pairs past the first failure are cancelled on the device
+                    arr = reference.array
+                    ctx.set_early_exit(_pair_keys(arr[:, :2]).astype(np.uint64), arr[:, 2])
+                try:
+                    pairs, raw, lk, flags, _ = run_device_pipeline(model, excluded, params, ctx=ctx, snapshot=snap,
+                                                                   mode=ds_mode(choice.ds_variant))
+                finally:
+                    if early_exit:
+                        ctx.set_early_exit(None)
             except Exception:
                 ctx.session.release()
                 raise

@@ -552,6 +552,17 @@ int lc_run_pipeline_sharded(lc_ctx *ctx, const uint64_t *excluded_keys, int64_t 
     });
 }
 
+int lc_set_early_exit(lc_ctx *ctx, const uint64_t *ref_keys, const int64_t *ref_lk, int64_t n_ref, int enable) {
+    return guarded(ctx, [&] { ctx->pipe.set_early_exit(ref_keys, ref_lk, n_ref, enable != 0); });
+}
+
+int lc_early_exit_stats(lc_ctx *ctx, int64_t *first_fail_place, int64_t *n_evaluated) {
+    return guarded(ctx, [&] {
+        if (first_fail_place) *first_fail_place = ctx->pipe.ee_first_fail;
+        if (n_evaluated) *n_evaluated = ctx->pipe.ee_n_eval;
+    });
+}
+
 int lc_shard_finish(lc_ctx *ctx, int *fused) {
     if (fused) *fused = 0;
     int fr = FAST_FALLBACK;

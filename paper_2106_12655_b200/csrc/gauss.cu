@@ -527,7 +527,7 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) gauss_pairs_kernel(
     unsigned long long *__restrict__ counter, const int *__restrict__ abort, const int64_t *__restrict__ d_bounds,
     int shard, double *__restrict__ partials, double *__restrict__ raw, int64_t *__restrict__ lk,
     uint8_t *__restrict__ flags, double *__restrict__ h_raw, int64_t *__restrict__ h_lk,
-    uint8_t *__restrict__ h_flags, const Pass1Args chk) {
+    uint8_t *__restrict__ h_flags, const Pass1Args chk, const EarlyExitArgs ee) {
     __shared__ int32_t sidx[kCtaThreads / 32][2][kAnyCap];
     __shared__ float sbox[kCtaThreads / 32][2][6 * kAnyCap];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -551,6 +551,10 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) gauss_pairs_kernel(
         const int64_t p = b + k;
         if (p >= e) break;
 #endif
+        if (ee.posv) {   // early exit: a pair past the first failure found so far is cancelled
+            if ((unsigned long long)ee.posv[p] > *(volatile unsigned long long *)ee.first_fail) continue;
+            if (lane == 0) atomicAdd(ee.n_eval, 1ULL);
+        }
         if (chk.box)   // the pair's pass-1 check (a hit aborts the fused run: staged path)
             brute_any_pair(p, chk.box, chk.fbox, chk.M, chk.loff, chk.lbox, chk.L, chk.pairs, sidx[w][0], sidx[w][1],
                            sbox[w][0], sbox[w][1], lane, chk.marked, chk.abort);
@@ -576,6 +580,9 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) gauss_pairs_kernel(
                 h_raw[p] = s;
                 h_lk[p] = r;
                 h_flags[p] = f;
+                // NaN / ambiguous raw: compute_link raises there (kernels.py:68-73), which ends the
+                // reference's evaluation order too
+                if (ee.posv && (r != ee.want[p] || f)) atomicMin(ee.first_fail, (unsigned long long)ee.posv[p]);
             }
         }
     }
@@ -857,11 +864,12 @@ void launch_gauss_items(int mode, const double *X, const double *Y, const double
 void launch_gauss_pairs(int mode, const double *X, const double *Y, const double *Z, const PairGeom *pg,
                         const int64_t *d_P, int64_t pcap, unsigned long long *counter, const int *abort,
                         const int64_t *d_bounds, int shard, double *partials, double *raw, int64_t *lk, uint8_t *flags,
-                        double *h_raw, int64_t *h_lk, uint8_t *h_flags, cudaStream_t s, const Pass1Args &chk) {
+                        double *h_raw, int64_t *h_lk, uint8_t *h_flags, cudaStream_t s, const Pass1Args &chk,
+                        const EarlyExitArgs &ee) {
     if (pcap <= 0) return;
     using Kern = void (*)(const double *, const double *, const double *, const PairGeom *, const int64_t *, int64_t,
                           unsigned long long *, const int *, const int64_t *, int, double *, double *, int64_t *,
-                          uint8_t *, double *, int64_t *, uint8_t *, const Pass1Args);
+                          uint8_t *, double *, int64_t *, uint8_t *, const Pass1Args, const EarlyExitArgs);
     Kern fn;
     switch (mode) {
         case GAUSS_PHASE: fn = gauss_pairs_kernel<GAUSS_PHASE, LC_MINB>; break;
@@ -898,7 +906,60 @@ void launch_gauss_pairs(int mode, const double *X, const double *Y, const double
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     LC_CUDA(cudaLaunchKernelEx(&cfg, fn, X, Y, Z, pg, d_P, pcap, counter, abort, d_bounds, shard, partials, raw, lk,
-                               flags, h_raw, h_lk, h_flags, chk));
+                               flags, h_raw, h_lk, h_flags, chk, ee));
+    LC_CHECK_LAUNCH();
+}
+
+namespace {
+__device__ __forceinline__ int64_t find_key(const uint64_t *__restrict__ keys, int64_t n, uint64_t k) {
+    int64_t lo = 0, hi = n;   // first index with keys[idx] >= k
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (keys[mid] < k) lo = mid + 1; else hi = mid;
+    }
+    return lo < n && keys[lo] == k ? lo : -1;
+}
+
+__device__ __forceinline__ uint64_t pair_key(const int32_t *__restrict__ pairs, int64_t p) {
+    return ((uint64_t)(uint32_t)pairs[2 * p] << 32) | (uint32_t)pairs[2 * p + 1];
+}
+
+// Threads [0, pcap): candidate pairs; threads [pcap, pcap + n_ref): certificate entries.
+__global__ void early_exit_order_kernel(const int32_t *__restrict__ pairs, const int64_t *__restrict__ dP,
+                                        int64_t pcap, const uint64_t *__restrict__ ref_keys,
+                                        const int64_t *__restrict__ ref_lk, int64_t n_ref,
+                                        int64_t *__restrict__ posv, int64_t *__restrict__ want,
+                                        unsigned long long *__restrict__ first_fail) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t P = *dP < pcap ? *dP : pcap;
+    if (t < pcap) {
+        if (t >= P) return;
+        const int64_t r = find_key(ref_keys, n_ref, pair_key(pairs, t));
+        posv[t] = r >= 0 ? r : n_ref + t;   // certificate pairs first, then the other candidates
+        want[t] = r >= 0 ? ref_lk[r] : 0;
+        return;
+    }
+    const int64_t r = t - pcap;
+    if (r >= n_ref) return;
+    // binary search of the certificate pair among the P sorted candidates
+    const uint64_t k = ref_keys[r];
+    int64_t lo = 0, hi = P;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (pair_key(pairs, mid) < k) lo = mid + 1; else hi = mid;
+    }
+    if (!(lo < P && pair_key(pairs, lo) == k) && ref_lk[r] != 0)
+        atomicMin(first_fail, (unsigned long long)r);   // not a candidate: computed as 0 (certify.py:203-206)
+}
+}  // namespace
+
+void launch_early_exit_order(const int32_t *pairs, const int64_t *d_P, int64_t pcap, const uint64_t *ref_keys,
+                             const int64_t *ref_lk, int64_t n_ref, int64_t *posv, int64_t *want,
+                             unsigned long long *first_fail, cudaStream_t s) {
+    const int64_t n = pcap + n_ref;
+    if (n <= 0) return;
+    early_exit_order_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(pairs, d_P, pcap, ref_keys, ref_lk, n_ref, posv,
+                                                                       want, first_fail);
     LC_CHECK_LAUNCH();
 }
 

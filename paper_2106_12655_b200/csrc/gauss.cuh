@@ -124,11 +124,29 @@ struct Pass1Args {
     unsigned long long *marked = nullptr;
     int *abort = nullptr;
 };
+// Device early exit of verify(early_exit=True) (certify.py:195-216): the pairs are
+// evaluated against the reference certificate in the reference's ordering
+// (reference pairs in key order, then the other candidates in key order);
+// posv[p] is pair p's place in that order (an order-preserving value), want[p] the
+// certificate's value (0 if absent).  *first_fail = smallest place whose value
+// differs; a pair whose place is past it is skipped (cancelled).
+struct EarlyExitArgs {
+    const int64_t *posv = nullptr;
+    const int64_t *want = nullptr;
+    unsigned long long *first_fail = nullptr;
+    unsigned long long *n_eval = nullptr;
+};
 void launch_gauss_pairs(int mode, const double *X, const double *Y, const double *Z, const PairGeom *pg,
                         const int64_t *d_P, int64_t pcap, unsigned long long *counter, const int *abort,
                         const int64_t *d_bounds, int shard, double *partials, double *raw, int64_t *lk, uint8_t *flags,
                         double *h_raw, int64_t *h_lk, uint8_t *h_flags, cudaStream_t s,
-                        const Pass1Args &chk = Pass1Args());
+                        const Pass1Args &chk = Pass1Args(), const EarlyExitArgs &ee = EarlyExitArgs());
+// Early-exit preparation after the PLS: posv / want of every candidate pair (binary
+// search of its key in the certificate) and *first_fail lowered to the place of every
+// certificate pair that is no longer a candidate (its value is 0 there: a failure).
+void launch_early_exit_order(const int32_t *pairs, const int64_t *d_P, int64_t pcap, const uint64_t *ref_keys,
+                             const int64_t *ref_lk, int64_t n_ref, int64_t *posv, int64_t *want,
+                             unsigned long long *first_fail, cudaStream_t s);
 
 // Cost-balanced shard boundaries of the item list (item_off null: of the pair list): bounds[0..shards] (device),
 // shard r owns items [bounds[r], bounds[r+1]); each shard's segment-pair cost is

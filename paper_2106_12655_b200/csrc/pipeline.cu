@@ -48,7 +48,8 @@ __global__ void export_results_kernel(const int64_t *__restrict__ dP, int64_t ca
                                       const double *__restrict__ raw, const int64_t *__restrict__ lk,
                                       const uint8_t *__restrict__ flags, FastStatus *__restrict__ st,
                                       int2 *__restrict__ h_pairs, double *__restrict__ h_raw,
-                                      int64_t *__restrict__ h_lk, uint8_t *__restrict__ h_flags) {
+                                      int64_t *__restrict__ h_lk, uint8_t *__restrict__ h_flags,
+                                      const unsigned long long *__restrict__ ee = nullptr) {
     const int64_t P = *dP < cap ? *dP : cap;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += stride) {
@@ -70,6 +71,8 @@ __global__ void export_results_kernel(const int64_t *__restrict__ dP, int64_t ca
         f.marked = ctr->marked;
         f.val_err[0] = val_err[0];
         f.val_err[1] = val_err[1];
+        f.first_fail = ee ? ee[0] : ~0ULL;
+        f.n_eval = ee ? ee[1] : ~0ULL;
         *st = f;
     }
 }
@@ -147,6 +150,8 @@ __global__ void __launch_bounds__(256) reduce_export_kernel(
         f.marked = ctr->marked;
         f.val_err[0] = val_err[0];
         f.val_err[1] = val_err[1];
+        f.first_fail = ~0ULL;
+        f.n_eval = ~0ULL;
         *st = f;
     }
 }
@@ -181,7 +186,7 @@ void Pipeline::init(cudaStream_t st) {
 }
 
 void Pipeline::release() {
-    DevBuf *bufs[] = {&d_bounds, &d_tot, &d_coeffs, &d_t, &d_loff, &d_seg_box, &d_seg_fbox, &d_loop_keys, &d_seg_loop, &d_loop_box, &d_min_diag, &d_model_exp,
+    DevBuf *bufs[] = {&d_ref_keys, &d_ref_lk, &d_posv, &d_want, &d_ee, &d_bounds, &d_tot, &d_coeffs, &d_t, &d_loff, &d_seg_box, &d_seg_fbox, &d_loop_keys, &d_seg_loop, &d_loop_box, &d_min_diag, &d_model_exp,
                       &d_verts_in, &d_aos, &d_in_off, &d_voff, &d_X, &d_Y, &d_Z, &d_exp, &d_tmp_aos, &d_pairs,
                       &d_pg, &d_item_off, &d_item_pair, &d_scan, &d_counter, &d_partials, &d_raw, &d_lk, &d_flags,
                       &d_quads, &d_qout, &dout.X, &dout.Y, &dout.Z, &dout.voff, &dout.vert_off};
@@ -644,6 +649,12 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
     reserve_pls_grid(L, pls_sc, s);   // prezeroed by the run's first kernel
     d_tot.reserve(4 * sizeof(int64_t), s);
     part_cap = pcap;   // pair partials (sharded); a shard writes only its cost-balanced pair range
+    const bool ee = ee_on && !sharded;   // device early exit (single GPU; sharded runs replay it on the host)
+    if (ee) {
+        d_posv.reserve(sizeof(int64_t) * pcap, s);
+        d_want.reserve(sizeof(int64_t) * pcap, s);
+        d_ee.reserve(2 * sizeof(unsigned long long), s);
+    }
     d_partials.reserve(sizeof(double) * part_cap, s);
     d_bounds.reserve(sizeof(int64_t) * (shards + 1), s);
     d_item_pair.reserve(sizeof(ItemRec) * icap, s);
@@ -703,6 +714,8 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
                 {disc_sc.val_err2.ptr, 2, (unsigned)INT_MAX}, // validation: first bad loop / pair
                 {d_counter.ptr, 2, 0u},                       // Gauss item claim counter
                 {d_model_exp.ptr, 1, 0u},                     // coordinate exponent (atomicMax)
+                {ee ? d_ee.ptr : nullptr, ee ? 2 : 0, ~0u},  // early exit: first failure (~0)
+                {ee ? static_cast<unsigned *>(d_ee.ptr) + 2 : nullptr, ee ? 2 : 0, 0u},   // pairs evaluated
             };
             launch_grid_prezero(L, pls_sc, extra, (int)(sizeof extra / sizeof extra[0]), s);
         }
@@ -760,6 +773,16 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
             LC_CHECK_LAUNCH();
             launch_shard_bounds(d_pg.as<PairGeom>(), nullptr, pcap, dP, shards, d_bounds.as<int64_t>(), s);
         }
+        EarlyExitArgs eea;
+        if (ee) {   // the certificate's ordering of the candidates, and certificate pairs no longer candidates
+            launch_early_exit_order(d_pairs.as<int32_t>(), dP, pcap, d_ref_keys.as<uint64_t>(),
+                                    d_ref_lk.as<int64_t>(), n_ref, d_posv.as<int64_t>(), d_want.as<int64_t>(),
+                                    d_ee.as<unsigned long long>(), s);
+            eea.posv = d_posv.as<int64_t>();
+            eea.want = d_want.as<int64_t>();
+            eea.first_fail = d_ee.as<unsigned long long>();
+            eea.n_eval = d_ee.as<unsigned long long>() + 1;
+        }
         LC_CUDA(cudaStreamWaitEvent(s, ev_chords, 0));   // the sum reads the chords
         tl_mark("chords_joined", s);
         record(EV_GAUSS0);
@@ -786,7 +809,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
                            sharded ? d_bounds.as<int64_t>() : nullptr, shard,
                            via_partials ? d_partials.as<double>() : nullptr, d_raw.as<double>(), d_lk.as<int64_t>(),
                            d_flags.as<uint8_t>(), reinterpret_cast<double *>(hr), reinterpret_cast<int64_t *>(hl),
-                           reinterpret_cast<uint8_t *>(hf), s, Pass1Args());
+                           reinterpret_cast<uint8_t *>(hf), s, Pass1Args(), eea);
         record(EV_GAUSS1);
         tl_mark("gauss", s);
         LC_CUDA(cudaStreamWaitEvent(s, ev_checks, 0));
@@ -797,7 +820,8 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
                                  reinterpret_cast<uint8_t *>(hf), s);
         } else {   // the run's status record (sharded: lc_shard_finish reduces after the exchange)
             export_results_kernel<<<1, 32, 0, s>>>(dP, pcap, d_items, dmx, ctr, dout.d_val_err, nullptr, nullptr,
-                                                   nullptr, nullptr, st, nullptr, nullptr, nullptr, nullptr);
+                                                   nullptr, nullptr, st, nullptr, nullptr, nullptr, nullptr,
+                                                   ee ? d_ee.as<unsigned long long>() : nullptr);
             LC_CHECK_LAUNCH();
         }
         record(EV_END);   // "reduce" = Gauss end -> status in pinned memory
@@ -811,7 +835,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
         return e && e[0] == '1';
     }();
     FastKey key{L, M, pcap, icap, n_excl, mode, model_poly ? 1 : 0, shard, sharded ? shards : 0, prm.epsilon * prm.xi,
-                2.220446049250313e-16 * prm.xi, alloc_generation().load()};
+                2.220446049250313e-16 * prm.xi, alloc_generation().load(), ee ? n_ref : -1};
     last_fast_graph = false;
     if (!no_graph && graph_exec && key == graph_key) {
         LC_CUDA(cudaGraphLaunch(graph_exec, s));
@@ -892,6 +916,8 @@ int Pipeline::finish_fast() {
     fast_seen_valid = true;
 
     const FastStatus f = *pend.st;
+    ee_first_fail = f.first_fail == ~0ULL ? -1 : (int64_t)f.first_fail;
+    ee_n_eval = f.n_eval == ~0ULL ? -1 : (int64_t)f.n_eval;
     if (f.n_items > items_cap) items_cap = f.n_items;
     if (f.P > pairs_seen) pairs_seen = f.P;
     if (f.max_row > kRowSlots || f.P > pcap || f.zero_loop != INT_MAX || f.n_large != 0 || f.marked != 0 ||
@@ -938,6 +964,23 @@ int Pipeline::shard_finish() {
         fused_shard_pending = false;
     }
     return r;
+}
+
+void Pipeline::set_early_exit(const uint64_t *keys, const int64_t *lk, int64_t n, bool enable) {
+    ee_on = enable;
+    if (!enable) return;
+    if (n < 0 || (n > 0 && (!keys || !lk))) throw Error(LC_ERR_ARG, "bad certificate arrays");
+    for (int64_t k = 1; k < n; ++k)
+        if (keys[k] <= keys[k - 1]) throw Error(LC_ERR_ARG, "certificate keys must be sorted unique");
+    n_ref = n;
+    d_ref_keys.reserve(sizeof(uint64_t) * (n > 0 ? n : 1), s);
+    d_ref_lk.reserve(sizeof(int64_t) * (n > 0 ? n : 1), s);
+    d_ee.reserve(2 * sizeof(unsigned long long), s);
+    if (n > 0) {
+        LC_CUDA(cudaMemcpyAsync(d_ref_keys.ptr, keys, sizeof(uint64_t) * n, cudaMemcpyHostToDevice, s));
+        LC_CUDA(cudaMemcpyAsync(d_ref_lk.ptr, lk, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+    }
+    LC_CUDA(cudaStreamSynchronize(s));   // the caller's arrays may go after return
 }
 
 void Pipeline::prefill_partials_neg_zero(int64_t n) {

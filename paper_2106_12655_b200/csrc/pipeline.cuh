@@ -14,6 +14,8 @@ struct FastStatus {
     int max_row, zero_loop, n_unpaired, n_large;
     unsigned long long marked;
     int val_err[2];
+    unsigned long long first_fail;   // early exit: place of the first failing pair (~0: none)
+    unsigned long long n_eval;       // early exit: pairs evaluated
 };
 
 enum FastResult : int { FAST_OK = 0, FAST_FALLBACK = 1, FAST_INVALID = 2, FAST_PENDING = 3 };
@@ -101,6 +103,12 @@ struct Pipeline {
     // build items and read back n_items together with a deferred discretize
     // validation result (one sync); false + derr on a ValidationError
     bool build_gauss_items_checked(int mode = GAUSS_PHASE);
+    // Device early exit of verify(early_exit=True): the certificate's sorted keys and values
+    DevBuf d_ref_keys, d_ref_lk, d_posv, d_want, d_ee;
+    int64_t n_ref = 0;
+    bool ee_on = false;
+    int64_t ee_first_fail = -1, ee_n_eval = -1;   // last fused run (-1: not an early-exit run)
+    void set_early_exit(const uint64_t *keys, const int64_t *lk, int64_t n, bool enable);
     bool items_seq = false;   // the current items are whole-row (sequential-mode) items
     bool items_ready = false; // d_item_pair holds the item records of the current pairs
     void run_gauss(int mode, int64_t item_begin, int64_t item_end, double *partials_ext, cudaEvent_t ev0,
@@ -145,10 +153,11 @@ struct Pipeline {
         int mode, model_poly, shard, shards;
         double min_diam, poly_thr;
         unsigned long long gen;
+        int64_t n_ref;   // early-exit certificate size (-1: off)
         bool operator==(const FastKey &o) const {
             return L == o.L && M == o.M && pcap == o.pcap && icap == o.icap && n_excl == o.n_excl &&
                    mode == o.mode && model_poly == o.model_poly && shard == o.shard && shards == o.shards &&
-                   min_diam == o.min_diam && poly_thr == o.poly_thr && gen == o.gen;
+                   min_diam == o.min_diam && poly_thr == o.poly_thr && gen == o.gen && n_ref == o.n_ref;
         }
     };
     FastKey fast_seen{}, graph_key{};

@@ -860,7 +860,7 @@ void launch_seg_boxes(const double *coeffs, const double *t, const double *verts
 
 
 namespace {
-constexpr int kMaxZeroRanges = 12;
+constexpr int kMaxZeroRanges = 16;
 struct ZeroList {
     ZeroRange r[kMaxZeroRanges];
     int n;
