@@ -108,6 +108,16 @@ void lc_destroy(lc_ctx *ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     ctx->pipe.release();
+    BhScratch &b = ctx->bh;   // the context's other device buffers (Barnes-Hut, tight-box scratch)
+    for (DevBuf *x : {&b.fr[0], &b.fr[1], &b.val, &b.cnt, &b.off, &b.key, &b.uniq, &b.agg, &b.nruns, &b.tmp, &b.tot,
+                      &b.beta, &b.pairs, &b.leaves, &ctx->tb_coeffs, &ctx->tb_t, &ctx->tb_box, &ctx->tb_loop,
+                      &ctx->tb_off, &ctx->tb_flag})
+        x->release(ctx->stream);
+    b.host.release();
+    try {
+        comm_destroy(ctx->comm);
+    } catch (...) {
+    }
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->own_stream && ctx->stream) {

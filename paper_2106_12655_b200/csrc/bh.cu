@@ -407,6 +407,11 @@ __global__ void bh_roots_kernel(const int32_t *__restrict__ pairs, int64_t P, co
 }
 
 // One frontier level: far field, leaf pair, or split (barneshut.py:196-240).
+// The far field is evaluated here; a leaf pair is only flagged — the level's
+// leaf pairs are evaluated together by bh_leaf_pairs_kernel (no divergence
+// between the far-field and segment-pair arithmetic inside a warp).
+// cnt packs the split count (low 32 bits) and the leaf flag (high 32 bits), so
+// one exclusive scan gives both the next frontier's and the leaf list's offsets.
 __global__ void __launch_bounds__(128) bh_visit_kernel(const int4 *__restrict__ fr, int64_t n, View A, View B,
                                                        const double *__restrict__ beta, int quad, double k_const,
                                                        double2 *__restrict__ val, int64_t *__restrict__ cnt,
@@ -428,8 +433,7 @@ __global__ void __launch_bounds__(128) bh_visit_kernel(const int4 *__restrict__ 
               (ra * Rb[BH_NCM] * Ra[BH_NCQ] + rb * Ra[BH_NCM] * Rb[BH_NCQ] +
                3.0 * (Ra[BH_NCD] * Rb[BH_NCQ] + Ra[BH_NCQ] * Rb[BH_NCD]));
     } else if (A.left[e.x] < 0 && B.left[e.y] < 0) {
-        const double *sa = A.seg + 6 * (int64_t)A.leaf_prim[e.x], *sb = B.seg + 6 * (int64_t)B.leaf_prim[e.y];
-        lam = ref_pair_lambda(sa[0], sa[1], sa[2], sa[3], sa[4], sa[5], sb[0], sb[1], sb[2], sb[3], sb[4], sb[5]);
+        c = int64_t(1) << 32;   // leaf pair: batched (bh_leaf_pairs_kernel)
     } else {
         c = 2;
     }
@@ -440,14 +444,18 @@ __global__ void __launch_bounds__(128) bh_visit_kernel(const int4 *__restrict__ 
 
 __global__ void bh_expand_kernel(const int4 *__restrict__ fr, int64_t n, View A, View B,
                                  const int64_t *__restrict__ cnt, const int64_t *__restrict__ off,
-                                 int4 *__restrict__ next) {
+                                 int4 *__restrict__ next, int *__restrict__ leaves) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n || cnt[i] == 0) return;
+    if (cnt[i] >> 32) {   // leaf pair: its frontier index into the level's leaf list
+        leaves[off[i] >> 32] = (int)i;
+        return;
+    }
     const int4 e = fr[i];
     const bool a_leaf = A.left[e.x] < 0, b_leaf = B.left[e.y] < 0;
     const bool descend_a = !a_leaf && (b_leaf || A.rec[kBhRec * (int64_t)e.x + BH_RADIUS] >
                                                      B.rec[kBhRec * (int64_t)e.y + BH_RADIUS]);
-    const int64_t o = off[i];
+    const int64_t o = off[i] & 0xffffffffLL;
     if (descend_a) {
         next[o] = make_int4(A.left[e.x], e.y, e.z, 0);
         next[o + 1] = make_int4(A.right[e.x], e.y, e.z, 0);
@@ -455,6 +463,21 @@ __global__ void bh_expand_kernel(const int4 *__restrict__ fr, int64_t n, View A,
         next[o] = make_int4(e.x, B.left[e.y], e.z, 0);
         next[o + 1] = make_int4(e.x, B.right[e.y], e.z, 0);
     }
+}
+
+// The level's leaf pairs as one batch: thread per pair, the reference formula
+// (direct._pair_lambda, direct.py:19-46) — the per-pair arithmetic of the Gauss
+// kernel's reference mode (geom.cuh ref_pair_lambda), bitwise as before.
+__global__ void __launch_bounds__(128) bh_leaf_pairs_kernel(const int4 *__restrict__ fr,
+                                                            const int *__restrict__ leaves, int64_t n_leaf, View A,
+                                                            View B, double2 *__restrict__ val) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= n_leaf) return;
+    const int i = leaves[k];
+    const int4 e = fr[i];
+    const double *sa = A.seg + 6 * (int64_t)A.leaf_prim[e.x], *sb = B.seg + 6 * (int64_t)B.leaf_prim[e.y];
+    val[i] = make_double2(
+        ref_pair_lambda(sa[0], sa[1], sa[2], sa[3], sa[4], sa[5], sb[0], sb[1], sb[2], sb[3], sb[4], sb[5]), 0.0);
 }
 
 __global__ void bh_accumulate_kernel(const int *__restrict__ uniq, const double2 *__restrict__ agg,
@@ -798,7 +821,7 @@ void bh_eval(const BhForest &a, const BhForest &b, const int32_t *pairs, int64_t
     int64_t n = P, total = 0;
     int64_t *h_next = static_cast<int64_t *>(sc.host.ptr);
     while (n > 0) {
-        if (n >= (int64_t(1) << 31) - 1) throw Error(LC_ERR_ARG, "Barnes-Hut frontier exceeds 2^31 node pairs");
+        if (n >= (int64_t(1) << 30)) throw Error(LC_ERR_ARG, "Barnes-Hut frontier exceeds 2^30 node pairs");
         total += n;
         sc.val.reserve(sizeof(double2) * n, s);
         sc.agg.reserve(sizeof(double2) * n, s);
@@ -820,20 +843,25 @@ void bh_eval(const BhForest &a, const BhForest &b, const int32_t *pairs, int64_t
         LC_CUB(cub::DeviceScan::ExclusiveSum(sc.tmp.ptr, bs, sc.cnt.as<int64_t>(), sc.off.as<int64_t>(), (int)(n + 1),
                                              s));
         LC_CUDA(cudaMemcpyAsync(h_next, sc.off.as<int64_t>() + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        LC_CUDA(cudaStreamSynchronize(s));
+        const int64_t nn = *h_next & 0xffffffffLL, n_leaf = *h_next >> 32;
+        sc.fr[cur ^ 1].reserve(sizeof(int4) * (nn > 0 ? nn : 1), s);
+        sc.leaves.reserve(sizeof(int) * (n_leaf > 0 ? n_leaf : 1), s);
+        bh_expand_kernel<<<blocks_for(n, 256), 256, 0, s>>>(sc.fr[cur].as<int4>(), n, A, B, sc.cnt.as<int64_t>(),
+                                                            sc.off.as<int64_t>(), sc.fr[cur ^ 1].as<int4>(),
+                                                            sc.leaves.as<int>());
+        LC_CHECK_LAUNCH();
+        if (n_leaf > 0) {
+            bh_leaf_pairs_kernel<<<blocks_for(n_leaf, 128), 128, 0, s>>>(sc.fr[cur].as<int4>(), sc.leaves.as<int>(),
+                                                                         n_leaf, A, B, sc.val.as<double2>());
+            LC_CHECK_LAUNCH();
+        }
         br = sc.tmp.bytes;
         LC_CUB(cub::DeviceReduce::ReduceByKey(sc.tmp.ptr, br, sc.key.as<int>(), sc.uniq.as<int>(), sc.val.as<double2>(),
                                               sc.agg.as<double2>(), sc.nruns.as<int>(), Add2(), (int)n, s));
         bh_accumulate_kernel<<<blocks_for(n, 256), 256, 0, s>>>(sc.uniq.as<int>(), sc.agg.as<double2>(),
                                                                 sc.nruns.as<int>(), n, sc.tot.as<double2>());
         LC_CHECK_LAUNCH();
-        LC_CUDA(cudaStreamSynchronize(s));
-        const int64_t nn = *h_next;
-        if (nn > 0) {
-            sc.fr[cur ^ 1].reserve(sizeof(int4) * nn, s);
-            bh_expand_kernel<<<blocks_for(n, 256), 256, 0, s>>>(sc.fr[cur].as<int4>(), n, A, B, sc.cnt.as<int64_t>(),
-                                                                sc.off.as<int64_t>(), sc.fr[cur ^ 1].as<int4>());
-            LC_CHECK_LAUNCH();
-        }
         cur ^= 1;
         n = nn;
     }

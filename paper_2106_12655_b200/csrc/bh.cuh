@@ -34,7 +34,7 @@ struct BhForest {
 
 // Scratch of the dual-tree traversal (grow-only, reused across calls).
 struct BhScratch {
-    DevBuf fr[2], val, cnt, off, key, uniq, agg, nruns, tmp, tot, beta, pairs;
+    DevBuf fr[2], val, cnt, off, key, uniq, agg, nruns, tmp, tot, beta, pairs, leaves;
     PinnedBuf host;
 };
 
