@@ -129,7 +129,41 @@ def run_case(m, params=None):
         return (o[1], o[2]) == (g[1], g[2]), f"errors {o[1:]} vs {g[1:]}"
     same = np.array_equal(o[1], g[1]) and np.array_equal(o[2], g[2])
     err = float(np.max(np.abs(o[3] - g[3]))) if len(o[3]) else 0.0
-    return same and err < 1e-9, f"entries equal={same} max raw err={err:.3g}"
+    ee_ok, ee_why = early_exit_case(m, params, o[1], o[2])
+    return same and err < 1e-9 and ee_ok, f"entries equal={same} max raw err={err:.3g} {ee_why}"
+
+
+def early_exit_case(m, params, want, pairs):
+    """verify(early_exit=True) on a perturbed certificate (the oracle's entries with one
+    flipped, one dropped, one added pair) against the reference's evaluation order
+    replayed on the oracle's values (certify.py:195-216)."""
+    import warnings
+
+    rng = np.random.default_rng(len(want) * 7919 + len(pairs))
+    ref = {(int(i), int(j)): int(v) for i, j, v in want}
+    edits = []
+    if ref:
+        k = list(ref)[int(rng.integers(len(ref)))]
+        ref[k] = -ref[k] if rng.random() < 0.5 else ref[k] + 1
+        edits.append("changed")
+    if len(ref) > 1 and rng.random() < 0.5:
+        ref.pop(list(ref)[int(rng.integers(len(ref)))])
+        edits.append("dropped")
+    if m.num_loops > 3 and rng.random() < 0.5:
+        i, j = sorted(rng.choice(m.num_loops, 2, replace=False).tolist())
+        ref.setdefault((i, j), 3)
+        edits.append("added")
+    ref = {k: v for k, v in ref.items() if v != 0}   # a certificate stores no zero entries
+    cert = lc.LinkMatrix(m.num_loops, tuple(sorted((i, j, v) for (i, j), v in ref.items())))
+    values = {(int(i), int(j)): int(v) for i, j, v in want}
+    cand = [(int(i), int(j)) for i, j in pairs]
+    ordering = sorted(ref) + sorted(set(cand) - set(ref))
+    first = next((p for p in ordering if values.get(p, 0) != ref.get(p, 0)), None)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        rep = lc.verify(m, cert, early_exit=True, params=params)
+    ok = rep.first_failure == first and rep.status == ("Pass" if first is None else "Aborted")
+    return ok, f"early exit {'+'.join(edits) or 'none'} first={first} got={rep.first_failure}"
 
 
 def main():
