@@ -104,6 +104,10 @@ LC_API int lc_stage_polylines(lc_ctx *ctx, const double *verts, const int64_t *v
                        const int32_t *pairs, int64_t P, int mode, int64_t *n_items);
 LC_API int lc_gauss_run(lc_ctx *ctx, int mode, int64_t item_begin, int64_t item_end, double *partials_dev);
 LC_API int lc_gauss_reduce(lc_ctx *ctx, const double *partials_dev, double *raw, int64_t *lk, uint8_t *flags);
+/* The fused path's pair-claiming Gauss kernel over the staged pairs (their raw sums
+ * into the library's partials buffer; timing A/B against lc_gauss_run — read the
+ * time with lc_gauss_event_ms). */
+LC_API int lc_gauss_run_pairs(lc_ctx *ctx, int mode);
 /* Duration of the last lc_gauss_run kernel (waits for it). */
 LC_API int lc_gauss_event_ms(lc_ctx *ctx, float *ms);
 

@@ -57,6 +57,7 @@ SIGNATURES = {
                                            _c_int64_p]),
     "lc_gauss_run": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, _vp]),
     "lc_gauss_reduce": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
+    "lc_gauss_run_pairs": (ctypes.c_int, [_vp, ctypes.c_int]),
     "lc_gauss_event_ms": (ctypes.c_int, [_vp, _c_float_p]),
     "lc_probe_fp64_peak": (ctypes.c_int, [_vp, _c_double_p, _c_float_p]),
     "lc_probe_fp64_dmma_peak": (ctypes.c_int, [_vp, _c_double_p, _c_float_p]),
@@ -380,6 +381,11 @@ class Context:
         with self.lock:
             _check(self.lib.lc_gauss_run(self.handle, int(mode), int(item_begin), int(item_end),
                                          ctypes.c_void_p(partials_dev_ptr) if partials_dev_ptr else None))
+
+    def gauss_run_pairs(self, mode):
+        """Pair-claiming kernel over the staged pairs (timing A/B; gauss_event_ms reads it)."""
+        with self.lock:
+            _check(self.lib.lc_gauss_run_pairs(self.handle, int(mode)))
 
     def gauss_reduce(self, partials_dev_ptr=None):
         P = self._staged_pairs

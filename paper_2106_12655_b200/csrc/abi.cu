@@ -211,6 +211,24 @@ int lc_gauss_run(lc_ctx *ctx, int mode, int64_t item_begin, int64_t item_end, do
     });
 }
 
+int lc_gauss_run_pairs(lc_ctx *ctx, int mode) {
+    return guarded(ctx, [&] {
+        Pipeline &p = ctx->pipe;
+        if (!p.items_ready || p.items_seq) throw Error(LC_ERR_STATE, "no tile work items built (lc_prepare_gauss)");
+        p.d_tot.reserve(4 * sizeof(int64_t), ctx->stream);
+        p.d_counter.reserve(2 * sizeof(unsigned long long), ctx->stream);
+        p.d_partials.reserve(sizeof(double) * (size_t)(p.P > 0 ? p.P : 1), ctx->stream);
+        LC_CUDA(cudaMemcpyAsync(p.d_tot.ptr, &p.P, sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+        LC_CUDA(cudaMemsetAsync(p.d_counter.ptr, 0, sizeof(unsigned long long), ctx->stream));
+        LC_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+        launch_gauss_pairs(mode, p.gX, p.gY, p.gZ, p.d_pg.as<PairGeom>(), p.d_tot.as<int64_t>(), p.P,
+                           p.d_counter.as<unsigned long long>(), nullptr, nullptr, 0, p.d_partials.as<double>(),
+                           nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, ctx->stream);
+        LC_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+        LC_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
 int lc_gauss_reduce(lc_ctx *ctx, const double *partials_dev, double *raw, int64_t *lk, uint8_t *flags) {
     return guarded(ctx, [&] {
         ctx->pipe.reduce_pairs(partials_dev);

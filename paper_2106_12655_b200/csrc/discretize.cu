@@ -238,6 +238,10 @@ __global__ void __launch_bounds__(32 * kAnyWarps, 4) brute_any_kernel(
     const int64_t *__restrict__ dP, unsigned long long *__restrict__ marked, int *__restrict__ abort) {
     __shared__ int32_t sidx[kAnyWarps][2][kAnyCap];
     __shared__ float sbox[kAnyWarps][2][6 * kAnyCap];
+    // programmatic dependent launch: the Gauss kernel queued behind this one on the
+    // critical stream may start as soon as every CTA here is resident (it does not read
+    // these results; it polls the abort flag), so the check runs beside the sum
+    asm volatile("griddepcontrol.launch_dependents;");
     if (dP && *dP < P) P = *dP;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t nw = (int64_t)gridDim.x * kAnyWarps;
@@ -1176,9 +1180,19 @@ void launch_discretize_chords(const DiscInput &in, const DiscParams &prm, DiscSc
     launch_write_all(in, poly_thr, out, sc.val_flags.as<unsigned>(), s);
 }
 
+void launch_pass1_brute(const DiscInput &in, const int64_t *d_P, DiscScratch &sc, cudaStream_t s) {
+    const int64_t Pcap = in.P, M = in.M;
+    if (Pcap <= 0 || M <= 0) return;
+    PreCounters *ctr = sc.prectr.as<PreCounters>();
+    const int64_t blocks = ceil_div(Pcap, kAnyWarps) < 148 * 8 ? ceil_div(Pcap, kAnyWarps) : 148 * 8;
+    brute_any_kernel<<<(unsigned)blocks, 32 * kAnyWarps, 0, s>>>(in.seg_box, in.seg_fbox, M, in.loff, in.loop_box,
+                                                                 in.L, in.pairs, Pcap, d_P, &ctr->marked, &ctr->abort);
+    LC_CHECK_LAUNCH();
+}
+
 void launch_discretize_checks(const DiscInput &in, const int64_t *d_P, const DiscParams &prm, DiscScratch &sc,
                               DiscOutput &out, cudaStream_t s, cudaEvent_t chords_done, const PreCounters **d_ctr,
-                              bool brute_in_gauss) {
+                              bool brute_in_gauss, cudaStream_t brute_stream) {
     const int64_t L = in.L, M = in.M, Pcap = in.P;
     const double min_diam = prm.epsilon * prm.xi;
     PreCounters *ctr = sc.prectr.as<PreCounters>();
@@ -1194,7 +1208,7 @@ void launch_discretize_checks(const DiscInput &in, const int64_t *d_P, const Dis
         pre_loops_kernel<<<grid_for(L, 32), 32, 0, s>>>(in.loop_min_diag, sc.paired.as<uint8_t>(), L, min_diam, ctr);
         LC_CHECK_LAUNCH();
     }
-    if (Pcap > 0 && M > 0 && !brute_in_gauss) {
+    if (Pcap > 0 && M > 0 && !brute_in_gauss && !brute_stream) {   // brute_stream: launch_pass1_brute by the caller
         // the 8-warp grid-stride kernel (default) runs in the slots the short-lived Gauss
         // CTAs free; LINKCERT_BRUTE_LITE=1 selects the single-warp variant (A/B: 0.460 vs
         // 0.463 ms per Kusari step)

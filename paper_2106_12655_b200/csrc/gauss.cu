@@ -37,13 +37,19 @@ constexpr double kInvTwoPi = 0.15915494309189535;     // 1 / (2 pi), correctly r
 #endif
 constexpr int kGaussCarveout = LC_GAUSS_CARVEOUT;
 #ifndef LC_PAIRS_STATIC
-#define LC_PAIRS_STATIC 1          // pair kernel: static chunks, short-lived CTAs (0: persistent claiming)
+#define LC_PAIRS_STATIC 0          // pair kernel: 1 = static chunks, short-lived CTAs; 0 = persistent claiming
 #endif
 #ifndef LC_PAIRS_WAVES
 #define LC_PAIRS_WAVES 16          // CTA waves of the static pair kernel (A/B: 4 / 8 / 16 -> 16 best)
 #endif
 #ifndef LC_PAIRS_PRIORITY_LOW
-#define LC_PAIRS_PRIORITY_LOW 1    // launch the pair kernel at the lowest stream priority
+#define LC_PAIRS_PRIORITY_LOW 0    // launch the pair kernel at the lowest stream priority
+#endif
+#ifndef LC_PAIRS_PREFETCH
+#define LC_PAIRS_PREFETCH 1        // persistent pair kernel: prefetch the next claim / pair geometry
+#endif
+#ifndef LC_PAIRS_PASS1
+#define LC_PAIRS_PASS1 0
 #endif
 #ifndef LC_MINB
 #define LC_MINB 2   // resident CTAs per SM the phase kernel is compiled for (A/B: -DLC_MINB=n)
@@ -528,8 +534,10 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) gauss_pairs_kernel(
     int shard, double *__restrict__ partials, double *__restrict__ raw, int64_t *__restrict__ lk,
     uint8_t *__restrict__ flags, double *__restrict__ h_raw, int64_t *__restrict__ h_lk,
     uint8_t *__restrict__ h_flags, const Pass1Args chk, const EarlyExitArgs ee) {
+#if LC_PAIRS_PASS1
     __shared__ int32_t sidx[kCtaThreads / 32][2][kAnyCap];
     __shared__ float sbox[kCtaThreads / 32][2][6 * kAnyCap];
+#endif
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     int64_t b = 0, e = *dP < pcap ? *dP : pcap;
     if (d_bounds) {
@@ -544,21 +552,44 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) gauss_pairs_kernel(
     const int64_t cb = b + (int64_t)blockIdx.x * chunk, ce = cb + chunk < e ? cb + chunk : e;
     for (int64_t p = cb + w; p < ce; p += kCtaThreads / 32) {
         if (abort && __shfl_sync(0xffffffffu, lane == 0 ? *(volatile const int *)abort : 0, 0)) break;
+#elif LC_PAIRS_PREFETCH
+    // two-stage software pipeline of the per-pair prologue: the claim of pair n+2 and the
+    // PairGeom load of pair n+1 are issued while pair n is summed, so a pair starts with
+    // its vertex loads instead of claim -> geometry -> vertices (three dependent round trips)
+    int64_t k1, k2;
+    bool ok1 = claim(counter, abort, lane, k1);
+    bool ok2 = ok1 && claim(counter, abort, lane, k2);
+    PairGeom g1 = {};
+    if (ok1 && b + k1 < e) g1 = pg[b + k1];
+    for (;;) {
+        if (!ok1) break;
+        const int64_t p = b + k1;
+        if (p >= e) break;
+        const PairGeom g = g1;
+        ok1 = ok2;
+        k1 = k2;
+        if (ok1 && b + k1 < e) g1 = pg[b + k1];
+        if (ok1) ok2 = claim(counter, abort, lane, k2);
 #else
     for (;;) {
         int64_t k;
         if (!claim(counter, abort, lane, k)) break;
         const int64_t p = b + k;
         if (p >= e) break;
+        const PairGeom g = pg[p];
+#endif
+#if LC_PAIRS_STATIC
+        const PairGeom g = pg[p];
 #endif
         if (ee.posv) {   // early exit: a pair past the first failure found so far is cancelled
             if ((unsigned long long)ee.posv[p] > *(volatile unsigned long long *)ee.first_fail) continue;
             if (lane == 0) atomicAdd(ee.n_eval, 1ULL);
         }
-        if (chk.box)   // the pair's pass-1 check (a hit aborts the fused run: staged path)
+#if LC_PAIRS_PASS1   // A/B: the pair's pass-1 check inside the sum (measured slower than the checks branch)
+        if (chk.box)
             brute_any_pair(p, chk.box, chk.fbox, chk.M, chk.loff, chk.lbox, chk.L, chk.pairs, sidx[w][0], sidx[w][1],
                            sbox[w][0], sbox[w][1], lane, chk.marked, chk.abort);
-        const PairGeom g = pg[p];
+#endif
         const int n = g.items_r * g.items_c;
         double s = 0.0;
         for (int it = 0; it < n; ++it) {
@@ -865,7 +896,7 @@ void launch_gauss_pairs(int mode, const double *X, const double *Y, const double
                         const int64_t *d_P, int64_t pcap, unsigned long long *counter, const int *abort,
                         const int64_t *d_bounds, int shard, double *partials, double *raw, int64_t *lk, uint8_t *flags,
                         double *h_raw, int64_t *h_lk, uint8_t *h_flags, cudaStream_t s, const Pass1Args &chk,
-                        const EarlyExitArgs &ee) {
+                        const EarlyExitArgs &ee, bool pdl) {
     if (pcap <= 0) return;
     using Kern = void (*)(const double *, const double *, const double *, const PairGeom *, const int64_t *, int64_t,
                           unsigned long long *, const int *, const int64_t *, int, double *, double *, int64_t *,
@@ -898,13 +929,17 @@ void launch_gauss_pairs(int mode, const double *X, const double *Y, const double
     cfg.gridDim = dim3((unsigned)blocks);
     cfg.blockDim = dim3(threads);
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     int prio_lo = 0, prio_hi = 0;
     LC_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     attr[0].id = cudaLaunchAttributePriority;
     attr[0].val.priority = LC_PAIRS_PRIORITY_LOW ? prio_lo : prio_hi;   // below the checks branch
+    // pdl: a programmatic dependent of the kernel before it on the stream (the pass-1
+    // check), launched once that kernel's CTAs are all resident
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl ? 2 : 1;
     LC_CUDA(cudaLaunchKernelEx(&cfg, fn, X, Y, Z, pg, d_P, pcap, counter, abort, d_bounds, shard, partials, raw, lk,
                                flags, h_raw, h_lk, h_flags, chk, ee));
     LC_CHECK_LAUNCH();

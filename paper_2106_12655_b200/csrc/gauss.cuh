@@ -140,7 +140,8 @@ void launch_gauss_pairs(int mode, const double *X, const double *Y, const double
                         const int64_t *d_P, int64_t pcap, unsigned long long *counter, const int *abort,
                         const int64_t *d_bounds, int shard, double *partials, double *raw, int64_t *lk, uint8_t *flags,
                         double *h_raw, int64_t *h_lk, uint8_t *h_flags, cudaStream_t s,
-                        const Pass1Args &chk = Pass1Args(), const EarlyExitArgs &ee = EarlyExitArgs());
+                        const Pass1Args &chk = Pass1Args(), const EarlyExitArgs &ee = EarlyExitArgs(),
+                        bool pdl = false);
 // Early-exit preparation after the PLS: posv / want of every candidate pair (binary
 // search of its key in the certificate) and *first_fail lowered to the place of every
 // certificate pair that is no longer a candidate (its value is 0 there: a failure).

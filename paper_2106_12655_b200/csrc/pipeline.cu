@@ -11,6 +11,11 @@
 
 namespace lc {
 
+#ifndef LC_BRUTE_PDL
+#define LC_BRUTE_PDL 1
+#endif
+constexpr bool kBrutePdl = LC_BRUTE_PDL;
+
 namespace {
 
 // Closed polylines from vertices: exactly LoopGeometry.from_polyline's arrays
@@ -759,7 +764,11 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
         LC_CUDA(cudaStreamWaitEvent(side[1], ev_pairs, 0));
         // (Pass1Args: the pass-1 pair check can also run inside the Gauss kernel — measured
         // slower than this branch beside it, 0.49 vs 0.47 ms per Kusari step)
-        launch_discretize_checks(in, dP, prm, disc_sc, dout, side[1], ev_chords, &ctr, /*brute_in_gauss=*/false);
+        // the pass-1 pair check goes on the critical stream right before the sum, which
+        // starts beside it as its programmatic dependent (LC_BRUTE_PDL); the rest of the
+        // checks stay on this branch
+        launch_discretize_checks(in, dP, prm, disc_sc, dout, side[1], ev_chords, &ctr, /*brute_in_gauss=*/false,
+                                 kBrutePdl ? s : nullptr);
         tl_mark("S1:checks", side[1]);
         record(EV_DISC, side[1]);
         // the pair list is final: the copy engine moves the whole capacity to pinned
@@ -783,9 +792,12 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
             eea.first_fail = d_ee.as<unsigned long long>();
             eea.n_eval = d_ee.as<unsigned long long>() + 1;
         }
-        LC_CUDA(cudaStreamWaitEvent(s, ev_chords, 0));   // the sum reads the chords
+        LC_CUDA(cudaStreamWaitEvent(s, ev_chords, 0));   // the sum reads the chords (the check, the segment boxes)
         tl_mark("chords_joined", s);
         record(EV_GAUSS0);
+#ifndef LC_AB_NO_PASS1   // (A/B measurement builds only: without the pass-1 check the fused result is unchecked)
+        if (kBrutePdl) launch_pass1_brute(in, dP, disc_sc, s);   // immediately before the sum: its PDL primary
+#endif
         // warps claim whole pairs; unsharded, each pair's raw / lk / flags go straight to
         // the pinned result arrays as it completes (no reduce / export pass after the sum)
         // (LINKCERT_PAIR_EXPORT=1: A/B — the sums go to the partials, a coalesced export follows)
@@ -809,7 +821,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
                            sharded ? d_bounds.as<int64_t>() : nullptr, shard,
                            via_partials ? d_partials.as<double>() : nullptr, d_raw.as<double>(), d_lk.as<int64_t>(),
                            d_flags.as<uint8_t>(), reinterpret_cast<double *>(hr), reinterpret_cast<int64_t *>(hl),
-                           reinterpret_cast<uint8_t *>(hf), s, Pass1Args(), eea);
+                           reinterpret_cast<uint8_t *>(hf), s, Pass1Args(), eea, kBrutePdl);
         record(EV_GAUSS1);
         tl_mark("gauss", s);
         LC_CUDA(cudaStreamWaitEvent(s, ev_checks, 0));

@@ -22,6 +22,12 @@ def bench_staged(ctx, modes, reps, label, sp):
             ctx.gauss_run(mode, 0, n)
             ts.append(ctx.gauss_event_ms())
         raw, lk, fl = ctx.gauss_reduce()
+        if mode == 0:   # the fused path's pair-claiming kernel on the same pairs
+            tp = []
+            for _ in range(reps + 2):
+                ctx.gauss_run_pairs(mode)
+                tp.append(ctx.gauss_event_ms())
+            print(f"{label:10s} pair kernel best {min(tp[2:]):8.3f} ms med {float(np.median(tp[2:])):8.3f} ms", flush=True)
         if base is None:
             base = raw
         best = min(ts[2:])
