@@ -91,6 +91,9 @@ __global__ void export_results_kernel(const int64_t *__restrict__ dP, int64_t ca
 #endif
 constexpr int kExportChunk = LC_EXPORT_CHUNK;
 constexpr int kPairsPerWarp = kExportChunk / 8;
+// 8 warps x kPairsPerWarp pairs per block; lane j + 1 carries pair j's end offset
+static_assert(kExportChunk % 8 == 0 && kPairsPerWarp >= 1 && kPairsPerWarp < 32,
+              "LC_EXPORT_CHUNK must be a multiple of 8 below 256");
 __global__ void __launch_bounds__(256) reduce_export_kernel(
     const double *__restrict__ partials, const int64_t *__restrict__ item_off, const int64_t *__restrict__ dP,
     int64_t cap, const int64_t *__restrict__ d_items, const int *__restrict__ d_max_row,
