@@ -100,6 +100,28 @@ struct PinnedBuf {
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Programmatic dependent launch along the fused run's critical path: a kernel
+// launched with pdl = true may become resident while its predecessor on the
+// stream still runs (once every predecessor CTA has executed LC_PDL_TRIGGER or
+// exited); it must LC_PDL_WAIT before touching the predecessor's outputs.  Both
+// device macros are no-ops for kernels launched without the attribute.
+#define LC_PDL_TRIGGER() asm volatile("griddepcontrol.launch_dependents;")
+#define LC_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, bool pdl, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.stream = s;
+    cudaLaunchAttribute a[1];
+    a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    a[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = a;
+    cfg.numAttrs = pdl ? 1 : 0;
+    check_cuda(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...), "cudaLaunchKernelEx", __FILE__, __LINE__);
+    launch_counter().fetch_add(1, std::memory_order_relaxed);
+}
+
 // Debug timeline of the fused run (LINKCERT_TIMELINE=1): external event-record
 // nodes after each stage (captured into the CUDA graph like the stage events),
 // printed to stderr after the run's sync as microseconds from the first mark.

@@ -15,6 +15,10 @@ namespace lc {
 #define LC_BRUTE_PDL 1
 #endif
 constexpr bool kBrutePdl = LC_BRUTE_PDL;
+#ifndef LC_CHAIN_PDL
+#define LC_CHAIN_PDL 1   // programmatic dependent launch along the PLS chain of the fused run
+#endif
+constexpr bool kChainPdl = LC_CHAIN_PDL;
 
 namespace {
 
@@ -736,7 +740,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
             const double *cp = model_poly ? nullptr : d_coeffs.as<double>(), *tp = model_poly ? nullptr : d_t.as<double>();
             // loop boxes + minimum diagonals with the PLS grid reduction folded in
             launch_loop_grid(cp, tp, vp, d_loff.as<int64_t>(), L, d_min_diag.as<unsigned long long>(),
-                             d_loop_box.as<double>(), pls_sc, s);
+                             d_loop_box.as<double>(), pls_sc, s, kChainPdl && !timeline().on);
             tl_mark("loop_boxes", s);
         }
         LC_CUDA(cudaEventRecord(ev_fork, s));
@@ -758,7 +762,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
         const int *dmx = nullptr;
         launch_pls_grid(d_loop_box.as<double>(), L, n_excl, pls_sc, d_pairs.as<int32_t>(), pcap, d_loff.as<int64_t>(),
                         d_pg.as<PairGeom>(), d_item_off.as<int64_t>(), d_tot.as<int64_t>(), icap, s, &dmx,
-                        /*prezeroed=*/true, /*grid_ready=*/split);
+                        /*prezeroed=*/true, /*grid_ready=*/split, kChainPdl && !timeline().on);
         const int64_t *dP = d_tot.as<int64_t>(), *d_items = d_tot.as<int64_t>() + 1;
         record(EV_PLS);
         // branch 2: pass-1 detection + validation only feed the status — they run

@@ -404,6 +404,8 @@ __device__ __forceinline__ int64_t owner_cell(const double *__restrict__ lbox, i
 // cell of each loop's lower corner and the loop's rank within that cell
 __global__ void cell_count_kernel(const double *__restrict__ lbox, int64_t L, const GridParams *__restrict__ gp,
                                   int64_t *__restrict__ count, int32_t *__restrict__ lcell, int32_t *__restrict__ lrank) {
+    LC_PDL_TRIGGER();
+    LC_PDL_WAIT();
     const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (l >= L) return;
     const GridParams g = *gp;
@@ -416,6 +418,8 @@ __global__ void cell_count_kernel(const double *__restrict__ lbox, int64_t L, co
 __global__ void cell_scatter_kernel(const double *__restrict__ lbox, int64_t L, const int64_t *__restrict__ cell_off,
                                     const int32_t *__restrict__ lcell, const int32_t *__restrict__ lrank,
                                     int32_t *__restrict__ cell_loops, double *__restrict__ cbox) {
+    LC_PDL_TRIGGER();
+    LC_PDL_WAIT();
     const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (l >= L) return;
     const int64_t pos = cell_off[lcell[l]] + lrank[l];
@@ -438,6 +442,8 @@ __global__ void grid_query_warp_kernel(const double *__restrict__ lbox, int64_t 
                                        const int64_t *__restrict__ offs, uint64_t *__restrict__ keys,
                                        int64_t *__restrict__ counts64, int *__restrict__ overflow,
                                        const int64_t *__restrict__ item_loff) {
+    LC_PDL_TRIGGER();
+    LC_PDL_WAIT();
     const int lane = threadIdx.x & 31;
     const int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     if (a >= L) return;
@@ -615,6 +621,8 @@ __global__ void __launch_bounds__(128) loop_grid_kernel(const double *__restrict
                                                         double *__restrict__ lbox, unsigned long long *__restrict__ acc,
                                                         unsigned *__restrict__ done, int64_t max_cells,
                                                         GridParams *__restrict__ gp) {
+    LC_PDL_TRIGGER();
+    LC_PDL_WAIT();
     __shared__ unsigned long long sk[4][7];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // block accumulators (ordered keys): min lo x3, max hi x3, max extent
@@ -732,6 +740,8 @@ __global__ void slots_compact_items_kernel(const int *__restrict__ row_count, co
                                            int64_t cap, const int64_t *__restrict__ loff, PairGeom *__restrict__ pg,
                                            int64_t *__restrict__ item_off, int64_t *__restrict__ d_tot,
                                            const int *__restrict__ overflow, int64_t item_cap) {
+    LC_PDL_TRIGGER();
+    LC_PDL_WAIT();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= L) return;
     const int64_t mask = (int64_t(1) << kPackShift) - 1;
@@ -866,6 +876,7 @@ struct ZeroList {
     int n;
 };
 __global__ void prezero_kernel(ZeroList zl) {
+    LC_PDL_TRIGGER();
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     for (int k = 0; k < zl.n; ++k) {
@@ -907,7 +918,8 @@ void launch_grid_prezero(int64_t L, PlsScratch &sc, const ZeroRange *extra, int 
 // host sync): sc.offs[L] = P, *sc.counter = largest row count, slots in
 // sc.pair_keys, row counts in sc.idx.  Excluded keys already in sc.excl.
 static void grid_prefix(const double *loop_box, int64_t L, int64_t n_excl, PlsScratch &sc, cudaStream_t s,
-                        const int64_t *item_loff = nullptr, bool prezeroed = false, bool grid_ready = false) {
+                        const int64_t *item_loff = nullptr, bool prezeroed = false, bool grid_ready = false,
+                        bool pdl = false) {
     const int64_t max_cells = pls_grid_max_cells(L);
     sc.axis.reserve(sizeof(GridParams), s);
     sc.keys.reserve(sizeof(int64_t) * (max_cells + 1), s);         // cell counts
@@ -939,23 +951,19 @@ static void grid_prefix(const double *loop_box, int64_t L, int64_t n_excl, PlsSc
     if (!prezeroed) LC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (max_cells + 1), s));
     // thread-per-loop kernels in 64-thread blocks: the latency chains spread over every SM
     const unsigned gl = (unsigned)ceil_div(L, 64);
-    cell_count_kernel<<<gl, 64, 0, s>>>(loop_box, L, gp, cnt, sc.lcell.as<int32_t>(), sc.lrank.as<int32_t>());
-    LC_CHECK_LAUNCH();
+    launch_pdl(cell_count_kernel, gl, 64, s, pdl, loop_box, L, gp, cnt, sc.lcell.as<int32_t>(), sc.lrank.as<int32_t>());
     tl_mark("cell_count", s);
     const size_t b = exclusive_scan_i64_tmp_bytes(max_cells + 1), b2 = exclusive_scan_i64_tmp_bytes(L + 1);
     sc.cub_tmp.reserve((b > b2 ? b : b2) + 16, s);
     exclusive_scan_i64(cnt, coff, max_cells + 1, sc.cub_tmp.ptr, sc.cub_tmp.bytes, s);
     tl_mark("cell_scan", s);
-    cell_scatter_kernel<<<gl, 64, 0, s>>>(loop_box, L, coff, sc.lcell.as<int32_t>(), sc.lrank.as<int32_t>(),
-                                           sc.perm.as<int32_t>(), sc.sbox.as<double>());
-    LC_CHECK_LAUNCH();
+    launch_pdl(cell_scatter_kernel, gl, 64, s, pdl, loop_box, L, coff, sc.lcell.as<int32_t>(),
+               sc.lrank.as<int32_t>(), sc.perm.as<int32_t>(), sc.sbox.as<double>());
     tl_mark("cell_scatter", s);
     if (!prezeroed) LC_CUDA(cudaMemsetAsync(max_count, 0, sizeof(int), s));
-    grid_query_warp_kernel<true><<<(unsigned)ceil_div(L * 32, 256), 256, 0, s>>>(loop_box, L, gp, coff, sc.perm.as<int32_t>(),
-                                               sc.sbox.as<double>(), sc.excl.as<uint64_t>(), n_excl, row_count,
-                                               sc.pair_keys.as<int32_t>(), nullptr, nullptr,
-                                               sc.counts.as<int64_t>(), max_count, item_loff);
-    LC_CHECK_LAUNCH();
+    launch_pdl(grid_query_warp_kernel<true>, (unsigned)ceil_div(L * 32, 256), 256, s, pdl, loop_box, L, gp, coff,
+               sc.perm.as<int32_t>(), sc.sbox.as<double>(), sc.excl.as<uint64_t>(), n_excl, row_count,
+               sc.pair_keys.as<int32_t>(), nullptr, nullptr, sc.counts.as<int64_t>(), max_count, item_loff);
     tl_mark("query", s);
     // (a single-block scan measured 14 us here vs 8.4 us for DeviceScan's init + scan)
     exclusive_scan_i64(sc.counts.as<int64_t>(), sc.offs.as<int64_t>(), L + 1, sc.cub_tmp.ptr, sc.cub_tmp.bytes, s);
@@ -1060,7 +1068,8 @@ int64_t run_pls(const double *loop_box, int64_t L, const uint64_t *h_excl, int64
 }
 
 void launch_loop_grid(const double *coeffs, const double *t, const double *verts, const int64_t *loff, int64_t L,
-                      unsigned long long *loop_min_diag2, double *loop_box, PlsScratch &sc, cudaStream_t s) {
+                      unsigned long long *loop_min_diag2, double *loop_box, PlsScratch &sc, cudaStream_t s,
+                      bool pdl) {
     const int64_t max_cells = pls_grid_max_cells(L);
     sc.axis.reserve(sizeof(GridParams), s);
     sc.counts.reserve(sizeof(int64_t) * (L + 8 > 8 ? L + 8 : 8), s);
@@ -1068,25 +1077,22 @@ void launch_loop_grid(const double *coeffs, const double *t, const double *verts
     int64_t blocks = ceil_div(L, 4);
     if (blocks > 148 * 6) blocks = 148 * 6;
     if (verts)
-        loop_grid_kernel<true><<<(unsigned)blocks, 128, 0, s>>>(nullptr, nullptr, verts, loff, L, loop_min_diag2,
-                                                                loop_box, acc, reinterpret_cast<unsigned *>(acc + 7),
-                                                                max_cells, sc.axis.as<GridParams>());
+        launch_pdl(loop_grid_kernel<true>, (unsigned)blocks, 128, s, pdl, (const double *)nullptr,
+                   (const double *)nullptr, verts, loff, L, loop_min_diag2, loop_box, acc,
+                   reinterpret_cast<unsigned *>(acc + 7), max_cells, sc.axis.as<GridParams>());
     else
-        loop_grid_kernel<false><<<(unsigned)blocks, 128, 0, s>>>(coeffs, t, nullptr, loff, L, loop_min_diag2,
-                                                                 loop_box, acc, reinterpret_cast<unsigned *>(acc + 7),
-                                                                 max_cells, sc.axis.as<GridParams>());
-    LC_CHECK_LAUNCH();
+        launch_pdl(loop_grid_kernel<false>, (unsigned)blocks, 128, s, pdl, coeffs, t, (const double *)nullptr, loff, L,
+                   loop_min_diag2, loop_box, acc, reinterpret_cast<unsigned *>(acc + 7), max_cells,
+                   sc.axis.as<GridParams>());
 }
 
 void launch_pls_grid(const double *loop_box, int64_t L, int64_t n_excl, PlsScratch &sc, int32_t *pairs, int64_t cap,
                      const int64_t *loff, PairGeom *pg, int64_t *item_off, int64_t *d_tot, int64_t item_cap,
-                     cudaStream_t s, const int **d_max_row, bool prezeroed, bool grid_ready) {
-    grid_prefix(loop_box, L, n_excl, sc, s, loff, prezeroed, grid_ready);
-    slots_compact_items_kernel<<<(unsigned)ceil_div(L, 64), 64, 0, s>>>(sc.idx.as<int>(), sc.offs.as<int64_t>(), L,
-                                                                          sc.pair_keys.as<int32_t>(), pairs, cap, loff,
-                                                                          pg, item_off, d_tot, sc.counter.as<int>(),
-                                                                          item_cap);
-    LC_CHECK_LAUNCH();
+                     cudaStream_t s, const int **d_max_row, bool prezeroed, bool grid_ready, bool pdl) {
+    grid_prefix(loop_box, L, n_excl, sc, s, loff, prezeroed, grid_ready, pdl);
+    launch_pdl(slots_compact_items_kernel, (unsigned)ceil_div(L, 64), 64, s, pdl, sc.idx.as<int>(),
+               sc.offs.as<int64_t>(), L, sc.pair_keys.as<int32_t>(), pairs, cap, loff, pg, item_off, d_tot,
+               sc.counter.as<int>(), item_cap);
     *d_max_row = sc.counter.as<int>();
 }
 

@@ -64,12 +64,14 @@ constexpr int kRowSlots = 16;
 struct PairGeom;
 void launch_pls_grid(const double *loop_box, int64_t L, int64_t n_excl, PlsScratch &sc, int32_t *pairs, int64_t cap,
                      const int64_t *loff, PairGeom *pg, int64_t *item_off, int64_t *d_tot, int64_t item_cap,
-                     cudaStream_t s, const int **d_max_row, bool prezeroed = false, bool grid_ready = false);
+                     cudaStream_t s, const int **d_max_row, bool prezeroed = false, bool grid_ready = false,
+                     bool pdl = false);
 // Fused path: loop boxes + minimum squared diagonals with the grid reduction folded
 // in (launch_pls_grid(..., grid_ready = true) then skips its reduction); needs the
 // keys prezeroed (launch_grid_prezero) and loops of <= 1024 segments.
 void launch_loop_grid(const double *coeffs, const double *t, const double *verts, const int64_t *loff, int64_t L,
-                      unsigned long long *loop_min_diag2, double *loop_box, PlsScratch &sc, cudaStream_t s);
+                      unsigned long long *loop_min_diag2, double *loop_box, PlsScratch &sc, cudaStream_t s,
+                      bool pdl = false);
 
 // Scratch sizes of launch_pls_grid, and one kernel doing the memsets it issues
 // (grid-reduce keys, cell counts, largest row count) plus `extra` int ranges —
