@@ -1192,7 +1192,7 @@ void launch_pass1_brute(const DiscInput &in, const int64_t *d_P, DiscScratch &sc
 
 void launch_discretize_checks(const DiscInput &in, const int64_t *d_P, const DiscParams &prm, DiscScratch &sc,
                               DiscOutput &out, cudaStream_t s, cudaEvent_t chords_done, const PreCounters **d_ctr,
-                              bool brute_in_gauss, cudaStream_t brute_stream) {
+                              bool brute_by_caller) {
     const int64_t L = in.L, M = in.M, Pcap = in.P;
     const double min_diam = prm.epsilon * prm.xi;
     PreCounters *ctr = sc.prectr.as<PreCounters>();
@@ -1208,7 +1208,7 @@ void launch_discretize_checks(const DiscInput &in, const int64_t *d_P, const Dis
         pre_loops_kernel<<<grid_for(L, 32), 32, 0, s>>>(in.loop_min_diag, sc.paired.as<uint8_t>(), L, min_diam, ctr);
         LC_CHECK_LAUNCH();
     }
-    if (Pcap > 0 && M > 0 && !brute_in_gauss && !brute_stream) {   // brute_stream: launch_pass1_brute by the caller
+    if (Pcap > 0 && M > 0 && !brute_by_caller) {   // else launch_pass1_brute on the caller's stream
         // the 8-warp grid-stride kernel (default) runs in the slots the short-lived Gauss
         // CTAs free; LINKCERT_BRUTE_LITE=1 selects the single-warp variant (A/B: 0.460 vs
         // 0.463 ms per Kusari step)

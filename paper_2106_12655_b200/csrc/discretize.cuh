@@ -109,7 +109,7 @@ void launch_discretize_chords(const DiscInput &in, const DiscParams &prm, DiscSc
                               cudaStream_t s);
 void launch_discretize_checks(const DiscInput &in, const int64_t *d_P, const DiscParams &prm, DiscScratch &sc,
                               DiscOutput &out, cudaStream_t s, cudaEvent_t chords_done, const PreCounters **d_ctr,
-                              bool brute_in_gauss = false, cudaStream_t brute_stream = nullptr);
+                              bool brute_by_caller = false);
 // The pass-1 pair check alone (brute_any_kernel, grid-stride over *d_P pairs): on the
 // critical stream after the segment boxes, followed by the Gauss sum as its
 // programmatic dependent (the kernel triggers its dependents as it starts).

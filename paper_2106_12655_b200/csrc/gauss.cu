@@ -23,7 +23,6 @@
 // the item range across GPUs.
 #include "gauss.cuh"
 #include "geom.cuh"
-#include "pass1.cuh"
 
 #include "scan.cuh"
 
@@ -36,20 +35,8 @@ constexpr double kInvTwoPi = 0.15915494309189535;     // 1 / (2 pi), correctly r
 #define LC_GAUSS_CARVEOUT 10   // % of the unified L1 kept as shared memory beside the Gauss CTAs
 #endif
 constexpr int kGaussCarveout = LC_GAUSS_CARVEOUT;
-#ifndef LC_PAIRS_STATIC
-#define LC_PAIRS_STATIC 0          // pair kernel: 1 = static chunks, short-lived CTAs; 0 = persistent claiming
-#endif
-#ifndef LC_PAIRS_WAVES
-#define LC_PAIRS_WAVES 16          // CTA waves of the static pair kernel (A/B: 4 / 8 / 16 -> 16 best)
-#endif
-#ifndef LC_PAIRS_PRIORITY_LOW
-#define LC_PAIRS_PRIORITY_LOW 0    // launch the pair kernel at the lowest stream priority
-#endif
 #ifndef LC_PAIRS_PREFETCH
 #define LC_PAIRS_PREFETCH 1        // persistent pair kernel: prefetch the next claim / pair geometry
-#endif
-#ifndef LC_PAIRS_PASS1
-#define LC_PAIRS_PASS1 0
 #endif
 #ifndef LC_MINB
 #define LC_MINB 2   // resident CTAs per SM the phase kernel is compiled for (A/B: -DLC_MINB=n)
@@ -533,26 +520,14 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) gauss_pairs_kernel(
     unsigned long long *__restrict__ counter, const int *__restrict__ abort, const int64_t *__restrict__ d_bounds,
     int shard, double *__restrict__ partials, double *__restrict__ raw, int64_t *__restrict__ lk,
     uint8_t *__restrict__ flags, double *__restrict__ h_raw, int64_t *__restrict__ h_lk,
-    uint8_t *__restrict__ h_flags, const Pass1Args chk, const EarlyExitArgs ee) {
-#if LC_PAIRS_PASS1
-    __shared__ int32_t sidx[kCtaThreads / 32][2][kAnyCap];
-    __shared__ float sbox[kCtaThreads / 32][2][6 * kAnyCap];
-#endif
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint8_t *__restrict__ h_flags, const EarlyExitArgs ee) {
+    const int lane = threadIdx.x & 31;
     int64_t b = 0, e = *dP < pcap ? *dP : pcap;
     if (d_bounds) {
         b = d_bounds[shard];
         e = d_bounds[shard + 1];
     }
-#if LC_PAIRS_STATIC
-    // non-persistent: CTA c takes a contiguous chunk of the pairs (its warps
-    // interleaved) and exits, so higher-priority kernels (the pass-1 checks) get
-    // the SM slots the retiring CTAs free instead of waiting for the kernel's end
-    const int64_t chunk = (e - b + gridDim.x - 1) / gridDim.x;
-    const int64_t cb = b + (int64_t)blockIdx.x * chunk, ce = cb + chunk < e ? cb + chunk : e;
-    for (int64_t p = cb + w; p < ce; p += kCtaThreads / 32) {
-        if (abort && __shfl_sync(0xffffffffu, lane == 0 ? *(volatile const int *)abort : 0, 0)) break;
-#elif LC_PAIRS_PREFETCH
+#if LC_PAIRS_PREFETCH
     // two-stage software pipeline of the per-pair prologue: the claim of pair n+2 and the
     // PairGeom load of pair n+1 are issued while pair n is summed, so a pair starts with
     // its vertex loads instead of claim -> geometry -> vertices (three dependent round trips)
@@ -578,18 +553,10 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) gauss_pairs_kernel(
         if (p >= e) break;
         const PairGeom g = pg[p];
 #endif
-#if LC_PAIRS_STATIC
-        const PairGeom g = pg[p];
-#endif
         if (ee.posv) {   // early exit: a pair past the first failure found so far is cancelled
             if ((unsigned long long)ee.posv[p] > *(volatile unsigned long long *)ee.first_fail) continue;
             if (lane == 0) atomicAdd(ee.n_eval, 1ULL);
         }
-#if LC_PAIRS_PASS1   // A/B: the pair's pass-1 check inside the sum (measured slower than the checks branch)
-        if (chk.box)
-            brute_any_pair(p, chk.box, chk.fbox, chk.M, chk.loff, chk.lbox, chk.L, chk.pairs, sidx[w][0], sidx[w][1],
-                           sbox[w][0], sbox[w][1], lane, chk.marked, chk.abort);
-#endif
         const int n = g.items_r * g.items_c;
         double s = 0.0;
         for (int it = 0; it < n; ++it) {
@@ -895,12 +862,12 @@ void launch_gauss_items(int mode, const double *X, const double *Y, const double
 void launch_gauss_pairs(int mode, const double *X, const double *Y, const double *Z, const PairGeom *pg,
                         const int64_t *d_P, int64_t pcap, unsigned long long *counter, const int *abort,
                         const int64_t *d_bounds, int shard, double *partials, double *raw, int64_t *lk, uint8_t *flags,
-                        double *h_raw, int64_t *h_lk, uint8_t *h_flags, cudaStream_t s, const Pass1Args &chk,
-                        const EarlyExitArgs &ee, bool pdl) {
+                        double *h_raw, int64_t *h_lk, uint8_t *h_flags, cudaStream_t s, const EarlyExitArgs &ee,
+                        bool pdl) {
     if (pcap <= 0) return;
     using Kern = void (*)(const double *, const double *, const double *, const PairGeom *, const int64_t *, int64_t,
                           unsigned long long *, const int *, const int64_t *, int, double *, double *, int64_t *,
-                          uint8_t *, double *, int64_t *, uint8_t *, const Pass1Args, const EarlyExitArgs);
+                          uint8_t *, double *, int64_t *, uint8_t *, const EarlyExitArgs);
     Kern fn;
     switch (mode) {
         case GAUSS_PHASE: fn = gauss_pairs_kernel<GAUSS_PHASE, LC_MINB>; break;
@@ -920,28 +887,21 @@ void launch_gauss_pairs(int mode, const double *X, const double *Y, const double
         occ[mode] = per < 1 ? 1 : per;
     }
     int64_t blocks = (int64_t)num_sms() * occ[mode];
-#if LC_PAIRS_STATIC
-    blocks *= LC_PAIRS_WAVES;   // several short-lived CTA waves (see the kernel)
-#endif
     const int64_t need = ceil_div(pcap, threads / 32);
     if (blocks > need) blocks = need;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)blocks);
     cfg.blockDim = dim3(threads);
     cfg.stream = s;
-    cudaLaunchAttribute attr[2];
-    int prio_lo = 0, prio_hi = 0;
-    LC_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-    attr[0].id = cudaLaunchAttributePriority;
-    attr[0].val.priority = LC_PAIRS_PRIORITY_LOW ? prio_lo : prio_hi;   // below the checks branch
     // pdl: a programmatic dependent of the kernel before it on the stream (the pass-1
     // check), launched once that kernel's CTAs are all resident
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 2 : 1;
+    cfg.numAttrs = pdl ? 1 : 0;
     LC_CUDA(cudaLaunchKernelEx(&cfg, fn, X, Y, Z, pg, d_P, pcap, counter, abort, d_bounds, shard, partials, raw, lk,
-                               flags, h_raw, h_lk, h_flags, chk, ee));
+                               flags, h_raw, h_lk, h_flags, ee));
     LC_CHECK_LAUNCH();
 }
 

@@ -111,19 +111,6 @@ void launch_gauss_items(int mode, const double *X, const double *Y, const double
 // cost-balanced pair split) and evaluate each pair's items in order; raw is bitwise the
 // item path's per-pair sum.  partials == null: raw / lk / flags written to the device
 // arrays and to the pinned host arrays; else raw to partials[p] (the sharded exchange).
-// Pass-1 check inputs (pass1.cuh brute_any_pair): when box != null every claimed
-// pair is checked first (hits -> *marked, *abort = 1).
-struct Pass1Args {
-    const double *box = nullptr;   // segment boxes (6 x M)
-    const float *fbox = nullptr;   // outward-rounded float copy
-    int64_t M = 0;
-    const int64_t *loff = nullptr;
-    const double *lbox = nullptr;  // loop boxes (6 x L)
-    int64_t L = 0;
-    const int32_t *pairs = nullptr;
-    unsigned long long *marked = nullptr;
-    int *abort = nullptr;
-};
 // Device early exit of verify(early_exit=True) (certify.py:195-216): the pairs are
 // evaluated against the reference certificate in the reference's ordering
 // (reference pairs in key order, then the other candidates in key order);
@@ -140,8 +127,7 @@ void launch_gauss_pairs(int mode, const double *X, const double *Y, const double
                         const int64_t *d_P, int64_t pcap, unsigned long long *counter, const int *abort,
                         const int64_t *d_bounds, int shard, double *partials, double *raw, int64_t *lk, uint8_t *flags,
                         double *h_raw, int64_t *h_lk, uint8_t *h_flags, cudaStream_t s,
-                        const Pass1Args &chk = Pass1Args(), const EarlyExitArgs &ee = EarlyExitArgs(),
-                        bool pdl = false);
+                        const EarlyExitArgs &ee = EarlyExitArgs(), bool pdl = false);
 // Early-exit preparation after the PLS: posv / want of every candidate pair (binary
 // search of its key in the certificate) and *first_fail lowered to the place of every
 // certificate pair that is no longer a candidate (its value is 0 there: a failure).

@@ -1,7 +1,6 @@
 // Pass-1 detection of one loop pair (discretize.py:151-159 marking, only "was
-// anything marked"), shared by the checks branch of the fused pipeline
-// (discretize.cu) and the pair-claiming Gauss kernel (gauss.cu), which runs it
-// on every pair it claims so the check needs no SM slots of its own.
+// anything marked"): the fused pipeline's check that a model needs no
+// refinement (brute_any_kernel / brute_any_lite_kernel, discretize.cu).
 #pragma once
 #include <cuda_runtime.h>
 

@@ -769,13 +769,11 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
         // beside the work items and the Gauss sum
         LC_CUDA(cudaEventRecord(ev_pairs, s));
         LC_CUDA(cudaStreamWaitEvent(side[1], ev_pairs, 0));
-        // (Pass1Args: the pass-1 pair check can also run inside the Gauss kernel — measured
-        // slower than this branch beside it, 0.49 vs 0.47 ms per Kusari step)
         // the pass-1 pair check goes on the critical stream right before the sum, which
-        // starts beside it as its programmatic dependent (LC_BRUTE_PDL); the rest of the
-        // checks stay on this branch
-        launch_discretize_checks(in, dP, prm, disc_sc, dout, side[1], ev_chords, &ctr, /*brute_in_gauss=*/false,
-                                 kBrutePdl ? s : nullptr);
+        // starts beside it as its programmatic dependent; the rest of the checks stay on
+        // this branch (measured: the check inside the Gauss kernel, 0.49 ms per Kusari
+        // step, or starved on this branch behind the persistent sum, 0.47 ms)
+        launch_discretize_checks(in, dP, prm, disc_sc, dout, side[1], ev_chords, &ctr, kBrutePdl);
         tl_mark("S1:checks", side[1]);
         record(EV_DISC, side[1]);
         // the pair list is final: the copy engine moves the whole capacity to pinned
@@ -807,42 +805,20 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
 #endif
         // warps claim whole pairs; unsharded, each pair's raw / lk / flags go straight to
         // the pinned result arrays as it completes (no reduce / export pass after the sum)
-        // (LINKCERT_PAIR_EXPORT=1: A/B — the sums go to the partials, a coalesced export follows)
-        static const bool pair_export = [] {
-            const char *e = getenv("LINKCERT_PAIR_EXPORT");
-            return e && e[0] == '1';
-        }();
-        const bool via_partials = sharded || pair_export;
-        Pass1Args chk;
-        chk.box = d_seg_box.as<double>();
-        chk.fbox = d_seg_fbox.as<float>();
-        chk.M = M;
-        chk.loff = d_loff.as<int64_t>();
-        chk.lbox = d_loop_box.as<double>();
-        chk.L = L;
-        chk.pairs = d_pairs.as<int32_t>();
-        chk.marked = &disc_sc.prectr.as<PreCounters>()->marked;
-        chk.abort = &disc_sc.prectr.as<PreCounters>()->abort;
         launch_gauss_pairs(mode, dout.X.as<double>(), dout.Y.as<double>(), dout.Z.as<double>(), d_pg.as<PairGeom>(), dP,
                            pcap, d_counter.as<unsigned long long>(), &disc_sc.prectr.as<PreCounters>()->abort,
                            sharded ? d_bounds.as<int64_t>() : nullptr, shard,
-                           via_partials ? d_partials.as<double>() : nullptr, d_raw.as<double>(), d_lk.as<int64_t>(),
+                           sharded ? d_partials.as<double>() : nullptr, d_raw.as<double>(), d_lk.as<int64_t>(),
                            d_flags.as<uint8_t>(), reinterpret_cast<double *>(hr), reinterpret_cast<int64_t *>(hl),
-                           reinterpret_cast<uint8_t *>(hf), s, Pass1Args(), eea, kBrutePdl);
+                           reinterpret_cast<uint8_t *>(hf), s, eea, kBrutePdl);
         record(EV_GAUSS1);
         tl_mark("gauss", s);
         LC_CUDA(cudaStreamWaitEvent(s, ev_checks, 0));
-        if (!sharded && pair_export) {
-            launch_reduce_export(d_partials.as<double>(), nullptr, dP, pcap, d_items, dmx, ctr, dout.d_val_err, st,
-                                 d_raw.as<double>(), d_lk.as<int64_t>(), d_flags.as<uint8_t>(),
-                                 reinterpret_cast<double *>(hr), reinterpret_cast<int64_t *>(hl),
-                                 reinterpret_cast<uint8_t *>(hf), s);
-        } else {   // the run's status record (sharded: lc_shard_finish reduces after the exchange)
-            export_results_kernel<<<1, 32, 0, s>>>(dP, pcap, d_items, dmx, ctr, dout.d_val_err, nullptr, nullptr,
-                                                   nullptr, nullptr, st, nullptr, nullptr, nullptr, nullptr,
-                                                   ee ? d_ee.as<unsigned long long>() : nullptr);
-            LC_CHECK_LAUNCH();
-        }
+        // the run's status record (sharded: lc_shard_finish reduces after the exchange)
+        export_results_kernel<<<1, 32, 0, s>>>(dP, pcap, d_items, dmx, ctr, dout.d_val_err, nullptr, nullptr, nullptr,
+                                               nullptr, st, nullptr, nullptr, nullptr, nullptr,
+                                               ee ? d_ee.as<unsigned long long>() : nullptr);
+        LC_CHECK_LAUNCH();
         record(EV_END);   // "reduce" = Gauss end -> status in pinned memory
         tl_mark("export", s);
         LC_CUDA(cudaEventRecord(ev_leave, crit));
