@@ -426,22 +426,21 @@ __device__ __forceinline__ int64_t find_pair(const int64_t *__restrict__ item_of
     return lo;
 }
 
-// One work item (row-block group ir, column-strip group ic of pair tiling g):
-// every lane's strip, then the fixed xor butterfly.  Returns the butterfly sum
-// (lane 0's value is the item partial of every path).
+// Lane `vl`'s strip of work item (ir, ic) of pair tiling g, before the butterfly:
+// row block vl & (2^rb - 1) of row group ir, column strip vl >> rb of column group ic.
 template <int MODE, bool KSM>
-__device__ __forceinline__ double item_value(const double *__restrict__ X, const double *__restrict__ Y,
-                                             const double *__restrict__ Z, const PairGeom &g, int ir, int ic, int lane,
-                                             double *ksh) {
+__device__ __forceinline__ double vlane_value(const double *__restrict__ X, const double *__restrict__ Y,
+                                              const double *__restrict__ Z, const PairGeom &g, int ir, int ic, int vl,
+                                              double *ksh) {
     const int rbm = (1 << g.rb_log2) - 1;
-    const int my_rb = lane & rbm, my_cs = lane >> g.rb_log2;
+    const int my_rb = vl & rbm, my_cs = vl >> g.rb_log2;
     const int row0 = ((ir << g.rb_log2) + my_rb) * R;
     const int64_t c0l = ((int64_t)ic * (32 >> g.rb_log2) + my_cs) * g.cl;
     const int c0 = (int)(c0l < g.ncols ? c0l : g.ncols);
     const int c1 = min(c0 + g.cl, g.ncols);
     double val = 0.0;
     if constexpr (MODE == GAUSS_ANGLESUM) {   // items of 32 whole rows: lane = row
-        const int row = (ir << 5) + lane;
+        const int row = (ir << 5) + vl;
         if (row < g.nrows) val = lane_anglesum(X, Y, Z, g.row_off, row, g.col_off, g.ncols);
     } else if (row0 < g.nrows && c0 < c1) {
         if (MODE == GAUSS_REF) {
@@ -458,6 +457,17 @@ __device__ __forceinline__ double item_value(const double *__restrict__ X, const
                       : lane_strip<MODE, false>(X, Y, Z, g.row_off, g.nrows, g.col_off, row0, c0, c1, kv);
         }
     }
+    return val;
+}
+
+// One work item (row-block group ir, column-strip group ic of pair tiling g):
+// every lane's strip, then the fixed xor butterfly.  Returns the butterfly sum
+// (lane 0's value is the item partial of every path).
+template <int MODE, bool KSM>
+__device__ __forceinline__ double item_value(const double *__restrict__ X, const double *__restrict__ Y,
+                                             const double *__restrict__ Z, const PairGeom &g, int ir, int ic, int lane,
+                                             double *ksh) {
+    double val = vlane_value<MODE, KSM>(X, Y, Z, g, ir, ic, lane, ksh);
 #pragma unroll
     for (int off = 16; off; off >>= 1) val += __shfl_xor_sync(0xffffffffu, val, off);
     return val;
