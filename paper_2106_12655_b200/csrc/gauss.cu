@@ -585,9 +585,11 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) gauss_pairs_kernel(
                 raw[p] = s;
                 lk[p] = r;
                 flags[p] = f;
+#ifndef LC_AB_NO_HOSTW
                 h_raw[p] = s;
                 h_lk[p] = r;
                 h_flags[p] = f;
+#endif
                 // NaN / ambiguous raw: compute_link raises there (kernels.py:68-73), which ends the
                 // reference's evaluation order too
                 if (ee.posv && (r != ee.want[p] || f)) atomicMin(ee.first_fail, (unsigned long long)ee.posv[p]);

@@ -1,5 +1,6 @@
 // Pipeline stage orchestration on one device/stream (host side of the C-ABI).
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cstring>
 #include <thread>
@@ -204,7 +205,8 @@ void Pipeline::release() {
                       &d_quads, &d_qout, &dout.X, &dout.Y, &dout.Z, &dout.voff, &dout.vert_off};
     for (DevBuf *b : bufs) b->release(s);
     DevBuf *pb[] = {&pls_sc.keys, &pls_sc.keys_sorted, &pls_sc.idx, &pls_sc.perm, &pls_sc.sbox, &pls_sc.counter,
-                    &pls_sc.cub_tmp, &pls_sc.pair_keys, &pls_sc.pair_keys_sorted, &pls_sc.axis, &pls_sc.excl};
+                    &pls_sc.cub_tmp, &pls_sc.pair_keys, &pls_sc.pair_keys_sorted, &pls_sc.axis, &pls_sc.excl,
+                    &pls_sc.counts, &pls_sc.offs, &pls_sc.lcell, &pls_sc.lrank};
     for (DevBuf *b : pb) b->release(s);
     DiscScratch &d = disc_sc;
     DevBuf *db[] = {&d.paired, &d.act_seg, &d.act_loop, &d.act_tlo, &d.act_thi, &d.act_off, &d.nxt_seg,
@@ -833,7 +835,20 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
                 2.220446049250313e-16 * prm.xi, alloc_generation().load(), ee ? n_ref : -1};
     last_fast_graph = false;
     if (!no_graph && graph_exec && key == graph_key) {
+        static const bool ginfo = [] {
+            const char *e = getenv("LINKCERT_GRAPH_INFO");
+            return e && e[0] == '1';
+        }();
+        const auto t0 = std::chrono::steady_clock::now();
         LC_CUDA(cudaGraphLaunch(graph_exec, s));
+        if (ginfo) {
+            const auto t1 = std::chrono::steady_clock::now();
+            cudaStreamSynchronize(s);
+            const auto t2 = std::chrono::steady_clock::now();
+            fprintf(stderr, "[graph] launch call %.2f us, to sync return %.2f us\n",
+                    std::chrono::duration<double, std::micro>(t1 - t0).count(),
+                    std::chrono::duration<double, std::micro>(t2 - t0).count());
+        }
         launch_counter().fetch_add(graph_launches, std::memory_order_relaxed);
         last_fast_graph = true;
         derived = true;
@@ -863,6 +878,22 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
         }
         LC_CUDA(cudaStreamEndCapture(s, &g));
         graph_launches = launch_counter().load() - n0;
+        if (const char *gi = getenv("LINKCERT_GRAPH_INFO"); gi && gi[0] == '1') {   // debug: node census
+            size_t nn = 0;
+            LC_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
+            std::vector<cudaGraphNode_t> nodes(nn);
+            LC_CUDA(cudaGraphGetNodes(g, nodes.data(), &nn));
+            int by_type[32] = {};
+            for (auto n : nodes) {
+                cudaGraphNodeType t;
+                LC_CUDA(cudaGraphNodeGetType(n, &t));
+                by_type[(int)t & 31]++;
+            }
+            fprintf(stderr, "[graph] %zu nodes:", nn);
+            for (int t = 0; t < 32; ++t)
+                if (by_type[t]) fprintf(stderr, " type%d=%d", t, by_type[t]);
+            fprintf(stderr, "\n");
+        }
         const bool same_gen = alloc_generation().load() == key.gen;
         if (same_gen) {
             // honour the captured per-node priorities (critical path / checks high, chords low)
