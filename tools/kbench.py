@@ -40,6 +40,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--modes", default="0")
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--no-ribbon", action="store_true", help="skip the 100k x 100k ribbon pair (its pair-kernel run is ~20 s)")
     a = ap.parse_args()
     modes = [int(x) for x in a.modes.split(",")]
     ctx = _native.context(0)
@@ -52,7 +53,7 @@ def main():
     nv = np.diff(voff)
     sp = int(np.sum(nv[pairs[:, 0]] * nv[pairs[:, 1]]))
     bench_staged(ctx, modes, a.reps, "kusari", sp)
-    for n in (100_000,):
+    for n in () if a.no_ribbon else (100_000,):
         x, y = gen.ribbon_pair(10, n)
         off2 = np.array([0, n, 2 * n], dtype=np.int64)
         ctx.stage_polylines(np.concatenate([x, y]), off2, np.array([[0, 1]], dtype=np.int32))
