@@ -1,8 +1,11 @@
 """Per-kernel table of the last device step in an ncu launch list (--metrics gpu__time_duration.sum CSV).
 
 usage: python tools/step_table.py launches.csv [first_kernel_regex]
-The step is taken as the kernels from the last occurrence of the first-kernel
-pattern (default: seg_boxes) to the end of the list.
+A step is the run of kernels from one occurrence of the first-kernel pattern
+(default: prezero_kernel, the fused graph's first node) to the next; the table
+shows the last step that ran the fused pair Gauss kernel (bench.py's timed
+steps), not the e2e verifies, the standalone kernel timing or the peak probes
+that follow them in the list.
 """
 import collections
 import csv
@@ -10,7 +13,7 @@ import re
 import sys
 
 path = sys.argv[1]
-first = re.compile(sys.argv[2] if len(sys.argv) > 2 else "seg_boxes")
+first = re.compile(sys.argv[2] if len(sys.argv) > 2 else "prezero_kernel")
 rows = list(csv.reader(open(path)))
 hdr, recs = None, []
 for r in rows:
@@ -21,9 +24,11 @@ for r in rows:
         d = dict(zip(hdr, r))
         name = re.sub(r"\(.*", "", d["Kernel Name"])[:80]
         recs.append((name, float(d["Metric Value"].replace(",", "")) / 1000.0))
-starts = [i for i, (k, _) in enumerate(recs) if first.search(k)]
-start = starts[-1]            # the last step in the list runs to its end
-step = [r for r in recs[start:] if "dfma_chain" not in r[0]]   # not the bench's peak probe
+starts = [i for i, (k, _) in enumerate(recs) if first.search(k)] + [len(recs)]
+steps = [recs[a:b] for a, b in zip(starts, starts[1:])]
+probe = re.compile("dfma_chain|dmma_chain|gauss_items_kernel|item_pair|pair_geom_kernel")
+steps = [[r for r in st if not probe.search(r[0])] for st in steps if any("gauss_pairs" in k for k, _ in st)]
+step = steps[-1]
 tot = sum(v for _, v in step)
 agg = collections.OrderedDict()
 for k, v in step:
