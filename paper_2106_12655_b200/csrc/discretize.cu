@@ -235,7 +235,8 @@ constexpr int kAnyWarps = 8;
 __global__ void __launch_bounds__(32 * kAnyWarps, 4) brute_any_kernel(
     const double *__restrict__ box, const float *__restrict__ fbox, int64_t M, const int64_t *__restrict__ loff,
     const double *__restrict__ lbox, int64_t L, const int32_t *__restrict__ pairs, int64_t P,
-    const int64_t *__restrict__ dP, unsigned long long *__restrict__ marked, int *__restrict__ abort) {
+    const int64_t *__restrict__ dP, unsigned long long *__restrict__ marked, int *__restrict__ abort,
+    const float *__restrict__ sub) {
     __shared__ int32_t sidx[kAnyWarps][2][kAnyCap];
     __shared__ float sbox[kAnyWarps][2][6 * kAnyCap];
     // programmatic dependent launch: the Gauss kernel queued behind this one on the
@@ -245,6 +246,11 @@ __global__ void __launch_bounds__(32 * kAnyWarps, 4) brute_any_kernel(
     if (dP && *dP < P) P = *dP;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t nw = (int64_t)gridDim.x * kAnyWarps;
+    if (sub) {   // the 8-segment group boxes exist (fused path, loops of <= 1024 segments)
+        for (int64_t p = blockIdx.x * (int64_t)kAnyWarps + w; p < P; p += nw)
+            brute_any_pair_sub(p, box, fbox, sub, M, L, loff, pairs, lane, marked, abort);
+        return;
+    }
     for (int64_t p = blockIdx.x * (int64_t)kAnyWarps + w; p < P; p += nw)
         brute_any_pair(p, box, fbox, M, loff, lbox, L, pairs, sidx[w][0], sidx[w][1], sbox[w][0], sbox[w][1], lane,
                        marked, abort);
@@ -1186,7 +1192,8 @@ void launch_pass1_brute(const DiscInput &in, const int64_t *d_P, DiscScratch &sc
     PreCounters *ctr = sc.prectr.as<PreCounters>();
     const int64_t blocks = ceil_div(Pcap, kAnyWarps) < 148 * 8 ? ceil_div(Pcap, kAnyWarps) : 148 * 8;
     brute_any_kernel<<<(unsigned)blocks, 32 * kAnyWarps, 0, s>>>(in.seg_box, in.seg_fbox, M, in.loff, in.loop_box,
-                                                                 in.L, in.pairs, Pcap, d_P, &ctr->marked, &ctr->abort);
+                                                                 in.L, in.pairs, Pcap, d_P, &ctr->marked, &ctr->abort,
+                                                                 in.seg_sub);
     LC_CHECK_LAUNCH();
 }
 
@@ -1223,7 +1230,7 @@ void launch_discretize_checks(const DiscInput &in, const int64_t *d_P, const Dis
             const int64_t blocks = ceil_div(Pcap, kAnyWarps) < 148 * 8 ? ceil_div(Pcap, kAnyWarps) : 148 * 8;
             brute_any_kernel<<<(unsigned)blocks, 32 * kAnyWarps, 0, s>>>(in.seg_box, in.seg_fbox, M, in.loff,
                                                                          in.loop_box, L, in.pairs, Pcap, d_P,
-                                                                         &ctr->marked, &ctr->abort);
+                                                                         &ctr->marked, &ctr->abort, in.seg_sub);
         }
         LC_CHECK_LAUNCH();
         tl_mark("S1:brute", s);

@@ -63,6 +63,8 @@ struct DiscInput {
     const int32_t *pairs;                   // (P, 2), sorted PairList
     int64_t P;
     const float *seg_fbox = nullptr;        // seg_box rounded outward to float (prefilter), optional
+    const float *seg_sub = nullptr;         // float boxes of 8-segment groups (SoA 6 x M, at each group's
+                                            // first segment; fused split path only), optional
     const double *verts = nullptr;          // closed-polyline model: vertices (M,3) (coeffs are then
                                             // LoopGeometry.from_polyline's); lets the no-split chord
                                             // write read 24 B instead of 112 B per segment

@@ -6,6 +6,8 @@
 
 #include <cstdint>
 
+#include "pls.cuh"
+
 namespace lc {
 namespace {
 
@@ -154,6 +156,73 @@ __device__ __forceinline__ void brute_any_pair(int64_t p, const double *__restri
 #undef sbox_at
 }
 
+
+// brute_any_pair with the 8-segment group boxes of seg_boxes_loop_kernel (`sub`,
+// layout pass1_group_slot; float, outward, NaN -> unbounded):
+// lane k holds group k of both loops (<= 32 groups: both loops have <= 256
+// segments); group pairs are tested a row of the warp at a time, and only
+// overlapping group pairs test their 8 x 8 segment pairs (float, then the exact
+// closed test on the double boxes).  Same decision as brute_any_pair: a segment
+// pair overlaps exactly => its float boxes and its groups overlap.
+__device__ __forceinline__ void brute_any_pair_sub(int64_t p, const double *__restrict__ box,
+                                                   const float *__restrict__ fbox, const float *__restrict__ sub,
+                                                   int64_t M, int64_t L, const int64_t *__restrict__ loff,
+                                                   const int32_t *__restrict__ pairs, int lane,
+                                                   unsigned long long *__restrict__ marked, int *__restrict__ abort) {
+    const int i = pairs[2 * p], j = pairs[2 * p + 1];
+    const int64_t bi = loff[i], ni = loff[i + 1] - bi;
+    const int64_t bj = loff[j], nj = loff[j + 1] - bj;
+    if (ni == 0 || nj == 0 || !brute_pair(ni, nj)) return;
+    const int gi = (int)((ni + 7) >> 3), gj = (int)((nj + 7) >> 3);
+    const int64_t S = pass1_group_stride(M, L), qi = pass1_group_slot(bi, i), qj = pass1_group_slot(bj, j);
+    float si[6], sj[6];
+#pragma unroll
+    for (int d = 0; d < 6; ++d) {
+        si[d] = lane < gi ? sub[d * S + qi + lane] : 0.f;
+        sj[d] = lane < gj ? sub[d * S + qj + lane] : 0.f;
+    }
+    const int u = lane & 7, w = lane >> 3;   // segment pair (u, w) and (u, w + 4) of a group pair
+    int hits = 0;
+    for (int a = 0; a < gi; ++a) {
+        float o[6];
+#pragma unroll
+        for (int d = 0; d < 6; ++d) o[d] = __shfl_sync(0xffffffffu, si[d], a);
+        const bool ov = lane < gj && !(o[0] > sj[3] || sj[0] > o[3] || o[1] > sj[4] || sj[1] > o[4] ||
+                                       o[2] > sj[5] || sj[2] > o[5]);
+        unsigned bal = __ballot_sync(0xffffffffu, ov);
+        while (bal) {
+            const int c = __ffs(bal) - 1;
+            bal &= bal - 1;
+            const int64_t ki = 8 * a + u;
+            if (ki >= ni) continue;
+            const int64_t ei = bi + ki;
+            float x[6];
+#pragma unroll
+            for (int d = 0; d < 6; ++d) x[d] = fbox[d * M + ei];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t kj = 8 * c + w + 4 * h;
+                if (kj >= nj) continue;
+                const int64_t ej = bj + kj;
+                float y[6];
+#pragma unroll
+                for (int d = 0; d < 6; ++d) y[d] = fbox[d * M + ej];
+                if (x[0] > y[3] || y[0] > x[3] || x[1] > y[4] || y[1] > x[4] || x[2] > y[5] || y[2] > x[5]) continue;
+                double lo[3], hi[3];   // a float hit: the exact closed test on the double boxes (bvh.py:93-98)
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    lo[d] = box[d * M + ei];
+                    hi[d] = box[(3 + d) * M + ei];
+                }
+                if (box_overlap(box, M, ej, lo, hi)) ++hits;
+            }
+        }
+    }
+    if (hits) {
+        atomicAdd(marked, (unsigned long long)hits);
+        if (abort) *abort = 1;
+    }
+}
 
 }  // namespace
 }  // namespace lc

@@ -20,6 +20,10 @@ constexpr bool kBrutePdl = LC_BRUTE_PDL;
 #define LC_CHAIN_PDL 1   // programmatic dependent launch along the PLS chain of the fused run
 #endif
 constexpr bool kChainPdl = LC_CHAIN_PDL;
+#ifndef LC_PASS1_GROUPS
+#define LC_PASS1_GROUPS 1   // fused pass-1 check through 8-segment group boxes (brute_any_pair_sub)
+#endif
+constexpr bool kPass1Groups = LC_PASS1_GROUPS;
 
 namespace {
 
@@ -199,7 +203,7 @@ void Pipeline::init(cudaStream_t st) {
 }
 
 void Pipeline::release() {
-    DevBuf *bufs[] = {&d_ref_keys, &d_ref_lk, &d_posv, &d_want, &d_ee, &d_bounds, &d_tot, &d_coeffs, &d_t, &d_loff, &d_seg_box, &d_seg_fbox, &d_loop_keys, &d_seg_loop, &d_loop_box, &d_min_diag, &d_model_exp,
+    DevBuf *bufs[] = {&d_ref_keys, &d_ref_lk, &d_posv, &d_want, &d_ee, &d_bounds, &d_tot, &d_coeffs, &d_t, &d_loff, &d_seg_box, &d_seg_fbox, &d_seg_sub, &d_loop_keys, &d_seg_loop, &d_loop_box, &d_min_diag, &d_model_exp,
                       &d_verts_in, &d_aos, &d_in_off, &d_voff, &d_X, &d_Y, &d_Z, &d_exp, &d_tmp_aos, &d_pairs,
                       &d_pg, &d_item_off, &d_item_pair, &d_scan, &d_counter, &d_partials, &d_raw, &d_lk, &d_flags,
                       &d_quads, &d_qout, &dout.X, &dout.Y, &dout.Z, &dout.voff, &dout.vert_off};
@@ -256,6 +260,7 @@ float Pipeline::stage_ms(int e0, int e1) {
 void Pipeline::reserve_derived() {
     d_seg_box.reserve(sizeof(double) * 6 * (M > 0 ? M : 1), s);
     d_seg_fbox.reserve(sizeof(float) * 6 * (M > 0 ? M : 1), s);
+    if (kPass1Groups) d_seg_sub.reserve(sizeof(float) * 6 * pass1_group_stride(M, L), s);
     d_seg_loop.reserve(sizeof(int32_t) * (M > 0 ? M : 1), s);
     d_loop_box.reserve(sizeof(double) * 6 * (L > 0 ? L : 1), s);
     d_min_diag.reserve(sizeof(unsigned long long) * (L > 0 ? L : 1), s);
@@ -711,6 +716,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
                      d_model_exp.as<int>(), L, M, d_pairs.as<int32_t>(), pcap};
         in.verts = model_poly ? d_verts_in.as<double>() : nullptr;
         in.seg_fbox = d_seg_fbox.as<float>();
+        in.seg_sub = split && kPass1Groups ? d_seg_sub.as<float>() : nullptr;   // written by the segment half
         reserve_discretize_fast(in, disc_sc, dout, s);
         // one node for every initial value of the run: the pass-1 counters + abort
         // flag and validation slots (launch_discretize_init's values, before any
@@ -752,7 +758,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
             const double *cp = model_poly ? nullptr : d_coeffs.as<double>(), *tp = model_poly ? nullptr : d_t.as<double>();
             launch_seg_boxes_split(cp, tp, vp, d_loff.as<int64_t>(), L, M, false, d_seg_box.as<double>(),
                                    d_seg_fbox.as<float>(), d_seg_loop.as<int32_t>(), d_model_exp.as<int>(), nullptr,
-                                   nullptr, side[0]);
+                                   nullptr, side[0], const_cast<float *>(in.seg_sub));
             tl_mark("S0:seg_boxes", side[0]);
         }
         launch_discretize_chords(in, prm, disc_sc, dout, side[0]);

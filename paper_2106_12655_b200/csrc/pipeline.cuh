@@ -32,7 +32,7 @@ struct Pipeline {
     cudaEvent_t ev_enter = nullptr, ev_leave = nullptr;   // caller stream <-> crit joins
 
     // Model: packed monomial cubics (linkcert LoopGeometry arrays, geometry.py:206-296).
-    DevBuf d_coeffs, d_t, d_loff, d_seg_box, d_seg_fbox, d_loop_keys, d_seg_loop, d_loop_box, d_min_diag, d_model_exp, d_verts_in;
+    DevBuf d_coeffs, d_t, d_loff, d_seg_box, d_seg_fbox, d_seg_sub, d_loop_keys, d_seg_loop, d_loop_box, d_min_diag, d_model_exp, d_verts_in;
     int64_t L = 0, M = 0;
     int64_t max_loop = -1;       // most segments in one loop (host-known at upload)
     bool model_ready = false;

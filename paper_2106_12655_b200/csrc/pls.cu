@@ -168,7 +168,8 @@ __global__ void seg_boxes_loop_kernel(const double *__restrict__ coeffs, const d
                                       const double *__restrict__ verts, const int64_t *__restrict__ loff, int64_t L,
                                       int64_t M, double *__restrict__ box, float *__restrict__ fbox,
                                       int32_t *__restrict__ seg_loop, unsigned long long *__restrict__ loop_min_diag2,
-                                      double *__restrict__ lbox, int *__restrict__ max_exp) {
+                                      double *__restrict__ lbox, int *__restrict__ max_exp,
+                                      float *__restrict__ sub = nullptr) {
     const int lane = threadIdx.x & 31;
     const int64_t l = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     if (l >= L) return;   // the whole warp
@@ -176,42 +177,73 @@ __global__ void seg_boxes_loop_kernel(const double *__restrict__ coeffs, const d
     double v[6] = {CUDART_INF, CUDART_INF, CUDART_INF, -CUDART_INF, -CUDART_INF, -CUDART_INF};
     unsigned long long dg = ~0ULL;
     int ex = 0;
+    // whole-warp iterations (the group boxes below reduce over lanes); lanes past the
+    // loop's end carry empty boxes
 #pragma unroll 2   // both segments' loads of a 64-segment loop in flight together
-    for (int64_t m = b + lane; m < e; m += 32) {
-        double bl[3], bh[3];
-        if (POLY) {   // see seg_boxes_kernel: the box of a from_polyline segment
-            const int64_t nx = m + 1 < e ? m + 1 : b;
+    for (int64_t k0 = 0; k0 < e - b; k0 += 32) {
+        const int64_t m = b + k0 + lane;
+        const bool ok = m < e;
+        double bl[3] = {CUDART_INF, CUDART_INF, CUDART_INF}, bh[3] = {-CUDART_INF, -CUDART_INF, -CUDART_INF};
+        if (ok) {
+            if (POLY) {   // see seg_boxes_kernel: the box of a from_polyline segment
+                const int64_t nx = m + 1 < e ? m + 1 : b;
 #pragma unroll
-            for (int d = 0; d < 3; ++d) {
-                const double a0 = verts[3 * m + d], a1 = verts[3 * nx + d] - a0;
-                // eval_axis at t = 0 and 1 with a2 = a3 = 0, bitwise: a0 (+0 for -0) and a0 + a1 (+0 for -0)
-                const double v0 = __dadd_rn(a0, 0.0), v1 = __dadd_rn(__dadd_rn(a0, a1), 0.0);
-                bl[d] = np_min(v0, v1);
-                bh[d] = np_max(v0, v1);
+                for (int d = 0; d < 3; ++d) {
+                    const double a0 = verts[3 * m + d], a1 = verts[3 * nx + d] - a0;
+                    // eval_axis at t = 0 and 1 with a2 = a3 = 0, bitwise: a0 (+0 for -0) and a0 + a1 (+0 for -0)
+                    const double v0 = __dadd_rn(a0, 0.0), v1 = __dadd_rn(__dadd_rn(a0, a1), 0.0);
+                    bl[d] = np_min(v0, v1);
+                    bh[d] = np_max(v0, v1);
+                }
+            } else {
+                tight_box(coeffs + 12 * m, t[2 * m], t[2 * m + 1], bl, bh);
             }
-        } else {
-            tight_box(coeffs + 12 * m, t[2 * m], t[2 * m + 1], bl, bh);
         }
-        if (SEG_OUT) seg_loop[m] = (int32_t)l;
+        if (SEG_OUT && ok) seg_loop[m] = (int32_t)l;
+        float fl[6];
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-            if (SEG_OUT) {
+            fl[d] = __double2float_rd(bl[d]);
+            fl[3 + d] = __double2float_ru(bh[d]);
+            if (SEG_OUT && ok) {
                 box[d * M + m] = bl[d];
                 box[(3 + d) * M + m] = bh[d];
                 if (fbox) {
-                    fbox[d * M + m] = __double2float_rd(bl[d]);
-                    fbox[(3 + d) * M + m] = __double2float_ru(bh[d]);
+                    fbox[d * M + m] = fl[d];
+                    fbox[(3 + d) * M + m] = fl[3 + d];
                 }
                 ex = max(ex, max(exp_field(bl[d]), exp_field(bh[d])));
             }
             v[d] = np_min(v[d], bl[d]);
             v[3 + d] = np_max(v[3 + d], bh[d]);
         }
-        if (LOOP_OUT) {
+        if (LOOP_OUT && ok) {
             const double dx = __dsub_rn(bh[0], bl[0]), dy = __dsub_rn(bh[1], bl[1]), dz = __dsub_rn(bh[2], bl[2]);
             const unsigned long long q = (unsigned long long)__double_as_longlong(
                 __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
             dg = q < dg ? q : dg;
+        }
+        if (SEG_OUT && sub) {
+            // float boxes of 8-segment groups (the pass-1 check's first level): 8-lane
+            // min / max; a NaN coordinate makes the group unbounded on that axis (the
+            // segment-level test then sees the NaN)
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                fl[d] = fl[d] != fl[d] ? -CUDART_INF_F : fl[d];
+                fl[3 + d] = fl[3 + d] != fl[3 + d] ? CUDART_INF_F : fl[3 + d];
+            }
+#pragma unroll
+            for (int off = 1; off < 8; off <<= 1)
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    fl[d] = fminf(fl[d], __shfl_xor_sync(0xffffffffu, fl[d], off));
+                    fl[3 + d] = fmaxf(fl[3 + d], __shfl_xor_sync(0xffffffffu, fl[3 + d], off));
+                }
+            if ((lane & 7) == 0 && ok) {
+                const int64_t slot = pass1_group_slot(m, l), S = pass1_group_stride(M, L);
+#pragma unroll
+                for (int d = 0; d < 6; ++d) sub[d * S + slot] = fl[d];
+            }
         }
     }
     if (!LOOP_OUT) {   // segment outputs only: the exponent is the one loop-level value they need
@@ -806,7 +838,8 @@ bool seg_boxes_split_ok(int64_t L, int64_t max_loop_segments) {
 
 void launch_seg_boxes_split(const double *coeffs, const double *t, const double *verts, const int64_t *loff, int64_t L,
                             int64_t M, bool loop_part, double *seg_box, float *seg_fbox, int32_t *seg_loop,
-                            int *max_exp, unsigned long long *loop_min_diag2, double *loop_box, cudaStream_t s) {
+                            int *max_exp, unsigned long long *loop_min_diag2, double *loop_box, cudaStream_t s,
+                            float *seg_sub) {
     const unsigned blocks = (unsigned)ceil_div(L * 32, 128);
     if (loop_part) {
         if (verts)
@@ -821,11 +854,11 @@ void launch_seg_boxes_split(const double *coeffs, const double *t, const double 
         if (verts)
             seg_boxes_loop_kernel<true, true, false><<<blocks, 128, 0, s>>>(nullptr, nullptr, verts, loff, L, M, seg_box,
                                                                             seg_fbox, seg_loop, nullptr, nullptr,
-                                                                            max_exp);
+                                                                            max_exp, seg_fbox ? seg_sub : nullptr);
         else
             seg_boxes_loop_kernel<false, true, false><<<blocks, 128, 0, s>>>(coeffs, t, nullptr, loff, L, M, seg_box,
                                                                              seg_fbox, seg_loop, nullptr, nullptr,
-                                                                             max_exp);
+                                                                             max_exp, seg_fbox ? seg_sub : nullptr);
     }
     LC_CHECK_LAUNCH();
 }

@@ -22,11 +22,19 @@ namespace lc {
 // The fused path's derive in two halves on two streams (loops of <= 1024 segments):
 // loop_part = loop boxes + minimum squared diagonals; otherwise the segment
 // boxes, float boxes, segment loops and the coordinate exponent (max_exp zeroed
-// by the caller).
+// by the caller), and with seg_sub the float boxes of 8-segment groups (the
+// pass-1 check's first level; layout: pass1_group_slot).
+// Float boxes of 8-segment groups, SoA 6 x pass1_group_stride(M, L): the group of
+// loop l starting at segment m (m - loff[l] a multiple of 8) sits at slot m / 8 + l —
+// consecutive within a loop, and distinct across loops (a loop adds at most one
+// partial 8-block).
+__host__ __device__ inline int64_t pass1_group_slot(int64_t m, int64_t l) { return (m >> 3) + l; }
+__host__ __device__ inline int64_t pass1_group_stride(int64_t M, int64_t L) { return (M >> 3) + L + 1; }
 bool seg_boxes_split_ok(int64_t L, int64_t max_loop_segments);
 void launch_seg_boxes_split(const double *coeffs, const double *t, const double *verts, const int64_t *loff, int64_t L,
                             int64_t M, bool loop_part, double *seg_box, float *seg_fbox, int32_t *seg_loop,
-                            int *max_exp, unsigned long long *loop_min_diag2, double *loop_box, cudaStream_t s);
+                            int *max_exp, unsigned long long *loop_min_diag2, double *loop_box, cudaStream_t s,
+                            float *seg_sub = nullptr);
 void launch_seg_boxes(const double *coeffs, const double *t, const double *verts, const int64_t *loff, int64_t L,
                       int64_t M, double *seg_box, int32_t *seg_loop, unsigned long long *loop_min_diag2, int *max_exp,
                       cudaStream_t s, float *seg_fbox = nullptr, unsigned long long *loop_keys = nullptr,
