@@ -76,8 +76,10 @@ def build(force: bool = False, verbose: bool = False, variant: str = "", defines
         if src.suffix == ".cpp":     # host-only code: the host compiler directly
             cmd = [CXX, *CXX_FLAGS, "-I", _fmt_include(), "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)]
         else:
-            cmd = [NVCC, *NVCC_FLAGS, *EXTRA_FLAGS.get(src.name, []), *[f"-D{d}" for d in defines], "-I", str(ROOT / "include"), "-c", str(src),
-                   "-o", str(obj)]
+            # LC_NVCC_EXTRA: extra nvcc flags for A/B variant builds only (e.g. "-Xptxas -regUsageLevel=8")
+            extra = os.environ.get("LC_NVCC_EXTRA", "").split() if variant else []
+            cmd = [NVCC, *NVCC_FLAGS, *EXTRA_FLAGS.get(src.name, []), *extra, *[f"-D{d}" for d in defines], "-I",
+                   str(ROOT / "include"), "-c", str(src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))

@@ -39,7 +39,10 @@ constexpr int kGaussCarveout = LC_GAUSS_CARVEOUT;
 #define LC_PAIRS_PREFETCH 1        // persistent pair kernel: prefetch the next claim / pair geometry
 #endif
 #ifndef LC_MINB
-#define LC_MINB 2   // resident CTAs per SM the phase kernel is compiled for (A/B: -DLC_MINB=n)
+#define LC_MINB 2   // resident CTAs per SM the phase items kernel is compiled for (A/B: -DLC_MINB=n)
+#endif
+#ifndef LC_PAIRS_MINB
+#define LC_PAIRS_MINB LC_MINB   // ... and the phase pair kernel (fused path)
 #endif
 
 __device__ __forceinline__ int sbit(double x) { return (int)((unsigned)__double2hiint(x) >> 31); }
@@ -882,7 +885,7 @@ void launch_gauss_pairs(int mode, const double *X, const double *Y, const double
                           uint8_t *, double *, int64_t *, uint8_t *, const EarlyExitArgs);
     Kern fn;
     switch (mode) {
-        case GAUSS_PHASE: fn = gauss_pairs_kernel<GAUSS_PHASE, LC_MINB>; break;
+        case GAUSS_PHASE: fn = gauss_pairs_kernel<GAUSS_PHASE, LC_PAIRS_MINB>; break;
         case GAUSS_ATAN: fn = gauss_pairs_kernel<GAUSS_ATAN, 1>; break;
         case GAUSS_REF: fn = gauss_pairs_kernel<GAUSS_REF, 1>; break;
         default: throw Error(LC_ERR_ARG, "the pair-claiming Gauss kernel takes modes phase / atan / ref");
