@@ -718,37 +718,39 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
         in.seg_fbox = d_seg_fbox.as<float>();
         in.seg_sub = split && kPass1Groups ? d_seg_sub.as<float>() : nullptr;   // written by the segment half
         reserve_discretize_fast(in, disc_sc, dout, s);
-        // one node for every initial value of the run: the pass-1 counters + abort
-        // flag and validation slots (launch_discretize_init's values, before any
-        // branch reads them), the grid PLS memsets and the Gauss item counter
-        {
-            static_assert(sizeof(PreCounters) == 32 && offsetof(PreCounters, marked) == 16 &&
-                              offsetof(PreCounters, err_loop) == 24,
-                          "prezero word layout of PreCounters");
-            unsigned *pc = disc_sc.prectr.as<unsigned>();
-            const ZeroRange extra[] = {
-                {pc, 1, (unsigned)INT_MAX},                   // zero_loop
-                {pc + 1, 5, 0u},                              // n_unpaired, n_large, abort, marked
-                {pc + 6, 1, (unsigned)INT_MAX},               // err_loop
-                {pc + 7, 1, 0u},                              // pad
-                {disc_sc.val_err2.ptr, 2, (unsigned)INT_MAX}, // validation: first bad loop / pair
-                {d_counter.ptr, 2, 0u},                       // Gauss item claim counter
-                {d_model_exp.ptr, 1, 0u},                     // coordinate exponent (atomicMax)
-                {ee ? d_ee.ptr : nullptr, ee ? 2 : 0, ~0u},  // early exit: first failure (~0)
-                {ee ? static_cast<unsigned *>(d_ee.ptr) + 2 : nullptr, ee ? 2 : 0, 0u},   // pairs evaluated
-            };
-            launch_grid_prezero(L, pls_sc, extra, (int)(sizeof extra / sizeof extra[0]), s);
+        // every initial value of the run — the pass-1 counters + abort flag and
+        // validation slots (launch_discretize_init's values, before any branch reads
+        // them), the grid PLS memsets, the Gauss claim counter — written by the run's
+        // first kernel: the loop-box kernel on the split path, else one prezero node
+        static_assert(sizeof(PreCounters) == 32 && offsetof(PreCounters, marked) == 16 &&
+                          offsetof(PreCounters, err_loop) == 24,
+                      "prezero word layout of PreCounters");
+        unsigned *pc = disc_sc.prectr.as<unsigned>();
+        const ZeroRange extra[] = {
+            {pc, 1, (unsigned)INT_MAX},                   // zero_loop
+            {pc + 1, 5, 0u},                              // n_unpaired, n_large, abort, marked
+            {pc + 6, 1, (unsigned)INT_MAX},               // err_loop
+            {pc + 7, 1, 0u},                              // pad
+            {disc_sc.val_err2.ptr, 2, (unsigned)INT_MAX}, // validation: first bad loop / pair
+            {d_counter.ptr, 2, 0u},                       // Gauss item claim counter
+            {d_model_exp.ptr, 1, 0u},                     // coordinate exponent (atomicMax)
+            {ee ? d_ee.ptr : nullptr, ee ? 2 : 0, ~0u},  // early exit: first failure (~0)
+            {ee ? static_cast<unsigned *>(d_ee.ptr) + 2 : nullptr, ee ? 2 : 0, 0u},   // pairs evaluated
+        };
+        const int n_extra = (int)(sizeof extra / sizeof extra[0]);
+        if (!split) {
+            launch_grid_prezero(L, pls_sc, extra, n_extra, s);
+            tl_mark("prezero", s);
         }
-        tl_mark("prezero", s);
         // branch 1: the chords need only the model — they run beside the PLS; the
         // segment half of derive goes with them, after the loop half (which it
         // would otherwise slow down by sharing the HBM bandwidth on the critical path)
         if (split) {
             const double *vp = model_poly ? d_verts_in.as<double>() : nullptr;
             const double *cp = model_poly ? nullptr : d_coeffs.as<double>(), *tp = model_poly ? nullptr : d_t.as<double>();
-            // loop boxes + minimum diagonals with the PLS grid reduction folded in
+            // loop boxes + minimum diagonals with the PLS grid reduction folded in, and the initial values
             launch_loop_grid(cp, tp, vp, d_loff.as<int64_t>(), L, d_min_diag.as<unsigned long long>(),
-                             d_loop_box.as<double>(), pls_sc, s, kChainPdl && !timeline().on);
+                             d_loop_box.as<double>(), pls_sc, s, kChainPdl && !timeline().on, extra, n_extra);
             tl_mark("loop_boxes", s);
         }
         LC_CUDA(cudaEventRecord(ev_fork, s));

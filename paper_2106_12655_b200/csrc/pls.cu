@@ -23,6 +23,31 @@ namespace {
 
 constexpr int kPackShift = 24;   // fused-path row scan: pair count in the low 24 bits, items above
 
+// The initial values of a fused run (counters, flags, cell counts ...), written by
+// the first kernel of the run (grid-stride over every range).
+constexpr int kMaxZeroRanges = 16;
+struct ZeroList {
+    ZeroRange r[kMaxZeroRanges];
+    int n;
+};
+__device__ __forceinline__ void zero_ranges(const ZeroList &zl) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (int k = 0; k < zl.n; ++k) {
+        unsigned *p = static_cast<unsigned *>(zl.r[k].ptr);
+        const unsigned v = zl.r[k].value;
+        for (int64_t i = t0; i < zl.r[k].words; i += stride) p[i] = v;
+    }
+}
+
+// acc = the grid reduction's ordered keys (3 min, 4 max) + its block counter, kept
+// at the identity between runs: set once at allocation, restored by the last
+// block of every reduction after it has read them.
+__device__ __forceinline__ void reset_grid_keys(unsigned long long *acc) {
+    for (int q = 0; q < 3; ++q) acc[q] = ~0ULL;
+    for (int q = 3; q < 8; ++q) acc[q] = 0ULL;
+}
+
 __device__ __forceinline__ int exp_field(double x) { return (__double2hiint(x) >> 20) & 0x7ff; }
 
 // Ordered 64-bit keys of doubles for atomicMin/atomicMax: monotone for
@@ -634,7 +659,7 @@ __global__ void grid_reduce_kernel(const double *__restrict__ lbox, int64_t L, u
         unsigned long long a[7];
         for (int k = 0; k < 7; ++k) a[k] = atomicAdd(acc + k, 0ULL);   // L2-coherent reads
         grid_finalize(a, max_cells, gp);
-        *done = 0;   // ready for the next run
+        reset_grid_keys(acc);   // (and the block counter, acc[7]): ready for the next run
     }
 }
 
@@ -652,9 +677,10 @@ __global__ void __launch_bounds__(128) loop_grid_kernel(const double *__restrict
                                                         unsigned long long *__restrict__ loop_min_diag2,
                                                         double *__restrict__ lbox, unsigned long long *__restrict__ acc,
                                                         unsigned *__restrict__ done, int64_t max_cells,
-                                                        GridParams *__restrict__ gp) {
+                                                        GridParams *__restrict__ gp, const ZeroList zl) {
     LC_PDL_TRIGGER();
     LC_PDL_WAIT();
+    zero_ranges(zl);   // the run's initial values, read by the kernels after this one
     __shared__ unsigned long long sk[4][7];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // block accumulators (ordered keys): min lo x3, max hi x3, max extent
@@ -732,7 +758,7 @@ __global__ void __launch_bounds__(128) loop_grid_kernel(const double *__restrict
             unsigned long long a[7];
             for (int q = 0; q < 7; ++q) a[q] = atomicAdd(acc + q, 0ULL);   // L2-coherent reads
             grid_finalize(a, max_cells, gp);
-            *done = 0;
+            reset_grid_keys(acc);   // (and the block counter)
         }
     }
 }
@@ -903,20 +929,9 @@ void launch_seg_boxes(const double *coeffs, const double *t, const double *verts
 
 
 namespace {
-constexpr int kMaxZeroRanges = 16;
-struct ZeroList {
-    ZeroRange r[kMaxZeroRanges];
-    int n;
-};
 __global__ void prezero_kernel(ZeroList zl) {
     LC_PDL_TRIGGER();
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    for (int k = 0; k < zl.n; ++k) {
-        unsigned *p = static_cast<unsigned *>(zl.r[k].ptr);
-        const unsigned v = zl.r[k].value;
-        for (int64_t i = t0; i < zl.r[k].words; i += stride) p[i] = v;
-    }
+    zero_ranges(zl);
 }
 }  // namespace
 
@@ -929,21 +944,32 @@ void reserve_pls_grid(int64_t L, PlsScratch &sc, cudaStream_t s) {
     sc.keys.reserve(sizeof(int64_t) * (max_cells + 1), s);
     sc.counter.reserve(sizeof(unsigned long long), s);
     sc.counts.reserve(sizeof(int64_t) * (L + 8 > 8 ? L + 8 : 8), s);
+    sc.acc.reserve(8 * sizeof(unsigned long long), s);
+    if (sc.acc.ptr != sc.acc_ready) {   // a new buffer: the reductions' keys at the identity, once
+        unsigned long long *acc = sc.acc.as<unsigned long long>();
+        LC_CUDA(cudaMemsetAsync(acc, 0xff, 3 * sizeof(unsigned long long), s));
+        LC_CUDA(cudaMemsetAsync(acc + 3, 0, 5 * sizeof(unsigned long long), s));
+        sc.acc_ready = sc.acc.ptr;
+    }
 }
 
-void launch_grid_prezero(int64_t L, PlsScratch &sc, const ZeroRange *extra, int n_extra, cudaStream_t s) {
+namespace {
+// grid_prefix's memsets (cell counts, largest row count) + the caller's ranges
+ZeroList grid_zero_list(int64_t L, PlsScratch &sc, const ZeroRange *extra, int n_extra) {
     const int64_t max_cells = pls_grid_max_cells(L);
-    reserve_pls_grid(L, sc, s);
-    if (n_extra < 0 || n_extra > kMaxZeroRanges - 4) throw Error(LC_ERR_ARG, "too many prezero ranges");
+    if (n_extra < 0 || n_extra > kMaxZeroRanges - 2) throw Error(LC_ERR_ARG, "too many prezero ranges");
     ZeroList zl{};
-    // the memsets of grid_prefix: 3 min keys (all ones), 4 max keys + block counter, cell counts, largest row count
-    zl.r[0] = ZeroRange{sc.counts.ptr, 6, 0xffffffffu};
-    zl.r[1] = ZeroRange{static_cast<unsigned long long *>(sc.counts.ptr) + 3, 10, 0u};
-    zl.r[2] = ZeroRange{sc.keys.ptr, 2 * (max_cells + 1), 0u};
-    zl.r[3] = ZeroRange{sc.counter.ptr, 1, 0u};
-    zl.n = 4;
+    zl.r[0] = ZeroRange{sc.keys.ptr, 2 * (max_cells + 1), 0u};
+    zl.r[1] = ZeroRange{sc.counter.ptr, 1, 0u};
+    zl.n = 2;
     for (int k = 0; k < n_extra; ++k) zl.r[zl.n++] = extra[k];
-    prezero_kernel<<<2 * 148, 256, 0, s>>>(zl);
+    return zl;
+}
+}  // namespace
+
+void launch_grid_prezero(int64_t L, PlsScratch &sc, const ZeroRange *extra, int n_extra, cudaStream_t s) {
+    reserve_pls_grid(L, sc, s);
+    prezero_kernel<<<2 * 148, 256, 0, s>>>(grid_zero_list(L, sc, extra, n_extra));
     LC_CHECK_LAUNCH();
 }
 
@@ -970,11 +996,8 @@ static void grid_prefix(const double *loop_box, int64_t L, int64_t n_excl, PlsSc
     int64_t *cnt = sc.keys.as<int64_t>(), *coff = sc.keys_sorted.as<int64_t>();
     int *row_count = sc.idx.as<int>(), *max_count = sc.counter.as<int>();
     sc.counts.reserve(sizeof(int64_t) * (L + 8 > 8 ? L + 8 : 8), s);
-    unsigned long long *acc = (unsigned long long *)sc.counts.ptr;   // 7 ordered keys, reused below
-    if (!prezeroed) {   // else done by the caller's init kernel (launch_grid_prezero)
-        LC_CUDA(cudaMemsetAsync(acc, 0xff, 3 * sizeof(unsigned long long), s));
-        LC_CUDA(cudaMemsetAsync(acc + 3, 0, 5 * sizeof(unsigned long long), s));   // + the block counter
-    }
+    reserve_pls_grid(L, sc, s);
+    unsigned long long *acc = sc.acc.as<unsigned long long>();   // 7 ordered keys + block counter, at the identity
     if (!grid_ready) {   // else loop_grid_kernel derived the grid parameters with the loop boxes
         grid_reduce_kernel<<<(unsigned)(ceil_div(L, 256) < 148 ? ceil_div(L, 256) : 148), 256, 0, s>>>(
             loop_box, L, acc, reinterpret_cast<unsigned *>(acc + 7), max_cells, gp);
@@ -1102,21 +1125,22 @@ int64_t run_pls(const double *loop_box, int64_t L, const uint64_t *h_excl, int64
 
 void launch_loop_grid(const double *coeffs, const double *t, const double *verts, const int64_t *loff, int64_t L,
                       unsigned long long *loop_min_diag2, double *loop_box, PlsScratch &sc, cudaStream_t s,
-                      bool pdl) {
+                      bool pdl, const ZeroRange *extra, int n_extra) {
     const int64_t max_cells = pls_grid_max_cells(L);
     sc.axis.reserve(sizeof(GridParams), s);
-    sc.counts.reserve(sizeof(int64_t) * (L + 8 > 8 ? L + 8 : 8), s);
-    unsigned long long *acc = (unsigned long long *)sc.counts.ptr;   // prezeroed keys + block counter
+    reserve_pls_grid(L, sc, s);
+    unsigned long long *acc = sc.acc.as<unsigned long long>();   // keys + block counter, at the identity
+    const ZeroList zl = grid_zero_list(L, sc, extra, n_extra);
     int64_t blocks = ceil_div(L, 4);
     if (blocks > 148 * 6) blocks = 148 * 6;
     if (verts)
         launch_pdl(loop_grid_kernel<true>, (unsigned)blocks, 128, s, pdl, (const double *)nullptr,
                    (const double *)nullptr, verts, loff, L, loop_min_diag2, loop_box, acc,
-                   reinterpret_cast<unsigned *>(acc + 7), max_cells, sc.axis.as<GridParams>());
+                   reinterpret_cast<unsigned *>(acc + 7), max_cells, sc.axis.as<GridParams>(), zl);
     else
         launch_pdl(loop_grid_kernel<false>, (unsigned)blocks, 128, s, pdl, coeffs, t, (const double *)nullptr, loff, L,
                    loop_min_diag2, loop_box, acc, reinterpret_cast<unsigned *>(acc + 7), max_cells,
-                   sc.axis.as<GridParams>());
+                   sc.axis.as<GridParams>(), zl);
 }
 
 void launch_pls_grid(const double *loop_box, int64_t L, int64_t n_excl, PlsScratch &sc, int32_t *pairs, int64_t cap,

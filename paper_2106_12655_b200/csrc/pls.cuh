@@ -43,7 +43,8 @@ void launch_seg_boxes(const double *coeffs, const double *t, const double *verts
 
 struct PlsScratch {
     DevBuf keys, keys_sorted, idx, perm, sbox, counter, cub_tmp, pair_keys, pair_keys_sorted, axis, excl, counts,
-        offs, lcell, lrank;
+        offs, lcell, lrank, acc;
+    const void *acc_ready = nullptr;   // the acc buffer whose keys were set to the identity
     int64_t cap = 0;
 };
 
@@ -75,11 +76,14 @@ void launch_pls_grid(const double *loop_box, int64_t L, int64_t n_excl, PlsScrat
                      cudaStream_t s, const int **d_max_row, bool prezeroed = false, bool grid_ready = false,
                      bool pdl = false);
 // Fused path: loop boxes + minimum squared diagonals with the grid reduction folded
-// in (launch_pls_grid(..., grid_ready = true) then skips its reduction); needs the
-// keys prezeroed (launch_grid_prezero) and loops of <= 1024 segments.
+// in (launch_pls_grid(..., grid_ready = true) then skips its reduction), loops of
+// <= 1024 segments.  As the run's first kernel it also writes launch_grid_prezero's
+// initial values (the grid PLS's and the caller's `extra` ranges; the reduction
+// keys stay at the identity between runs).
+struct ZeroRange;
 void launch_loop_grid(const double *coeffs, const double *t, const double *verts, const int64_t *loff, int64_t L,
                       unsigned long long *loop_min_diag2, double *loop_box, PlsScratch &sc, cudaStream_t s,
-                      bool pdl = false);
+                      bool pdl, const ZeroRange *extra, int n_extra);
 
 // Scratch sizes of launch_pls_grid, and one kernel doing the memsets it issues
 // (grid-reduce keys, cell counts, largest row count) plus `extra` int ranges —
