@@ -15,8 +15,13 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 from operator import attrgetter, itemgetter
+from struct import Struct
 
 import numpy as np
+
+# a closed from_polyline loop's vertex-array address and row count, packed (uint64,
+# int64) so a snapshot joins every loop's record into one buffer
+_pack_pn = Struct("<Qq").pack
 
 MACHINE_EPS = np.finfo(np.float64).eps          # geometry.py:14
 CONTINUITY_TOL = 1e-12                           # geometry.py:18
@@ -253,7 +258,7 @@ class LoopGeometry:
         self = cls.__new__(cls)
         d = self.__dict__
         d["_coeffs"], d["_t"], d["_closed"], d["_cp"] = coeffs, t, True, verts
-        d["_pv"] = (verts, ptr, verts.shape[0])
+        d["_pv"] = (verts, _pack_pn(ptr, verts.shape[0]))
         d["_stamp"] = 0
         return self
 
@@ -291,7 +296,7 @@ class LoopGeometry:
         coeffs[:, 0] = starts
         coeffs[:, 1] = ends - starts
         loop = LoopGeometry.__new__(LoopGeometry)
-        pv = (verts, verts.ctypes.data, len(verts)) if closed and len(verts) else None
+        pv = (verts, _pack_pn(verts.ctypes.data, len(verts))) if closed and len(verts) else None
         loop._setup(coeffs, None, closed, verts, None, pv)
         return loop
 
@@ -334,7 +339,7 @@ def compute_xi(loops):
     return total / count if count else 0.0
 
 
-_get_pv, _item0, _item1, _item2 = attrgetter("_pv"), itemgetter(0), itemgetter(1), itemgetter(2)
+_get_pv, _item1 = attrgetter("_pv"), itemgetter(1)
 
 
 class ModelSnapshot:
@@ -355,13 +360,20 @@ class ModelSnapshot:
         self.epoch = epoch
         self._packed = None
         L = len(self.key)
-        pv = list(map(_get_pv, self.key))          # C-level iteration: ~0.05 us per loop
-        self.poly = L > 0 and None not in pv
+        # two C-level passes over the loops: their (vertices, packed address + rows)
+        # and the packed records joined into one buffer (~0.07 us per loop)
+        pv = list(map(_get_pv, self.key))
+        try:
+            blob = b"".join(map(_item1, pv))       # TypeError: some loop is not a closed from_polyline loop
+            self.poly = L > 0
+        except TypeError:
+            self.poly = False
         self.off = np.zeros(L + 1, dtype=np.int64)
         if self.poly:
-            self.vrefs = list(map(_item0, pv))
-            self.vptrs = np.fromiter(map(_item1, pv), dtype=np.uint64, count=L)
-            np.cumsum(np.fromiter(map(_item2, pv), dtype=np.int64, count=L), out=self.off[1:])
+            pn = np.frombuffer(blob, dtype=np.uint64).reshape(L, 2)
+            self.vrefs = pv                        # keeps the vertex arrays alive while their addresses are used
+            self.vptrs = np.ascontiguousarray(pn[:, 0])
+            np.cumsum(pn[:, 1].view(np.int64), out=self.off[1:])
             self.closed = np.ones(L, dtype=np.uint8)
         else:
             self.vrefs = self.vptrs = None
@@ -396,7 +408,7 @@ class ModelSnapshot:
 
     def vertices(self):
         """Packed (M, 3) vertices of a poly snapshot (a host copy; tests / tools)."""
-        return np.concatenate(self.vrefs) if self.vrefs else np.zeros((0, 3))
+        return np.concatenate([p[0] for p in self.vrefs]) if self.vrefs else np.zeros((0, 3))
 
 
 @dataclass
