@@ -2,7 +2,7 @@
 
 usage: python tools/step_table.py launches.csv [first_kernel_regex]
 A step is the run of kernels from one occurrence of the first-kernel pattern
-(default: prezero_kernel, the fused graph's first node) to the next; the table
+(default: loop_grid_kernel, the fused graph's first kernel) to the next; the table
 shows the last step that ran the fused pair Gauss kernel (bench.py's timed
 steps), not the e2e verifies, the standalone kernel timing or the peak probes
 that follow them in the list.
@@ -13,7 +13,7 @@ import re
 import sys
 
 path = sys.argv[1]
-first = re.compile(sys.argv[2] if len(sys.argv) > 2 else "prezero_kernel")
+first = re.compile(sys.argv[2] if len(sys.argv) > 2 else "loop_grid_kernel|prezero_kernel")
 rows = list(csv.reader(open(path)))
 hdr, recs = None, []
 for r in rows:
