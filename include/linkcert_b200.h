@@ -267,6 +267,14 @@ LC_API int lc_model_digest(const double *coeffs, const double *t, const int64_t 
  * coefficient array is needed.  -1: non-finite coordinate, -2: null pointer. */
 LC_API int lc_model_digest_polylines(const double *const *loop_verts, const int64_t *loop_off, int64_t L,
                                      int nthreads, char *hex_out);
+/* lc_model_digest_polylines over input that is still being written: the caller
+ * fills loop_verts[l] and loop_off[l + 1] in loop order and publishes progress
+ * by storing the count of filled loops into *ready (release order; x86 stores),
+ * so hashing starts before the caller has walked every loop.  *ready < 0 aborts
+ * (-3: e.g. a loop turned out not to be a closed polyline); the caller must
+ * eventually store L or a negative value.  -1 non-finite, -2 null pointer. */
+LC_API int lc_model_digest_polylines_stream(const double *const *loop_verts, const int64_t *loop_off, int64_t L,
+                                            const int64_t *ready, int nthreads, char *hex_out);
 /* SHA-256 hex of a buffer (test hook; force_portable skips SHA-NI); returns 1 if SHA-NI exists. */
 LC_API int lc_sha256_hex(const void *data, int64_t n, int force_portable, char *hex_out);
 /* Page-locked host memory for model arrays (the per-call H2D copies of verify

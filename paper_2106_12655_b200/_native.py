@@ -65,6 +65,8 @@ SIGNATURES = {
     "lc_model_upload_polylines": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64]),
     "lc_model_upload_polyline_ptrs": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64]),
     "lc_model_digest_polylines": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p]),
+    "lc_model_digest_polylines_stream": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, ctypes.c_int,
+                                                        ctypes.c_char_p]),
     "lc_tight_boxes": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, _vp, _vp]),
     "lc_loop_boxes": (ctypes.c_int, [_vp, _vp, _vp]),
     "lc_potential_link_search": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _c_int64_p]),
@@ -144,6 +146,27 @@ def model_digest_polylines(vptrs, loop_off, nthreads=0):
     if rc == -2:
         raise NativeError(LC_ERR_ARG, "lc_model_digest_polylines: null loop pointer")
     return None if rc != 0 else out.value.decode()
+
+
+def model_digest_polylines_stream(vptrs, loop_off, ready, nthreads=0):
+    """model_digest_polylines while vptrs (uint64 (L)) / loop_off (int64 (L+1)) are
+    being filled in loop order; ready (int64 (1)) holds the count of filled loops
+    (negative: abort).  Returns the digest, None for a non-finite coordinate, or
+    raises Aborted."""
+    lib = load_library()
+    assert vptrs.dtype == np.uint64 and loop_off.dtype == np.int64 and ready.dtype == np.int64
+    out = ctypes.create_string_buffer(65)
+    rc = lib.lc_model_digest_polylines_stream(_ptr(vptrs), _ptr(loop_off), len(loop_off) - 1, _ptr(ready),
+                                              int(nthreads), out)
+    if rc == -2:
+        raise NativeError(LC_ERR_ARG, "lc_model_digest_polylines_stream: null loop pointer")
+    if rc == -3:
+        raise DigestAborted()
+    return None if rc != 0 else out.value.decode()
+
+
+class DigestAborted(Exception):
+    """A streamed digest whose input was withdrawn (the model is not all closed polylines)."""
 
 
 def comm_unique_id():

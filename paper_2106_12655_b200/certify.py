@@ -210,6 +210,38 @@ def ensure_comm(ctx, dist):
     ctx.comm_init(obj[0], world, rank)
 
 
+def snapshot_and_digest(model, dist):
+    """(model.snapshot(), digest_on_rank0's callable).  Single process, fresh
+    snapshot of closed polylines: the digest starts on its helper thread after
+    the snapshot's first piece of loops (a streamed digest), so the ~1 ms walk
+    over the loops overlaps the hash instead of preceding it."""
+    if dist is not None:
+        snap = model.snapshot()
+        return snap, digest_on_rank0(model, snap, dist)
+    started = []
+
+    def start(sn):
+        started.append(_digest_pool_submit(_native.model_digest_polylines_stream, sn.vptrs, sn.off, sn.ready))
+
+    snap = model.snapshot(on_start=start)
+    if not started:
+        return snap, digest_on_rank0(model, snap, None)
+    fut = started[0]
+    if not snap.poly:   # the stream was aborted (a loop is not a closed polyline): the regular digest
+        fut = _digest_async(model, snap)
+
+    def result():
+        try:
+            digest = fut.result()
+        except _native.DigestAborted:   # (not reached: an aborted stream is replaced above)
+            digest = model_digest(model, snap)
+        if digest is None:
+            raise ValidationError("cannot serialize non-finite coordinate")
+        return digest
+
+    return snap, result
+
+
 def digest_on_rank0(model, snapshot, dist):
     """model_digest computed once per job: rank 0 hashes (helper thread, overlapped
     with the GPU), the other ranks receive the string.  Returns a callable giving
@@ -286,14 +318,18 @@ def run_device_pipeline(model: CurveModel, excluded=(), params=None, timings=Non
 _digest_pool = None
 
 
-def _digest_async(model, snapshot=None, nthreads=0):
-    """model_digest on a helper thread (native, GIL released) to overlap it with the GPU."""
+def _digest_pool_submit(fn, *args):
     global _digest_pool
     if _digest_pool is None:
         from concurrent.futures import ThreadPoolExecutor
 
         _digest_pool = ThreadPoolExecutor(max_workers=1, thread_name_prefix="linkcert-digest")
-    return _digest_pool.submit(model_digest, model, snapshot, nthreads)
+    return _digest_pool.submit(fn, *args)
+
+
+def _digest_async(model, snapshot=None, nthreads=0):
+    """model_digest on a helper thread (native, GIL released) to overlap it with the GPU."""
+    return _digest_pool_submit(model_digest, model, snapshot, nthreads)
 
 
 def _raise_for_flags(raw, flags, order=None):
@@ -396,8 +432,7 @@ def compute_linking_matrix(
             timings.update(pls=0.0, discretize=0.0, kernel=0.0)
         digest = model_digest(model)
     else:
-        snap = model.snapshot()
-        digest_of = digest_on_rank0(model, snap, _dist())
+        snap, digest_of = snapshot_and_digest(model, _dist())
         ctx = _native.context()
         try:
             with ctx.session:   # the result views stay ours until copied into arr
@@ -441,8 +476,7 @@ def verify(
         return diff_arrays(reference.array, pairs, raw, lk, flags, early_exit)
     # the digest (host, native) overlaps the device pipeline; its check and
     # warning come first, as in the reference (certify.py:188-193)
-    snap = model.snapshot()
-    digest_of = digest_on_rank0(model, snap, _dist())
+    snap, digest_of = snapshot_and_digest(model, _dist())
     ctx = None
     try:
         if model.num_loops < 1:

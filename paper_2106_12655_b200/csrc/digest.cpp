@@ -448,6 +448,10 @@ struct Job {
     const int64_t *off;
     const uint8_t *closed;
     const double *const *vptr = nullptr;  // per-loop vertex rows of closed polylines (coeffs/t unused)
+    // streamed input (lc_model_digest_polylines_stream): loops [0, *ready) of vptr / off
+    // are filled; a negative value aborts the digest
+    const volatile int64_t *ready = nullptr;
+    std::atomic<bool> aborted{false}, null_loop{false};
     std::vector<Chunk> chunks;
     std::atomic<int64_t> next{0};
     bool check_finite = false;           // digest: validate the chunk's coefficients in the worker
@@ -484,7 +488,32 @@ struct Job {
         cv.notify_all();
     }
 
+    // streamed input: wait until the chunk's loops are filled (or the caller aborts)
+    bool wait_input(const Chunk &c) {
+        if (!ready) return true;
+        for (int spins = 0;; ++spins) {   // the caller publishes a piece every ~0.1 ms: poll, then sleep
+            const int64_t r = *ready;
+            if (r < 0) return false;
+            if (r >= c.l1) break;
+            if (spins > 16) std::this_thread::sleep_for(std::chrono::microseconds(20));
+        }
+        std::atomic_thread_fence(std::memory_order_acquire);
+        for (int64_t l = c.l0; l < c.l1; ++l)
+            if (off[l + 1] > off[l] && !vptr[l]) return null_loop.store(true), false;
+        return true;
+    }
+
     void format_vertices(Chunk &c) {
+        if (!wait_input(c)) {   // nothing to format: the hasher stops at this chunk
+            aborted.store(true);
+            c.size = 0;
+            {
+                std::lock_guard<std::mutex> g(mu);
+                c.ready.store(true, std::memory_order_release);
+            }
+            cv.notify_all();
+            return;
+        }
         size_t bound = 1;
         for (int64_t l = c.l0; l < c.l1; ++l) bound += loop_bound(off[l + 1] - off[l], true) + 1;
         bool fin = true;
@@ -540,6 +569,22 @@ void make_chunks(Job &job, int64_t L, int64_t M, int64_t target) {
     (void)M;
 }
 
+// Streamed input: chunk boundaries by loop count (the offsets are not known yet).
+void make_chunks_by_loops(Job &job, int64_t L, int64_t per_chunk) {
+    std::vector<std::pair<int64_t, int64_t>> r;
+    for (int64_t l = 0; l < L;) {
+        const int64_t want = r.size() < 4 ? (per_chunk / 8 > 0 ? per_chunk / 8 : 1) : per_chunk;
+        const int64_t e = l + want < L ? l + want : L;
+        r.emplace_back(l, e);
+        l = e;
+    }
+    job.chunks = std::vector<Chunk>(r.size());
+    for (size_t k = 0; k < r.size(); ++k) {
+        job.chunks[k].l0 = r[k].first;
+        job.chunks[k].l1 = r[k].second;
+    }
+}
+
 int resolve_threads(int nthreads) {
     if (nthreads <= 0) nthreads = (int)std::thread::hardware_concurrency();
     if (nthreads < 1) nthreads = 1;
@@ -590,10 +635,13 @@ static int digest_job(Job &job, int64_t L, int nthreads, char *hex_out) {
         return std::chrono::duration<double, std::milli>(b - a).count();
     };
     const auto t_begin = clk::now();
-    const int64_t M = L > 0 ? job.off[L] : 0;
+    const int64_t M = L > 0 && !job.ready ? job.off[L] : 0;   // streamed: off is being filled
     job.check_finite = true;
     std::lock_guard<std::mutex> pool_lock(g_pool_mu);
-    make_chunks(job, L, M, 4096);
+    if (job.ready)
+        make_chunks_by_loops(job, L, 64);   // ~4096 segments for chainmail-sized loops
+    else
+        make_chunks(job, L, M, 4096);
     pool_reserve(job.chunks.size());
     const int nt = resolve_threads(nthreads);
     std::vector<std::thread> th;
@@ -618,6 +666,7 @@ static int digest_job(Job &job, int64_t L, int nthreads, char *hex_out) {
             job.wait(c);
             h.update(c.data, c.size);
         }
+        if (job.aborted.load()) break;
     }
     h.update("]}", 2);
     const auto t_hashed = clk::now();
@@ -628,6 +677,8 @@ static int digest_job(Job &job, int64_t L, int nthreads, char *hex_out) {
                      "lc_model_digest: threads %d chunks %zu setup %.2f wait %.2f hash %.2f join %.2f total %.2f ms\n",
                      nt, job.chunks.size(), ms(t_begin, t_spawned), t_wait, t_hash, ms(t_hashed, t_joined),
                      ms(t_begin, t_joined));
+    if (job.null_loop.load()) return -2;
+    if (job.aborted.load()) return -3;
     if (job.nonfinite.load()) return -1;
     h.hex(hex_out);
     return 0;
@@ -645,6 +696,15 @@ LC_API int lc_model_digest_polylines(const double *const *loop_verts, const int6
         if (loop_off[l + 1] > loop_off[l] && !loop_verts[l]) return -2;
     Job job{nullptr, nullptr, loop_off, nullptr};
     job.vptr = loop_verts;
+    return digest_job(job, L, nthreads, hex_out);
+}
+
+LC_API int lc_model_digest_polylines_stream(const double *const *loop_verts, const int64_t *loop_off, int64_t L,
+                                            const int64_t *ready, int nthreads, char *hex_out) {
+    if (!ready || (L > 0 && (!loop_verts || !loop_off))) return -2;
+    Job job{nullptr, nullptr, loop_off, nullptr};
+    job.vptr = loop_verts;
+    job.ready = ready;
     return digest_job(job, L, nthreads, hex_out);
 }
 

@@ -340,6 +340,7 @@ def compute_xi(loops):
 
 
 _get_pv, _item1 = attrgetter("_pv"), itemgetter(1)
+_PIECE = 1024   # loops per piece of a streamed snapshot
 
 
 class ModelSnapshot:
@@ -353,13 +354,16 @@ class ModelSnapshot:
     in page-locked memory.
     """
 
-    __slots__ = ("key", "epoch", "poly", "off", "closed", "vptrs", "vrefs", "_packed")
+    __slots__ = ("key", "epoch", "poly", "off", "closed", "vptrs", "vrefs", "ready", "_packed")
 
-    def __init__(self, loops, epoch):
+    def __init__(self, loops, epoch, on_start=None):
         self.key = tuple(loops)
         self.epoch = epoch
         self._packed = None
+        self.ready = None
         L = len(self.key)
+        if on_start is not None and L > 2 * _PIECE and self._stream(on_start):
+            return
         # two C-level passes over the loops: their (vertices, packed address + rows)
         # and the packed records joined into one buffer (~0.07 us per loop)
         pv = list(map(_get_pv, self.key))
@@ -380,6 +384,42 @@ class ModelSnapshot:
             if L:
                 np.cumsum(np.fromiter((len(lp) for lp in self.key), dtype=np.int64, count=L), out=self.off[1:])
             self.closed = np.fromiter((lp.closed for lp in self.key), dtype=np.uint8, count=L)
+
+    def _stream(self, on_start):
+        """A poly snapshot built piece by piece: after the first piece `on_start(self)`
+        may hand vptrs / off / ready to a streamed digest, which formats and hashes
+        loops [0, ready[0]) while the rest are walked.  False (and ready[0] = -1,
+        aborting a started stream) when some loop is not a closed from_polyline loop."""
+        key, L = self.key, len(self.key)
+        self.vptrs = np.zeros(L, dtype=np.uint64)
+        self.off = np.zeros(L + 1, dtype=np.int64)
+        self.ready = np.zeros(1, dtype=np.int64)
+        self.vrefs = []
+        started = False
+        try:
+            for a in range(0, L, _PIECE):
+                pv = list(map(_get_pv, key[a:a + _PIECE]))
+                try:
+                    blob = b"".join(map(_item1, pv))
+                except TypeError:
+                    return False
+                n = len(pv)
+                pn = np.frombuffer(blob, dtype=np.uint64).reshape(n, 2)
+                self.vptrs[a:a + n] = pn[:, 0]
+                part = self.off[a + 1:a + n + 1]
+                np.cumsum(pn[:, 1].view(np.int64), out=part)
+                part += self.off[a]
+                self.vrefs.extend(pv)
+                self.ready[0] = a + n         # published after the loops' entries (x86 store order)
+                if not started:
+                    on_start(self)
+                    started = True
+            self.poly = True
+            self.closed = np.ones(L, dtype=np.uint8)
+            return True
+        finally:
+            if self.ready[0] != L:
+                self.ready[0] = -1
 
     def valid_for(self, loops, epoch):
         if self.key != tuple(loops):          # identity per element (LoopGeometry has no __eq__)
@@ -429,15 +469,17 @@ class CurveModel:
         return len(self.loops)
 
     # ---- B200 snapshot of the loops -------------------------------------------
-    def snapshot(self) -> ModelSnapshot:
+    def snapshot(self, on_start=None) -> ModelSnapshot:
         """The loops as the device upload and the digest consume them.  Cached
         while the loop list holds the same objects and none of them had an
-        attribute reassigned (their arrays are read-only); O(L) to check."""
+        attribute reassigned (their arrays are read-only); O(L) to check.
+        on_start: see ModelSnapshot._stream (called only when a new snapshot of
+        closed polylines is built)."""
         epoch = _EPOCH[0]
         snap = self.__dict__.get("_snapshot")
         if snap is not None and snap.valid_for(self.loops, epoch):
             return snap
-        snap = ModelSnapshot(self.loops, epoch)
+        snap = ModelSnapshot(self.loops, epoch, on_start)
         self.__dict__["_snapshot"] = snap
         return snap
 

@@ -277,6 +277,34 @@ def test_digest_cubics_and_open_loops():
     assert lc.model_digest(m2) == model_digest_python(m2)
 
 
+def test_streamed_snapshot_digest():
+    """verify / compute_linking_matrix start the digest after the snapshot's first
+    piece of loops (lc_model_digest_polylines_stream): the same digest as the
+    finished snapshot's, the same snapshot arrays; a loop that is not a closed
+    polyline past the first piece aborts the stream and the regular digest runs."""
+    from paper_2106_12655_b200 import certify, workloads
+    from paper_2106_12655_b200.geometry import ModelSnapshot
+
+    v, off = workloads.kusari_tube_vertices(rows=40, n_around=60)
+    loops = [lc.LoopGeometry.from_polyline(v[off[k]:off[k + 1]]) for k in range(len(off) - 1)]
+    assert len(loops) > 2 * 1024
+    m = lc.CurveModel(list(loops))
+    want = model_digest_python(m)
+    snap, digest_of = certify.snapshot_and_digest(m, None)
+    assert snap.ready is not None and snap.ready[0] == len(loops)        # it was streamed
+    assert digest_of() == want == lc.model_digest(lc.CurveModel(list(loops)))
+    plain = ModelSnapshot(loops, 0)
+    assert np.array_equal(snap.off, plain.off) and np.array_equal(snap.vptrs, plain.vptrs)
+    assert np.array_equal(snap.vertices(), v)
+    spline = lc.LoopGeometry.from_catmull_rom(v[off[3]:off[4]])
+    mixed = lc.CurveModel(loops[:1500] + [spline] + loops[1500:2500])
+    snap, digest_of = certify.snapshot_and_digest(mixed, None)
+    assert not snap.poly and snap.ready[0] == -1                          # aborted after the first piece
+    assert digest_of() == model_digest_python(mixed)
+    snap, digest_of = certify.snapshot_and_digest(mixed, None)            # cached snapshot: regular digest
+    assert digest_of() == model_digest_python(mixed)
+
+
 # ------------------------------------------------------------- sharding
 
 def _gloo_comm_worker(rank, world, port, q):
