@@ -440,21 +440,23 @@ __global__ void sweep_warp_kernel(const double *__restrict__ sbox, const int32_t
 
 struct GridParams {
     double o[3];
-    double c;
+    double c, ic;   // cell size (>= the largest loop extent) and 1 / c
     int dims[3];
     int pad;
 };
 
-__device__ __forceinline__ int cell_coord(double x, double o, double c, int dim) {
-    const double f = floor((x - o) / c);
+// (x - o) * (1/c): any monotone map of x works (the query's two-cell margin absorbs
+// the rounding) and a multiply replaces an FP64 division per coordinate
+__device__ __forceinline__ int cell_coord(double x, double o, double ic, int dim) {
+    const double f = floor((x - o) * ic);
     return f < 0.0 ? 0 : (f >= (double)dim ? dim - 1 : (int)f);
 }
 
 __device__ __forceinline__ int64_t owner_cell(const double *__restrict__ lbox, int64_t L, int64_t l,
                                               const GridParams &g) {
-    const int cx = cell_coord(lbox[l], g.o[0], g.c, g.dims[0]);
-    const int cy = cell_coord(lbox[L + l], g.o[1], g.c, g.dims[1]);
-    const int cz = cell_coord(lbox[2 * L + l], g.o[2], g.c, g.dims[2]);
+    const int cx = cell_coord(lbox[l], g.o[0], g.ic, g.dims[0]);
+    const int cy = cell_coord(lbox[L + l], g.o[1], g.ic, g.dims[1]);
+    const int cz = cell_coord(lbox[2 * L + l], g.o[2], g.ic, g.dims[2]);
     return ((int64_t)cz * g.dims[1] + cy) * g.dims[0] + cx;
 }
 
@@ -511,8 +513,8 @@ __global__ void grid_query_warp_kernel(const double *__restrict__ lbox, int64_t 
     for (int d = 0; d < 3; ++d) {
         al[d] = lbox[d * L + a];
         ah[d] = lbox[(3 + d) * L + a];
-        c0[d] = max(cell_coord(al[d], g.o[d], g.c, g.dims[d]) - 2, 0);
-        c1[d] = cell_coord(ah[d], g.o[d], g.c, g.dims[d]);
+        c0[d] = max(cell_coord(al[d], g.o[d], g.ic, g.dims[d]) - 2, 0);
+        c1[d] = cell_coord(ah[d], g.o[d], g.ic, g.dims[d]);
     }
     const int ny = c1[1] - c0[1] + 1, nrows_all = ny * (c1[2] - c0[2] + 1);   // <= 25 (cells >= any extent)
     int n = 0;
@@ -616,6 +618,7 @@ __device__ void grid_finalize(const unsigned long long *acc, int64_t max_cells, 
         c *= 1.25;
     }
     gp->c = c;
+    gp->ic = 1.0 / c;
     for (int d = 0; d < 3; ++d) gp->dims[d] = (int)(floor(span[d] / c) + 1.0);
 }
 
