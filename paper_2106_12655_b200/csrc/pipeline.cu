@@ -210,8 +210,9 @@ void Pipeline::release() {
     for (DevBuf *b : bufs) b->release(s);
     DevBuf *pb[] = {&pls_sc.keys, &pls_sc.keys_sorted, &pls_sc.idx, &pls_sc.perm, &pls_sc.sbox, &pls_sc.counter,
                     &pls_sc.cub_tmp, &pls_sc.pair_keys, &pls_sc.pair_keys_sorted, &pls_sc.axis, &pls_sc.excl,
-                    &pls_sc.counts, &pls_sc.offs, &pls_sc.lcell, &pls_sc.lrank};
+                    &pls_sc.counts, &pls_sc.offs, &pls_sc.lcell, &pls_sc.lrank, &pls_sc.acc};
     for (DevBuf *b : pb) b->release(s);
+    pls_sc.acc_ready = nullptr;   // a new acc buffer gets its identity keys again
     DiscScratch &d = disc_sc;
     DevBuf *db[] = {&d.paired, &d.act_seg, &d.act_loop, &d.act_tlo, &d.act_thi, &d.act_off, &d.nxt_seg,
                     &d.nxt_loop, &d.nxt_tlo, &d.nxt_thi, &d.nxt_off, &d.nxt_partner, &d.box, &d.nxt_box,
