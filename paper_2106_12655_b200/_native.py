@@ -654,23 +654,26 @@ class Context:
     def result_views(self):
         """(pairs (P,2) int32, raw, lk, flags) views into the library's pinned result
         buffer — valid until the next pipeline call; copy what must be kept."""
-        ptrs = [_vp() for _ in range(4)]
-        n = ctypes.c_int64(0)
-        with self.lock:
-            _check(self.lib.lc_result_views(self.handle, *[ctypes.byref(p) for p in ptrs], ctypes.byref(n)))
-        P = n.value
+        with self.lock:   # the output slots are per context, filled and read under its lock
+            out = self.__dict__.get("_rv_out")
+            if out is None:
+                ptrs, n = [_vp() for _ in range(4)], ctypes.c_int64(0)
+                out = self._rv_out = (ptrs, n, [ctypes.byref(p) for p in ptrs] + [ctypes.byref(n)])
+            ptrs, n, refs = out
+            _check(self.lib.lc_result_views(self.handle, *refs))
+            P = n.value
+            key = (P, ptrs[0].value, ptrs[1].value, ptrs[2].value, ptrs[3].value)
         if P == 0:
             return (np.zeros((0, 2), np.int32), np.zeros(0), np.zeros(0, np.int64), np.zeros(0, np.uint8))
-        key = (P, *(p.value for p in ptrs))
         cached = getattr(self, "_views", None)
         if cached is not None and cached[0] == key:   # same buffer, same P: the same views
             return cached[1]
 
-        def view(p, ctype, shape):
-            return np.ctypeslib.as_array(ctypes.cast(p, ctypes.POINTER(ctype)), shape=shape)
+        def view(addr, ctype, shape):
+            return np.ctypeslib.as_array(ctypes.cast(_vp(addr), ctypes.POINTER(ctype)), shape=shape)
 
-        views = (view(ptrs[0], ctypes.c_int32, (P, 2)), view(ptrs[1], ctypes.c_double, (P,)),
-                 view(ptrs[2], ctypes.c_int64, (P,)), view(ptrs[3], ctypes.c_uint8, (P,)))
+        views = (view(key[1], ctypes.c_int32, (P, 2)), view(key[2], ctypes.c_double, (P,)),
+                 view(key[3], ctypes.c_int64, (P,)), view(key[4], ctypes.c_uint8, (P,)))
         self._views = (key, views)
         return views
 
