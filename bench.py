@@ -335,6 +335,15 @@ def main():
                 n_sp = seg_pairs(pairs, voff)
                 n_closed = int(voff[-1]) + len(voff) - 1     # closed SoA vertices read by the kernel
     clocks = clk.result
+    # stage breakdown (diagnostic, after the timed region): a few more steps with every
+    # stage event recorded (the timed steps record only the Gauss stage's two events)
+    detail = []
+    for k in range(6):
+        flush.zero_()
+        torch.cuda.synchronize()
+        device_step(ctx, after.xi, ex, params, timings={})   # (a timings request turns stage detail on)
+        if k >= 2:
+            detail.append(ctx.stage_times())
     ms = statistics.mean(step_ms)
     if world > 1:
         tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -434,8 +443,11 @@ def main():
                      "peak_probes_tflops": {"dfma": peak_dfma / 1e12, "dmma": peak_dmma / 1e12},
                      "peak_source": "max(FP64 DFMA-chain, FP64 tensor-core MMA) probes measured live on this GPU "
                                     "(MEASURED_PEAKS.json has no FP64 entry)"},
-        # the library's stage events of the timed steps (median per stage)
-        "stage_ms": {k: round(statistics.median(x[k] for x in stages), 4) for k in stages[0]},
+        # the library's stage events (median per stage) of 4 steps run after the timed
+        # region with every stage event on; the timed steps time the Gauss stage only
+        "stage_ms": {k: (round(statistics.median(x[k] for x in detail), 4) if detail[0][k] is not None else None)
+                     for k in detail[0]},
+        "stage_ms_gauss_timed": round(statistics.median(x["gauss"] for x in stages), 4),
         "clocks": clocks,
         "gpu_launches": int(sum(launches)),
     }

@@ -244,8 +244,13 @@ LC_API int lc_early_exit_stats(lc_ctx *ctx, int64_t *first_fail_place, int64_t *
  * the captured CUDA graph (same shape as the previous run, no reallocation). */
 LC_API int lc_last_run_fused(lc_ctx *ctx);
 /* Device times (ms) of the last pipeline: [derive + PLS, discretize, Gauss kernel, reduce,
- * first stage start -> reduce end] (ms must hold 5 floats). */
+ * first stage start -> reduce end] (ms must hold 5 floats); -1 for the stages a
+ * fused run without stage detail did not time (it records only the Gauss stage). */
 LC_API int lc_stage_times(lc_ctx *ctx, float *ms);
+/* Fused runs record every stage event (on) or only the Gauss stage's (off, the
+ * default: each event-record node adds ~0.8 us to the graph launch).  The env
+ * LINKCERT_STAGE_TIMES=1 forces detail on. */
+LC_API int lc_set_stage_detail(lc_ctx *ctx, int on);
 
 /* ---- Canonical model serialization (host, multithreaded) ----
  * Bytes of json.dumps(model_to_dict(model), sort_keys=True,

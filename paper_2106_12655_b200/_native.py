@@ -85,6 +85,7 @@ SIGNATURES = {
     "lc_result_views": (ctypes.c_int, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp),
                                         ctypes.POINTER(_vp), _c_int64_p]),
     "lc_stage_times": (ctypes.c_int, [_vp, _c_float_p]),
+    "lc_set_stage_detail": (ctypes.c_int, [_vp, ctypes.c_int]),
     "lc_model_json_bound": (ctypes.c_int64, [_vp, ctypes.c_int64]),
     "lc_model_json": (ctypes.c_int64, [_vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, ctypes.c_int64]),
     "lc_float_repr": (ctypes.c_int, [ctypes.c_double, ctypes.c_char_p]),
@@ -678,10 +679,21 @@ class Context:
         return views
 
     def stage_times(self):
+        """Device ms of the last pipeline's stages; None for a stage the last fused run
+        did not time (stage detail off: only the Gauss stage)."""
         ms = (ctypes.c_float * 5)()
         with self.lock:
             _check(self.lib.lc_stage_times(self.handle, ms))
-        return {"pls": ms[0], "discretize": ms[1], "gauss": ms[2], "reduce": ms[3], "begin_to_reduce": ms[4]}
+        names = ("pls", "discretize", "gauss", "reduce", "begin_to_reduce")
+        return {k: (v if v >= 0.0 else None) for k, v in zip(names, ms)}
+
+    def set_stage_detail(self, on):
+        """Fused runs time every stage (on) or only the Gauss stage (off, the default)."""
+        on = bool(on)
+        if getattr(self, "_stage_detail", False) != on:
+            with self.lock:
+                _check(self.lib.lc_set_stage_detail(self.handle, int(on)))
+            self._stage_detail = on
 
     def bh_forest(self, verts, loop_off):
         """Moment trees of closed polylines on this device (Barnes-Hut)."""

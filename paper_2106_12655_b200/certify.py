@@ -281,6 +281,7 @@ def device_step(ctx, xi, excl_keys, params, mode=None, timings=None):
     args = (excl_keys, xi, params.epsilon, params.max_passes, params.max_subsegments, mode)
     if dist is not None and dist.get_backend() != "nccl":
         raise _native.NativeUnavailable("the multi-GPU path needs the NCCL backend on CUDA devices")
+    ctx.set_stage_detail(timings is not None)   # every stage event only when the caller wants the stages
     try:
         if dist is None:
             ctx.run_pipeline(*args)          # one C-ABI call for the whole device path

@@ -632,12 +632,18 @@ int lc_get_results(lc_ctx *ctx, double *raw, int64_t *lk, uint8_t *flags) {
 int lc_stage_times(lc_ctx *ctx, float *ms) {
     return guarded(ctx, [&] {
         Pipeline &p = ctx->pipe;
-        ms[0] = p.stage_ms(EV_BEGIN, EV_PLS);
-        ms[1] = p.stage_ms(EV_PLS, EV_DISC);
+        // a fused run without stage detail records only the Gauss-stage events
+        const bool all = ctx->last_fused == 0 || p.last_detail;
+        ms[0] = all ? p.stage_ms(EV_BEGIN, EV_PLS) : -1.f;
+        ms[1] = all ? p.stage_ms(EV_PLS, EV_DISC) : -1.f;
         ms[2] = p.stage_ms(EV_GAUSS0, EV_GAUSS1);
-        ms[3] = p.stage_ms(EV_GAUSS1, EV_END);
-        ms[4] = p.stage_ms(EV_BEGIN, EV_END);
+        ms[3] = all ? p.stage_ms(EV_GAUSS1, EV_END) : -1.f;
+        ms[4] = all ? p.stage_ms(EV_BEGIN, EV_END) : -1.f;
     });
+}
+
+int lc_set_stage_detail(lc_ctx *ctx, int on) {
+    return guarded(ctx, [&] { ctx->pipe.stage_detail = on != 0; });
 }
 
 void *lc_host_alloc(int64_t bytes) {

@@ -693,6 +693,11 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
     // buffers are sized, no host-pageable copies, no host syncs).
     const bool split = seg_boxes_split_ok(L, max_loop);
     if (split) reserve_derived();
+    static const bool env_detail = [] {
+        const char *e = getenv("LINKCERT_STAGE_TIMES");
+        return e && e[0] == '1';
+    }();
+    const bool detail = stage_detail || env_detail;
     auto enqueue = [&]() {
         // the whole sequence runs on the high-priority critical stream, joined to the
         // caller's stream at both ends (captured with it into the graph)
@@ -706,7 +711,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
         } restore{s, caller};
         tl_reset();
         if (split) {   // the loop half of derive on the critical path, the segment half on the chord branch
-            record(EV_BEGIN);
+            if (detail) record(EV_BEGIN);
             derived = true;
             derived_in_run = true;
         } else {
@@ -775,7 +780,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
                         d_pg.as<PairGeom>(), d_item_off.as<int64_t>(), d_tot.as<int64_t>(), icap, s, &dmx,
                         /*prezeroed=*/true, /*grid_ready=*/split, kChainPdl && !timeline().on);
         const int64_t *dP = d_tot.as<int64_t>(), *d_items = d_tot.as<int64_t>() + 1;
-        record(EV_PLS);
+        if (detail) record(EV_PLS);
         // branch 2: pass-1 detection + validation only feed the status — they run
         // beside the work items and the Gauss sum
         LC_CUDA(cudaEventRecord(ev_pairs, s));
@@ -786,7 +791,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
         // step, or starved on this branch behind the persistent sum, 0.47 ms)
         launch_discretize_checks(in, dP, prm, disc_sc, dout, side[1], ev_chords, &ctr, kBrutePdl);
         tl_mark("S1:checks", side[1]);
-        record(EV_DISC, side[1]);
+        if (detail) record(EV_DISC, side[1]);
         // the pair list is final: the copy engine moves the whole capacity to pinned
         // memory while the sums run (no SM time; the host reads the first P)
         LC_CUDA(cudaMemcpyAsync(hp, d_pairs.ptr, sizeof(int32_t) * 2 * pcap, cudaMemcpyDeviceToHost, side[1]));
@@ -830,7 +835,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
                                                nullptr, st, nullptr, nullptr, nullptr, nullptr,
                                                ee ? d_ee.as<unsigned long long>() : nullptr);
         LC_CHECK_LAUNCH();
-        record(EV_END);   // "reduce" = Gauss end -> status in pinned memory
+        if (detail) record(EV_END);   // "reduce" = Gauss end -> status in pinned memory
         tl_mark("export", s);
         LC_CUDA(cudaEventRecord(ev_leave, crit));
         LC_CUDA(cudaStreamWaitEvent(caller, ev_leave, 0));
@@ -841,7 +846,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
         return e && e[0] == '1';
     }();
     FastKey key{L, M, pcap, icap, n_excl, mode, model_poly ? 1 : 0, shard, sharded ? shards : 0, prm.epsilon * prm.xi,
-                2.220446049250313e-16 * prm.xi, alloc_generation().load(), ee ? n_ref : -1};
+                2.220446049250313e-16 * prm.xi, alloc_generation().load(), ee ? n_ref : -1, detail};
     last_fast_graph = false;
     if (!no_graph && graph_exec && key == graph_key) {
         static const bool ginfo = [] {
@@ -921,6 +926,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
     } else {
         enqueue();
     }
+    last_detail = detail;
     pend.on = true;
     pend.key = key;
     pend.pcap = pcap;

@@ -107,6 +107,10 @@ struct Pipeline {
     DevBuf d_ref_keys, d_ref_lk, d_posv, d_want, d_ee;
     int64_t n_ref = 0;
     bool ee_on = false;
+    // fused runs record only the Gauss-stage events unless stage_detail (or the env
+    // LINKCERT_STAGE_TIMES=1): an external event-record node costs ~0.8 us of graph
+    // launch; last_detail = the last run recorded every stage event
+    bool stage_detail = false, last_detail = true;
     int64_t ee_first_fail = -1, ee_n_eval = -1;   // last fused run (-1: not an early-exit run)
     void set_early_exit(const uint64_t *keys, const int64_t *lk, int64_t n, bool enable);
     bool items_seq = false;   // the current items are whole-row (sequential-mode) items
@@ -154,10 +158,12 @@ struct Pipeline {
         double min_diam, poly_thr;
         unsigned long long gen;
         int64_t n_ref;   // early-exit certificate size (-1: off)
+        bool detail;     // every stage event recorded
         bool operator==(const FastKey &o) const {
             return L == o.L && M == o.M && pcap == o.pcap && icap == o.icap && n_excl == o.n_excl &&
                    mode == o.mode && model_poly == o.model_poly && shard == o.shard && shards == o.shards &&
-                   min_diam == o.min_diam && poly_thr == o.poly_thr && gen == o.gen && n_ref == o.n_ref;
+                   min_diam == o.min_diam && poly_thr == o.poly_thr && gen == o.gen && n_ref == o.n_ref &&
+                   detail == o.detail;
         }
     };
     FastKey fast_seen{}, graph_key{};

@@ -340,10 +340,18 @@ def test_fused_graph_replay_bitwise(monkeypatch):
             run_device_pipeline(lc.generators.kusari_tube(n_around=16, rows=6, partial=3))
         *got, ctx = run_device_pipeline(m)
         paths.append(ctx.last_run_fused())
-        assert all(v >= 0.0 for v in ctx.stage_times().values())   # events recorded inside the graph
+        st = ctx.stage_times()   # without stage detail the graph records only the Gauss-stage events
+        assert st["gauss"] > 0.0 and all(v is None for k, v in st.items() if k != "gauss")
         for a, b in zip(want, got):
             assert np.array_equal(a, np.asarray(b)) and np.asarray(b).dtype == a.dtype
     assert paths[0] >= 1 and 2 in paths, paths
+    for rep in range(3):   # with detail (a caller asking for timings): every stage, replayed graphs too
+        tm = {}
+        *got, ctx = run_device_pipeline(m, timings=tm)
+        assert all(v is not None and v >= 0.0 for v in ctx.stage_times().values())
+        assert tm["kernel"] > 0.0 and tm["pls"] > 0.0
+        for a, b in zip(want, got):
+            assert np.array_equal(a, np.asarray(b))
 
 
 def test_fused_pair_capacity_growth(monkeypatch, cert_models):

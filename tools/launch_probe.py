@@ -4,6 +4,7 @@ host time of the C-ABI call, and the event-timed step with the GPU idle at launc
     python tools/launch_probe.py
 """
 import os
+os.environ.setdefault("LINKCERT_STAGE_TIMES", "1")   # every stage timed (diagnostic)
 import statistics
 import sys
 import time

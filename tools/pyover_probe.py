@@ -1,4 +1,5 @@
 import sys, time, statistics, os
+os.environ.setdefault("LINKCERT_STAGE_TIMES", "1")   # every stage timed (diagnostic)
 sys.path.insert(0, os.getcwd())
 import torch
 from paper_2106_12655_b200 import _native, generators as gen

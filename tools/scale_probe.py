@@ -1,6 +1,7 @@
 """Larger-than-benchmark models through the fused path (GPU box): correctness vs the
 oracle on the integers and the device time per certificate."""
 import os, sys, time, warnings
+os.environ.setdefault("LINKCERT_STAGE_TIMES", "1")   # every stage timed (diagnostic)
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
 import numpy as np

@@ -4,6 +4,7 @@ without an L2 flush between steps — for A/B builds (LINKCERT_LIB=...).  GPU bo
 """
 import argparse
 import os
+os.environ.setdefault("LINKCERT_STAGE_TIMES", "1")   # every stage timed (diagnostic)
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

@@ -1,6 +1,7 @@
 """Stage times of the fused device step under different conditions (GPU box; not a bench number).
     python tools/step_probe.py [--flush] [--serial-checks]"""
 import argparse, os, statistics, sys
+os.environ.setdefault("LINKCERT_STAGE_TIMES", "1")   # every stage timed (diagnostic)
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 ap = argparse.ArgumentParser()
 ap.add_argument("--flush", action="store_true")

@@ -5,6 +5,7 @@ from the first mark to the end of each stage, main stream and the two side branc
 """
 import argparse
 import os
+os.environ.setdefault("LINKCERT_STAGE_TIMES", "1")   # every stage timed (diagnostic)
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
