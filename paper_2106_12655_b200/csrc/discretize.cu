@@ -512,9 +512,13 @@ __global__ void out_counts_kernel(const unsigned long long *__restrict__ dcnt, c
     }
 }
 
-__global__ void closed_offsets_kernel(const int64_t *__restrict__ off, int64_t L, int64_t *__restrict__ voff) {
+__global__ void closed_offsets_kernel(const int64_t *__restrict__ off, int64_t L, int64_t *__restrict__ voff,
+                                      int64_t *__restrict__ vert_off = nullptr) {
     const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (l <= L) voff[l] = off[l] + l;
+    if (l <= L) {
+        voff[l] = off[l] + l;
+        if (vert_off) vert_off[l] = off[l];   // the chords' open offsets = the model's
+    }
 }
 
 __device__ __forceinline__ void put_closed(double *__restrict__ X, double *__restrict__ Y, double *__restrict__ Z,
@@ -1172,17 +1176,17 @@ void reserve_discretize_fast(const DiscInput &in, DiscScratch &sc, DiscOutput &o
 }
 
 void launch_discretize_chords(const DiscInput &in, const DiscParams &prm, DiscScratch &sc, DiscOutput &out,
-                              cudaStream_t s) {
+                              cudaStream_t s, bool prezeroed) {
     const int64_t L = in.L, M = in.M;
     const double poly_thr = kMachineEps * prm.xi;
     out.passes = 1;
     out.splits = 0;
     out.V = M;
     out.Vc = M + L;
-    LC_CUDA(cudaMemcpyAsync(out.vert_off.ptr, in.loff, sizeof(int64_t) * (L + 1), cudaMemcpyDeviceToDevice, s));
-    closed_offsets_kernel<<<grid_for(L + 1), 256, 0, s>>>(in.loff, L, out.voff.as<int64_t>());
+    closed_offsets_kernel<<<grid_for(L + 1), 256, 0, s>>>(in.loff, L, out.voff.as<int64_t>(),
+                                                           out.vert_off.as<int64_t>());
     LC_CHECK_LAUNCH();
-    LC_CUDA(cudaMemsetAsync(sc.val_flags.ptr, 0, sizeof(unsigned) * (L > 0 ? L : 1), s));
+    if (!prezeroed) LC_CUDA(cudaMemsetAsync(sc.val_flags.ptr, 0, sizeof(unsigned) * (L > 0 ? L : 1), s));
     launch_write_all(in, poly_thr, out, sc.val_flags.as<unsigned>(), s);
 }
 
@@ -1199,11 +1203,11 @@ void launch_pass1_brute(const DiscInput &in, const int64_t *d_P, DiscScratch &sc
 
 void launch_discretize_checks(const DiscInput &in, const int64_t *d_P, const DiscParams &prm, DiscScratch &sc,
                               DiscOutput &out, cudaStream_t s, cudaEvent_t chords_done, const PreCounters **d_ctr,
-                              bool brute_by_caller) {
+                              bool brute_by_caller, bool prezeroed) {
     const int64_t L = in.L, M = in.M, Pcap = in.P;
     const double min_diam = prm.epsilon * prm.xi;
     PreCounters *ctr = sc.prectr.as<PreCounters>();
-    LC_CUDA(cudaMemsetAsync(sc.paired.ptr, 0, L > 0 ? L : 1, s));
+    if (!prezeroed) LC_CUDA(cudaMemsetAsync(sc.paired.ptr, 0, L > 0 ? L : 1, s));
     if (Pcap > 0) {
         // single-warp blocks: they fit beside the Gauss kernel's CTAs (this branch runs under it)
         pre_pairs_kernel<<<std::min(grid_for(Pcap, 32), kChecksBlocks), 32, 0, s>>>(in.pairs, Pcap, d_P, in.loff, in.loop_box, L,

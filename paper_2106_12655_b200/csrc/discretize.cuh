@@ -108,10 +108,10 @@ void launch_discretize_fast(const DiscInput &in, const int64_t *d_P, const DiscP
 // after `chords_done` — the validation ranking).
 void reserve_discretize_fast(const DiscInput &in, DiscScratch &sc, DiscOutput &out, cudaStream_t s);
 void launch_discretize_chords(const DiscInput &in, const DiscParams &prm, DiscScratch &sc, DiscOutput &out,
-                              cudaStream_t s);
+                              cudaStream_t s, bool prezeroed = false);
 void launch_discretize_checks(const DiscInput &in, const int64_t *d_P, const DiscParams &prm, DiscScratch &sc,
                               DiscOutput &out, cudaStream_t s, cudaEvent_t chords_done, const PreCounters **d_ctr,
-                              bool brute_by_caller = false);
+                              bool brute_by_caller = false, bool prezeroed = false);
 // The pass-1 pair check alone (brute_any_kernel, grid-stride over *d_P pairs): on the
 // critical stream after the segment boxes, followed by the Gauss sum as its
 // programmatic dependent (the kernel triggers its dependents as it starts).

@@ -742,6 +742,8 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
             {d_model_exp.ptr, 1, 0u},                     // coordinate exponent (atomicMax)
             {ee ? d_ee.ptr : nullptr, ee ? 2 : 0, ~0u},  // early exit: first failure (~0)
             {ee ? static_cast<unsigned *>(d_ee.ptr) + 2 : nullptr, ee ? 2 : 0, 0u},   // pairs evaluated
+            {disc_sc.val_flags.ptr, L > 0 ? L : 1, 0u},                 // chords: PolylineLoop flags
+            {disc_sc.paired.ptr, (L + 3) / 4 > 0 ? (L + 3) / 4 : 1, 0u}, // checks: paired-loop bytes
         };
         const int n_extra = (int)(sizeof extra / sizeof extra[0]);
         if (!split) {
@@ -769,7 +771,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
                                    nullptr, side[0], const_cast<float *>(in.seg_sub));
             tl_mark("S0:seg_boxes", side[0]);
         }
-        launch_discretize_chords(in, prm, disc_sc, dout, side[0]);
+        launch_discretize_chords(in, prm, disc_sc, dout, side[0], /*prezeroed=*/true);
         tl_mark("S0:chords", side[0]);
         LC_CUDA(cudaEventRecord(ev_chords, side[0]));
         if (n_excl > 0)
@@ -789,7 +791,8 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
         // starts beside it as its programmatic dependent; the rest of the checks stay on
         // this branch (measured: the check inside the Gauss kernel, 0.49 ms per Kusari
         // step, or starved on this branch behind the persistent sum, 0.47 ms)
-        launch_discretize_checks(in, dP, prm, disc_sc, dout, side[1], ev_chords, &ctr, kBrutePdl);
+        launch_discretize_checks(in, dP, prm, disc_sc, dout, side[1], ev_chords, &ctr, kBrutePdl,
+                                 /*prezeroed=*/true);
         tl_mark("S1:checks", side[1]);
         if (detail) record(EV_DISC, side[1]);
         // the pair list is final: the copy engine moves the whole capacity to pinned
