@@ -21,3 +21,7 @@ __version__ = getattr(_pkg, "__version__", "b200")
 class BraidModel:   # braid closure is outside the hot path (SURVEY §2 OUT); the reference conftest imports it
     def __init__(self, *args, **kwargs):
         raise NotImplementedError("braid closure is outside this build's scope")
+
+
+def link_count_crossings(*args, **kwargs):   # crossing counting (crossings.py) is outside this build's scope
+    raise NotImplementedError("crossing counting is outside this build's scope")
