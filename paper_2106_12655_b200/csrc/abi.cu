@@ -164,19 +164,7 @@ int lc_link_direct(lc_ctx *ctx, const double *loop1, int64_t n1, const double *l
                    int mode, double *raw) {
     return guarded(ctx, [&] {
         if (!loop1 || !loop2 || n1 < 1 || n2 < 1) throw Error(LC_ERR_ARG, "lc_link_direct: bad arguments");
-        std::vector<double> v((size_t)(n1 + n2) * 3);
-        std::copy(loop1, loop1 + 3 * n1, v.begin());
-        std::copy(loop2, loop2 + 3 * n2, v.begin() + 3 * n1);
-        const int64_t off[3] = {0, n1, n1 + n2};
-        const int32_t pr[2] = {0, 1};
-        int64_t lk = 0;
-        uint8_t fl = 0;
-        ctx->pipe.upload_polylines(v.data(), off, 2);
-        ctx->pipe.upload_pairs(pr, 1);
-        ctx->pipe.build_gauss_items(mode);
-        ctx->pipe.run_gauss(mode, 0, ctx->pipe.n_items, nullptr, ctx->ev0, ctx->ev1);
-        ctx->pipe.reduce_pairs(nullptr);
-        ctx->pipe.download_results(raw, &lk, &fl);
+        *raw = ctx->pipe.link_direct(loop1, n1, loop2, n2, mode, ctx->ev0, ctx->ev1);
         LC_CUDA(cudaEventElapsedTime(&ctx->last_gauss_ms, ctx->ev0, ctx->ev1));
     });
 }

@@ -58,8 +58,9 @@ struct ItemRec {
 // Tiling of pair (column loop i, row loop j) from the two loops' closed-vertex
 // offsets and segment counts (one definition for every path that builds items).
 // seq: items of the sequential (anglesum) modes — 32 whole rows per item, one per lane.
+// max_cl: a smaller column-strip cap for a lone pair (more, shorter items: link_direct).
 __host__ __device__ inline PairGeom make_pair_geom(int64_t col_off, int64_t row_off, int ncols, int nrows,
-                                                   bool seq = false) {
+                                                   bool seq = false, int max_cl = kMaxColsPerLane) {
     PairGeom g;
     g.col_off = col_off;
     g.row_off = row_off;
@@ -79,7 +80,7 @@ __host__ __device__ inline PairGeom make_pair_geom(int64_t col_off, int64_t row_
     g.rb_log2 = rbl;
     const int cs = 32 >> rbl;
     const int cl = (ncols + cs - 1) / cs;
-    g.cl = cl < kMaxColsPerLane ? (cl > 0 ? cl : 1) : kMaxColsPerLane;
+    g.cl = cl < max_cl ? (cl > 0 ? cl : 1) : max_cl;
     g.items_r = (nrows + (kRowsPerLane << rbl) - 1) / (kRowsPerLane << rbl);
     const int64_t span = (int64_t)cs * g.cl;
     g.items_c = (int)((ncols + span - 1) / span);

@@ -521,6 +521,87 @@ void Pipeline::upload_polylines(const double *verts, const int64_t *vert_off, in
     LC_CUDA(cudaStreamSynchronize(s));
 }
 
+double Pipeline::link_direct(const double *loop1, int64_t n1, const double *loop2, int64_t n2, int mode,
+                             cudaEvent_t ev0, cudaEvent_t ev1) {
+    if (!gauss_mode_valid(mode)) throw Error(LC_ERR_ARG, "unknown Gauss-sum mode");
+    const int64_t Vc = n1 + n2 + 2;   // both loops closed (their first vertex repeated)
+    // the exact power-of-two scale of upload_polylines (largest exponent field of any coordinate)
+    int emax = 0;
+    for (int k = 0; k < 2; ++k) {
+        const double *a = k ? loop2 : loop1;
+        const int64_t n = 3 * (k ? n2 : n1);
+        for (int64_t q = 0; q < n; ++q) {
+            uint64_t b;
+            std::memcpy(&b, a + q, 8);
+            const int e = (int)((b >> 52) & 0x7ff);
+            emax = e > emax ? e : emax;
+        }
+    }
+    int e = emax - 1023;
+    e = e < -1022 ? -1022 : (e > 1022 ? 1022 : e);
+    double scale;
+    const uint64_t sbits = (uint64_t)(1023 - e) << 52;
+    std::memcpy(&scale, &sbits, 8);
+    // pair (0, 1): loop 1 = columns ("l"), loop 2 = rows ("k"), as the staged path tiles it
+    const bool seq = gauss_mode_sequential(mode);
+    PairGeom g = make_pair_geom(0, n1 + 1, (int)n1, (int)n2, seq);
+    // one pair alone: shorter column strips until there are ~8 items per SM (a 1024 x 1024
+    // pair is otherwise 8 items — 8 warps on the whole GPU)
+    for (int cl = g.cl; !seq && (int64_t)g.items_r * g.items_c < 8 * (int64_t)num_sms() && cl > 16;) {
+        cl = cl / 2 > 16 ? cl / 2 : 16;
+        g = make_pair_geom(0, n1 + 1, (int)n1, (int)n2, false, cl);
+    }
+    const int64_t items = (int64_t)g.items_r * g.items_c;
+    // staging layout: X | Y | Z (Vc each, padded to 8 doubles) | items | item_off[2]
+    const int64_t cv = (Vc + 7) & ~int64_t(7);
+    const size_t bytes = sizeof(double) * 3 * cv + sizeof(ItemRec) * (items > 0 ? items : 1) + 2 * sizeof(int64_t);
+    h_ld.reserve(bytes);
+    d_ld.reserve(bytes, s);
+    d_ld_out.reserve(sizeof(double) * (items > 0 ? items : 1) + 64, s);
+    d_counter.reserve(sizeof(unsigned long long), s);
+    char *h = static_cast<char *>(h_ld.ptr);   // (the previous call's copies completed with its sync)
+    double *X = reinterpret_cast<double *>(h), *Y = X + cv, *Z = Y + cv;
+    int64_t v = 0;
+    for (int k = 0; k < 2; ++k) {
+        const double *a = k ? loop2 : loop1;
+        const int64_t n = k ? n2 : n1;
+        for (int64_t q = 0; q <= n; ++q, ++v) {
+            const int64_t src = q < n ? q : 0;
+            X[v] = a[3 * src] * scale;
+            Y[v] = a[3 * src + 1] * scale;
+            Z[v] = a[3 * src + 2] * scale;
+        }
+    }
+    ItemRec *it = reinterpret_cast<ItemRec *>(h + sizeof(double) * 3 * cv);
+    for (int64_t k = 0; k < items; ++k) {
+        it[k].g = g;
+        it[k].ir = (int32_t)(k / g.items_c);
+        it[k].ic = (int32_t)(k % g.items_c);
+    }
+    int64_t *ioff = reinterpret_cast<int64_t *>(reinterpret_cast<char *>(it) + sizeof(ItemRec) * (items > 0 ? items : 1));
+    ioff[0] = 0;
+    ioff[1] = items;
+    LC_CUDA(cudaMemcpyAsync(d_ld.ptr, h, bytes, cudaMemcpyHostToDevice, s));
+    char *d = static_cast<char *>(d_ld.ptr);
+    const double *dX = reinterpret_cast<const double *>(d), *dY = dX + cv, *dZ = dY + cv;
+    const ItemRec *dit = reinterpret_cast<const ItemRec *>(d + sizeof(double) * 3 * cv);
+    const int64_t *dioff =
+        reinterpret_cast<const int64_t *>(d + sizeof(double) * 3 * cv + sizeof(ItemRec) * (items > 0 ? items : 1));
+    double *partials = d_ld_out.as<double>();
+    double *raw = reinterpret_cast<double *>(reinterpret_cast<char *>(partials) + sizeof(double) * (items > 0 ? items : 1));
+    int64_t *lk = reinterpret_cast<int64_t *>(raw + 1);
+    uint8_t *fl = reinterpret_cast<uint8_t *>(lk + 1);
+    LC_CUDA(cudaEventRecord(ev0, s));
+    launch_gauss_items(mode, dX, dY, dZ, dit, 0, items, d_counter.as<unsigned long long>(), partials, s);
+    LC_CUDA(cudaEventRecord(ev1, s));
+    launch_reduce_pairs(partials, dioff, 1, raw, lk, fl, s);
+    double out = 0.0;
+    LC_CUDA(cudaMemcpyAsync(h, raw, sizeof(double), cudaMemcpyDeviceToHost, s));
+    LC_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(&out, h, sizeof(double));
+    return out;
+}
+
 void Pipeline::upload_pairs(const int32_t *pairs, int64_t npairs) {
     P = npairs;
     d_pairs.reserve(sizeof(int32_t) * 2 * (size_t)(P > 0 ? P : 1), s);

@@ -184,6 +184,13 @@ struct Pipeline {
     PinnedBuf h_excl;               // excluded keys staged for the graph's H2D copy
     bool last_fast_graph = false;
     void segment_pair_lambda(const double *quads, int64_t n, double *out);
+    // link_direct of two open-vertex loops (direct.py:149-161): closed scaled SoA and the
+    // pair's work items built on the host, one H2D copy, the items kernel, the fixed-order
+    // reduction, one D2H of the raw sum; the resident model is left untouched
+    double link_direct(const double *loop1, int64_t n1, const double *loop2, int64_t n2, int mode,
+                       cudaEvent_t ev0, cudaEvent_t ev1);
+    PinnedBuf h_ld;
+    DevBuf d_ld, d_ld_out;
 
     float stage_ms(int e0, int e1);
     void record(int e, cudaStream_t st = nullptr);
