@@ -603,7 +603,7 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) gauss_pairs_kernel(
 
 __global__ void pair_geom_kernel(const int32_t *__restrict__ pairs, int64_t P, const int64_t *__restrict__ dP,
                                  const int64_t *__restrict__ voff, PairGeom *__restrict__ pg,
-                                 int64_t *__restrict__ nitems, bool seq) {
+                                 int64_t *__restrict__ nitems, bool seq, int max_cl) {
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p >= P) return;
     if (dP && p >= *dP) {   // fused path: capacity slots beyond the device pair count hold no items
@@ -612,7 +612,7 @@ __global__ void pair_geom_kernel(const int32_t *__restrict__ pairs, int64_t P, c
     }
     const int i = pairs[2 * p], j = pairs[2 * p + 1];
     const PairGeom g = make_pair_geom(voff[i], voff[j], (int)(voff[i + 1] - voff[i] - 1),
-                                      (int)(voff[j + 1] - voff[j] - 1), seq);
+                                      (int)(voff[j + 1] - voff[j] - 1), seq, max_cl);
     pg[p] = g;
     nitems[p] = (int64_t)g.items_r * g.items_c;
 }
@@ -712,10 +712,22 @@ __global__ void item_pair_fill_kernel(const int64_t *__restrict__ item_off, cons
 // cost crosses floor(k * total / shards), inside pair p at item
 // item_off[p] + ceil((t_k - C_p) * items_p / cost_p) (items of a pair are
 // near-equal).  One block; bounds[0] = 0, bounds[shards] = the item count.
+// Segment pairs of the first k items of pair tiling g (items in order: ir * items_c + ic;
+// only the last item row / column of a pair is partial).
+__device__ __forceinline__ int64_t items_prefix_cost(const PairGeom &g, int64_t k, bool seq) {
+    const int64_t rows_per = seq ? 32 : (int64_t)kRowsPerLane << g.rb_log2;
+    const int64_t span = seq ? g.ncols : (int64_t)(32 >> g.rb_log2) * g.cl;
+    const int64_t ir = k / g.items_c, ic = k % g.items_c;
+    const int64_t rows_done = ir * rows_per < g.nrows ? ir * rows_per : g.nrows;
+    const int64_t rows_cur = g.nrows - rows_done < rows_per ? g.nrows - rows_done : rows_per;
+    const int64_t cols_done = ic * span < g.ncols ? ic * span : g.ncols;
+    return rows_done * g.ncols + rows_cur * cols_done;
+}
+
 __global__ void __launch_bounds__(1024) shard_bounds_kernel(const PairGeom *__restrict__ pg,
                                                             const int64_t *__restrict__ item_off, int64_t Pcap,
                                                             const int64_t *__restrict__ dP, int shards,
-                                                            int64_t *__restrict__ bounds) {
+                                                            int64_t *__restrict__ bounds, bool seq) {
     __shared__ int64_t wsum[32];
     __shared__ int64_t s_total, s_carry;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
@@ -756,9 +768,19 @@ __global__ void __launch_bounds__(1024) shard_bounds_kernel(const PairGeom *__re
             for (int k = 1; k < shards; ++k) {
                 const int64_t t = (int64_t)((__int128)total * k / shards);
                 if (excl <= t && t < excl + c) {
+                    // the first item of the pair that starts at or after the target cost
                     const int64_t items_p = item_off ? item_off[p + 1] - item_off[p] : 1;
-                    int64_t local = (int64_t)(((__int128)(t - excl) * items_p + c - 1) / c);
-                    bounds[k] = (item_off ? item_off[p] : p) + (local < items_p ? local : items_p);
+                    int64_t lo = 0, hi = items_p;
+                    if (item_off) {
+                        const PairGeom g = pg[p];
+                        while (lo < hi) {
+                            const int64_t mid = (lo + hi) >> 1;
+                            if (items_prefix_cost(g, mid, seq) >= t - excl) hi = mid; else lo = mid + 1;
+                        }
+                    } else {
+                        lo = t > excl ? 1 : 0;
+                    }
+                    bounds[k] = (item_off ? item_off[p] : p) + lo;
                 }
             }
         __syncthreads();
@@ -770,8 +792,8 @@ __global__ void __launch_bounds__(1024) shard_bounds_kernel(const PairGeom *__re
 }  // namespace
 
 void launch_shard_bounds(const PairGeom *pg, const int64_t *item_off, int64_t Pcap, const int64_t *d_P, int shards,
-                         int64_t *bounds, cudaStream_t s) {
-    shard_bounds_kernel<<<1, 1024, 0, s>>>(pg, item_off, Pcap, d_P, shards, bounds);
+                         int64_t *bounds, cudaStream_t s, bool seq) {
+    shard_bounds_kernel<<<1, 1024, 0, s>>>(pg, item_off, Pcap, d_P, shards, bounds, seq);
     LC_CHECK_LAUNCH();
 }
 
@@ -819,14 +841,15 @@ size_t build_items_scan_bytes(int64_t P) { return exclusive_scan_i64_tmp_bytes(P
 
 int64_t build_items(const int32_t *d_pairs, int64_t P, const int64_t *d_voff, PairGeom *d_pg,
                     int64_t *d_item_off, void *d_scan_tmp, size_t scan_tmp_bytes, cudaStream_t s, bool read_back,
-                    const int64_t *d_P, bool seq) {
+                    const int64_t *d_P, bool seq, int max_cl) {
     if (P == 0) {
         LC_CUDA(cudaMemsetAsync(d_item_off, 0, sizeof(int64_t), s));
         return 0;
     }
     // nitems written into item_off[0..P), item_off[P] = 0, then in-place exclusive scan.
     LC_CUDA(cudaMemsetAsync(d_item_off + P, 0, sizeof(int64_t), s));
-    pair_geom_kernel<<<(unsigned)ceil_div(P, 256), 256, 0, s>>>(d_pairs, P, d_P, d_voff, d_pg, d_item_off, seq);
+    pair_geom_kernel<<<(unsigned)ceil_div(P, 256), 256, 0, s>>>(d_pairs, P, d_P, d_voff, d_pg, d_item_off, seq,
+                                                                 max_cl);
     LC_CHECK_LAUNCH();
     exclusive_scan_i64(d_item_off, d_item_off, P + 1, d_scan_tmp, scan_tmp_bytes, s);
     if (!read_back) return -1;   // caller reads item_off[P] together with other results

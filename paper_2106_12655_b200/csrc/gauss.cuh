@@ -94,7 +94,8 @@ __host__ __device__ inline PairGeom make_pair_geom(int64_t col_off, int64_t row_
 // capacity slots past it get no items (item_off[P] is still the total).
 int64_t build_items(const int32_t *d_pairs, int64_t P, const int64_t *d_voff, PairGeom *d_pg,
                     int64_t *d_item_off, void *d_scan_tmp, size_t scan_tmp_bytes, cudaStream_t s,
-                    bool read_back = true, const int64_t *d_P = nullptr, bool seq = false);
+                    bool read_back = true, const int64_t *d_P = nullptr, bool seq = false,
+                    int max_cl = kMaxColsPerLane);
 size_t build_items_scan_bytes(int64_t P);
 
 // Evaluates items [item_begin, item_end) into partials[item] (absolute index).
@@ -140,7 +141,8 @@ void launch_early_exit_order(const int32_t *pairs, const int64_t *d_P, int64_t p
 // shard r owns items [bounds[r], bounds[r+1]); each shard's segment-pair cost is
 // within one item of total / shards.  d_P: device pair count (<= Pcap) or null.
 void launch_shard_bounds(const PairGeom *pg, const int64_t *item_off, int64_t Pcap, const int64_t *d_P, int shards,
-                         int64_t *bounds, cudaStream_t s);
+                         int64_t *bounds, cudaStream_t s,
+                         bool seq = false);
 
 // items[it] = the record of work item `it` (pair tiling + the item's place in it).
 void launch_item_pairs(const int64_t *item_off, const PairGeom *pg, int64_t P, int64_t n_items, ItemRec *items,

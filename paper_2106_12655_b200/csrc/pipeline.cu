@@ -629,7 +629,21 @@ void Pipeline::build_gauss_items(int mode) {
     d_counter.reserve(sizeof(unsigned long long), s);
     n_items = build_items(d_pairs.as<int32_t>(), P, gvoff, d_pg.as<PairGeom>(), d_item_off.as<int64_t>(), d_scan.ptr,
                           d_scan.bytes, s, true, nullptr, items_seq);
+    retile_few_items();
     finish_items();
+}
+
+// Few work items (a pair or two of long loops: a lone 1024 x 1024 pair is 8 items,
+// 8 warps on the GPU): rebuild with shorter column strips for ~8 items per SM.  Only
+// where no fused run of the same model exists to stay bitwise equal to — polylines
+// staged directly, or a model with a loop the fused path does not take (> 256 segments).
+void Pipeline::retile_few_items() {
+    const int64_t target = 8 * (int64_t)num_sms();
+    if (items_seq || n_items <= 0 || n_items >= target || (polylines_from_model && max_loop <= 256)) return;
+    int max_cl = kMaxColsPerLane;
+    for (int64_t est = n_items; est < target && max_cl > 16; est *= 2) max_cl /= 2;
+    n_items = build_items(d_pairs.as<int32_t>(), P, gvoff, d_pg.as<PairGeom>(), d_item_off.as<int64_t>(), d_scan.ptr,
+                          d_scan.bytes, s, true, nullptr, false, max_cl);
 }
 
 bool Pipeline::build_gauss_items_checked(int mode) {
@@ -656,6 +670,7 @@ bool Pipeline::build_gauss_items_checked(int mode) {
             return false;
         }
     }
+    retile_few_items();
     finish_items();
     return true;
 }
@@ -1120,7 +1135,8 @@ void Pipeline::shard_bounds(int shards, int64_t *out) {
     if (!polylines_ready) throw Error(LC_ERR_STATE, "no work items built");
     if (shards < 1) throw Error(LC_ERR_ARG, "shards must be >= 1");
     d_bounds.reserve(sizeof(int64_t) * (shards + 1), s);
-    launch_shard_bounds(d_pg.as<PairGeom>(), d_item_off.as<int64_t>(), P, nullptr, shards, d_bounds.as<int64_t>(), s);
+    launch_shard_bounds(d_pg.as<PairGeom>(), d_item_off.as<int64_t>(), P, nullptr, shards, d_bounds.as<int64_t>(), s,
+                        items_seq);
     if (out) {
         LC_CUDA(cudaMemcpyAsync(out, d_bounds.ptr, sizeof(int64_t) * (shards + 1), cudaMemcpyDeviceToHost, s));
         LC_CUDA(cudaStreamSynchronize(s));

@@ -184,6 +184,7 @@ struct Pipeline {
     PinnedBuf h_excl;               // excluded keys staged for the graph's H2D copy
     bool last_fast_graph = false;
     void segment_pair_lambda(const double *quads, int64_t n, double *out);
+    void retile_few_items();   // build_gauss_items*: more, shorter items when there are very few
     // link_direct of two open-vertex loops (direct.py:149-161): closed scaled SoA and the
     // pair's work items built on the host, one H2D copy, the items kernel, the fixed-order
     // reduction, one D2H of the raw sum; the resident model is left untouched

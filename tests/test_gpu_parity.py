@@ -428,20 +428,33 @@ def test_cost_balanced_shard_bounds(gpu, shards):
     # per-item cost on the host from the pair sizes (items of a pair tile it exactly)
     _, voff = ctx.get_polylines()
     nseg = np.diff(voff)
-    items = []
-    for i, j in pairs:
-        g_rows, g_cols = int(nseg[j]), int(nseg[i])
-        nb = -(-g_rows // 4)
-        rbl = 0
-        while (1 << rbl) < nb and rbl < 5:
-            rbl += 1
-        cs = 32 >> rbl
-        cl = min(max(-(-g_cols // cs), 1), 2048)
-        rows_per, span = 4 << rbl, cs * cl
-        for ir in range(-(-g_rows // rows_per)):
-            for ic in range(-(-g_cols // span)):
-                items.append(min(rows_per, g_rows - ir * rows_per) * min(span, g_cols - ic * span))
-    items = np.array(items, dtype=np.int64)
+
+    def tile(max_cl):
+        items = []
+        for i, j in pairs:
+            g_rows, g_cols = int(nseg[j]), int(nseg[i])
+            nb = -(-g_rows // 4)
+            rbl = 0
+            while (1 << rbl) < nb and rbl < 5:
+                rbl += 1
+            cs = 32 >> rbl
+            cl = min(max(-(-g_cols // cs), 1), max_cl)
+            rows_per, span = 4 << rbl, cs * cl
+            for ir in range(-(-g_rows // rows_per)):
+                for ic in range(-(-g_cols // span)):
+                    items.append(min(rows_per, g_rows - ir * rows_per) * min(span, g_cols - ic * span))
+        return np.array(items, dtype=np.int64)
+
+    items = tile(2048)
+    # Pipeline::retile_few_items: a model with loops the fused path does not take (> 256
+    # segments) and fewer than 8 items per SM is tiled with shorter column strips
+    import torch
+    target = 8 * torch.cuda.get_device_properties(0).multi_processor_count
+    if len(items) < target and nseg.max() > 256:
+        max_cl, est = 2048, len(items)
+        while est < target and max_cl > 16:
+            est, max_cl = 2 * est, max_cl // 2
+        items = tile(max_cl)
     assert b[-1] == len(items)
     total = items.sum()
     cum = np.concatenate([[0], np.cumsum(items)])
