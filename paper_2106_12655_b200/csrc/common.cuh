@@ -105,6 +105,9 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // stream still runs (once every predecessor CTA has executed LC_PDL_TRIGGER or
 // exited); it must LC_PDL_WAIT before touching the predecessor's outputs.  Both
 // device macros are no-ops for kernels launched without the attribute.
+#ifndef LC_EXPORT_PDL
+#define LC_EXPORT_PDL 0   // the fused run's status export as the sum's programmatic dependent (A/B)
+#endif
 #define LC_PDL_TRIGGER() asm volatile("griddepcontrol.launch_dependents;")
 #define LC_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
 template <typename... KArgs, typename... Args>

@@ -534,6 +534,9 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) gauss_pairs_kernel(
     int shard, double *__restrict__ partials, double *__restrict__ raw, int64_t *__restrict__ lk,
     uint8_t *__restrict__ flags, double *__restrict__ h_raw, int64_t *__restrict__ h_lk,
     uint8_t *__restrict__ h_flags, const EarlyExitArgs ee) {
+#if LC_EXPORT_PDL
+    LC_PDL_TRIGGER();   // the status export after the sum may become resident (it waits for the sum)
+#endif
     const int lane = threadIdx.x & 31;
     int64_t b = 0, e = *dP < pcap ? *dP : pcap;
     if (d_bounds) {

@@ -64,6 +64,7 @@ __global__ void export_results_kernel(const int64_t *__restrict__ dP, int64_t ca
                                       int2 *__restrict__ h_pairs, double *__restrict__ h_raw,
                                       int64_t *__restrict__ h_lk, uint8_t *__restrict__ h_flags,
                                       const unsigned long long *__restrict__ ee = nullptr) {
+    LC_PDL_WAIT();   // launched as the sum's programmatic dependent (LC_EXPORT_PDL); else a no-op
     const int64_t P = *dP < cap ? *dP : cap;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += stride) {
@@ -926,6 +927,17 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
                            sharded ? d_partials.as<double>() : nullptr, d_raw.as<double>(), d_lk.as<int64_t>(),
                            d_flags.as<uint8_t>(), reinterpret_cast<double *>(hr), reinterpret_cast<int64_t *>(hl),
                            reinterpret_cast<uint8_t *>(hf), s, eea, kBrutePdl);
+#if LC_EXPORT_PDL
+        // the status export as the sum's programmatic dependent (no event node between them)
+        LC_CUDA(cudaStreamWaitEvent(s, ev_checks, 0));
+        launch_pdl(export_results_kernel, dim3(1), dim3(32), s, !timeline().on, dP, pcap, d_items, dmx, ctr,
+                   (const int *)dout.d_val_err, (const int2 *)nullptr, (const double *)nullptr,
+                   (const int64_t *)nullptr, (const uint8_t *)nullptr, st, (int2 *)nullptr, (double *)nullptr,
+                   (int64_t *)nullptr, (uint8_t *)nullptr,
+                   (const unsigned long long *)(ee ? d_ee.as<unsigned long long>() : nullptr));
+        record(EV_GAUSS1);
+        tl_mark("gauss", s);
+#else
         record(EV_GAUSS1);
         tl_mark("gauss", s);
         LC_CUDA(cudaStreamWaitEvent(s, ev_checks, 0));
@@ -933,6 +945,7 @@ int Pipeline::run_fast(const uint64_t *excl_keys, int64_t n_excl, const DiscPara
         export_results_kernel<<<1, 32, 0, s>>>(dP, pcap, d_items, dmx, ctr, dout.d_val_err, nullptr, nullptr, nullptr,
                                                nullptr, st, nullptr, nullptr, nullptr, nullptr,
                                                ee ? d_ee.as<unsigned long long>() : nullptr);
+#endif
         LC_CHECK_LAUNCH();
         if (detail) record(EV_END);   // "reduce" = Gauss end -> status in pinned memory
         tl_mark("export", s);
