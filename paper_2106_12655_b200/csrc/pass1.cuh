@@ -25,6 +25,10 @@ __device__ __forceinline__ bool box_overlap(const double *__restrict__ b, int64_
              lo[2] > b[5 * stride + e] || b[2 * stride + e] > hi[2]);
 }
 
+#ifndef LC_PASS1_LANE_PAIRS
+#define LC_PASS1_LANE_PAIRS 1   // group pairs one per lane; 0: a row of groups per step (shuffles; A/B)
+#endif
+
 constexpr int kAnyCap = 64;   // staged survivors per side; beyond that the test reads global memory
 
 // One pair: the warp's share of the pass-1 detection (see brute_any_kernel).
@@ -159,10 +163,10 @@ __device__ __forceinline__ void brute_any_pair(int64_t p, const double *__restri
 
 // brute_any_pair with the 8-segment group boxes of seg_boxes_loop_kernel (`sub`,
 // layout pass1_group_slot; float, outward, NaN -> unbounded):
-// lane k holds group k of both loops (<= 32 groups: both loops have <= 256
-// segments); group pairs are tested a row of the warp at a time, and only
-// overlapping group pairs test their 8 x 8 segment pairs (float, then the exact
-// closed test on the double boxes).  Same decision as brute_any_pair: a segment
+// each lane tests one group pair (<= 32 groups per loop: both loops have <= 256
+// segments; 24 % fewer instructions than a row of shuffled groups per step,
+// profiles/r02/ab_pass1_lane_pairs.log), and only overlapping group pairs test
+// their 8 x 8 segment pairs (float, then the exact closed test on the double boxes).  Same decision as brute_any_pair: a segment
 // pair overlaps exactly => its float boxes and its groups overlap.
 __device__ __forceinline__ void brute_any_pair_sub(int64_t p, const double *__restrict__ box,
                                                    const float *__restrict__ fbox, const float *__restrict__ sub,
@@ -175,14 +179,37 @@ __device__ __forceinline__ void brute_any_pair_sub(int64_t p, const double *__re
     if (ni == 0 || nj == 0 || !brute_pair(ni, nj)) return;
     const int gi = (int)((ni + 7) >> 3), gj = (int)((nj + 7) >> 3);
     const int64_t S = pass1_group_stride(M, L), qi = pass1_group_slot(bi, i), qj = pass1_group_slot(bj, j);
+    const int u = lane & 7, w = lane >> 3;   // segment pair (u, w) and (u, w + 4) of a group pair
+    int hits = 0;
+#if LC_PASS1_LANE_PAIRS
+    // lane = one group pair (a, c): c = lane mod 2^sh (2^sh >= gj), a = a0 + lane >> sh;
+    // loop j's group box stays in the lane across chunks, loop i's is loaded per chunk
+    // (no shuffles: 4 chunk loads instead of 8 rows of 6 shuffles for 64-segment loops)
+    const int sh = 32 - __clz(gj - 1);
+    const int per = 32 >> sh, cl = lane & ((1 << sh) - 1), da = lane >> sh;
+    float sj[6];
+#pragma unroll
+    for (int d = 0; d < 6; ++d) sj[d] = cl < gj ? sub[d * S + qj + cl] : 0.f;
+    for (int a0 = 0; a0 < gi; a0 += per) {
+        const int ga = a0 + da;
+        const bool valid = cl < gj && ga < gi;
+        float o[6];
+#pragma unroll
+        for (int d = 0; d < 6; ++d) o[d] = valid ? sub[d * S + qi + ga] : 0.f;
+        const bool ov = valid && !(o[0] > sj[3] || sj[0] > o[3] || o[1] > sj[4] || sj[1] > o[4] ||
+                                   o[2] > sj[5] || sj[2] > o[5]);
+        unsigned bal = __ballot_sync(0xffffffffu, ov);
+        while (bal) {
+            const int bit = __ffs(bal) - 1;
+            bal &= bal - 1;
+            const int a = a0 + (bit >> sh), c = bit & ((1 << sh) - 1);
+#else
     float si[6], sj[6];
 #pragma unroll
     for (int d = 0; d < 6; ++d) {
         si[d] = lane < gi ? sub[d * S + qi + lane] : 0.f;
         sj[d] = lane < gj ? sub[d * S + qj + lane] : 0.f;
     }
-    const int u = lane & 7, w = lane >> 3;   // segment pair (u, w) and (u, w + 4) of a group pair
-    int hits = 0;
     for (int a = 0; a < gi; ++a) {
         float o[6];
 #pragma unroll
@@ -193,6 +220,7 @@ __device__ __forceinline__ void brute_any_pair_sub(int64_t p, const double *__re
         while (bal) {
             const int c = __ffs(bal) - 1;
             bal &= bal - 1;
+#endif
             const int64_t ki = 8 * a + u;
             if (ki >= ni) continue;
             const int64_t ei = bi + ki;
