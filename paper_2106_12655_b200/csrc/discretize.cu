@@ -232,7 +232,10 @@ __global__ void __launch_bounds__(32 * kBruteWarps) brute_kernel(ActView v, cons
 // test on the double boxes (bvh.py:93-98).  Hits are counted into *marked.
 constexpr int kAnyWarps = 8;
 
-__global__ void __launch_bounds__(32 * kAnyWarps, 4) brute_any_kernel(
+#ifndef LC_ANY_MINB
+#define LC_ANY_MINB 4   // blocks per SM the pass-1 kernel is compiled for (64 registers)
+#endif
+__global__ void __launch_bounds__(32 * kAnyWarps, LC_ANY_MINB) brute_any_kernel(
     const double *__restrict__ box, const float *__restrict__ fbox, int64_t M, const int64_t *__restrict__ loff,
     const double *__restrict__ lbox, int64_t L, const int32_t *__restrict__ pairs, int64_t P,
     const int64_t *__restrict__ dP, unsigned long long *__restrict__ marked, int *__restrict__ abort,
