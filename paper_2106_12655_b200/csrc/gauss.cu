@@ -278,11 +278,36 @@ __device__ __forceinline__ void col_step(const Col &A, Col &B, double lx, double
     }
 }
 
+#ifndef LC_ITEMS_PREFETCH
+#define LC_ITEMS_PREFETCH 0   // (A/B) items kernel: next claim + record fetched a unit ahead
+#endif
+#ifndef LC_PAIRS_L1PF
+#define LC_PAIRS_L1PF 1   // prefetch the next pair's first-item vertices into L1 (0: off, A/B)
+#endif
+__device__ __forceinline__ void l1_prefetch(const double *q) { asm volatile("prefetch.global.L1 [%0];" ::"l"(q)); }
+// The lines this lane's strip of item (ir, ic) of pair tiling g starts with: its
+// R + 1 row vertices and its first column vertex, per coordinate array.
+struct NextItem {
+    const PairGeom *g;   // nullptr: nothing to prefetch
+    int ir, ic;
+};
+__device__ __forceinline__ void l1_prefetch_item(const double *__restrict__ X, const double *__restrict__ Y,
+                                                 const double *__restrict__ Z, const PairGeom &g, int ir, int ic,
+                                                 int vl) {
+    const int row0 = ((ir << g.rb_log2) + (vl & ((1 << g.rb_log2) - 1))) * R;
+    const int64_t c0 = ((int64_t)ic * (32 >> g.rb_log2) + (vl >> g.rb_log2)) * g.cl;
+    if (row0 >= g.nrows || c0 >= g.ncols) return;
+    const int64_t r0 = g.row_off + row0, r1 = g.row_off + min(row0 + R, g.nrows), cc = g.col_off + c0;
+    l1_prefetch(X + r0); l1_prefetch(Y + r0); l1_prefetch(Z + r0);
+    l1_prefetch(X + r1); l1_prefetch(Y + r1); l1_prefetch(Z + r1);
+    l1_prefetch(X + cc); l1_prefetch(Y + cc); l1_prefetch(Z + cc);
+}
+
 // Sum over rows [row0, row0+R) x columns [c0, c1) of one pair, in turns.
 template <int MODE, bool FULL, class K>
 __device__ double lane_strip(const double *__restrict__ X, const double *__restrict__ Y,
                              const double *__restrict__ Z, int64_t row_off, int nrows, int64_t col_off, int row0,
-                             int c0, int c1, K &kv) {
+                             int c0, int c1, K &kv, NextItem pf = {nullptr, 0, 0}, int vl = 0) {
     bool rv[R];
 #pragma unroll
     for (int m = 0; m <= R; ++m) {
@@ -294,6 +319,9 @@ __device__ double lane_strip(const double *__restrict__ X, const double *__restr
     const double *px = X + col_off, *py = Y + col_off, *pz = Z + col_off;
     Col A, B;
     col_fill<MODE != GAUSS_PHASE>(A, __ldg(px + c0), __ldg(py + c0), __ldg(pz + c0), kv);
+#if LC_PAIRS_L1PF
+    if (pf.g) l1_prefetch_item(X, Y, Z, *pf.g, pf.ir, pf.ic, vl);   // the next unit's rows + first column, a strip ahead
+#endif
     Acc acc;
     int c = c0;
 #ifdef LC_PREFETCH
@@ -434,7 +462,7 @@ __device__ __forceinline__ int64_t find_pair(const int64_t *__restrict__ item_of
 template <int MODE, bool KSM>
 __device__ __forceinline__ double vlane_value(const double *__restrict__ X, const double *__restrict__ Y,
                                               const double *__restrict__ Z, const PairGeom &g, int ir, int ic, int vl,
-                                              double *ksh) {
+                                              double *ksh, NextItem pf = {nullptr, 0, 0}) {
     const int rbm = (1 << g.rb_log2) - 1;
     const int my_rb = vl & rbm, my_cs = vl >> g.rb_log2;
     const int row0 = ((ir << g.rb_log2) + my_rb) * R;
@@ -456,8 +484,8 @@ __device__ __forceinline__ double vlane_value(const double *__restrict__ X, cons
         } else {
             KReg kv;
             val = row0 + R <= g.nrows
-                      ? lane_strip<MODE, true>(X, Y, Z, g.row_off, g.nrows, g.col_off, row0, c0, c1, kv)
-                      : lane_strip<MODE, false>(X, Y, Z, g.row_off, g.nrows, g.col_off, row0, c0, c1, kv);
+                      ? lane_strip<MODE, true>(X, Y, Z, g.row_off, g.nrows, g.col_off, row0, c0, c1, kv, pf, vl)
+                      : lane_strip<MODE, false>(X, Y, Z, g.row_off, g.nrows, g.col_off, row0, c0, c1, kv, pf, vl);
         }
     }
     return val;
@@ -469,8 +497,8 @@ __device__ __forceinline__ double vlane_value(const double *__restrict__ X, cons
 template <int MODE, bool KSM>
 __device__ __forceinline__ double item_value(const double *__restrict__ X, const double *__restrict__ Y,
                                              const double *__restrict__ Z, const PairGeom &g, int ir, int ic, int lane,
-                                             double *ksh) {
-    double val = vlane_value<MODE, KSM>(X, Y, Z, g, ir, ic, lane, ksh);
+                                             double *ksh, NextItem pf = {nullptr, 0, 0}) {
+    double val = vlane_value<MODE, KSM>(X, Y, Z, g, ir, ic, lane, ksh, pf);
 #pragma unroll
     for (int off = 16; off; off >>= 1) val += __shfl_xor_sync(0xffffffffu, val, off);
     return val;
@@ -506,6 +534,26 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) gauss_items_kernel(
         const int64_t n = *d_end;
         if (n < item_end) item_end = n;
     }
+#if LC_ITEMS_PREFETCH
+    // the next claim and its record are fetched while the current item is summed, and
+    // its first vertex lines are prefetched into L1 (LC_PAIRS_L1PF)
+    int64_t k1;
+    bool ok1 = claim(counter, abort, lane, k1);
+    ItemRec r1 = {};
+    if (ok1 && item_begin + k1 < item_end) r1 = items[item_begin + k1];
+    for (;;) {
+        if (!ok1) break;
+        const int64_t it = item_begin + k1;
+        if (it >= item_end) break;
+        const ItemRec rec = r1;
+        ok1 = claim(counter, abort, lane, k1);
+        const bool nx = ok1 && item_begin + k1 < item_end;
+        if (nx) r1 = items[item_begin + k1];
+        const NextItem pf{(LC_PAIRS_L1PF && nx) ? &r1.g : nullptr, r1.ir, r1.ic};
+        const double val = item_value<MODE, KSM>(X, Y, Z, rec.g, rec.ir, rec.ic, lane, ksh, pf);
+        if (lane == 0) partials[it] = val;
+    }
+#else
     for (;;) {
         int64_t k;
         if (!claim(counter, abort, lane, k)) break;
@@ -515,6 +563,7 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) gauss_items_kernel(
         const double val = item_value<MODE, KSM>(X, Y, Z, rec.g, rec.ir, rec.ic, lane, ksh);
         if (lane == 0) partials[it] = val;
     }
+#endif
 }
 
 // Fused path: warps claim whole PAIRS (loops of <= 256 segments: 1-2 items each)
@@ -576,8 +625,13 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) gauss_pairs_kernel(
         const int n = g.items_r * g.items_c;
         double s = 0.0;
         for (int it = 0; it < n; ++it) {
+#if LC_PAIRS_L1PF && LC_PAIRS_PREFETCH
+            const NextItem pf{(it == 0 && ok1 && b + k1 < e) ? &g1 : nullptr, 0, 0};   // the next pair's item 0
+#else
+            const NextItem pf{nullptr, 0, 0};
+#endif
             const double v = __shfl_sync(0xffffffffu, item_value<MODE, false>(X, Y, Z, g, it / g.items_c,
-                                                                                it % g.items_c, lane, nullptr), 0);
+                                                                                it % g.items_c, lane, nullptr, pf), 0);
             if (lane == (it & 31)) s += v;
         }
 #pragma unroll
