@@ -9,3 +9,5 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 python tools/step_table.py gpurun_out/launches.csv > gpurun_out/step_table.md
 python tools/step_time.py --steps 3 > gpurun_out/plain_step.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:brute_any -c 1 -o gpurun_out/brute_any_kusari python tools/step_time.py --steps 3 > gpurun_out/ncu_brute.log 2>&1
+python tools/prof_gauss.py --case kusari --mode phase --reps 3 > gpurun_out/plain_prof.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:gauss_pairs -s 2 -c 1 -o gpurun_out/gauss_pairs_kusari python tools/prof_gauss.py --case kusari --mode phase --reps 3 > gpurun_out/ncu_full.log 2>&1
