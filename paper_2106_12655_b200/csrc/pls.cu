@@ -673,8 +673,12 @@ __global__ void grid_reduce_kernel(const double *__restrict__ lbox, int64_t L, u
 // (ordered-key warp reductions, then shared memory) into the model box and the
 // largest loop extent (one atomic set per block), and the last block derives
 // the grid parameters — grid_reduce_kernel's outputs with no second pass.
+#ifndef LC_LOOPGRID_WARPS
+#define LC_LOOPGRID_WARPS 4   // loop-box kernel: warps per block (one loop per warp per step)
+#endif
+constexpr int kLgWarps = LC_LOOPGRID_WARPS;
 template <bool POLY>
-__global__ void __launch_bounds__(128) loop_grid_kernel(const double *__restrict__ coeffs, const double *__restrict__ t,
+__global__ void __launch_bounds__(32 * kLgWarps) loop_grid_kernel(const double *__restrict__ coeffs, const double *__restrict__ t,
                                                         const double *__restrict__ verts,
                                                         const int64_t *__restrict__ loff, int64_t L,
                                                         unsigned long long *__restrict__ loop_min_diag2,
@@ -684,12 +688,12 @@ __global__ void __launch_bounds__(128) loop_grid_kernel(const double *__restrict
     LC_PDL_TRIGGER();
     LC_PDL_WAIT();
     zero_ranges(zl);   // the run's initial values, read by the kernels after this one
-    __shared__ unsigned long long sk[4][7];
+    __shared__ unsigned long long sk[kLgWarps][7];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // block accumulators (ordered keys): min lo x3, max hi x3, max extent
     unsigned long long bk[7] = {~0ULL, ~0ULL, ~0ULL, 0ULL, 0ULL, 0ULL, 0ULL};
-    const int64_t nw = (int64_t)gridDim.x * 4;
-    for (int64_t l = (int64_t)blockIdx.x * 4 + warp; l < L; l += nw) {
+    const int64_t nw = (int64_t)gridDim.x * kLgWarps;
+    for (int64_t l = (int64_t)blockIdx.x * kLgWarps + warp; l < L; l += nw) {
         const int64_t b = loff[l], e = loff[l + 1];
         double v[6] = {CUDART_INF, CUDART_INF, CUDART_INF, -CUDART_INF, -CUDART_INF, -CUDART_INF};
         unsigned long long dg = ~0ULL;
@@ -748,7 +752,7 @@ __global__ void __launch_bounds__(128) loop_grid_kernel(const double *__restrict
         for (int q = 0; q < 7; ++q) sk[warp][q] = bk[q];
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int w = 1; w < 4; ++w) {
+        for (int w = 1; w < kLgWarps; ++w) {
             for (int q = 0; q < 3; ++q) bk[q] = sk[w][q] < bk[q] ? sk[w][q] : bk[q];
             for (int q = 3; q < 7; ++q) bk[q] = sk[w][q] > bk[q] ? sk[w][q] : bk[q];
         }
@@ -1126,6 +1130,9 @@ int64_t run_pls(const double *loop_box, int64_t L, const uint64_t *h_excl, int64
     return (int64_t)P;
 }
 
+#ifndef LC_LOOPGRID_BPS
+#define LC_LOOPGRID_BPS 6   // loop-box kernel: blocks per SM cap (4 warps each, grid-stride over loops)
+#endif
 void launch_loop_grid(const double *coeffs, const double *t, const double *verts, const int64_t *loff, int64_t L,
                       unsigned long long *loop_min_diag2, double *loop_box, PlsScratch &sc, cudaStream_t s,
                       bool pdl, const ZeroRange *extra, int n_extra) {
@@ -1134,14 +1141,14 @@ void launch_loop_grid(const double *coeffs, const double *t, const double *verts
     reserve_pls_grid(L, sc, s);
     unsigned long long *acc = sc.acc.as<unsigned long long>();   // keys + block counter, at the identity
     const ZeroList zl = grid_zero_list(L, sc, extra, n_extra);
-    int64_t blocks = ceil_div(L, 4);
-    if (blocks > 148 * 6) blocks = 148 * 6;
+    int64_t blocks = ceil_div(L, kLgWarps);
+    if (blocks > 148 * LC_LOOPGRID_BPS) blocks = 148 * LC_LOOPGRID_BPS;
     if (verts)
-        launch_pdl(loop_grid_kernel<true>, (unsigned)blocks, 128, s, pdl, (const double *)nullptr,
+        launch_pdl(loop_grid_kernel<true>, (unsigned)blocks, 32 * kLgWarps, s, pdl, (const double *)nullptr,
                    (const double *)nullptr, verts, loff, L, loop_min_diag2, loop_box, acc,
                    reinterpret_cast<unsigned *>(acc + 7), max_cells, sc.axis.as<GridParams>(), zl);
     else
-        launch_pdl(loop_grid_kernel<false>, (unsigned)blocks, 128, s, pdl, coeffs, t, (const double *)nullptr, loff, L,
+        launch_pdl(loop_grid_kernel<false>, (unsigned)blocks, 32 * kLgWarps, s, pdl, coeffs, t, (const double *)nullptr, loff, L,
                    loop_min_diag2, loop_box, acc, reinterpret_cast<unsigned *>(acc + 7), max_cells,
                    sc.axis.as<GridParams>(), zl);
 }
