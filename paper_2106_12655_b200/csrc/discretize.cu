@@ -1193,11 +1193,14 @@ void launch_discretize_chords(const DiscInput &in, const DiscParams &prm, DiscSc
     launch_write_all(in, poly_thr, out, sc.val_flags.as<unsigned>(), s);
 }
 
+#ifndef LC_BRUTE_BPS
+#define LC_BRUTE_BPS 8   // pass-1 check on the critical stream: blocks per SM cap (8 warps each, grid-stride)
+#endif
 void launch_pass1_brute(const DiscInput &in, const int64_t *d_P, DiscScratch &sc, cudaStream_t s) {
     const int64_t Pcap = in.P, M = in.M;
     if (Pcap <= 0 || M <= 0) return;
     PreCounters *ctr = sc.prectr.as<PreCounters>();
-    const int64_t blocks = ceil_div(Pcap, kAnyWarps) < 148 * 8 ? ceil_div(Pcap, kAnyWarps) : 148 * 8;
+    const int64_t blocks = ceil_div(Pcap, kAnyWarps) < 148 * LC_BRUTE_BPS ? ceil_div(Pcap, kAnyWarps) : 148 * LC_BRUTE_BPS;
     brute_any_kernel<<<(unsigned)blocks, 32 * kAnyWarps, 0, s>>>(in.seg_box, in.seg_fbox, M, in.loff, in.loop_box,
                                                                  in.L, in.pairs, Pcap, d_P, &ctr->marked, &ctr->abort,
                                                                  in.seg_sub);
